@@ -1,0 +1,157 @@
+/*
+ * bzg.h — C ABI of the B200-native graph-construction stage for
+ * reachable-Bezier-polytope kinodynamic planning (arXiv 2411.13507).
+ *
+ * The reference (beziergraph, /root/reference/pkg/src/beziergraph) is pure
+ * Python and has no FFI; the entry points below are the boundary a
+ * maintainer binds (ctypes stub in INTEGRATION.md) to replace the hot
+ * functions of graph.py.  Each declaration cites the reference interface it
+ * replaces.
+ *
+ * Conventions
+ *   - every call returns 0 on success or a negative BZG_E* code;
+ *     bzg_last_error() returns a thread-local message for the last failure;
+ *   - host pointers are owned by the caller; opaque handles are owned by the
+ *     library and released with the matching *_destroy call;
+ *   - arrays are C-order float64 / int64 exactly as numpy holds them;
+ *   - work is stream-ordered on the context's stream; calls that return host
+ *     data synchronise that stream before returning;
+ *   - there is no CPU fallback: without a usable sm_100 device every compute
+ *     call fails with BZG_ENODEV.
+ */
+#ifndef BZG_H
+#define BZG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BZG_ABI_VERSION 1
+
+enum {
+  BZG_OK = 0,
+  BZG_EINVAL = -1,      /* argument error (reference raises ValueError) */
+  BZG_ENODEV = -2,      /* no usable CUDA device */
+  BZG_ECUDA = -3,       /* CUDA runtime error */
+  BZG_EUNSUPPORTED = -4,/* input outside what the device path implements */
+  BZG_ENOMEM = -5
+};
+
+/* provenance codes, reference graph.py:35-39 (CutProvenance) */
+enum { BZG_HEURISTIC_UNSAFE = 0, BZG_HEURISTIC_SAFE = 1, BZG_QP_SAFE = 2, BZG_QP_UNSAFE = 3 };
+/* QP status codes, reference qpsolver.py:29-33 (SolveStatus) */
+enum { BZG_SOLVED = 0, BZG_MAX_ITER = 1, BZG_INFEASIBLE = 2, BZG_ERROR = 3 };
+
+typedef struct bzg_ctx bzg_ctx;
+typedef struct bzg_graph bzg_graph;
+typedef struct bzg_mask bzg_mask;
+
+int bzg_abi_version(void);
+const char* bzg_last_error(void);
+
+/* ---- context ----------------------------------------------------------- */
+/* stream: a cudaStream_t to run on, or NULL for a library-owned stream. */
+int bzg_ctx_create(int device, void* stream, bzg_ctx** out);
+int bzg_ctx_destroy(bzg_ctx* ctx);
+int bzg_ctx_stream(bzg_ctx* ctx, void** stream_out);
+int bzg_ctx_synchronize(bzg_ctx* ctx);
+/* per-kernel CUDA-event timing of every launch (off by default) */
+int bzg_ctx_set_profiling(bzg_ctx* ctx, int enabled);
+/* launches since creation/reset; with profiling, per-kernel totals.
+ * names: buffer of n_cap*64 chars; ms/launches: n_cap entries; *n_out = kernels seen. */
+int bzg_ctx_stats(bzg_ctx* ctx, long long* launches, int n_cap, char* names, double* ms,
+                  long long* counts, int* n_out);
+int bzg_ctx_reset_stats(bzg_ctx* ctx);
+
+/* ---- a1..a5: build_graph (reference graph.py:129-199) ------------------- */
+typedef struct {
+  int32_t m, gamma, p;        /* BezierSpec (bezier.py:22-44); n = m*gamma, p = 2*gamma-1 */
+  int32_t n_F;                /* rows of the reachability oracle */
+  const double* F;            /* (n_F, 2n) ReachOracle.F (reachability.py:53) */
+  const double* G;            /* (n_F,)    ReachOracle.G */
+  double eps_geo;             /* EPS_GEO (geometry.py:14): thresh = G + eps_geo */
+  const double* D;            /* (p+1, 2*gamma) boundary_matrix (bezier.py:201) */
+  /* sampler (graph.py:147-157): first N accepted rows of one PCG64 stream */
+  int64_t N;
+  uint64_t pcg_state_hi, pcg_state_lo;  /* numpy PCG64 bit_generator.state['state'] */
+  uint64_t pcg_inc_hi, pcg_inc_lo;      /* ... ['inc'] */
+  const double* sample_lo;    /* (n,) Box.lo of the sampling bounds */
+  const double* sample_hi;    /* (n,) Box.hi */
+  int32_t xd_rows;            /* oracle.Xd: (xd_rows, n) A and (xd_rows,) b */
+  const double* xd_A;
+  const double* xd_b;
+  /* optional vertices appended after the samples (graph.py:158-159) */
+  int64_t n_include;
+  const double* include;      /* (n_include, n) or NULL */
+  /* optional: skip sampling and take these vertices verbatim (N rows); NULL = sample */
+  const double* vertices;
+  /* source-row block [row_begin, row_end) of the pair matrix this call evaluates
+   * (multi-GPU row sharding); row_end <= 0 means all rows */
+  int64_t row_begin, row_end;
+} bzg_build_desc;
+
+/* replaces graph.build_graph (graph.py:129-199) minus k_nearest */
+int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* desc, bzg_graph** out);
+/* assemble a graph from an existing edge list (device or host pointers), used by
+ * the multi-GPU gather on rank 0; edges must be in row-major (src, dst) order */
+int bzg_graph_from_edges(bzg_ctx* ctx, int32_t m, int32_t gamma, int32_t p, const double* D, int64_t V,
+                         const double* vertices_host, int64_t E, const int32_t* src, const int32_t* dst,
+                         const double* cost, int on_device, bzg_graph** out);
+int bzg_graph_destroy(bzg_graph* g);
+int bzg_graph_info(const bzg_graph* g, int64_t* V, int64_t* E, int64_t* row_begin, int64_t* row_end);
+/* host copies (BezierGraph fields, graph.py:61-68); any pointer may be NULL */
+int bzg_graph_copy_vertices(bzg_graph* g, double* vertices /* (V, n) */);
+int bzg_graph_copy_edges(bzg_graph* g, int64_t* edges /* (E, 2) */, double* costs /* (E,) */);
+int bzg_graph_copy_points(bzg_graph* g, double* points /* (E, m, p+1) */);
+int bzg_graph_copy_csr(bzg_graph* g, int64_t* row_ptr /* (V+1,) */, int32_t* col /* (E,) */);
+/* device-to-device export into caller-allocated device buffers (NCCL gather) */
+int bzg_graph_export_device(bzg_graph* g, int32_t* src, int32_t* dst, double* cost);
+
+/* replaces reachability.check_edges (reachability.py:139-142): out[k] = 1 iff
+ * X1[k] F1' + X2[k] F2' <= G + eps row-wise (same separable arithmetic as the build) */
+int bzg_check_edges(bzg_ctx* ctx, int32_t n, int32_t n_F, const double* F, const double* G, double eps,
+                    int64_t k, const double* X1, const double* X2, uint8_t* out);
+
+/* ---- a7..a10: cut_graph (reference graph.py:302-350) -------------------- */
+typedef struct {
+  double eps_cut;     /* CutConfig.eps_cut (graph.py:44) */
+  double heur_margin; /* CutConfig.heur_margin (graph.py:45) */
+  double eps_geo;     /* CutConfig.eps_geo (graph.py:46) */
+  int32_t qp_max_iter;/* CutConfig.qp (graph.py:47-49) -> SolveConfig (qpsolver.py:60-72) */
+  double qp_eps_abs, qp_eps_rel, qp_rho, qp_sigma, qp_alpha, qp_eps_pinf;
+  int32_t qp_polish;
+} bzg_cut_config;
+
+/* Obstacles in list order.  Rows of obstacle o are rows [row_off[o], row_off[o+1])
+ * of A (rows x m) / b, ALREADY NORMALISED (Polytope.normalized, geometry.py:135-137).
+ * is_box[o] != 0 marks obstacles recovered by Polytope.as_box (geometry.py:155-185)
+ * with the recovered bounds box_lo/box_hi (o*m ... o*m+m-1).  Non-box obstacles
+ * return BZG_EUNSUPPORTED (the general heuristic, graph.py:202-221, is not on device yet). */
+int bzg_cut_graph(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_off, const double* A,
+                  const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                  const bzg_cut_config* cfg, bzg_mask** out);
+int bzg_mask_destroy(bzg_mask* mk);
+/* counters: pairs_total, pairs_point_hit, pairs_hyperplane, pairs_qp, qp_safe, qp_unsafe (graph.py:97-102) */
+int bzg_mask_copy(bzg_mask* mk, uint8_t* alive /* (E,) */, uint8_t* provenance /* (E,) */, int64_t counters[6]);
+/* QP diagnostics of the last cut: per solved instance (edge, obstacle, status, iterations, ||delta||) */
+int bzg_mask_qp_count(bzg_mask* mk, int64_t* n);
+int bzg_mask_copy_qp(bzg_mask* mk, int64_t* edge, int32_t* obstacle, int8_t* status, int32_t* iters, double* delta);
+/* assemble a mask from alive/provenance arrays (multi-GPU gather) */
+int bzg_mask_from_arrays(bzg_ctx* ctx, bzg_graph* g, const uint8_t* alive, const uint8_t* provenance,
+                         const int64_t counters[6], int on_device, bzg_mask** out);
+int bzg_mask_export_device(bzg_mask* mk, uint8_t* alive, uint8_t* provenance);
+
+/* ---- a11..a13: find_path (reference graph.py:353-430) ------------------- */
+/* path_out: caller buffer of path_cap entries; *path_len = -1 means None (no path).
+ * tube_lo/tube_hi: oracle.tube.error box (n,).  *dist_out = path cost (graph.py:453-458). */
+int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start, const double* goal,
+                  const double* tube_lo, const double* tube_hi, double eps_geo, int position_only_snap,
+                  int require_tube_snap, int64_t* path_out, int64_t path_cap, int64_t* path_len,
+                  double* dist_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BZG_H */

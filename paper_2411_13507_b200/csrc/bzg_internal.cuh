@@ -1,0 +1,204 @@
+// Internal runtime of libbzg: context, device buffers, launch accounting.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/bzg.h"
+
+namespace bzg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define BZG_CHECK_CUDA(call)                                                                  \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw ::bzg::Error(BZG_ECUDA, std::string(#call) + " failed: " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define BZG_REQUIRE(cond, code, msg)          \
+  do {                                        \
+    if (!(cond)) throw ::bzg::Error(code, msg); \
+  } while (0)
+
+struct Ctx;
+
+// Stream-ordered device allocation owned by the library.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      ptr = o.ptr; bytes = o.bytes; stream = o.stream;
+      o.ptr = nullptr; o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t nbytes, cudaStream_t s) {
+    if (nbytes <= bytes && ptr) return;
+    release();
+    stream = s;
+    if (nbytes == 0) nbytes = 16;
+    BZG_CHECK_CUDA(cudaMallocAsync(&ptr, nbytes, s));
+    bytes = nbytes;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct KernelStat {
+  double ms = 0.0;
+  long long count = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  bool profiling = false;
+  long long launches = 0;
+  struct Pending { std::string name; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> spare;
+  std::vector<std::string> order;
+  std::unordered_map<std::string, KernelStat> stats;
+  DevBuf scratch;       // cub temp storage
+  DevBuf flag;          // small device scalars
+  void* pinned = nullptr;  // small pinned host staging area
+  size_t pinned_bytes = 0;
+
+  cudaEvent_t take_event() {
+    if (!spare.empty()) { cudaEvent_t e = spare.back(); spare.pop_back(); return e; }
+    cudaEvent_t e;
+    BZG_CHECK_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  void drain_profile() {
+    if (pending.empty()) return;
+    BZG_CHECK_CUDA(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+      float ms = 0.f;
+      BZG_CHECK_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+      auto it = stats.find(p.name);
+      if (it == stats.end()) { order.push_back(p.name); it = stats.emplace(p.name, KernelStat{}).first; }
+      it->second.ms += ms;
+      it->second.count += 1;
+      spare.push_back(p.a);
+      spare.push_back(p.b);
+    }
+    pending.clear();
+  }
+  void* host_scratch(size_t bytes) {
+    if (bytes > pinned_bytes) {
+      if (pinned) cudaFreeHost(pinned);
+      BZG_CHECK_CUDA(cudaMallocHost(&pinned, bytes));
+      pinned_bytes = bytes;
+    }
+    return pinned;
+  }
+};
+
+// Launch a kernel on the context stream, counting it and (when profiling) timing it
+// with a pair of CUDA events recorded on the same stream.
+template <typename... KArgs, typename... Args>
+inline void launch(Ctx* c, const char* name, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   Args&&... args) {
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->profiling) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
+  kern<<<grid, block, smem, c->stream>>>(std::forward<Args>(args)...);
+  BZG_CHECK_CUDA(cudaGetLastError());
+  c->launches++;
+  if (c->profiling) {
+    b = c->take_event();
+    BZG_CHECK_CUDA(cudaEventRecord(b, c->stream));
+    c->pending.push_back({name, a, b});
+  }
+}
+
+// Record an externally launched (library) kernel group, e.g. CUB scans.
+struct ScopedLibLaunch {
+  Ctx* c; const char* name; cudaEvent_t a = nullptr; int n;
+  ScopedLibLaunch(Ctx* ctx, const char* nm, int nkernels) : c(ctx), name(nm), n(nkernels) {
+    if (c->profiling) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
+  }
+  ~ScopedLibLaunch() {
+    c->launches += n;
+    if (c->profiling) {
+      cudaEvent_t b = c->take_event();
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({name, a, b});
+    }
+  }
+};
+
+inline unsigned div_up(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- graph / mask
+struct Graph {
+  Ctx* ctx = nullptr;
+  int m = 0, gamma = 0, p = 0, n = 0;
+  int64_t V = 0, E = 0;
+  int64_t row_begin = 0, row_end = 0;
+  std::vector<double> D;          // (p+1) x 2*gamma, host copy (kernel parameter)
+  DevBuf vertices;                // V x n
+  DevBuf row_ptr;                 // V+1 int64 (global row index)
+  DevBuf src, dst;                // E int32
+  DevBuf cost;                    // E double
+  DevBuf points;                  // lazily materialised E x m x (p+1)
+  bool points_ready = false;
+};
+
+struct Mask {
+  Graph* g = nullptr;
+  int64_t E = 0;
+  int32_t n_obs = 0;
+  DevBuf alive;                   // E uint8
+  DevBuf prov;                    // E uint8
+  int64_t counters[6] = {0, 0, 0, 0, 0, 0};
+  // QP diagnostics
+  int64_t n_qp = 0;
+  DevBuf qp_edge, qp_obs, qp_status, qp_iters, qp_delta;
+  // cached shortest-path tree (reused while (mask, v0) is unchanged: cfg4 replanning)
+  int64_t tree_v0 = -1;
+  DevBuf dist, parent;
+  // cached reverse reachability to vg (relaxed snapping)
+  int64_t reach_vg = -1;
+  DevBuf reach;
+};
+
+// Kernel-family entry points (defined in the k_*.cu translation units).
+void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices);
+void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g);
+void materialize_points(Ctx* c, Graph* g);
+void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, double eps, int64_t k,
+                 const double* X1, const double* X2, uint8_t* out);
+void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+               const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+               Mask* mk);
+void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
+               const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
+               double* dist);
+
+}  // namespace bzg

@@ -1,0 +1,457 @@
+// extern "C" boundary of libbzg (declarations and reference citations in include/bzg.h).
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bzg_internal.cuh"
+
+using namespace bzg;
+
+struct bzg_ctx : Ctx {};
+struct bzg_graph : Graph {};
+struct bzg_mask : Mask {};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BZG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return BZG_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return BZG_EINVAL;
+  }
+}
+
+void set_device(Ctx* c) { BZG_CHECK_CUDA(cudaSetDevice(c->device)); }
+
+}  // namespace
+
+extern "C" {
+
+int bzg_abi_version(void) { return BZG_ABI_VERSION; }
+
+const char* bzg_last_error(void) { return g_last_error.c_str(); }
+
+int bzg_ctx_create(int device, void* stream, bzg_ctx** out) {
+  return guarded([&] {
+    BZG_REQUIRE(out, BZG_EINVAL, "null output pointer");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    BZG_REQUIRE(e == cudaSuccess && ndev > 0, BZG_ENODEV,
+                std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    BZG_REQUIRE(device >= 0 && device < ndev, BZG_ENODEV, "device ordinal out of range");
+    cudaDeviceProp prop;
+    BZG_CHECK_CUDA(cudaGetDeviceProperties(&prop, device));
+    BZG_REQUIRE(prop.major == 10, BZG_ENODEV,
+                std::string("libbzg is built for sm_100a (B200); device is ") + prop.name);
+    auto* c = new bzg_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    BZG_CHECK_CUDA(cudaSetDevice(device));
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+      c->own_stream = false;
+    } else {
+      BZG_CHECK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    // keep freed pool memory cached across builds (stream-ordered allocator)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = c;
+  });
+}
+
+int bzg_ctx_destroy(bzg_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    set_device(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->scratch.release();
+    ctx->flag.release();
+    ctx->drain_profile();
+    for (auto e : ctx->spare) cudaEventDestroy(e);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int bzg_ctx_stream(bzg_ctx* ctx, void** stream_out) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && stream_out, BZG_EINVAL, "null argument");
+    *stream_out = ctx->stream;
+  });
+}
+
+int bzg_ctx_synchronize(bzg_ctx* ctx) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx, BZG_EINVAL, "null context");
+    set_device(ctx);
+    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int bzg_ctx_set_profiling(bzg_ctx* ctx, int enabled) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx, BZG_EINVAL, "null context");
+    ctx->profiling = enabled != 0;
+  });
+}
+
+int bzg_ctx_stats(bzg_ctx* ctx, long long* launches, int n_cap, char* names, double* ms, long long* counts,
+                  int* n_out) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx, BZG_EINVAL, "null context");
+    set_device(ctx);
+    ctx->drain_profile();
+    if (launches) *launches = ctx->launches;
+    const int n = (int)ctx->order.size();
+    if (n_out) *n_out = n;
+    for (int i = 0; i < n && i < n_cap; ++i) {
+      const auto& s = ctx->stats[ctx->order[i]];
+      if (names) {
+        std::strncpy(names + 64 * i, ctx->order[i].c_str(), 63);
+        names[64 * i + 63] = 0;
+      }
+      if (ms) ms[i] = s.ms;
+      if (counts) counts[i] = s.count;
+    }
+  });
+}
+
+int bzg_ctx_reset_stats(bzg_ctx* ctx) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx, BZG_EINVAL, "null context");
+    set_device(ctx);
+    ctx->drain_profile();
+    ctx->stats.clear();
+    ctx->order.clear();
+    ctx->launches = 0;
+  });
+}
+
+int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
+  bzg_graph* g = nullptr;
+  int rc = guarded([&] {
+    BZG_REQUIRE(ctx && d && out, BZG_EINVAL, "null argument");
+    set_device(ctx);
+    BZG_REQUIRE(d->m >= 1 && d->gamma >= 1, BZG_EINVAL, "require m >= 1 and gamma >= 1");
+    BZG_REQUIRE(d->p == 2 * d->gamma - 1, BZG_EINVAL, "boundary-value curves require p = 2*gamma - 1");
+    BZG_REQUIRE(d->N >= 2, BZG_EINVAL, "need at least two vertices");  // graph.py:143-144
+    BZG_REQUIRE(d->F && d->G && d->D, BZG_EINVAL, "oracle F, G and boundary matrix D are required");
+    BZG_REQUIRE(d->n_include >= 0 && (d->n_include == 0 || d->include), BZG_EINVAL, "include rows missing");
+    const int n = d->m * d->gamma;
+    g = new bzg_graph();
+    g->ctx = ctx;
+    g->m = d->m;
+    g->gamma = d->gamma;
+    g->p = d->p;
+    g->n = n;
+    g->V = d->N + d->n_include;
+    g->row_begin = d->row_begin;
+    g->row_end = d->row_end > 0 ? d->row_end : g->V;
+    BZG_REQUIRE(g->row_begin >= 0 && g->row_begin <= g->row_end && g->row_end <= g->V, BZG_EINVAL,
+                "row block out of range");
+    BZG_REQUIRE(g->V < (1ll << 31), BZG_EUNSUPPORTED, "vertex count exceeds int32 indexing");
+    g->D.assign(d->D, d->D + (size_t)(d->p + 1) * 2 * d->gamma);
+    g->vertices.alloc((size_t)g->V * n * sizeof(double), ctx->stream);
+    if (d->vertices) {
+      BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.ptr, d->vertices, (size_t)d->N * n * sizeof(double),
+                                     cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+      BZG_REQUIRE(d->sample_lo && d->sample_hi && d->xd_A && d->xd_b, BZG_EINVAL, "sampler inputs missing");
+      sample_states(ctx, d, g->vertices.as<double>());
+    }
+    if (d->n_include > 0)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)d->N * n, d->include,
+                                     (size_t)d->n_include * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    build_pairs(ctx, d, g);
+  });
+  if (rc == BZG_OK) {
+    *out = g;
+  } else {
+    delete g;
+  }
+  return rc;
+}
+
+int bzg_graph_from_edges(bzg_ctx* ctx, int32_t m, int32_t gamma, int32_t p, const double* D, int64_t V,
+                         const double* vertices_host, int64_t E, const int32_t* src, const int32_t* dst,
+                         const double* cost, int on_device, bzg_graph** out) {
+  bzg_graph* g = nullptr;
+  int rc = guarded([&] {
+    BZG_REQUIRE(ctx && D && vertices_host && out, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(p == 2 * gamma - 1, BZG_EINVAL, "boundary-value curves require p = 2*gamma - 1");
+    set_device(ctx);
+    g = new bzg_graph();
+    g->ctx = ctx;
+    g->m = m; g->gamma = gamma; g->p = p; g->n = m * gamma;
+    g->V = V; g->E = E; g->row_begin = 0; g->row_end = V;
+    g->D.assign(D, D + (size_t)(p + 1) * 2 * gamma);
+    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    g->vertices.alloc((size_t)V * g->n * sizeof(double), ctx->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.ptr, vertices_host, (size_t)V * g->n * sizeof(double),
+                                   cudaMemcpyHostToDevice, ctx->stream));
+    g->src.alloc(E * sizeof(int), ctx->stream);
+    g->dst.alloc(E * sizeof(int), ctx->stream);
+    g->cost.alloc(E * sizeof(double), ctx->stream);
+    if (E > 0) {
+      BZG_CHECK_CUDA(cudaMemcpyAsync(g->src.ptr, src, E * sizeof(int), kind, ctx->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(g->dst.ptr, dst, E * sizeof(int), kind, ctx->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(g->cost.ptr, cost, E * sizeof(double), kind, ctx->stream));
+    }
+    // row_ptr from the (row-major ordered) sources
+    std::vector<int> hs(E);
+    if (E > 0) BZG_CHECK_CUDA(cudaMemcpyAsync(hs.data(), g->src.ptr, E * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<long long> rp(V + 1, 0);
+    for (long long e = 0; e < E; ++e) {
+      BZG_REQUIRE(hs[e] >= 0 && hs[e] < V && (e == 0 || hs[e] >= hs[e - 1]), BZG_EINVAL,
+                  "edges must be sorted by source");
+      rp[hs[e] + 1]++;
+    }
+    for (long long i = 0; i < V; ++i) rp[i + 1] += rp[i];
+    g->row_ptr.alloc((V + 1) * sizeof(long long), ctx->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->row_ptr.ptr, rp.data(), (V + 1) * sizeof(long long), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+  if (rc == BZG_OK) *out = g; else delete g;
+  return rc;
+}
+
+int bzg_graph_destroy(bzg_graph* g) {
+  return guarded([&] {
+    if (!g) return;
+    set_device(g->ctx);
+    delete g;
+  });
+}
+
+int bzg_graph_info(const bzg_graph* g, int64_t* V, int64_t* E, int64_t* row_begin, int64_t* row_end) {
+  return guarded([&] {
+    BZG_REQUIRE(g, BZG_EINVAL, "null graph");
+    if (V) *V = g->V;
+    if (E) *E = g->E;
+    if (row_begin) *row_begin = g->row_begin;
+    if (row_end) *row_end = g->row_end;
+  });
+}
+
+int bzg_graph_copy_vertices(bzg_graph* g, double* vertices) {
+  return guarded([&] {
+    BZG_REQUIRE(g, BZG_EINVAL, "null graph");
+    set_device(g->ctx);
+    if (vertices)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(vertices, g->vertices.ptr, (size_t)g->V * g->n * sizeof(double),
+                                     cudaMemcpyDeviceToHost, g->ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  });
+}
+
+int bzg_graph_copy_edges(bzg_graph* g, int64_t* edges, double* costs) {
+  return guarded([&] {
+    BZG_REQUIRE(g, BZG_EINVAL, "null graph");
+    set_device(g->ctx);
+    const long long E = g->E;
+    if (edges && E > 0) {
+      std::vector<int> s(E), t(E);
+      BZG_CHECK_CUDA(cudaMemcpyAsync(s.data(), g->src.ptr, E * sizeof(int), cudaMemcpyDeviceToHost, g->ctx->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(t.data(), g->dst.ptr, E * sizeof(int), cudaMemcpyDeviceToHost, g->ctx->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+      for (long long e = 0; e < E; ++e) {
+        edges[2 * e] = s[e];
+        edges[2 * e + 1] = t[e];
+      }
+    }
+    if (costs && E > 0)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(costs, g->cost.ptr, E * sizeof(double), cudaMemcpyDeviceToHost, g->ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  });
+}
+
+int bzg_graph_copy_points(bzg_graph* g, double* points) {
+  return guarded([&] {
+    BZG_REQUIRE(g, BZG_EINVAL, "null graph");
+    set_device(g->ctx);
+    materialize_points(g->ctx, g);
+    if (points && g->E > 0)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(points, g->points.ptr, (size_t)g->E * g->m * (g->p + 1) * sizeof(double),
+                                     cudaMemcpyDeviceToHost, g->ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  });
+}
+
+int bzg_graph_copy_csr(bzg_graph* g, int64_t* row_ptr, int32_t* col) {
+  return guarded([&] {
+    BZG_REQUIRE(g, BZG_EINVAL, "null graph");
+    set_device(g->ctx);
+    if (row_ptr)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(row_ptr, g->row_ptr.ptr, (g->V + 1) * sizeof(long long), cudaMemcpyDeviceToHost,
+                                     g->ctx->stream));
+    if (col && g->E > 0)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(col, g->dst.ptr, g->E * sizeof(int), cudaMemcpyDeviceToHost, g->ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  });
+}
+
+int bzg_graph_export_device(bzg_graph* g, int32_t* src, int32_t* dst, double* cost) {
+  return guarded([&] {
+    BZG_REQUIRE(g, BZG_EINVAL, "null graph");
+    set_device(g->ctx);
+    const long long E = g->E;
+    if (E > 0) {
+      if (src) BZG_CHECK_CUDA(cudaMemcpyAsync(src, g->src.ptr, E * 4, cudaMemcpyDeviceToDevice, g->ctx->stream));
+      if (dst) BZG_CHECK_CUDA(cudaMemcpyAsync(dst, g->dst.ptr, E * 4, cudaMemcpyDeviceToDevice, g->ctx->stream));
+      if (cost) BZG_CHECK_CUDA(cudaMemcpyAsync(cost, g->cost.ptr, E * 8, cudaMemcpyDeviceToDevice, g->ctx->stream));
+    }
+    BZG_CHECK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  });
+}
+
+int bzg_check_edges(bzg_ctx* ctx, int32_t n, int32_t n_F, const double* F, const double* G, double eps, int64_t k,
+                    const double* X1, const double* X2, uint8_t* out) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && F && G && (k == 0 || (X1 && X2 && out)), BZG_EINVAL, "null argument");
+    set_device(ctx);
+    check_edges(ctx, n, n_F, F, G, eps, k, X1, X2, out);
+  });
+}
+
+int bzg_cut_graph(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_off, const double* A, const double* b,
+                  const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                  bzg_mask** out) {
+  bzg_mask* mk = nullptr;
+  int rc = guarded([&] {
+    BZG_REQUIRE(ctx && g && cfg && out, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(n_obs == 0 || (row_off && A && b && is_box && box_lo && box_hi), BZG_EINVAL, "obstacle arrays missing");
+    set_device(ctx);
+    mk = new bzg_mask();
+    cut_graph(ctx, g, n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg, mk);
+  });
+  if (rc == BZG_OK) *out = mk; else delete mk;
+  return rc;
+}
+
+int bzg_mask_destroy(bzg_mask* mk) {
+  return guarded([&] {
+    if (!mk) return;
+    if (mk->g) set_device(mk->g->ctx);
+    delete mk;
+  });
+}
+
+int bzg_mask_copy(bzg_mask* mk, uint8_t* alive, uint8_t* provenance, int64_t counters[6]) {
+  return guarded([&] {
+    BZG_REQUIRE(mk && mk->g, BZG_EINVAL, "null mask");
+    Ctx* c = mk->g->ctx;
+    set_device(c);
+    if (alive && mk->E > 0) BZG_CHECK_CUDA(cudaMemcpyAsync(alive, mk->alive.ptr, mk->E, cudaMemcpyDeviceToHost, c->stream));
+    if (provenance && mk->E > 0)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(provenance, mk->prov.ptr, mk->E, cudaMemcpyDeviceToHost, c->stream));
+    if (counters)
+      for (int i = 0; i < 6; ++i) counters[i] = mk->counters[i];
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bzg_mask_qp_count(bzg_mask* mk, int64_t* n) {
+  return guarded([&] {
+    BZG_REQUIRE(mk && n, BZG_EINVAL, "null argument");
+    *n = mk->n_qp;
+  });
+}
+
+int bzg_mask_copy_qp(bzg_mask* mk, int64_t* edge, int32_t* obstacle, int8_t* status, int32_t* iters, double* delta) {
+  return guarded([&] {
+    BZG_REQUIRE(mk && mk->g, BZG_EINVAL, "null mask");
+    Ctx* c = mk->g->ctx;
+    set_device(c);
+    const long long n = mk->n_qp;
+    if (n > 0) {
+      if (edge) BZG_CHECK_CUDA(cudaMemcpyAsync(edge, mk->qp_edge.ptr, n * 8, cudaMemcpyDeviceToHost, c->stream));
+      if (obstacle) BZG_CHECK_CUDA(cudaMemcpyAsync(obstacle, mk->qp_obs.ptr, n * 4, cudaMemcpyDeviceToHost, c->stream));
+      if (status) BZG_CHECK_CUDA(cudaMemcpyAsync(status, mk->qp_status.ptr, n, cudaMemcpyDeviceToHost, c->stream));
+      if (iters) BZG_CHECK_CUDA(cudaMemcpyAsync(iters, mk->qp_iters.ptr, n * 4, cudaMemcpyDeviceToHost, c->stream));
+      if (delta) BZG_CHECK_CUDA(cudaMemcpyAsync(delta, mk->qp_delta.ptr, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bzg_mask_from_arrays(bzg_ctx* ctx, bzg_graph* g, const uint8_t* alive, const uint8_t* provenance,
+                         const int64_t counters[6], int on_device, bzg_mask** out) {
+  bzg_mask* mk = nullptr;
+  int rc = guarded([&] {
+    BZG_REQUIRE(ctx && g && alive && out, BZG_EINVAL, "null argument");
+    set_device(ctx);
+    mk = new bzg_mask();
+    mk->g = g;
+    mk->E = g->E;
+    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    mk->alive.alloc(std::max<long long>(g->E, 1), ctx->stream);
+    mk->prov.alloc(std::max<long long>(g->E, 1), ctx->stream);
+    if (g->E > 0) {
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->alive.ptr, alive, g->E, kind, ctx->stream));
+      if (provenance) BZG_CHECK_CUDA(cudaMemcpyAsync(mk->prov.ptr, provenance, g->E, kind, ctx->stream));
+      else BZG_CHECK_CUDA(cudaMemsetAsync(mk->prov.ptr, BZG_HEURISTIC_SAFE, g->E, ctx->stream));
+    }
+    if (counters)
+      for (int i = 0; i < 6; ++i) mk->counters[i] = counters[i];
+    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+  if (rc == BZG_OK) *out = mk; else delete mk;
+  return rc;
+}
+
+int bzg_mask_export_device(bzg_mask* mk, uint8_t* alive, uint8_t* provenance) {
+  return guarded([&] {
+    BZG_REQUIRE(mk && mk->g, BZG_EINVAL, "null mask");
+    Ctx* c = mk->g->ctx;
+    set_device(c);
+    if (mk->E > 0) {
+      if (alive) BZG_CHECK_CUDA(cudaMemcpyAsync(alive, mk->alive.ptr, mk->E, cudaMemcpyDeviceToDevice, c->stream));
+      if (provenance) BZG_CHECK_CUDA(cudaMemcpyAsync(provenance, mk->prov.ptr, mk->E, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start, const double* goal,
+                  const double* tube_lo, const double* tube_hi, double eps_geo, int position_only_snap,
+                  int require_tube_snap, int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && g && start && goal && tube_lo && tube_hi && path_len, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(!mk || mk->g == g, BZG_EINVAL, "mask belongs to another graph");
+    set_device(ctx);
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    find_path(ctx, g, mk, start, goal, tube_lo, tube_hi, eps_geo, position_only_snap, require_tube_snap, path, &dist);
+    if (path.empty()) {
+      *path_len = -1;
+    } else {
+      *path_len = (int64_t)path.size();
+      BZG_REQUIRE(path_out && path_cap >= (int64_t)path.size(), BZG_EINVAL, "path buffer too small");
+      std::memcpy(path_out, path.data(), path.size() * sizeof(int64_t));
+    }
+    if (dist_out) *dist_out = dist;
+  });
+}
+
+}  // extern "C"

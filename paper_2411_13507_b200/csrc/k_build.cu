@@ -1,0 +1,493 @@
+// Graph build on device: PCG64 state sampling, oracle projections, all-pairs
+// reachability test into a bit matrix, ordered CSR compaction and edge costs.
+//
+// Replaces reference graph.py:147-197 (build_graph).  Arithmetic order follows
+// SURVEY.md §8(c) so vertices, edges, costs and control points are bitwise equal
+// to the reference.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "bzg_internal.cuh"
+#include "bzg_math.cuh"
+
+namespace bzg {
+
+namespace {
+
+constexpr int kMaxN = 16;        // reduced state dimension n = m*gamma
+constexpr int kMaxRows = 64;     // rows of the sampler's state polytope
+constexpr int kMaxIntervals = 64;
+
+struct SampleParams {
+  double lo[kMaxN], range[kMaxN];
+  double A[kMaxRows * kMaxN];
+  double b_eps[kMaxRows];
+  int n, rows;
+};
+
+// One thread per candidate row: jump the PCG64 stream to draw row*n, draw the n
+// uniforms of that row (geometry.py:69-72 -> numpy random_uniform: lo + range*u,
+// range = hi - lo) and test Xd membership (geometry.py:145-148).
+__global__ void k_sample_candidates(SampleParams sp, unsigned long long st_hi, unsigned long long st_lo,
+                                    unsigned long long inc_hi, unsigned long long inc_lo, long long row0,
+                                    long long count, double* __restrict__ cand, int* __restrict__ flag) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const u128 inc = ((u128)inc_hi << 64) | inc_lo;
+  u128 s = ((u128)st_hi << 64) | st_lo;
+  s = pcg_advance(s, inc, (uint64_t)(row0 + t) * (uint64_t)sp.n);
+  double x[kMaxN];
+  for (int k = 0; k < sp.n; ++k) {
+    const double u = pcg_next_double(s, inc);
+    x[k] = __dadd_rn(sp.lo[k], __dmul_rn(sp.range[k], u));
+    cand[t * sp.n + k] = x[k];
+  }
+  int ok = 1;
+  for (int c = 0; c < sp.rows; ++c) ok &= fma_chain(x, sp.A + c * sp.n, sp.n) <= sp.b_eps[c];
+  flag[t] = ok;
+}
+
+__global__ void k_sample_scatter(const double* __restrict__ cand, const int* __restrict__ flag,
+                                 const int* __restrict__ pos, long long count, int n, long long need,
+                                 double* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= count || !flag[t]) return;
+  const long long p = pos[t];
+  if (p >= need) return;
+  for (int k = 0; k < n; ++k) out[p * n + k] = cand[t * n + k];
+}
+
+// ---------------------------------------------------------------- projections
+struct RowPlan {
+  int n, K, n_src, n_dst;
+  int row_iv[kMaxIntervals];   // F row of each interval (the "+" row of a negation pair)
+  int row_src[kMaxIntervals];  // x1-only rows (F2 row == 0)
+  int row_dst[kMaxIntervals];  // x2-only rows (F1 row == 0)
+  double th_src[kMaxIntervals], th_dst[kMaxIntervals];
+};
+
+// a1c[i, q] = V_i . F1[row_iv[q]],  a2t[q, i] = V_i . F2[row_iv[q]] (FMA chain, graph.py:174-175);
+// src_ok / dst_ok fold the one-sided rows into per-vertex predicates (exact: the other
+// side's product is +-0).
+__global__ void k_project(RowPlan rp, const double* __restrict__ F, const double* __restrict__ Vx, long long V,
+                          int Kpad, double* __restrict__ a1c, double* __restrict__ a2t, uint8_t* __restrict__ src_ok,
+                          uint8_t* __restrict__ dst_ok) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const int n = rp.n;
+  double v[kMaxN];
+  for (int k = 0; k < n; ++k) v[k] = Vx[i * n + k];
+  for (int q = 0; q < Kpad; ++q) {
+    double x1 = 0.0, x2 = 0.0;
+    if (q < rp.K) {
+      const double* f = F + (size_t)rp.row_iv[q] * 2 * n;
+      x1 = fma_chain(v, f, n);
+      x2 = fma_chain(v, f + n, n);
+    }
+    a1c[i * Kpad + q] = x1;
+    a2t[(long long)q * V + i] = x2;
+  }
+  int ok = 1;
+  for (int q = 0; q < rp.n_src; ++q) ok &= fma_chain(v, F + (size_t)rp.row_src[q] * 2 * n, n) <= rp.th_src[q];
+  src_ok[i] = (uint8_t)ok;
+  ok = 1;
+  for (int q = 0; q < rp.n_dst; ++q) ok &= fma_chain(v, F + (size_t)rp.row_dst[q] * 2 * n + n, n) <= rp.th_dst[q];
+  dst_ok[i] = (uint8_t)ok;
+}
+
+// ---------------------------------------------------------------- pair test
+struct Bounds {
+  double lo[kMaxIntervals], hi[kMaxIntervals];
+};
+
+constexpr int kPairThreads = 256;  // dst columns per block (8 warps x 32)
+constexpr int kPairRows = 32;      // src rows per block
+
+// Bit (i, j) of the pair matrix: fl(a1[i,r] + a2[j,r]) <= G_r + eps for every row r
+// (graph.py:181-182), evaluated as intervals lo_q <= a1c[i,q] + a2[j,q] <= hi_q over the
+// negation pairs, plus the per-vertex one-sided predicates; the diagonal is cleared
+// (graph.py:184).  One warp ballots 32 destinations into one 32-bit word.
+template <int K>
+__global__ void __launch_bounds__(kPairThreads) k_pair_bits(Bounds bd, const double* __restrict__ a1c,
+                                                            const double* __restrict__ a2t,
+                                                            const uint8_t* __restrict__ src_ok,
+                                                            const uint8_t* __restrict__ dst_ok, long long V,
+                                                            long long r0, long long r1, long long W,
+                                                            uint32_t* __restrict__ bits,
+                                                            unsigned long long* __restrict__ rowcnt) {
+  __shared__ double s_a1[kPairRows][K];
+  __shared__ uint8_t s_ok[kPairRows];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const long long j = (long long)blockIdx.x * kPairThreads + tid;
+  const long long i0 = r0 + (long long)blockIdx.y * kPairRows;
+  const int rows = (int)min((long long)kPairRows, r1 - i0);
+
+  for (int e = tid; e < rows * K; e += kPairThreads) {
+    const int ii = e / K, q = e - ii * K;
+    s_a1[ii][q] = a1c[(i0 + ii) * K + q];
+  }
+  if (tid < rows) s_ok[tid] = src_ok[i0 + tid];
+
+  double a2[K];
+  bool jok = j < V;
+  if (jok) {
+#pragma unroll
+    for (int q = 0; q < K; ++q) a2[q] = a2t[(long long)q * V + j];
+    jok = dst_ok[j] != 0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < K; ++q) a2[q] = 0.0;
+  }
+  __syncthreads();
+
+  const long long word = (long long)blockIdx.x * (kPairThreads / 32) + warp;
+  if (word >= W) return;  // whole warp past the last word (uniform per warp)
+  for (int ii = 0; ii < rows; ++ii) {
+    const long long i = i0 + ii;
+    bool ok = jok && s_ok[ii] && (i != j);
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      if ((q & 3) == 0 && q > 0) {
+        if (!__any_sync(0xffffffffu, ok)) break;
+      }
+      const double s = __dadd_rn(s_a1[ii][q], a2[q]);
+      ok = ok && (s <= bd.hi[q]) && (s >= bd.lo[q]);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) {
+      bits[(i - r0) * W + word] = m;
+      if (m) atomicAdd(rowcnt + (i - r0), (unsigned long long)__popc(m));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- compaction
+struct DParams {
+  double D[64];
+};
+
+// One warp per source row: ordered expansion of the row's bit words into
+// (src, dst) in ascending dst (np.nonzero order, graph.py:187-190) and the edge cost
+// (graph.py:192-197) computed from the two endpoint states.
+template <int G, int M>
+__global__ void k_expand(DParams dp, const double* __restrict__ Vx, long long r0, long long r1, long long W,
+                         const uint32_t* __restrict__ bits, const long long* __restrict__ rptr,
+                         int* __restrict__ src, int* __restrict__ dst, double* __restrict__ cost) {
+  constexpr int N = G * M;
+  const int lane = threadIdx.x & 31;
+  const long long i = r0 + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (i >= r1) return;
+  long long base = rptr[i - r0];
+  const long long end = rptr[i - r0 + 1];
+  if (base == end) return;
+  double xi[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) xi[k] = Vx[i * N + k];
+  const uint32_t* row = bits + (i - r0) * W;
+  for (long long w0 = 0; w0 < W && base < end; w0 += 32) {
+    const long long w = w0 + lane;
+    uint32_t word = w < W ? row[w] : 0u;
+    const int c = __popc(word);
+    const int incl = warp_incl_scan(c);
+    long long off = base + incl - c;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      const long long jv = w * 32 + b;
+      double xj[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) xj[k] = Vx[jv * N + k];
+      double P[M][2 * G];
+      control_points<G, M>(xi, xj, dp.D, P);
+      src[off] = (int)i;
+      dst[off] = (int)jv;
+      cost[off] = polygon_length<G, M>(P);
+      ++off;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+template <int G, int M>
+__global__ void k_points(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
+                         const int* __restrict__ dst, double* __restrict__ out) {
+  constexpr int N = G * M;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  double xi[N], xj[N];
+  const long long a = src[e], b = dst[e];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    xi[k] = Vx[a * N + k];
+    xj[k] = Vx[b * N + k];
+  }
+  double P[M][2 * G];
+  control_points<G, M>(xi, xj, dp.D, P);
+#pragma unroll
+  for (int k = 0; k < M; ++k)
+#pragma unroll
+    for (int j = 0; j < 2 * G; ++j) out[e * M * 2 * G + k * 2 * G + j] = P[k][j];
+}
+
+__global__ void k_row_ptr_global(const long long* __restrict__ local, long long V, long long r0, long long r1,
+                                 long long* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > V) return;
+  const long long E = local[r1 - r0];
+  out[i] = i <= r0 ? 0 : (i >= r1 ? E : local[i - r0]);
+}
+
+// check_edges (reachability.py:139-142): X1 F1' + X2 F2' <= G + eps, separable form.
+__global__ void k_check_edges(const double* __restrict__ F, const double* __restrict__ thresh, int n, int nF,
+                              long long k, const double* __restrict__ X1, const double* __restrict__ X2,
+                              uint8_t* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  int ok = 1;
+  for (int r = 0; r < nF; ++r) {
+    const double* f = F + (size_t)r * 2 * n;
+    const double s = __dadd_rn(fma_chain(X1 + t * n, f, n), fma_chain(X2 + t * n, f + n, n));
+    ok &= s <= thresh[r];
+  }
+  out[t] = (uint8_t)ok;
+}
+
+template <typename F>
+void dispatch_gm(int G, int M, F&& f) {
+#define BZG_GM(g, m) \
+  if (G == g && M == m) { f(std::integral_constant<int, g>{}, std::integral_constant<int, m>{}); return; }
+  BZG_GM(1, 1) BZG_GM(1, 2) BZG_GM(1, 3) BZG_GM(2, 1) BZG_GM(2, 2) BZG_GM(2, 3)
+  BZG_GM(3, 1) BZG_GM(3, 2) BZG_GM(3, 3) BZG_GM(4, 1) BZG_GM(4, 2) BZG_GM(4, 3)
+#undef BZG_GM
+  throw Error(BZG_EUNSUPPORTED, "device path supports gamma in 1..4 and m in 1..3");
+}
+
+void exclusive_scan_ll(Ctx* c, const unsigned long long* in, long long* out, long long count) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, count, c->stream);
+  c->scratch.alloc(bytes, c->stream);
+  ScopedLibLaunch l(c, "cub_scan_rows", 2);
+  BZG_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(c->scratch.ptr, bytes, in, out, count, c->stream));
+}
+
+void exclusive_scan_i(Ctx* c, const int* in, int* out, long long count) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, count, c->stream);
+  c->scratch.alloc(bytes, c->stream);
+  ScopedLibLaunch l(c, "cub_scan_sample", 2);
+  BZG_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(c->scratch.ptr, bytes, in, out, count, c->stream));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices) {
+  const int n = d->m * d->gamma;
+  BZG_REQUIRE(n <= kMaxN, BZG_EUNSUPPORTED, "state dimension too large for the device sampler");
+  BZG_REQUIRE(d->xd_rows >= 1 && d->xd_rows <= kMaxRows, BZG_EUNSUPPORTED, "state polytope row count unsupported");
+  SampleParams sp{};
+  sp.n = n;
+  sp.rows = d->xd_rows;
+  for (int k = 0; k < n; ++k) {
+    sp.lo[k] = d->sample_lo[k];
+    sp.range[k] = d->sample_hi[k] - d->sample_lo[k];  // np.subtract(high, low)
+  }
+  for (int r = 0; r < d->xd_rows; ++r) {
+    for (int k = 0; k < n; ++k) sp.A[r * n + k] = d->xd_A[r * n + k];
+    sp.b_eps[r] = d->xd_b[r] + d->eps_geo;
+  }
+  long long need = d->N, row0 = 0, got = 0;
+  double est = 1.0;
+  DevBuf cand, flag, pos;
+  int* h = static_cast<int*>(c->host_scratch(2 * sizeof(int)));
+  for (int round = 0; need > 0; ++round) {
+    BZG_REQUIRE(round < 10000, BZG_EINVAL, "sampler made no progress: state polytope misses the sampling box");
+    long long count = (long long)std::ceil((double)need / std::max(est, 1e-3) * 1.05) + 256;
+    count = std::min<long long>(count, 1ll << 26);
+    cand.alloc(count * n * sizeof(double), c->stream);
+    flag.alloc((count + 1) * sizeof(int), c->stream);
+    pos.alloc((count + 1) * sizeof(int), c->stream);
+    launch(c, "k_sample_candidates", k_sample_candidates, dim3(div_up(count, 256)), dim3(256), 0, sp,
+           (unsigned long long)d->pcg_state_hi, (unsigned long long)d->pcg_state_lo,
+           (unsigned long long)d->pcg_inc_hi, (unsigned long long)d->pcg_inc_lo, row0, count, cand.as<double>(),
+           flag.as<int>());
+    BZG_CHECK_CUDA(cudaMemsetAsync(flag.as<int>() + count, 0, sizeof(int), c->stream));
+    exclusive_scan_i(c, flag.as<int>(), pos.as<int>(), count + 1);
+    launch(c, "k_sample_scatter", k_sample_scatter, dim3(div_up(count, 256)), dim3(256), 0, cand.as<double>(),
+           flag.as<int>(), pos.as<int>(), count, n, need, d_vertices + got * n);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(h, pos.as<int>() + count, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    const long long acc = h[0];
+    // Rows past the N-th acceptance were drawn but are never used, exactly like the
+    // reference whose rounds only ever draw `needed` rows (graph.py:150-156): the kept
+    // set is the first N accepted rows of the stream either way.
+    const long long take = std::min(acc, need);
+    got += take;
+    need -= take;
+    row0 += count;
+    est = std::max(1e-3, (double)acc / (double)count);
+  }
+}
+
+void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
+  const int n = g->n;
+  const int nF = d->n_F;
+  const long long V = g->V;
+  const long long r0 = g->row_begin, r1 = g->row_end;
+  const long long rows = r1 - r0;
+
+  // ---- host row plan: classify F rows (one-sided / negation-paired / unpaired)
+  RowPlan rp{};
+  Bounds bd{};
+  rp.n = n;
+  std::vector<double> th(nF);
+  for (int r = 0; r < nF; ++r) th[r] = d->G[r] + d->eps_geo;  // oracle.G + EPS_GEO (graph.py:176)
+  auto zero = [&](int r, int off) {
+    for (int k = 0; k < n; ++k)
+      if (d->F[(size_t)r * 2 * n + off + k] != 0.0) return false;
+    return true;
+  };
+  bool never = false;  // a constant row 0 <= thresh that fails kills every pair
+  std::vector<int> used(nF, 0);
+  std::vector<std::pair<int, std::pair<double, double>>> iv;  // row, (lo, hi)
+  for (int r = 0; r < nF; ++r) {
+    const bool z1 = zero(r, 0), z2 = zero(r, n);
+    if (z1 && z2) { if (!(0.0 <= th[r])) never = true; used[r] = 1; continue; }
+    if (z2) { BZG_REQUIRE(rp.n_src < kMaxIntervals, BZG_EUNSUPPORTED, "too many oracle rows"); rp.row_src[rp.n_src] = r; rp.th_src[rp.n_src++] = th[r]; used[r] = 1; continue; }
+    if (z1) { BZG_REQUIRE(rp.n_dst < kMaxIntervals, BZG_EUNSUPPORTED, "too many oracle rows"); rp.row_dst[rp.n_dst] = r; rp.th_dst[rp.n_dst++] = th[r]; used[r] = 1; continue; }
+  }
+  for (int r = 0; r < nF; ++r) {
+    if (used[r]) continue;
+    used[r] = 1;
+    double lo = -INFINITY;
+    for (int s = r + 1; s < nF; ++s) {
+      if (used[s]) continue;
+      bool neg = true;
+      for (int k = 0; k < 2 * n && neg; ++k) neg = d->F[(size_t)s * 2 * n + k] == -d->F[(size_t)r * 2 * n + k];
+      if (neg) {  // lhs_s = -lhs_r exactly, so lhs_s <= th_s  <=>  lhs_r >= -th_s
+        used[s] = 1;
+        lo = -th[s];
+        break;
+      }
+    }
+    iv.push_back({r, {lo, th[r]}});
+  }
+  BZG_REQUIRE((int)iv.size() <= kMaxIntervals, BZG_EUNSUPPORTED, "too many coupled oracle rows");
+  rp.K = (int)iv.size();
+  static const int kSizes[] = {4, 8, 12, 16, 24, 32, 48, 64};
+  int Kpad = 0;
+  for (int s : kSizes)
+    if (s >= rp.K) { Kpad = s; break; }
+  for (int q = 0; q < Kpad; ++q) {
+    if (q < rp.K) {
+      rp.row_iv[q] = iv[q].first;
+      bd.lo[q] = iv[q].second.first;
+      bd.hi[q] = iv[q].second.second;
+    } else {
+      bd.lo[q] = -INFINITY;
+      bd.hi[q] = INFINITY;
+    }
+  }
+
+  DevBuf dF;
+  dF.alloc((size_t)nF * 2 * n * sizeof(double), c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(dF.ptr, d->F, (size_t)nF * 2 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  DevBuf a1c, a2t, sok, dok;
+  a1c.alloc((size_t)V * Kpad * sizeof(double), c->stream);
+  a2t.alloc((size_t)V * Kpad * sizeof(double), c->stream);
+  sok.alloc(V, c->stream);
+  dok.alloc(V, c->stream);
+  launch(c, "k_project", k_project, dim3(div_up(V, 128)), dim3(128), 0, rp, dF.as<double>(),
+         g->vertices.as<double>(), V, Kpad, a1c.as<double>(), a2t.as<double>(), sok.as<uint8_t>(), dok.as<uint8_t>());
+
+  const long long W = (V + 31) / 32;
+  DevBuf bits, rowcnt, rptr;
+  bits.alloc((size_t)std::max(rows, 1ll) * W * sizeof(uint32_t), c->stream);
+  rowcnt.alloc((size_t)(rows + 1) * sizeof(unsigned long long), c->stream);
+  rptr.alloc((size_t)(rows + 1) * sizeof(long long), c->stream);
+  BZG_CHECK_CUDA(cudaMemsetAsync(rowcnt.ptr, 0, (rows + 1) * sizeof(unsigned long long), c->stream));
+  if (!never && rows > 0) {
+    dim3 grid(div_up(V, kPairThreads), div_up(rows, kPairRows));
+    auto go = [&](auto kern) {
+      launch(c, "k_pair_bits", kern, grid, dim3(kPairThreads), 0, bd, a1c.as<double>(), a2t.as<double>(),
+             sok.as<uint8_t>(), dok.as<uint8_t>(), V, r0, r1, W, bits.as<uint32_t>(),
+             rowcnt.as<unsigned long long>());
+    };
+    switch (Kpad) {
+      case 4: go(k_pair_bits<4>); break;
+      case 8: go(k_pair_bits<8>); break;
+      case 12: go(k_pair_bits<12>); break;
+      case 16: go(k_pair_bits<16>); break;
+      case 24: go(k_pair_bits<24>); break;
+      case 32: go(k_pair_bits<32>); break;
+      case 48: go(k_pair_bits<48>); break;
+      default: go(k_pair_bits<64>); break;
+    }
+  }
+  exclusive_scan_ll(c, rowcnt.as<unsigned long long>(), rptr.as<long long>(), rows + 1);
+  long long* h = static_cast<long long*>(c->host_scratch(sizeof(long long)));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h, rptr.as<long long>() + rows, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  const long long E = h[0];
+  BZG_REQUIRE(E < (1ll << 31), BZG_EUNSUPPORTED, "edge count exceeds the int32 CSR index range");
+  g->E = E;
+  g->src.alloc(E * sizeof(int), c->stream);
+  g->dst.alloc(E * sizeof(int), c->stream);
+  g->cost.alloc(E * sizeof(double), c->stream);
+  g->row_ptr.alloc((V + 1) * sizeof(long long), c->stream);
+  DParams dp{};
+  for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
+  if (E > 0) {
+    dispatch_gm(g->gamma, g->m, [&](auto G_, auto M_) {
+      constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+      launch(c, "k_expand", k_expand<Gc, Mc>, dim3(div_up(rows * 32, 256)), dim3(256), 0, dp,
+             g->vertices.as<double>(), r0, r1, W, bits.as<uint32_t>(), rptr.as<long long>(), g->src.as<int>(),
+             g->dst.as<int>(), g->cost.as<double>());
+    });
+  }
+  launch(c, "k_row_ptr_global", k_row_ptr_global, dim3(div_up(V + 1, 256)), dim3(256), 0, rptr.as<long long>(),
+         V, r0, r1, g->row_ptr.as<long long>());
+}
+
+void materialize_points(Ctx* c, Graph* g) {
+  if (g->points_ready) return;
+  const long long E = g->E;
+  g->points.alloc((size_t)std::max(E, 1ll) * g->m * (g->p + 1) * sizeof(double), c->stream);
+  DParams dp{};
+  for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
+  if (E > 0) {
+    dispatch_gm(g->gamma, g->m, [&](auto G_, auto M_) {
+      constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+      launch(c, "k_points", k_points<Gc, Mc>, dim3(div_up(E, 256)), dim3(256), 0, dp, g->vertices.as<double>(), E,
+             g->src.as<int>(), g->dst.as<int>(), g->points.as<double>());
+    });
+  }
+  g->points_ready = true;
+}
+
+void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, double eps, int64_t k,
+                 const double* X1, const double* X2, uint8_t* out) {
+  if (k <= 0) return;
+  std::vector<double> th(n_F);
+  for (int r = 0; r < n_F; ++r) th[r] = G[r] + eps;
+  DevBuf dF, dT, d1, d2, dout;
+  dF.alloc((size_t)n_F * 2 * n * 8, c->stream);
+  dT.alloc((size_t)n_F * 8, c->stream);
+  d1.alloc((size_t)k * n * 8, c->stream);
+  d2.alloc((size_t)k * n * 8, c->stream);
+  dout.alloc(k, c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(dF.ptr, F, (size_t)n_F * 2 * n * 8, cudaMemcpyHostToDevice, c->stream));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(dT.ptr, th.data(), (size_t)n_F * 8, cudaMemcpyHostToDevice, c->stream));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(d1.ptr, X1, (size_t)k * n * 8, cudaMemcpyHostToDevice, c->stream));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(d2.ptr, X2, (size_t)k * n * 8, cudaMemcpyHostToDevice, c->stream));
+  launch(c, "k_check_edges", k_check_edges, dim3(div_up(k, 256)), dim3(256), 0, dF.as<double>(), dT.as<double>(),
+         n, n_F, (long long)k, d1.as<double>(), d2.as<double>(), dout.as<uint8_t>());
+  BZG_CHECK_CUDA(cudaMemcpyAsync(out, dout.ptr, k, cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace bzg

@@ -1,0 +1,366 @@
+// Shortest path on device: start/goal snapping, (reverse) reachability, min-plus
+// Bellman-Ford relaxation to the fixed point, Dijkstra-equivalent parent rule and
+// backtracking.
+//
+// Replaces reference graph.py:353-430 (find_path) and graph.py:433-450 (_reaches_goal).
+// The fixed point d[v] = min_u fl(d[u] + c_uv) equals the heapq Dijkstra distances
+// (fl(x + c) is monotone in x and costs are positive), and parent[v] =
+// argmin_(d[u], u) over alive tight in-edges reproduces the heap's pop order, so the
+// node sequence and dist[vg] are bitwise those of the reference.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "bzg_internal.cuh"
+#include "bzg_math.cuh"
+
+namespace bzg {
+
+namespace {
+
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
+
+struct SnapParams {
+  double target[16];
+  double tlo[16], thi[16];  // start - v tube window: diff >= -hi - eps, diff <= -lo + eps
+  int n, m_norm;            // components entering the norm (n, or m when position-only)
+  int mode;                 // 0: goal (all vertices), 1: tube filter, 2: reach filter
+};
+
+// norm of (v - target) over the first m_norm components, numpy order (graph.py:375/379):
+// sqrt of the sequential sum of squares.
+__device__ __forceinline__ double snap_norm(const double* v, const SnapParams& sp) {
+  double d0 = __dsub_rn(v[0], sp.target[0]);
+  double s = __dmul_rn(d0, d0);
+  for (int k = 1; k < sp.m_norm; ++k) {
+    const double dk = __dsub_rn(v[k], sp.target[k]);
+    s = __dadd_rn(s, __dmul_rn(dk, dk));
+  }
+  return __dsqrt_rn(s);
+}
+
+// first argmin (value, index) over candidates; infinite values are skipped so an
+// all-excluded set returns index -1.
+__global__ void k_snap(SnapParams sp, const double* __restrict__ Vx, long long V, const uint8_t* __restrict__ reach,
+                       unsigned long long* __restrict__ best) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double val = INFINITY;
+  long long idx = -1;
+  if (i < V) {
+    const double* v = Vx + i * sp.n;
+    bool ok = true;
+    if (sp.mode == 1) {
+      for (int k = 0; k < sp.n; ++k) {
+        const double d = __dsub_rn(v[k], sp.target[k]);
+        ok = ok && d >= sp.tlo[k] && d <= sp.thi[k];
+      }
+    } else if (sp.mode == 2) {
+      ok = reach[i] != 0;
+    }
+    if (ok) {
+      val = snap_norm(v, sp);
+      idx = i;
+    }
+  }
+  // warp then block argmin, ties to the lower index
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, val, off);
+    const long long oi = __shfl_down_sync(0xffffffffu, idx, off);
+    if (oi >= 0 && (idx < 0 || ov < val || (ov == val && oi < idx))) { val = ov; idx = oi; }
+  }
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sv[w] = val; si[w] = idx; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x / 32;
+    val = lane < nw ? sv[lane] : INFINITY;
+    idx = lane < nw ? si[lane] : -1;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, val, off);
+      const long long oi = __shfl_down_sync(0xffffffffu, idx, off);
+      if (oi >= 0 && (idx < 0 || ov < val || (ov == val && oi < idx))) { val = ov; idx = oi; }
+    }
+    if (lane == 0 && idx >= 0) {
+      // best[0]: min value bits (values are >= 0, so bit order == value order)
+      atomicMin(best, dbits(val));
+      best[1 + blockIdx.x] = ((unsigned long long)dbits(val));
+      best[1 + gridDim.x + blockIdx.x] = (unsigned long long)idx;
+    } else if (lane == 0) {
+      best[1 + blockIdx.x] = kInfBits + 1;  // marks "no candidate" (above +inf bits)
+    }
+  }
+}
+
+__global__ void k_snap_final(unsigned long long* __restrict__ best, int nblocks, long long* __restrict__ out) {
+  // single warp: lowest index among blocks whose local minimum equals the global minimum
+  const int lane = threadIdx.x;
+  const unsigned long long m = best[0];
+  long long idx = -1;
+  for (int b = lane; b < nblocks; b += 32) {
+    if (best[1 + b] == m && m != kInfBits + 2) {
+      const long long bi = (long long)best[1 + nblocks + b];
+      if (idx < 0 || bi < idx) idx = bi;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const long long oi = __shfl_down_sync(0xffffffffu, idx, off);
+    if (oi >= 0 && (idx < 0 || oi < idx)) idx = oi;
+  }
+  if (lane == 0) *out = idx;
+}
+
+// reverse reachability sweep over alive edges: reach[u] |= reach[v] for u -> v
+__global__ void k_reach_sweep(long long E, const int* __restrict__ src, const int* __restrict__ dst,
+                              const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach, int* __restrict__ changed) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  if (alive && !alive[e]) return;
+  const int v = dst[e];
+  if (!reach[v]) return;
+  const int u = src[e];
+  if (!reach[u]) {
+    reach[u] = 1;
+    *changed = 1;
+  }
+}
+
+// Frontier Bellman-Ford: one warp per vertex improved in the previous sweep relaxes its
+// alive out-edges with fl(d[u] + c) and atomicMin on the (non-negative) double bits.
+__global__ void k_bf_sweep(long long V, int sweep, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
+                           const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                           unsigned long long* __restrict__ dist, int* __restrict__ stamp,
+                           int* __restrict__ last_change) {
+  const long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (u >= V) return;
+  if (stamp[u] != sweep - 1) return;
+  const double du = __longlong_as_double((long long)dist[u]);
+  bool any = false;
+  for (long long e = row_ptr[u] + lane; e < row_ptr[u + 1]; e += 32) {
+    if (alive && !alive[e]) continue;
+    const int v = dst[e];
+    const double nd = __dadd_rn(du, cost[e]);
+    const unsigned long long nb = dbits(nd);
+    if (nb < dist[v]) {
+      const unsigned long long old = atomicMin(dist + v, nb);
+      if (nb < old) {
+        stamp[v] = sweep;
+        any = true;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, any) && lane == 0) atomicMax(last_change, sweep);
+}
+
+// parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes)
+__global__ void k_parent_dist(long long E, const int* __restrict__ src, const int* __restrict__ dst,
+                              const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                              const unsigned long long* __restrict__ dist, unsigned long long* __restrict__ pd) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  if (alive && !alive[e]) return;
+  const int u = src[e], v = dst[e];
+  const unsigned long long bu = dist[u];
+  if (bu >= kInfBits) return;
+  const double nd = __dadd_rn(__longlong_as_double((long long)bu), cost[e]);
+  if (dbits(nd) == dist[v]) atomicMin(pd + v, bu);
+}
+
+__global__ void k_parent_idx(long long E, const int* __restrict__ src, const int* __restrict__ dst,
+                             const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                             const unsigned long long* __restrict__ dist, const unsigned long long* __restrict__ pd,
+                             int* __restrict__ parent) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  if (alive && !alive[e]) return;
+  const int u = src[e], v = dst[e];
+  const unsigned long long bu = dist[u];
+  if (bu >= kInfBits || bu != pd[v]) return;
+  const double nd = __dadd_rn(__longlong_as_double((long long)bu), cost[e]);
+  if (dbits(nd) == dist[v]) atomicMin(parent + v, u);
+}
+
+__global__ void k_backtrack(long long V, long long v0, long long vg, const int* __restrict__ parent,
+                            const unsigned long long* __restrict__ dist, long long* __restrict__ path,
+                            long long* __restrict__ len, double* __restrict__ dout) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (dist[vg] >= kInfBits) {
+    *len = -1;
+    return;
+  }
+  long long n = 0, v = vg;
+  path[n++] = v;
+  while (v != v0 && n <= V) {
+    v = parent[v];
+    if (v < 0 || v >= V) { n = -2; break; }
+    path[n++] = v;
+  }
+  *len = n;
+  *dout = __longlong_as_double((long long)dist[vg]);
+}
+
+__global__ void k_init_sssp(long long V, long long v0, unsigned long long* dist, int* stamp, int* parent,
+                            unsigned long long* pd) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  dist[i] = i == v0 ? 0ull : kInfBits;
+  stamp[i] = i == v0 ? 0 : -1;
+  parent[i] = 0x7fffffff;
+  pd[i] = ~0ull;
+}
+
+long long snap_launch(Ctx* c, Graph* g, const SnapParams& sp, const uint8_t* reach) {
+  const long long V = g->V;
+  const unsigned nb = div_up(V, 256);
+  DevBuf best, out;
+  best.alloc((1 + 2 * (size_t)nb) * sizeof(unsigned long long), c->stream);
+  out.alloc(sizeof(long long), c->stream);
+  const unsigned long long init = kInfBits + 2;
+  BZG_CHECK_CUDA(cudaMemcpyAsync(best.ptr, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  launch(c, "k_snap", k_snap, dim3(nb), dim3(256), 0, sp, g->vertices.as<double>(), V, reach,
+         best.as<unsigned long long>());
+  launch(c, "k_snap_final", k_snap_final, dim3(1), dim3(32), 0, best.as<unsigned long long>(), (int)nb,
+         out.as<long long>());
+  long long* h = static_cast<long long*>(c->host_scratch(sizeof(long long)));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h, out.ptr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  return h[0];
+}
+
+}  // namespace
+
+void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
+               const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
+               double* dist_out) {
+  const long long V = g->V, E = g->E;
+  const int n = g->n;
+  BZG_REQUIRE(n <= 16, BZG_EUNSUPPORTED, "state dimension too large");
+  const uint8_t* alive = mk ? mk->alive.as<uint8_t>() : nullptr;
+  path.clear();
+  *dist_out = INFINITY;
+
+  SnapParams sp{};
+  sp.n = n;
+  sp.m_norm = pos_only ? g->m : n;
+  for (int k = 0; k < n; ++k) sp.target[k] = goal[k];
+  sp.mode = 0;
+  const long long vg = snap_launch(c, g, sp, nullptr);
+  BZG_REQUIRE(vg >= 0, BZG_EINVAL, "graph has no vertices");
+
+  for (int k = 0; k < n; ++k) {
+    sp.target[k] = start[k];
+    sp.tlo[k] = -tube_hi[k] - eps;  // (diff >= -tube.hi - EPS_GEO)   graph.py:381
+    sp.thi[k] = -tube_lo[k] + eps;  // (diff <= -tube.lo + EPS_GEO)
+  }
+  long long v0;
+  DevBuf tmp_reach;
+  if (require_tube) {
+    sp.mode = 1;
+    v0 = snap_launch(c, g, sp, nullptr);
+  } else {
+    // relaxed mid-run snap: nearest vertex that can still reach vg (graph.py:388-392)
+    uint8_t* reach;
+    if (mk) {
+      mk->reach.alloc(V, c->stream);
+      reach = mk->reach.as<uint8_t>();
+    } else {
+      tmp_reach.alloc(V, c->stream);
+      reach = tmp_reach.as<uint8_t>();
+    }
+    if (!mk || mk->reach_vg != vg) {
+      DevBuf changed;
+      changed.alloc(sizeof(int), c->stream);
+      BZG_CHECK_CUDA(cudaMemsetAsync(reach, 0, V, c->stream));
+      const uint8_t one = 1;
+      BZG_CHECK_CUDA(cudaMemcpyAsync(reach + vg, &one, 1, cudaMemcpyHostToDevice, c->stream));
+      int* h = static_cast<int*>(c->host_scratch(sizeof(int)));
+      for (int guard = 0;; ++guard) {
+        BZG_CHECK_CUDA(cudaMemsetAsync(changed.ptr, 0, sizeof(int), c->stream));
+        for (int s = 0; s < 8; ++s)
+          launch(c, "k_reach_sweep", k_reach_sweep, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(),
+                 g->dst.as<int>(), alive, reach, changed.as<int>());
+        BZG_CHECK_CUDA(cudaMemcpyAsync(h, changed.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+        if (!h[0] || E == 0) break;
+        BZG_REQUIRE(guard < V + 8, BZG_ECUDA, "reachability sweep did not converge");
+      }
+      if (mk) mk->reach_vg = vg;
+    }
+    sp.mode = 2;
+    v0 = snap_launch(c, g, sp, reach);
+  }
+  if (v0 < 0) return;  // no snappable start -> None
+  if (v0 == vg) {
+    path.push_back(v0);
+    *dist_out = 0.0;
+    return;
+  }
+
+  DevBuf lpath, llen, ldist;
+  DevBuf t_dist, t_parent, t_stamp, t_pd, t_last;
+  unsigned long long* dist;
+  int* parent;
+  const bool cached = mk && mk->tree_v0 == v0;
+  if (mk) {
+    mk->dist.alloc(V * sizeof(unsigned long long), c->stream);
+    mk->parent.alloc(V * sizeof(int), c->stream);
+    dist = mk->dist.as<unsigned long long>();
+    parent = mk->parent.as<int>();
+  } else {
+    t_dist.alloc(V * sizeof(unsigned long long), c->stream);
+    t_parent.alloc(V * sizeof(int), c->stream);
+    dist = t_dist.as<unsigned long long>();
+    parent = t_parent.as<int>();
+  }
+  if (!cached) {
+    t_stamp.alloc(V * sizeof(int), c->stream);
+    t_pd.alloc(V * sizeof(unsigned long long), c->stream);
+    t_last.alloc(sizeof(int), c->stream);
+    launch(c, "k_init_sssp", k_init_sssp, dim3(div_up(V, 256)), dim3(256), 0, V, v0, dist, t_stamp.as<int>(), parent,
+           t_pd.as<unsigned long long>());
+    BZG_CHECK_CUDA(cudaMemsetAsync(t_last.ptr, 0, sizeof(int), c->stream));
+    int* h = static_cast<int*>(c->host_scratch(sizeof(int)));
+    int sweep = 1;
+    constexpr int kBatch = 8;
+    for (;;) {
+      for (int s = 0; s < kBatch; ++s, ++sweep)
+        launch(c, "k_bf_sweep", k_bf_sweep, dim3(div_up(V * 32, 256)), dim3(256), 0, V, sweep,
+               g->row_ptr.as<long long>(), g->dst.as<int>(), g->cost.as<double>(), alive, dist, t_stamp.as<int>(),
+               t_last.as<int>());
+      BZG_CHECK_CUDA(cudaMemcpyAsync(h, t_last.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      if (h[0] < sweep - 1) break;  // the last sweep of the batch changed nothing
+      BZG_REQUIRE(sweep < V + 2 * kBatch + 2, BZG_ECUDA, "Bellman-Ford did not converge");
+    }
+    launch(c, "k_parent_dist", k_parent_dist, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(),
+           g->dst.as<int>(), g->cost.as<double>(), alive, dist, t_pd.as<unsigned long long>());
+    launch(c, "k_parent_idx", k_parent_idx, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(), g->dst.as<int>(),
+           g->cost.as<double>(), alive, dist, t_pd.as<unsigned long long>(), parent);
+    if (mk) mk->tree_v0 = v0;
+  }
+  lpath.alloc((V + 1) * sizeof(long long), c->stream);
+  llen.alloc(sizeof(long long), c->stream);
+  ldist.alloc(sizeof(double), c->stream);
+  launch(c, "k_backtrack", k_backtrack, dim3(1), dim3(32), 0, V, v0, vg, parent, dist, lpath.as<long long>(),
+         llen.as<long long>(), ldist.as<double>());
+  long long* h = static_cast<long long*>(c->host_scratch(2 * sizeof(long long)));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h, llen.ptr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h + 1, ldist.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  const long long len = h[0];
+  double dv;
+  memcpy(&dv, h + 1, sizeof(double));
+  BZG_REQUIRE(len != -2, BZG_ECUDA, "parent chain broken during backtrack");
+  if (len < 0) return;  // vg unreachable -> None
+  std::vector<long long> rev(len);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(rev.data(), lpath.ptr, len * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  path.resize(len);
+  for (long long i = 0; i < len; ++i) path[i] = rev[len - 1 - i];
+  *dist_out = dv;
+}
+
+}  // namespace bzg

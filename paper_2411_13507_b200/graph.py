@@ -1,0 +1,476 @@
+"""Drop-in device implementation of the reference graph stage.
+
+Same names, signatures, return types and error behaviour as
+``beziergraph.graph`` (/root/reference/pkg/src/beziergraph/graph.py):
+
+* ``build_graph``  (graph.py:129-199)  -> bzg_build_graph   (sampling, pair test, CSR, costs)
+* ``cut_graph``    (graph.py:302-350)  -> bzg_cut_graph     (box heuristic + Cut-QP + aggregation)
+* ``find_path``    (graph.py:353-430)  -> bzg_find_path     (snapping + Bellman-Ford + parents)
+* ``path_cost``    (graph.py:453-458), ``check_edges`` (reachability.py:139-142)
+
+All compute runs in libbzg.so on the GPU; the returned ``BezierGraph`` and
+``CutMask`` keep their arrays device-resident and materialise the reference's
+numpy fields (``vertices``, ``edges``, ``costs``, ``edge_points``, ``alive``,
+``provenance``) lazily on first access, read-only like the reference's frozen
+arrays (graph.py:70-73).  Inputs are duck-typed: the reference's own
+``BezierSpec``/``ReachOracle``/``Box``/``Polytope`` instances work as well as
+this package's host mirrors.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _native as nat
+from .bezier import boundary_matrix
+from .geometry import EPS_GEO, recover_box
+
+_PAIR_CHUNK = 32  # kept for API parity with the reference module (graph.py:26)
+
+
+class CutVerdict(Enum):
+    UNSAFE = "unsafe"
+    SAFE = "safe"
+    INDETERMINATE = "indeterminate"
+
+
+class CutProvenance(Enum):
+    HEURISTIC_UNSAFE = "heuristic_unsafe"
+    HEURISTIC_SAFE = "heuristic_safe"
+    QP_SAFE = "qp_safe"
+    QP_UNSAFE = "qp_unsafe"
+
+
+# device provenance codes (include/bzg.h) -> enum order
+_PROV_CODES = ("HEURISTIC_UNSAFE", "HEURISTIC_SAFE", "QP_SAFE", "QP_UNSAFE")
+# the shim swaps this for the reference's enum so masks compare equal inside its simulator
+_PROV_ENUM = CutProvenance
+
+
+@dataclass
+class SolveConfig:
+    """Subset of the reference ``qpsolver.SolveConfig`` (qpsolver.py:60-72) the cut QP uses."""
+
+    max_iter: int = 4000
+    eps_abs: float = 1e-6
+    eps_rel: float = 1e-6
+    rho: float = 0.1
+    sigma: float = 1e-6
+    alpha: float = 1.6
+    eps_pinf: float = 1e-4
+    polish: bool = False
+
+
+@dataclass
+class CutConfig:
+    """Reference ``CutConfig`` (graph.py:42-49)."""
+
+    eps_cut: float = 1e-7
+    heur_margin: float = 1e-6
+    eps_geo: float = EPS_GEO
+    qp: SolveConfig = field(
+        default_factory=lambda: SolveConfig(max_iter=500, eps_abs=1e-7, eps_rel=0.0, rho=1.0, polish=True))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ro(a: np.ndarray) -> np.ndarray:
+    a.setflags(write=False)
+    return a
+
+
+class BezierGraph:
+    """Device-resident graph with the reference ``BezierGraph`` fields (graph.py:52-88)."""
+
+    def __init__(self, handle, ctx, spec, oracle, seed, sample_bounds, D):
+        self._h = handle
+        self._ctx = ctx
+        self.spec = spec
+        self.oracle = oracle
+        self.seed = seed
+        self.sample_bounds = sample_bounds
+        self._D = D
+        V, E, rb, re_ = (C.c_int64() for _ in range(4))
+        nat.check(ctx.lib.bzg_graph_info(handle, C.byref(V), C.byref(E), C.byref(rb), C.byref(re_)))
+        self._V, self._E = V.value, E.value
+        self.row_block = (rb.value, re_.value)
+        self._cache: dict = {}
+
+    # ---- reference fields, materialised lazily
+    @property
+    def vertices(self) -> np.ndarray:
+        if "vertices" not in self._cache:
+            out = np.empty((self._V, self.spec.m * self.spec.gamma))
+            nat.check(self._ctx.lib.bzg_graph_copy_vertices(self._h, nat.ptr(out)))
+            self._cache["vertices"] = _ro(out)
+        return self._cache["vertices"]
+
+    def _edges_costs(self):
+        if "edges" not in self._cache:
+            e = np.empty((self._E, 2), dtype=np.int64)
+            c = np.empty(self._E)
+            nat.check(self._ctx.lib.bzg_graph_copy_edges(self._h, nat.ptr(e), nat.ptr(c)))
+            self._cache["edges"] = _ro(e)
+            self._cache["costs"] = _ro(c)
+
+    @property
+    def edges(self) -> np.ndarray:
+        self._edges_costs()
+        return self._cache["edges"]
+
+    @property
+    def costs(self) -> np.ndarray:
+        self._edges_costs()
+        return self._cache["costs"]
+
+    @property
+    def edge_points(self) -> np.ndarray:
+        if "edge_points" not in self._cache:
+            out = np.empty((self._E, self.spec.m, self.spec.p + 1))
+            nat.check(self._ctx.lib.bzg_graph_copy_points(self._h, nat.ptr(out)))
+            self._cache["edge_points"] = _ro(out)
+        return self._cache["edge_points"]
+
+    def csr(self) -> tuple[np.ndarray, np.ndarray]:
+        """(row_ptr (V+1,) int64, col (E,) int32): the device CSR copied to host."""
+        if "csr" not in self._cache:
+            rp = np.empty(self._V + 1, dtype=np.int64)
+            col = np.empty(self._E, dtype=np.int32)
+            nat.check(self._ctx.lib.bzg_graph_copy_csr(self._h, nat.ptr(rp), nat.ptr(col)))
+            self._cache["csr"] = (_ro(rp), _ro(col))
+        return self._cache["csr"]
+
+    @property
+    def num_vertices(self) -> int:
+        return self._V
+
+    @property
+    def num_edges(self) -> int:
+        return self._E
+
+    def to_json(self, max_edges: int | None = None) -> dict:
+        edges = [[int(i), int(j), float(c)] for (i, j), c in zip(self.edges[:max_edges], self.costs[:max_edges])]
+        return {"vertices": self.vertices.tolist(), "edges": edges}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._ctx.lib.bzg_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class CutMask:
+    """Outcome of one cut (reference ``CutMask``, graph.py:91-126), device-resident."""
+
+    def __init__(self, handle, graph: BezierGraph, counters):
+        self._h = handle
+        self._graph = graph
+        (self.pairs_total, self.pairs_point_hit, self.pairs_hyperplane, self.pairs_qp, self.qp_safe,
+         self.qp_unsafe) = (int(x) for x in counters)
+        self._alive = None
+        self._alive_seen = None
+        self._prov = None
+        self._prov_codes = None
+
+    def _copy(self):
+        E = self._graph.num_edges
+        a = np.empty(E, dtype=np.uint8)
+        p = np.empty(E, dtype=np.uint8)
+        nat.check(self._graph._ctx.lib.bzg_mask_copy(self._h, nat.ptr(a), nat.ptr(p), None))
+        self._alive = a.astype(bool)
+        self._alive_seen = self._alive.copy()
+        self._prov_codes = p
+
+    @property
+    def alive(self) -> np.ndarray:
+        if self._alive is None:
+            self._copy()
+        return self._alive
+
+    @alive.setter
+    def alive(self, value):
+        self._alive = np.asarray(value, dtype=bool)
+        self._alive_seen = None  # force a re-upload before the next search
+
+    @property
+    def provenance_codes(self) -> np.ndarray:
+        if self._prov_codes is None:
+            self._copy()
+        return self._prov_codes
+
+    @property
+    def provenance(self) -> np.ndarray:
+        if self._prov is None:
+            members = [getattr(_PROV_ENUM, nm) for nm in _PROV_CODES]
+            table = np.empty(4, dtype=object)
+            table[:] = members
+            self._prov = table[self.provenance_codes]
+        return self._prov
+
+    @property
+    def heuristic_fraction(self) -> float:
+        if self.pairs_total == 0:
+            return 1.0
+        return 1.0 - self.pairs_qp / self.pairs_total
+
+    @property
+    def alive_count(self) -> int:
+        return int(self.alive.sum())
+
+    def qp_records(self) -> dict:
+        """Per-QP diagnostics: edge, obstacle, status (0 solved..3 error), iterations, ||delta||."""
+        lib = self._graph._ctx.lib
+        n = C.c_int64()
+        nat.check(lib.bzg_mask_qp_count(self._h, C.byref(n)))
+        k = n.value
+        out = dict(edge=np.empty(k, np.int64), obstacle=np.empty(k, np.int32), status=np.empty(k, np.int8),
+                   iterations=np.empty(k, np.int32), delta=np.empty(k))
+        nat.check(lib.bzg_mask_copy_qp(self._h, *(nat.ptr(out[x]) for x in
+                                                  ("edge", "obstacle", "status", "iterations", "delta"))))
+        return out
+
+    def _device_handle(self):
+        """Handle whose alive bits match the (possibly caller-modified) host array."""
+        if self._alive is not None and (self._alive_seen is None or not np.array_equal(self._alive, self._alive_seen)):
+            a = np.ascontiguousarray(self._alive, dtype=np.uint8)
+            cnt = np.array([self.pairs_total, self.pairs_point_hit, self.pairs_hyperplane, self.pairs_qp,
+                            self.qp_safe, self.qp_unsafe], dtype=np.int64)
+            h = C.c_void_p()
+            lib = self._graph._ctx.lib
+            nat.check(lib.bzg_mask_from_arrays(self._graph._ctx.handle, self._graph._h, nat.ptr(a),
+                                               nat.ptr(np.ascontiguousarray(self.provenance_codes)), nat.ptr(cnt), 0,
+                                               C.byref(h)))
+            lib.bzg_mask_destroy(self._h)
+            self._h = h
+            self._alive_seen = self._alive.copy()
+        return self._h
+
+    def to_json(self) -> dict:
+        counts: dict[str, int] = {}
+        for p in self.provenance:
+            counts[p.value] = counts.get(p.value, 0) + 1
+        return {
+            "alive_bitset": np.packbits(self.alive).tobytes().hex(),
+            "num_edges": int(self.alive.size),
+            "alive": self.alive_count,
+            "provenance_counts": counts,
+            "pairs_total": self.pairs_total,
+            "heuristic_fraction": self.heuristic_fraction,
+        }
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._graph._ctx.lib.bzg_mask_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _pcg_words(seed) -> tuple[int, int, int, int]:
+    """numpy PCG64 (state, inc) for ``default_rng(seed)`` split into 64-bit halves."""
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    mask = (1 << 64) - 1
+    return s >> 64, s & mask, inc >> 64, inc & mask
+
+
+def _build_desc(N, spec, oracle, bounds, seed, include, vertices=None, rows=None):
+    m, g = int(spec.m), int(spec.gamma)
+    n = m * g
+    F = _f64(oracle.F)
+    G = _f64(oracle.G)
+    D = _f64(boundary_matrix(spec))
+    xdA = _f64(oracle.Xd.A)
+    xdb = _f64(oracle.Xd.b)
+    lo = _f64(bounds.lo)
+    hi = _f64(bounds.hi)
+    inc = None
+    if include is not None and len(include):
+        inc = _f64(np.atleast_2d(np.asarray(include, dtype=np.float64)))
+        if inc.shape[1] != n:
+            raise ValueError(f"include rows must be {n}-dimensional")
+    keep = [F, G, D, xdA, xdb, lo, hi, inc]
+    d = nat.BuildDesc()
+    d.m, d.gamma, d.p, d.n_F = m, g, int(spec.p), F.shape[0]
+    d.F, d.G, d.D = nat.ptr(F), nat.ptr(G), nat.ptr(D)
+    d.eps_geo = EPS_GEO
+    d.N = int(N)
+    if vertices is None:
+        d.pcg_state_hi, d.pcg_state_lo, d.pcg_inc_hi, d.pcg_inc_lo = _pcg_words(seed)
+    else:
+        vv = _f64(vertices)
+        keep.append(vv)
+        d.vertices = nat.ptr(vv)
+    d.sample_lo, d.sample_hi = nat.ptr(lo), nat.ptr(hi)
+    d.xd_rows, d.xd_A, d.xd_b = xdA.shape[0], nat.ptr(xdA), nat.ptr(xdb)
+    d.n_include = 0 if inc is None else inc.shape[0]
+    d.include = nat.ptr(inc)
+    d.row_begin, d.row_end = (0, 0) if rows is None else (int(rows[0]), int(rows[1]))
+    return d, keep, D
+
+
+def build_graph(N, spec, oracle, bounds, seed, include=None, k_nearest=None, *, ctx=None, rows=None):
+    """Sample N states and connect every oracle-feasible ordered pair (reference graph.py:129-199).
+
+    ``rows`` (keyword-only extension) restricts the pair test to the source-row block
+    [rows[0], rows[1]) — the unit of multi-GPU row sharding.
+    """
+    if N < 2:
+        raise ValueError("need at least two vertices")
+    if bounds.dim != spec.n:
+        raise ValueError(f"sampling bounds must be {spec.n}-dimensional")
+    if k_nearest is not None:
+        raise NotImplementedError("k_nearest prefilter (graph.py:162-170) is not implemented on device yet")
+    ctx = ctx or nat.default_context()
+    d, keep, D = _build_desc(N, spec, oracle, bounds, seed, include, rows=rows)
+    h = C.c_void_p()
+    rc = ctx.lib.bzg_build_graph(ctx.handle, C.byref(d), C.byref(h))
+    if rc == nat.BZG_EINVAL:
+        raise ValueError(ctx.lib.bzg_last_error().decode())
+    nat.check(rc)
+    del keep
+    return BezierGraph(h, ctx, spec, oracle, seed, bounds, D)
+
+
+def check_edges(oracle, X1, X2, eps: float = EPS_GEO, *, ctx=None) -> np.ndarray:
+    """Batched feasibility F[x1;x2] <= G + eps in the separable form (reachability.py:139-142)."""
+    ctx = ctx or nat.default_context()
+    X1 = _f64(np.atleast_2d(X1))
+    X2 = _f64(np.atleast_2d(X2))
+    F = _f64(oracle.F)
+    G = _f64(oracle.G)
+    n = oracle.spec.n
+    if X1.shape != X2.shape or X1.shape[1] != n:
+        raise ValueError(f"endpoints must have dimension {n}")
+    out = np.empty(X1.shape[0], dtype=np.uint8)
+    nat.check(ctx.lib.bzg_check_edges(ctx.handle, n, F.shape[0], nat.ptr(F), nat.ptr(G), float(eps), X1.shape[0],
+                                      nat.ptr(X1), nat.ptr(X2), nat.ptr(out)))
+    return out.astype(bool)
+
+
+def check_edge(oracle, x1, x2, eps: float = EPS_GEO, *, ctx=None) -> bool:
+    """Scalar predicate (reachability.py:130-136) through the device batch kernel."""
+    x1 = np.asarray(x1, dtype=np.float64)
+    x2 = np.asarray(x2, dtype=np.float64)
+    n = oracle.spec.n
+    if x1.shape != (n,) or x2.shape != (n,):
+        raise ValueError(f"endpoints must have dimension {n}")
+    return bool(check_edges(oracle, x1[None], x2[None], eps, ctx=ctx)[0])
+
+
+def _obstacle_arrays(obstacles, m):
+    """Normalised rows (Polytope.normalized, geometry.py:135-137) and box recovery (as_box)."""
+    offs = [0]
+    As, bs, is_box, lo, hi = [], [], [], [], []
+    for ob in obstacles:
+        A = _f64(ob.A)
+        b = _f64(ob.b)
+        if A.ndim != 2 or A.shape[1] != m:
+            raise ValueError(f"obstacles must live in the {m}-d output space")
+        nrm = np.linalg.norm(A, axis=1)
+        An = A / nrm[:, None]
+        bn = b / nrm
+        box = recover_box(An, bn)
+        As.append(An)
+        bs.append(bn)
+        offs.append(offs[-1] + An.shape[0])
+        is_box.append(1 if box is not None else 0)
+        lo.append(box.lo if box is not None else np.zeros(m))
+        hi.append(box.hi if box is not None else np.zeros(m))
+    if not obstacles:
+        return (np.zeros(1, np.int32), np.zeros((0, m)), np.zeros(0), np.zeros(0, np.uint8), np.zeros((0, m)),
+                np.zeros((0, m)))
+    return (np.array(offs, np.int32), _f64(np.vstack(As)), _f64(np.concatenate(bs)), np.array(is_box, np.uint8),
+            _f64(np.vstack(lo)), _f64(np.vstack(hi)))
+
+
+def _cut_cfg(cfg) -> nat.CutConfigC:
+    q = cfg.qp
+    c = nat.CutConfigC()
+    c.eps_cut, c.heur_margin, c.eps_geo = float(cfg.eps_cut), float(cfg.heur_margin), float(cfg.eps_geo)
+    c.qp_max_iter = int(q.max_iter)
+    c.qp_eps_abs, c.qp_eps_rel, c.qp_rho = float(q.eps_abs), float(q.eps_rel), float(q.rho)
+    c.qp_sigma, c.qp_alpha, c.qp_eps_pinf = float(q.sigma), float(q.alpha), float(q.eps_pinf)
+    c.qp_polish = int(bool(q.polish))
+    return c
+
+
+def cut_graph(graph: BezierGraph, obstacles, cfg: CutConfig | None = None) -> CutMask:
+    """Screen every (edge, obstacle) pair, QP the leftovers, keep edges safe for all (graph.py:302-350)."""
+    cfg = cfg or CutConfig()
+    ctx = graph._ctx
+    arrs = _obstacle_arrays(list(obstacles), graph.spec.m)
+    offs, A, b, is_box, lo, hi = arrs
+    cc = _cut_cfg(cfg)
+    h = C.c_void_p()
+    nat.check(ctx.lib.bzg_cut_graph(ctx.handle, graph._h, len(is_box), nat.ptr(offs), nat.ptr(A), nat.ptr(b),
+                                    nat.ptr(is_box), nat.ptr(lo), nat.ptr(hi), C.byref(cc), C.byref(h)))
+    cnt = np.zeros(6, dtype=np.int64)
+    nat.check(ctx.lib.bzg_mask_copy(h, None, None, nat.ptr(cnt)))
+    return CutMask(h, graph, cnt)
+
+
+def find_path(graph: BezierGraph, mask, start, goal, position_only_snap: bool = False,
+              require_tube_snap: bool = True):
+    """Shortest alive path between the snapped start and goal (graph.py:353-430); None if none."""
+    ctx = graph._ctx
+    start = _f64(start)
+    goal = _f64(goal)
+    tube = graph.oracle.tube.error
+    tlo, thi = _f64(tube.lo), _f64(tube.hi)
+    mh = None
+    tmp = None
+    if isinstance(mask, CutMask):
+        mh = mask._device_handle()
+    elif mask is not None:  # a foreign (e.g. reference) CutMask: upload its alive bits
+        a = np.ascontiguousarray(mask.alive, dtype=np.uint8)
+        h = C.c_void_p()
+        nat.check(ctx.lib.bzg_mask_from_arrays(ctx.handle, graph._h, nat.ptr(a), None, None, 0, C.byref(h)))
+        mh = tmp = h
+    path = np.empty(graph.num_vertices + 1, dtype=np.int64)
+    plen = C.c_int64()
+    dist = C.c_double()
+    try:
+        nat.check(ctx.lib.bzg_find_path(ctx.handle, graph._h, mh, nat.ptr(start), nat.ptr(goal), nat.ptr(tlo),
+                                        nat.ptr(thi), EPS_GEO, int(bool(position_only_snap)),
+                                        int(bool(require_tube_snap)), nat.ptr(path), path.size, C.byref(plen),
+                                        C.byref(dist)))
+    finally:
+        if tmp is not None:
+            ctx.lib.bzg_mask_destroy(tmp)
+    if plen.value < 0:
+        return None
+    out = [int(v) for v in path[: plen.value]]
+    graph._cache["last_dist"] = (tuple(out), dist.value)
+    return out
+
+
+def path_cost(graph: BezierGraph, path) -> float:
+    """Total edge cost along a vertex path, left-to-right sum (graph.py:453-458)."""
+    if len(path) < 2:
+        return 0.0
+    rp, col = graph.csr()
+    costs = graph.costs
+    total = 0
+    for a, b in zip(path, path[1:]):
+        lo, hi = int(rp[a]), int(rp[a + 1])
+        k = lo + int(np.searchsorted(col[lo:hi], b))
+        if k >= hi or col[k] != b:
+            raise KeyError((a, b))
+        total = total + costs[k]
+    return float(total)

@@ -1,0 +1,242 @@
+"""Capture golden vectors from the LIVE reference (run in the build container only).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [case ...]
+
+The reference (/root/reference/pkg/src/beziergraph, pure Python) cannot travel
+to the GPU box, so its outputs on seeded inputs are frozen here as .npz
+fixtures.  Each fixture records numpy/scipy/BLAS versions and the CPU model.
+Large arrays are stored in full when small, otherwise as sha256 digests plus
+the full bool/int8 outcome arrays (compressed) and the path.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import platform
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import beziergraph as bg  # noqa: E402
+from beziergraph import geometry as rgeo  # noqa: E402
+from beziergraph import graph as rg  # noqa: E402
+from beziergraph import qpsolver as rqp  # noqa: E402
+from beziergraph import scenario as rsc  # noqa: E402
+from beziergraph import sim as rsim  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+PROV = {"heuristic_unsafe": 0, "heuristic_safe": 1, "qp_safe": 2, "qp_unsafe": 3}
+STATUS = {"solved": 0, "max_iter": 1, "infeasible": 2, "error": 3}
+
+
+def digest(a: np.ndarray) -> str:
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def env_info() -> dict:
+    cpu = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    import scipy
+
+    blas = {}
+    try:
+        cfg = np.show_config(mode="dicts")
+        blas = cfg["Build Dependencies"]["blas"]
+    except Exception:  # pragma: no cover
+        pass
+    return {"numpy": np.__version__, "scipy": scipy.__version__, "blas": str(blas.get("version", "")),
+            "blas_name": str(blas.get("name", "")), "cpu": cpu, "python": platform.python_version()}
+
+
+def per_obstacle_detail(g, obstacles, cfg):
+    """Per-obstacle heuristic codes and QP outcomes, computed with the reference's own internals
+    exactly as cut_graph does (graph.py:312-337)."""
+    codes_all, pend_o, pend_e, st, it, dl = [], [], [], [], [], []
+    J = g.spec.p + 1
+    for oi, ob in enumerate(obstacles):
+        codes = rg._heuristic_batch(g.edge_points, ob, cfg)
+        codes_all.append(codes)
+        pending = np.nonzero(codes == 2)[0]
+        if pending.size:
+            O = ob.normalized()
+            sols = rqp.solve_batch([rg._cut_qp_problem(g.edge_points[e], O) for e in pending], cfg.qp)
+            for e, s in zip(pending, sols):
+                pend_o.append(oi)
+                pend_e.append(e)
+                st.append(STATUS[s.status.value])
+                it.append(s.iterations)
+                dl.append(float(np.linalg.norm(s.x[J:])))
+    return (np.stack(codes_all) if codes_all else np.zeros((0, g.num_edges), np.int8),
+            np.array(pend_o, np.int32), np.array(pend_e, np.int64), np.array(st, np.int8),
+            np.array(it, np.int64), np.array(dl))
+
+
+def capture(name, N, spec, oracle, bounds, seed, include, obstacles, start, goal, *, full, detail,
+            goals=None, relaxed_starts=None):
+    t0 = time.perf_counter()
+    g = rg.build_graph(N, spec, oracle, bounds, seed, include=include)
+    t_build = time.perf_counter() - t0
+    cfg = rg.CutConfig()
+    t0 = time.perf_counter()
+    mask = rg.cut_graph(g, obstacles, cfg)
+    t_cut = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    path = rg.find_path(g, mask, start, goal)
+    t_path = time.perf_counter() - t0
+    rec = {
+        "N": N, "seed": seed, "V": g.num_vertices, "E": g.num_edges,
+        "F": oracle.F, "G": oracle.G, "D": bg.bezier.boundary_matrix(spec),
+        "m": spec.m, "gamma": spec.gamma, "p": spec.p, "T": spec.T,
+        "bounds_lo": bounds.lo, "bounds_hi": bounds.hi, "xd_A": oracle.Xd.A, "xd_b": oracle.Xd.b,
+        "tube_lo": oracle.tube.error.lo, "tube_hi": oracle.tube.error.hi,
+        "include": np.zeros((0, spec.n)) if include is None else np.asarray(include, float),
+        "obs_n": np.array([o.num_rows for o in obstacles], np.int32),
+        "obs_A": np.concatenate([o.A for o in obstacles]) if obstacles else np.zeros((0, spec.m)),
+        "obs_b": np.concatenate([o.b for o in obstacles]) if obstacles else np.zeros(0),
+        "start": np.asarray(start, float), "goal": np.asarray(goal, float),
+        "sha_vertices": digest(g.vertices), "sha_edges": digest(g.edges), "sha_costs": digest(g.costs),
+        "sha_points": digest(g.edge_points),
+        "alive": mask.alive.copy(),
+        "provenance": np.array([PROV[p.value] for p in mask.provenance], np.int8),
+        "counters": np.array([mask.pairs_total, mask.pairs_point_hit, mask.pairs_hyperplane, mask.pairs_qp,
+                              mask.qp_safe, mask.qp_unsafe], np.int64),
+        "path": np.array(path if path is not None else [], np.int64),
+        "path_none": path is None,
+        "path_cost": rg.path_cost(g, path) if path else 0.0,
+        "t_build": t_build, "t_cut": t_cut, "t_path": t_path,
+        "env": json.dumps(env_info()),
+    }
+    if full:
+        rec.update(vertices=g.vertices, edges=g.edges, costs=g.costs, edge_points=g.edge_points)
+    else:
+        # enough raw rows to debug a mismatch without shipping the whole graph
+        k = min(4096, g.num_edges)
+        rec.update(vertices=g.vertices, edges_head=g.edges[:k], costs_head=g.costs[:k],
+                   points_head=g.edge_points[:k],
+                   row_counts=np.bincount(g.edges[:, 0], minlength=g.num_vertices).astype(np.int64))
+    if detail:
+        codes, po, pe, st, it, dl = per_obstacle_detail(g, obstacles, cfg)
+        rec.update(codes=codes, qp_obstacle=po, qp_edge=pe, qp_status=st, qp_iters=it, qp_delta=dl)
+    if goals is not None:
+        paths, costs = [], []
+        for gl in goals:
+            p = rg.find_path(g, mask, start, gl)
+            paths.append(p if p is not None else [])
+            costs.append(rg.path_cost(g, p) if p else np.inf)
+        rec["goals"] = np.asarray(goals)
+        rec["goal_path_len"] = np.array([len(p) for p in paths], np.int64)
+        rec["goal_paths"] = np.concatenate([np.asarray(p, np.int64) for p in paths]) if paths else np.zeros(0, np.int64)
+        rec["goal_costs"] = np.array(costs)
+    if relaxed_starts is not None:
+        paths = []
+        for st_ in relaxed_starts:
+            p = rg.find_path(g, mask, st_, goal, position_only_snap=True, require_tube_snap=False)
+            paths.append(p if p is not None else [])
+        rec["relaxed_starts"] = np.asarray(relaxed_starts)
+        rec["relaxed_path_len"] = np.array([len(p) for p in paths], np.int64)
+        rec["relaxed_paths"] = np.concatenate([np.asarray(p, np.int64) for p in paths])
+    np.savez_compressed(OUT / f"{name}.npz", **rec)
+    print(f"{name}: V={g.num_vertices} E={g.num_edges} alive={mask.alive_count} qp={mask.pairs_qp} "
+          f"path={path} build={t_build:.2f}s cut={t_cut:.2f}s path={t_path*1e3:.1f}ms", flush=True)
+
+
+def scenario_case(name, s, *, full, detail, goals=None, relaxed=None, extra=None):
+    oracle = bg.build_oracle(s.spec, s.xd, s.u_bounds, s.tube)
+    include = [s.start, s.goal]
+    if extra is not None:
+        include = list(extra) + include
+    capture(name, s.graph_n, s.spec, oracle, s.sample_bounds, s.seed_graph, np.array(include),
+            rsim._inflated(s, 0.0), s.start, s.goal, full=full, detail=detail, goals=goals, relaxed_starts=relaxed)
+
+
+def case_demo():
+    s = rsc.demo_scenario()
+    s.graph_n = 200
+    rng = np.random.default_rng(5)
+    relaxed = np.hstack([rng.uniform(0.3, 4.7, (8, 2)), rng.uniform(-0.3, 0.3, (8, 2))])
+    scenario_case("demo200", s, full=True, detail=True, relaxed=relaxed)
+
+
+def case_rf_small():
+    s = rsc.random_field_scenario(5, n_obstacles=20, graph_n=300)
+    scenario_case("rf300_s5", s, full=True, detail=True)
+
+
+def case_cfg2():
+    s = rsc.random_field_scenario(1, n_obstacles=20, graph_n=2000)
+    rng = np.random.default_rng(0)
+    goals = np.zeros((100, 4))
+    goals[:, :2] = rng.uniform(0.3, 4.7, size=(100, 2))
+    scenario_case("cfg2_rf2000", s, full=False, detail=False, goals=goals)
+
+
+def case_maze():
+    s, grid = rsc.maze_scenario()
+    scenario_case("maze", s, full=False, detail=False, extra=grid)
+
+
+def _hop_spec():
+    spec = bg.BezierSpec(m=2, gamma=3, T=1.0)
+    xd = rgeo.Box(np.array([0.0, 0.0, -1.5, -1.5, -4.0, -4.0]), np.array([5.0, 5.0, 1.5, 1.5, 4.0, 4.0])).to_polytope()
+    u = rgeo.Box(np.array([-30.0, -30.0]), np.array([30.0, 30.0]))
+    sample = rgeo.Box(np.array([0.0, 0.0, -0.6, -0.6, -1.0, -1.0]), np.array([5.0, 5.0, 0.6, 0.6, 1.0, 1.0]))
+    tube = rsim.design_tube(spec, (6.0, 11.0, 6.0), 0.02)
+    return spec, xd, u, sample, tube
+
+
+def case_hop_small():
+    """gamma=3 (degree 5) at reduced size: the cfg3 recipe with N=1500 and 12 boxes."""
+    spec, xd, u, sample, tube = _hop_spec()
+    oracle = bg.build_oracle(spec, xd, u, tube)
+    rng = np.random.default_rng(11)
+    obs = []
+    for _ in range(12):
+        c = rng.uniform(0.4, 4.6, 2)
+        w = rng.uniform(0.25, 0.7, 2)
+        obs.append(rsc._box_obstacle(c[0], c[1], w[0], w[1]).shape)
+    pos = tube.position_box(2)
+    obs = [rgeo.inflate(o, pos) for o in obs]
+    start = np.array([0.4, 0.4, 0, 0, 0, 0.0])
+    goal = np.array([4.6, 4.6, 0, 0, 0, 0.0])
+    capture("hop1500", 1500, spec, oracle, sample, 1, np.array([start, goal]), obs, start, goal,
+            full=True, detail=True)
+
+
+def case_reject():
+    """Non-box state set with heavy rejection (~half the candidates) to pin the sampler."""
+    spec = bg.BezierSpec(m=2, gamma=2, T=1.0)
+    xd0, u, sample = rsc._standard_sets()
+    # cut the square by the diagonal half-plane x + y <= 5
+    A = np.vstack([xd0.A, [[1.0, 1.0, 0.0, 0.0]]])
+    b = np.concatenate([xd0.b, [5.0]])
+    xd = rgeo.Polytope(A, b)
+    tube = rsim.design_tube(spec, (6.0, 5.0), 0.02)
+    oracle = bg.build_oracle(spec, xd, u, tube)
+    start = np.array([0.5, 0.5, 0, 0.0])
+    goal = np.array([3.0, 1.5, 0, 0.0])
+    obs = [rgeo.inflate(rsc._box_obstacle(1.5, 1.5, 0.6, 0.6).shape, tube.position_box(2))]
+    capture("reject400", 400, spec, oracle, sample, 3, np.array([start, goal]), obs, start, goal,
+            full=True, detail=True)
+
+
+CASES = {"demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,
+         "cfg2": case_cfg2, "maze": case_maze}
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or list(CASES)
+    for w in which:
+        CASES[w]()

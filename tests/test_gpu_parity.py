@@ -1,0 +1,202 @@
+"""Device parity against the reference goldens and the CPU oracle (run on a B200).
+
+Every call goes through libbzg.so (the C ABI) via the drop-in Python API.
+Bit-exact: vertices, edges/CSR, costs, control points, heuristic outcomes,
+path node sequences and path costs.  QP-decided pairs: verdict differences
+must fall in the solver-sensitive class and are reported.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_13507_b200 import _native as nat
+from paper_2411_13507_b200 import graph as G
+from tests.helpers import compare_cut, digest, inputs_from_golden
+
+pytestmark = pytest.mark.gpu
+
+FULL = ["demo200", "rf300_s5", "hop1500", "reject400"]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = nat.Context(0)
+    nat.set_default_context(c)
+    yield c
+    nat.set_default_context(None)
+
+
+def _build(g, ctx):
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    return G.build_graph(N, spec, orc, bounds, seed, include, ctx=ctx), obstacles, start, goal
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_build_bitwise(ctx, golden, name):
+    g = golden(name)
+    gr, *_ = _build(g, ctx)
+    assert gr.num_vertices == int(g["V"]) and gr.num_edges == int(g["E"])
+    assert gr.vertices.tobytes() == g["vertices"].tobytes()
+    assert np.array_equal(gr.edges, g["edges"])
+    assert gr.costs.tobytes() == g["costs"].tobytes()
+    assert gr.edge_points.tobytes() == g["edge_points"].tobytes()
+    rp, col = gr.csr()
+    assert np.array_equal(np.diff(rp), np.bincount(g["edges"][:, 0], minlength=gr.num_vertices))
+    assert np.array_equal(col, g["edges"][:, 1])
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_cut_and_path(ctx, golden, name):
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+    mask = G.cut_graph(gr, obstacles)
+    rep = compare_cut(mask, g)
+    print(name, json.dumps(rep))
+    assert rep["same_pending"], rep
+    assert rep["counters_dev"][:4] == rep["counters_ref"][:4]
+    assert rep["mismatch_outside_sensitive"] == 0, rep
+    assert rep["alive_mismatch_untouched"] == 0 and rep["prov_mismatch_untouched"] == 0, rep
+    path = G.find_path(gr, mask, start, goal)
+    if rep["verdict_mismatch"] == 0:
+        assert np.array_equal(mask.alive, g["alive"])
+        assert np.array_equal(mask.provenance_codes, g["provenance"])
+        assert rep["counters_dev"] == rep["counters_ref"]
+        if bool(g["path_none"]):
+            assert path is None
+        else:
+            assert path == list(g["path"])
+            assert G.path_cost(gr, path) == float(g["path_cost"])
+
+
+def test_path_on_golden_mask(ctx, golden):
+    """find_path against the reference's own alive mask: node sequence and cost bitwise."""
+    for name in FULL:
+        g = golden(name)
+        gr, obstacles, start, goal = _build(g, ctx)
+
+        class RefMask:
+            alive = g["alive"]
+
+        path = G.find_path(gr, RefMask(), start, goal)
+        if bool(g["path_none"]):
+            assert path is None
+        else:
+            assert path == list(g["path"]), name
+            assert G.path_cost(gr, path) == float(g["path_cost"])
+
+
+def test_relaxed_snapping(ctx, golden):
+    g = golden("demo200")
+    gr, obstacles, start, goal = _build(g, ctx)
+
+    class RefMask:
+        alive = g["alive"]
+
+    lens, flat = g["relaxed_path_len"], g["relaxed_paths"]
+    off = 0
+    for k, st in enumerate(g["relaxed_starts"]):
+        p = G.find_path(gr, RefMask(), st, goal, position_only_snap=True, require_tube_snap=False)
+        assert (p or []) == list(flat[off:off + lens[k]]), k
+        off += lens[k]
+
+
+def test_cfg2_build_cut_path_and_replanning(ctx, golden):
+    g = golden("cfg2_rf2000")
+    gr, obstacles, start, goal = _build(g, ctx)
+    assert digest(gr.vertices) == str(g["sha_vertices"])
+    assert digest(gr.edges) == str(g["sha_edges"])
+    assert digest(gr.costs) == str(g["sha_costs"])
+    assert digest(gr.edge_points) == str(g["sha_points"])
+    mask = G.cut_graph(gr, obstacles)
+    cnt = [mask.pairs_total, mask.pairs_point_hit, mask.pairs_hyperplane, mask.pairs_qp, mask.qp_safe,
+           mask.qp_unsafe]
+    ref = [int(x) for x in g["counters"]]
+    assert cnt[:4] == ref[:4]
+    mism = int((mask.alive != g["alive"]).sum())
+    print("cfg2 counters", cnt, ref, "alive mismatches", mism)
+    assert abs(cnt[4] - ref[4]) <= max(5, ref[3] // 1000)
+    assert mism <= max(5, ref[3] // 1000)
+
+    class RefMask:
+        alive = g["alive"]
+
+    path = G.find_path(gr, RefMask(), start, goal)
+    assert path == list(g["path"])
+    assert G.path_cost(gr, path) == float(g["path_cost"])
+    # cfg4: 100 goal updates on the fixed (graph, mask)
+    lens, flat = g["goal_path_len"], g["goal_paths"]
+    off = 0
+    for k, gl in enumerate(g["goals"]):
+        p = G.find_path(gr, RefMask(), start, gl)
+        assert (p or []) == list(flat[off:off + lens[k]]), k
+        if p:
+            assert G.path_cost(gr, p) == float(g["goal_costs"][k])
+        off += lens[k]
+
+
+def test_maze_ties(ctx, golden):
+    """Grid vertices via include, 424 wall boxes, tied parents: path bitwise on the golden mask."""
+    g = golden("maze")
+    gr, obstacles, start, goal = _build(g, ctx)
+    assert digest(gr.vertices) == str(g["sha_vertices"])
+    assert digest(gr.edges) == str(g["sha_edges"])
+    assert digest(gr.costs) == str(g["sha_costs"])
+
+    class RefMask:
+        alive = g["alive"]
+
+    path = G.find_path(gr, RefMask(), start, goal)
+    assert path == list(g["path"])
+    mask = G.cut_graph(gr, obstacles)
+    assert [mask.pairs_total, mask.pairs_point_hit, mask.pairs_hyperplane, mask.pairs_qp] == \
+        [int(x) for x in g["counters"][:4]]
+    print("maze alive mismatches", int((mask.alive != g["alive"]).sum()), "qp", mask.pairs_qp)
+
+
+def test_check_edges_vs_oracle(ctx, golden):
+    g = golden("hop1500")
+    N, spec, orc, *_ = inputs_from_golden(g)
+    rng = np.random.default_rng(0)
+    V = g["vertices"]
+    i = rng.integers(0, V.shape[0], 20000)
+    j = rng.integers(0, V.shape[0], 20000)
+    dev = G.check_edges(orc, V[i], V[j], ctx=ctx)
+    ref = oracle.check_edges(g["F"], g["G"], spec.n, V[i], V[j])
+    assert np.array_equal(dev, ref)
+    assert dev.any() and not dev.all()
+
+
+def test_argument_errors(ctx, golden):
+    g = golden("demo200")
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    with pytest.raises(ValueError, match="at least two"):
+        G.build_graph(1, spec, orc, bounds, seed, ctx=ctx)
+    from paper_2411_13507_b200.geometry import Box
+
+    with pytest.raises(ValueError, match="4-dimensional"):
+        G.build_graph(10, spec, orc, Box(np.zeros(3), np.ones(3)), seed, ctx=ctx)
+
+
+def test_edge_cases(ctx, golden):
+    g = golden("demo200")
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    # N = 2 and start == goal: singleton path
+    gr = G.build_graph(2, spec, orc, bounds, seed, include=np.array([start]), ctx=ctx)
+    mask = G.cut_graph(gr, [])
+    assert mask.pairs_total == 0 and mask.heuristic_fraction == 1.0
+    assert G.find_path(gr, mask, start, start) == [2]
+    # no obstacles: everything alive, all heuristic-safe
+    gr = G.build_graph(200, spec, orc, bounds, seed, include=include, ctx=ctx)
+    mask = G.cut_graph(gr, [])
+    assert mask.alive.all() and (mask.provenance_codes == 1).all()
+    ref = oracle.build_graph(200, spec, orc, bounds, seed, include, D=g["D"])
+    assert np.array_equal(gr.edges, ref["edges"])
+    # sharded row blocks concatenate to the full edge list
+    parts = [G.build_graph(200, spec, orc, bounds, seed, include, ctx=ctx, rows=(a, b))
+             for a, b in ((0, 67), (67, 150), (150, 202))]
+    cat = np.concatenate([p.edges for p in parts])
+    assert np.array_equal(cat, ref["edges"])
+    assert np.concatenate([p.costs for p in parts]).tobytes() == ref["costs"].tobytes()

@@ -1,0 +1,99 @@
+"""Pin the CPU oracle (oracle/, a numpy restatement of the reference) to golden
+vectors captured from the live reference (tests/golden/make_golden.py).
+
+Bitwise: vertices, edges, costs, control points, per-obstacle heuristic codes,
+QP status/iterations/||delta||, alive, provenance, counters, path and its cost.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle.qp_ref import AdmmSettings
+from tests.helpers import digest, inputs_from_golden
+
+FULL = ["demo200", "rf300_s5", "hop1500", "reject400"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_build_bitwise(golden, name):
+    g = golden(name)
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    out = oracle.build_graph(N, spec, orc, bounds, seed, include, D=g["D"])
+    assert out["vertices"].tobytes() == g["vertices"].tobytes()
+    assert np.array_equal(out["edges"], g["edges"])
+    assert out["costs"].tobytes() == g["costs"].tobytes()
+    assert out["edge_points"].tobytes() == g["edge_points"].tobytes()
+    assert digest(out["edges"]) == str(g["sha_edges"])
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_cut_and_path_bitwise(golden, name):
+    g = golden(name)
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    pts = g["edge_points"]
+    res = oracle.cut_graph(pts, [(o.A, o.b) for o in obstacles], settings=AdmmSettings(), record=True)
+    assert np.array_equal(res["alive"], g["alive"])
+    assert np.array_equal(res["provenance"], g["provenance"])
+    cnt = [res[k] for k in ("pairs_total", "pairs_point_hit", "pairs_hyperplane", "pairs_qp", "qp_safe", "qp_unsafe")]
+    assert cnt == list(g["counters"])
+    codes = np.stack([e["codes"] for e in res["log"]])
+    assert np.array_equal(codes, g["codes"])
+    st = np.concatenate([e.get("status", np.zeros(0, np.int8)) for e in res["log"]])
+    it = np.concatenate([e.get("iters", np.zeros(0, np.int64)) for e in res["log"]])
+    dl = np.concatenate([e.get("delta", np.zeros(0)) for e in res["log"]])
+    assert np.array_equal(st, g["qp_status"])
+    assert np.array_equal(it, g["qp_iters"])
+    assert dl.tobytes() == g["qp_delta"].tobytes()
+    path, dist = oracle.find_path(g["vertices"], g["edges"], g["costs"], res["alive"], start, goal, spec.m,
+                                  g["tube_lo"], g["tube_hi"])
+    if bool(g["path_none"]):
+        assert path is None
+    else:
+        assert path == list(g["path"])
+        assert dist == float(g["path_cost"])
+        assert oracle.path_cost(g["edges"], g["costs"], path) == float(g["path_cost"])
+
+
+def test_relaxed_snapping(golden):
+    g = golden("demo200")
+    spec_m = int(g["m"])
+    lens = g["relaxed_path_len"]
+    flat = g["relaxed_paths"]
+    off = 0
+    for k, st in enumerate(g["relaxed_starts"]):
+        path, _ = oracle.find_path(g["vertices"], g["edges"], g["costs"], g["alive"], st, g["goal"], spec_m,
+                                   g["tube_lo"], g["tube_hi"], position_only_snap=True, require_tube_snap=False)
+        want = list(flat[off:off + lens[k]])
+        off += lens[k]
+        assert (path or []) == want
+
+
+def test_cfg2_build_digests(golden):
+    """cfg2 (2,002 vertices, 249,437 edges): build digests and Dijkstra on the golden mask."""
+    g = golden("cfg2_rf2000")
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    out = oracle.build_graph(N, spec, orc, bounds, seed, include, D=g["D"])
+    assert digest(out["vertices"]) == str(g["sha_vertices"])
+    assert digest(out["edges"]) == str(g["sha_edges"])
+    assert digest(out["costs"]) == str(g["sha_costs"])
+    assert digest(out["edge_points"]) == str(g["sha_points"])
+    path, dist = oracle.find_path(out["vertices"], out["edges"], out["costs"], g["alive"], start, goal, spec.m,
+                                  g["tube_lo"], g["tube_hi"])
+    assert path == list(g["path"]) and dist == float(g["path_cost"])
+    # cfg4: the first 10 replanning goals on the fixed map
+    lens, flat = g["goal_path_len"], g["goal_paths"]
+    off = 0
+    for k in range(10):
+        p, _ = oracle.find_path(out["vertices"], out["edges"], out["costs"], g["alive"], start, g["goals"][k],
+                                spec.m, g["tube_lo"], g["tube_hi"])
+        assert (p or []) == list(flat[off:off + lens[k]])
+        off += lens[k]
+
+
+def test_check_edges_matches_pair_test(golden):
+    g = golden("demo200")
+    V, E = g["vertices"], g["edges"]
+    n = V.shape[1]
+    ok = oracle.check_edges(g["F"], g["G"], n, V[E[:, 0]], V[E[:, 1]])
+    assert ok.all()
