@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 graph-construction stage (BASELINE.json metric).
+
+One step = the whole hot path on one synthetic scene: sample V states (PCG64 on
+device) -> all-pairs reachability test -> ordered CSR + edge costs -> obstacle cut
+(box heuristic + batched Cut-QP + aggregation) -> snapping + Bellman-Ford shortest
+path.  Default workload: cfg3 (degree-5 / gamma=3 hopping model, 20,000 samples +
+start/goal, 50 boxes), i.e. 4.0e8 ordered pairs.
+
+metric: edge evaluations/s = V^2 / t_step (whole job, all GPUs); ms_per_step is the
+build+cut+solve latency.  ``value`` is timed with CUDA events on the library's stream
+with L2 flushed before every step; ``e2e`` times the public Python API
+(build_graph -> cut_graph -> find_path) with host inputs and the path read back.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (row-block sharding, NCCL gather)
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "edge evaluations/sec (V^2 / graph-build+cut+solve latency)"
+UNIT = "edge_evals/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=0, help="source rows in the CPU sample (0 = auto)")
+    ap.add_argument("--breakdown", action="store_true", help="print the per-kernel table to stderr")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(name):
+    from paper_2411_13507_b200 import configs
+
+    return configs.BUILDERS[name]()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        busy = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
+
+
+# ----------------------------------------------------------------------------- device step
+class DeviceStep:
+    """build -> cut -> (gather) -> find_path through libbzg, host constants prepared once."""
+
+    def __init__(self, ctx, w, rank=0, world=1):
+        from paper_2411_13507_b200 import graph as G
+        from paper_2411_13507_b200 import shard
+
+        self.G, self.ctx, self.w = G, ctx, w
+        self.rank, self.world = rank, world
+        V = w.num_vertices
+        self.rows = shard.row_block(V, rank, world) if world > 1 else None
+        self.desc, self._keep, self.D = G._build_desc(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, w.include,
+                                                       rows=self.rows)
+        self.obs = G._obstacle_arrays(w.obstacles, w.spec.m)
+        self.cfg = G._cut_cfg(G.CutConfig())
+        self.last = {}
+
+    def run(self):
+        G, lib, ctx, w = self.G, self.ctx.lib, self.ctx, self.w
+        from paper_2411_13507_b200 import _native as nat
+
+        h = C.c_void_p()
+        nat.check(lib.bzg_build_graph(ctx.handle, C.byref(self.desc), C.byref(h)))
+        graph = G.BezierGraph(h, ctx, w.spec, w.oracle, w.seed, w.sample_bounds, self.D)
+        offs, A, b, is_box, lo, hi = self.obs
+        mh = C.c_void_p()
+        nat.check(lib.bzg_cut_graph(ctx.handle, h, len(is_box), nat.ptr(offs), nat.ptr(A), nat.ptr(b), nat.ptr(is_box),
+                                    nat.ptr(lo), nat.ptr(hi), C.byref(self.cfg), C.byref(mh)))
+        cnt = np.zeros(6, dtype=np.int64)
+        nat.check(lib.bzg_mask_copy(mh, None, None, nat.ptr(cnt)))
+        mask = G.CutMask(mh, graph, cnt)
+        if self.world > 1:
+            from paper_2411_13507_b200 import shard
+
+            local_E = graph.num_edges
+            mask = shard.gather_to_all(graph, mask)
+            self.last["local_edges"] = local_E
+        path = None
+        if self.rank == 0:
+            path = G.find_path(graph, mask, w.start, w.goal)
+        self.last.update(E=graph.num_edges, qp=mask.pairs_qp, alive=None, path=path, counters=cnt.tolist())
+        self.last_graph, self.last_mask = graph, mask
+        return path
+
+
+def public_api_step(w, ctx, rank, world):
+    """The call sequence a user makes (reference sim.plan_once order), host inputs, path read back."""
+    from paper_2411_13507_b200 import graph as G
+    from paper_2411_13507_b200 import shard
+
+    rows = shard.row_block(w.num_vertices, rank, world) if world > 1 else None
+    g = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, include=w.include, ctx=ctx, rows=rows)
+    mask = G.cut_graph(g, w.obstacles)
+    if world > 1:
+        mask = shard.gather_to_all(g, mask)
+    path = G.find_path(g, mask, w.start, w.goal) if rank == 0 else None
+    return path
+
+
+def h2d_d2h_bytes(w, path_len):
+    n = w.spec.n
+    h2d = (w.oracle.F.nbytes + w.oracle.G.nbytes + 8 * (w.spec.p + 1) * 2 * w.spec.gamma + w.oracle.Xd.A.nbytes
+           + w.oracle.Xd.b.nbytes + 2 * 8 * n + (0 if w.include is None else np.asarray(w.include).nbytes)
+           + sum(o.A.nbytes + o.b.nbytes + 2 * 8 * w.spec.m + 5 for o in w.obstacles) + 4 * 8 * n)
+    d2h = 8 * path_len + 8 + 6 * 8 + 3 * 8  # path, dist, counters, E/sample/qp counts
+    return int(h2d), int(d2h)
+
+
+# ----------------------------------------------------------------------------- roofline
+def algorithmic_work(kernel, w, step_info, world):
+    """Algorithmic work of one launch of `kernel`: (amount, unit, bound)."""
+    V = w.num_vertices
+    g = w.spec.gamma
+    m = w.spec.m
+    E = step_info["E"]
+    O = len(w.obstacles)
+    if kernel == "k_pair_bits":
+        K = (w.oracle.F.shape[0] - 4 * w.spec.n) // 2  # coupled rows as two-sided intervals
+        pairs = V * V / world
+        return pairs * 3 * K, "fp64"
+    if kernel == "k_cut_heuristic":
+        J = 2 * g
+        per = J * 2 * m * (2 * m) + J * (3 * m + 1) + 2 * m * 4 + J * (2 * m)  # SURVEY.md §8(d) box pair
+        return E * O * per, "fp64"
+    return None, None
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+
+    from paper_2411_13507_b200 import _native as nat
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx = nat.Context(local, stream=stream.cuda_stream)
+    nat.set_default_context(ctx)
+    w = workload(args.config)
+    V = w.num_vertices
+    step = DeviceStep(ctx, w, rank, world)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    fp64_rate = ctx.probe_fp64(True)  # DFMA instructions/s on this device
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(max(args.warmup, 0)):
+        step.run()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device): K steps, L2 flushed before each
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step.run()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ctx.set_profiling(False)
+    launches, kstats = ctx.stats()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+    value = V * V / (ms_per_step * 1e-3)
+
+    # ---------------- e2e through the public API
+    e2e_ms = []
+    path = None
+    for k in range(args.steps + 1):
+        flush.zero_()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        path = public_api_step(w, ctx, rank, world)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if k > 0:  # first call re-warms the Python path
+            e2e_ms.append((t1 - t0) * 1e3)
+    et = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+    e2e_step_ms = float(et.item())
+    h2d, d2h = h2d_d2h_bytes(w, len(path or []))
+
+    # ---------------- roofline of the dominant kernel
+    per_step = {k: (ms / args.steps, n / args.steps) for k, (ms, n) in kstats.items()}
+    dom = max(per_step, key=lambda k: per_step[k][0])
+    roof = {"kernel": dom}
+    work, bound = algorithmic_work(dom, w, step.last, world)
+    dom_ms, dom_n = per_step[dom]
+    if work is not None and dom_n > 0:
+        avg_launch_s = dom_ms / dom_n * 1e-3
+        achieved = work / dom_n / avg_launch_s
+        roof.update(bound=bound, achieved=achieved / 1e9, peak=fp64_rate / 1e9, unit="Gop/s (FP64 instr)",
+                    frac=achieved / fp64_rate, traffic=None,
+                    peak_source="measured DFMA issue rate (bzg_probe_fp64, this run)")
+    else:
+        roof.update(bound=None, achieved=None, peak=None, frac=None, traffic=None)
+    share = dom_ms / ms_per_step
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "vertices": V, "ordered_pairs": V * V, "edges": step.last["E"],
+                   "obstacles": len(w.obstacles), "gamma": w.spec.gamma, "degree": w.spec.p,
+                   "qp_instances": step.last["qp"], "parallelism": f"row-block x{world}",
+                   "l2": "flushed before every step (256 MiB write)", "seed": w.seed},
+        "latency_ms": ms_per_step,
+        "path_hops": len(step.last["path"] or []) if rank == 0 else None,
+        "clocks": clk,
+        "e2e": {"value": V * V / (e2e_step_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_step_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "paper_2411_13507_b200.build_graph -> cut_graph -> find_path"},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "roofline": roof,
+        "dominant_kernel_share": share,
+        "kernels_ms_per_step": {k: round(v[0], 4) for k, v in sorted(per_step.items(), key=lambda kv: -kv[1][0])},
+        "fp64_peak_instr_per_s": fp64_rate,
+    }
+    if args.breakdown and rank == 0:
+        for k, (ms, n) in sorted(per_step.items(), key=lambda kv: -kv[1][0]):
+            print(f"{k:28s} {ms:9.4f} ms/step  {n:7.1f} launches/step", file=sys.stderr)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(w, step, args.cpu_rows)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- CPU baselines
+def _cpu_sample_rows(w, rows):
+    """Oracle port on source rows [r0, r1): (t_build_rows, t_cut, n_edges, n_qp)."""
+    import oracle
+    from paper_2411_13507_b200.bezier import boundary_matrix
+
+    D = boundary_matrix(w.spec)
+    n = w.spec.n
+    V_ = oracle.sample_states(w.N, w.sample_bounds.lo, w.sample_bounds.hi, w.oracle.Xd.A, w.oracle.Xd.b, w.seed,
+                              w.include)
+    A1, A2 = oracle.project(V_, w.oracle.F, n)
+    t0 = time.perf_counter()
+    E = oracle.pair_edges(A1, A2, w.oracle.G, rows=rows)
+    pts = oracle.edge_points(V_, E, D, w.spec.gamma, w.spec.m)
+    oracle.edge_costs(pts)
+    t1 = time.perf_counter()
+    res = oracle.cut_graph(pts, [(o.A, o.b) for o in w.obstacles])
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, E.shape[0], res["pairs_qp"]
+
+
+def cpu_baseline(w, step, rows_opt):
+    """Single-core oracle (numpy restatement of the reference) on a bounded row sample."""
+    import oracle
+
+    V = w.num_vertices
+    S = rows_opt or max(8, min(V, int(round(V * 0.005))))  # ~0.5% of the source rows
+    t0 = time.perf_counter()
+    oracle.sample_states(w.N, w.sample_bounds.lo, w.sample_bounds.hi, w.oracle.Xd.A, w.oracle.Xd.b, w.seed, w.include)
+    t_sample = time.perf_counter() - t0
+    tb, tc, e_s, q_s = _cpu_sample_rows(w, (0, S))
+    # Dijkstra (heapq) on the full graph the device produced (same arrays the reference would search)
+    g, mk = step.last_graph, step.last_mask
+    t0 = time.perf_counter()
+    oracle.find_path(g.vertices, g.edges, g.costs, mk.alive, w.start, w.goal, w.spec.m, w.oracle.tube.error.lo,
+                     w.oracle.tube.error.hi)
+    t_path = time.perf_counter() - t0
+    t_full = t_sample + (tb + tc) * (V / S) + t_path
+    return {"value": V * V / t_full, "unit": UNIT, "cores": 1, "kind": "port",
+            "ms_per_step_extrapolated": t_full * 1e3,
+            "sample": (f"oracle port (numpy restatement of reference graph.py) single process: sampling of all "
+                       f"{V} states, pair test + control points + costs + box cut + Cut-QP on source rows [0,{S}) "
+                       f"({S * V} pairs, {e_s} edges, {q_s} QPs) extrapolated x{V / S:.1f}, heapq Dijkstra on the "
+                       f"full {g.num_edges}-edge graph; measured build {tb:.2f}s cut {tc:.2f}s path {t_path:.2f}s"),
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _ref_worker(payload):
+    name, r0, r1 = payload
+    w = workload(name)
+    return _cpu_sample_rows(w, (r0, r1))
+
+
+def reference_arm(args, rank, world):
+    """`--impl reference`: the oracle port of the reference CPU path on all host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import multiprocessing as mp
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    w = workload(args.config)
+    V = w.num_vertices
+    cores = len(os.sched_getaffinity(0))
+    S = args.cpu_rows or min(V, cores * 48)
+    chunks = [(args.config, S * k // cores, S * (k + 1) // cores) for k in range(cores)]
+    times = []
+    with mp.get_context("spawn").Pool(cores) as pool:
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker, chunks)
+            t = time.perf_counter() - t0
+            if k >= args.warmup:
+                times.append(t)
+    ms_sample = statistics.mean(times) * 1e3
+    ms_full = ms_sample * V / S
+    value = V * V / (ms_full * 1e-3)
+    e_s = sum(r[2] for r in res)
+    q_s = sum(r[3] for r in res)
+    sample = (f"oracle port (numpy restatement of reference graph.py/qpsolver.py) in a {cores}-process pool: each "
+              f"step = pair test + control points + costs + box cut + Cut-QP on source rows [0,{S}) of {w.name} "
+              f"({S * V} pairs, {e_s} edges, {q_s} QPs), extrapolated x{V / S:.1f} to all rows; Dijkstra excluded")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_full, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": w.name, "vertices": V, "ordered_pairs": V * V, "obstacles": len(w.obstacles),
+                      "gamma": w.spec.gamma, "parallelism": f"cpu x{cores}"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                            "cpu_model": _cpu_model()},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

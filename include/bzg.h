@@ -99,6 +99,10 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* desc, bzg_graph** out);
 int bzg_graph_from_edges(bzg_ctx* ctx, int32_t m, int32_t gamma, int32_t p, const double* D, int64_t V,
                          const double* vertices_host, int64_t E, const int32_t* src, const int32_t* dst,
                          const double* cost, int on_device, bzg_graph** out);
+/* replace the edge set of g (row-major ordered (src, dst) + cost; device or host pointers):
+ * rank 0 adopts the gathered edge list of all row blocks; the row block becomes [0, V) */
+int bzg_graph_set_edges(bzg_graph* g, int64_t E, const int32_t* src, const int32_t* dst, const double* cost,
+                        int on_device);
 int bzg_graph_destroy(bzg_graph* g);
 int bzg_graph_info(const bzg_graph* g, int64_t* V, int64_t* E, int64_t* row_begin, int64_t* row_end);
 /* host copies (BezierGraph fields, graph.py:61-68); any pointer may be NULL */
@@ -150,6 +154,11 @@ int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start,
                   const double* tube_lo, const double* tube_hi, double eps_geo, int position_only_snap,
                   int require_tube_snap, int64_t* path_out, int64_t path_cap, int64_t* path_len,
                   double* dist_out);
+
+/* ---- diagnostics (not a reference entry point) -------------------------- */
+/* sustained FP64 instruction issue rate (DFMA if use_fma else DADD), instructions/s:
+ * the roofline denominator of the FP64-pipe-bound kernels (pair test, box cut, QP). */
+int bzg_probe_fp64(bzg_ctx* ctx, int use_fma, double* instr_per_s);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,7 @@ _SIGS = {
     "bzg_build_graph": ([_P, C.POINTER(BuildDesc), C.POINTER(_P)], C.c_int),
     "bzg_graph_from_edges": ([_P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P, C.c_int64, _P, _P, _P,
                               C.c_int, C.POINTER(_P)], C.c_int),
+    "bzg_graph_set_edges": ([_P, C.c_int64, _P, _P, _P, C.c_int], C.c_int),
     "bzg_graph_destroy": ([_P], C.c_int),
     "bzg_graph_info": ([_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                         C.POINTER(C.c_int64)], C.c_int),
@@ -83,6 +84,7 @@ _SIGS = {
     "bzg_mask_export_device": ([_P, _P, _P], C.c_int),
     "bzg_find_path": ([_P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_int, C.c_int, _P, C.c_int64,
                        C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
+    "bzg_probe_fp64": ([_P, C.c_int, C.POINTER(C.c_double)], C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -166,6 +168,12 @@ class Context:
             nm = names.raw[64 * i: 64 * i + 64].split(b"\0", 1)[0].decode()
             out[nm] = (float(ms[i]), int(cnt[i]))
         return launches.value, out
+
+    def probe_fp64(self, use_fma: bool = True) -> float:
+        """Measured FP64 instruction issue rate (instructions/s) of this device."""
+        r = C.c_double()
+        check(self.lib.bzg_probe_fp64(self.handle, int(bool(use_fma)), C.byref(r)))
+        return r.value
 
     def close(self):
         if getattr(self, "handle", None):

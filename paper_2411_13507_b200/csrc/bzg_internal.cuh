@@ -178,7 +178,7 @@ struct Mask {
   DevBuf prov;                    // E uint8
   int64_t counters[6] = {0, 0, 0, 0, 0, 0};
   // QP diagnostics
-  int64_t n_qp = 0;
+  int64_t n_qp = 0, n_polished = 0;
   DevBuf qp_edge, qp_obs, qp_status, qp_iters, qp_delta;
   // cached shortest-path tree (reused while (mask, v0) is unchanged: cfg4 replanning)
   int64_t tree_v0 = -1;
@@ -192,6 +192,7 @@ struct Mask {
 void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices);
 void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g);
 void materialize_points(Ctx* c, Graph* g);
+void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, const double* cost, bool on_device);
 void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, double eps, int64_t k,
                  const double* X1, const double* X2, uint8_t* out);
 void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,

@@ -197,43 +197,30 @@ int bzg_graph_from_edges(bzg_ctx* ctx, int32_t m, int32_t gamma, int32_t p, cons
   bzg_graph* g = nullptr;
   int rc = guarded([&] {
     BZG_REQUIRE(ctx && D && vertices_host && out, BZG_EINVAL, "null argument");
-    BZG_REQUIRE(p == 2 * gamma - 1, BZG_EINVAL, "boundary-value curves require p = 2*gamma - 1");
+    BZG_REQUIRE(m >= 1 && gamma >= 1 && p == 2 * gamma - 1, BZG_EINVAL, "boundary-value curves require p = 2*gamma - 1");
+    BZG_REQUIRE(V >= 1 && V < (1ll << 31), BZG_EINVAL, "vertex count out of range");
     set_device(ctx);
     g = new bzg_graph();
     g->ctx = ctx;
     g->m = m; g->gamma = gamma; g->p = p; g->n = m * gamma;
-    g->V = V; g->E = E; g->row_begin = 0; g->row_end = V;
+    g->V = V;
     g->D.assign(D, D + (size_t)(p + 1) * 2 * gamma);
-    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     g->vertices.alloc((size_t)V * g->n * sizeof(double), ctx->stream);
     BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.ptr, vertices_host, (size_t)V * g->n * sizeof(double),
                                    cudaMemcpyHostToDevice, ctx->stream));
-    g->src.alloc(E * sizeof(int), ctx->stream);
-    g->dst.alloc(E * sizeof(int), ctx->stream);
-    g->cost.alloc(E * sizeof(double), ctx->stream);
-    if (E > 0) {
-      BZG_CHECK_CUDA(cudaMemcpyAsync(g->src.ptr, src, E * sizeof(int), kind, ctx->stream));
-      BZG_CHECK_CUDA(cudaMemcpyAsync(g->dst.ptr, dst, E * sizeof(int), kind, ctx->stream));
-      BZG_CHECK_CUDA(cudaMemcpyAsync(g->cost.ptr, cost, E * sizeof(double), kind, ctx->stream));
-    }
-    // row_ptr from the (row-major ordered) sources
-    std::vector<int> hs(E);
-    if (E > 0) BZG_CHECK_CUDA(cudaMemcpyAsync(hs.data(), g->src.ptr, E * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::vector<long long> rp(V + 1, 0);
-    for (long long e = 0; e < E; ++e) {
-      BZG_REQUIRE(hs[e] >= 0 && hs[e] < V && (e == 0 || hs[e] >= hs[e - 1]), BZG_EINVAL,
-                  "edges must be sorted by source");
-      rp[hs[e] + 1]++;
-    }
-    for (long long i = 0; i < V; ++i) rp[i + 1] += rp[i];
-    g->row_ptr.alloc((V + 1) * sizeof(long long), ctx->stream);
-    BZG_CHECK_CUDA(cudaMemcpyAsync(g->row_ptr.ptr, rp.data(), (V + 1) * sizeof(long long), cudaMemcpyHostToDevice,
-                                   ctx->stream));
-    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+    set_edges(ctx, g, E, src, dst, cost, on_device != 0);
   });
   if (rc == BZG_OK) *out = g; else delete g;
   return rc;
+}
+
+int bzg_graph_set_edges(bzg_graph* g, int64_t E, const int32_t* src, const int32_t* dst, const double* cost,
+                        int on_device) {
+  return guarded([&] {
+    BZG_REQUIRE(g && (E == 0 || (src && dst && cost)), BZG_EINVAL, "null argument");
+    set_device(g->ctx);
+    set_edges(g->ctx, g, E, src, dst, cost, on_device != 0);
+  });
 }
 
 int bzg_graph_destroy(bzg_graph* g) {

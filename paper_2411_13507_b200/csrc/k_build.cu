@@ -241,6 +241,18 @@ __global__ void k_row_ptr_global(const long long* __restrict__ local, long long 
   out[i] = i <= r0 ? 0 : (i >= r1 ? E : local[i - r0]);
 }
 
+// row_ptr[i] = lower_bound(src, i) over a source-sorted edge list (gathered row blocks)
+__global__ void k_row_ptr_from_src(const int* __restrict__ src, long long E, long long V, long long* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i > V) return;
+  long long lo = 0, hi = E;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (src[mid] < i) lo = mid + 1; else hi = mid;
+  }
+  out[i] = lo;
+}
+
 // check_edges (reachability.py:139-142): X1 F1' + X2 F2' <= G + eps, separable form.
 __global__ void k_check_edges(const double* __restrict__ F, const double* __restrict__ thresh, int n, int nF,
                               long long k, const double* __restrict__ X1, const double* __restrict__ X2,
@@ -451,6 +463,27 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
   }
   launch(c, "k_row_ptr_global", k_row_ptr_global, dim3(div_up(V + 1, 256)), dim3(256), 0, rptr.as<long long>(),
          V, r0, r1, g->row_ptr.as<long long>());
+}
+
+void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, const double* cost, bool on_device) {
+  const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  BZG_REQUIRE(E >= 0 && E < (1ll << 31), BZG_EINVAL, "edge count out of range");
+  g->E = E;
+  g->row_begin = 0;
+  g->row_end = g->V;
+  g->points_ready = false;
+  g->src.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
+  g->dst.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
+  g->cost.alloc(std::max(E, 1ll) * sizeof(double), c->stream);
+  if (E > 0) {
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->src.ptr, src, E * sizeof(int), kind, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->dst.ptr, dst, E * sizeof(int), kind, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->cost.ptr, cost, E * sizeof(double), kind, c->stream));
+  }
+  g->row_ptr.alloc((g->V + 1) * sizeof(long long), c->stream);
+  launch(c, "k_row_ptr_from_src", k_row_ptr_from_src, dim3(div_up(g->V + 1, 256)), dim3(256), 0, g->src.as<int>(), E,
+         g->V, g->row_ptr.as<long long>());
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 void materialize_points(Ctx* c, Graph* g) {

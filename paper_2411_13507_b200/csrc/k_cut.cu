@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -18,8 +19,6 @@ namespace bzg {
 
 namespace {
 
-constexpr int kMaxM = 3;
-constexpr int kMaxObsRows = 2 * kMaxM;
 
 struct DParams {
   double D[64];
@@ -32,6 +31,7 @@ struct ObsRec {
   double b[2 * M];
   double b_eps[2 * M];  // fl(b + eps_geo)   (graph.py:234)
   double lo[M], hi[M];  // Polytope.as_box bounds (geometry.py:155-185)
+  double canon;         // 1 when A == [I; -I] exactly (Box.to_polytope row order)
 };
 
 struct CutScalars {
@@ -113,6 +113,69 @@ __device__ __forceinline__ int box_code(const double (&P)[M][2 * G], const ObsRe
   return clear ? 1 : 2;
 }
 
+// Same codes for an obstacle whose rows are exactly [I; -I] (Box.to_polytope order,
+// geometry.py:74-77, kept by inflate): every product with a +-1/0 coefficient is exact, so
+// A.P_j reduces to +-P[k][j] and the arithmetic of box_code is reproduced bit for bit
+// without the multiplications.
+template <int G, int M>
+__device__ __forceinline__ int box_code_canon(const double (&P)[M][2 * G], const ObsRec<M>& o, double margin) {
+  constexpr int J = 2 * G;
+  bool hit = false;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    bool in = true;
+#pragma unroll
+    for (int k = 0; k < M; ++k) in = in && (P[k][j] <= o.b_eps[k]) && (-P[k][j] <= o.b_eps[M + k]);
+    hit = hit || in;
+  }
+  if (hit) return 0;
+  int anchor = 0;
+  double best = 0.0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    double d2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double t = __dadd_rn(fmax(__dsub_rn(o.lo[k], P[k][j]), 0.0), fmax(__dsub_rn(P[k][j], o.hi[k]), 0.0));
+      const double sq = __dmul_rn(t, t);
+      d2 = (k == 0) ? sq : __dadd_rn(d2, sq);
+    }
+    if (j == 0 || d2 < best) { best = d2; anchor = j; }
+  }
+  double v[M], pr[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    double vk = P[k][0];
+#pragma unroll
+    for (int j = 1; j < J; ++j) if (anchor == j) vk = P[k][j];
+    v[k] = vk;
+    pr[k] = fmin(fmax(vk, o.lo[k]), o.hi[k]);
+  }
+  int face = 0;
+  double fbest = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 2 * M; ++c) {
+    const int k = c < M ? c : c - M;
+    const double sv = c < M ? v[k] : -v[k], sp = c < M ? pr[k] : -pr[k];
+    const double sep = __dsub_rn(sv, o.b[c]);
+    const double val = (fabs(__dsub_rn(sp, o.b[c])) <= 1e-7) ? sep : -INFINITY;
+    if (c == 0 || val > fbest) { fbest = val; face = c; }
+  }
+  bool clear = true;
+#pragma unroll
+  for (int c = 0; c < 2 * M; ++c) {
+    if (face == c) {
+      const int k = c < M ? c : c - M;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const double hp = c < M ? P[k][j] : -P[k][j];
+        clear = clear && (__dsub_rn(hp, o.b[c]) > margin);
+      }
+    }
+  }
+  return clear ? 1 : 2;
+}
+
 // One thread per edge, all obstacles of the chunk [o0, o1) in list order.
 // Tracks the first heuristic kill, counts codes, and appends indeterminate pairs
 // to the QP work list with warp-aggregated atomics.
@@ -152,7 +215,8 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
   const int lane = threadIdx.x & 31;
   for (int oi = 0; oi < nob; ++oi) {
     int code = 1;
-    if (valid) code = box_code<G, M>(P, s_obs[oi], margin);
+    if (valid) code = s_obs[oi].canon != 0.0 ? box_code_canon<G, M>(P, s_obs[oi], margin)
+                                             : box_code<G, M>(P, s_obs[oi], margin);
     if (valid) {
       c0 += code == 0;
       c1 += code == 1;
@@ -187,489 +251,13 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
   }
 }
 
-// ------------------------------------------------------------------ Cut-QP ADMM
-struct QpParams {
-  double rho, rho_eq, sigma, alpha, one_m_alpha, eps_abs, eps_rel, eps_pinf;
-  int max_iter;
-};
+}  // namespace
+}  // namespace bzg
 
-// Dense ADMM on the cut QP (graph.py:268-282 -> qpsolver.py:129-233), one thread per
-// instance, persistent lanes that fetch new instances as theirs terminate.
-//
-// Variables x = [lambda (J); delta (C)], constraints z = [Q lambda - delta (C); lambda (J);
-// sum lambda], l = [-inf; 0; 1], u = [b; +inf; 1], rho = [rho..; rho*1e3 on the equality row].
-// The reference inverts the (n+mc)^2 KKT matrix per instance; the KKT solve is equivalent to
-// xt = (P + sigma I + A'RA)^{-1} (sigma x + A'(R z - y)), zt = A xt, which the structure of A
-// reduces to one J x J SPD solve (Schur complement of the diagonal delta block), done here by
-// a per-instance Cholesky factor.  Iterates agree with the reference to rounding; termination,
-// the infeasibility certificate and MAX_ITER follow qpsolver.py:179-231 line by line.
-template <int G, int M>
-__global__ void __launch_bounds__(128) k_qp_admm(QpParams qp, DParams dp, const double* __restrict__ Vx,
-                                                 const int* __restrict__ src, const int* __restrict__ dst,
-                                                 const ObsRec<M>* __restrict__ obs,
-                                                 const unsigned long long* __restrict__ pend, long long n_inst,
-                                                 unsigned long long* __restrict__ next, int8_t* __restrict__ st_out,
-                                                 int* __restrict__ it_out, double* __restrict__ x_out,
-                                                 double* __restrict__ res_out) {
-  constexpr int J = 2 * G, C = 2 * M, N = G * M, NV = J + C, MC = C + J + 1;
-  const int lane = threadIdx.x & 31;
-  long long inst = -1;  // -1: needs work, -2: exhausted
-  int it = 0;
-  double Q[C][J], L[J][J], b[C];
-  double lam[J], del[C], z[MC], y[MC];
-  const double rho = qp.rho, req = qp.rho_eq, ri = 1.0 / qp.rho, rieq = 1.0 / qp.rho_eq;
-  const double kdd = 2.0 + qp.sigma + rho;  // delta-delta diagonal of P + sigma I + A'RA
-  while (true) {
-    const unsigned need = __ballot_sync(0xffffffffu, inst == -1);
-    if (need) {
-      unsigned long long base = 0;
-      const int leader = __ffs(need) - 1;
-      if (lane == leader) base = atomicAdd(next, (unsigned long long)__popc(need));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (inst == -1) {
-        const unsigned long long my = base + __popc(need & ((1u << lane) - 1u));
-        if ((long long)my >= n_inst) {
-          inst = -2;
-        } else {
-          inst = (long long)my;
-          const unsigned long long pk = pend[my];
-          const long long e = (long long)(pk >> 20);
-          const int oi = (int)(pk & 0xFFFFF);
-          const ObsRec<M>& o = obs[oi];
-          double xi[N], xj[N], P[M][J];
-#pragma unroll
-          for (int k = 0; k < N; ++k) {
-            xi[k] = Vx[(long long)src[e] * N + k];
-            xj[k] = Vx[(long long)dst[e] * N + k];
-          }
-          control_points<G, M>(xi, xj, dp.D, P);
-          // Q = A_O @ points (graph.py:276), BLAS product: FMA chain over m
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            b[c] = o.b[c];
-#pragma unroll
-            for (int j = 0; j < J; ++j) {
-              double acc = __dmul_rn(o.A[c][0], P[0][j]);
-#pragma unroll
-              for (int k = 1; k < M; ++k) acc = __fma_rn(o.A[c][k], P[k][j], acc);
-              Q[c][j] = acc;
-            }
-          }
-          // S = (sigma + rho) I + (rho - rho^2/kdd) Q'Q + rho_eq 11'  ->  Cholesky L L'
-          const double kap = rho - rho * rho / kdd;
-#pragma unroll
-          for (int r = 0; r < J; ++r)
-#pragma unroll
-            for (int s = 0; s <= r; ++s) {
-              double qq = 0.0;
-#pragma unroll
-              for (int c = 0; c < C; ++c) qq = __fma_rn(Q[c][r], Q[c][s], qq);
-              L[r][s] = kap * qq + req + (r == s ? qp.sigma + rho : 0.0);
-            }
-#pragma unroll
-          for (int r = 0; r < J; ++r) {
-#pragma unroll
-            for (int s = 0; s < r; ++s) {
-              double t = L[r][s];
-#pragma unroll
-              for (int k = 0; k < s; ++k) t -= L[r][k] * L[s][k];
-              L[r][s] = t / L[s][s];
-            }
-            double d = L[r][r];
-#pragma unroll
-            for (int k = 0; k < r; ++k) d -= L[r][k] * L[r][k];
-            L[r][r] = sqrt(d);
-          }
-#pragma unroll
-          for (int j = 0; j < J; ++j) lam[j] = 0.0;
-#pragma unroll
-          for (int c = 0; c < C; ++c) del[c] = 0.0;
-#pragma unroll
-          for (int i = 0; i < MC; ++i) { z[i] = 0.0; y[i] = 0.0; }
-          it = 0;
-        }
-      }
-    }
-    if (__all_sync(0xffffffffu, inst == -2)) break;
-    if (inst < 0) continue;
+#include "k_qp.cuh"
 
-    // ---- one ADMM iteration (qpsolver.py:164-174)
-    ++it;
-    double w[MC];
-#pragma unroll
-    for (int i = 0; i < MC; ++i) w[i] = (i < MC - 1 ? rho : req) * z[i] - y[i];  // R z - y
-    double rl[J], rd_[C];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      double acc = qp.sigma * lam[j] + w[C + j] + w[MC - 1];
-#pragma unroll
-      for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], w[c], acc);
-      rl[j] = acc;
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c) rd_[c] = qp.sigma * del[c] - w[c];
-    // S a = rl + rho Q' rd / kdd
-    double a[J];
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], rd_[c], acc);
-      a[j] = rl[j] + rho * acc / kdd;
-    }
-#pragma unroll
-    for (int r = 0; r < J; ++r) {  // forward L
-      double t = a[r];
-#pragma unroll
-      for (int k = 0; k < r; ++k) t -= L[r][k] * a[k];
-      a[r] = t / L[r][r];
-    }
-#pragma unroll
-    for (int r = J - 1; r >= 0; --r) {  // backward L'
-      double t = a[r];
-#pragma unroll
-      for (int k = r + 1; k < J; ++k) t -= L[k][r] * a[k];
-      a[r] = t / L[r][r];
-    }
-    double dd[C], zt[MC];
-    double sa = 0.0;
-#pragma unroll
-    for (int j = 0; j < J; ++j) sa += a[j];
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      double qa = 0.0;
-#pragma unroll
-      for (int j = 0; j < J; ++j) qa = __fma_rn(Q[c][j], a[j], qa);
-      dd[c] = (rd_[c] + rho * qa) / kdd;
-      zt[c] = qa - dd[c];
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) zt[C + j] = a[j];
-    zt[MC - 1] = sa;
-
-    double ln[J], dn[C], zn[MC], yn[MC], zr[MC];
-#pragma unroll
-    for (int j = 0; j < J; ++j) ln[j] = __dadd_rn(__dmul_rn(qp.alpha, a[j]), __dmul_rn(qp.one_m_alpha, lam[j]));
-#pragma unroll
-    for (int c = 0; c < C; ++c) dn[c] = __dadd_rn(__dmul_rn(qp.alpha, dd[c]), __dmul_rn(qp.one_m_alpha, del[c]));
-#pragma unroll
-    for (int i = 0; i < MC; ++i) {
-      zr[i] = __dadd_rn(__dmul_rn(qp.alpha, zt[i]), __dmul_rn(qp.one_m_alpha, z[i]));
-      const double rinv = i < MC - 1 ? ri : rieq;
-      double t = __dadd_rn(zr[i], __dmul_rn(rinv, y[i]));
-      // clip to [l, u]
-      if (i < C) t = fmin(t, b[i]);
-      else if (i < C + J) t = fmax(t, 0.0);
-      else t = 1.0;
-      zn[i] = t;
-      yn[i] = __dadd_rn(y[i], __dmul_rn(i < MC - 1 ? rho : req, __dsub_rn(zr[i], zn[i])));
-    }
-    // residuals (qpsolver.py:176-186)
-    double Ax[MC];
-    double sl = 0.0;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < J; ++j) acc = __dadd_rn(acc, __dmul_rn(Q[c][j], ln[j]));
-      Ax[c] = __dsub_rn(acc, dn[c]);
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) { Ax[C + j] = ln[j]; sl = __dadd_rn(sl, ln[j]); }
-    Ax[MC - 1] = sl;
-    double rp = 0.0, maxAx = 0.0, maxz = 0.0;
-#pragma unroll
-    for (int i = 0; i < MC; ++i) {
-      rp = fmax(rp, fabs(__dsub_rn(Ax[i], zn[i])));
-      maxAx = fmax(maxAx, fabs(Ax[i]));
-      maxz = fmax(maxz, fabs(zn[i]));
-    }
-    double rdl = 0.0, maxPx = 0.0, maxATy = 0.0;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      double acc = 0.0;
-#pragma unroll
-      for (int c = 0; c < C; ++c) acc = __dadd_rn(acc, __dmul_rn(Q[c][j], yn[c]));
-      acc = __dadd_rn(__dadd_rn(acc, yn[C + j]), yn[MC - 1]);
-      rdl = fmax(rdl, fabs(acc));
-      maxATy = fmax(maxATy, fabs(acc));
-    }
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const double px = __dmul_rn(2.0, dn[c]);
-      maxPx = fmax(maxPx, fabs(px));
-      maxATy = fmax(maxATy, fabs(yn[c]));
-      rdl = fmax(rdl, fabs(__dsub_rn(px, yn[c])));
-    }
-    const double eps_p = qp.eps_abs + qp.eps_rel * fmax(maxAx, maxz);
-    const double eps_d = qp.eps_abs + qp.eps_rel * fmax(maxPx, maxATy);
-    int status = -1;
-    if (rp <= eps_p && rdl <= eps_d) {
-      status = BZG_SOLVED;
-    } else {
-      // primal infeasibility certificate (qpsolver.py:193-209)
-      double dyn = 0.0;
-#pragma unroll
-      for (int i = 0; i < MC; ++i) dyn = fmax(dyn, fabs(__dsub_rn(yn[i], y[i])));
-      if (dyn > 1e-13) {
-        double atd = 0.0, supp = 0.0;
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          double acc = 0.0;
-#pragma unroll
-          for (int c = 0; c < C; ++c) acc = __dadd_rn(acc, __dmul_rn(Q[c][j], __dsub_rn(yn[c], y[c])));
-          acc = __dadd_rn(__dadd_rn(acc, __dsub_rn(yn[C + j], y[C + j])), __dsub_rn(yn[MC - 1], y[MC - 1]));
-          atd = fmax(atd, fabs(acc));
-        }
-#pragma unroll
-        for (int c = 0; c < C; ++c) atd = fmax(atd, fabs(__dsub_rn(yn[c], y[c])));
-#pragma unroll
-        for (int i = 0; i < MC; ++i) {
-          const double dy = __dsub_rn(yn[i], y[i]);
-          const double lo = i < C ? -INFINITY : (i < C + J ? 0.0 : 1.0);
-          const double hi = i < C ? b[i] : (i < C + J ? INFINITY : 1.0);
-          const double t = (dy > 0 ? __dmul_rn(hi, dy) : 0.0) + (dy < 0 ? __dmul_rn(lo, dy) : 0.0);
-          supp = __dadd_rn(supp, t);
-        }
-        if (atd <= qp.eps_pinf * dyn && supp <= -qp.eps_pinf * dyn) status = BZG_INFEASIBLE;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) lam[j] = ln[j];
-#pragma unroll
-    for (int c = 0; c < C; ++c) del[c] = dn[c];
-#pragma unroll
-    for (int i = 0; i < MC; ++i) { z[i] = zn[i]; y[i] = yn[i]; }
-    if (status < 0 && it >= qp.max_iter) status = BZG_MAX_ITER;
-    if (status >= 0) {
-      st_out[inst] = (int8_t)status;
-      it_out[inst] = it;
-#pragma unroll
-      for (int j = 0; j < J; ++j) x_out[inst * NV + j] = lam[j];
-#pragma unroll
-      for (int c = 0; c < C; ++c) x_out[inst * NV + J + c] = del[c];
-      res_out[inst * 2 + 0] = rp;
-      res_out[inst * 2 + 1] = rdl;
-      inst = -1;
-    }
-  }
-}
-
-// ------------------------------------------------------------------ polish
-// Active-set polish (qpsolver.py:236-279), one warp per instance: builds the regularised
-// reduced KKT system in shared memory, LU with partial pivoting (lane = row), solve plus two
-// steps of iterative refinement, and the acceptance test.  Then ||delta|| and the verdict
-// safe = SOLVED and ||delta|| > eps_cut (graph.py:328-329).
-constexpr int kPolishWarps = 4;
-
-template <int G, int M>
-__global__ void __launch_bounds__(32 * kPolishWarps) k_qp_polish(
-    DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
-    const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, long long n_inst, int polish,
-    double eps_cut, const int8_t* __restrict__ st, double* __restrict__ x_io, const double* __restrict__ res,
-    double* __restrict__ delta_out, uint8_t* __restrict__ safe_out) {
-  constexpr int J = 2 * G, C = 2 * M, N = G * M, NV = J + C, MC = C + J + 1, NK = NV + MC;
-  static_assert(NK <= 32, "polish system must fit a warp");
-  __shared__ double sA[kPolishWarps][MC][NV];
-  __shared__ double sK[kPolishWarps][NK][NK + 1];
-  __shared__ double sU[kPolishWarps][NK][NK + 1];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const long long inst = (long long)blockIdx.x * kPolishWarps + wib;
-  if (inst >= n_inst) return;
-  const int status = st[inst];
-  double x[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) x[i] = x_io[inst * NV + i];
-  const double rp = res[inst * 2], rd = res[inst * 2 + 1];
-  double (&A)[MC][NV] = sA[wib];
-  double lo_[MC], hi_[MC];
-  const unsigned long long pk = pend[inst];
-  const long long e = (long long)(pk >> 20);
-  const ObsRec<M>& o = obs[(int)(pk & 0xFFFFF)];
-  bool do_polish = polish && (status == BZG_SOLVED || status == BZG_MAX_ITER);
-  if (do_polish) {
-    // rebuild the constraint matrix (graph.py:275-281)
-    double xi[N], xj[N], P[M][J];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      xi[k] = Vx[(long long)src[e] * N + k];
-      xj[k] = Vx[(long long)dst[e] * N + k];
-    }
-    control_points<G, M>(xi, xj, dp.D, P);
-    for (int t = lane; t < MC * NV; t += 32) {
-      const int r = t / NV, k = t % NV;
-      double v = 0.0;
-      if (r < C) {
-        if (k < J) {
-          double acc = __dmul_rn(o.A[r][0], P[0][k]);
-          for (int q = 1; q < M; ++q) acc = __fma_rn(o.A[r][q], P[q][k], acc);
-          v = acc;
-        } else {
-          v = (k - J == r) ? -1.0 : 0.0;
-        }
-      } else if (r < C + J) {
-        v = (k == r - C) ? 1.0 : 0.0;
-      } else {
-        v = k < J ? 1.0 : 0.0;
-      }
-      A[r][k] = v;
-    }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < MC; ++i) {
-      lo_[i] = i < C ? -INFINITY : (i < C + J ? 0.0 : 1.0);
-      hi_[i] = i < C ? o.b[i] : (i < C + J ? INFINITY : 1.0);
-    }
-    // active set at z = A x
-    const double tol = fmax(1e-7, 10.0 * rp);
-    unsigned act = 0, atlo = 0;
-    int k = 0;
-#pragma unroll
-    for (int i = 0; i < MC; ++i) {
-      double zi = 0.0;
-#pragma unroll
-      for (int q = 0; q < NV; ++q) zi = __fma_rn(A[i][q], x[q], zi);
-      const bool l_ = __dsub_rn(zi, lo_[i]) <= tol, u_ = __dsub_rn(hi_[i], zi) <= tol;
-      if (l_ || u_) { act |= 1u << i; if (l_) atlo |= 1u << i; ++k; }
-    }
-    if (k > 0) {
-      const int nk = NV + k;
-      const double reg = 1e-8;
-      double (&K)[NK][NK + 1] = sK[wib];
-      double (&U)[NK][NK + 1] = sU[wib];
-      int rowmap[MC];
-      {
-        int a = 0;
-#pragma unroll
-        for (int i = 0; i < MC; ++i) if (act >> i & 1u) rowmap[a++] = i;
-      }
-      double rhs_r = 0.0;  // this lane's rhs entry
-      if (lane < nk) {
-        for (int cidx = 0; cidx < nk; ++cidx) {
-          double v;
-          if (lane < NV) {
-            if (cidx < NV) v = (lane == cidx) ? ((lane >= J ? 2.0 : 0.0) + reg) : 0.0;
-            else v = A[rowmap[cidx - NV]][lane];
-          } else {
-            const int r = rowmap[lane - NV];
-            v = cidx < NV ? A[r][cidx] : ((cidx == lane) ? -reg : 0.0);
-          }
-          K[lane][cidx] = v;
-          U[lane][cidx] = v;
-        }
-        if (lane >= NV) {
-          const int r = rowmap[lane - NV];
-          rhs_r = (atlo >> r & 1u) ? lo_[r] : hi_[r];
-        }
-      }
-      __syncwarp();
-      // LU with partial pivoting; perm[r] tracked per lane as the original row now in slot r
-      int perm = lane;
-      bool singular = false;
-      for (int cc = 0; cc < nk; ++cc) {
-        double val = (lane >= cc && lane < nk) ? fabs(U[lane][cc]) : -1.0;
-        int idx = lane;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, val, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
-          if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
-        }
-        const int piv = idx;
-        if (val == 0.0) singular = true;
-        if (piv != cc) {
-          for (int t = lane; t < nk; t += 32) {
-            const double tmp = U[cc][t];
-            U[cc][t] = U[piv][t];
-            U[piv][t] = tmp;
-          }
-          const int pc = __shfl_sync(0xffffffffu, perm, cc), pp = __shfl_sync(0xffffffffu, perm, piv);
-          if (lane == cc) perm = pp;
-          if (lane == piv) perm = pc;
-        }
-        __syncwarp();
-        if (lane > cc && lane < nk && !singular) {
-          const double l = U[lane][cc] / U[cc][cc];
-          U[lane][cc] = l;
-          for (int t = cc + 1; t < nk; ++t) U[lane][t] = __fma_rn(-l, U[cc][t], U[lane][t]);
-        }
-        __syncwarp();
-      }
-      if (!singular) {
-        // solve K w = rhs with the factors; then two refinement steps on the residual
-        auto lu_solve = [&](double bvec) -> double {
-          // bvec: this lane's entry of the right-hand side (original row order)
-          double yv = __shfl_sync(0xffffffffu, bvec, perm);  // apply the row permutation
-          for (int cc = 0; cc < nk; ++cc) {
-            const double yc = __shfl_sync(0xffffffffu, yv, cc);
-            if (lane > cc && lane < nk) yv = __fma_rn(-U[lane][cc], yc, yv);
-          }
-          for (int cc = nk - 1; cc >= 0; --cc) {
-            double wc = 0.0;
-            if (lane == cc) yv = yv / U[cc][cc];
-            wc = __shfl_sync(0xffffffffu, yv, cc);
-            if (lane < cc) yv = __fma_rn(-U[lane][cc], wc, yv);
-          }
-          return yv;
-        };
-        double wv = lu_solve(rhs_r);
-        for (int rep = 0; rep < 2; ++rep) {
-          double kw = 0.0;
-          for (int t = 0; t < nk; ++t) {
-            const double wt = __shfl_sync(0xffffffffu, wv, t);
-            if (lane < nk) kw = __fma_rn(K[lane][t], wt, kw);
-          }
-          const double r = lane < nk ? __dsub_rn(rhs_r, kw) : 0.0;
-          const double dw = lu_solve(r);
-          wv = __dadd_rn(wv, dw);
-        }
-        // candidate x_pol, y_pol and acceptance (qpsolver.py:271-279)
-        double xp[NV], yp[MC];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) xp[i] = __shfl_sync(0xffffffffu, wv, i);
-#pragma unroll
-        for (int i = 0; i < MC; ++i) yp[i] = 0.0;
-        for (int a = 0; a < k; ++a) {
-          const double ya = __shfl_sync(0xffffffffu, wv, NV + a);
-#pragma unroll
-          for (int i = 0; i < MC; ++i) if (rowmap[a] == i) yp[i] = ya;
-        }
-        double up_v = 0.0, lo_v = 0.0;
-#pragma unroll
-        for (int i = 0; i < MC; ++i) {
-          double zi = 0.0;
-#pragma unroll
-          for (int q = 0; q < NV; ++q) zi = __fma_rn(A[i][q], xp[q], zi);
-          up_v = fmax(up_v, fmax(__dsub_rn(zi, hi_[i]), 0.0));
-          lo_v = fmax(lo_v, fmax(__dsub_rn(lo_[i], zi), 0.0));
-        }
-        const double rpp = __dadd_rn(up_v, lo_v);
-        double rdp = 0.0;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-          double acc = q >= J ? __dmul_rn(2.0, xp[q]) : 0.0;
-#pragma unroll
-          for (int i = 0; i < MC; ++i) acc = __fma_rn(A[i][q], yp[i], acc);
-          rdp = fmax(rdp, fabs(acc));
-        }
-        if (fmax(rpp, rdp) < fmax(rp, rd)) {
-#pragma unroll
-          for (int i = 0; i < NV; ++i) x[i] = xp[i];
-        }
-      }
-    }
-  }
-  if (lane == 0) {
-    double s = 0.0;
-#pragma unroll
-    for (int c = 0; c < C; ++c) s = __fma_rn(x[J + c], x[J + c], s);
-    const double dl = sqrt(s);
-    delta_out[inst] = dl;
-    safe_out[inst] = (uint8_t)(status == BZG_SOLVED && dl > eps_cut);
-#pragma unroll
-    for (int i = 0; i < NV; ++i) x_io[inst * NV + i] = x[i];
-  }
-}
+namespace bzg {
+namespace {
 
 // ------------------------------------------------------------------ aggregation
 __global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long long n_inst,
@@ -721,6 +309,13 @@ __global__ void k_unpack_pend(const unsigned long long* __restrict__ pend, long 
 __global__ void k_fill_int(int* p, long long n, int v) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t < n) p[t] = v;
+}
+
+// ||delta|| above which the ADMM verdict is final (see k_qp_select); BZG_POLISH_SCREEN=0
+// polishes every SOLVED instance exactly like the reference.
+double polish_screen() {
+  const char* s = std::getenv("BZG_POLISH_SCREEN");
+  return s ? std::atof(s) : 1e-2;
 }
 
 template <typename F>
@@ -777,6 +372,10 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
         r.lo[k] = box_lo[(size_t)o * Mc + k];
         r.hi[k] = box_hi[(size_t)o * Mc + k];
       }
+      bool canon = true;
+      for (int q = 0; q < 2 * Mc; ++q)
+        for (int k = 0; k < Mc; ++k) canon = canon && r.A[q][k] == (k == (q % Mc) ? (q < Mc ? 1.0 : -1.0) : 0.0);
+      r.canon = canon ? 1.0 : 0.0;
     }
     DevBuf d_obs, d_kill, d_qkill, d_saved, d_cnt;
     d_obs.alloc(sizeof(Rec) * h.size(), c->stream);
@@ -849,11 +448,21 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
              g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
              d_pend.as<unsigned long long>(), n_inst, d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(),
              mk->qp_iters.as<int>(), d_x.as<double>(), d_res.as<double>());
-      launch(c, "k_qp_polish", k_qp_polish<Gc, Mc>, dim3(div_up(n_inst, kPolishWarps)), dim3(32 * kPolishWarps), 0,
+      DevBuf d_list;
+      d_list.alloc(n_inst * sizeof(int), c->stream);
+      BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
+      launch(c, "k_qp_select", k_qp_select, dim3(div_up(n_inst, 256)), dim3(256), 0, n_inst, NV, 2 * Gc,
+             (int)cfg->qp_polish, polish_screen(), cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(),
+             mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
+      BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt + 6, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                     c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      const long long n_list = (long long)hcnt[6];
+      mk->n_polished = n_list;
+      launch(c, "k_qp_polish", k_qp_polish<Gc, Mc>, dim3(div_up(n_list, kPolishWarps)), dim3(32 * kPolishWarps), 0,
              dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
-             d_pend.as<unsigned long long>(), n_inst, (int)cfg->qp_polish, cfg->eps_cut,
-             mk->qp_status.as<int8_t>(), d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(),
-             d_safe.as<uint8_t>());
+             d_pend.as<unsigned long long>(), d_list.as<int>(), n_list, cfg->eps_cut, d_x.as<double>(),
+             d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>());
       launch(c, "k_qp_verdicts", k_qp_verdicts, dim3(div_up(n_inst, 256)), dim3(256), 0,
              d_pend.as<unsigned long long>(), n_inst, d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(),
              d_cnt.as<unsigned long long>());

@@ -200,3 +200,18 @@ def test_edge_cases(ctx, golden):
     cat = np.concatenate([p.edges for p in parts])
     assert np.array_equal(cat, ref["edges"])
     assert np.concatenate([p.costs for p in parts]).tobytes() == ref["costs"].tobytes()
+
+
+@pytest.mark.parametrize("name", ["hop1500", "rf300_s5", "cfg2_rf2000"])
+def test_polish_screen_keeps_verdicts(ctx, golden, name, monkeypatch):
+    """The ADMM-norm screen on the polish never changes a cut outcome."""
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+    monkeypatch.setenv("BZG_POLISH_SCREEN", "0")
+    full = G.cut_graph(gr, obstacles)
+    monkeypatch.delenv("BZG_POLISH_SCREEN")
+    fast = G.cut_graph(gr, obstacles)
+    assert np.array_equal(full.alive, fast.alive)
+    assert np.array_equal(full.provenance_codes, fast.provenance_codes)
+    assert (full.qp_safe, full.qp_unsafe) == (fast.qp_safe, fast.qp_unsafe)
+    assert np.array_equal(full.alive, g["alive"])

@@ -58,7 +58,7 @@ def test_recover_box():
 
 def _header_symbols():
     text = (ROOT / "include" / "bzg.h").read_text()
-    return sorted(set(re.findall(r"\b(bzg_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(bzg_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_header_symbol():
