@@ -83,7 +83,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
 
@@ -145,6 +145,7 @@ class DeviceStep:
         cnt = np.zeros(6, dtype=np.int64)
         nat.check(lib.bzg_mask_copy(mh, None, None, nat.ptr(cnt)))
         mask = G.CutMask(mh, graph, cnt)
+        self.local_mask = mask
         if self.world > 1:
             from paper_2411_13507_b200 import shard
 
@@ -198,7 +199,35 @@ def algorithmic_work(kernel, w, step_info, world):
         J = 2 * g
         per = J * 2 * m * (2 * m) + J * (3 * m + 1) + 2 * m * 4 + J * (2 * m)  # SURVEY.md §8(d) box pair
         return E * O * per, "fp64"
+    if kernel == "k_qp_admm":
+        return step_info["qp_iterations"] * admm_ops_per_iteration(2 * g, 2 * m), "fp64"
     return None, None
+
+
+def admm_ops_per_iteration(J: int, C: int) -> int:
+    """FP64 operations of one reduced-form ADMM iteration: KKT step
+    (3C + 1 + J(3+C) + J^2), relaxation/projection/dual update (17J + C(J+17) + 7) and the
+    termination test (J + 2 + C(J+3) + J(C+2) + 3C).  384 for J=6, C=4 (gamma=3, m=2)."""
+    return (3 * C + 1 + J * (3 + C) + J * J) + (17 * J + C * (J + 17) + 7) + (J + 2 + C * (J + 3) + J * (C + 2) + 3 * C)
+
+
+_BYTE_UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch of `kernel` from the newest committed `ncu --set full`
+    summary (profiles/r*_ncu_full_<kernel>.json, tools/summarize_ncu.py), else None."""
+    files = sorted((ROOT / "profiles").glob(f"r*_ncu_full_{kernel}.json"))
+    if not files:
+        return None, None
+    rec = json.loads(files[-1].read_text())["kernels"][0]
+    tot = 0.0
+    for key in ("dram_read_bytes", "dram_write_bytes"):
+        v = rec.get(key)
+        if not isinstance(v, dict):
+            return None, None
+        tot += float(v["value"]) * _BYTE_UNITS.get(v["unit"], 1.0)
+    return tot, files[-1].name
 
 
 def main():
@@ -283,6 +312,10 @@ def main():
     h2d, d2h = h2d_d2h_bytes(w, len(path or []))
 
     # ---------------- roofline of the dominant kernel
+    if step.local_mask is not None and step.local_mask.pairs_qp:
+        step.last["qp_iterations"] = int(step.local_mask.qp_records()["iterations"].astype(np.int64).sum())
+    else:
+        step.last["qp_iterations"] = 0
     per_step = {k: (ms / args.steps, n / args.steps) for k, (ms, n) in kstats.items()}
     dom = max(per_step, key=lambda k: per_step[k][0])
     roof = {"kernel": dom}
@@ -291,9 +324,12 @@ def main():
     if work is not None and dom_n > 0:
         avg_launch_s = dom_ms / dom_n * 1e-3
         achieved = work / dom_n / avg_launch_s
+        traffic, tsrc = ncu_traffic(dom)
         roof.update(bound=bound, achieved=achieved / 1e9, peak=fp64_rate / 1e9, unit="Gop/s (FP64 instr)",
-                    frac=achieved / fp64_rate, traffic=None,
-                    peak_source="measured DFMA issue rate (bzg_probe_fp64, this run)")
+                    frac=achieved / fp64_rate, traffic=traffic, traffic_source=tsrc,
+                    algorithmic_ops_per_launch=work / dom_n, avg_launch_ms=dom_ms / dom_n,
+                    peak_source="measured DFMA issue rate (bzg_probe_fp64, this run); "
+                                "MEASURED_PEAKS.json has no FP64 figure")
     else:
         roof.update(bound=None, achieved=None, peak=None, frac=None, traffic=None)
     share = dom_ms / ms_per_step

@@ -113,21 +113,28 @@ def random_field(seed: int = 1, n_obstacles: int = 20, graph_n: int = 2000, side
                     np.array([start, goal]), _inflated(obs, tube, spec.m), start, goal)
 
 
-def hopping_deg5(graph_n: int = 20000, n_obstacles: int = 50, seed: int = 1, obstacle_seed: int = 11) -> Workload:
-    """cfg3: gamma=3 (degree-5 curves), 20k samples, 50 boxes."""
+def hopping_deg5(graph_n: int = 20000, n_obstacles: int = 50, seed: int = 1, obstacle_seed: int = 11,
+                 clear_endpoints: bool = True) -> Workload:
+    """cfg3: gamma=3 (degree-5 curves), 20k samples, 50 boxes.
+
+    With ``clear_endpoints`` obstacle centres within 0.9 of start/goal are redrawn, the
+    rule of the reference's random field (scenario.py:373-374), so a path exists.
+    """
     spec = BezierSpec(m=2, gamma=3, T=1.0)
     xd = Box(np.array([0.0, 0.0, -1.5, -1.5, -4.0, -4.0]), np.array([5.0, 5.0, 1.5, 1.5, 4.0, 4.0])).to_polytope()
     u = Box(np.array([-30.0, -30.0]), np.array([30.0, 30.0]))
     sample = Box(np.array([0.0, 0.0, -0.6, -0.6, -1.0, -1.0]), np.array([5.0, 5.0, 0.6, 0.6, 1.0, 1.0]))
     tube = design_tube(spec, (6.0, 11.0, 6.0), 0.02)
-    rng = np.random.default_rng(obstacle_seed)
-    obs = []
-    for _ in range(n_obstacles):
-        c = rng.uniform(0.4, 4.6, 2)
-        w = rng.uniform(0.25, 0.7, 2)
-        obs.append(box_obstacle(c[0], c[1], w[0], w[1]))
     start = np.array([0.4, 0.4, 0.0, 0.0, 0.0, 0.0])
     goal = np.array([4.6, 4.6, 0.0, 0.0, 0.0, 0.0])
+    rng = np.random.default_rng(obstacle_seed)
+    obs = []
+    while len(obs) < n_obstacles:
+        c = rng.uniform(0.4, 4.6, 2)
+        w = rng.uniform(0.25, 0.7, 2)
+        if clear_endpoints and (np.linalg.norm(c - start[:2]) < 0.9 or np.linalg.norm(c - goal[:2]) < 0.9):
+            continue
+        obs.append(box_obstacle(c[0], c[1], w[0], w[1]))
     oracle = build_oracle(spec, xd, u, tube)
     return Workload("cfg3-hop-deg5-20k", spec, oracle, sample, graph_n, seed, np.array([start, goal]),
                     _inflated(obs, tube, spec.m), start, goal)

@@ -254,7 +254,9 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
 }  // namespace
 }  // namespace bzg
 
-#include "k_qp.cuh"
+#include "k_qp_common.cuh"
+#include "k_admm.cuh"
+#include "k_polish.cuh"
 
 namespace bzg {
 namespace {

@@ -1,0 +1,54 @@
+// Batched Cut-QP on device: dense ADMM (one thread per instance) and active-set polish
+// (one warp per instance).  Included by k_cut.cu.
+//
+// Problem (reference graph.py:268-282, _cut_qp_problem), per (edge, obstacle):
+//   x = [lambda (J); delta (C)],  min delta' delta
+//   s.t.  Q lambda - delta <= b  (C rows, Q = A_O P),  lambda >= 0 (J rows),  sum lambda = 1
+// solved by the dense ADMM of qpsolver.py:129-233 and polished by qpsolver.py:236-279.
+#pragma once
+
+namespace bzg {
+namespace {
+
+struct QpParams {
+  double rho, rho_eq, sigma, alpha, one_m_alpha, eps_abs, eps_rel, eps_pinf;
+  int max_iter;
+};
+
+// Q = A_O @ points (graph.py:276): BLAS product, FMA chain over the m output dimensions.
+template <int G, int M>
+__device__ __forceinline__ void cut_q_matrix(const ObsRec<M>& o, const double (&P)[M][2 * G], double (&Q)[2 * M][2 * G]) {
+#pragma unroll
+  for (int c = 0; c < 2 * M; ++c)
+#pragma unroll
+    for (int j = 0; j < 2 * G; ++j) {
+      double acc = __dmul_rn(o.A[c][0], P[0][j]);
+#pragma unroll
+      for (int k = 1; k < M; ++k) acc = __fma_rn(o.A[c][k], P[k][j], acc);
+      Q[c][j] = acc;
+    }
+}
+
+template <int G, int M>
+__device__ __forceinline__ void load_instance(const DParams& dp, const double* __restrict__ Vx,
+                                              const int* __restrict__ src, const int* __restrict__ dst,
+                                              const ObsRec<M>* __restrict__ obs, unsigned long long pk,
+                                              double (&Q)[2 * M][2 * G], double (&b)[2 * M]) {
+  constexpr int N = G * M;
+  const long long e = (long long)(pk >> 20);
+  const ObsRec<M>& o = obs[(int)(pk & 0xFFFFF)];
+  double xi[N], xj[N], P[M][2 * G];
+  const long long a = src[e], c = dst[e];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    xi[k] = Vx[a * N + k];
+    xj[k] = Vx[c * N + k];
+  }
+  control_points<G, M>(xi, xj, dp.D, P);
+  cut_q_matrix<G, M>(o, P, Q);
+#pragma unroll
+  for (int k = 0; k < 2 * M; ++k) b[k] = o.b[k];
+}
+
+}  // namespace
+}  // namespace bzg

@@ -1,0 +1,50 @@
+"""Wire the device stage into the reference package ``beziergraph``.
+
+The reference simulator imports its graph module as ``graphmod`` and calls
+``graphmod.build_graph`` / ``graphmod.cut_graph`` / ``graphmod.find_path``
+(sim.py:20, 202-209, 255-257, 324-335), so replacing those module attributes is
+enough for ``plan_once`` and ``run_closed_loop`` to run on the GPU stage::
+
+    import beziergraph
+    from paper_2411_13507_b200 import shim
+    shim.install(beziergraph)          # beziergraph.graph.* now run on the B200
+    beziergraph.plan_once(beziergraph.demo_scenario())
+    shim.uninstall(beziergraph)
+
+The reference's own ``CutProvenance`` enum is used for ``CutMask.provenance`` while
+installed, so masks compare equal to the reference's.
+"""
+
+from __future__ import annotations
+
+from . import graph as _dev
+
+_PATCHED = ("build_graph", "cut_graph", "find_path", "path_cost")
+_saved: dict = {}
+
+
+def install(beziergraph_pkg) -> None:
+    """Patch ``beziergraph.graph`` (and the package re-exports) with the device functions."""
+    gmod = beziergraph_pkg.graph
+    if _saved:
+        return
+    for name in _PATCHED:
+        _saved[("graph", name)] = getattr(gmod, name)
+        setattr(gmod, name, getattr(_dev, name))
+        if hasattr(beziergraph_pkg, name):
+            _saved[("pkg", name)] = getattr(beziergraph_pkg, name)
+            setattr(beziergraph_pkg, name, getattr(_dev, name))
+    _saved[("prov",)] = _dev._PROV_ENUM
+    _dev._PROV_ENUM = gmod.CutProvenance
+
+
+def uninstall(beziergraph_pkg) -> None:
+    gmod = beziergraph_pkg.graph
+    for key, fn in list(_saved.items()):
+        if key[0] == "graph":
+            setattr(gmod, key[1], fn)
+        elif key[0] == "pkg":
+            setattr(beziergraph_pkg, key[1], fn)
+        elif key[0] == "prov":
+            _dev._PROV_ENUM = fn
+    _saved.clear()

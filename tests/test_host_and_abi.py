@@ -36,7 +36,7 @@ def test_cfg2_and_hop_constants(golden):
     assert np.vstack([o.A for o in w.obstacles]).tobytes() == g["obs_A"].tobytes()
     assert np.concatenate([o.b for o in w.obstacles]).tobytes() == g["obs_b"].tobytes()
     h = golden("hop1500")
-    wh = configs.hopping_deg5(graph_n=1500, n_obstacles=12)
+    wh = configs.hopping_deg5(graph_n=1500, n_obstacles=12, clear_endpoints=False)
     assert wh.oracle.F.tobytes() == h["F"].tobytes() and wh.oracle.G.tobytes() == h["G"].tobytes()
     assert np.vstack([o.A for o in wh.obstacles]).tobytes() == h["obs_A"].tobytes()
     assert np.concatenate([o.b for o in wh.obstacles]).tobytes() == h["obs_b"].tobytes()
