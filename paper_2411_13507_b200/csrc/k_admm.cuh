@@ -13,8 +13,10 @@
 // reference by rounding.
 //
 // Scheduling: persistent lanes.  Each lane owns one instance; between batches of
-// kBatch iterations, lanes whose instance terminated fetch the next one with one
+// kAdmmBatch iterations, lanes whose instance terminated fetch the next one with one
 // warp-aggregated atomic, so the 500-iteration MAX_ITER instances do not idle the warp.
+// The hot loop only decides termination (compare-only tests); the residual maxima the
+// polish needs are recomputed from the stored (x, z, y) by k_qp_select.
 #pragma once
 
 namespace bzg {
@@ -75,26 +77,75 @@ __device__ __forceinline__ void admm_setup(double (&Q)[2 * M][2 * G], double (&S
     }
 }
 
-template <int G, int M>
-__global__ void __launch_bounds__(128) k_qp_admm(QpParams qp, DParams dp, const double* __restrict__ Vx,
+// !(v > 0) and !(v < 0) from the bit pattern (integer pipe; the FP64 pipe is the bound)
+__device__ __forceinline__ bool not_pos(double v) {
+  const long long b = __double_as_longlong(v);
+  return (b < 0) | (b == 0);
+}
+__device__ __forceinline__ bool not_neg(double v) {
+  const long long b = __double_as_longlong(v);
+  return (b >= 0) | (b == (long long)0x8000000000000000ull);
+}
+// max(t, 0): clip to [0, +inf) (the sign of a zero result is immaterial downstream)
+__device__ __forceinline__ double clip_nonneg(double t) { return __double_as_longlong(t) < 0 ? 0.0 : t; }
+
+// Constraint-matrix products of the cut QP.  Q = A_O P (C x J).  For a canonical box
+// (A_O = [I; -I], Box.to_polytope order) Q = [P; -P] exactly, so only the M rows of P are
+// kept and every product is formed once per output dimension.
+template <int G, int M, bool CANON>
+struct QOps {
+  static constexpr int J = 2 * G, C = 2 * M, R = CANON ? M : C;
+  double q[R][J];
+  __device__ __forceinline__ void load(const double (&Q)[C][J]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int j = 0; j < J; ++j) q[r][j] = Q[r][j];
+  }
+  // out_c = Q_c . v   (FMA chain over j)
+  __device__ __forceinline__ void mul(const double (&v)[J], double (&out)[C]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc = __fma_rn(q[r][j], v[j], acc);
+      out[r] = acc;
+      if (CANON) out[r + M] = -acc;
+    }
+  }
+  // returns acc + sum_c Q_cj w_c
+  __device__ __forceinline__ double tmul(int j, const double (&w)[C], double acc) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc = __fma_rn(q[r][j], CANON ? __dsub_rn(w[r], w[r + M]) : w[r], acc);
+    return acc;
+  }
+};
+
+// REL: eps_rel != 0 (termination tolerances depend on the iterate, qpsolver.py:181-186)
+// UNIT: rho == 1 (CutConfig default) -- the multiplications by rho and 1/rho are exact and skipped
+// CANON: every obstacle is a canonical box (see QOps)
+template <int G, int M, bool REL, bool UNIT, bool CANON>
+__global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, const double* __restrict__ Vx,
                                                  const int* __restrict__ src, const int* __restrict__ dst,
                                                  const ObsRec<M>* __restrict__ obs,
                                                  const unsigned long long* __restrict__ pend, long long n_inst,
                                                  unsigned long long* __restrict__ next, int8_t* __restrict__ st_out,
                                                  int* __restrict__ it_out, double* __restrict__ x_out,
-                                                 double* __restrict__ res_out) {
-  constexpr int J = 2 * G, C = 2 * M, NV = J + C;
+                                                 double* __restrict__ zy_out) {
+  constexpr int J = 2 * G, C = 2 * M, NV = J + C, MC = C + J + 1;
   const int lane = threadIdx.x & 31;
-  const double rho = qp.rho, req = qp.rho_eq, ri = 1.0 / qp.rho;
-  const double sig = qp.sigma, al = qp.alpha, oma = qp.one_m_alpha;
+  const double rho = UNIT ? 1.0 : qp.rho, req = qp.rho_eq, ri = UNIT ? 1.0 : 1.0 / qp.rho;
+  const double sig = qp.sigma, al = qp.alpha, oma = qp.one_m_alpha, eps = qp.eps_abs;
   const double kdd = 2.0 + sig + rho, ikdd = 1.0 / kdd, kp = rho * ikdd;
-  const bool rel = qp.eps_rel != 0.0;
 
   long long inst = -1;  // -1 needs work, -2 exhausted
   int it = 0;
-  double Q[C][J], Si[J * (J + 1) / 2], b[C];
+  QOps<G, M, CANON> Q;
+  double Si[J * (J + 1) / 2], b[C];
   double lam[J], del[C], zc[C], zl[J], ze, yc[C], yl[J], ye;
 #define SI(r, s) Si[(r) >= (s) ? (r) * ((r) + 1) / 2 + (s) : (s) * ((s) + 1) / 2 + (r)]
+#define RHO_MUL(v) (UNIT ? (v) : __dmul_rn(rho, (v)))
+#define RI_MUL(v) (UNIT ? (v) : __dmul_rn(ri, (v)))
 
   while (true) {
     // ---- refill lanes whose instance terminated (one atomic per warp)
@@ -108,8 +159,10 @@ __global__ void __launch_bounds__(128) k_qp_admm(QpParams qp, DParams dp, const 
         const unsigned long long my = base + __popc(need & ((1u << lane) - 1u));
         inst = (long long)my < n_inst ? (long long)my : -2;
         if (inst >= 0) {
-          load_instance<G, M>(dp, Vx, src, dst, obs, pend[inst], Q, b);
-          admm_setup<G, M>(Q, Si, rho, req, sig, ikdd);
+          double Qf[C][J];
+          load_instance<G, M>(dp, Vx, src, dst, obs, pend[inst], Qf, b);
+          admm_setup<G, M>(Qf, Si, rho, req, sig, ikdd);
+          Q.load(Qf);
         }
 #pragma unroll
         for (int j = 0; j < J; ++j) { lam[j] = 0.0; zl[j] = 0.0; yl[j] = 0.0; }
@@ -130,18 +183,16 @@ __global__ void __launch_bounds__(128) k_qp_admm(QpParams qp, DParams dp, const 
       double rdel[C], tC[C];
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const double wc = __fma_rn(rho, zc[c], -yc[c]);  // (R z - y)_c
-        rdel[c] = __fma_rn(sig, del[c], -wc);          // sigma delta - w_c
+        const double wc = UNIT ? __dsub_rn(zc[c], yc[c]) : __fma_rn(rho, zc[c], -yc[c]);  // (R z - y)_c
+        rdel[c] = __fma_rn(sig, del[c], -wc);                                            // sigma delta - w_c
         tC[c] = __fma_rn(kp, rdel[c], wc);
       }
       const double we = __fma_rn(req, ze, -ye);
       double rv[J];
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        double acc = __fma_rn(sig, lam[j], __fma_rn(rho, zl[j], -yl[j]) + we);
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], tC[c], acc);
-        rv[j] = acc;
+        const double wl = UNIT ? __dsub_rn(zl[j], yl[j]) : __fma_rn(rho, zl[j], -yl[j]);
+        rv[j] = Q.tmul(j, tC, __fma_rn(sig, lam[j], __dadd_rn(wl, we)));
       }
       double a[J];
 #pragma unroll
@@ -153,33 +204,38 @@ __global__ void __launch_bounds__(128) k_qp_admm(QpParams qp, DParams dp, const 
       }
       // relaxation, projection onto [l, u] and dual update, row block by row block
       bool sign_ok = true;  // the certificate needs dy_c >= 0 and dy_lambda <= 0 (finite bounds)
-      bool pbad = false;    // some |(A x - z)_i| > eps_p
+      bool conv = true;     // every |(A x - z)_i| <= eps_p and |(P x + A'y)_j| <= eps_d
       double dyc[C], dyl[J];
       double sa = 0.0;
+      double maxAx = 0.0, maxz = 1.0, maxPx = 0.0, maxATy = 0.0, rprim = 0.0, rdual = 0.0;  // REL only
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         sa += a[j];
         const double zr = __dadd_rn(__dmul_rn(al, a[j]), __dmul_rn(oma, zl[j]));
-        const double zn = fmax(__dadd_rn(zr, __dmul_rn(ri, yl[j])), 0.0);
-        const double yn = __dadd_rn(yl[j], __dmul_rn(rho, __dsub_rn(zr, zn)));
+        const double zn = clip_nonneg(__dadd_rn(zr, RI_MUL(yl[j])));
+        const double yn = __dadd_rn(yl[j], RHO_MUL(__dsub_rn(zr, zn)));
         dyl[j] = __dsub_rn(yn, yl[j]);
-        sign_ok = sign_ok && !(dyl[j] > 0.0);
+        sign_ok &= not_pos(dyl[j]);
         lam[j] = __dadd_rn(__dmul_rn(al, a[j]), __dmul_rn(oma, lam[j]));
         zl[j] = zn;
         yl[j] = yn;
-        pbad = pbad || !(fabs(__dsub_rn(lam[j], zn)) <= qp.eps_abs);
+        const double r = __dsub_rn(lam[j], zn);
+        if (REL) {
+          rprim = fmax(rprim, fabs(r)); maxAx = fmax(maxAx, fabs(lam[j])); maxz = fmax(maxz, fabs(zn));
+        } else {
+          conv &= fabs(r) <= eps;
+        }
       }
+      double qa[C];
+      Q.mul(a, qa);
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        double qa = 0.0;
-#pragma unroll
-        for (int j = 0; j < J; ++j) qa = __fma_rn(Q[c][j], a[j], qa);
-        const double d = __fma_rn(rdel[c], ikdd, kp * qa);
-        const double zr = __dadd_rn(__dmul_rn(al, __dsub_rn(qa, d)), __dmul_rn(oma, zc[c]));
-        const double zn = fmin(__dadd_rn(zr, __dmul_rn(ri, yc[c])), b[c]);
-        const double yn = __dadd_rn(yc[c], __dmul_rn(rho, __dsub_rn(zr, zn)));
+        const double d = __fma_rn(rdel[c], ikdd, kp * qa[c]);
+        const double zr = __dadd_rn(__dmul_rn(al, __dsub_rn(qa[c], d)), __dmul_rn(oma, zc[c]));
+        const double zn = fmin(__dadd_rn(zr, RI_MUL(yc[c])), b[c]);
+        const double yn = __dadd_rn(yc[c], RHO_MUL(__dsub_rn(zr, zn)));
         dyc[c] = __dsub_rn(yn, yc[c]);
-        sign_ok = sign_ok && !(dyc[c] < 0.0);
+        sign_ok &= not_neg(dyc[c]);
         del[c] = __dadd_rn(__dmul_rn(al, d), __dmul_rn(oma, del[c]));
         zc[c] = zn;
         yc[c] = yn;
@@ -196,104 +252,79 @@ __global__ void __launch_bounds__(128) k_qp_admm(QpParams qp, DParams dp, const 
       double sl = 0.0;
 #pragma unroll
       for (int j = 0; j < J; ++j) sl = __dadd_rn(sl, lam[j]);
-      pbad = pbad || !(fabs(__dsub_rn(sl, 1.0)) <= qp.eps_abs);
+      {
+        const double r = __dsub_rn(sl, 1.0);
+        if (REL) { rprim = fmax(rprim, fabs(r)); maxAx = fmax(maxAx, fabs(sl)); }
+        else conv &= fabs(r) <= eps;
+      }
+      double ql[C];
+      Q.mul(lam, ql);
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < J; ++j) acc = __fma_rn(Q[c][j], lam[j], acc);
-        pbad = pbad || !(fabs(__dsub_rn(__dsub_rn(acc, del[c]), zc[c])) <= qp.eps_abs);
+        const double ax = __dsub_rn(ql[c], del[c]);
+        const double r = __dsub_rn(ax, zc[c]);
+        if (REL) {
+          rprim = fmax(rprim, fabs(r)); maxAx = fmax(maxAx, fabs(ax)); maxz = fmax(maxz, fabs(zc[c]));
+        } else {
+          conv &= fabs(r) <= eps;
+        }
       }
-      bool dbad = false;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        double acc = __dadd_rn(yl[j], ye);
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], yc[c], acc);
-        dbad = dbad || !(fabs(acc) <= qp.eps_abs);
+        const double acc = Q.tmul(j, yc, __dadd_rn(yl[j], ye));
+        if (REL) { rdual = fmax(rdual, fabs(acc)); maxATy = fmax(maxATy, fabs(acc)); }
+        else conv &= fabs(acc) <= eps;
       }
 #pragma unroll
-      for (int c = 0; c < C; ++c) dbad = dbad || !(fabs(__dsub_rn(__dmul_rn(2.0, del[c]), yc[c])) <= qp.eps_abs);
+      for (int c = 0; c < C; ++c) {
+        const double px = __dmul_rn(2.0, del[c]);
+        const double r = __dsub_rn(px, yc[c]);
+        if (REL) {
+          rdual = fmax(rdual, fabs(r)); maxPx = fmax(maxPx, fabs(px)); maxATy = fmax(maxATy, fabs(yc[c]));
+        } else {
+          conv &= fabs(r) <= eps;
+        }
+      }
+      if (REL) conv = rprim <= eps + qp.eps_rel * fmax(maxAx, maxz) && rdual <= eps + qp.eps_rel * fmax(maxPx, maxATy);
 
-      int status = -1;
-      double rprim = 0.0, rdual = 0.0;
-      if (rel || !(pbad || dbad) || sign_ok || it >= qp.max_iter) {
-        // rare path: exact residual maxima (qpsolver.py:179-186) and the relative tolerances
-        double maxAx = 0.0, maxz = 1.0, maxPx = 0.0, maxATy = 0.0;
-        rprim = fabs(__dsub_rn(sl, 1.0));
-        maxAx = fabs(sl);
+      int status = conv ? BZG_SOLVED : -1;
+      if (!conv && sign_ok) {
+        // primal-infeasibility certificate (qpsolver.py:193-209): with every dy_i on a finite
+        // bound, support = sum_c b_c dy_c + dy_eq
+        double dmax = fabs(dye), atd = 0.0, supp = 0.0;
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          rprim = fmax(rprim, fabs(__dsub_rn(lam[j], zl[j])));
-          maxAx = fmax(maxAx, fabs(lam[j]));
-          maxz = fmax(maxz, fabs(zl[j]));
+          dmax = fmax(dmax, fabs(dyl[j]));
+          atd = fmax(atd, fabs(Q.tmul(j, dyc, __dadd_rn(dyl[j], dye))));
         }
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-          double acc = 0.0;
-#pragma unroll
-          for (int j = 0; j < J; ++j) acc = __fma_rn(Q[c][j], lam[j], acc);
-          const double ax = __dsub_rn(acc, del[c]);
-          rprim = fmax(rprim, fabs(__dsub_rn(ax, zc[c])));
-          maxAx = fmax(maxAx, fabs(ax));
-          maxz = fmax(maxz, fabs(zc[c]));
+          dmax = fmax(dmax, fabs(dyc[c]));
+          atd = fmax(atd, fabs(dyc[c]));
+          supp = __dadd_rn(supp, __dmul_rn(b[c], dyc[c]));
         }
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          double acc = __dadd_rn(yl[j], ye);
-#pragma unroll
-          for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], yc[c], acc);
-          rdual = fmax(rdual, fabs(acc));
-          maxATy = fmax(maxATy, fabs(acc));
-        }
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          const double px = __dmul_rn(2.0, del[c]);
-          rdual = fmax(rdual, fabs(__dsub_rn(px, yc[c])));
-          maxPx = fmax(maxPx, fabs(px));
-          maxATy = fmax(maxATy, fabs(yc[c]));
-        }
-        const double eps_p = rel ? qp.eps_abs + qp.eps_rel * fmax(maxAx, maxz) : qp.eps_abs;
-        const double eps_d = rel ? qp.eps_abs + qp.eps_rel * fmax(maxPx, maxATy) : qp.eps_abs;
-        if (rprim <= eps_p && rdual <= eps_d) {
-          status = BZG_SOLVED;
-        } else if (sign_ok) {
-          // primal-infeasibility certificate (qpsolver.py:193-209): with every dy_i on a finite
-          // bound, support = sum_c b_c dy_c + dy_eq
-          double dmax = fabs(dye), atd = 0.0, supp = 0.0;
-#pragma unroll
-          for (int j = 0; j < J; ++j) {
-            dmax = fmax(dmax, fabs(dyl[j]));
-            double acc = __dadd_rn(dyl[j], dye);
-#pragma unroll
-            for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], dyc[c], acc);
-            atd = fmax(atd, fabs(acc));
-          }
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            dmax = fmax(dmax, fabs(dyc[c]));
-            atd = fmax(atd, fabs(dyc[c]));
-            supp = __dadd_rn(supp, __dmul_rn(b[c], dyc[c]));
-          }
-          supp = __dadd_rn(supp, dye);
-          if (dmax > 1e-13 && atd <= qp.eps_pinf * dmax && supp <= -qp.eps_pinf * dmax) status = BZG_INFEASIBLE;
-        }
-        if (status < 0 && it >= qp.max_iter) status = BZG_MAX_ITER;
+        supp = __dadd_rn(supp, dye);
+        if (dmax > 1e-13 && atd <= qp.eps_pinf * dmax && supp <= -qp.eps_pinf * dmax) status = BZG_INFEASIBLE;
       }
+      if (status < 0 && it >= qp.max_iter) status = BZG_MAX_ITER;
       if (status >= 0) {
         st_out[inst] = (int8_t)status;
         it_out[inst] = it;
+        double* xo = x_out + inst * NV;
+        double* zo = zy_out + inst * 2 * MC;
 #pragma unroll
-        for (int j = 0; j < J; ++j) x_out[inst * NV + j] = lam[j];
+        for (int j = 0; j < J; ++j) { xo[j] = lam[j]; zo[C + j] = zl[j]; zo[MC + C + j] = yl[j]; }
 #pragma unroll
-        for (int c = 0; c < C; ++c) x_out[inst * NV + J + c] = del[c];
-        res_out[inst * 2 + 0] = rprim;
-        res_out[inst * 2 + 1] = rdual;
+        for (int c = 0; c < C; ++c) { xo[J + c] = del[c]; zo[c] = zc[c]; zo[MC + c] = yc[c]; }
+        zo[MC - 1] = ze;
+        zo[2 * MC - 1] = ye;
         inst = -1;
       }
     }
   }
 #undef SI
+#undef RHO_MUL
+#undef RI_MUL
 }
 
 }  // namespace

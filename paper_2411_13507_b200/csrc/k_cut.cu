@@ -446,22 +446,36 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       qp.max_iter = cfg->qp_max_iter;
       // persistent grid: enough resident warps to cover the SMs several times
       const long long blocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 16);
-      launch(c, "k_qp_admm", k_qp_admm<Gc, Mc>, dim3((unsigned)blocks), dim3(128), 0, qp, dp,
-             g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
-             d_pend.as<unsigned long long>(), n_inst, d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(),
-             mk->qp_iters.as<int>(), d_x.as<double>(), d_res.as<double>());
+      constexpr int MCc = 2 * Mc + 2 * Gc + 1;
+      DevBuf d_zy;
+      d_zy.alloc(n_inst * 2 * MCc * sizeof(double), c->stream);
+      const bool rel = cfg->qp_eps_rel != 0.0, unit = cfg->qp_rho == 1.0;
+      bool canon = true;
+      for (int o = 0; o < n_obs; ++o) canon = canon && h[o].canon != 0.0;
+      auto admm = rel ? (unit ? k_qp_admm<Gc, Mc, true, true, false> : k_qp_admm<Gc, Mc, true, false, false>)
+                      : (unit ? (canon ? k_qp_admm<Gc, Mc, false, true, true> : k_qp_admm<Gc, Mc, false, true, false>)
+                              : k_qp_admm<Gc, Mc, false, false, false>);
+      launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, dp, g->vertices.as<double>(),
+             g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), d_pend.as<unsigned long long>(), n_inst,
+             d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
+             d_zy.as<double>());
       DevBuf d_list;
       d_list.alloc(n_inst * sizeof(int), c->stream);
       BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
-      launch(c, "k_qp_select", k_qp_select, dim3(div_up(n_inst, 256)), dim3(256), 0, n_inst, NV, 2 * Gc,
-             (int)cfg->qp_polish, polish_screen(), cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(),
+      launch(c, "k_qp_select", k_qp_select<Gc, Mc>, dim3(div_up(n_inst, 256)), dim3(256), 0, dp,
+             g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
+             d_pend.as<unsigned long long>(), n_inst, (int)cfg->qp_polish, polish_screen(), cfg->eps_cut,
+             mk->qp_status.as<int8_t>(), d_x.as<double>(), d_zy.as<double>(), d_res.as<double>(),
              mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
       BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt + 6, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                      c->stream));
       BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
       const long long n_list = (long long)hcnt[6];
       mk->n_polished = n_list;
-      launch(c, "k_qp_polish", k_qp_polish<Gc, Mc>, dim3(div_up(n_list, kPolishWarps)), dim3(32 * kPolishWarps), 0,
+      constexpr int NR = polish_dim<Gc, Mc>();
+      const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
+      BZG_CHECK_CUDA(cudaFuncSetAttribute(k_qp_polish<Gc, Mc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+      launch(c, "k_qp_polish", k_qp_polish<Gc, Mc>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
              dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
              d_pend.as<unsigned long long>(), d_list.as<int>(), n_list, cfg->eps_cut, d_x.as<double>(),
              d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>());
