@@ -113,11 +113,21 @@ struct QOps {
       if (CANON) out[r + M] = -acc;
     }
   }
-  // returns acc + sum_c Q_cj w_c
-  __device__ __forceinline__ double tmul(int j, const double (&w)[C], double acc) const {
+  // f = w folded onto the stored rows: w_r - w_{r+M} (canonical box) or w itself
+  __device__ __forceinline__ void fold(const double (&w)[C], double (&f)[R]) const {
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc = __fma_rn(q[r][j], CANON ? __dsub_rn(w[r], w[r + M]) : w[r], acc);
+    for (int r = 0; r < R; ++r) f[r] = CANON ? __dsub_rn(w[r], w[r + M]) : w[r];
+  }
+  // returns acc + sum_c Q_cj w_c, with f = fold(w)
+  __device__ __forceinline__ double tmulf(int j, const double (&f)[R], double acc) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc = __fma_rn(q[r][j], f[r], acc);
     return acc;
+  }
+  __device__ __forceinline__ double tmul(int j, const double (&w)[C], double acc) const {
+    double f[R];
+    fold(w, f);
+    return tmulf(j, f, acc);
   }
 };
 
@@ -188,11 +198,12 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, con
         tC[c] = __fma_rn(kp, rdel[c], wc);
       }
       const double we = __fma_rn(req, ze, -ye);
-      double rv[J];
+      double rv[J], fT[QOps<G, M, CANON>::R];
+      Q.fold(tC, fT);
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const double wl = UNIT ? __dsub_rn(zl[j], yl[j]) : __fma_rn(rho, zl[j], -yl[j]);
-        rv[j] = Q.tmul(j, tC, __fma_rn(sig, lam[j], __dadd_rn(wl, we)));
+        rv[j] = Q.tmulf(j, fT, __fma_rn(sig, lam[j], __dadd_rn(wl, we)));
       }
       double a[J];
 #pragma unroll
@@ -269,9 +280,11 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, con
           conv &= fabs(r) <= eps;
         }
       }
+      double fY[QOps<G, M, CANON>::R];
+      Q.fold(yc, fY);
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        const double acc = Q.tmul(j, yc, __dadd_rn(yl[j], ye));
+        const double acc = Q.tmulf(j, fY, __dadd_rn(yl[j], ye));
         if (REL) { rdual = fmax(rdual, fabs(acc)); maxATy = fmax(maxATy, fabs(acc)); }
         else conv &= fabs(acc) <= eps;
       }

@@ -32,7 +32,35 @@ struct ObsRec {
   double b_eps[2 * M];  // fl(b + eps_geo)   (graph.py:234)
   double lo[M], hi[M];  // Polytope.as_box bounds (geometry.py:155-185)
   double canon;         // 1 when A == [I; -I] exactly (Box.to_polytope row order)
+  double act_hi[M];     // hi - 1e-6: a point below it cannot make face +k active
+  double act_lo[M];     // lo + 1e-6
+  double thin[M];       // 1 when hi - lo <= 1e-6 (both faces of axis k may be active)
 };
+
+// Exact certificate that box_code_canon returns 1 (safe), from the bounding box
+// [mn, mx] of the control points.  (1) No control point is inside when, for some axis,
+// every point is beyond b + eps on one side.  (2) The face the reference picks is active
+// at the anchor's projection, and face +k can only be active if some point has
+// P_k > hi_k - 1e-6 (|clip(v_k) - hi_k| <= 1e-7 otherwise fails; thin boxes excepted),
+// likewise -k.  (3) If every possibly-active face is cleared by all points
+// (fl(P_kj - b) > margin for all j  <=>  fl(min_j P_kj - b) > margin, monotone rounding),
+// the clearance test passes whichever of them is chosen, so the code is 1.
+template <int M>
+__device__ __forceinline__ bool canon_safe_cert(const double (&mn)[M], const double (&mx)[M], const ObsRec<M>& o,
+                                                double margin) {
+  bool noin = false, ok = true;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    noin |= (mn[k] > o.b_eps[k]) | (-mx[k] > o.b_eps[M + k]);
+    const bool thin = o.thin[k] != 0.0;
+    const bool pa_hi = thin | (mx[k] > o.act_hi[k]);
+    const bool pa_lo = thin | (mn[k] < o.act_lo[k]);
+    const bool clr_hi = __dsub_rn(mn[k], o.b[k]) > margin;
+    const bool clr_lo = __dsub_rn(-mx[k], o.b[M + k]) > margin;
+    ok &= (!pa_hi | clr_hi) & (!pa_lo | clr_lo);
+  }
+  return noin & ok;
+}
 
 struct CutScalars {
   double margin;  // CutConfig.heur_margin
@@ -125,8 +153,8 @@ __device__ __forceinline__ int box_code_canon(const double (&P)[M][2 * G], const
   for (int j = 0; j < J; ++j) {
     bool in = true;
 #pragma unroll
-    for (int k = 0; k < M; ++k) in = in && (P[k][j] <= o.b_eps[k]) && (-P[k][j] <= o.b_eps[M + k]);
-    hit = hit || in;
+    for (int k = 0; k < M; ++k) in &= (P[k][j] <= o.b_eps[k]) & (-P[k][j] <= o.b_eps[M + k]);
+    hit |= in;
   }
   if (hit) return 0;
   int anchor = 0;
@@ -136,7 +164,8 @@ __device__ __forceinline__ int box_code_canon(const double (&P)[M][2 * G], const
     double d2 = 0.0;
 #pragma unroll
     for (int k = 0; k < M; ++k) {
-      const double t = __dadd_rn(fmax(__dsub_rn(o.lo[k], P[k][j]), 0.0), fmax(__dsub_rn(P[k][j], o.hi[k]), 0.0));
+      // max(lo-P, 0) + max(P-hi, 0) == max(lo-P, P-hi, 0) exactly when lo <= hi (as_box)
+      const double t = fmax(fmax(__dsub_rn(o.lo[k], P[k][j]), __dsub_rn(P[k][j], o.hi[k])), 0.0);
       const double sq = __dmul_rn(t, t);
       d2 = (k == 0) ? sq : __dadd_rn(d2, sq);
     }
@@ -213,23 +242,41 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
   }
   unsigned c0 = 0, c1 = 0, c2 = 0;
   const int lane = threadIdx.x & 31;
-  for (int oi = 0; oi < nob; ++oi) {
-    int code = 1;
-    if (valid) code = s_obs[oi].canon != 0.0 ? box_code_canon<G, M>(P, s_obs[oi], margin)
-                                             : box_code<G, M>(P, s_obs[oi], margin);
-    if (valid) {
-      c0 += code == 0;
-      c1 += code == 1;
-      c2 += code == 2;
-      if (code == 0 && kill > o0 + oi) kill = o0 + oi;
+  // pass 1 (coherent across the warp): certify code 1 from the control-polygon bounding box
+  unsigned long long hard = 0;
+  if (valid) {
+    double mn[M], mx[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      mn[k] = P[k][0];
+      mx[k] = P[k][0];
+#pragma unroll
+      for (int j = 1; j < 2 * G; ++j) { mn[k] = fmin(mn[k], P[k][j]); mx[k] = fmax(mx[k], P[k][j]); }
     }
-    const unsigned want = __ballot_sync(0xffffffffu, valid && code == 2);
+    for (int oi = 0; oi < nob; ++oi) {
+      const ObsRec<M>& o = s_obs[oi];
+      if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
+      else hard |= 1ull << oi;
+    }
+  }
+  // pass 2: exact codes for the remaining obstacles, in list order
+  while (hard) {
+    const int oi = __ffsll((long long)hard) - 1;
+    hard &= hard - 1;
+    const int code = s_obs[oi].canon != 0.0 ? box_code_canon<G, M>(P, s_obs[oi], margin)
+                                            : box_code<G, M>(P, s_obs[oi], margin);
+    c0 += code == 0;
+    c1 += code == 1;
+    c2 += code == 2;
+    if (code == 0 && kill > o0 + oi) kill = o0 + oi;
+    const unsigned am = __activemask();
+    const unsigned want = __ballot_sync(am, code == 2);
     if (want) {
       unsigned long long base = 0;
       const int leader = __ffs(want) - 1;
       if (lane == leader) base = atomicAdd(n_pend, (unsigned long long)__popc(want));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (valid && code == 2) {
+      base = __shfl_sync(am, base, leader);
+      if (code == 2) {
         const unsigned long long slot = base + __popc(want & ((1u << lane) - 1u));
         if (slot < cap) pend[slot] = ((unsigned long long)e << 20) | (unsigned long long)(o0 + oi);
       }
@@ -378,6 +425,11 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       for (int q = 0; q < 2 * Mc; ++q)
         for (int k = 0; k < Mc; ++k) canon = canon && r.A[q][k] == (k == (q % Mc) ? (q < Mc ? 1.0 : -1.0) : 0.0);
       r.canon = canon ? 1.0 : 0.0;
+      for (int k = 0; k < Mc; ++k) {
+        r.act_hi[k] = r.hi[k] - 1e-6;
+        r.act_lo[k] = r.lo[k] + 1e-6;
+        r.thin[k] = (r.hi[k] - r.lo[k] > 1e-6) ? 0.0 : 1.0;
+      }
     }
     DevBuf d_obs, d_kill, d_qkill, d_saved, d_cnt;
     d_obs.alloc(sizeof(Rec) * h.size(), c->stream);
@@ -395,7 +447,8 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     unsigned long long cap = (unsigned long long)std::max<long long>(1 << 20, E * (long long)n_obs / 32);
     DevBuf d_pend;
     unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
-    const int chunk = std::max(1, (int)(96 * 1024 / sizeof(Rec)));
+    // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
+    const int chunk = std::min(64, std::max(1, (int)(96 * 1024 / sizeof(Rec))));
     for (int attempt = 0; attempt < 2; ++attempt) {
       d_pend.alloc(cap * sizeof(unsigned long long), c->stream);
       for (int o0 = 0; o0 < n_obs; o0 += chunk) {
