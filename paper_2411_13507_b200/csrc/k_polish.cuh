@@ -80,18 +80,20 @@ __global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int
 // The reference solves the regularised reduced KKT system
 //   K = [[P + d I, G'], [G, -d I]],  d = 1e-8,  G = active rows of A,  rhs = [-q; g]
 // by LU with partial pivoting (np.linalg.solve) plus two refinement steps against K.
-// The delta block of P + d I is (2 + d) I and each delta_c appears only in obstacle row
-// c of G (coefficient -1), so delta is eliminated exactly with the well-conditioned pivot
-// 2 + d; the remaining (lambda, nu) system
-//   R = [[d I_J, G_l'], [G_l, -diag(d + [obstacle row] / (2 + d))]]
-// (inactive constraint slots as decoupled identity rows) is factored by LU with partial
-// pivoting in this thread's slice of shared memory.  Residuals of the refinement steps
-// are taken against the full K, so the iterate converges to the same regularised solution
-// as the reference; then the acceptance test max(rp', rd') < max(rp, rd).
+// Here K is solved by exact block elimination with well-conditioned pivots, then a small
+// dense LU with partial pivoting:
+//   * delta_c (pivot 2 + d): it appears only in obstacle row c of G (coefficient -1);
+//   * each active lambda-bound row j (G row e_j) with lambda_j: the 2x2 pivot
+//     [[d, 1], [1, -d]] (determinant -(1 + d^2));
+//   * the remaining "core" unknowns (free lambda_j, nu of active obstacle rows, nu of the
+//     sum row) form an (J + C + 1)-dim system with unused slots as identity rows.
+// Residuals of the two refinement steps are taken against the full K, so the iterate
+// converges to the same regularised solution as the reference; then the acceptance test
+// max(rp', rd') < max(rp, rd).
 constexpr int kPolishThreads = 64;
 
 template <int G, int M>
-constexpr int polish_dim() { return 2 * G + (2 * M + 2 * G + 1); }  // J + MC
+constexpr int polish_dim() { return 2 * G + 2 * M + 1; }  // core: J + C + 1
 
 template <int G, int M>
 __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
@@ -99,15 +101,16 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
     const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
     long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ res,
     double* __restrict__ delta_out, uint8_t* __restrict__ safe_out) {
-  constexpr int J = 2 * G, C = 2 * M, NV = J + C, MC = C + J + 1, NR = J + MC;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* Rm = reinterpret_cast<double*>(smem_raw) + threadIdx.x;  // element (r, c) at Rm[(r*NR+c)*BS]
-  double* Ym = Rm + NR * NR * kPolishThreads;                      // y[r] at Ym[r*BS]
+  constexpr int J = 2 * G, C = 2 * M, NV = J + C, MC = C + J + 1, NC = J + C + 1;
   constexpr int BS = kPolishThreads;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Rm = reinterpret_cast<double*>(smem_raw) + threadIdx.x;  // core (r, c) at Rm[(r*NC+c)*BS]
+  double* Ym = Rm + NC * NC * BS;                                   // work vector y[r] at Ym[r*BS]
   const long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (li >= n_list) return;
   const long long inst = list[li];
-  auto R = [&](int r, int c) -> double& { return Rm[(r * NR + c) * BS]; };
+  auto R = [&](int r, int c) -> double& { return Rm[(r * NC + c) * BS]; };
+  auto Y = [&](int r) -> double& { return Ym[r * BS]; };
 
   double x[NV];
 #pragma unroll
@@ -115,31 +118,23 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
   const double rp = res[inst * 2], rd = res[inst * 2 + 1];
   double Q[C][J], b[C];
   load_instance<G, M>(dp, Vx, src, dst, obs, pend[inst], Q, b);
-  // constraint rows of A (graph.py:275-281): i < C: [Q_i, -e_i]; C <= i < C+J: [e_{i-C}, 0];
-  // i = C+J: [1..1, 0]
-  auto a_dot = [&](int i, const double (&v)[NV]) -> double {  // A_i . v, FMA chain over columns
+  // constraint slot i of A (graph.py:275-281): i < C obstacle row [Q_i, -e_i];
+  // C <= i < C+J lambda bound [e_{i-C}, 0]; i = C+J the sum row [1..1, 0]
+  auto Gl = [&](int i, int j) -> double {  // lambda part of row i (compile-time i, j)
+    return i < C ? Q[i < C ? i : 0][j] : (i < C + J ? (i - C == j ? 1.0 : 0.0) : 1.0);
+  };
+  auto a_dot = [&](int i, const double (&v)[NV]) -> double {
     double acc = 0.0;
-    if (i < C) {
 #pragma unroll
-      for (int j = 0; j < J; ++j) acc = __fma_rn(Q[i][j], v[j], acc);
-#pragma unroll
-      for (int c = 0; c < C; ++c) if (c == i) acc = __fma_rn(-1.0, v[J + c], acc);
-    } else if (i < C + J) {
-#pragma unroll
-      for (int j = 0; j < J; ++j) if (j == i - C) acc = __fma_rn(1.0, v[j], acc);
-    } else {
-#pragma unroll
-      for (int j = 0; j < J; ++j) acc = __fma_rn(1.0, v[j], acc);
+    for (int j = 0; j < J; ++j) {
+      const double g = Gl(i, j);
+      if (g != 0.0) acc = __fma_rn(g, v[j], acc);
     }
+    if (i < C) acc = __fma_rn(-1.0, v[J + (i < C ? i : 0)], acc);
     return acc;
   };
   auto lo_of = [&](int i) -> double { return i < C ? -INFINITY : (i < C + J ? 0.0 : 1.0); };
-  auto hi_of = [&](int i) -> double {
-    double v = i < C + J ? INFINITY : 1.0;
-#pragma unroll
-    for (int c = 0; c < C; ++c) if (c == i) v = b[c];
-    return v;
-  };
+  auto hi_of = [&](int i) -> double { return i < C ? b[i < C ? i : 0] : (i < C + J ? INFINITY : 1.0); };
   // active set at z = A x (qpsolver.py:245-249)
   const double tol = fmax(1e-7, 10.0 * rp);
   unsigned act = 0, atlo = 0;
@@ -153,43 +148,55 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
   bool accept = false;
   double xp[NV];
   if (act) {
-    const double reg = 1e-8, i2 = 1.0 / (2.0 + reg);
-    // ---- build R (compile-time indices keep Q in registers) and factor it
+    const double reg = 1e-8, i2 = 1.0 / (2.0 + reg), e2 = reg / (1.0 + reg * reg), r2 = 1.0 / (1.0 + reg * reg);
+    auto a_on = [&](int i) -> bool { return act >> i & 1u; };
+    // core slot of row/column r: r < J lambda_r (used iff lambda bound r inactive),
+    // J <= r < J+C nu of obstacle row r-J, r = J+C nu of the sum row
+    auto core_used = [&](int r) -> bool { return r < J ? !a_on(C + r) : (r < J + C ? a_on(r - J) : a_on(C + J)); };
+    auto core_row = [&](int r) -> int { return r < J ? -1 : (r < J + C ? r - J : C + J); };  // constraint slot
+    // ---- build the core matrix (compile-time indices keep Q in registers)
 #pragma unroll
-    for (int r = 0; r < NR; ++r)
+    for (int r = 0; r < NC; ++r)
 #pragma unroll
-      for (int c = 0; c < NR; ++c) {
+      for (int c = 0; c < NC; ++c) {
         double v = 0.0;
-        if (r < J && c < J) {
-          v = r == c ? reg : 0.0;
-        } else if (r < J) {  // G_l' : column c-J is constraint slot i, row r is lambda_r
-          const int i = c - J;
-          if (act >> i & 1u) v = i < C ? Q[i < C ? i : 0][r] : (i < C + J ? (i - C == r ? 1.0 : 0.0) : 1.0);
+        if (!core_used(r) || !core_used(c)) {
+          v = (r == c) ? 1.0 : 0.0;
+        } else if (r < J && c < J) {
+          v = (r == c) ? reg : 0.0;
+        } else if (r < J) {
+          v = Gl(core_row(c), r);
+        } else if (c < J) {
+          v = Gl(core_row(r), c);
         } else {
-          const int i = r - J;
-          if (!(act >> i & 1u)) v = (c == r) ? 1.0 : 0.0;
-          else if (c < J) v = i < C ? Q[i < C ? i : 0][c < J ? c : 0] : (i < C + J ? (i - C == c ? 1.0 : 0.0) : 1.0);
-          else if (c == r) v = -(reg + (i < C ? i2 : 0.0));
+          const int i = core_row(r), k = core_row(c);
+          double s = 0.0;  // sum over eliminated lambda bounds j of G[i][j] G[k][j]
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+            if (a_on(C + j)) s = __fma_rn(Gl(i, j), Gl(k, j), s);
+          v = -e2 * s;
+          if (r == c) v = __dsub_rn(v, i < C ? reg + i2 : reg);
         }
         R(r, c) = v;
       }
-    unsigned char perm[NR];
+    // ---- LU with partial pivoting (first max |.|, reciprocal scaling as dgetf2)
+    unsigned char perm[NC];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) perm[r] = (unsigned char)r;
+    for (int r = 0; r < NC; ++r) perm[r] = (unsigned char)r;
     bool singular = false;
 #pragma unroll 1
-    for (int cc = 0; cc < NR; ++cc) {
+    for (int cc = 0; cc < NC; ++cc) {
       int piv = cc;
       double best = fabs(R(cc, cc));
 #pragma unroll 1
-      for (int r = cc + 1; r < NR; ++r) {
+      for (int r = cc + 1; r < NC; ++r) {
         const double v = fabs(R(r, cc));
         if (v > best) { best = v; piv = r; }
       }
       if (best == 0.0) { singular = true; break; }
       if (piv != cc) {
 #pragma unroll 1
-        for (int c = 0; c < NR; ++c) {
+        for (int c = 0; c < NC; ++c) {
           const double t = R(cc, c);
           R(cc, c) = R(piv, c);
           R(piv, c) = t;
@@ -200,50 +207,79 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
       }
       const double rpv = 1.0 / R(cc, cc);
 #pragma unroll 1
-      for (int r = cc + 1; r < NR; ++r) {
+      for (int r = cc + 1; r < NC; ++r) {
         const double l = __dmul_rn(R(r, cc), rpv);
         R(r, cc) = l;
         if (l != 0.0) {
 #pragma unroll 1
-          for (int c = cc + 1; c < NR; ++c) R(r, c) = __fma_rn(-l, R(cc, c), R(r, c));
+          for (int c = cc + 1; c < NC; ++c) R(r, c) = __fma_rn(-l, R(cc, c), R(r, c));
         }
       }
     }
     if (!singular) {
-      // solve K w = r for the full unknown w = (x (NV), nu (MC slots)); r given as (rx, rn)
+      // solve K w = (rx, rn) for w = (x (NV), nu (MC slots; 0 on inactive slots))
       auto solve = [&](const double (&rx)[NV], const double (&rn)[MC], double (&wx)[NV], double (&wn)[MC]) {
-        double v[NR];  // reduced rhs in original row order: lambda rows, then constraint slots
+        double rr[MC];  // constraint rhs after eliminating delta
 #pragma unroll
-        for (int j = 0; j < J; ++j) v[j] = rx[j];
+        for (int i = 0; i < MC; ++i) rr[i] = (i < C && a_on(i)) ? __fma_rn(rx[J + (i < C ? i : 0)], i2, rn[i]) : rn[i];
+        double lamb[J];  // a_j + e2 (b_j - d a_j): the eliminated lambda_j without its nu coupling
 #pragma unroll
-        for (int i = 0; i < MC; ++i) {
-          double t = rn[i];
-          if (i < C && (act >> i & 1u)) t = __fma_rn(rx[J + i], i2, t);  // + r_delta_c / (2 + d)
-          v[J + i] = (act >> i & 1u) ? t : 0.0;
+        for (int j = 0; j < J; ++j) lamb[j] = __fma_rn(e2, __fma_rn(-reg, rr[C + j], rx[j]), rr[C + j]);
+        double v[NC];
+#pragma unroll
+        for (int r = 0; r < NC; ++r) {
+          double t = 0.0;
+          if (core_used(r)) {
+            if (r < J) {
+              t = rx[r];
+            } else {
+              const int i = core_row(r);
+              t = rr[i];
+#pragma unroll
+              for (int j = 0; j < J; ++j)
+                if (a_on(C + j)) t = __fma_rn(-Gl(i, j), lamb[j], t);
+            }
+          }
+          v[r] = t;
         }
-        auto y = [&](int r) -> double& { return Ym[r * BS]; };
 #pragma unroll 1
-        for (int r = 0; r < NR; ++r) {
+        for (int r = 0; r < NC; ++r) {
           double t = 0.0;
 #pragma unroll
-          for (int q = 0; q < NR; ++q) if (q == perm[r]) t = v[q];
+          for (int q = 0; q < NC; ++q) if (q == perm[r]) t = v[q];
 #pragma unroll 1
-          for (int c = 0; c < r; ++c) t = __fma_rn(-R(r, c), y(c), t);
-          y(r) = t;
+          for (int c = 0; c < r; ++c) t = __fma_rn(-R(r, c), Y(c), t);
+          Y(r) = t;
         }
 #pragma unroll 1
-        for (int r = NR - 1; r >= 0; --r) {
-          double t = y(r);
+        for (int r = NC - 1; r >= 0; --r) {
+          double t = Y(r);
 #pragma unroll 1
-          for (int c = r + 1; c < NR; ++c) t = __fma_rn(-R(r, c), y(c), t);
-          y(r) = t / R(r, r);
+          for (int c = r + 1; c < NC; ++c) t = __fma_rn(-R(r, c), Y(c), t);
+          Y(r) = t / R(r, r);
+        }
+        double core[NC];
+#pragma unroll
+        for (int r = 0; r < NC; ++r) core[r] = core_used(r) ? Y(r) : 0.0;
+#pragma unroll
+        for (int i = 0; i < MC; ++i) wn[i] = 0.0;
+#pragma unroll
+        for (int r = J; r < NC; ++r) wn[core_row(r)] = core[r];
+        // recover the eliminated lambda-bound pairs, then lambda_free, then delta
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          if (a_on(C + j)) {
+            double t = __fma_rn(-reg, rr[C + j], rx[j]);
+#pragma unroll
+            for (int r = J; r < NC; ++r) t = __fma_rn(-Gl(core_row(r), j), core[r], t);
+            wn[C + j] = __dmul_rn(t, r2);
+            wx[j] = __fma_rn(reg, wn[C + j], rr[C + j]);
+          } else {
+            wx[j] = core[j];
+          }
         }
 #pragma unroll
-        for (int j = 0; j < J; ++j) wx[j] = y(j);
-#pragma unroll
-        for (int i = 0; i < MC; ++i) wn[i] = (act >> i & 1u) ? y(J + i) : 0.0;
-#pragma unroll
-        for (int c = 0; c < C; ++c) wx[J + c] = __dmul_rn(__dadd_rn(rx[J + c], wn[c]), i2);
+        for (int c = 0; c < C; ++c) wx[J + c] = __dmul_rn(__dadd_rn(rx[J + c], a_on(c) ? wn[c] : 0.0), i2);
       };
       // K w for the full system (rows: x then active constraint slots)
       auto kmul = [&](const double (&wx)[NV], const double (&wn)[MC], double (&ox)[NV], double (&on)[MC]) {
@@ -251,23 +287,20 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
         for (int j = 0; j < J; ++j) {
           double acc = __dmul_rn(reg, wx[j]);
 #pragma unroll
-          for (int i = 0; i < MC; ++i) {
-            if (!(act >> i & 1u)) continue;
-            const double g = i < C ? Q[i][j] : (i < C + J ? (i - C == j ? 1.0 : 0.0) : 1.0);
-            acc = __fma_rn(g, wn[i], acc);
-          }
+          for (int i = 0; i < MC; ++i)
+            if (a_on(i)) acc = __fma_rn(Gl(i, j), wn[i], acc);
           ox[j] = acc;
         }
 #pragma unroll
-        for (int c = 0; c < C; ++c) ox[J + c] = __fma_rn(2.0 + reg, wx[J + c], (act >> c & 1u) ? -wn[c] : 0.0);
+        for (int c = 0; c < C; ++c) ox[J + c] = __fma_rn(2.0 + reg, wx[J + c], a_on(c) ? -wn[c] : 0.0);
 #pragma unroll
-        for (int i = 0; i < MC; ++i) on[i] = (act >> i & 1u) ? __fma_rn(-reg, wn[i], a_dot(i, wx)) : 0.0;
+        for (int i = 0; i < MC; ++i) on[i] = a_on(i) ? __fma_rn(-reg, wn[i], a_dot(i, wx)) : 0.0;
       };
       double bx[NV], bn[MC], wx[NV], wn[MC];
 #pragma unroll
       for (int t = 0; t < NV; ++t) bx[t] = 0.0;  // -q = 0
 #pragma unroll
-      for (int i = 0; i < MC; ++i) bn[i] = (act >> i & 1u) ? ((atlo >> i & 1u) ? lo_of(i) : hi_of(i)) : 0.0;
+      for (int i = 0; i < MC; ++i) bn[i] = a_on(i) ? ((atlo >> i & 1u) ? lo_of(i) : hi_of(i)) : 0.0;
       solve(bx, bn, wx, wn);
 #pragma unroll 1
       for (int rep = 0; rep < 2; ++rep) {
@@ -293,18 +326,14 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
       }
       double rdt = 0.0;
 #pragma unroll
-      for (int t = 0; t < NV; ++t) {  // |P x + A' y|_t with y = nu on active rows
-        double acc = t >= J ? __dmul_rn(2.0, wx[t]) : 0.0;
+      for (int j = 0; j < J; ++j) {  // |P x + A' y| with y = nu on active slots
+        double acc = 0.0;
 #pragma unroll
-        for (int i = 0; i < MC; ++i) {
-          double a;
-          if (i < C) a = t < J ? Q[i][t] : (t - J == i ? -1.0 : 0.0);
-          else if (i < C + J) a = (t == i - C) ? 1.0 : 0.0;
-          else a = t < J ? 1.0 : 0.0;
-          acc = __fma_rn(a, wn[i], acc);
-        }
+        for (int i = 0; i < MC; ++i) acc = __fma_rn(Gl(i, j), wn[i], acc);
         rdt = fmax(rdt, fabs(acc));
       }
+#pragma unroll
+      for (int c = 0; c < C; ++c) rdt = fmax(rdt, fabs(__fma_rn(-1.0, wn[c], __dmul_rn(2.0, wx[J + c]))));
       if (fmax(__dadd_rn(upv, lov), rdt) < fmax(rp, rd)) {
         accept = true;
 #pragma unroll
