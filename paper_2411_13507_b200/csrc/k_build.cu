@@ -69,14 +69,52 @@ struct RowPlan {
   double th_src[kMaxIntervals], th_dst[kMaxIntervals];
 };
 
-// a1c[i, q] = V_i . F1[row_iv[q]],  a2t[q, i] = V_i . F2[row_iv[q]] (FMA chain, graph.py:174-175);
-// src_ok / dst_ok fold the one-sided rows into per-vertex predicates (exact: the other
-// side's product is +-0).
-__global__ void k_project(RowPlan rp, const double* __restrict__ F, const double* __restrict__ Vx, long long V,
-                          int Kpad, double* __restrict__ a1c, double* __restrict__ a2t, uint8_t* __restrict__ src_ok,
-                          uint8_t* __restrict__ dst_ok) {
+// ---------------------------------------------------------------- pair test
+struct Bounds {
+  double lo[kMaxIntervals], hi[kMaxIntervals];
+};
+
+constexpr int kPairThreads = 256;  // dst columns per block (8 warps x 32)
+
+// Bit (i, j) of the pair matrix (graph.py:181-184): fl(a1[i,r] + a2[j,r]) <= G_r + eps for
+// every row r, evaluated as intervals lo_q <= a1c[i,q] + a2[j,q] <= hi_q over the negation
+// pairs plus the per-vertex one-sided predicates, diagonal cleared.
+// ---------------------------------------------------------------- spatially tiled pair test
+// Vertices are visited in Morton order of their position so that a warp's 32 destinations
+// (a "group") and a block's 32 sources (a "tile") are close in state space.  Per interval q
+// the group's [min, max] of a2 and the tile's [min, max] of a1 bound every pair sum; since
+// fl(a + b) is monotone in each argument, fl(min1 + min2) > hi_q (or fl(max1 + max2) < lo_q)
+// proves every pair of the block fails row q -- an exact cull.  Surviving (source, group)
+// pairs are culled again with the source's own a1, and only then tested lane by lane.  Edge
+// bits land in the original-index bit matrix (atomicOr), so the CSR order is unchanged.
+constexpr int kTile = 32;
+
+__global__ void k_morton(const double* __restrict__ Vx, long long V, int n, int m, double lo0, double lo1,
+                         double lo2, double s0, double s1, double s2, unsigned* __restrict__ key, int* __restrict__ idx) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= V) return;
+  const int bits = m == 1 ? 30 : (m == 2 ? 16 : 10);
+  const unsigned cap = (1u << bits) - 1u;
+  auto cell = [&](int k, double lo, double s) -> unsigned {
+    const double t = (Vx[i * n + k] - lo) * s;
+    return t <= 0.0 ? 0u : (t >= (double)cap ? cap : (unsigned)t);
+  };
+  unsigned c[3] = {cell(0, lo0, s0), m > 1 ? cell(1, lo1, s1) : 0u, m > 2 ? cell(2, lo2, s2) : 0u};
+  unsigned code = 0;
+  for (int b = bits - 1; b >= 0; --b)
+    for (int k = 0; k < m; ++k) code = (code << 1) | ((c[k] >> b) & 1u);
+  key[i] = code;
+  idx[i] = (int)i;
+}
+
+// projections at sorted position s (vertex perm[s]); src_ok also requires the row block
+__global__ void k_project_sorted(RowPlan rp, const double* __restrict__ F, const double* __restrict__ Vx,
+                                 const int* __restrict__ perm, long long V, int Kpad, long long r0, long long r1,
+                                 double* __restrict__ a1c, double* __restrict__ a2t, uint8_t* __restrict__ src_ok,
+                                 uint8_t* __restrict__ dst_ok) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= V) return;
+  const long long i = perm[s];
   const int n = rp.n;
   double v[kMaxN];
   for (int k = 0; k < n; ++k) v[k] = Vx[i * n + k];
@@ -87,80 +125,115 @@ __global__ void k_project(RowPlan rp, const double* __restrict__ F, const double
       x1 = fma_chain(v, f, n);
       x2 = fma_chain(v, f + n, n);
     }
-    a1c[i * Kpad + q] = x1;
-    a2t[(long long)q * V + i] = x2;
+    a1c[s * Kpad + q] = x1;
+    a2t[(long long)q * V + s] = x2;
   }
-  int ok = 1;
+  int ok = i >= r0 && i < r1;
   for (int q = 0; q < rp.n_src; ++q) ok &= fma_chain(v, F + (size_t)rp.row_src[q] * 2 * n, n) <= rp.th_src[q];
-  src_ok[i] = (uint8_t)ok;
+  src_ok[s] = (uint8_t)ok;
   ok = 1;
   for (int q = 0; q < rp.n_dst; ++q) ok &= fma_chain(v, F + (size_t)rp.row_dst[q] * 2 * n + n, n) <= rp.th_dst[q];
-  dst_ok[i] = (uint8_t)ok;
+  dst_ok[s] = (uint8_t)ok;
 }
 
-// ---------------------------------------------------------------- pair test
-struct Bounds {
-  double lo[kMaxIntervals], hi[kMaxIntervals];
-};
+// [min, max] per (32-vertex group, interval) over the group's valid vertices
+__global__ void k_group_bounds(const double* __restrict__ a, int transposed, long long V, int Kpad,
+                               const uint8_t* __restrict__ ok, double* __restrict__ gmin, double* __restrict__ gmax) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long ng = (V + kTile - 1) / kTile;
+  if (t >= ng * Kpad) return;
+  const long long g = t / Kpad;
+  const int q = (int)(t - g * Kpad);
+  double mn = INFINITY, mx = -INFINITY;
+  for (int l = 0; l < kTile; ++l) {
+    const long long s = g * kTile + l;
+    if (s >= V || !ok[s]) continue;
+    const double v = transposed ? a[(long long)q * V + s] : a[s * Kpad + q];
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  gmin[t] = mn;
+  gmax[t] = mx;
+}
 
-constexpr int kPairThreads = 256;  // dst columns per block (8 warps x 32)
-constexpr int kPairRows = 32;      // src rows per block
-
-// Bit (i, j) of the pair matrix: fl(a1[i,r] + a2[j,r]) <= G_r + eps for every row r
-// (graph.py:181-182), evaluated as intervals lo_q <= a1c[i,q] + a2[j,q] <= hi_q over the
-// negation pairs, plus the per-vertex one-sided predicates; the diagonal is cleared
-// (graph.py:184).  One warp ballots 32 destinations into one 32-bit word.
 template <int K>
-__global__ void __launch_bounds__(kPairThreads) k_pair_bits(Bounds bd, const double* __restrict__ a1c,
-                                                            const double* __restrict__ a2t,
-                                                            const uint8_t* __restrict__ src_ok,
-                                                            const uint8_t* __restrict__ dst_ok, long long V,
-                                                            long long r0, long long r1, long long W,
-                                                            uint32_t* __restrict__ bits,
-                                                            unsigned long long* __restrict__ rowcnt) {
-  __shared__ double s_a1[kPairRows][K];
-  __shared__ uint8_t s_ok[kPairRows];
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const long long j = (long long)blockIdx.x * kPairThreads + tid;
-  const long long i0 = r0 + (long long)blockIdx.y * kPairRows;
-  const int rows = (int)min((long long)kPairRows, r1 - i0);
-
+__global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
+    Bounds bd, const double* __restrict__ a1c, const double* __restrict__ a2t, const uint8_t* __restrict__ src_ok,
+    const uint8_t* __restrict__ dst_ok, const int* __restrict__ perm, const double* __restrict__ tmin,
+    const double* __restrict__ tmax, const double* __restrict__ gmin, const double* __restrict__ gmax, long long V,
+    long long r0, long long W, uint32_t* __restrict__ bits, unsigned long long* __restrict__ rowcnt) {
+  __shared__ double s_a1[kTile][K];
+  __shared__ uint8_t s_ok[kTile];
+  __shared__ int s_orig[kTile];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long tile = blockIdx.y;
+  const long long i0 = tile * kTile;
+  const int rows = (int)min((long long)kTile, V - i0);
   for (int e = tid; e < rows * K; e += kPairThreads) {
     const int ii = e / K, q = e - ii * K;
     s_a1[ii][q] = a1c[(i0 + ii) * K + q];
   }
-  if (tid < rows) s_ok[tid] = src_ok[i0 + tid];
-
+  if (tid < rows) {
+    s_ok[tid] = src_ok[i0 + tid];
+    s_orig[tid] = perm[i0 + tid];
+  }
+  __syncthreads();
+  const long long g = (long long)blockIdx.x * (kPairThreads / 32) + warp;
+  if (g * kTile >= V) return;
+  // interval bounds this lane watches in the cull tests: q = lane, lane + 32
+  constexpr int QL = (K + 31) / 32;
+  double gl[QL], gh[QL], lo_[QL], hi_[QL];
+  bool cull = false;
+#pragma unroll
+  for (int u = 0; u < QL; ++u) {
+    const int q = lane + 32 * u;
+    const bool on = q < K;
+    gl[u] = on ? gmin[g * K + q] : 0.0;
+    gh[u] = on ? gmax[g * K + q] : 0.0;
+    lo_[u] = on ? bd.lo[q] : -INFINITY;
+    hi_[u] = on ? bd.hi[q] : INFINITY;
+    if (on) cull |= (__dadd_rn(tmin[tile * K + q], gl[u]) > hi_[u]) | (__dadd_rn(tmax[tile * K + q], gh[u]) < lo_[u]);
+  }
+  if (__any_sync(0xffffffffu, cull)) return;  // no pair of (tile, group) can pass
+  const long long j = g * kTile + lane;
   double a2[K];
   bool jok = j < V;
+  int orig_j = 0;
   if (jok) {
 #pragma unroll
     for (int q = 0; q < K; ++q) a2[q] = a2t[(long long)q * V + j];
     jok = dst_ok[j] != 0;
+    orig_j = perm[j];
   } else {
 #pragma unroll
     for (int q = 0; q < K; ++q) a2[q] = 0.0;
   }
-  __syncthreads();
-
-  const long long word = (long long)blockIdx.x * (kPairThreads / 32) + warp;
-  if (word >= W) return;  // whole warp past the last word (uniform per warp)
   for (int ii = 0; ii < rows; ++ii) {
-    const long long i = i0 + ii;
-    bool ok = jok && s_ok[ii] && (i != j);
+    if (!s_ok[ii]) continue;
+    bool c2 = false;
+#pragma unroll
+    for (int u = 0; u < QL; ++u) {
+      const int q = lane + 32 * u;
+      if (q < K) {
+        const double a = s_a1[ii][q];
+        c2 |= (__dadd_rn(a, gl[u]) > hi_[u]) | (__dadd_rn(a, gh[u]) < lo_[u]);
+      }
+    }
+    if (__any_sync(0xffffffffu, c2)) continue;
+    bool ok = jok && (i0 + ii != j);
 #pragma unroll
     for (int q = 0; q < K; ++q) {
-      if ((q & 3) == 0 && q > 0) {
+      if ((q & 1) == 0 && q > 0) {
         if (!__any_sync(0xffffffffu, ok)) break;
       }
       const double s = __dadd_rn(s_a1[ii][q], a2[q]);
       ok = ok && (s <= bd.hi[q]) && (s >= bd.lo[q]);
     }
-    const unsigned m = __ballot_sync(0xffffffffu, ok);
-    if (lane == 0) {
-      bits[(i - r0) * W + word] = m;
-      if (m) atomicAdd(rowcnt + (i - r0), (unsigned long long)__popc(m));
+    const unsigned mk = __ballot_sync(0xffffffffu, ok);
+    if (mk) {
+      const long long row = (long long)s_orig[ii] - r0;
+      if (ok) atomicOr(bits + row * W + (orig_j >> 5), 1u << (orig_j & 31));
+      if (lane == 0) atomicAdd(rowcnt + row, (unsigned long long)__popc(mk));
     }
   }
 }
@@ -413,31 +486,79 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
   a2t.alloc((size_t)V * Kpad * sizeof(double), c->stream);
   sok.alloc(V, c->stream);
   dok.alloc(V, c->stream);
-  launch(c, "k_project", k_project, dim3(div_up(V, 128)), dim3(128), 0, rp, dF.as<double>(),
-         g->vertices.as<double>(), V, Kpad, a1c.as<double>(), a2t.as<double>(), sok.as<uint8_t>(), dok.as<uint8_t>());
-
   const long long W = (V + 31) / 32;
   DevBuf bits, rowcnt, rptr;
   bits.alloc((size_t)std::max(rows, 1ll) * W * sizeof(uint32_t), c->stream);
   rowcnt.alloc((size_t)(rows + 1) * sizeof(unsigned long long), c->stream);
   rptr.alloc((size_t)(rows + 1) * sizeof(long long), c->stream);
   BZG_CHECK_CUDA(cudaMemsetAsync(rowcnt.ptr, 0, (rows + 1) * sizeof(unsigned long long), c->stream));
+  BZG_CHECK_CUDA(cudaMemsetAsync(bits.ptr, 0, (size_t)std::max(rows, 1ll) * W * sizeof(uint32_t), c->stream));
+
+  // ---- Morton order of the positions (first m coordinates); the box only steers tiling
+  const int m = g->m;
+  double plo[3] = {0, 0, 0}, phi[3] = {1, 1, 1};
+  for (int k = 0; k < m && k < 3; ++k) {
+    double lo = INFINITY, hi = -INFINITY;
+    if (d->vertices) {
+      for (long long i = 0; i < d->N; ++i) { lo = std::min(lo, d->vertices[i * n + k]); hi = std::max(hi, d->vertices[i * n + k]); }
+    } else {
+      lo = d->sample_lo[k];
+      hi = d->sample_hi[k];
+    }
+    for (long long i = 0; i < d->n_include; ++i) {
+      lo = std::min(lo, d->include[i * n + k]);
+      hi = std::max(hi, d->include[i * n + k]);
+    }
+    plo[k] = lo;
+    phi[k] = hi > lo ? hi : lo + 1.0;
+  }
+  const double cells = m == 1 ? 1073741823.0 : (m == 2 ? 65535.0 : 1023.0);
+  DevBuf key, key2, idx, perm;
+  key.alloc(V * sizeof(unsigned), c->stream);
+  key2.alloc(V * sizeof(unsigned), c->stream);
+  idx.alloc(V * sizeof(int), c->stream);
+  perm.alloc(V * sizeof(int), c->stream);
+  launch(c, "k_morton", k_morton, dim3(div_up(V, 256)), dim3(256), 0, g->vertices.as<double>(), V, n, std::min(m, 3),
+         plo[0], plo[1], plo[2], cells / (phi[0] - plo[0]), cells / (phi[1] - plo[1]), cells / (phi[2] - plo[2]),
+         key.as<unsigned>(), idx.as<int>());
+  {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.as<unsigned>(), key2.as<unsigned>(), idx.as<int>(),
+                                    perm.as<int>(), V, 0, 32, c->stream);
+    c->scratch.alloc(bytes, c->stream);
+    ScopedLibLaunch l(c, "cub_sort_morton", 4);
+    BZG_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(c->scratch.ptr, bytes, key.as<unsigned>(), key2.as<unsigned>(),
+                                                   idx.as<int>(), perm.as<int>(), V, 0, 32, c->stream));
+  }
+  launch(c, "k_project_sorted", k_project_sorted, dim3(div_up(V, 128)), dim3(128), 0, rp, dF.as<double>(),
+         g->vertices.as<double>(), perm.as<int>(), V, Kpad, r0, r1, a1c.as<double>(), a2t.as<double>(),
+         sok.as<uint8_t>(), dok.as<uint8_t>());
+  const long long ng = (V + kTile - 1) / kTile;
+  DevBuf tmin, tmax, gmin, gmax;
+  tmin.alloc(ng * Kpad * sizeof(double), c->stream);
+  tmax.alloc(ng * Kpad * sizeof(double), c->stream);
+  gmin.alloc(ng * Kpad * sizeof(double), c->stream);
+  gmax.alloc(ng * Kpad * sizeof(double), c->stream);
+  launch(c, "k_group_bounds", k_group_bounds, dim3(div_up(ng * Kpad, 256)), dim3(256), 0, a1c.as<double>(), 0, V, Kpad,
+         sok.as<uint8_t>(), tmin.as<double>(), tmax.as<double>());
+  launch(c, "k_group_bounds", k_group_bounds, dim3(div_up(ng * Kpad, 256)), dim3(256), 0, a2t.as<double>(), 1, V, Kpad,
+         dok.as<uint8_t>(), gmin.as<double>(), gmax.as<double>());
   if (!never && rows > 0) {
-    dim3 grid(div_up(V, kPairThreads), div_up(rows, kPairRows));
+    dim3 grid(div_up(V, kPairThreads), (unsigned)ng);
     auto go = [&](auto kern) {
-      launch(c, "k_pair_bits", kern, grid, dim3(kPairThreads), 0, bd, a1c.as<double>(), a2t.as<double>(),
-             sok.as<uint8_t>(), dok.as<uint8_t>(), V, r0, r1, W, bits.as<uint32_t>(),
-             rowcnt.as<unsigned long long>());
+      launch(c, "k_pair_tiles", kern, grid, dim3(kPairThreads), 0, bd, a1c.as<double>(), a2t.as<double>(),
+             sok.as<uint8_t>(), dok.as<uint8_t>(), perm.as<int>(), tmin.as<double>(), tmax.as<double>(),
+             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>());
     };
     switch (Kpad) {
-      case 4: go(k_pair_bits<4>); break;
-      case 8: go(k_pair_bits<8>); break;
-      case 12: go(k_pair_bits<12>); break;
-      case 16: go(k_pair_bits<16>); break;
-      case 24: go(k_pair_bits<24>); break;
-      case 32: go(k_pair_bits<32>); break;
-      case 48: go(k_pair_bits<48>); break;
-      default: go(k_pair_bits<64>); break;
+      case 4: go(k_pair_tiles<4>); break;
+      case 8: go(k_pair_tiles<8>); break;
+      case 12: go(k_pair_tiles<12>); break;
+      case 16: go(k_pair_tiles<16>); break;
+      case 24: go(k_pair_tiles<24>); break;
+      case 32: go(k_pair_tiles<32>); break;
+      case 48: go(k_pair_tiles<48>); break;
+      default: go(k_pair_tiles<64>); break;
     }
   }
   exclusive_scan_ll(c, rowcnt.as<unsigned long long>(), rptr.as<long long>(), rows + 1);
