@@ -59,6 +59,9 @@ int bzg_ctx_stream(bzg_ctx* ctx, void** stream_out);
 int bzg_ctx_synchronize(bzg_ctx* ctx);
 /* per-kernel CUDA-event timing of every launch (off by default) */
 int bzg_ctx_set_profiling(bzg_ctx* ctx, int enabled);
+/* restrict profiling to launches of one kernel (NULL or "" = all), so timing a step adds
+ * only two event records per launch of that kernel */
+int bzg_ctx_profile_only(bzg_ctx* ctx, const char* kernel);
 /* launches since creation/reset; with profiling, per-kernel totals.
  * names: buffer of n_cap*64 chars; ms/launches: n_cap entries; *n_out = kernels seen. */
 int bzg_ctx_stats(bzg_ctx* ctx, long long* launches, int n_cap, char* names, double* ms,

@@ -60,6 +60,7 @@ _SIGS = {
     "bzg_ctx_stream": ([_P, C.POINTER(_P)], C.c_int),
     "bzg_ctx_synchronize": ([_P], C.c_int),
     "bzg_ctx_set_profiling": ([_P, C.c_int], C.c_int),
+    "bzg_ctx_profile_only": ([_P, C.c_char_p], C.c_int),
     "bzg_ctx_stats": ([_P, C.POINTER(C.c_longlong), C.c_int, C.c_char_p, _P, _P, C.POINTER(C.c_int)], C.c_int),
     "bzg_ctx_reset_stats": ([_P], C.c_int),
     "bzg_build_graph": ([_P, C.POINTER(BuildDesc), C.POINTER(_P)], C.c_int),
@@ -150,6 +151,9 @@ class Context:
 
     def set_profiling(self, on: bool):
         check(self.lib.bzg_ctx_set_profiling(self.handle, int(bool(on))))
+
+    def profile_only(self, kernel: str | None):
+        check(self.lib.bzg_ctx_profile_only(self.handle, kernel.encode() if kernel else None))
 
     def reset_stats(self):
         check(self.lib.bzg_ctx_reset_stats(self.handle))

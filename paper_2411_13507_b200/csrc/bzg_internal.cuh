@@ -77,7 +77,9 @@ struct Ctx {
   bool own_stream = false;
   int num_sms = 148;
   bool profiling = false;
+  std::string profile_only;  // when non-empty, time only launches of this kernel
   long long launches = 0;
+  bool timed(const char* name) const { return profiling && (profile_only.empty() || profile_only == name); }
   struct Pending { std::string name; cudaEvent_t a, b; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> spare;
@@ -126,11 +128,12 @@ inline void launch(Ctx* c, const char* name, void (*kern)(KArgs...), dim3 grid, 
                    Args&&... args) {
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
   cudaEvent_t a = nullptr, b = nullptr;
-  if (c->profiling) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
+  const bool timed = c->timed(name);
+  if (timed) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
   kern<<<grid, block, smem, c->stream>>>(std::forward<Args>(args)...);
   BZG_CHECK_CUDA(cudaGetLastError());
   c->launches++;
-  if (c->profiling) {
+  if (timed) {
     b = c->take_event();
     BZG_CHECK_CUDA(cudaEventRecord(b, c->stream));
     c->pending.push_back({name, a, b});
@@ -141,11 +144,11 @@ inline void launch(Ctx* c, const char* name, void (*kern)(KArgs...), dim3 grid, 
 struct ScopedLibLaunch {
   Ctx* c; const char* name; cudaEvent_t a = nullptr; int n;
   ScopedLibLaunch(Ctx* ctx, const char* nm, int nkernels) : c(ctx), name(nm), n(nkernels) {
-    if (c->profiling) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
+    if (c->timed(name)) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
   }
   ~ScopedLibLaunch() {
     c->launches += n;
-    if (c->profiling) {
+    if (a) {
       cudaEvent_t b = c->take_event();
       cudaEventRecord(b, c->stream);
       c->pending.push_back({name, a, b});

@@ -114,6 +114,13 @@ int bzg_ctx_set_profiling(bzg_ctx* ctx, int enabled) {
   });
 }
 
+int bzg_ctx_profile_only(bzg_ctx* ctx, const char* kernel) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx, BZG_EINVAL, "null context");
+    ctx->profile_only = kernel ? kernel : "";
+  });
+}
+
 int bzg_ctx_stats(bzg_ctx* ctx, long long* launches, int n_cap, char* names, double* ms, long long* counts,
                   int* n_out) {
   return guarded([&] {

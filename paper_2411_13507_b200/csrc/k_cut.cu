@@ -8,6 +8,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <vector>
@@ -405,6 +407,16 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
 
   DParams dp{};
   for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
+  // BZG_TRACE=1: host wall time of each cut phase (synchronising), for diagnosing launch gaps
+  static const bool trace_on = std::getenv("BZG_TRACE") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto trace = [&](const char* what) {
+    if (!trace_on) return;
+    cudaStreamSynchronize(c->stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bzg cut] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t_prev).count());
+    t_prev = now;
+  };
   dispatch_cut(g->gamma, m, [&](auto G_, auto M_) {
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
     using Rec = ObsRec<Mc>;
@@ -442,6 +454,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
     launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
     launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
+    trace("setup");
 
     // ---- heuristic screen (obstacle chunks sized to shared memory)
     unsigned long long cap = (unsigned long long)std::max<long long>(1 << 20, E * (long long)n_obs / 32);
@@ -469,6 +482,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 8 * sizeof(unsigned long long), c->stream));
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
     }
+    trace("heuristic");
     const long long n_inst = (long long)hcnt[5];
     mk->counters[1] = (long long)hcnt[0];
     mk->counters[2] = (long long)hcnt[1];
@@ -508,10 +522,12 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       auto admm = rel ? (unit ? k_qp_admm<Gc, Mc, true, true, false> : k_qp_admm<Gc, Mc, true, false, false>)
                       : (unit ? (canon ? k_qp_admm<Gc, Mc, false, true, true> : k_qp_admm<Gc, Mc, false, true, false>)
                               : k_qp_admm<Gc, Mc, false, false, false>);
+      trace("qp alloc");
       launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, dp, g->vertices.as<double>(),
              g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), d_pend.as<unsigned long long>(), n_inst,
              d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
              d_zy.as<double>());
+      trace("admm");
       DevBuf d_list;
       d_list.alloc(n_inst * sizeof(int), c->stream);
       BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
@@ -532,6 +548,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
              dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
              d_pend.as<unsigned long long>(), d_list.as<int>(), n_list, cfg->eps_cut, d_x.as<double>(),
              d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>());
+      trace("select+polish");
       launch(c, "k_qp_verdicts", k_qp_verdicts, dim3(div_up(n_inst, 256)), dim3(256), 0,
              d_pend.as<unsigned long long>(), n_inst, d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(),
              d_cnt.as<unsigned long long>());

@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _native as nat
 from .bezier import boundary_matrix
-from .geometry import EPS_GEO, recover_box
+from .geometry import EPS_GEO, recover_box, recover_boxes  # noqa: F401
 
 _PAIR_CHUNK = 32  # kept for API parity with the reference module (graph.py:26)
 
@@ -374,29 +374,40 @@ def check_edge(oracle, x1, x2, eps: float = EPS_GEO, *, ctx=None) -> bool:
 
 
 def _obstacle_arrays(obstacles, m):
-    """Normalised rows (Polytope.normalized, geometry.py:135-137) and box recovery (as_box)."""
-    offs = [0]
-    As, bs, is_box, lo, hi = [], [], [], [], []
-    for ob in obstacles:
-        A = _f64(ob.A)
-        b = _f64(ob.b)
-        if A.ndim != 2 or A.shape[1] != m:
-            raise ValueError(f"obstacles must live in the {m}-d output space")
-        nrm = np.linalg.norm(A, axis=1)
-        An = A / nrm[:, None]
-        bn = b / nrm
-        box = recover_box(An, bn)
-        As.append(An)
-        bs.append(bn)
-        offs.append(offs[-1] + An.shape[0])
-        is_box.append(1 if box is not None else 0)
-        lo.append(box.lo if box is not None else np.zeros(m))
-        hi.append(box.hi if box is not None else np.zeros(m))
+    """Normalised rows (Polytope.normalized, geometry.py:135-137) and box recovery (as_box,
+    geometry.py:155-185), vectorised over obstacles of 2m rows (the box shape)."""
     if not obstacles:
         return (np.zeros(1, np.int32), np.zeros((0, m)), np.zeros(0), np.zeros(0, np.uint8), np.zeros((0, m)),
                 np.zeros((0, m)))
-    return (np.array(offs, np.int32), _f64(np.vstack(As)), _f64(np.concatenate(bs)), np.array(is_box, np.uint8),
-            _f64(np.vstack(lo)), _f64(np.vstack(hi)))
+    As = [np.asarray(ob.A, dtype=np.float64) for ob in obstacles]
+    bs = [np.asarray(ob.b, dtype=np.float64) for ob in obstacles]
+    for A in As:
+        if A.ndim != 2 or A.shape[1] != m:
+            raise ValueError(f"obstacles must live in the {m}-d output space")
+    O = len(As)
+    rows = np.array([A.shape[0] for A in As])
+    is_box = np.zeros(O, np.uint8)
+    lo = np.zeros((O, m))
+    hi = np.zeros((O, m))
+    An_l, bn_l = [None] * O, [None] * O
+    sq = np.nonzero(rows == 2 * m)[0]
+    if sq.size:
+        A3 = np.stack([As[i] for i in sq])
+        b2 = np.stack([bs[i] for i in sq])
+        nrm = np.linalg.norm(A3, axis=2)
+        An3 = A3 / nrm[:, :, None]
+        bn2 = b2 / nrm
+        ok, l3, h3 = recover_boxes(An3, bn2)
+        is_box[sq] = ok
+        lo[sq] = l3
+        hi[sq] = h3
+        for k, i in enumerate(sq):
+            An_l[i], bn_l[i] = An3[k], bn2[k]
+    for i in np.nonzero(rows != 2 * m)[0]:
+        nrm = np.linalg.norm(As[i], axis=1)
+        An_l[i], bn_l[i] = As[i] / nrm[:, None], bs[i] / nrm
+    offs = np.concatenate([[0], np.cumsum(rows)]).astype(np.int32)
+    return offs, _f64(np.vstack(An_l)), _f64(np.concatenate(bn_l)), is_box, _f64(lo), _f64(hi)
 
 
 def _cut_cfg(cfg) -> nat.CutConfigC:

@@ -56,6 +56,27 @@ def test_recover_box():
     assert recover_box(tri.A, tri.b) is None
 
 
+def test_obstacle_arrays_match_scalar_box_recovery():
+    """The vectorised obstacle preparation equals Polytope.normalized + as_box per obstacle."""
+    from paper_2411_13507_b200 import graph as G
+
+    rng = np.random.default_rng(3)
+    obs = list(configs.hopping_deg5(graph_n=50).obstacles)
+    obs.append(Polytope(np.array([[0.6, 0.8], [-0.8, 0.6], [-0.6, -0.8], [0.8, -0.6]]), np.ones(4)))  # rotated
+    obs.append(Polytope(np.array([[0.0, 2.0], [-3.0, 0.0], [0.0, -1.0], [1.0, 0.0]]), np.array([2.0, 3.0, 1.0, 4.0])))
+    obs.append(Polytope(np.array([[1.0, 1.0], [-1.0, 0.0], [0.0, -1.0]]), np.array([1.0, 0.0, 0.0])))  # triangle
+    obs.append(Polytope(np.array([[1.0, 1e-13], [0.0, 1.0], [-1.0, 0.0], [0.0, -1.0]]), rng.uniform(1, 2, 4)))
+    offs, A, b, is_box, lo, hi = G._obstacle_arrays(obs, 2)
+    for o, ob in enumerate(obs):
+        nrm = np.linalg.norm(ob.A, axis=1)
+        An, bn = ob.A / nrm[:, None], ob.b / nrm
+        assert A[offs[o]:offs[o + 1]].tobytes() == An.tobytes() and b[offs[o]:offs[o + 1]].tobytes() == bn.tobytes()
+        bx = recover_box(An, bn)
+        assert bool(is_box[o]) == (bx is not None)
+        if bx is not None:
+            assert lo[o].tobytes() == bx.lo.tobytes() and hi[o].tobytes() == bx.hi.tobytes()
+
+
 def _header_symbols():
     text = (ROOT / "include" / "bzg.h").read_text()
     return sorted(set(re.findall(r"\b(bzg_[a-z0-9_]+)\s*\(", text)))
