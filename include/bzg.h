@@ -93,7 +93,20 @@ typedef struct {
   /* source-row block [row_begin, row_end) of the pair matrix this call evaluates
    * (multi-GPU row sharding); row_end <= 0 means all rows */
   int64_t row_begin, row_end;
+  /* optional keep-in free regions (north-star configs 1 and 5, paper_2411_13507_b200/regions.py):
+   * region r adds rows [region_row_off[r], region_row_off[r+1]) of region_F (rows, 2n) and
+   * region_G to the base oracle; edge i->j needs the base test AND some region r whose added
+   * rows all hold.  Added rows must be one-sided (position rows of a minimal-degree curve are:
+   * the first gamma control points depend on x1 only, the last gamma on x2 only). */
+  int32_t n_regions;
+  const int32_t* region_row_off;
+  const double* region_F;
+  const double* region_G;
 } bzg_build_desc;
+
+/* the sampler alone (graph.py:147-157): N accepted states of one PCG64 stream written to a
+ * host buffer (N, n); uses desc's m, gamma, N, pcg_*, sample_lo/hi, xd_*, eps_geo */
+int bzg_sample_states(bzg_ctx* ctx, const bzg_build_desc* desc, double* out_host);
 
 /* replaces graph.build_graph (graph.py:129-199) minus k_nearest */
 int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* desc, bzg_graph** out);

@@ -38,6 +38,8 @@ class BuildDesc(C.Structure):
         ("n_include", C.c_int64), ("include", C.c_void_p),
         ("vertices", C.c_void_p),
         ("row_begin", C.c_int64), ("row_end", C.c_int64),
+        ("n_regions", C.c_int32), ("region_row_off", C.c_void_p), ("region_F", C.c_void_p),
+        ("region_G", C.c_void_p),
     ]
 
 
@@ -64,6 +66,7 @@ _SIGS = {
     "bzg_ctx_stats": ([_P, C.POINTER(C.c_longlong), C.c_int, C.c_char_p, _P, _P, C.POINTER(C.c_int)], C.c_int),
     "bzg_ctx_reset_stats": ([_P], C.c_int),
     "bzg_build_graph": ([_P, C.POINTER(BuildDesc), C.POINTER(_P)], C.c_int),
+    "bzg_sample_states": ([_P, C.POINTER(BuildDesc), _P], C.c_int),
     "bzg_graph_from_edges": ([_P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P, C.c_int64, _P, _P, _P,
                               C.c_int, C.POINTER(_P)], C.c_int),
     "bzg_graph_set_edges": ([_P, C.c_int64, _P, _P, _P, C.c_int], C.c_int),

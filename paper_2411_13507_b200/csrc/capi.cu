@@ -198,6 +198,23 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
   return rc;
 }
 
+int bzg_sample_states(bzg_ctx* ctx, const bzg_build_desc* d, double* out_host) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && d && out_host, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(d->m >= 1 && d->gamma >= 1 && d->N >= 0, BZG_EINVAL, "bad sampler dimensions");
+    BZG_REQUIRE(d->sample_lo && d->sample_hi && d->xd_A && d->xd_b, BZG_EINVAL, "sampler inputs missing");
+    set_device(ctx);
+    if (d->N == 0) return;
+    const int n = d->m * d->gamma;
+    DevBuf out;
+    out.alloc((size_t)d->N * n * sizeof(double), ctx->stream);
+    sample_states(ctx, d, out.as<double>());
+    BZG_CHECK_CUDA(cudaMemcpyAsync(out_host, out.ptr, (size_t)d->N * n * sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int bzg_graph_from_edges(bzg_ctx* ctx, int32_t m, int32_t gamma, int32_t p, const double* D, int64_t V,
                          const double* vertices_host, int64_t E, const int32_t* src, const int32_t* dst,
                          const double* cost, int on_device, bzg_graph** out) {

@@ -156,15 +156,91 @@ __global__ void k_group_bounds(const double* __restrict__ a, int transposed, lon
   gmax[t] = mx;
 }
 
-template <int K>
+// ---------------------------------------------------------------- keep-in regions
+// Region r's added rows are one-sided, so region membership is a per-vertex bit: smask (as
+// source, x1-only rows) and dmask (as destination, x2-only rows); an edge needs the base
+// test and a common region, (S_i & D_j) != 0.
+constexpr int kMaxRegionWords = 4;  // up to 256 regions
+
+struct RegionRowsDev {
+  const int* src_off;  // per region, rows [src_off[r], src_off[r+1]) of src_F / src_th
+  const double* src_F; // (rows, n): F1 part of x1-only rows
+  const double* src_th;
+  const int* dst_off;
+  const double* dst_F; // (rows, n): F2 part of x2-only rows
+  const double* dst_th;
+  int R, RW, n;
+};
+
+__global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, const int* __restrict__ perm,
+                               long long V, unsigned long long* __restrict__ smask,
+                               unsigned long long* __restrict__ dmask, uint8_t* __restrict__ src_ok,
+                               uint8_t* __restrict__ dst_ok) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= V) return;
+  const long long i = perm[s];
+  const int n = rr.n;
+  double v[kMaxN];
+  for (int k = 0; k < n; ++k) v[k] = Vx[i * n + k];
+  unsigned long long sm[kMaxRegionWords] = {0, 0, 0, 0}, dm[kMaxRegionWords] = {0, 0, 0, 0};
+  for (int r = 0; r < rr.R; ++r) {
+    int in_s = 1, in_d = 1;
+    for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q) in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
+    for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q) in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
+#pragma unroll
+    for (int w = 0; w < kMaxRegionWords; ++w) {
+      if (w == (r >> 6)) {
+        sm[w] |= (unsigned long long)in_s << (r & 63);
+        dm[w] |= (unsigned long long)in_d << (r & 63);
+      }
+    }
+  }
+  bool any_s = false, any_d = false;
+#pragma unroll
+  for (int w = 0; w < kMaxRegionWords; ++w) {
+    if (w < rr.RW) {
+      smask[s * rr.RW + w] = sm[w];
+      dmask[s * rr.RW + w] = dm[w];
+      any_s |= sm[w] != 0;
+      any_d |= dm[w] != 0;
+    }
+  }
+  if (!any_s) src_ok[s] = 0;
+  if (!any_d) dst_ok[s] = 0;
+}
+
+// OR of the masks over each 32-vertex group (tile / destination group cull)
+__global__ void k_mask_or(const unsigned long long* __restrict__ mask, const uint8_t* __restrict__ ok, long long V,
+                          int RW, unsigned long long* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long ng = (V + kTile - 1) / kTile;
+  if (t >= ng * RW) return;
+  const long long g = t / RW;
+  const int w = (int)(t - g * RW);
+  unsigned long long acc = 0;
+  for (int l = 0; l < kTile; ++l) {
+    const long long s = g * kTile + l;
+    if (s < V && ok[s]) acc |= mask[s * RW + w];
+  }
+  out[t] = acc;
+}
+
+struct RegionMasks {
+  const unsigned long long *smask, *dmask, *tile_or, *group_or;
+  int RW;
+};
+
+template <int K, bool REG>
 __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
     Bounds bd, const double* __restrict__ a1c, const double* __restrict__ a2t, const uint8_t* __restrict__ src_ok,
     const uint8_t* __restrict__ dst_ok, const int* __restrict__ perm, const double* __restrict__ tmin,
     const double* __restrict__ tmax, const double* __restrict__ gmin, const double* __restrict__ gmax, long long V,
-    long long r0, long long W, uint32_t* __restrict__ bits, unsigned long long* __restrict__ rowcnt) {
+    long long r0, long long W, uint32_t* __restrict__ bits, unsigned long long* __restrict__ rowcnt,
+    RegionMasks rm) {
   __shared__ double s_a1[kTile][K];
   __shared__ uint8_t s_ok[kTile];
   __shared__ int s_orig[kTile];
+  __shared__ unsigned long long s_sm[REG ? kTile : 1][kMaxRegionWords];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long tile = blockIdx.y;
   const long long i0 = tile * kTile;
@@ -176,10 +252,24 @@ __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
   if (tid < rows) {
     s_ok[tid] = src_ok[i0 + tid];
     s_orig[tid] = perm[i0 + tid];
+    if (REG)
+      for (int w = 0; w < kMaxRegionWords; ++w) s_sm[tid][w] = w < rm.RW ? rm.smask[(i0 + tid) * rm.RW + w] : 0ull;
   }
   __syncthreads();
   const long long g = (long long)blockIdx.x * (kPairThreads / 32) + warp;
   if (g * kTile >= V) return;
+  unsigned long long gor[kMaxRegionWords] = {0, 0, 0, 0}, dm[kMaxRegionWords] = {0, 0, 0, 0};
+  if (REG) {
+    bool share = false;
+#pragma unroll
+    for (int w = 0; w < kMaxRegionWords; ++w) {
+      if (w < rm.RW) {
+        gor[w] = rm.group_or[g * rm.RW + w];
+        share |= (gor[w] & rm.tile_or[tile * rm.RW + w]) != 0;
+      }
+    }
+    if (!share) return;  // no region holds a source of the tile and a destination of the group
+  }
   // interval bounds this lane watches in the cull tests: q = lane, lane + 32
   constexpr int QL = (K + 31) / 32;
   double gl[QL], gh[QL], lo_[QL], hi_[QL];
@@ -204,12 +294,27 @@ __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
     for (int q = 0; q < K; ++q) a2[q] = a2t[(long long)q * V + j];
     jok = dst_ok[j] != 0;
     orig_j = perm[j];
+    if (REG) {
+#pragma unroll
+      for (int w = 0; w < kMaxRegionWords; ++w) dm[w] = w < rm.RW ? rm.dmask[j * rm.RW + w] : 0ull;
+    }
   } else {
 #pragma unroll
     for (int q = 0; q < K; ++q) a2[q] = 0.0;
   }
   for (int ii = 0; ii < rows; ++ii) {
     if (!s_ok[ii]) continue;
+    bool jreg = true;
+    if (REG) {
+      bool share = false;
+      jreg = false;
+#pragma unroll
+      for (int w = 0; w < kMaxRegionWords; ++w) {
+        share |= (s_sm[ii][w] & gor[w]) != 0;
+        jreg |= (s_sm[ii][w] & dm[w]) != 0;
+      }
+      if (!share) continue;  // uniform: the source shares no region with the group
+    }
     bool c2 = false;
 #pragma unroll
     for (int u = 0; u < QL; ++u) {
@@ -220,7 +325,7 @@ __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
       }
     }
     if (__any_sync(0xffffffffu, c2)) continue;
-    bool ok = jok && (i0 + ii != j);
+    bool ok = jok && jreg && (i0 + ii != j);
 #pragma unroll
     for (int q = 0; q < K; ++q) {
       if ((q & 1) == 0 && q > 0) {
@@ -534,6 +639,60 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
          g->vertices.as<double>(), perm.as<int>(), V, Kpad, r0, r1, a1c.as<double>(), a2t.as<double>(),
          sok.as<uint8_t>(), dok.as<uint8_t>());
   const long long ng = (V + kTile - 1) / kTile;
+  // ---- keep-in regions: per-vertex membership masks from the one-sided added rows
+  RegionMasks rm{nullptr, nullptr, nullptr, nullptr, 0};
+  DevBuf r_soff, r_sF, r_sth, r_doff, r_dF, r_dth, smask, dmask, tor, gor;
+  const int R = d->n_regions;
+  if (R > 0) {
+    BZG_REQUIRE(R <= 64 * kMaxRegionWords, BZG_EUNSUPPORTED, "at most 256 keep-in regions");
+    BZG_REQUIRE(d->region_row_off && d->region_F && d->region_G, BZG_EINVAL, "region rows missing");
+    std::vector<int> soff(1, 0), doff(1, 0);
+    std::vector<double> sF, sth, dF_, dth;
+    for (int r = 0; r < R; ++r) {
+      bool never_r = false;
+      for (int q = d->region_row_off[r]; q < d->region_row_off[r + 1]; ++q) {
+        const double* f = d->region_F + (size_t)q * 2 * n;
+        bool z1 = true, z2 = true;
+        for (int k = 0; k < n; ++k) { z1 &= f[k] == 0.0; z2 &= f[n + k] == 0.0; }
+        const double th = d->region_G[q] + d->eps_geo;  // check_edges: G + eps (reachability.py:142)
+        BZG_REQUIRE(z1 || z2, BZG_EUNSUPPORTED, "a keep-in region row couples both endpoints");
+        if (z1 && z2) { never_r |= !(0.0 <= th); continue; }
+        if (z2) { sF.insert(sF.end(), f, f + n); sth.push_back(th); }
+        else { dF_.insert(dF_.end(), f + n, f + 2 * n); dth.push_back(th); }
+      }
+      if (never_r) {  // a constant row that fails: the region admits no edge
+        sF.insert(sF.end(), n, 0.0);
+        sth.push_back(-1.0);
+      }
+      soff.push_back((int)sth.size());
+      doff.push_back((int)dth.size());
+    }
+    auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+      buf.alloc(std::max<size_t>(bytes, 8), c->stream);
+      if (bytes) BZG_CHECK_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    };
+    up(r_soff, soff.data(), soff.size() * sizeof(int));
+    up(r_sF, sF.data(), sF.size() * sizeof(double));
+    up(r_sth, sth.data(), sth.size() * sizeof(double));
+    up(r_doff, doff.data(), doff.size() * sizeof(int));
+    up(r_dF, dF_.data(), dF_.size() * sizeof(double));
+    up(r_dth, dth.data(), dth.size() * sizeof(double));
+    RegionRowsDev rr{r_soff.as<int>(), r_sF.as<double>(), r_sth.as<double>(), r_doff.as<int>(), r_dF.as<double>(),
+                     r_dth.as<double>(), R, (R + 63) / 64, n};
+    smask.alloc(V * rr.RW * sizeof(unsigned long long), c->stream);
+    dmask.alloc(V * rr.RW * sizeof(unsigned long long), c->stream);
+    tor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
+    gor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
+    launch(c, "k_region_masks", k_region_masks, dim3(div_up(V, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
+           perm.as<int>(), V, smask.as<unsigned long long>(), dmask.as<unsigned long long>(), sok.as<uint8_t>(),
+           dok.as<uint8_t>());
+    launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256)), dim3(256), 0, smask.as<unsigned long long>(),
+           sok.as<uint8_t>(), V, rr.RW, tor.as<unsigned long long>());
+    launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256)), dim3(256), 0, dmask.as<unsigned long long>(),
+           dok.as<uint8_t>(), V, rr.RW, gor.as<unsigned long long>());
+    rm = RegionMasks{smask.as<unsigned long long>(), dmask.as<unsigned long long>(), tor.as<unsigned long long>(),
+                     gor.as<unsigned long long>(), rr.RW};
+  }
   DevBuf tmin, tmax, gmin, gmax;
   tmin.alloc(ng * Kpad * sizeof(double), c->stream);
   tmax.alloc(ng * Kpad * sizeof(double), c->stream);
@@ -548,18 +707,16 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
     auto go = [&](auto kern) {
       launch(c, "k_pair_tiles", kern, grid, dim3(kPairThreads), 0, bd, a1c.as<double>(), a2t.as<double>(),
              sok.as<uint8_t>(), dok.as<uint8_t>(), perm.as<int>(), tmin.as<double>(), tmax.as<double>(),
-             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>());
+             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>(), rm);
     };
+    const bool reg = R > 0;
+#define BZG_K(k) \
+  case k: if (reg) go(k_pair_tiles<k, true>); else go(k_pair_tiles<k, false>); break;
     switch (Kpad) {
-      case 4: go(k_pair_tiles<4>); break;
-      case 8: go(k_pair_tiles<8>); break;
-      case 12: go(k_pair_tiles<12>); break;
-      case 16: go(k_pair_tiles<16>); break;
-      case 24: go(k_pair_tiles<24>); break;
-      case 32: go(k_pair_tiles<32>); break;
-      case 48: go(k_pair_tiles<48>); break;
-      default: go(k_pair_tiles<64>); break;
+      BZG_K(4) BZG_K(8) BZG_K(12) BZG_K(16) BZG_K(24) BZG_K(32) BZG_K(48)
+      default: if (reg) go(k_pair_tiles<64, true>); else go(k_pair_tiles<64, false>); break;
     }
+#undef BZG_K
   }
   exclusive_scan_ll(c, rowcnt.as<unsigned long long>(), rptr.as<long long>(), rows + 1);
   long long* h = static_cast<long long*>(c->host_scratch(sizeof(long long)));

@@ -1,0 +1,158 @@
+"""Keep-in free-space polytopes (north-star extension of build_graph, configs 1 and 5).
+
+The reference has a single state set X_d (scenario.py:64).  BASELINE.json's configs 1 and 5
+ask for graphs over several convex free regions.  The semantics are frozen here, composed
+only from reference primitives (SURVEY.md §8(c) "Keep-in free polytopes"):
+
+* region r is a position-space polytope {p : A_r p <= b_r}; its state set is
+  X_d,r = Polytope([X_d.A; lift(A_r)], [X_d.b; b_r]) (lift pads the derivative columns
+  with zeros) and its oracle is build_oracle(spec, X_d,r, U, tube) (reachability.py:97);
+* vertices: per region, build_graph's sampler (graph.py:147-157) with
+  bounds = bounding_box(region) x the derivative part of the sample box, accepting in
+  X_d,r, and seed default_rng([seed, r]); regions are concatenated in order, then
+  ``include`` rows;
+* edge i -> j (i != j) iff OR_r check_edges(oracle_r, V[i], V[j]) (reachability.py:139-142,
+  the same separable arithmetic as the pair test).
+
+Every region oracle's F contains the base oracle's rows unchanged (the eroded X_d rows and
+the input rows are computed row by row by the same products), so the device test is
+base(i, j) AND OR_r region_r(i, j), where region_r covers only the rows the region adds:
+its first/last-control-point rows are per-vertex membership predicates and its interior
+rows are pair intervals.  ``region_rows`` extracts them and checks that claim bit for bit.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .geometry import Box, Polytope, bounding_box
+from .reachability import build_oracle
+
+
+def lift(region: Polytope, n: int) -> Polytope:
+    """Position-space rows padded with zeros for the derivative coordinates."""
+    A = np.asarray(region.A, dtype=np.float64)
+    return Polytope(np.hstack([A, np.zeros((A.shape[0], n - A.shape[1]))]), region.b)
+
+
+def region_state_set(xd: Polytope, region: Polytope, n: int) -> Polytope:
+    L = lift(region, n)
+    return Polytope(np.vstack([xd.A, L.A]), np.concatenate([xd.b, L.b]))
+
+
+def region_oracles(spec, xd: Polytope, U: Box, tube, regions) -> list:
+    return [build_oracle(spec, region_state_set(xd, R, spec.n), U, tube) for R in regions]
+
+
+def region_sample_bounds(region: Polytope, sample: Box, m: int) -> Box:
+    bb = bounding_box(region)
+    lo = np.concatenate([bb.lo, sample.lo[m:]])
+    hi = np.concatenate([bb.hi, sample.hi[m:]])
+    return Box(lo, hi)
+
+
+@dataclass
+class RegionRows:
+    """Rows a region adds to the base oracle: F (k, 2n) and G (k,) for each region."""
+
+    F: list
+    G: list
+
+
+def region_rows(base, oracles) -> RegionRows:
+    """Per region, the F rows (and G) that are not rows of the base oracle.
+
+    Raises if a base row is missing or differs in any bit (the device test relies on
+    base(i, j) being a factor of every region's predicate).
+    """
+    base_rows = {(tuple(f), g) for f, g in zip(np.asarray(base.F), np.asarray(base.G))}
+    Fs, Gs = [], []
+    for o in oracles:
+        F = np.asarray(o.F)
+        G = np.asarray(o.G)
+        keys = [(tuple(f), g) for f, g in zip(F, G)]
+        present = set(keys)
+        missing = [k for k in base_rows if k not in present]
+        if missing:
+            raise ValueError("a region oracle does not contain the base oracle's rows bit for bit")
+        extra = np.array([k not in base_rows for k in keys])
+        Fs.append(np.ascontiguousarray(F[extra]))
+        Gs.append(np.ascontiguousarray(G[extra]))
+    return RegionRows(Fs, Gs)
+
+
+def sample_region_states(N_per_region, spec, xd: Polytope, regions, sample: Box, seed, *, ctx=None) -> np.ndarray:
+    """Per-region samples (build_graph's sampler, default_rng([seed, r])) concatenated in region order."""
+    import ctypes as C
+
+    from . import _native as nat
+    from .graph import EPS_GEO, _f64, _pcg_words
+
+    ctx = ctx or nat.default_context()
+    counts = [N_per_region] * len(regions) if np.isscalar(N_per_region) else list(N_per_region)
+    parts = []
+    for r, (R, N) in enumerate(zip(regions, counts)):
+        bnd = region_sample_bounds(R, sample, spec.m)
+        X = region_state_set(xd, R, spec.n)
+        A, b, lo, hi = _f64(X.A), _f64(X.b), _f64(bnd.lo), _f64(bnd.hi)
+        d = nat.BuildDesc()
+        d.m, d.gamma, d.p = int(spec.m), int(spec.gamma), int(spec.p)
+        d.N = int(N)
+        d.eps_geo = EPS_GEO
+        d.pcg_state_hi, d.pcg_state_lo, d.pcg_inc_hi, d.pcg_inc_lo = _pcg_words([seed, r])
+        d.sample_lo, d.sample_hi = nat.ptr(lo), nat.ptr(hi)
+        d.xd_rows, d.xd_A, d.xd_b = A.shape[0], nat.ptr(A), nat.ptr(b)
+        out = np.empty((int(N), spec.n))
+        nat.check(ctx.lib.bzg_sample_states(ctx.handle, C.byref(d), nat.ptr(out)))
+        parts.append(out)
+    return np.vstack(parts) if parts else np.zeros((0, spec.n))
+
+
+def build_region_graph(N_per_region, spec, oracle, regions, sample: Box, seed, include=None, *, ctx=None,
+                       rows=None):
+    """Graph over several keep-in regions (module docstring); returns a ``graph.BezierGraph``.
+
+    ``oracle`` is the base ReachOracle (X_d, U, tube); ``regions`` are position-space polytopes.
+    """
+    import ctypes as C
+
+    from . import _native as nat
+    from . import graph as G
+
+    ctx = ctx or nat.default_context()
+    if sample.dim != spec.n:
+        raise ValueError(f"sampling bounds must be {spec.n}-dimensional")
+    oracles = region_oracles(spec, oracle.Xd, oracle.U, oracle.tube, regions)
+    rr = region_rows(oracle, oracles)
+    V = sample_region_states(N_per_region, spec, oracle.Xd, regions, sample, seed, ctx=ctx)
+    if V.shape[0] < 2:
+        raise ValueError("need at least two vertices")
+    d, keep, D = G._build_desc(V.shape[0], spec, oracle, sample, seed, include, vertices=V, rows=rows)
+    off = np.concatenate([[0], np.cumsum([f.shape[0] for f in rr.F])]).astype(np.int32)
+    RF = G._f64(np.vstack(rr.F)) if rr.F else np.zeros((0, 2 * spec.n))
+    RG = G._f64(np.concatenate(rr.G)) if rr.G else np.zeros(0)
+    keep += [off, RF, RG]
+    d.n_regions = len(regions)
+    d.region_row_off, d.region_F, d.region_G = nat.ptr(off), nat.ptr(RF), nat.ptr(RG)
+    h = C.c_void_p()
+    rc = ctx.lib.bzg_build_graph(ctx.handle, C.byref(d), C.byref(h))
+    if rc == nat.BZG_EINVAL:
+        raise ValueError(ctx.lib.bzg_last_error().decode())
+    nat.check(rc)
+    del keep
+    return G.BezierGraph(h, ctx, spec, oracle, seed, sample, D)
+
+
+def grid_regions(nx: int, ny: int, side_x: float, side_y: float, overlap: float = 0.10) -> list:
+    """nx x ny axis-aligned cells of the [0, side_x] x [0, side_y] map, each grown by
+    ``overlap`` of its size on every side (clipped to the map) so neighbours overlap."""
+    cw, ch = side_x / nx, side_y / ny
+    out = []
+    for iy in range(ny):
+        for ix in range(nx):
+            lo = np.array([max(0.0, (ix - overlap) * cw), max(0.0, (iy - overlap) * ch)])
+            hi = np.array([min(side_x, (ix + 1 + overlap) * cw), min(side_y, (iy + 1 + overlap) * ch)])
+            out.append(Box(lo, hi).to_polytope())
+    return out

@@ -30,6 +30,8 @@ def allgather_varlen(t, sizes, group=None):
 
     world = len(sizes)
     mx = max(int(s) for s in sizes)
+    if mx == 0:
+        return torch.zeros(0, dtype=t.dtype, device=t.device)
     pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
     pad[: t.numel()] = t
     out = torch.empty(world * mx, dtype=t.dtype, device=t.device)

@@ -233,7 +233,64 @@ def case_reject():
             full=True, detail=True)
 
 
-CASES = {"demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,
+def case_regions4(name="regions4", quads=None):
+    """cfg1: 4 overlapping quadrant keep-in regions x 50 samples, composed from reference objects
+    (SURVEY.md §8(c)): X_d,r = [X_d; lift(region)], oracle_r = build_oracle(X_d,r), sampler of
+    graph.py:147-157 with default_rng([seed, r]), edges = OR_r check_edges(oracle_r)."""
+    spec = bg.BezierSpec(m=2, gamma=2, T=1.0)
+    xd, U, sample = rsc._standard_sets()
+    tube = rsim.design_tube(spec, (6.0, 5.0), 0.02)
+    base = bg.build_oracle(spec, xd, U, tube)
+    quads = quads or [((0.0, 0.0), (3.0, 3.0)), ((2.0, 0.0), (5.0, 3.0)), ((0.0, 2.0), (3.0, 5.0)), ((2.0, 2.0), (5.0, 5.0))]
+    seed, N = 4, 50
+    parts, oracles, F_l, G_l = [], [], [], []
+    for r, (lo, hi) in enumerate(quads):
+        R = rgeo.Box(np.array(lo), np.array(hi)).to_polytope()
+        lifted = np.hstack([R.A, np.zeros((R.A.shape[0], spec.n - spec.m))])
+        Xr = rgeo.Polytope(np.vstack([xd.A, lifted]), np.concatenate([xd.b, R.b]))
+        o = bg.build_oracle(spec, Xr, U, tube)
+        oracles.append(o)
+        F_l.append(o.F)
+        G_l.append(o.G)
+        bb = rgeo.bounding_box(R)
+        bounds = rgeo.Box(np.concatenate([bb.lo, sample.lo[2:]]), np.concatenate([bb.hi, sample.hi[2:]]))
+        rng = np.random.default_rng([seed, r])  # graph.py:147-157 with the region's X_d
+        got, need = [], N
+        while need > 0:
+            cand = bounds.sample(rng, need)
+            acc = cand[Xr.contains_many(cand)]
+            if acc.size:
+                got.append(acc)
+                need -= acc.shape[0]
+        parts.append(np.vstack(got)[:N])
+    start = np.array([0.5, 0.5, 0.0, 0.0])
+    goal = np.array([4.5, 4.5, 0.0, 0.0])
+    V = np.vstack(parts + [np.array([start, goal])])
+    Vn = V.shape[0]
+    I, Jx = np.meshgrid(np.arange(Vn), np.arange(Vn), indexing="ij")
+    I, Jx = I.ravel(), Jx.ravel()
+    feas = np.zeros(I.size, dtype=bool)
+    for o in oracles:
+        feas |= bg.reachability.check_edges(o, V[I], V[Jx])
+    feas &= I != Jx
+    E = np.stack([I[feas], Jx[feas]], axis=1).astype(np.int64)
+    D = bg.bezier.boundary_matrix(spec)
+    x1 = V[E[:, 0]].reshape(-1, spec.gamma, spec.m)
+    x2 = V[E[:, 1]].reshape(-1, spec.gamma, spec.m)
+    pts = np.einsum("pq,eqm->emp", D, np.concatenate([x1, x2], axis=1))
+    costs = np.linalg.norm(np.diff(pts, axis=2), axis=1).sum(axis=1)
+    base_only = int(bg.reachability.check_edges(base, V[I], V[Jx])[I != Jx].sum())
+    np.savez_compressed(OUT / f"{name}.npz", vertices=V, edges=E, costs=costs, edge_points=pts, seed=seed,
+                        N_per=N, quads=np.array(quads, dtype=float), start=start, goal=goal,
+                        F_regions=np.stack(F_l), G_regions=np.stack(G_l), base_F=base.F, base_G=base.G, D=D,
+                        base_only_edges=base_only, env=json.dumps(env_info()))
+    print(f"{name}: V={Vn} E={E.shape[0]} (base oracle alone: {base_only})")
+
+
+CASES = {"regions4": case_regions4,
+         "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
+                                                              ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
+                                                              ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,
          "cfg2": case_cfg2, "maze": case_maze}
 
 if __name__ == "__main__":
