@@ -43,7 +43,8 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg1-demo", "cfg2", "cfg3", "cfg5"])
+    ap.add_argument("--nodes", type=int, default=0, help="cfg5: number of states (10k-100k)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="source rows in the CPU sample (0 = auto)")
@@ -58,9 +59,11 @@ def dist_env():
     return rank, world, local
 
 
-def workload(name):
+def workload(name, nodes=0):
     from paper_2411_13507_b200 import configs
 
+    if name == "cfg5" and nodes:
+        return configs.scaling_sweep(nodes)
     return configs.BUILDERS[name]()
 
 
@@ -125,8 +128,28 @@ class DeviceStep:
         self.rank, self.world = rank, world
         V = w.num_vertices
         self.rows = shard.row_block(V, rank, world) if world > 1 else None
-        self.desc, self._keep, self.D = G._build_desc(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, w.include,
-                                                       rows=self.rows)
+        regs = w.extra.get("regions")
+        if regs:
+            # keep-in regions (cfg1/cfg5): per-region samples drawn once on the device, then every step
+            # builds from those vertices (pair test over base rows AND shared region membership)
+            from paper_2411_13507_b200 import regions as R
+
+            Vh = R.sample_region_states(w.extra["per_region"], w.spec, w.oracle.Xd, regs, w.sample_bounds, w.seed,
+                                        ctx=ctx)
+            rr = R.region_rows(w.oracle, R.region_oracles(w.spec, w.oracle.Xd, w.oracle.U, w.oracle.tube, regs))
+            self.desc, self._keep, self.D = G._build_desc(Vh.shape[0], w.spec, w.oracle, w.sample_bounds, w.seed,
+                                                           w.include, vertices=Vh, rows=self.rows)
+            off = np.concatenate([[0], np.cumsum([f.shape[0] for f in rr.F])]).astype(np.int32)
+            RF, RG = G._f64(np.vstack(rr.F)), G._f64(np.concatenate(rr.G))
+            blo, bhi = R.region_boxes(regs)
+            self._keep += [off, RF, RG, blo, bhi]
+            self.desc.n_regions = len(regs)
+            self.desc.region_row_off, self.desc.region_F, self.desc.region_G = (nat_ptr(off), nat_ptr(RF),
+                                                                                nat_ptr(RG))
+            self.desc.region_box_lo, self.desc.region_box_hi = nat_ptr(blo), nat_ptr(bhi)
+        else:
+            self.desc, self._keep, self.D = G._build_desc(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, w.include,
+                                                           rows=self.rows)
         self.obs = G._obstacle_arrays(w.obstacles, w.spec.m)
         self.cfg = G._cut_cfg(G.CutConfig())
         self.last = {}
@@ -160,13 +183,25 @@ class DeviceStep:
         return path
 
 
+def nat_ptr(a):
+    from paper_2411_13507_b200 import _native as nat
+
+    return nat.ptr(a)
+
+
 def public_api_step(w, ctx, rank, world):
     """The call sequence a user makes (reference sim.plan_once order), host inputs, path read back."""
     from paper_2411_13507_b200 import graph as G
     from paper_2411_13507_b200 import shard
 
     rows = shard.row_block(w.num_vertices, rank, world) if world > 1 else None
-    g = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, include=w.include, ctx=ctx, rows=rows)
+    if w.extra.get("regions"):
+        from paper_2411_13507_b200 import regions as R
+
+        g = R.build_region_graph(w.extra["per_region"], w.spec, w.oracle, w.extra["regions"], w.sample_bounds,
+                                 w.seed, include=w.include, ctx=ctx, rows=rows)
+    else:
+        g = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, include=w.include, ctx=ctx, rows=rows)
     mask = G.cut_graph(g, w.obstacles)
     if world > 1:
         mask = shard.gather_to_all(g, mask)
@@ -256,7 +291,7 @@ def main():
     torch.cuda.set_stream(stream)
     ctx = nat.Context(local, stream=stream.cuda_stream)
     nat.set_default_context(ctx)
-    w = workload(args.config)
+    w = workload(args.config, args.nodes)
     V = w.num_vertices
     step = DeviceStep(ctx, w, rank, world)
 

@@ -102,6 +102,10 @@ typedef struct {
   const int32_t* region_row_off;
   const double* region_F;
   const double* region_G;
+  /* optional (n_regions, m) position bounding boxes of the regions, NULL = none: a vertex
+   * outside a region's box (by more than 1e-6) is not tested against its rows */
+  const double* region_box_lo;
+  const double* region_box_hi;
 } bzg_build_desc;
 
 /* the sampler alone (graph.py:147-157): N accepted states of one PCG64 stream written to a

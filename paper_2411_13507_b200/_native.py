@@ -39,7 +39,7 @@ class BuildDesc(C.Structure):
         ("vertices", C.c_void_p),
         ("row_begin", C.c_int64), ("row_end", C.c_int64),
         ("n_regions", C.c_int32), ("region_row_off", C.c_void_p), ("region_F", C.c_void_p),
-        ("region_G", C.c_void_p),
+        ("region_G", C.c_void_p), ("region_box_lo", C.c_void_p), ("region_box_hi", C.c_void_p),
     ]
 
 

@@ -140,6 +140,44 @@ def hopping_deg5(graph_n: int = 20000, n_obstacles: int = 50, seed: int = 1, obs
                     _inflated(obs, tube, spec.m), start, goal)
 
 
+def keepin_quadrants(per_region: int = 50, seed: int = 4) -> Workload:
+    """cfg1: 2D double integrator, 4 overlapping quadrant keep-in regions x 50 samples (200 states)
+    + start/goal, the demo's 3 boxes as keep-out obstacles (regions.py semantics)."""
+    w = demo(200, seed)
+    quads = [((0.0, 0.0), (3.0, 3.0)), ((2.0, 0.0), (5.0, 3.0)), ((0.0, 2.0), (3.0, 5.0)), ((2.0, 2.0), (5.0, 5.0))]
+    w.name = "cfg1-keepin-4"
+    w.N = per_region * len(quads)
+    w.extra = {"regions": [Box(np.array(lo), np.array(hi)).to_polytope() for lo, hi in quads],
+               "per_region": per_region}
+    return w
+
+
+def scaling_sweep(nodes: int = 20000, n_regions=(20, 10), n_obstacles: int = 50, seed: int = 1) -> Workload:
+    """cfg5: gamma=2 graph of `nodes` states over 200 keep-in cells (20 x 10 grid, 10% overlap) on a
+    map of side 5 sqrt(N/2000) (mean out-degree held near cfg2's), 50 random boxes."""
+    from .regions import grid_regions
+
+    spec = BezierSpec(m=2, gamma=2, T=1.0)
+    side = 5.0 * float(np.sqrt(nodes / 2000.0))
+    xd, u, sample = standard_sets(side=side)
+    tube = design_tube(spec, (6.0, 5.0), 0.02)
+    regs = grid_regions(n_regions[0], n_regions[1], side, side)
+    per = max(1, nodes // len(regs))
+    rng = np.random.default_rng(seed + 100)
+    start = np.array([0.4, 0.4, 0.0, 0.0])
+    goal = np.array([side - 0.4, side - 0.4, 0.0, 0.0])
+    obs = []
+    while len(obs) < n_obstacles:
+        c = rng.uniform(0.4, side - 0.4, 2)
+        wd = rng.uniform(0.25, 0.7, 2)
+        if np.linalg.norm(c - start[:2]) < 0.9 or np.linalg.norm(c - goal[:2]) < 0.9:
+            continue
+        obs.append(box_obstacle(c[0], c[1], wd[0], wd[1]))
+    oracle = build_oracle(spec, xd, u, tube)
+    return Workload(f"cfg5-sweep-{nodes}", spec, oracle, sample, per * len(regs), seed, np.array([start, goal]),
+                    _inflated(obs, tube, spec.m), start, goal, extra={"regions": regs, "per_region": per})
+
+
 def replanning_goals(w: Workload, count: int = 100, seed: int = 0) -> np.ndarray:
     """cfg4: goal positions U(0.3, 4.7)^2 with zero higher derivatives."""
     rng = np.random.default_rng(seed)
@@ -150,7 +188,9 @@ def replanning_goals(w: Workload, count: int = 100, seed: int = 0) -> np.ndarray
 
 
 BUILDERS = {
-    "cfg1": demo,
+    "cfg1": keepin_quadrants,
+    "cfg1-demo": demo,
     "cfg2": random_field,
     "cfg3": hopping_deg5,
+    "cfg5": scaling_sweep,
 }

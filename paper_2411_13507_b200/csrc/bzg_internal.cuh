@@ -140,6 +140,20 @@ inline void launch(Ctx* c, const char* name, void (*kern)(KArgs...), dim3 grid, 
   }
 }
 
+// Cooperative launch (all blocks co-resident, grid-wide sync allowed), counted and timed like launch().
+inline void launch_coop(Ctx* c, const char* name, const void* kern, dim3 grid, dim3 block, void** args) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  const bool timed = c->timed(name);
+  if (timed) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
+  BZG_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, grid, block, args, 0, c->stream));
+  c->launches++;
+  if (timed) {
+    b = c->take_event();
+    BZG_CHECK_CUDA(cudaEventRecord(b, c->stream));
+    c->pending.push_back({name, a, b});
+  }
+}
+
 // Record an externally launched (library) kernel group, e.g. CUB scans.
 struct ScopedLibLaunch {
   Ctx* c; const char* name; cudaEvent_t a = nullptr; int n;

@@ -172,38 +172,42 @@ struct RegionRowsDev {
   int R, RW, n;
 };
 
+// one thread per sorted vertex: regions whose (1e-6-grown) position box misses the vertex are
+// skipped (membership implies P_0 = x1 resp. P_p = x2 lies in the region), the rest are tested
+// row by row.  Masks pre-zeroed.
 __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, const int* __restrict__ perm,
-                               long long V, unsigned long long* __restrict__ smask,
-                               unsigned long long* __restrict__ dmask, uint8_t* __restrict__ src_ok,
-                               uint8_t* __restrict__ dst_ok) {
+                               long long V, int m, const double* __restrict__ blo, const double* __restrict__ bhi,
+                               unsigned long long* __restrict__ smask, unsigned long long* __restrict__ dmask) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= V) return;
   const long long i = perm[s];
   const int n = rr.n;
   double v[kMaxN];
   for (int k = 0; k < n; ++k) v[k] = Vx[i * n + k];
-  unsigned long long sm[kMaxRegionWords] = {0, 0, 0, 0}, dm[kMaxRegionWords] = {0, 0, 0, 0};
   for (int r = 0; r < rr.R; ++r) {
+    if (blo) {
+      bool inbox = true;
+      for (int k = 0; k < m; ++k) inbox &= (v[k] >= blo[r * m + k] - 1e-6) & (v[k] <= bhi[r * m + k] + 1e-6);
+      if (!inbox) continue;
+    }
     int in_s = 1, in_d = 1;
     for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q) in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
     for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q) in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
-#pragma unroll
-    for (int w = 0; w < kMaxRegionWords; ++w) {
-      if (w == (r >> 6)) {
-        sm[w] |= (unsigned long long)in_s << (r & 63);
-        dm[w] |= (unsigned long long)in_d << (r & 63);
-      }
-    }
+    const unsigned long long bit = 1ull << (r & 63);
+    if (in_s) smask[s * rr.RW + (r >> 6)] |= bit;
+    if (in_d) dmask[s * rr.RW + (r >> 6)] |= bit;
   }
+}
+
+// vertices in no region can neither start nor end an edge
+__global__ void k_region_fold(const unsigned long long* __restrict__ smask, const unsigned long long* __restrict__ dmask,
+                              long long V, int RW, uint8_t* __restrict__ src_ok, uint8_t* __restrict__ dst_ok) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= V) return;
   bool any_s = false, any_d = false;
-#pragma unroll
-  for (int w = 0; w < kMaxRegionWords; ++w) {
-    if (w < rr.RW) {
-      smask[s * rr.RW + w] = sm[w];
-      dmask[s * rr.RW + w] = dm[w];
-      any_s |= sm[w] != 0;
-      any_d |= dm[w] != 0;
-    }
+  for (int w = 0; w < RW; ++w) {
+    any_s |= smask[s * RW + w] != 0;
+    any_d |= dmask[s * RW + w] != 0;
   }
   if (!any_s) src_ok[s] = 0;
   if (!any_d) dst_ok[s] = 0;
@@ -683,9 +687,18 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
     dmask.alloc(V * rr.RW * sizeof(unsigned long long), c->stream);
     tor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
     gor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
+    BZG_CHECK_CUDA(cudaMemsetAsync(smask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
+    BZG_CHECK_CUDA(cudaMemsetAsync(dmask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
+    DevBuf rblo, rbhi;
+    if (d->region_box_lo && d->region_box_hi) {
+      up(rblo, d->region_box_lo, (size_t)R * m * sizeof(double));
+      up(rbhi, d->region_box_hi, (size_t)R * m * sizeof(double));
+    }
     launch(c, "k_region_masks", k_region_masks, dim3(div_up(V, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
-           perm.as<int>(), V, smask.as<unsigned long long>(), dmask.as<unsigned long long>(), sok.as<uint8_t>(),
-           dok.as<uint8_t>());
+           perm.as<int>(), V, m, rblo.as<double>(), rbhi.as<double>(), smask.as<unsigned long long>(),
+           dmask.as<unsigned long long>());
+    launch(c, "k_region_fold", k_region_fold, dim3(div_up(V, 256)), dim3(256), 0, smask.as<unsigned long long>(),
+           dmask.as<unsigned long long>(), V, rr.RW, sok.as<uint8_t>(), dok.as<uint8_t>());
     launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256)), dim3(256), 0, smask.as<unsigned long long>(),
            sok.as<uint8_t>(), V, rr.RW, tor.as<unsigned long long>());
     launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256)), dim3(256), 0, dmask.as<unsigned long long>(),

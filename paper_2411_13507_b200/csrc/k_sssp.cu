@@ -12,8 +12,12 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "bzg_internal.cuh"
 #include "bzg_math.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace bzg {
 
@@ -127,32 +131,44 @@ __global__ void k_reach_sweep(long long E, const int* __restrict__ src, const in
   }
 }
 
-// Frontier Bellman-Ford: one warp per vertex improved in the previous sweep relaxes its
-// alive out-edges with fl(d[u] + c) and atomicMin on the (non-negative) double bits.
-__global__ void k_bf_sweep(long long V, int sweep, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
-                           const double* __restrict__ cost, const uint8_t* __restrict__ alive,
-                           unsigned long long* __restrict__ dist, int* __restrict__ stamp,
-                           int* __restrict__ last_change) {
-  const long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+// Frontier Bellman-Ford as one persistent cooperative kernel: a queue of the vertices
+// improved in the previous sweep (each enqueued once per sweep through its stamp); one warp
+// per queued vertex relaxes its alive out-edges with fl(d[u] + c) and atomicMin on the
+// (non-negative) double bits; grid-wide barriers between sweeps; stops when a sweep improves
+// nothing.  No host round trip per sweep.
+__global__ void k_bf_persistent(long long V, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
+                                const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                                unsigned long long* __restrict__ dist, int* __restrict__ stamp, int* __restrict__ qa,
+                                int* __restrict__ qb, int* __restrict__ counts, int max_sweeps) {
+  cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
-  if (u >= V) return;
-  if (stamp[u] != sweep - 1) return;
-  const double du = __longlong_as_double((long long)dist[u]);
-  bool any = false;
-  for (long long e = row_ptr[u] + lane; e < row_ptr[u + 1]; e += 32) {
-    if (alive && !alive[e]) continue;
-    const int v = dst[e];
-    const double nd = __dadd_rn(du, cost[e]);
-    const unsigned long long nb = dbits(nd);
-    if (nb < dist[v]) {
-      const unsigned long long old = atomicMin(dist + v, nb);
-      if (nb < old) {
-        stamp[v] = sweep;
-        any = true;
+  const long long wg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const long long nw = ((long long)gridDim.x * blockDim.x) / 32;
+  int sweep = 1;
+  for (; sweep <= max_sweeps; ++sweep) {
+    const int* qin = (sweep & 1) ? qa : qb;
+    int* qout = (sweep & 1) ? qb : qa;
+    const int cin = *(volatile int*)&counts[(sweep - 1) & 1];
+    if (cin == 0) break;
+    for (long long k = wg; k < cin; k += nw) {
+      const int u = qin[k];
+      const double du = __longlong_as_double((long long)__ldcg(dist + u));
+      const long long e1 = row_ptr[u + 1];
+      for (long long e = row_ptr[u] + lane; e < e1; e += 32) {
+        if (alive && !alive[e]) continue;
+        const int v = dst[e];
+        const unsigned long long nb = dbits(__dadd_rn(du, cost[e]));
+        if (nb < __ldcg(dist + v)) {
+          const unsigned long long old = atomicMin(dist + v, nb);
+          if (nb < old && atomicExch(stamp + v, sweep) != sweep) qout[atomicAdd(counts + (sweep & 1), 1)] = v;
+        }
       }
     }
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) counts[(sweep - 1) & 1] = 0;  // consumed; reused by sweep + 1
+    grid.sync();
   }
-  if (__any_sync(0xffffffffu, any) && lane == 0) atomicMax(last_change, sweep);
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[2] = sweep - 1;
 }
 
 // parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes)
@@ -322,19 +338,29 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     launch(c, "k_init_sssp", k_init_sssp, dim3(div_up(V, 256)), dim3(256), 0, V, v0, dist, t_stamp.as<int>(), parent,
            t_pd.as<unsigned long long>());
     BZG_CHECK_CUDA(cudaMemsetAsync(t_last.ptr, 0, sizeof(int), c->stream));
-    int* h = static_cast<int*>(c->host_scratch(sizeof(int)));
-    int sweep = 1;
-    constexpr int kBatch = 8;
-    for (;;) {
-      for (int s = 0; s < kBatch; ++s, ++sweep)
-        launch(c, "k_bf_sweep", k_bf_sweep, dim3(div_up(V * 32, 256)), dim3(256), 0, V, sweep,
-               g->row_ptr.as<long long>(), g->dst.as<int>(), g->cost.as<double>(), alive, dist, t_stamp.as<int>(),
-               t_last.as<int>());
-      BZG_CHECK_CUDA(cudaMemcpyAsync(h, t_last.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-      if (h[0] < sweep - 1) break;  // the last sweep of the batch changed nothing
-      BZG_REQUIRE(sweep < V + 2 * kBatch + 2, BZG_ECUDA, "Bellman-Ford did not converge");
-    }
+    // frontier Bellman-Ford in one cooperative launch (all blocks resident)
+    DevBuf qa, qb, cnt;
+    qa.alloc(std::max(V, 1ll) * sizeof(int), c->stream);
+    qb.alloc(std::max(V, 1ll) * sizeof(int), c->stream);
+    cnt.alloc(4 * sizeof(int), c->stream);
+    const int init[4] = {1, 0, 0, 0};
+    const int v0i = (int)v0;
+    BZG_CHECK_CUDA(cudaMemcpyAsync(cnt.ptr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(qa.ptr, &v0i, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    int per_sm = 0;
+    BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bf_persistent, 256, 0));
+    const int blocks = std::max(1, std::min(per_sm, 4) * c->num_sms);
+    long long Vl = V;
+    const long long* rp = g->row_ptr.as<long long>();
+    const int* dd = g->dst.as<int>();
+    const double* cc = g->cost.as<double>();
+    int* st = t_stamp.as<int>();
+    int* pa = qa.as<int>();
+    int* pb = qb.as<int>();
+    int* pc = cnt.as<int>();
+    int maxs = (int)std::min<long long>(V + 2, 1 << 30);
+    void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &st, &pa, &pb, &pc, &maxs};
+    launch_coop(c, "k_bf_persistent", (const void*)k_bf_persistent, dim3(blocks), dim3(256), args);
     launch(c, "k_parent_dist", k_parent_dist, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(),
            g->dst.as<int>(), g->cost.as<double>(), alive, dist, t_pd.as<unsigned long long>());
     launch(c, "k_parent_idx", k_parent_idx, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(), g->dst.as<int>(),

@@ -83,6 +83,12 @@ def region_rows(base, oracles) -> RegionRows:
     return RegionRows(Fs, Gs)
 
 
+def region_boxes(regions) -> tuple[np.ndarray, np.ndarray]:
+    """(R, m) position bounding boxes (membership culling hint for the device)."""
+    boxes = [bounding_box(R) for R in regions]
+    return (np.ascontiguousarray(np.stack([b.lo for b in boxes])), np.ascontiguousarray(np.stack([b.hi for b in boxes])))
+
+
 def sample_region_states(N_per_region, spec, xd: Polytope, regions, sample: Box, seed, *, ctx=None) -> np.ndarray:
     """Per-region samples (build_graph's sampler, default_rng([seed, r])) concatenated in region order."""
     import ctypes as C
@@ -133,9 +139,11 @@ def build_region_graph(N_per_region, spec, oracle, regions, sample: Box, seed, i
     off = np.concatenate([[0], np.cumsum([f.shape[0] for f in rr.F])]).astype(np.int32)
     RF = G._f64(np.vstack(rr.F)) if rr.F else np.zeros((0, 2 * spec.n))
     RG = G._f64(np.concatenate(rr.G)) if rr.G else np.zeros(0)
-    keep += [off, RF, RG]
+    blo, bhi = region_boxes(regions)
+    keep += [off, RF, RG, blo, bhi]
     d.n_regions = len(regions)
     d.region_row_off, d.region_F, d.region_G = nat.ptr(off), nat.ptr(RF), nat.ptr(RG)
+    d.region_box_lo, d.region_box_hi = nat.ptr(blo), nat.ptr(bhi)
     h = C.c_void_p()
     rc = ctx.lib.bzg_build_graph(ctx.handle, C.byref(d), C.byref(h))
     if rc == nat.BZG_EINVAL:
