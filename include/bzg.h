@@ -151,11 +151,24 @@ typedef struct {
 /* Obstacles in list order.  Rows of obstacle o are rows [row_off[o], row_off[o+1])
  * of A (rows x m) / b, ALREADY NORMALISED (Polytope.normalized, geometry.py:135-137).
  * is_box[o] != 0 marks obstacles recovered by Polytope.as_box (geometry.py:155-185)
- * with the recovered bounds box_lo/box_hi (o*m ... o*m+m-1).  Non-box obstacles
- * return BZG_EUNSUPPORTED (the general heuristic, graph.py:202-221, is not on device yet). */
+ * with the recovered bounds box_lo/box_hi (o*m ... o*m+m-1); they take the closed-form
+ * screen (graph.py:249-264).  Other obstacles (1..8 rows) take the per-edge cut_heuristic
+ * (graph.py:202-221, projection QPs of geometry.py:202-252).  More than 8 rows:
+ * BZG_EUNSUPPORTED.  An obstacle whose projection QP certifies it empty: BZG_EINVAL
+ * (the reference raises ValueError). */
 int bzg_cut_graph(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_off, const double* A,
                   const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
                   const bzg_cut_config* cfg, bzg_mask** out);
+/* The scalar entry points on explicit control points: B sets of (m x J) control points
+ * (row-major, J = p + 1 even), set i tested against obstacle obs_index[i] of the list
+ * (same obstacle arrays as bzg_cut_graph).
+ *   mode 0 = cut_heuristic (graph.py:202-221): code[i] = 0 unsafe / 1 safe / 2 indeterminate;
+ *   mode 1 = cut_qp (graph.py:285-299): code[i] = safe flag, delta[i] = ||delta*||,
+ *            status[i] = solver status (BZG_SOLVED ...).  delta/status may be NULL. */
+int bzg_cut_points(bzg_ctx* ctx, int32_t m, int32_t J, int64_t B, const double* points, const int32_t* obs_index,
+                   int32_t n_obs, const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
+                   const double* box_lo, const double* box_hi, const bzg_cut_config* cfg, int32_t mode, int8_t* code,
+                   double* delta, int8_t* status);
 int bzg_mask_destroy(bzg_mask* mk);
 /* counters: pairs_total, pairs_point_hit, pairs_hyperplane, pairs_qp, qp_safe, qp_unsafe (graph.py:97-102) */
 int bzg_mask_copy(bzg_mask* mk, uint8_t* alive /* (E,) */, uint8_t* provenance /* (E,) */, int64_t counters[6]);

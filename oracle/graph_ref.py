@@ -150,10 +150,71 @@ def as_box(A, b):
     return lo, hi
 
 
+_PROJ_QP = AdmmSettings(max_iter=20000, eps_abs=1e-10, eps_rel=1e-10, rho=0.1, sigma=1e-6, alpha=1.6,
+                        eps_pinf=1e-4, polish=True)  # closest_point's SolveConfig (geometry.py:224)
+
+
+def closest_point(A, b, x, eps=EPS_GEO):
+    """Euclidean projection onto {A y <= b} (geometry.py:202-230): x itself when inside, the
+    box clamp for boxes, else the dense ADMM QP with polish.  Raises on an empty polytope."""
+    from .qp_ref import INFEASIBLE, _admm, _polish
+
+    x = np.asarray(x, np.float64)
+    if np.all(A @ x <= b + eps):  # Polytope.contains (geometry.py:139-143)
+        return x.copy()
+    box = as_box(A, b)
+    if box is not None:
+        return np.minimum(np.maximum(x, box[0]), box[1])  # Box.clamp
+    d = A.shape[1]
+    P = 2.0 * np.eye(d)
+    q = -2.0 * x
+    lo = np.full(A.shape[0], -np.inf)
+    u = b.copy()
+    xs, ys, st, _, rp, rd = _admm(P[None], q[None], A[None], lo[None], u[None], _PROJ_QP)
+    if st[0] == INFEASIBLE:
+        raise ValueError("cannot project onto an empty polytope")
+    xo = xs[0]
+    if st[0] in (SOLVED, 1):  # polish on SOLVED / MAX_ITER (qpsolver.py:301-303)
+        xo, _ = _polish(P, q, A, lo, u, xo, ys[0], float(rp[0]), float(rd[0]))
+    return xo
+
+
+def adjacent_hyperplane(A, b, x, eps=EPS_GEO):
+    """(unit normal, offset) of the deepest face active at the projection of x (geometry.py:233-252)."""
+    x = np.asarray(x, np.float64)
+    nrm = np.linalg.norm(A, axis=1)
+    slack = (b - A @ x) / nrm
+    if np.all(slack > eps):
+        raise ValueError("adjacent_hyperplane requires a point outside the interior")
+    y = closest_point(A, b, x, eps)
+    residual = (b - A @ y) / nrm
+    active = residual <= 1e-7
+    if not np.any(active):
+        active = np.ones(A.shape[0], dtype=bool)
+    idx = int(np.argmax(np.where(active, -slack, -np.inf)))
+    n = A[idx]
+    nn = np.linalg.norm(n)
+    return n / nn, float(b[idx]) / nn  # Hyperplane.__post_init__ (geometry.py:94-100)
+
+
+def cut_heuristic(points, A, b, eps_geo=EPS_GEO, margin=1e-6):
+    """Scalar three-branch screen of one edge (graph.py:202-221): 0 unsafe, 1 safe, 2 indeterminate."""
+    pts = np.atleast_2d(np.asarray(points, np.float64))
+    OA, Ob = normalized(A, b)
+    if np.any(np.all(pts.T @ OA.T <= Ob + eps_geo, axis=1)):  # contains_many (geometry.py:145-148)
+        return 0
+    proj = [closest_point(OA, Ob, p) for p in pts.T]
+    dists = [np.linalg.norm(pr - p) for pr, p in zip(proj, pts.T)]
+    anchor = int(np.argmin(dists))
+    normal, off = adjacent_hyperplane(OA, Ob, pts[:, anchor])
+    return 1 if np.all(normal @ pts - off > margin) else 2
+
+
 def heuristic_codes(points, A, b, eps_geo=EPS_GEO, margin=1e-6):
     """int8 codes 0 unsafe / 1 safe / 2 indeterminate for one obstacle (graph.py:224-265).
 
-    Box obstacles only (the closed-form branch); general polytopes raise.
+    Boxes take the closed-form branch; other polytopes run cut_heuristic per edge past
+    branch 1 (graph.py:242-247).
     """
     E = points.shape[0]
     OA, Ob = normalized(A, b)
@@ -167,7 +228,9 @@ def heuristic_codes(points, A, b, eps_geo=EPS_GEO, margin=1e-6):
         return codes
     box = as_box(OA, Ob)
     if box is None:
-        raise NotImplementedError("general-polytope heuristic (graph.py:243-247) is not in the oracle")
+        for e in rest:
+            codes[e] = cut_heuristic(points[e], A, b, eps_geo, margin)
+        return codes
     lo, hi = box
     pts = points[rest]
     below = np.maximum(lo[None, :, None] - pts, 0.0)

@@ -21,6 +21,10 @@ from .graph import (
     check_edge,
     check_edges,
     cut_graph,
+    cut_heuristic,
+    cut_heuristic_batch,
+    cut_qp,
+    cut_qp_batch,
     find_path,
     path_cost,
 )
@@ -32,6 +36,7 @@ __all__ = [
     "BezierSpec", "boundary_matrix", "derivative_matrix",
     "EPS_GEO", "Box", "Hyperplane", "Polytope", "bounding_box", "erode", "inflate",
     "BezierGraph", "CutConfig", "CutMask", "CutProvenance", "CutVerdict", "SolveConfig",
-    "build_graph", "check_edge", "check_edges", "cut_graph", "find_path", "path_cost",
+    "build_graph", "check_edge", "check_edges", "cut_graph", "cut_heuristic", "cut_heuristic_batch", "cut_qp",
+    "cut_qp_batch", "find_path", "path_cost",
     "ReachOracle", "TrackingTube", "build_oracle",
 ]

@@ -26,6 +26,10 @@ class BzgError(RuntimeError):
         self.code = code
 
 
+class BzgValueError(BzgError, ValueError):
+    """BZG_EINVAL: invalid input, where the reference raises ValueError."""
+
+
 class BuildDesc(C.Structure):
     _fields_ = [
         ("m", C.c_int32), ("gamma", C.c_int32), ("p", C.c_int32), ("n_F", C.c_int32),
@@ -80,6 +84,8 @@ _SIGS = {
     "bzg_graph_export_device": ([_P, _P, _P, _P], C.c_int),
     "bzg_check_edges": ([_P, C.c_int32, C.c_int32, _P, _P, C.c_double, C.c_int64, _P, _P, _P], C.c_int),
     "bzg_cut_graph": ([_P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, C.POINTER(CutConfigC), C.POINTER(_P)], C.c_int),
+    "bzg_cut_points": ([_P, C.c_int32, C.c_int32, C.c_int64, _P, _P, C.c_int32, _P, _P, _P, _P, _P, _P,
+                        C.POINTER(CutConfigC), C.c_int32, _P, _P, _P], C.c_int),
     "bzg_mask_destroy": ([_P], C.c_int),
     "bzg_mask_copy": ([_P, _P, _P, _P], C.c_int),
     "bzg_mask_qp_count": ([_P, C.POINTER(C.c_int64)], C.c_int),
@@ -122,7 +128,7 @@ def load(path: Path | str | None = None):
 def check(rc: int) -> None:
     if rc != BZG_OK:
         msg = _lib.bzg_last_error().decode(errors="replace") if _lib is not None else "?"
-        raise BzgError(rc, msg)
+        raise (BzgValueError if rc == BZG_EINVAL else BzgError)(rc, msg)
 
 
 def ptr(a: np.ndarray | None):

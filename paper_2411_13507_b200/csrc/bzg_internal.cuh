@@ -215,6 +215,10 @@ void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, doubl
 void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
                const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
                Mask* mk);
+void cut_points(Ctx* c, int m, int J, long long B, const double* points, const int32_t* obs_index, int n_obs,
+                const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
+                const double* box_hi, const bzg_cut_config* cfg, int mode, int8_t* code_out, double* delta_out,
+                int8_t* status_out);
 void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
                const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
                double* dist);

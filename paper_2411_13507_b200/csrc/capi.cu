@@ -360,6 +360,20 @@ int bzg_cut_graph(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_
   return rc;
 }
 
+int bzg_cut_points(bzg_ctx* ctx, int32_t m, int32_t J, int64_t B, const double* points, const int32_t* obs_index,
+                   int32_t n_obs, const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
+                   const double* box_lo, const double* box_hi, const bzg_cut_config* cfg, int32_t mode, int8_t* code,
+                   double* delta, int8_t* status) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && cfg && code && (B == 0 || (points && obs_index)), BZG_EINVAL, "null argument");
+    BZG_REQUIRE(row_off && A && b && is_box && box_lo && box_hi, BZG_EINVAL, "obstacle arrays missing");
+    BZG_REQUIRE(m >= 1 && m <= 3, BZG_EUNSUPPORTED, "device cut supports m in 1..3");
+    set_device(ctx);
+    cut_points(ctx, m, J, B, points, obs_index, n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg, mode, code, delta,
+               status);
+  });
+}
+
 int bzg_mask_destroy(bzg_mask* mk) {
   return guarded([&] {
     if (!mk) return;

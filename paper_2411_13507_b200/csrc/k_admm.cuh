@@ -24,10 +24,10 @@ namespace {
 
 constexpr int kAdmmBatch = 8;
 
-template <int G, int M>
-__device__ __forceinline__ void admm_setup(double (&Q)[2 * M][2 * G], double (&Si)[G * (2 * G + 1)], double rho,
+template <int G, int M, int C>
+__device__ __forceinline__ void admm_setup(double (&Q)[C][2 * G], double (&Si)[G * (2 * G + 1)], double rho,
                                            double req, double sig, double ikdd) {
-  constexpr int J = 2 * G, C = 2 * M;
+  constexpr int J = 2 * G;
   const double kap = rho - rho * rho * ikdd;
   double L[J][J], dinv[J];
 #pragma unroll
@@ -92,9 +92,9 @@ __device__ __forceinline__ double clip_nonneg(double t) { return __double_as_lon
 // Constraint-matrix products of the cut QP.  Q = A_O P (C x J).  For a canonical box
 // (A_O = [I; -I], Box.to_polytope order) Q = [P; -P] exactly, so only the M rows of P are
 // kept and every product is formed once per output dimension.
-template <int G, int M, bool CANON>
+template <int G, int M, int C, bool CANON>
 struct QOps {
-  static constexpr int J = 2 * G, C = 2 * M, R = CANON ? M : C;
+  static constexpr int J = 2 * G, R = CANON ? M : C;
   double q[R][J];
   __device__ __forceinline__ void load(const double (&Q)[C][J]) {
 #pragma unroll
@@ -134,7 +134,7 @@ struct QOps {
 // REL: eps_rel != 0 (termination tolerances depend on the iterate, qpsolver.py:181-186)
 // UNIT: rho == 1 (CutConfig default) -- the multiplications by rho and 1/rho are exact and skipped
 // CANON: every obstacle is a canonical box (see QOps)
-template <int G, int M, bool REL, bool UNIT, bool CANON>
+template <int G, int M, int C, bool REL, bool UNIT, bool CANON>
 __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, const double* __restrict__ Vx,
                                                  const int* __restrict__ src, const int* __restrict__ dst,
                                                  const ObsRec<M>* __restrict__ obs,
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, con
                                                  unsigned long long* __restrict__ next, int8_t* __restrict__ st_out,
                                                  int* __restrict__ it_out, double* __restrict__ x_out,
                                                  double* __restrict__ zy_out) {
-  constexpr int J = 2 * G, C = 2 * M, NV = J + C, MC = C + J + 1;
+  constexpr int J = 2 * G, NV = J + C, MC = C + J + 1;
   const int lane = threadIdx.x & 31;
   const double rho = UNIT ? 1.0 : qp.rho, req = qp.rho_eq, ri = UNIT ? 1.0 : 1.0 / qp.rho;
   const double sig = qp.sigma, al = qp.alpha, oma = qp.one_m_alpha, eps = qp.eps_abs;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, con
 
   long long inst = -1;  // -1 needs work, -2 exhausted
   int it = 0;
-  QOps<G, M, CANON> Q;
+  QOps<G, M, C, CANON> Q;
   double Si[J * (J + 1) / 2], b[C];
   double lam[J], del[C], zc[C], zl[J], ze, yc[C], yl[J], ye;
 #define SI(r, s) Si[(r) >= (s) ? (r) * ((r) + 1) / 2 + (s) : (s) * ((s) + 1) / 2 + (r)]
@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, con
         inst = (long long)my < n_inst ? (long long)my : -2;
         if (inst >= 0) {
           double Qf[C][J];
-          load_instance<G, M>(dp, Vx, src, dst, obs, pend[inst], Qf, b);
-          admm_setup<G, M>(Qf, Si, rho, req, sig, ikdd);
+          load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[inst], Qf, b);
+          admm_setup<G, M, C>(Qf, Si, rho, req, sig, ikdd);
           Q.load(Qf);
         }
 #pragma unroll
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, con
         tC[c] = __fma_rn(kp, rdel[c], wc);
       }
       const double we = __fma_rn(req, ze, -ye);
-      double rv[J], fT[QOps<G, M, CANON>::R];
+      double rv[J], fT[QOps<G, M, C, CANON>::R];
       Q.fold(tC, fT);
 #pragma unroll
       for (int j = 0; j < J; ++j) {
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, DParams dp, con
           conv &= fabs(r) <= eps;
         }
       }
-      double fY[QOps<G, M, CANON>::R];
+      double fY[QOps<G, M, C, CANON>::R];
       Q.fold(yc, fY);
 #pragma unroll
       for (int j = 0; j < J; ++j) {

@@ -26,18 +26,44 @@ struct DParams {
   double D[64];
 };
 
-// Per-obstacle record staged in shared memory (box obstacles only).
+// Rows an obstacle may have on device (boxes have 2m; general polytopes up to this).
+constexpr int kObsRows = 8;
+
+// Per-obstacle record staged in shared memory.  Rows past `rows` are padding (A = 0,
+// b = 1e300): inert in every test and in the Cut-QP (k_qp_common.cuh).
 template <int M>
 struct ObsRec {
-  double A[2 * M][M];   // normalised rows (geometry.py:135-137)
-  double b[2 * M];
-  double b_eps[2 * M];  // fl(b + eps_geo)   (graph.py:234)
-  double lo[M], hi[M];  // Polytope.as_box bounds (geometry.py:155-185)
-  double canon;         // 1 when A == [I; -I] exactly (Box.to_polytope row order)
-  double act_hi[M];     // hi - 1e-6: a point below it cannot make face +k active
-  double act_lo[M];     // lo + 1e-6
-  double thin[M];       // 1 when hi - lo <= 1e-6 (both faces of axis k may be active)
+  double A[kObsRows][M];   // normalised rows (geometry.py:135-137)
+  double b[kObsRows];
+  double b_eps[kObsRows];  // fl(b + eps_geo)   (graph.py:234)
+  double norm2[kObsRows];  // row norms of the normalised rows (Polytope._row_norms of O)
+  double lo[M], hi[M];     // Polytope.as_box bounds (geometry.py:155-185)
+  double canon;            // 1 when A == [I; -I] exactly (Box.to_polytope row order)
+  double act_hi[M];        // hi - 1e-6: a point below it cannot make face +k active
+  double act_lo[M];        // lo + 1e-6
+  double thin[M];          // 1 when hi - lo <= 1e-6 (both faces of axis k may be active)
+  double rows;             // constraint rows
+  double is_box;           // 1 when as_box() recovers a box (the closed-form branch applies)
 };
+
+// Branch 1 of _heuristic_batch (graph.py:236-239): einsum("cm,emj->ecj"), sequential from 0.
+template <int G, int M>
+__device__ __forceinline__ bool any_inside_einsum(const double (&P)[M][2 * G], const ObsRec<M>& o) {
+  const int R = (int)o.rows;
+  bool hit = false;
+#pragma unroll
+  for (int j = 0; j < 2 * G; ++j) {
+    bool in = true;
+    for (int c = 0; c < R; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) acc = __dadd_rn(acc, __dmul_rn(o.A[c][k], P[k][j]));
+      in = in && (acc <= o.b_eps[c]);
+    }
+    hit = hit || in;
+  }
+  return hit;
+}
 
 // Exact certificate that box_code_canon returns 1 (safe), from the bounding box
 // [mn, mx] of the control points.  (1) No control point is inside when, for some axis,
@@ -210,12 +236,31 @@ __device__ __forceinline__ int box_code_canon(const double (&P)[M][2 * G], const
 // One thread per edge, all obstacles of the chunk [o0, o1) in list order.
 // Tracks the first heuristic kill, counts codes, and appends indeterminate pairs
 // to the QP work list with warp-aggregated atomics.
+// Pairs with a general (non-box) obstacle that pass branch 1 go to a second work list
+// (gen_pend) for k_cut_general, so the projection QPs do not weigh on this kernel.
+__device__ __forceinline__ void warp_append(bool want_me, unsigned long long item, unsigned long long* n,
+                                            unsigned long long cap, unsigned long long* list) {
+  const unsigned am = __activemask();
+  const unsigned want = __ballot_sync(am, want_me);
+  if (!want) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  const int leader = __ffs(want) - 1;
+  if (lane == leader) base = atomicAdd(n, (unsigned long long)__popc(want));
+  base = __shfl_sync(am, base, leader);
+  if (want_me) {
+    const unsigned long long slot = base + __popc(want & ((1u << lane) - 1u));
+    if (slot < cap) list[slot] = item;
+  }
+}
+
 template <int G, int M>
 __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
                                 const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs, int o0, int o1,
                                 double margin, int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                                 unsigned long long* __restrict__ n_pend, unsigned long long cap,
-                                unsigned long long* __restrict__ pend) {
+                                unsigned long long* __restrict__ pend, unsigned long long* __restrict__ n_gen,
+                                unsigned long long gen_cap, unsigned long long* __restrict__ gen_pend) {
   constexpr int N = G * M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ObsRec<M>* s_obs = reinterpret_cast<ObsRec<M>*>(smem_raw);
@@ -243,7 +288,6 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
     kill = first_kill[e];
   }
   unsigned c0 = 0, c1 = 0, c2 = 0;
-  const int lane = threadIdx.x & 31;
   // pass 1 (coherent across the warp): certify code 1 from the control-polygon bounding box
   unsigned long long hard = 0;
   if (valid) {
@@ -265,24 +309,17 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
   while (hard) {
     const int oi = __ffsll((long long)hard) - 1;
     hard &= hard - 1;
-    const int code = s_obs[oi].canon != 0.0 ? box_code_canon<G, M>(P, s_obs[oi], margin)
-                                            : box_code<G, M>(P, s_obs[oi], margin);
+    const ObsRec<M>& o = s_obs[oi];
+    int code;
+    if (o.is_box == 0.0) code = any_inside_einsum<G, M>(P, o) ? 0 : 3;  // 3: decided by k_cut_general
+    else code = o.canon != 0.0 ? box_code_canon<G, M>(P, o, margin) : box_code<G, M>(P, o, margin);
     c0 += code == 0;
     c1 += code == 1;
     c2 += code == 2;
     if (code == 0 && kill > o0 + oi) kill = o0 + oi;
-    const unsigned am = __activemask();
-    const unsigned want = __ballot_sync(am, code == 2);
-    if (want) {
-      unsigned long long base = 0;
-      const int leader = __ffs(want) - 1;
-      if (lane == leader) base = atomicAdd(n_pend, (unsigned long long)__popc(want));
-      base = __shfl_sync(am, base, leader);
-      if (code == 2) {
-        const unsigned long long slot = base + __popc(want & ((1u << lane) - 1u));
-        if (slot < cap) pend[slot] = ((unsigned long long)e << 20) | (unsigned long long)(o0 + oi);
-      }
-    }
+    const unsigned long long item = ((unsigned long long)e << 20) | (unsigned long long)(o0 + oi);
+    warp_append(code == 2, item, n_pend, cap, pend);
+    warp_append(code == 3, item, n_gen, gen_cap, gen_pend);
   }
   if (valid) first_kill[e] = kill;
   // block reduction of the three counters
@@ -306,9 +343,48 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
 #include "k_qp_common.cuh"
 #include "k_admm.cuh"
 #include "k_polish.cuh"
+#include "k_general.cuh"
 
 namespace bzg {
 namespace {
+
+constexpr double kEpsGeo = 1e-9;  // geometry.EPS_GEO (geometry.py:14), closest_point's default eps
+
+// cut_heuristic past branch 1 (graph.py:242-247 -> 202-221) for the general-obstacle pairs,
+// one thread per pair.  Same bookkeeping as k_cut_heuristic: first kill by atomicMin, codes
+// counted, indeterminate pairs appended to the QP work list.  counters[7] flags an
+// obstacle whose projection QP certified it empty (the reference raises ValueError).
+template <int G, int M>
+__global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const int* __restrict__ src,
+                              const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
+                              const unsigned long long* __restrict__ gen, long long n, double margin,
+                              int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
+                              unsigned long long* __restrict__ n_pend, unsigned long long cap,
+                              unsigned long long* __restrict__ pend, int8_t* __restrict__ code_out) {
+  constexpr int N = G * M;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int code = -2;
+  unsigned long long item = 0;
+  if (t < n) {
+    item = gen[t];
+    const long long e = (long long)(item >> 20);
+    const int oi = (int)(item & 0xFFFFF);
+    double xi[N], xj[N], P[M][2 * G];
+    const long long a = src[e], c = dst[e];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      xi[k] = Vx[a * N + k];
+      xj[k] = Vx[c * N + k];
+    }
+    control_points<G, M>(xi, xj, dp.D, P);
+    code = general_code<G, M>(P, obs[oi], margin, kEpsGeo);
+    if (code == 0) atomicMin(first_kill + e, oi);
+    if (code >= 0) atomicAdd(counters + code, 1ull);
+    if (code == -1) atomicOr(counters + 7, 1ull);
+    if (code_out) code_out[t] = (int8_t)code;
+  }
+  warp_append(code == 2, item, n_pend, cap, pend);
+}
 
 // ------------------------------------------------------------------ aggregation
 __global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long long n_inst,
@@ -379,6 +455,127 @@ void dispatch_cut(int G, int M, F&& f) {
   throw Error(BZG_EUNSUPPORTED, "device cut supports gamma in 1..3 and m in 1..3");
 }
 
+// Device records of the obstacle list; rows normalised by the caller (geometry.py:135-137).
+template <int M>
+std::vector<ObsRec<M>> fill_obs(int n_obs, const int32_t* row_off, const double* A, const double* b,
+                                const uint8_t* is_box, const double* box_lo, const double* box_hi, double eps_geo) {
+  std::vector<ObsRec<M>> h(std::max(n_obs, 1));
+  for (int o = 0; o < n_obs; ++o) {
+    ObsRec<M>& r = h[o];
+    const int rows = row_off[o + 1] - row_off[o];
+    r.rows = rows;
+    r.is_box = is_box[o] ? 1.0 : 0.0;
+    for (int q = 0; q < kObsRows; ++q) {
+      const int row = row_off[o] + q;
+      double s = 0.0;
+      for (int k = 0; k < M; ++k) {
+        r.A[q][k] = q < rows ? A[(size_t)row * M + k] : 0.0;
+        const double sq = r.A[q][k] * r.A[q][k];
+        s = k == 0 ? sq : s + sq;  // np.linalg.norm(axis=1): left fold of the squares
+      }
+      r.norm2[q] = q < rows ? std::sqrt(s) : 1.0;
+      r.b[q] = q < rows ? b[row] : 1e300;
+      r.b_eps[q] = q < rows ? b[row] + eps_geo : 1e300;  // O.b + eps_geo (graph.py:234)
+    }
+    for (int k = 0; k < M; ++k) {
+      r.lo[k] = box_lo[(size_t)o * M + k];
+      r.hi[k] = box_hi[(size_t)o * M + k];
+    }
+    bool canon = is_box[o] != 0;
+    for (int q = 0; q < 2 * M; ++q)
+      for (int k = 0; k < M; ++k) canon = canon && r.A[q][k] == (k == (q % M) ? (q < M ? 1.0 : -1.0) : 0.0);
+    r.canon = canon ? 1.0 : 0.0;
+    for (int k = 0; k < M; ++k) {
+      r.act_hi[k] = r.hi[k] - 1e-6;
+      r.act_lo[k] = r.lo[k] + 1e-6;
+      r.thin[k] = (r.hi[k] - r.lo[k] > 1e-6) ? 0.0 : 1.0;
+    }
+  }
+  return h;
+}
+
+// Batched Cut-QP over the work list pend[0 .. n_inst) (graph.py:320-337 / cut_qp 285-299):
+// ADMM, verdict selection, polish.  Fills mk->qp_status / qp_iters / qp_delta / n_polished
+// and d_safe (n_inst verdicts).  polish_mode: 0 none, 1 SOLVED, 2 SOLVED and MAX_ITER.
+template <int G, int M, int C, typename Trace>
+void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs, bool canon,
+              const unsigned long long* d_pend, long long n_inst, const bzg_cut_config* cfg, int polish_mode,
+              double screen, Mask* mk, DevBuf& d_safe, Trace&& trace) {
+  constexpr int NV = 2 * G + C, MCc = C + 2 * G + 1;
+  mk->qp_status.alloc(n_inst, c->stream);
+  mk->qp_iters.alloc(n_inst * sizeof(int), c->stream);
+  mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
+  DevBuf d_x, d_res, d_next, d_zy, d_list;
+  d_x.alloc(n_inst * NV * sizeof(double), c->stream);
+  d_res.alloc(n_inst * 2 * sizeof(double), c->stream);
+  d_safe.alloc(n_inst, c->stream);
+  d_next.alloc(sizeof(unsigned long long), c->stream);
+  d_zy.alloc(n_inst * 2 * MCc * sizeof(double), c->stream);
+  d_list.alloc(n_inst * sizeof(int), c->stream);
+  BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
+  QpParams qp{};
+  qp.rho = cfg->qp_rho;
+  qp.rho_eq = cfg->qp_rho * 1e3;  // equality rows (qpsolver.py:100-103, 137)
+  qp.sigma = cfg->qp_sigma;
+  qp.alpha = cfg->qp_alpha;
+  qp.one_m_alpha = 1.0 - cfg->qp_alpha;
+  qp.eps_abs = cfg->qp_eps_abs;
+  qp.eps_rel = cfg->qp_eps_rel;
+  qp.eps_pinf = cfg->qp_eps_pinf;
+  qp.max_iter = cfg->qp_max_iter;
+  // persistent grid: enough resident warps to cover the SMs several times
+  const long long blocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 16);
+  const bool rel = cfg->qp_eps_rel != 0.0, unit = cfg->qp_rho == 1.0;
+  auto admm = rel ? (unit ? k_qp_admm<G, M, C, true, true, false> : k_qp_admm<G, M, C, true, false, false>)
+                  : (unit ? k_qp_admm<G, M, C, false, true, false> : k_qp_admm<G, M, C, false, false, false>);
+  if constexpr (C == 2 * M)
+    if (canon && unit && !rel) admm = k_qp_admm<G, M, C, false, true, true>;
+  trace("qp alloc");
+  launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, dp, g->vertices.as<double>(),
+         g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, d_next.as<unsigned long long>(),
+         mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(), d_zy.as<double>());
+  trace("admm");
+  BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
+  launch(c, "k_qp_select", k_qp_select<G, M, C>, dim3(div_up(n_inst, 256)), dim3(256), 0, dp,
+         g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, polish_mode, screen,
+         cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(), d_zy.as<double>(), d_res.as<double>(),
+         mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
+  unsigned long long* hn = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long))) + 7;
+  BZG_CHECK_CUDA(cudaMemcpyAsync(hn, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  const long long n_list = (long long)*hn;
+  mk->n_polished = n_list;
+  constexpr int NR = polish_dim<G, M, C>();
+  const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
+  BZG_CHECK_CUDA(cudaFuncSetAttribute(k_qp_polish<G, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+  launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
+         dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
+         cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
+         mk->qp_status.as<int8_t>());
+  trace("select+polish");
+}
+
+// Validates the obstacle list; returns the padded row count of a Cut-QP launch
+// (2m when every obstacle fits, else kObsRows).
+int check_obstacles(int n_obs, const int32_t* row_off, const uint8_t* is_box, int m) {
+  int max_rows = 2 * m;
+  for (int o = 0; o < n_obs; ++o) {
+    const int rows = row_off[o + 1] - row_off[o];
+    BZG_REQUIRE(rows >= 1 && rows <= kObsRows, BZG_EUNSUPPORTED,
+                "obstacle " + std::to_string(o) + " has " + std::to_string(rows) + " rows; the device cut takes 1.." +
+                    std::to_string(kObsRows));
+    BZG_REQUIRE(!is_box[o] || rows == 2 * m, BZG_EINVAL, "box obstacle must have 2m rows");
+    max_rows = std::max(max_rows, rows);
+  }
+  return max_rows <= 2 * m ? 2 * m : kObsRows;
+}
+
+template <int M, typename F>
+void dispatch_rows(int qp_rows, F&& f) {
+  if (qp_rows <= 2 * M) f(std::integral_constant<int, 2 * M>{});
+  else if constexpr (2 * M < kObsRows) f(std::integral_constant<int, kObsRows>{});
+}
+
 }  // namespace
 
 void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
@@ -388,12 +585,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
   const int m = g->m;
   BZG_REQUIRE(n_obs >= 0 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
   BZG_REQUIRE(E < (1ll << 43), BZG_EUNSUPPORTED, "edge count too large for the QP work list");
-  for (int o = 0; o < n_obs; ++o) {
-    BZG_REQUIRE(is_box[o], BZG_EUNSUPPORTED,
-                "obstacle " + std::to_string(o) + " is not an axis-aligned box: the general-polytope "
-                "heuristic (graph.py:202-221) is not implemented on device");
-    BZG_REQUIRE(row_off[o + 1] - row_off[o] == 2 * m, BZG_EINVAL, "box obstacle must have 2m rows");
-  }
+  const int qp_rows = check_obstacles(n_obs, row_off, is_box, m);
   mk->g = g;
   mk->E = E;
   mk->n_obs = n_obs;
@@ -420,29 +612,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
   dispatch_cut(g->gamma, m, [&](auto G_, auto M_) {
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
     using Rec = ObsRec<Mc>;
-    std::vector<Rec> h(std::max(n_obs, 1));
-    for (int o = 0; o < n_obs; ++o) {
-      Rec& r = h[o];
-      for (int q = 0; q < 2 * Mc; ++q) {
-        const int row = row_off[o] + q;
-        for (int k = 0; k < Mc; ++k) r.A[q][k] = A[(size_t)row * Mc + k];
-        r.b[q] = b[row];
-        r.b_eps[q] = b[row] + cfg->eps_geo;  // O.b + eps_geo (graph.py:234)
-      }
-      for (int k = 0; k < Mc; ++k) {
-        r.lo[k] = box_lo[(size_t)o * Mc + k];
-        r.hi[k] = box_hi[(size_t)o * Mc + k];
-      }
-      bool canon = true;
-      for (int q = 0; q < 2 * Mc; ++q)
-        for (int k = 0; k < Mc; ++k) canon = canon && r.A[q][k] == (k == (q % Mc) ? (q < Mc ? 1.0 : -1.0) : 0.0);
-      r.canon = canon ? 1.0 : 0.0;
-      for (int k = 0; k < Mc; ++k) {
-        r.act_hi[k] = r.hi[k] - 1e-6;
-        r.act_lo[k] = r.lo[k] + 1e-6;
-        r.thin[k] = (r.hi[k] - r.lo[k] > 1e-6) ? 0.0 : 1.0;
-      }
-    }
+    const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
     DevBuf d_obs, d_kill, d_qkill, d_saved, d_cnt;
     d_obs.alloc(sizeof(Rec) * h.size(), c->stream);
     BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, h.data(), sizeof(Rec) * h.size(), cudaMemcpyHostToDevice, c->stream));
@@ -458,27 +628,43 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
 
     // ---- heuristic screen (obstacle chunks sized to shared memory)
     unsigned long long cap = (unsigned long long)std::max<long long>(1 << 20, E * (long long)n_obs / 32);
-    DevBuf d_pend;
+    bool any_general = false;
+    for (int o = 0; o < n_obs; ++o) any_general |= h[o].is_box == 0.0;
+    unsigned long long gen_cap = any_general ? cap : 1;
+    DevBuf d_pend, d_gen;
     unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
+    unsigned long long* dcnt = d_cnt.as<unsigned long long>();
     // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
     const int chunk = std::min(64, std::max(1, (int)(96 * 1024 / sizeof(Rec))));
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
       d_pend.alloc(cap * sizeof(unsigned long long), c->stream);
+      d_gen.alloc(gen_cap * sizeof(unsigned long long), c->stream);
       for (int o0 = 0; o0 < n_obs; o0 += chunk) {
         const int o1 = std::min(n_obs, o0 + chunk);
         const size_t smem = sizeof(Rec) * (o1 - o0);
         auto kern = k_cut_heuristic<Gc, Mc>;
         BZG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         launch(c, "k_cut_heuristic", kern, dim3(div_up(E, 256)), dim3(256), smem, dp, g->vertices.as<double>(), E,
-               g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), o0, o1, cfg->heur_margin, d_kill.as<int>(),
-               d_cnt.as<unsigned long long>(), d_cnt.as<unsigned long long>() + 5, cap,
-               d_pend.as<unsigned long long>());
+               g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), o0, o1, cfg->heur_margin, d_kill.as<int>(), dcnt,
+               dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>());
       }
       BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
       BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-      if (hcnt[5] <= cap) break;
-      // work list overflowed: grow it and rerun the screen from a clean state
-      cap = hcnt[5] + 1024;
+      const unsigned long long n_gen = hcnt[6];
+      if (n_gen > 0 && n_gen <= gen_cap) {
+        // general obstacles: cut_heuristic past branch 1, appending to the same QP work list
+        launch(c, "k_cut_general", k_cut_general<Gc, Mc>, dim3(div_up((long long)n_gen, 64)), dim3(64), 0, dp,
+               g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
+               d_gen.as<unsigned long long>(), (long long)n_gen, cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5,
+               cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr);
+        BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      }
+      BZG_REQUIRE(hcnt[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
+      if (hcnt[5] <= cap && n_gen <= gen_cap) break;
+      // a work list overflowed: grow it and rerun the screen from a clean state
+      cap = std::max(cap, hcnt[5] + 1024);
+      if (n_gen > gen_cap) gen_cap = n_gen + 1024;
       BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 8 * sizeof(unsigned long long), c->stream));
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
     }
@@ -490,65 +676,13 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
 
     // ---- QP fallback on every indeterminate pair (graph.py:320-337)
     mk->n_qp = n_inst;
-    if (n_inst > 0) {
-      constexpr int NV = 2 * Gc + 2 * Mc;
-      mk->qp_status.alloc(n_inst, c->stream);
-      mk->qp_iters.alloc(n_inst * sizeof(int), c->stream);
-      mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
-      DevBuf d_x, d_res, d_safe, d_next;
-      d_x.alloc(n_inst * NV * sizeof(double), c->stream);
-      d_res.alloc(n_inst * 2 * sizeof(double), c->stream);
-      d_safe.alloc(n_inst, c->stream);
-      d_next.alloc(sizeof(unsigned long long), c->stream);
-      BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
-      QpParams qp{};
-      qp.rho = cfg->qp_rho;
-      qp.rho_eq = cfg->qp_rho * 1e3;  // equality rows (qpsolver.py:100-103, 137)
-      qp.sigma = cfg->qp_sigma;
-      qp.alpha = cfg->qp_alpha;
-      qp.one_m_alpha = 1.0 - cfg->qp_alpha;
-      qp.eps_abs = cfg->qp_eps_abs;
-      qp.eps_rel = cfg->qp_eps_rel;
-      qp.eps_pinf = cfg->qp_eps_pinf;
-      qp.max_iter = cfg->qp_max_iter;
-      // persistent grid: enough resident warps to cover the SMs several times
-      const long long blocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 16);
-      constexpr int MCc = 2 * Mc + 2 * Gc + 1;
-      DevBuf d_zy;
-      d_zy.alloc(n_inst * 2 * MCc * sizeof(double), c->stream);
-      const bool rel = cfg->qp_eps_rel != 0.0, unit = cfg->qp_rho == 1.0;
-      bool canon = true;
-      for (int o = 0; o < n_obs; ++o) canon = canon && h[o].canon != 0.0;
-      auto admm = rel ? (unit ? k_qp_admm<Gc, Mc, true, true, false> : k_qp_admm<Gc, Mc, true, false, false>)
-                      : (unit ? (canon ? k_qp_admm<Gc, Mc, false, true, true> : k_qp_admm<Gc, Mc, false, true, false>)
-                              : k_qp_admm<Gc, Mc, false, false, false>);
-      trace("qp alloc");
-      launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, dp, g->vertices.as<double>(),
-             g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), d_pend.as<unsigned long long>(), n_inst,
-             d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
-             d_zy.as<double>());
-      trace("admm");
-      DevBuf d_list;
-      d_list.alloc(n_inst * sizeof(int), c->stream);
-      BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
-      launch(c, "k_qp_select", k_qp_select<Gc, Mc>, dim3(div_up(n_inst, 256)), dim3(256), 0, dp,
-             g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
-             d_pend.as<unsigned long long>(), n_inst, (int)cfg->qp_polish, polish_screen(), cfg->eps_cut,
-             mk->qp_status.as<int8_t>(), d_x.as<double>(), d_zy.as<double>(), d_res.as<double>(),
-             mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
-      BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt + 6, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                     c->stream));
-      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-      const long long n_list = (long long)hcnt[6];
-      mk->n_polished = n_list;
-      constexpr int NR = polish_dim<Gc, Mc>();
-      const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
-      BZG_CHECK_CUDA(cudaFuncSetAttribute(k_qp_polish<Gc, Mc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-      launch(c, "k_qp_polish", k_qp_polish<Gc, Mc>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
-             dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
-             d_pend.as<unsigned long long>(), d_list.as<int>(), n_list, cfg->eps_cut, d_x.as<double>(),
-             d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>());
-      trace("select+polish");
+    bool canon_all = true;
+    for (int o = 0; o < n_obs; ++o) canon_all = canon_all && h[o].canon != 0.0;
+    auto run_qp = [&](auto C_) {
+      constexpr int Cc = decltype(C_)::value;
+      DevBuf d_safe;
+      qp_solve<Gc, Mc, Cc>(c, g, dp, d_obs.as<Rec>(), canon_all, d_pend.as<unsigned long long>(), n_inst, cfg,
+                           cfg->qp_polish ? 1 : 0, polish_screen(), mk, d_safe, trace);
       launch(c, "k_qp_verdicts", k_qp_verdicts, dim3(div_up(n_inst, 256)), dim3(256), 0,
              d_pend.as<unsigned long long>(), n_inst, d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(),
              d_cnt.as<unsigned long long>());
@@ -556,13 +690,111 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       mk->qp_obs.alloc(n_inst * sizeof(int), c->stream);
       launch(c, "k_unpack_pend", k_unpack_pend, dim3(div_up(n_inst, 256)), dim3(256), 0,
              d_pend.as<unsigned long long>(), n_inst, mk->qp_edge.as<long long>(), mk->qp_obs.as<int>());
-    }
+    };
+    if (n_inst > 0) dispatch_rows<Mc>(qp_rows, run_qp);
     launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(E, 256)), dim3(256), 0, E, n_obs, d_kill.as<int>(),
            d_qkill.as<int>(), d_saved.as<uint8_t>(), mk->alive.as<uint8_t>(), mk->prov.as<uint8_t>());
     BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
     mk->counters[4] = (long long)hcnt[3];
     mk->counters[5] = (long long)hcnt[4];
+  });
+}
+
+// The reference's scalar entry points on explicit control-point sets: cut_heuristic
+// (graph.py:202-221, mode 0 -> code 0/1/2) and cut_qp (graph.py:285-299, mode 1 -> safe flag,
+// ||delta||, solver status), set b against obstacle obs_index[b].  The sets become a
+// pseudo-graph: vertex 2b holds control points 0..G-1 of set b, vertex 2b+1 points G..J-1,
+// edge b = (2b, 2b+1) and D = I, so control_points() reproduces every set exactly (products
+// with 1, FMAs with 0) and the graph kernels run unchanged.
+void cut_points(Ctx* c, int m, int J, long long B, const double* points, const int32_t* obs_index, int n_obs,
+                const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
+                const double* box_hi, const bzg_cut_config* cfg, int mode, int8_t* code_out, double* delta_out,
+                int8_t* status_out) {
+  BZG_REQUIRE(mode == 0 || mode == 1, BZG_EINVAL, "mode must be 0 (cut_heuristic) or 1 (cut_qp)");
+  BZG_REQUIRE(J >= 2 && J % 2 == 0, BZG_EUNSUPPORTED, "the device takes an even control-point count (p = 2*gamma - 1)");
+  BZG_REQUIRE(B >= 0 && B < (1ll << 30), BZG_EINVAL, "set count out of range");
+  BZG_REQUIRE(n_obs >= 1 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
+  const int qp_rows = check_obstacles(n_obs, row_off, is_box, m);
+  for (long long i = 0; i < B; ++i)
+    BZG_REQUIRE(obs_index[i] >= 0 && obs_index[i] < n_obs, BZG_EINVAL, "obstacle index out of range");
+  if (B == 0) return;
+  const int G = J / 2;
+  Graph g;
+  g.ctx = c;
+  g.m = m;
+  g.gamma = G;
+  g.p = J - 1;
+  g.n = m * G;
+  g.V = 2 * B;
+  g.D.assign((size_t)J * J, 0.0);
+  for (int j = 0; j < J; ++j) g.D[(size_t)j * J + j] = 1.0;
+  std::vector<double> V((size_t)2 * B * m * G);
+  std::vector<int32_t> src(B), dst(B);
+  std::vector<unsigned long long> items(B);
+  for (long long s = 0; s < B; ++s) {
+    const double* P = points + (size_t)s * m * J;
+    for (int q = 0; q < G; ++q)
+      for (int k = 0; k < m; ++k) {
+        V[(size_t)(2 * s) * m * G + q * m + k] = P[k * J + q];
+        V[(size_t)(2 * s + 1) * m * G + q * m + k] = P[k * J + G + q];
+      }
+    src[s] = (int32_t)(2 * s);
+    dst[s] = (int32_t)(2 * s + 1);
+    items[s] = ((unsigned long long)s << 20) | (unsigned long long)obs_index[s];
+  }
+  const std::vector<double> cost(B, 0.0);
+  g.vertices.alloc(V.size() * sizeof(double), c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(g.vertices.ptr, V.data(), V.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  set_edges(c, &g, B, src.data(), dst.data(), cost.data(), false);
+  DParams dp{};
+  for (size_t k = 0; k < g.D.size(); ++k) dp.D[k] = g.D[k];
+  dispatch_cut(G, m, [&](auto G_, auto M_) {
+    constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+    using Rec = ObsRec<Mc>;
+    const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
+    DevBuf d_obs, d_items;
+    d_obs.alloc(sizeof(Rec) * h.size(), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, h.data(), sizeof(Rec) * h.size(), cudaMemcpyHostToDevice, c->stream));
+    d_items.alloc(B * sizeof(unsigned long long), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_items.ptr, items.data(), B * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                                   c->stream));
+    if (mode == 0) {
+      DevBuf d_kill, d_cnt, d_pend, d_code;
+      d_kill.alloc(B * sizeof(int), c->stream);
+      d_cnt.alloc(8 * sizeof(unsigned long long), c->stream);
+      d_pend.alloc(B * sizeof(unsigned long long), c->stream);
+      d_code.alloc(B, c->stream);
+      BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 8 * sizeof(unsigned long long), c->stream));
+      launch(c, "k_fill_int", k_fill_int, dim3(div_up(B, 256)), dim3(256), 0, d_kill.as<int>(), B, n_obs);
+      unsigned long long* dcnt = d_cnt.as<unsigned long long>();
+      launch(c, "k_cut_general", k_cut_general<Gc, Mc>, dim3(div_up(B, 64)), dim3(64), 0, dp, g.vertices.as<double>(),
+             g.src.as<int>(), g.dst.as<int>(), d_obs.as<Rec>(), d_items.as<unsigned long long>(), B, cfg->heur_margin,
+             d_kill.as<int>(), dcnt, dcnt + 5, (unsigned long long)B, d_pend.as<unsigned long long>(),
+             d_code.as<int8_t>());
+      unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(code_out, d_code.ptr, B, cudaMemcpyDeviceToHost, c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      BZG_REQUIRE(hcnt[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
+      return;
+    }
+    bool canon_all = true;
+    for (int o = 0; o < n_obs; ++o) canon_all = canon_all && h[o].canon != 0.0;
+    Mask mk;
+    mk.g = &g;
+    mk.E = B;
+    DevBuf d_safe;
+    auto no_trace = [](const char*) {};
+    dispatch_rows<Mc>(qp_rows, [&](auto C_) {
+      qp_solve<Gc, Mc, decltype(C_)::value>(c, &g, dp, d_obs.as<Rec>(), canon_all, d_items.as<unsigned long long>(), B,
+                                            cfg, cfg->qp_polish ? 2 : 0, 0.0, &mk, d_safe, no_trace);
+    });
+    if (code_out) BZG_CHECK_CUDA(cudaMemcpyAsync(code_out, d_safe.ptr, B, cudaMemcpyDeviceToHost, c->stream));
+    if (delta_out)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(delta_out, mk.qp_delta.ptr, B * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (status_out) BZG_CHECK_CUDA(cudaMemcpyAsync(status_out, mk.qp_status.ptr, B, cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

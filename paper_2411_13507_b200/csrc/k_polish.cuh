@@ -15,7 +15,7 @@ namespace {
 // For the selected instances the residual maxima rp = max|A x - z|, rd = max|P x + A'y|
 // (qpsolver.py:179-180) are recomputed here from the stored terminal (x, z, y), exactly as
 // the reference records them with the snapshot (qpsolver.py:191).
-template <int G, int M>
+template <int G, int M, int C>
 __global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int* __restrict__ src,
                             const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
                             const unsigned long long* __restrict__ pend, long long n_inst, int polish,
@@ -24,7 +24,7 @@ __global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int
                             double* __restrict__ res_out, double* __restrict__ delta_out,
                             uint8_t* __restrict__ safe_out, int* __restrict__ list,
                             unsigned long long* __restrict__ n_list) {
-  constexpr int J = 2 * G, C = 2 * M, NV = J + C, MC = C + J + 1;
+  constexpr int J = 2 * G, NV = J + C, MC = C + J + 1;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   bool need = false;
   if (t < n_inst) {
@@ -35,10 +35,12 @@ __global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int
     const bool solved = st[t] == BZG_SOLVED;
     delta_out[t] = dl;
     safe_out[t] = (uint8_t)(solved && dl > eps_cut);
-    need = polish && solved && (screen <= 0.0 || dl < screen);
+    // polish 1: SOLVED only (the verdict is all cut_graph uses); 2: also MAX_ITER, whose
+    // polished x the reference returns from solve() (cut_qp's ||delta||)
+    need = polish && (solved || (polish == 2 && st[t] == BZG_MAX_ITER)) && (screen <= 0.0 || dl < screen);
     if (need) {
       double Q[C][J], b[C];
-      load_instance<G, M>(dp, Vx, src, dst, obs, pend[t], Q, b);
+      load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[t], Q, b);
       const double* xv = x + t * NV;
       const double* z = zy + t * 2 * MC;
       const double* y = z + MC;
@@ -92,16 +94,16 @@ __global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int
 // max(rp', rd') < max(rp, rd).
 constexpr int kPolishThreads = 64;
 
-template <int G, int M>
-constexpr int polish_dim() { return 2 * G + 2 * M + 1; }  // core: J + C + 1
+template <int G, int M, int C>
+constexpr int polish_dim() { return 2 * G + C + 1; }  // core: J + C + 1
 
-template <int G, int M>
+template <int G, int M, int C>
 __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
     DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
     const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
     long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ res,
-    double* __restrict__ delta_out, uint8_t* __restrict__ safe_out) {
-  constexpr int J = 2 * G, C = 2 * M, NV = J + C, MC = C + J + 1, NC = J + C + 1;
+    double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
+  constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NC = J + C + 1;
   constexpr int BS = kPolishThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Rm = reinterpret_cast<double*>(smem_raw) + threadIdx.x;  // core (r, c) at Rm[(r*NC+c)*BS]
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
   for (int t = 0; t < NV; ++t) x[t] = x_io[inst * NV + t];
   const double rp = res[inst * 2], rd = res[inst * 2 + 1];
   double Q[C][J], b[C];
-  load_instance<G, M>(dp, Vx, src, dst, obs, pend[inst], Q, b);
+  load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[inst], Q, b);
   // constraint slot i of A (graph.py:275-281): i < C obstacle row [Q_i, -e_i];
   // C <= i < C+J lambda bound [e_{i-C}, 0]; i = C+J the sum row [1..1, 0]
   auto Gl = [&](int i, int j) -> double {  // lambda part of row i (compile-time i, j)
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
   }
   const double dl = sqrt(s);
   delta_out[inst] = dl;
-  safe_out[inst] = (uint8_t)(dl > eps_cut);
+  safe_out[inst] = (uint8_t)(st[inst] == BZG_SOLVED && dl > eps_cut);
 }
 
 }  // namespace

@@ -1,10 +1,15 @@
-// Batched Cut-QP on device: dense ADMM (one thread per instance) and active-set polish
-// (one warp per instance).  Included by k_cut.cu.
+// Batched Cut-QP on device: shared pieces of the dense ADMM (k_admm.cuh) and the
+// active-set polish (k_polish.cuh).  Included by k_cut.cu.
 //
 // Problem (reference graph.py:268-282, _cut_qp_problem), per (edge, obstacle):
 //   x = [lambda (J); delta (C)],  min delta' delta
 //   s.t.  Q lambda - delta <= b  (C rows, Q = A_O P),  lambda >= 0 (J rows),  sum lambda = 1
 // solved by the dense ADMM of qpsolver.py:129-233 and polished by qpsolver.py:236-279.
+//
+// C is the padded obstacle row count of the launch: obstacles with fewer rows carry zero
+// rows with b = 1e300.  A padding row is exactly neutral: its delta_c, z_c, y_c stay 0.0
+// through every ADMM step (all their updates are sums of products with 0), it never enters
+// the polish active set, and it adds 0 to ||delta||.
 #pragma once
 
 namespace bzg {
@@ -16,10 +21,10 @@ struct QpParams {
 };
 
 // Q = A_O @ points (graph.py:276): BLAS product, FMA chain over the m output dimensions.
-template <int G, int M>
-__device__ __forceinline__ void cut_q_matrix(const ObsRec<M>& o, const double (&P)[M][2 * G], double (&Q)[2 * M][2 * G]) {
+template <int G, int M, int C>
+__device__ __forceinline__ void cut_q_matrix(const ObsRec<M>& o, const double (&P)[M][2 * G], double (&Q)[C][2 * G]) {
 #pragma unroll
-  for (int c = 0; c < 2 * M; ++c)
+  for (int c = 0; c < C; ++c)
 #pragma unroll
     for (int j = 0; j < 2 * G; ++j) {
       double acc = __dmul_rn(o.A[c][0], P[0][j]);
@@ -29,11 +34,11 @@ __device__ __forceinline__ void cut_q_matrix(const ObsRec<M>& o, const double (&
     }
 }
 
-template <int G, int M>
+template <int G, int M, int C>
 __device__ __forceinline__ void load_instance(const DParams& dp, const double* __restrict__ Vx,
                                               const int* __restrict__ src, const int* __restrict__ dst,
                                               const ObsRec<M>* __restrict__ obs, unsigned long long pk,
-                                              double (&Q)[2 * M][2 * G], double (&b)[2 * M]) {
+                                              double (&Q)[C][2 * G], double (&b)[C]) {
   constexpr int N = G * M;
   const long long e = (long long)(pk >> 20);
   const ObsRec<M>& o = obs[(int)(pk & 0xFFFFF)];
@@ -45,9 +50,9 @@ __device__ __forceinline__ void load_instance(const DParams& dp, const double* _
     xj[k] = Vx[c * N + k];
   }
   control_points<G, M>(xi, xj, dp.D, P);
-  cut_q_matrix<G, M>(o, P, Q);
+  cut_q_matrix<G, M, C>(o, P, Q);
 #pragma unroll
-  for (int k = 0; k < 2 * M; ++k) b[k] = o.b[k];
+  for (int k = 0; k < C; ++k) b[k] = o.b[k];
 }
 
 }  // namespace

@@ -436,6 +436,65 @@ def cut_graph(graph: BezierGraph, obstacles, cfg: CutConfig | None = None) -> Cu
     return CutMask(h, graph, cnt)
 
 
+# the shim swaps this for the reference's enum so verdicts compare equal inside its code
+_VERDICT_ENUM = CutVerdict
+
+
+def _cut_points(points, obstacles, obs_index, cfg, mode, ctx):
+    """bzg_cut_points over B control-point sets (B, m, J) (include/bzg.h)."""
+    cfg = cfg or CutConfig()
+    ctx = ctx or nat.default_context()
+    P = _f64(points)
+    if P.ndim != 3:
+        raise ValueError("points must be (B, m, p+1)")
+    B, m, J = P.shape
+    obstacles = list(obstacles)
+    if not obstacles:
+        raise ValueError("need at least one obstacle")
+    idx = np.zeros(B, np.int32) if obs_index is None else np.ascontiguousarray(obs_index, dtype=np.int32)
+    if idx.shape != (B,):
+        raise ValueError("obs_index must have one entry per point set")
+    offs, A, b, is_box, lo, hi = _obstacle_arrays(obstacles, m)
+    cc = _cut_cfg(cfg)
+    code = np.empty(B, np.int8)
+    delta = np.empty(B) if mode == 1 else None
+    status = np.empty(B, np.int8) if mode == 1 else None
+    rc = ctx.lib.bzg_cut_points(ctx.handle, m, J, B, nat.ptr(P), nat.ptr(idx), len(obstacles), nat.ptr(offs),
+                                nat.ptr(A), nat.ptr(b), nat.ptr(is_box), nat.ptr(lo), nat.ptr(hi), C.byref(cc), mode,
+                                nat.ptr(code), nat.ptr(delta) if delta is not None else None,
+                                nat.ptr(status) if status is not None else None)
+    nat.check(rc)
+    return code, delta, status
+
+
+def cut_heuristic_batch(points, obstacles, obs_index=None, cfg: CutConfig | None = None, *, ctx=None) -> np.ndarray:
+    """cut_heuristic (graph.py:202-221) for B control-point sets (B, m, p+1); set i against
+    obstacles[obs_index[i]] (all against obstacles[0] when obs_index is None).  int8 codes
+    0 unsafe / 1 safe / 2 indeterminate."""
+    return _cut_points(points, obstacles, obs_index, cfg, 0, ctx)[0]
+
+
+def cut_qp_batch(points, obstacles, obs_index=None, cfg: CutConfig | None = None, *, ctx=None):
+    """cut_qp (graph.py:285-299) for B control-point sets: (safe (B,) bool, ||delta*|| (B,),
+    solver status (B,) int8: 0 solved, 1 max_iter, 2 infeasible)."""
+    code, delta, status = _cut_points(points, obstacles, obs_index, cfg, 1, ctx)
+    return code.astype(bool), delta, status
+
+
+def cut_heuristic(points, obstacle, cfg: CutConfig | None = None, *, ctx=None):
+    """Three-branch screen for one edge's output control points (m, p+1) (graph.py:202-221)."""
+    pts = np.atleast_2d(_f64(points))
+    code = int(cut_heuristic_batch(pts[None], [obstacle], None, cfg, ctx=ctx)[0])
+    return (_VERDICT_ENUM.UNSAFE, _VERDICT_ENUM.SAFE, _VERDICT_ENUM.INDETERMINATE)[code]
+
+
+def cut_qp(points, obstacle, cfg: CutConfig | None = None, *, ctx=None) -> tuple[bool, float]:
+    """Slack-minimising hull/obstacle test (graph.py:285-299): (safe, ||delta*||)."""
+    pts = np.atleast_2d(_f64(points))
+    safe, delta, _ = cut_qp_batch(pts[None], [obstacle], None, cfg, ctx=ctx)
+    return bool(safe[0]), float(delta[0])
+
+
 def find_path(graph: BezierGraph, mask, start, goal, position_only_snap: bool = False,
               require_tube_snap: bool = True):
     """Shortest alive path between the snapped start and goal (graph.py:353-430); None if none."""

@@ -19,7 +19,7 @@ from __future__ import annotations
 
 from . import graph as _dev
 
-_PATCHED = ("build_graph", "cut_graph", "find_path", "path_cost")
+_PATCHED = ("build_graph", "cut_graph", "find_path", "path_cost", "cut_heuristic", "cut_qp")
 _saved: dict = {}
 
 
@@ -36,6 +36,8 @@ def install(beziergraph_pkg) -> None:
             setattr(beziergraph_pkg, name, getattr(_dev, name))
     _saved[("prov",)] = _dev._PROV_ENUM
     _dev._PROV_ENUM = gmod.CutProvenance
+    _saved[("verdict",)] = _dev._VERDICT_ENUM
+    _dev._VERDICT_ENUM = gmod.CutVerdict
 
 
 def uninstall(beziergraph_pkg) -> None:
@@ -47,4 +49,6 @@ def uninstall(beziergraph_pkg) -> None:
             setattr(beziergraph_pkg, key[1], fn)
         elif key[0] == "prov":
             _dev._PROV_ENUM = fn
+        elif key[0] == "verdict":
+            _dev._VERDICT_ENUM = fn
     _saved.clear()

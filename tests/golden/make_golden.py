@@ -287,7 +287,67 @@ def case_regions4(name="regions4", quads=None):
     print(f"{name}: V={Vn} E={E.shape[0]} (base oracle alone: {base_only})")
 
 
-CASES = {"regions4": case_regions4,
+def _regular_polygon(center, radius, k, phase):
+    ang = phase + 2 * np.pi * np.arange(k) / k
+    A = np.stack([np.cos(ang), np.sin(ang)], axis=1) * 1.7  # non-unit rows: normalisation is exercised
+    b = A @ np.asarray(center, float) + radius * 1.7
+    return rgeo.Polytope(A, b)
+
+
+def general_obstacles():
+    """Convex non-box obstacles with 3..8 rows (rotated square, triangle, pentagon, hexagon,
+    octagon) and one box, in the demo map."""
+    return [
+        _regular_polygon((2.5, 2.5), 0.45, 4, np.pi / 4 + 0.3),   # rotated square
+        _regular_polygon((1.3, 3.7), 0.35, 3, 0.2),               # triangle
+        _regular_polygon((3.7, 1.3), 0.40, 5, 0.1),               # pentagon
+        _regular_polygon((1.2, 1.6), 0.30, 6, 0.0),               # hexagon
+        _regular_polygon((3.6, 3.4), 0.38, 8, np.pi / 8),         # octagon
+        rgeo.Box(np.array([2.2, 0.3]), np.array([2.7, 0.9])).to_polytope(),
+    ]
+
+
+def case_general():
+    """Graph golden with general (non-box) obstacles: _heuristic_batch's per-edge
+    cut_heuristic branch (graph.py:242-247) and the Cut-QP on 3..8-row obstacles."""
+    s = rsc.demo_scenario()
+    oracle = bg.build_oracle(s.spec, s.xd, s.u_bounds, s.tube)
+    capture("general60", 60, s.spec, oracle, s.sample_bounds, 11, np.array([s.start, s.goal]),
+            general_obstacles(), s.start, s.goal, full=True, detail=True)
+
+
+def case_heur_general():
+    """Scalar cut_heuristic / closest_point / adjacent_hyperplane on random control polygons
+    near general obstacles (geometry.py:202-252, graph.py:202-221)."""
+    rng = np.random.default_rng(3)
+    obs = general_obstacles()[:5]
+    cfg = rg.CutConfig()
+    pts_l, oi_l, code_l, proj_l, hp_l = [], [], [], [], []
+    for i in range(400):
+        oi = i % len(obs)
+        O = obs[oi]
+        ctr = {0: (2.5, 2.5), 1: (1.3, 3.7), 2: (3.7, 1.3), 3: (1.2, 1.6), 4: (3.6, 3.4)}[oi]
+        pts = np.asarray(ctr)[:, None] + rng.uniform(-0.9, 0.9, (2, 1)) + rng.uniform(-0.35, 0.35, (2, 4))
+        pts_l.append(pts)
+        oi_l.append(oi)
+        code_l.append({rg.CutVerdict.UNSAFE: 0, rg.CutVerdict.SAFE: 1, rg.CutVerdict.INDETERMINATE: 2}[
+            rg.cut_heuristic(pts, O, cfg)])
+        On = O.normalized()
+        proj_l.append(np.stack([rgeo.closest_point(On, p) for p in pts.T]))
+        try:
+            hp = rgeo.adjacent_hyperplane(On, pts[:, 0])
+            hp_l.append(np.concatenate([hp.normal, [hp.offset]]))
+        except ValueError:
+            hp_l.append(np.full(3, np.nan))
+    np.savez_compressed(OUT / "heur_general.npz", points=np.stack(pts_l), obstacle=np.array(oi_l, np.int32),
+                        codes=np.array(code_l, np.int8), projections=np.stack(proj_l), hyperplanes=np.stack(hp_l),
+                        obs_n=np.array([o.num_rows for o in obs], np.int32),
+                        obs_A=np.concatenate([o.A for o in obs]), obs_b=np.concatenate([o.b for o in obs]),
+                        env=json.dumps(env_info()))
+    print("heur_general:", np.bincount(np.array(code_l), minlength=3))
+
+
+CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general,
          "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
                                                               ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
                                                               ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,

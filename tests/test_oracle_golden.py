@@ -97,3 +97,30 @@ def test_check_edges_matches_pair_test(golden):
     n = V.shape[1]
     ok = oracle.check_edges(g["F"], g["G"], n, V[E[:, 0]], V[E[:, 1]])
     assert ok.all()
+
+
+def _golden_obstacles(g):
+    off = np.concatenate([[0], np.cumsum(g["obs_n"])])
+    return [(g["obs_A"][off[i]:off[i + 1]], g["obs_b"][off[i]:off[i + 1]]) for i in range(len(g["obs_n"]))]
+
+
+def test_general_heuristic_bitwise(golden):
+    """Scalar cut_heuristic / closest_point / adjacent_hyperplane on non-box polytopes
+    (graph.py:202-221, geometry.py:202-252) against the live reference (a subset: each
+    projection is a 20000-iteration-capped ADMM in numpy)."""
+    g = golden("heur_general")
+    obs = _golden_obstacles(g)
+    gr = oracle.graph_ref
+    for i in range(0, len(g["codes"]), 8):
+        A, b = obs[int(g["obstacle"][i])]
+        pts = g["points"][i]
+        assert gr.cut_heuristic(pts, A, b) == int(g["codes"][i]), i
+        OA, Ob = gr.normalized(A, b)
+        proj = np.stack([gr.closest_point(OA, Ob, p) for p in pts.T])
+        assert proj.tobytes() == g["projections"][i].tobytes(), i
+        try:
+            n, o = gr.adjacent_hyperplane(OA, Ob, pts[:, 0])
+            hp = np.concatenate([n, [o]])
+        except ValueError:
+            hp = np.full(3, np.nan)
+        assert np.array_equal(hp, g["hyperplanes"][i], equal_nan=True), i
