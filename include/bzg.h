@@ -106,11 +106,23 @@ typedef struct {
    * outside a region's box (by more than 1e-6) is not tested against its rows */
   const double* region_box_lo;
   const double* region_box_hi;
+  /* k_nearest prefilter (graph.py:162-170): < 0 = off; else edge i->j also needs j among
+   * the min(k_nearest, V-1) nearest vertices of i by fl(sum_k (p_ik - p_jk)^2) over the m
+   * position coordinates.  Ties at the k-th distance keep the lowest indices (the
+   * reference's argpartition tie order is implementation-defined). */
+  int64_t k_nearest;
 } bzg_build_desc;
 
 /* the sampler alone (graph.py:147-157): N accepted states of one PCG64 stream written to a
  * host buffer (N, n); uses desc's m, gamma, N, pcg_*, sample_lo/hi, xd_*, eps_geo */
 int bzg_sample_states(bzg_ctx* ctx, const bzg_build_desc* desc, double* out_host);
+/* the sampler for several keep-in regions in one call (regions.py sample_region_states):
+ * region r draws N[r] states from its own PCG64 stream (pcg[4r..4r+3] = state_hi, state_lo,
+ * inc_hi, inc_lo of default_rng([seed, r])) in the box lo/hi (n_regions x n), accepting in
+ * rows [row_off[r], row_off[r+1]) of A (rows x n) / b; out_host = (sum N, n) in region order */
+int bzg_sample_region_states(bzg_ctx* ctx, int32_t n, int32_t n_regions, const int64_t* N, const uint64_t* pcg,
+                             const double* lo, const double* hi, const int32_t* row_off, const double* A,
+                             const double* b, double eps_geo, double* out_host);
 
 /* replaces graph.build_graph (graph.py:129-199) minus k_nearest */
 int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* desc, bzg_graph** out);

@@ -102,14 +102,28 @@ def edge_costs(points):
     return np.linalg.norm(np.diff(points, axis=2), axis=1).sum(axis=1)
 
 
-def build_graph(N, spec, oracle, bounds, seed, include=None, D=None):
-    """Whole ``build_graph`` (graph.py:129-199) minus k_nearest; returns a dict of arrays."""
+def knn_allowed(V, m, k_nearest):
+    """k_nearest prefilter mask (graph.py:162-170), same numpy calls (argpartition ties included)."""
+    pos = V[:, :m]
+    d2 = ((pos[:, None, :] - pos[None, :, :]) ** 2).sum(axis=2)
+    np.fill_diagonal(d2, np.inf)
+    n = V.shape[0]
+    k = min(k_nearest, n - 1)
+    nbr = np.argpartition(d2, k - 1, axis=1)[:, :k]
+    allowed = np.zeros((n, n), dtype=bool)
+    allowed[np.repeat(np.arange(n), k), nbr.ravel()] = True
+    return allowed
+
+
+def build_graph(N, spec, oracle, bounds, seed, include=None, D=None, k_nearest=None):
+    """Whole ``build_graph`` (graph.py:129-199); returns a dict of arrays."""
     if N < 2:
         raise ValueError("need at least two vertices")
     n = spec.m * spec.gamma
     V = sample_states(N, bounds.lo, bounds.hi, oracle.Xd.A, oracle.Xd.b, seed, include)
+    allowed = None if k_nearest is None else knn_allowed(V, spec.m, k_nearest)
     A1, A2 = project(V, oracle.F, n)
-    E = pair_edges(A1, A2, oracle.G)
+    E = pair_edges(A1, A2, oracle.G, allowed=allowed)
     if D is None:
         from paper_2411_13507_b200.bezier import boundary_matrix  # host constant (bezier.py:185-211)
         D = boundary_matrix(spec)

@@ -44,7 +44,13 @@ class BuildDesc(C.Structure):
         ("row_begin", C.c_int64), ("row_end", C.c_int64),
         ("n_regions", C.c_int32), ("region_row_off", C.c_void_p), ("region_F", C.c_void_p),
         ("region_G", C.c_void_p), ("region_box_lo", C.c_void_p), ("region_box_hi", C.c_void_p),
+        ("k_nearest", C.c_int64),
     ]
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        if "k_nearest" not in kw:
+            self.k_nearest = -1  # prefilter off
 
 
 class CutConfigC(C.Structure):
@@ -84,6 +90,7 @@ _SIGS = {
     "bzg_graph_export_device": ([_P, _P, _P, _P], C.c_int),
     "bzg_check_edges": ([_P, C.c_int32, C.c_int32, _P, _P, C.c_double, C.c_int64, _P, _P, _P], C.c_int),
     "bzg_cut_graph": ([_P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, C.POINTER(CutConfigC), C.POINTER(_P)], C.c_int),
+    "bzg_sample_region_states": ([_P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, C.c_double, _P], C.c_int),
     "bzg_cut_points": ([_P, C.c_int32, C.c_int32, C.c_int64, _P, _P, C.c_int32, _P, _P, _P, _P, _P, _P,
                         C.POINTER(CutConfigC), C.c_int32, _P, _P, _P], C.c_int),
     "bzg_mask_destroy": ([_P], C.c_int),

@@ -4,6 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
@@ -66,6 +70,15 @@ struct DevBuf {
   template <typename T> T* as() const { return static_cast<T*>(ptr); }
 };
 
+// workspace slots of Ctx::ws (each used by one buffer of one phase at a time)
+enum WsSlot {
+  WS_CAND, WS_FLAG, WS_POS,                                          // samplers
+  WS_BITS, WS_A1C, WS_A2T, WS_ROWCNT, WS_RPTR,                       // pair test
+  WS_KILL, WS_QKILL, WS_SAVED, WS_PEND, WS_GEN,                      // cut screen
+  WS_QX, WS_QZY, WS_QRES, WS_QSAFE, WS_QLIST,                        // Cut-QP
+  kWsSlots
+};
+
 struct KernelStat {
   double ms = 0.0;
   long long count = 0;
@@ -80,6 +93,16 @@ struct Ctx {
   std::string profile_only;  // when non-empty, time only launches of this kernel
   long long launches = 0;
   bool timed(const char* name) const { return profiling && (profile_only.empty() || profile_only == name); }
+  // BZG_TRACE=1: synchronising host wall-time trace of library phases (diagnosing launch gaps)
+  bool trace_on = std::getenv("BZG_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point trace_t = std::chrono::steady_clock::now();
+  void trace(const char* what) {
+    if (!trace_on) return;
+    cudaStreamSynchronize(stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bzg] %-24s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - trace_t).count());
+    trace_t = now;
+  }
   struct Pending { std::string name; cudaEvent_t a, b; };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> spare;
@@ -87,6 +110,11 @@ struct Ctx {
   std::unordered_map<std::string, KernelStat> stats;
   DevBuf scratch;       // cub temp storage
   DevBuf flag;          // small device scalars
+  // Grow-only workspaces for the per-call temporaries (pair bit matrix, sampler candidates,
+  // cut work lists, QP state): reused across calls on this stream, so repeated builds and
+  // cuts do not refragment the stream-ordered pool (a fresh 1 GB bit matrix per step made the
+  // pool map new memory at random steps, milliseconds each).
+  DevBuf ws[kWsSlots];
   void* pinned = nullptr;  // small pinned host staging area
   size_t pinned_bytes = 0;
 
@@ -207,6 +235,8 @@ struct Mask {
 
 // Kernel-family entry points (defined in the k_*.cu translation units).
 void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices);
+void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
+                    const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out);
 void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g);
 void materialize_points(Ctx* c, Graph* g);
 void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, const double* cost, bool on_device);

@@ -83,6 +83,7 @@ int bzg_ctx_destroy(bzg_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->scratch.release();
     ctx->flag.release();
+    for (auto& w : ctx->ws) w.release();
     ctx->drain_profile();
     for (auto e : ctx->spare) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -164,6 +165,7 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
     BZG_REQUIRE(d->F && d->G && d->D, BZG_EINVAL, "oracle F, G and boundary matrix D are required");
     BZG_REQUIRE(d->n_include >= 0 && (d->n_include == 0 || d->include), BZG_EINVAL, "include rows missing");
     const int n = d->m * d->gamma;
+    ctx->trace("build: enter");
     g = new bzg_graph();
     g->ctx = ctx;
     g->m = d->m;
@@ -188,7 +190,9 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
     if (d->n_include > 0)
       BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)d->N * n, d->include,
                                      (size_t)d->n_include * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->trace("build: vertices");
     build_pairs(ctx, d, g);
+    ctx->trace("build: pairs+csr");
   });
   if (rc == BZG_OK) {
     *out = g;
@@ -210,6 +214,31 @@ int bzg_sample_states(bzg_ctx* ctx, const bzg_build_desc* d, double* out_host) {
     out.alloc((size_t)d->N * n * sizeof(double), ctx->stream);
     sample_states(ctx, d, out.as<double>());
     BZG_CHECK_CUDA(cudaMemcpyAsync(out_host, out.ptr, (size_t)d->N * n * sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int bzg_sample_region_states(bzg_ctx* ctx, int32_t n, int32_t n_regions, const int64_t* N, const uint64_t* pcg,
+                             const double* lo, const double* hi, const int32_t* row_off, const double* A,
+                             const double* b, double eps_geo, double* out_host) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && N && pcg && lo && hi && row_off && A && b && out_host, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(n_regions >= 1, BZG_EINVAL, "need at least one region");
+    long long total = 0;
+    for (int r = 0; r < n_regions; ++r) {
+      BZG_REQUIRE(N[r] >= 0, BZG_EINVAL, "negative sample count");
+      BZG_REQUIRE(row_off[r + 1] > row_off[r], BZG_EINVAL, "every region needs state-set rows");
+      total += N[r];
+    }
+    set_device(ctx);
+    if (total == 0) return;
+    ctx->trace("sample_regions: enter");
+    DevBuf out;
+    out.alloc((size_t)total * n * sizeof(double), ctx->stream);
+    sample_regions(ctx, n, n_regions, N, pcg, lo, hi, row_off, A, b, eps_geo, out.as<double>());
+    ctx->trace("sample_regions: done");
+    BZG_CHECK_CUDA(cudaMemcpyAsync(out_host, out.ptr, (size_t)total * n * sizeof(double), cudaMemcpyDeviceToHost,
                                    ctx->stream));
     BZG_CHECK_CUDA(cudaStreamSynchronize(ctx->stream));
   });

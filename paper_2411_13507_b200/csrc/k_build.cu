@@ -60,6 +60,74 @@ __global__ void k_sample_scatter(const double* __restrict__ cand, const int* __r
   for (int k = 0; k < n; ++k) out[p * n + k] = cand[t * n + k];
 }
 
+// ---------------------------------------------------------------- multi-region sampler
+// All keep-in regions in one launch per round (regions.py sample_region_states): region r
+// draws from its own PCG64 stream (default_rng([seed, r])) inside its own sampling box and
+// accepts in its own state polytope rows [row_off[r], row_off[r+1]) -- build_graph's sampler
+// (graph.py:147-157) per region.  Candidate t belongs to region r with
+// cand_off[r] <= t < cand_off[r+1].
+struct RegionSampleDev {
+  const unsigned long long* pcg;  // R x 4: state_hi, state_lo, inc_hi, inc_lo
+  const double* lo;               // R x n
+  const double* range;            // R x n (hi - lo)
+  const int* row_off;             // R + 1
+  const double* A;                // rows x n
+  const double* b_eps;            // rows
+  const long long* cand_off;      // R + 1 (this round)
+  const long long* row0;          // R: first stream row of this round
+  int n, R;
+};
+
+__device__ __forceinline__ int region_of(const long long* off, int R, long long t) {
+  int lo = 0, hi = R;  // largest r with off[r] <= t
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_sample_regions(RegionSampleDev rs, long long total, double* __restrict__ cand,
+                                 int* __restrict__ flag) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int r = region_of(rs.cand_off, rs.R, t);
+  const int n = rs.n;
+  const unsigned long long* w = rs.pcg + 4 * r;
+  const u128 inc = ((u128)w[2] << 64) | w[3];
+  u128 s = ((u128)w[0] << 64) | w[1];
+  s = pcg_advance(s, inc, (uint64_t)(rs.row0[r] + (t - rs.cand_off[r])) * (uint64_t)n);
+  double x[kMaxN];
+  for (int k = 0; k < n; ++k) {
+    const double u = pcg_next_double(s, inc);
+    x[k] = __dadd_rn(rs.lo[r * n + k], __dmul_rn(rs.range[r * n + k], u));
+    cand[t * n + k] = x[k];
+  }
+  int ok = 1;
+  for (int c = rs.row_off[r]; c < rs.row_off[r + 1]; ++c) ok &= fma_chain(x, rs.A + (size_t)c * n, n) <= rs.b_eps[c];
+  flag[t] = ok;
+}
+
+// accepted candidate t of region r lands at dest[r] + (its rank among r's acceptances) if that
+// rank is below need[r]; acc[r] = acceptances of r this round
+__global__ void k_scatter_regions(const double* __restrict__ cand, const int* __restrict__ flag,
+                                  const int* __restrict__ pos, const long long* __restrict__ cand_off, int R,
+                                  long long total, int n, const long long* __restrict__ dest,
+                                  const long long* __restrict__ need, double* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= total || !flag[t]) return;
+  const int r = region_of(cand_off, R, t);
+  const long long p = pos[t] - pos[cand_off[r]];
+  if (p >= need[r]) return;
+  for (int k = 0; k < n; ++k) out[(dest[r] + p) * n + k] = cand[t * n + k];
+}
+
+__global__ void k_region_acc(const int* __restrict__ pos, const long long* __restrict__ cand_off, int R,
+                             long long* __restrict__ acc) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) acc[r] = (long long)pos[cand_off[r + 1]] - (long long)pos[cand_off[r]];
+}
+
 // ---------------------------------------------------------------- projections
 struct RowPlan {
   int n, K, n_src, n_dst;
@@ -347,6 +415,115 @@ __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
   }
 }
 
+// ---------------------------------------------------------------- k_nearest prefilter
+// graph.py:162-170: d2 = ((pos_i - pos_j)**2).sum(axis=2) -- squares, then a left fold over the
+// m position coordinates, no FMA -- with an infinite diagonal, k = min(k_nearest, V-1), and
+// edge i->j allowed iff j is among the k smallest of row i.  Non-negative doubles order like
+// their bit patterns, so the k-th smallest key of a row is found by an MSB-first radix
+// select (8-bit digits, warp-aggregated shared histograms).  Keys equal to it are kept
+// lowest index first (argpartition's tie order is implementation-defined).  One block per
+// source row masks the row's pair bits and recounts the row.
+constexpr int kKnnThreads = 256;
+
+__device__ __forceinline__ unsigned long long knn_key(const double* __restrict__ Vx, int n, int m,
+                                                      const double (&pi)[3], long long j) {
+  double s = 0.0;
+  for (int k = 0; k < m; ++k) {
+    const double d = __dsub_rn(pi[k], Vx[j * n + k]);
+    const double sq = __dmul_rn(d, d);
+    s = k == 0 ? sq : __dadd_rn(s, sq);
+  }
+  return (unsigned long long)__double_as_longlong(s);
+}
+
+__global__ void __launch_bounds__(kKnnThreads) k_knn_rows(const double* __restrict__ Vx, long long V, int n, int m,
+                                                          long long k, long long r0, long long W,
+                                                          uint32_t* __restrict__ bits,
+                                                          unsigned long long* __restrict__ rowcnt) {
+  typedef cub::BlockScan<unsigned long long, kKnnThreads> BS;
+  typedef cub::BlockReduce<unsigned long long, kKnnThreads> BR;
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ long long s_krem, s_last;
+  __shared__ union { typename BS::TempStorage scan; typename BR::TempStorage red; } tmp;
+  const long long row = blockIdx.x, i = r0 + row;
+  const int tid = threadIdx.x;
+  uint32_t* wrow = bits + row * W;
+  if (rowcnt[row] == 0) return;  // no pair edge to filter (uniform across the block)
+  if (k == 0) {
+    for (long long w = tid; w < W; w += kKnnThreads) wrow[w] = 0u;
+    if (tid == 0) rowcnt[row] = 0;
+    return;
+  }
+  double pi[3] = {0.0, 0.0, 0.0};
+  for (int q = 0; q < m; ++q) pi[q] = Vx[i * n + q];
+  unsigned long long prefix = 0;
+  long long krem = k;  // rank (1-based) of the wanted key among keys matching prefix
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = tid; b < 256; b += kKnnThreads) hist[b] = 0u;
+    __syncthreads();
+    const unsigned long long hi_mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (long long j0 = 0; j0 < V; j0 += kKnnThreads) {
+      const long long j = j0 + tid;
+      int digit = -1;
+      if (j < V && j != i) {
+        const unsigned long long key = knn_key(Vx, n, m, pi, j);
+        if ((key & hi_mask) == prefix) digit = (int)((key >> shift) & 255ull);
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, digit);
+      if (digit >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[digit], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long cum = 0;
+      for (int dgt = 0; dgt < 256; ++dgt) {
+        if (cum + hist[dgt] >= krem) {
+          s_prefix = prefix | ((unsigned long long)dgt << shift);
+          s_krem = krem - cum;
+          break;
+        }
+        cum += hist[dgt];
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    krem = s_krem;
+  }
+  // prefix = the k-th smallest key t; keep the first krem indices (ascending) whose key is t
+  const unsigned long long t = prefix;
+  const long long chunk = (V + kKnnThreads - 1) / kKnnThreads;
+  const long long j0 = tid * chunk, j1 = j0 + chunk < V ? j0 + chunk : V;
+  unsigned long long ties = 0;
+  for (long long j = j0; j < j1; ++j) ties += (j != i && knn_key(Vx, n, m, pi, j) == t);
+  unsigned long long before = 0;
+  BS(tmp.scan).ExclusiveSum(ties, before);
+  if ((long long)before < krem && (long long)(before + ties) >= krem) {
+    long long need = krem - (long long)before;
+    for (long long j = j0; j < j1; ++j)
+      if (j != i && knn_key(Vx, n, m, pi, j) == t && --need == 0) { s_last = j; break; }
+  }
+  __syncthreads();
+  const long long last = s_last;
+  unsigned long long total = 0;
+  for (long long w = tid; w < W; w += kKnnThreads) {
+    uint32_t word = wrow[w];
+    if (!word) continue;
+    uint32_t allow = 0u;
+    for (uint32_t rest = word; rest; rest &= rest - 1) {
+      const int b = __ffs(rest) - 1;
+      const long long j = w * 32 + b;
+      const unsigned long long key = knn_key(Vx, n, m, pi, j);
+      if (key < t || (key == t && j <= last)) allow |= 1u << b;
+    }
+    word &= allow;
+    wrow[w] = word;
+    total += __popc(word);
+  }
+  __syncthreads();
+  const unsigned long long sum = BR(tmp.red).Sum(total);
+  if (tid == 0) rowcnt[row] = sum;
+}
+
 // ---------------------------------------------------------------- compaction
 struct DParams {
   double D[64];
@@ -496,7 +673,7 @@ void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices) {
   }
   long long need = d->N, row0 = 0, got = 0;
   double est = 1.0;
-  DevBuf cand, flag, pos;
+  DevBuf &cand = c->ws[WS_CAND], &flag = c->ws[WS_FLAG], &pos = c->ws[WS_POS];
   int* h = static_cast<int*>(c->host_scratch(2 * sizeof(int)));
   for (int round = 0; need > 0; ++round) {
     BZG_REQUIRE(round < 10000, BZG_EINVAL, "sampler made no progress: state polytope misses the sampling box");
@@ -524,6 +701,82 @@ void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices) {
     need -= take;
     row0 += count;
     est = std::max(1e-3, (double)acc / (double)count);
+  }
+}
+
+void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
+                    const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out) {
+  BZG_REQUIRE(n >= 1 && n <= kMaxN, BZG_EUNSUPPORTED, "state dimension too large for the device sampler");
+  BZG_REQUIRE(R >= 1, BZG_EINVAL, "need at least one region");
+  std::vector<double> range((size_t)R * n), beps(row_off[R]);
+  for (size_t k = 0; k < range.size(); ++k) range[k] = hi[k] - lo[k];  // np.subtract(high, low)
+  for (int q = 0; q < row_off[R]; ++q) beps[q] = b[q] + eps_geo;
+  DevBuf d_pcg, d_lo, d_rng, d_off, d_A, d_b, d_coff, d_row0, d_dest, d_need, d_acc;
+  DevBuf &cand = c->ws[WS_CAND], &flag = c->ws[WS_FLAG], &pos = c->ws[WS_POS];
+  auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+    buf.alloc(std::max<size_t>(bytes, 8), c->stream);
+    if (bytes) BZG_CHECK_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  };
+  up(d_pcg, pcg, (size_t)R * 4 * sizeof(uint64_t));
+  up(d_lo, lo, (size_t)R * n * sizeof(double));
+  up(d_rng, range.data(), (size_t)R * n * sizeof(double));
+  up(d_off, row_off, (size_t)(R + 1) * sizeof(int32_t));
+  up(d_A, A, (size_t)row_off[R] * n * sizeof(double));
+  up(d_b, beps.data(), beps.size() * sizeof(double));
+  std::vector<long long> need(N, N + R), got(R, 0), row0(R, 0), base(R + 1, 0), coff(R + 1), dest(R);
+  std::vector<double> est(R, 1.0);
+  for (int r = 0; r < R; ++r) base[r + 1] = base[r] + N[r];
+  d_coff.alloc((R + 1) * sizeof(long long), c->stream);
+  d_row0.alloc(R * sizeof(long long), c->stream);
+  d_dest.alloc(R * sizeof(long long), c->stream);
+  d_need.alloc(R * sizeof(long long), c->stream);
+  d_acc.alloc(R * sizeof(long long), c->stream);
+  long long* hacc = static_cast<long long*>(c->host_scratch(R * sizeof(long long)));
+  for (int round = 0;; ++round) {
+    bool any = false;
+    coff[0] = 0;
+    for (int r = 0; r < R; ++r) {
+      long long cnt = 0;
+      if (need[r] > 0) {
+        any = true;
+        cnt = std::min<long long>((long long)std::ceil((double)need[r] / std::max(est[r], 1e-3) * 1.05) + 64, 1ll << 24);
+      }
+      coff[r + 1] = coff[r] + cnt;
+      dest[r] = base[r] + got[r];
+    }
+    if (!any) break;
+    BZG_REQUIRE(round < 10000, BZG_EINVAL, "sampler made no progress: a region's state set misses its sampling box");
+    const long long total = coff[R];
+    BZG_REQUIRE(total < (1ll << 30), BZG_EUNSUPPORTED, "too many sampler candidates in one round");
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_coff.ptr, coff.data(), (R + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_row0.ptr, row0.data(), R * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_dest.ptr, dest.data(), R * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_need.ptr, need.data(), R * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    cand.alloc(total * n * sizeof(double), c->stream);
+    flag.alloc((total + 1) * sizeof(int), c->stream);
+    pos.alloc((total + 1) * sizeof(int), c->stream);
+    RegionSampleDev rs{d_pcg.as<unsigned long long>(), d_lo.as<double>(), d_rng.as<double>(), d_off.as<int>(),
+                       d_A.as<double>(), d_b.as<double>(), d_coff.as<long long>(), d_row0.as<long long>(), n, R};
+    launch(c, "k_sample_regions", k_sample_regions, dim3(div_up(total, 256)), dim3(256), 0, rs, total,
+           cand.as<double>(), flag.as<int>());
+    BZG_CHECK_CUDA(cudaMemsetAsync(flag.as<int>() + total, 0, sizeof(int), c->stream));
+    exclusive_scan_i(c, flag.as<int>(), pos.as<int>(), total + 1);
+    launch(c, "k_scatter_regions", k_scatter_regions, dim3(div_up(total, 256)), dim3(256), 0, cand.as<double>(),
+           flag.as<int>(), pos.as<int>(), d_coff.as<long long>(), R, total, n, d_dest.as<long long>(),
+           d_need.as<long long>(), d_out);
+    launch(c, "k_region_acc", k_region_acc, dim3(div_up(R, 256)), dim3(256), 0, pos.as<int>(), d_coff.as<long long>(),
+           R, d_acc.as<long long>());
+    BZG_CHECK_CUDA(cudaMemcpyAsync(hacc, d_acc.ptr, R * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    for (int r = 0; r < R; ++r) {
+      if (need[r] <= 0) continue;
+      const long long cnt = coff[r + 1] - coff[r];
+      const long long take = std::min(hacc[r], need[r]);  // the first need[r] acceptances of the stream
+      got[r] += take;
+      need[r] -= take;
+      row0[r] += cnt;
+      est[r] = std::max(1e-3, (double)hacc[r] / (double)cnt);
+    }
   }
 }
 
@@ -590,18 +843,20 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
   DevBuf dF;
   dF.alloc((size_t)nF * 2 * n * sizeof(double), c->stream);
   BZG_CHECK_CUDA(cudaMemcpyAsync(dF.ptr, d->F, (size_t)nF * 2 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  DevBuf a1c, a2t, sok, dok;
+  DevBuf &a1c = c->ws[WS_A1C], &a2t = c->ws[WS_A2T];
+  DevBuf sok, dok;
   a1c.alloc((size_t)V * Kpad * sizeof(double), c->stream);
   a2t.alloc((size_t)V * Kpad * sizeof(double), c->stream);
   sok.alloc(V, c->stream);
   dok.alloc(V, c->stream);
   const long long W = (V + 31) / 32;
-  DevBuf bits, rowcnt, rptr;
+  DevBuf &bits = c->ws[WS_BITS], &rowcnt = c->ws[WS_ROWCNT], &rptr = c->ws[WS_RPTR];
   bits.alloc((size_t)std::max(rows, 1ll) * W * sizeof(uint32_t), c->stream);
   rowcnt.alloc((size_t)(rows + 1) * sizeof(unsigned long long), c->stream);
   rptr.alloc((size_t)(rows + 1) * sizeof(long long), c->stream);
   BZG_CHECK_CUDA(cudaMemsetAsync(rowcnt.ptr, 0, (rows + 1) * sizeof(unsigned long long), c->stream));
   BZG_CHECK_CUDA(cudaMemsetAsync(bits.ptr, 0, (size_t)std::max(rows, 1ll) * W * sizeof(uint32_t), c->stream));
+  c->trace("pairs: alloc+memset");
 
   // ---- Morton order of the positions (first m coordinates); the box only steers tiling
   const int m = g->m;
@@ -706,6 +961,7 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
     rm = RegionMasks{smask.as<unsigned long long>(), dmask.as<unsigned long long>(), tor.as<unsigned long long>(),
                      gor.as<unsigned long long>(), rr.RW};
   }
+  c->trace("pairs: morton+proj+regions");
   DevBuf tmin, tmax, gmin, gmax;
   tmin.alloc(ng * Kpad * sizeof(double), c->stream);
   tmax.alloc(ng * Kpad * sizeof(double), c->stream);
@@ -731,6 +987,13 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
     }
 #undef BZG_K
   }
+  if (d->k_nearest >= 0 && !never && rows > 0) {
+    BZG_REQUIRE(m <= 3, BZG_EUNSUPPORTED, "k_nearest prefilter supports m <= 3");
+    const long long k = std::min<long long>(d->k_nearest, V - 1);
+    launch(c, "k_knn_rows", k_knn_rows, dim3((unsigned)rows), dim3(kKnnThreads), 0, g->vertices.as<double>(), V, n, m,
+           k, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>());
+  }
+  c->trace("pairs: tiles(+knn)");
   exclusive_scan_ll(c, rowcnt.as<unsigned long long>(), rptr.as<long long>(), rows + 1);
   long long* h = static_cast<long long*>(c->host_scratch(sizeof(long long)));
   BZG_CHECK_CUDA(cudaMemcpyAsync(h, rptr.as<long long>() + rows, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
@@ -742,6 +1005,7 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
   g->dst.alloc(E * sizeof(int), c->stream);
   g->cost.alloc(E * sizeof(double), c->stream);
   g->row_ptr.alloc((V + 1) * sizeof(long long), c->stream);
+  c->trace("pairs: scan+csr alloc");
   DParams dp{};
   for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
   if (E > 0) {

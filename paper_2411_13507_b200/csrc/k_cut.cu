@@ -505,7 +505,8 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
   mk->qp_status.alloc(n_inst, c->stream);
   mk->qp_iters.alloc(n_inst * sizeof(int), c->stream);
   mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
-  DevBuf d_x, d_res, d_next, d_zy, d_list;
+  DevBuf &d_x = c->ws[WS_QX], &d_res = c->ws[WS_QRES], &d_zy = c->ws[WS_QZY], &d_list = c->ws[WS_QLIST];
+  DevBuf d_next;
   d_x.alloc(n_inst * NV * sizeof(double), c->stream);
   d_res.alloc(n_inst * 2 * sizeof(double), c->stream);
   d_safe.alloc(n_inst, c->stream);
@@ -613,7 +614,8 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
     using Rec = ObsRec<Mc>;
     const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
-    DevBuf d_obs, d_kill, d_qkill, d_saved, d_cnt;
+    DevBuf d_obs, d_cnt;
+    DevBuf &d_kill = c->ws[WS_KILL], &d_qkill = c->ws[WS_QKILL], &d_saved = c->ws[WS_SAVED];
     d_obs.alloc(sizeof(Rec) * h.size(), c->stream);
     BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, h.data(), sizeof(Rec) * h.size(), cudaMemcpyHostToDevice, c->stream));
     d_kill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
@@ -631,7 +633,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     bool any_general = false;
     for (int o = 0; o < n_obs; ++o) any_general |= h[o].is_box == 0.0;
     unsigned long long gen_cap = any_general ? cap : 1;
-    DevBuf d_pend, d_gen;
+    DevBuf &d_pend = c->ws[WS_PEND], &d_gen = c->ws[WS_GEN];
     unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
     unsigned long long* dcnt = d_cnt.as<unsigned long long>();
     // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
@@ -680,7 +682,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     for (int o = 0; o < n_obs; ++o) canon_all = canon_all && h[o].canon != 0.0;
     auto run_qp = [&](auto C_) {
       constexpr int Cc = decltype(C_)::value;
-      DevBuf d_safe;
+      DevBuf &d_safe = c->ws[WS_QSAFE];
       qp_solve<Gc, Mc, Cc>(c, g, dp, d_obs.as<Rec>(), canon_all, d_pend.as<unsigned long long>(), n_inst, cfg,
                            cfg->qp_polish ? 1 : 0, polish_screen(), mk, d_safe, trace);
       launch(c, "k_qp_verdicts", k_qp_verdicts, dim3(div_up(n_inst, 256)), dim3(256), 0,
@@ -784,7 +786,7 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
     Mask mk;
     mk.g = &g;
     mk.E = B;
-    DevBuf d_safe;
+    DevBuf &d_safe = c->ws[WS_QSAFE];
     auto no_trace = [](const char*) {};
     dispatch_rows<Mc>(qp_rows, [&](auto C_) {
       qp_solve<Gc, Mc, decltype(C_)::value>(c, &g, dp, d_obs.as<Rec>(), canon_all, d_items.as<unsigned long long>(), B,

@@ -334,10 +334,12 @@ def build_graph(N, spec, oracle, bounds, seed, include=None, k_nearest=None, *, 
         raise ValueError("need at least two vertices")
     if bounds.dim != spec.n:
         raise ValueError(f"sampling bounds must be {spec.n}-dimensional")
-    if k_nearest is not None:
-        raise NotImplementedError("k_nearest prefilter (graph.py:162-170) is not implemented on device yet")
+    if k_nearest is not None and int(k_nearest) < 0:
+        raise ValueError("k_nearest must be non-negative")
     ctx = ctx or nat.default_context()
     d, keep, D = _build_desc(N, spec, oracle, bounds, seed, include, rows=rows)
+    if k_nearest is not None:
+        d.k_nearest = int(k_nearest)  # graph.py:162-170, on device (k_knn_rows)
     h = C.c_void_p()
     rc = ctx.lib.bzg_build_graph(ctx.handle, C.byref(d), C.byref(h))
     if rc == nat.BZG_EINVAL:

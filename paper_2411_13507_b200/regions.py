@@ -89,38 +89,63 @@ def region_boxes(regions) -> tuple[np.ndarray, np.ndarray]:
     return (np.ascontiguousarray(np.stack([b.lo for b in boxes])), np.ascontiguousarray(np.stack([b.hi for b in boxes])))
 
 
-def sample_region_states(N_per_region, spec, xd: Polytope, regions, sample: Box, seed, *, ctx=None) -> np.ndarray:
-    """Per-region samples (build_graph's sampler, default_rng([seed, r])) concatenated in region order."""
-    import ctypes as C
+@dataclass
+class RegionSampling:
+    """Host arrays of bzg_sample_region_states for one (spec, X_d, regions, sample box, seed)."""
 
+    N: np.ndarray        # (R,) int64 samples per region
+    pcg: np.ndarray      # (R, 4) uint64 PCG64 words of default_rng([seed, r])
+    lo: np.ndarray       # (R, n) sampling boxes
+    hi: np.ndarray
+    row_off: np.ndarray  # (R+1,) int32 rows of each region's state set
+    A: np.ndarray        # (rows, n)
+    b: np.ndarray        # (rows,)
+
+    @property
+    def total(self) -> int:
+        return int(self.N.sum())
+
+
+def region_sampling(N_per_region, spec, xd: Polytope, regions, sample: Box, seed) -> RegionSampling:
+    from .graph import _f64, _pcg_words
+
+    R = len(regions)
+    counts = np.full(R, int(N_per_region), np.int64) if np.isscalar(N_per_region) else np.asarray(
+        N_per_region, np.int64)
+    pcg = np.array([_pcg_words([seed, r]) for r in range(R)], dtype=np.uint64).reshape(R, 4)
+    bnds = [region_sample_bounds(Rg, sample, spec.m) for Rg in regions]
+    sets = [region_state_set(xd, Rg, spec.n) for Rg in regions]
+    off = np.concatenate([[0], np.cumsum([s.A.shape[0] for s in sets])]).astype(np.int32)
+    return RegionSampling(counts, np.ascontiguousarray(pcg), _f64(np.stack([b.lo for b in bnds])),
+                          _f64(np.stack([b.hi for b in bnds])), off, _f64(np.vstack([s.A for s in sets])),
+                          _f64(np.concatenate([s.b for s in sets])))
+
+
+def sample_region_states(N_per_region, spec, xd: Polytope, regions, sample: Box, seed, *, ctx=None,
+                         sampling: RegionSampling | None = None) -> np.ndarray:
+    """Per-region samples (build_graph's sampler, default_rng([seed, r])) concatenated in region
+    order, all regions in one device call (bzg_sample_region_states)."""
     from . import _native as nat
-    from .graph import EPS_GEO, _f64, _pcg_words
+    from .graph import EPS_GEO
 
     ctx = ctx or nat.default_context()
-    counts = [N_per_region] * len(regions) if np.isscalar(N_per_region) else list(N_per_region)
-    parts = []
-    for r, (R, N) in enumerate(zip(regions, counts)):
-        bnd = region_sample_bounds(R, sample, spec.m)
-        X = region_state_set(xd, R, spec.n)
-        A, b, lo, hi = _f64(X.A), _f64(X.b), _f64(bnd.lo), _f64(bnd.hi)
-        d = nat.BuildDesc()
-        d.m, d.gamma, d.p = int(spec.m), int(spec.gamma), int(spec.p)
-        d.N = int(N)
-        d.eps_geo = EPS_GEO
-        d.pcg_state_hi, d.pcg_state_lo, d.pcg_inc_hi, d.pcg_inc_lo = _pcg_words([seed, r])
-        d.sample_lo, d.sample_hi = nat.ptr(lo), nat.ptr(hi)
-        d.xd_rows, d.xd_A, d.xd_b = A.shape[0], nat.ptr(A), nat.ptr(b)
-        out = np.empty((int(N), spec.n))
-        nat.check(ctx.lib.bzg_sample_states(ctx.handle, C.byref(d), nat.ptr(out)))
-        parts.append(out)
-    return np.vstack(parts) if parts else np.zeros((0, spec.n))
+    s = sampling or region_sampling(N_per_region, spec, xd, regions, sample, seed)
+    out = np.empty((s.total, spec.n))
+    if not len(s.N):
+        return out
+    nat.check(ctx.lib.bzg_sample_region_states(ctx.handle, spec.n, len(s.N), nat.ptr(s.N), nat.ptr(s.pcg),
+                                               nat.ptr(s.lo), nat.ptr(s.hi), nat.ptr(s.row_off), nat.ptr(s.A),
+                                               nat.ptr(s.b), EPS_GEO, nat.ptr(out)))
+    return out
 
 
 def build_region_graph(N_per_region, spec, oracle, regions, sample: Box, seed, include=None, *, ctx=None,
-                       rows=None):
+                       rows=None, rows_added: RegionRows | None = None, sampling: RegionSampling | None = None):
     """Graph over several keep-in regions (module docstring); returns a ``graph.BezierGraph``.
 
     ``oracle`` is the base ReachOracle (X_d, U, tube); ``regions`` are position-space polytopes.
+    ``rows_added`` / ``sampling`` take the host constants (region_rows of the region oracles,
+    region_sampling) when the caller keeps them across calls, as it keeps ``oracle``.
     """
     import ctypes as C
 
@@ -130,9 +155,10 @@ def build_region_graph(N_per_region, spec, oracle, regions, sample: Box, seed, i
     ctx = ctx or nat.default_context()
     if sample.dim != spec.n:
         raise ValueError(f"sampling bounds must be {spec.n}-dimensional")
-    oracles = region_oracles(spec, oracle.Xd, oracle.U, oracle.tube, regions)
-    rr = region_rows(oracle, oracles)
-    V = sample_region_states(N_per_region, spec, oracle.Xd, regions, sample, seed, ctx=ctx)
+    rr = rows_added
+    if rr is None:
+        rr = region_rows(oracle, region_oracles(spec, oracle.Xd, oracle.U, oracle.tube, regions))
+    V = sample_region_states(N_per_region, spec, oracle.Xd, regions, sample, seed, ctx=ctx, sampling=sampling)
     if V.shape[0] < 2:
         raise ValueError("need at least two vertices")
     d, keep, D = G._build_desc(V.shape[0], spec, oracle, sample, seed, include, vertices=V, rows=rows)

@@ -347,7 +347,25 @@ def case_heur_general():
     print("heur_general:", np.bincount(np.array(code_l), minlength=3))
 
 
-CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general,
+def case_knn():
+    """build_graph with the k_nearest prefilter (graph.py:162-170), k in {1, 12, 60} and k >= V-1."""
+    s = rsc.random_field_scenario(3, n_obstacles=0, graph_n=400)
+    oracle = bg.build_oracle(s.spec, s.xd, s.u_bounds, s.tube)
+    rec = {"env": json.dumps(env_info()), "F": oracle.F, "G": oracle.G, "xd_A": oracle.Xd.A, "xd_b": oracle.Xd.b,
+           "bounds_lo": s.sample_bounds.lo, "bounds_hi": s.sample_bounds.hi, "m": s.spec.m, "gamma": s.spec.gamma,
+           "T": s.spec.T, "N": 400, "seed": 7, "ks": np.array([1, 12, 60, 500])}
+    for k in rec["ks"]:
+        g = rg.build_graph(400, s.spec, oracle, s.sample_bounds, 7, k_nearest=int(k))
+        rec[f"edges_k{k}"] = g.edges
+        rec[f"costs_k{k}"] = g.costs
+    g = rg.build_graph(400, s.spec, oracle, s.sample_bounds, 7)
+    rec["edges_all"] = g.edges
+    rec["vertices"] = g.vertices
+    np.savez_compressed(OUT / "knn400.npz", **rec)
+    print("knn400:", {int(k): rec[f"edges_k{k}"].shape[0] for k in rec["ks"]}, "all", g.num_edges)
+
+
+CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general, "knn": case_knn,
          "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
                                                               ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
                                                               ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,

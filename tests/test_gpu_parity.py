@@ -215,3 +215,19 @@ def test_polish_screen_keeps_verdicts(ctx, golden, name, monkeypatch):
     assert np.array_equal(full.provenance_codes, fast.provenance_codes)
     assert (full.qp_safe, full.qp_unsafe) == (fast.qp_safe, fast.qp_unsafe)
     assert np.array_equal(full.alive, g["alive"])
+
+
+def test_knn_prefilter(ctx, golden):
+    """build_graph(k_nearest=k) on device (k_knn_rows) against the live reference's edges and costs."""
+    from tests.test_oracle_golden import _knn_inputs
+
+    g = golden("knn400")
+    spec, orc, bounds = _knn_inputs(g)
+    for k in g["ks"]:
+        gr = G.build_graph(int(g["N"]), spec, orc, bounds, int(g["seed"]), k_nearest=int(k), ctx=ctx)
+        assert np.array_equal(gr.edges, g[f"edges_k{k}"]), k
+        assert gr.costs.tobytes() == g[f"costs_k{k}"].tobytes(), k
+    gr = G.build_graph(int(g["N"]), spec, orc, bounds, int(g["seed"]), k_nearest=0, ctx=ctx)
+    assert gr.num_edges == 0
+    with pytest.raises(ValueError):
+        G.build_graph(int(g["N"]), spec, orc, bounds, int(g["seed"]), k_nearest=-1, ctx=ctx)

@@ -124,3 +124,23 @@ def test_general_heuristic_bitwise(golden):
         except ValueError:
             hp = np.full(3, np.nan)
         assert np.array_equal(hp, g["hyperplanes"][i], equal_nan=True), i
+
+
+def _knn_inputs(g):
+    from types import SimpleNamespace
+
+    from paper_2411_13507_b200.bezier import BezierSpec
+    from paper_2411_13507_b200.geometry import Box, Polytope
+
+    spec = BezierSpec(int(g["m"]), int(g["gamma"]), float(g["T"]))
+    orc = SimpleNamespace(F=g["F"], G=g["G"], Xd=Polytope(g["xd_A"], g["xd_b"]))
+    return spec, orc, Box(g["bounds_lo"], g["bounds_hi"])
+
+
+def test_knn_prefilter_bitwise(golden):
+    """k_nearest prefilter (graph.py:162-170) against the live reference."""
+    g = golden("knn400")
+    spec, orc, bounds = _knn_inputs(g)
+    for k in g["ks"]:
+        out = oracle.build_graph(int(g["N"]), spec, orc, bounds, int(g["seed"]), D=np.eye(4), k_nearest=int(k))
+        assert np.array_equal(out["edges"], g[f"edges_k{k}"]), k
