@@ -524,17 +524,29 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
   qp.eps_rel = cfg->qp_eps_rel;
   qp.eps_pinf = cfg->qp_eps_pinf;
   qp.max_iter = cfg->qp_max_iter;
+  static const int batch_env = std::getenv("BZG_ADMM_BATCH") ? std::atoi(std::getenv("BZG_ADMM_BATCH")) : 0;
+  qp.batch = batch_env > 0 ? batch_env : kAdmmBatch;
   // persistent grid: enough resident warps to cover the SMs several times
   const long long blocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 16);
   const bool rel = cfg->qp_eps_rel != 0.0, unit = cfg->qp_rho == 1.0;
   auto admm = rel ? (unit ? k_qp_admm<G, M, C, true, true, false> : k_qp_admm<G, M, C, true, false, false>)
                   : (unit ? k_qp_admm<G, M, C, false, true, false> : k_qp_admm<G, M, C, false, false, false>);
+  auto setup = k_qp_setup<G, M, C, false>;
+  size_t nconst = QpConsts<G, M, C, false>::N;
   if constexpr (C == 2 * M)
-    if (canon && unit && !rel) admm = k_qp_admm<G, M, C, false, true, true>;
+    if (canon && unit && !rel) {
+      admm = k_qp_admm<G, M, C, false, true, true>;
+      setup = k_qp_setup<G, M, C, true>;
+      nconst = QpConsts<G, M, C, true>::N;
+    }
+  DevBuf& d_consts = c->ws[WS_QCONST];
+  d_consts.alloc(n_inst * nconst * sizeof(double), c->stream);
   trace("qp alloc");
-  launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, dp, g->vertices.as<double>(),
-         g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, d_next.as<unsigned long long>(),
-         mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(), d_zy.as<double>());
+  launch(c, "k_qp_setup", setup, dim3(div_up(n_inst, 128)), dim3(128), 0, qp, dp, g->vertices.as<double>(),
+         g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, d_consts.as<double>());
+  launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, d_consts.as<double>(), n_inst,
+         d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
+         d_zy.as<double>());
   trace("admm");
   BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
   launch(c, "k_qp_select", k_qp_select<G, M, C>, dim3(div_up(n_inst, 256)), dim3(256), 0, dp,

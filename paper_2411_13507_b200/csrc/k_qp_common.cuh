@@ -18,6 +18,7 @@ namespace {
 struct QpParams {
   double rho, rho_eq, sigma, alpha, one_m_alpha, eps_abs, eps_rel, eps_pinf;
   int max_iter;
+  int batch;  // iterations between lane refills in k_qp_admm
 };
 
 // Q = A_O @ points (graph.py:276): BLAS product, FMA chain over the m output dimensions.
