@@ -343,17 +343,21 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
         // primal-infeasibility certificate (qpsolver.py:193-209): with every dy_i on a finite
         // bound, support = sum_c b_c dy_c + dy_eq.  The three conditions are tested cheapest
         // first (few lanes of a warp take this branch, so its length is paid warp-wide).
-        double dmax = fabs(dye);
+        // supp <= -eps_pinf * dmax with dmax > 1e-13 implies supp < 0: test that first
+        double supp = 0.0;
 #pragma unroll
-        for (int j = 0; j < J; ++j) dmax = max_nn(dmax, fabs(dyl[j]));
+        for (int c = 0; c < C; ++c) supp = __dadd_rn(supp, __dmul_rn(b[c], dyc[c]));
+        supp = __dadd_rn(supp, dye);
+        double dmax = 0.0;
+        if (supp < 0.0) {
+          dmax = fabs(dye);
 #pragma unroll
-        for (int c = 0; c < C; ++c) dmax = max_nn(dmax, fabs(dyc[c]));
+          for (int j = 0; j < J; ++j) dmax = max_nn(dmax, fabs(dyl[j]));
+#pragma unroll
+          for (int c = 0; c < C; ++c) dmax = max_nn(dmax, fabs(dyc[c]));
+        }
         if (dmax > 1e-13) {
           const double lim = qp.eps_pinf * dmax;
-          double supp = 0.0;
-#pragma unroll
-          for (int c = 0; c < C; ++c) supp = __dadd_rn(supp, __dmul_rn(b[c], dyc[c]));
-          supp = __dadd_rn(supp, dye);
           if (supp <= -lim) {  // then ||A'dy||_inf <= lim: delta columns, then lambda columns
             bool small = true;
 #pragma unroll
