@@ -260,8 +260,18 @@ __device__ __forceinline__ void warp_append(bool want_me, unsigned long long ite
   }
 }
 
+constexpr int kHeurThreads = 256, kHeurWarps = kHeurThreads / 32;
+constexpr int kHeurRound = 8;  // pass-2 pairs per edge per round
+
+// dynamic shared memory of k_cut_heuristic: obstacles, per-warp control points, pair lists, kills
 template <int G, int M>
-__global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
+size_t heur_smem(int nob) {
+  return sizeof(ObsRec<M>) * nob + (size_t)kHeurWarps * 32 * (M * 2 * G) * sizeof(double) +
+         (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t) + (size_t)kHeurWarps * 32 * sizeof(int);
+}
+
+template <int G, int M>
+__global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
                                 const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs, int o0, int o1,
                                 double margin, int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                                 unsigned long long* __restrict__ n_pend, unsigned long long cap,
@@ -280,7 +290,7 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
   __syncthreads();
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = e < E;
-  double P[M][2 * G];
+  double P[M][2 * G] = {};
   int kill = 0x7fffffff;
   if (valid) {
     double xi[N], xj[N];
@@ -311,23 +321,66 @@ __global__ void k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long 
       else hard |= 1ull << oi;
     }
   }
-  // pass 2: exact codes for the remaining obstacles, in list order
-  while (hard) {
-    const int oi = __ffsll((long long)hard) - 1;
-    hard &= hard - 1;
-    const ObsRec<M>& o = s_obs[oi];
-    int code;
-    if (o.is_box == 0.0) code = any_inside_einsum<G, M>(P, o) ? 0 : 3;  // 3: decided by k_cut_general
-    else code = o.canon != 0.0 ? box_code_canon<G, M>(P, o, margin) : box_code<G, M>(P, o, margin);
-    c0 += code == 0;
-    c1 += code == 1;
-    c2 += code == 2;
-    if (code == 0 && kill > o0 + oi) kill = o0 + oi;
-    const unsigned long long item = ((unsigned long long)e << 20) | (unsigned long long)(o0 + oi);
-    warp_append(code == 2, item, n_pend, cap, pend);
-    warp_append(code == 3, item, n_gen, gen_cap, gen_pend);
+  // pass 2 (warp-cooperative): the uncertified (edge, obstacle) pairs of the warp's 32 edges
+  // are dealt out to all 32 lanes, a round of at most kHeurRound pairs per edge at a time, so
+  // lanes whose edge has few hard obstacles do not idle while others work through theirs.
+  // Each lane's control points are staged in shared memory for the lanes that take its pairs.
+  constexpr int NP = M * 2 * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = smem_raw + sizeof(ObsRec<M>) * nob;
+  double* s_P = reinterpret_cast<double*>(base) + (size_t)warp * 32 * NP;
+  base += (size_t)kHeurWarps * 32 * NP * sizeof(double);
+  uint16_t* s_it = reinterpret_cast<uint16_t*>(base) + warp * 32 * kHeurRound;
+  base += (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t);
+  int* s_kill = reinterpret_cast<int*>(base) + warp * 32;
+#pragma unroll
+  for (int k = 0; k < M; ++k)
+#pragma unroll
+    for (int j = 0; j < 2 * G; ++j) s_P[lane * NP + k * 2 * G + j] = P[k][j];
+  s_kill[lane] = kill;
+  const long long e0 = e - lane;
+  __syncwarp();
+  while (__any_sync(0xffffffffu, hard != 0)) {
+    const int cnt = min(__popcll(hard), kHeurRound);
+    int off = cnt;  // inclusive warp scan of cnt
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, off, d);
+      if (lane >= d) off += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= cnt;
+    for (int q = 0; q < cnt; ++q) {
+      const int oi = __ffsll((long long)hard) - 1;
+      hard &= hard - 1;
+      s_it[off + q] = (uint16_t)((lane << 8) | oi);
+    }
+    __syncwarp();
+    for (int b0 = 0; b0 < total; b0 += 32) {
+      int code = -1;
+      unsigned long long item = 0;
+      if (b0 + lane < total) {
+        const int it = s_it[b0 + lane], owner = it >> 8, oi = it & 255;
+        double Pq[M][2 * G];
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+#pragma unroll
+          for (int j = 0; j < 2 * G; ++j) Pq[k][j] = s_P[owner * NP + k * 2 * G + j];
+        const ObsRec<M>& o = s_obs[oi];
+        if (o.is_box == 0.0) code = any_inside_einsum<G, M>(Pq, o) ? 0 : 3;  // 3: decided by k_cut_general
+        else code = o.canon != 0.0 ? box_code_canon<G, M>(Pq, o, margin) : box_code<G, M>(Pq, o, margin);
+        c0 += code == 0;
+        c1 += code == 1;
+        c2 += code == 2;
+        if (code == 0) atomicMin(s_kill + owner, o0 + oi);
+        item = ((unsigned long long)(e0 + owner) << 20) | (unsigned long long)(o0 + oi);
+      }
+      warp_append(code == 2, item, n_pend, cap, pend);
+      warp_append(code == 3, item, n_gen, gen_cap, gen_pend);
+    }
+    __syncwarp();
   }
-  if (valid) first_kill[e] = kill;
+  if (valid) first_kill[e] = s_kill[lane];
   // block reduction of the three counters
   typedef cub::BlockReduce<unsigned long long, 256> BR;
   __shared__ typename BR::TempStorage tmp;
@@ -661,10 +714,10 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       d_gen.alloc(gen_cap * sizeof(unsigned long long), c->stream);
       for (int o0 = 0; o0 < n_obs; o0 += chunk) {
         const int o1 = std::min(n_obs, o0 + chunk);
-        const size_t smem = sizeof(Rec) * (o1 - o0);
+        const size_t smem = heur_smem<Gc, Mc>(o1 - o0);
         auto kern = k_cut_heuristic<Gc, Mc>;
         BZG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        launch(c, "k_cut_heuristic", kern, dim3(div_up(E, 256)), dim3(256), smem, dp, g->vertices.as<double>(), E,
+        launch(c, "k_cut_heuristic", kern, dim3(div_up(E, kHeurThreads)), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(), E,
                g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), o0, o1, cfg->heur_margin, d_kill.as<int>(), dcnt,
                dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>());
       }
