@@ -306,34 +306,39 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
         if (REL) { rprim = fmax(rprim, fabs(r)); maxAx = fmax(maxAx, fabs(sl)); }
         else conv &= fabs(r) <= eps;
       }
-      double ql[C];
-      Q.mul(lam, ql);
+      // (forming these only when the cheaper tests passed was tried: the branch is taken by
+      // some lane of most warps and the kernel got 2% slower)
+      {
+        double ql[C];
+        Q.mul(lam, ql);
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const double ax = __dsub_rn(ql[c], del[c]);
-        const double r = __dsub_rn(ax, zc[c]);
-        if (REL) {
-          rprim = fmax(rprim, fabs(r)); maxAx = fmax(maxAx, fabs(ax)); maxz = fmax(maxz, fabs(zc[c]));
-        } else {
-          conv &= fabs(r) <= eps;
+        for (int c = 0; c < C; ++c) {
+          const double ax = __dsub_rn(ql[c], del[c]);
+          const double r = __dsub_rn(ax, zc[c]);
+          if (REL) {
+            rprim = fmax(rprim, fabs(r)); maxAx = fmax(maxAx, fabs(ax)); maxz = fmax(maxz, fabs(zc[c]));
+          } else {
+            conv &= fabs(r) <= eps;
+          }
         }
-      }
-      double fY[QOps<G, M, C, CANON>::R];
-      Q.fold(yc, fY);
+        double fY[QOps<G, M, C, CANON>::R];
+        Q.fold(yc, fY);
 #pragma unroll
-      for (int j = 0; j < J; ++j) {
-        const double acc = Q.tmulf(j, fY, __dadd_rn(yl[j], ye));
-        if (REL) { rdual = fmax(rdual, fabs(acc)); maxATy = fmax(maxATy, fabs(acc)); }
-        else conv &= fabs(acc) <= eps;
-      }
+        for (int j = 0; j < J; ++j) {
+          const double acc = Q.tmulf(j, fY, __dadd_rn(yl[j], ye));
+          if (REL) { rdual = fmax(rdual, fabs(acc)); maxATy = fmax(maxATy, fabs(acc)); }
+          else conv &= fabs(acc) <= eps;
+        }
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const double px = __dmul_rn(2.0, del[c]);
-        const double r = __dsub_rn(px, yc[c]);
-        if (REL) {
-          rdual = fmax(rdual, fabs(r)); maxPx = fmax(maxPx, fabs(px)); maxATy = fmax(maxATy, fabs(yc[c]));
-        } else {
-          conv &= fabs(r) <= eps;
+        for (int c = 0; c < C; ++c) {
+          // P x - ... = 2 delta_c - y_c; 2 delta_c is exact, so one FMA rounds like the subtraction
+          const double r = __fma_rn(2.0, del[c], -yc[c]);
+          if (REL) {
+            rdual = fmax(rdual, fabs(r)); maxPx = fmax(maxPx, fabs(__dmul_rn(2.0, del[c])));
+            maxATy = fmax(maxATy, fabs(yc[c]));
+          } else {
+            conv &= fabs(r) <= eps;
+          }
         }
       }
       if (REL) conv = rprim <= eps + qp.eps_rel * fmax(maxAx, maxz) && rdual <= eps + qp.eps_rel * fmax(maxPx, maxATy);
