@@ -617,6 +617,7 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
   BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
   const long long n_list = (long long)*hn;
   mk->n_polished = n_list;
+  if (c->trace_on) std::fprintf(stderr, "[bzg cut] qp instances %lld, polished %lld\n", n_inst, n_list);
   constexpr int NR = polish_dim<G, M, C>();
   const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
   BZG_CHECK_CUDA(cudaFuncSetAttribute(k_qp_polish<G, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));

@@ -365,7 +365,28 @@ def case_knn():
     print("knn400:", {int(k): rec[f"edges_k{k}"].shape[0] for k in rec["ks"]}, "all", g.num_edges)
 
 
+def case_m3():
+    """Three output dimensions (m=3, gamma=2): 3-D boxes through the whole path."""
+    spec = bg.BezierSpec(m=3, gamma=2, T=1.0)
+    xd = rgeo.Box(np.array([0.0, 0, 0, -1.5, -1.5, -1.5]), np.array([5.0, 5, 5, 1.5, 1.5, 1.5])).to_polytope()
+    u = rgeo.Box(np.full(3, -6.0), np.full(3, 6.0))
+    tube = rsim.design_tube(spec, (6.0, 5.0), 0.02)
+    oracle = bg.build_oracle(spec, xd, u, tube)
+    sample = rgeo.Box(np.array([0.0, 0, 0, -0.6, -0.6, -0.6]), np.array([5.0, 5, 5, 0.6, 0.6, 0.6]))
+    rng = np.random.default_rng(2)
+    obs = []
+    for _ in range(8):
+        c = rng.uniform(0.8, 4.2, 3)
+        s = rng.uniform(0.3, 0.9, 3)
+        obs.append(rgeo.inflate(rgeo.Box(c - s / 2, c + s / 2).to_polytope(), tube.position_box(3)))
+    start = np.array([0.3, 0.3, 0.3, 0, 0, 0])
+    goal = np.array([4.7, 4.7, 4.7, 0, 0, 0])
+    capture("m3_600", 600, spec, oracle, sample, 4, np.array([start, goal]), obs, start, goal, full=True,
+            detail=True)
+
+
 CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general, "knn": case_knn,
+         "m3": case_m3,
          "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
                                                               ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
                                                               ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,
