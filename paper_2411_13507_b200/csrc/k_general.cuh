@@ -9,11 +9,12 @@
 //             the projection (residual <= 1e-7), first row on ties
 //   SAFE iff hp.normal @ P - hp.offset > margin for every control point, else INDETERMINATE.
 //
-// BLAS orders of the small products (m = 2, measured on the reference host, OpenBLAS
-// 0.3.30 SkylakeX kernels): gemm (pts @ A.T) is an FMA chain from the first term; gemv
-// (A @ x) is fma(a0, x0, a1 x1); vector @ matrix (normal @ pts) is fma(a0, x0, a1 x1) on
-// columns in blocks of four and the FMA chain on the tail columns; the 1-D norm is
-// sqrt(fma(v1, v1, v0 v0)).  The ADMM itself agrees with the reference to rounding, so
+// BLAS orders of the small products (measured on the reference host, OpenBLAS 0.3.30
+// SkylakeX kernels): gemm (pts @ A.T) is an FMA chain from the first term (m = 2, 3); gemv
+// (A @ x) is fma(a0, x0, a1 x1), and fma(a2, x2, fma(a0, x0, a1 x1)) for m = 3; vector @
+// matrix (normal @ pts) is fma(a0, x0, a1 x1) (m = 2) / a2 x2 + fma(a0, x0, a1 x1) (m = 3) on
+// columns in blocks of four and the FMA chain on the tail columns; the 1-D norm is the FMA
+// chain sqrt(fma(v1, v1, v0 v0)) (m = 2, 3).  The ADMM itself agrees with the reference to rounding, so
 // this row's parity class is the epsilon band.
 #pragma once
 
@@ -26,9 +27,21 @@ constexpr int kGenMaxIter = 20000;
 template <int M>
 __device__ __forceinline__ double gemv_row(const double* a, const double* x) {  // A_c @ x (gemv order)
   if (M == 2) return __fma_rn(a[0], x[0], __dmul_rn(a[1], x[1]));
-  double acc = __dmul_rn(a[M - 1], x[M - 1]);
+  if (M == 3) return __fma_rn(a[2], x[2], __fma_rn(a[0], x[0], __dmul_rn(a[1], x[1])));
+  double acc = __dmul_rn(a[0], x[0]);
 #pragma unroll
-  for (int k = M - 2; k >= 0; --k) acc = __fma_rn(a[k], x[k], acc);
+  for (int k = 1; k < M; ++k) acc = __fma_rn(a[k], x[k], acc);
+  return acc;
+}
+
+// column of vector @ matrix inside a block of four columns (the tail columns take the chain)
+template <int M>
+__device__ __forceinline__ double vecmat_block(const double* n, const double* p) {
+  if (M == 2) return __fma_rn(n[0], p[0], __dmul_rn(n[1], p[1]));
+  if (M == 3) return __dadd_rn(__dmul_rn(n[2], p[2]), __fma_rn(n[0], p[0], __dmul_rn(n[1], p[1])));
+  double acc = __dmul_rn(n[0], p[0]);
+#pragma unroll
+  for (int k = 1; k < M; ++k) acc = __fma_rn(n[k], p[k], acc);
   return acc;
 }
 
@@ -320,7 +333,7 @@ __device__ int general_code(const double (&P)[M][2 * G], const ObsRec<M>& o, dou
     double p[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) p[k] = P[k][j];
-    const double hp = (M == 2 && j < tail0) ? gemv_row<M>(normal, p) : gemm_row<M>(normal, p);
+    const double hp = j < tail0 ? vecmat_block<M>(normal, p) : gemm_row<M>(normal, p);
     clear &= __dsub_rn(hp, off) > margin;
   }
   return clear ? 1 : 2;

@@ -365,6 +365,57 @@ def case_knn():
     print("knn400:", {int(k): rec[f"edges_k{k}"].shape[0] for k in rec["ks"]}, "all", g.num_edges)
 
 
+def _rotation(rng):
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    return q
+
+
+def general_obstacles_3d():
+    """3-D convex non-box obstacles: rotated box (6 rows), octahedron (8), tetrahedron (4)."""
+    rng = np.random.default_rng(9)
+    out = []
+    base = {
+        "box": np.vstack([np.eye(3), -np.eye(3)]),
+        "octa": np.array([[sx, sy, sz] for sx in (1, -1) for sy in (1, -1) for sz in (1, -1)], float),
+        "tetra": np.array([[1, 1, 1], [1, -1, -1], [-1, 1, -1], [-1, -1, 1]], float),
+    }
+    for name, ctr, rad in (("box", (2.5, 2.5, 2.5), 0.5), ("octa", (1.3, 3.6, 2.0), 0.45),
+                           ("tetra", (3.6, 1.4, 3.0), 0.35), ("box", (1.2, 1.2, 3.8), 0.3)):
+        A = base[name] @ _rotation(rng).T * 1.3
+        out.append(rgeo.Polytope(A, A @ np.asarray(ctr) + rad * np.linalg.norm(A, axis=1)))
+    return out
+
+
+def case_heur_general3():
+    """Scalar cut_heuristic / closest_point / adjacent_hyperplane for m = 3 polytopes."""
+    rng = np.random.default_rng(4)
+    obs = general_obstacles_3d()
+    ctrs = [(2.5, 2.5, 2.5), (1.3, 3.6, 2.0), (3.6, 1.4, 3.0), (1.2, 1.2, 3.8)]
+    cfg = rg.CutConfig()
+    pts_l, oi_l, code_l, proj_l, hp_l = [], [], [], [], []
+    for i in range(240):
+        oi = i % len(obs)
+        O = obs[oi]
+        pts = np.asarray(ctrs[oi])[:, None] + rng.uniform(-1.0, 1.0, (3, 1)) + rng.uniform(-0.35, 0.35, (3, 4))
+        pts_l.append(pts)
+        oi_l.append(oi)
+        code_l.append({rg.CutVerdict.UNSAFE: 0, rg.CutVerdict.SAFE: 1, rg.CutVerdict.INDETERMINATE: 2}[
+            rg.cut_heuristic(pts, O, cfg)])
+        On = O.normalized()
+        proj_l.append(np.stack([rgeo.closest_point(On, p) for p in pts.T]))
+        try:
+            hp = rgeo.adjacent_hyperplane(On, pts[:, 0])
+            hp_l.append(np.concatenate([hp.normal, [hp.offset]]))
+        except ValueError:
+            hp_l.append(np.full(4, np.nan))
+    np.savez_compressed(OUT / "heur_general3.npz", points=np.stack(pts_l), obstacle=np.array(oi_l, np.int32),
+                        codes=np.array(code_l, np.int8), projections=np.stack(proj_l), hyperplanes=np.stack(hp_l),
+                        obs_n=np.array([o.num_rows for o in obs], np.int32),
+                        obs_A=np.concatenate([o.A for o in obs]), obs_b=np.concatenate([o.b for o in obs]),
+                        env=json.dumps(env_info()))
+    print("heur_general3:", np.bincount(np.array(code_l), minlength=3))
+
+
 def case_m3():
     """Three output dimensions (m=3, gamma=2): 3-D boxes through the whole path."""
     spec = bg.BezierSpec(m=3, gamma=2, T=1.0)
@@ -386,7 +437,7 @@ def case_m3():
 
 
 CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general, "knn": case_knn,
-         "m3": case_m3,
+         "m3": case_m3, "heur_general3": case_heur_general3,
          "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
                                                               ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
                                                               ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,

@@ -38,12 +38,13 @@ def _golden_polytopes(g):
     return [Polytope(g["obs_A"][off[i]:off[i + 1]], g["obs_b"][off[i]:off[i + 1]]) for i in range(len(g["obs_n"]))]
 
 
-def test_cut_heuristic_general_vs_reference(ctx, golden):
-    g = golden("heur_general")
+@pytest.mark.parametrize("name", ["heur_general", "heur_general3"])
+def test_cut_heuristic_general_vs_reference(ctx, golden, name):
+    g = golden(name)
     obs = _golden_polytopes(g)
     codes = G.cut_heuristic_batch(g["points"], obs, g["obstacle"], ctx=ctx)
     mism = np.nonzero(codes != g["codes"])[0]
-    print("heur_general codes", np.bincount(codes, minlength=3), "mismatch", mism.tolist())
+    print(name, "codes", np.bincount(codes, minlength=3), "mismatch", mism.tolist())
     assert mism.size == 0
     for i in range(0, 40, 7):  # the scalar drop-in agrees with the batch
         v = G.cut_heuristic(g["points"][i], obs[int(g["obstacle"][i])])

@@ -104,11 +104,12 @@ def _golden_obstacles(g):
     return [(g["obs_A"][off[i]:off[i + 1]], g["obs_b"][off[i]:off[i + 1]]) for i in range(len(g["obs_n"]))]
 
 
-def test_general_heuristic_bitwise(golden):
+@pytest.mark.parametrize("name", ["heur_general", "heur_general3"])
+def test_general_heuristic_bitwise(golden, name):
     """Scalar cut_heuristic / closest_point / adjacent_hyperplane on non-box polytopes
-    (graph.py:202-221, geometry.py:202-252) against the live reference (a subset: each
-    projection is a 20000-iteration-capped ADMM in numpy)."""
-    g = golden("heur_general")
+    (graph.py:202-221, geometry.py:202-252), m = 2 and 3, against the live reference (a
+    subset: each projection is a 20000-iteration-capped ADMM in numpy)."""
+    g = golden(name)
     obs = _golden_obstacles(g)
     gr = oracle.graph_ref
     for i in range(0, len(g["codes"]), 8):
@@ -122,7 +123,7 @@ def test_general_heuristic_bitwise(golden):
             n, o = gr.adjacent_hyperplane(OA, Ob, pts[:, 0])
             hp = np.concatenate([n, [o]])
         except ValueError:
-            hp = np.full(3, np.nan)
+            hp = np.full(g["hyperplanes"].shape[1], np.nan)
         assert np.array_equal(hp, g["hyperplanes"][i], equal_nan=True), i
 
 
