@@ -314,11 +314,19 @@ def main():
 
     from paper_2411_13507_b200 import _native as nat
 
+    # BZG_BENCH_DEVICE / BZG_DIST_BACKEND=gloo: functional check of the N>1 path with every rank
+    # on one GPU and host-side collectives (never a performance number: ranks share the device)
+    if os.environ.get("BZG_BENCH_DEVICE") is not None:
+        local = int(os.environ["BZG_BENCH_DEVICE"])
+    backend = os.environ.get("BZG_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = nat.Context(local, stream=stream.cuda_stream)
@@ -371,7 +379,8 @@ def main():
     ctx.set_profiling(False)
     ctx.profile_only(None)
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=coll_dev)
     if world > 1:
         torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
     total_ms = float(tot.item())
@@ -393,7 +402,7 @@ def main():
             e2e_ms.append((t1 - t0) * 1e3)
     clk = clocks.stop()  # sampled over the timed region and the e2e pass that follows it
     clk["window"] = "device-timed steps + e2e steps"
-    et = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
+    et = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device=coll_dev)
     if world > 1:
         torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
     e2e_step_ms = float(et.item())

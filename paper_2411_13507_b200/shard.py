@@ -19,6 +19,16 @@ def row_block(V: int, rank: int, world: int) -> tuple[int, int]:
     return (V * rank) // world, (V * (rank + 1)) // world
 
 
+def _coll(t, group=None):
+    """The tensor a collective runs on: device tensors as-is for NCCL, host copies for gloo
+    (the CPU test backend, which has no CUDA collectives)."""
+    import torch.distributed as dist
+
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        return t.cpu()
+    return t
+
+
 def allgather_varlen(t, sizes, group=None):
     """All-gather a 1-D tensor whose length differs per rank; returns the rank-ordered concatenation.
 
@@ -34,9 +44,10 @@ def allgather_varlen(t, sizes, group=None):
         return torch.zeros(0, dtype=t.dtype, device=t.device)
     pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
     pad[: t.numel()] = t
-    out = torch.empty(world * mx, dtype=t.dtype, device=t.device)
+    pad = _coll(pad, group)
+    out = torch.empty(world * mx, dtype=t.dtype, device=pad.device)
     dist.all_gather_into_tensor(out, pad, group=group)
-    return torch.cat([out[r * mx: r * mx + int(sizes[r])] for r in range(world)])
+    return torch.cat([out[r * mx: r * mx + int(sizes[r])] for r in range(world)]).to(t.device)
 
 
 def exchange_sizes(n: int, device, group=None) -> list[int]:
@@ -44,8 +55,8 @@ def exchange_sizes(n: int, device, group=None) -> list[int]:
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    t = torch.tensor([n], dtype=torch.int64, device=device)
-    out = torch.empty(world, dtype=torch.int64, device=device)
+    t = _coll(torch.tensor([n], dtype=torch.int64, device=device), group)
+    out = torch.empty(world, dtype=torch.int64, device=t.device)
     dist.all_gather_into_tensor(out, t, group=group)
     return [int(x) for x in out.tolist()]
 
@@ -77,8 +88,8 @@ def gather_to_all(graph, mask, group=None):
                                          C.c_void_p(prov.data_ptr())))
     sizes = exchange_sizes(E, dev, group)
     parts = [allgather_varlen(x[:E], sizes, group) for x in (src, dst, cost, alive, prov)]
-    cnt = torch.tensor([mask.pairs_total, mask.pairs_point_hit, mask.pairs_hyperplane, mask.pairs_qp, mask.qp_safe,
-                        mask.qp_unsafe], dtype=torch.int64, device=dev)
+    cnt = _coll(torch.tensor([mask.pairs_total, mask.pairs_point_hit, mask.pairs_hyperplane, mask.pairs_qp,
+                              mask.qp_safe, mask.qp_unsafe], dtype=torch.int64, device=dev), group)
     dist.all_reduce(cnt, group=group)
     Et = sum(sizes)
     s, d, c, a, p = (x.contiguous() for x in parts)
