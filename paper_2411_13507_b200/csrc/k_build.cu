@@ -303,7 +303,7 @@ struct RegionMasks {
 };
 
 template <int K, bool REG>
-__global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
+__global__ void __launch_bounds__(kPairThreads, 3) k_pair_tiles(
     Bounds bd, const double* __restrict__ a1c, const double* __restrict__ a2t, const uint8_t* __restrict__ src_ok,
     const uint8_t* __restrict__ dst_ok, const int* __restrict__ perm, const double* __restrict__ tmin,
     const double* __restrict__ tmax, const double* __restrict__ gmin, const double* __restrict__ gmax, long long V,
@@ -317,6 +317,37 @@ __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
   const long long tile = blockIdx.y;
   const long long i0 = tile * kTile;
   const int rows = (int)min((long long)kTile, V - i0);
+  const long long g = (long long)blockIdx.x * (kPairThreads / 32) + warp;
+  // ---- (tile, group) culls first: a block whose eight groups all fail skips the staging
+  bool live = g * kTile < V;
+  unsigned long long gor[kMaxRegionWords] = {0, 0, 0, 0}, dm[kMaxRegionWords] = {0, 0, 0, 0};
+  if (REG && live) {
+    bool share = false;
+#pragma unroll
+    for (int w = 0; w < kMaxRegionWords; ++w) {
+      if (w < rm.RW) {
+        gor[w] = rm.group_or[g * rm.RW + w];
+        share |= (gor[w] & rm.tile_or[tile * rm.RW + w]) != 0;
+      }
+    }
+    live = share;  // no region holds a source of the tile and a destination of the group
+  }
+  // interval bounds this lane watches in the cull tests: q = lane, lane + 32
+  constexpr int QL = (K + 31) / 32;
+  double gl[QL], gh[QL], lo_[QL], hi_[QL];
+  bool cull = false;
+#pragma unroll
+  for (int u = 0; u < QL; ++u) {
+    const int q = lane + 32 * u;
+    const bool on = live && q < K;
+    gl[u] = on ? gmin[g * K + q] : 0.0;
+    gh[u] = on ? gmax[g * K + q] : 0.0;
+    lo_[u] = q < K ? bd.lo[q] : -INFINITY;
+    hi_[u] = q < K ? bd.hi[q] : INFINITY;
+    if (on) cull |= (__dadd_rn(tmin[tile * K + q], gl[u]) > hi_[u]) | (__dadd_rn(tmax[tile * K + q], gh[u]) < lo_[u]);
+  }
+  live = live && !__any_sync(0xffffffffu, cull);  // else no pair of (tile, group) can pass
+  if (!__syncthreads_or(live)) return;
   for (int e = tid; e < rows * K; e += kPairThreads) {
     const int ii = e / K, q = e - ii * K;
     s_a1[ii][q] = a1c[(i0 + ii) * K + q];
@@ -328,35 +359,7 @@ __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
       for (int w = 0; w < kMaxRegionWords; ++w) s_sm[tid][w] = w < rm.RW ? rm.smask[(i0 + tid) * rm.RW + w] : 0ull;
   }
   __syncthreads();
-  const long long g = (long long)blockIdx.x * (kPairThreads / 32) + warp;
-  if (g * kTile >= V) return;
-  unsigned long long gor[kMaxRegionWords] = {0, 0, 0, 0}, dm[kMaxRegionWords] = {0, 0, 0, 0};
-  if (REG) {
-    bool share = false;
-#pragma unroll
-    for (int w = 0; w < kMaxRegionWords; ++w) {
-      if (w < rm.RW) {
-        gor[w] = rm.group_or[g * rm.RW + w];
-        share |= (gor[w] & rm.tile_or[tile * rm.RW + w]) != 0;
-      }
-    }
-    if (!share) return;  // no region holds a source of the tile and a destination of the group
-  }
-  // interval bounds this lane watches in the cull tests: q = lane, lane + 32
-  constexpr int QL = (K + 31) / 32;
-  double gl[QL], gh[QL], lo_[QL], hi_[QL];
-  bool cull = false;
-#pragma unroll
-  for (int u = 0; u < QL; ++u) {
-    const int q = lane + 32 * u;
-    const bool on = q < K;
-    gl[u] = on ? gmin[g * K + q] : 0.0;
-    gh[u] = on ? gmax[g * K + q] : 0.0;
-    lo_[u] = on ? bd.lo[q] : -INFINITY;
-    hi_[u] = on ? bd.hi[q] : INFINITY;
-    if (on) cull |= (__dadd_rn(tmin[tile * K + q], gl[u]) > hi_[u]) | (__dadd_rn(tmax[tile * K + q], gh[u]) < lo_[u]);
-  }
-  if (__any_sync(0xffffffffu, cull)) return;  // no pair of (tile, group) can pass
+  if (!live) return;
   const long long j = g * kTile + lane;
   double a2[K];
   bool jok = j < V;
@@ -411,6 +414,162 @@ __global__ void __launch_bounds__(kPairThreads) k_pair_tiles(
       const long long row = (long long)s_orig[ii] - r0;
       if (ok) atomicOr(bits + row * W + (orig_j >> 5), 1u << (orig_j & 31));
       if (lane == 0) atomicAdd(rowcnt + row, (unsigned long long)__popc(mk));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- compacted (tile, group) pairs
+// The same exact culls as k_pair_tiles' prologue, one thread per (source tile, destination
+// group), the survivors appended to a list.  A 2-D grid over every (tile, group) spends most
+// of its blocks on pairs that cull (cfg5 at 100k nodes: 1.2 M blocks), so the tests below run
+// over the list only.
+__global__ void k_tile_group_cull(Bounds bd, const double* __restrict__ tmin, const double* __restrict__ tmax,
+                                  const double* __restrict__ gmin, const double* __restrict__ gmax, long long ng,
+                                  int K, RegionMasks rm, int reg, unsigned long long* __restrict__ list,
+                                  unsigned long long* __restrict__ n_list) {
+  const long long tile = blockIdx.y;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  bool live = g < ng;
+  if (reg && live) {
+    bool share = false;
+    for (int w = 0; w < rm.RW; ++w) share |= (rm.group_or[g * rm.RW + w] & rm.tile_or[tile * rm.RW + w]) != 0;
+    live = share;
+  }
+  if (live) {
+    bool cull = false;
+    for (int q = 0; q < K && !cull; ++q)
+      cull = (__dadd_rn(tmin[tile * K + q], gmin[g * K + q]) > bd.hi[q]) |
+             (__dadd_rn(tmax[tile * K + q], gmax[g * K + q]) < bd.lo[q]);
+    live = !cull;
+  }
+  const unsigned want = __ballot_sync(0xffffffffu, live);
+  if (!want) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(want) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(n_list, (unsigned long long)__popc(want));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (live) list[base + __popc(want & ((1u << lane) - 1u))] = ((unsigned long long)tile << 32) | (unsigned long long)g;
+}
+
+template <int K, bool REG>
+size_t pair_list_smem() {
+  constexpr int NW = kPairThreads / 32;
+  return sizeof(double) * NW * kTile * K + (REG ? sizeof(unsigned long long) * NW * kTile * kMaxRegionWords : 0) +
+         sizeof(int) * NW * kTile + NW * kTile;
+}
+
+// One warp per surviving (tile, group): the tile's 32 sources against the group's 32
+// destinations, exactly k_pair_tiles' per-source cull and pair test, with the tile staged in
+// the warp's own shared-memory slice.  Persistent grid over the device-side list length.
+template <int K, bool REG>
+__global__ void __launch_bounds__(kPairThreads, 3) k_pair_list(
+    Bounds bd, const double* __restrict__ a1c, const double* __restrict__ a2t, const uint8_t* __restrict__ src_ok,
+    const uint8_t* __restrict__ dst_ok, const int* __restrict__ perm, const double* __restrict__ gmin,
+    const double* __restrict__ gmax, long long V, long long r0, long long W, uint32_t* __restrict__ bits,
+    unsigned long long* __restrict__ rowcnt, RegionMasks rm, const unsigned long long* __restrict__ list,
+    const unsigned long long* __restrict__ n_list) {
+  constexpr int NW = kPairThreads / 32, QL = (K + 31) / 32;
+  // dynamic shared memory (pair_list_smem): per warp a1 tile, region masks, original ids, flags
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto* s_a1_all = reinterpret_cast<double (*)[kTile][K]>(smem_raw);
+  auto* s_sm_all = reinterpret_cast<unsigned long long (*)[kTile][kMaxRegionWords]>(smem_raw +
+                                                                                    sizeof(double) * NW * kTile * K);
+  int* s_orig_all = reinterpret_cast<int*>(smem_raw + sizeof(double) * NW * kTile * K +
+                                           (REG ? sizeof(unsigned long long) * NW * kTile * kMaxRegionWords : 0));
+  uint8_t* s_ok_all = reinterpret_cast<uint8_t*>(s_orig_all + NW * kTile);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double (*s_a1)[K] = s_a1_all[warp];
+  uint8_t* s_ok = s_ok_all + warp * kTile;
+  int* s_orig = s_orig_all + warp * kTile;
+  const long long n = (long long)*n_list;
+  for (long long e = (long long)blockIdx.x * NW + warp; e < n; e += (long long)gridDim.x * NW) {
+    const unsigned long long it = list[e];
+    const long long tile = (long long)(it >> 32), g = (long long)(it & 0xffffffffull);
+    const long long i0 = tile * kTile;
+    const int rows = (int)min((long long)kTile, V - i0);
+    __syncwarp();
+    for (int t = lane; t < rows * K; t += 32) {
+      const int ii = t / K, q = t - ii * K;
+      s_a1[ii][q] = a1c[(i0 + ii) * K + q];
+    }
+    if (lane < rows) {
+      s_ok[lane] = src_ok[i0 + lane];
+      s_orig[lane] = perm[i0 + lane];
+      if (REG)
+        for (int w = 0; w < kMaxRegionWords; ++w)
+          s_sm_all[warp][lane][w] = w < rm.RW ? rm.smask[(i0 + lane) * rm.RW + w] : 0ull;
+    }
+    __syncwarp();
+    unsigned long long gor[kMaxRegionWords] = {0, 0, 0, 0}, dm[kMaxRegionWords] = {0, 0, 0, 0};
+    if (REG) {
+#pragma unroll
+      for (int w = 0; w < kMaxRegionWords; ++w) gor[w] = w < rm.RW ? rm.group_or[g * rm.RW + w] : 0ull;
+    }
+    double gl[QL], gh[QL], lo_[QL], hi_[QL];
+#pragma unroll
+    for (int u = 0; u < QL; ++u) {
+      const int q = lane + 32 * u;
+      const bool on = q < K;
+      gl[u] = on ? gmin[g * K + q] : 0.0;
+      gh[u] = on ? gmax[g * K + q] : 0.0;
+      lo_[u] = on ? bd.lo[q] : -INFINITY;
+      hi_[u] = on ? bd.hi[q] : INFINITY;
+    }
+    const long long j = g * kTile + lane;
+    double a2[K];
+    bool jok = j < V;
+    int orig_j = 0;
+    if (jok) {
+#pragma unroll
+      for (int q = 0; q < K; ++q) a2[q] = a2t[(long long)q * V + j];
+      jok = dst_ok[j] != 0;
+      orig_j = perm[j];
+      if (REG) {
+#pragma unroll
+        for (int w = 0; w < kMaxRegionWords; ++w) dm[w] = w < rm.RW ? rm.dmask[j * rm.RW + w] : 0ull;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < K; ++q) a2[q] = 0.0;
+    }
+    for (int ii = 0; ii < rows; ++ii) {
+      if (!s_ok[ii]) continue;
+      bool jreg = true;
+      if (REG) {
+        bool share = false;
+        jreg = false;
+#pragma unroll
+        for (int w = 0; w < kMaxRegionWords; ++w) {
+          share |= (s_sm_all[warp][ii][w] & gor[w]) != 0;
+          jreg |= (s_sm_all[warp][ii][w] & dm[w]) != 0;
+        }
+        if (!share) continue;  // uniform: the source shares no region with the group
+      }
+      bool c2 = false;
+#pragma unroll
+      for (int u = 0; u < QL; ++u) {
+        const int q = lane + 32 * u;
+        if (q < K) {
+          const double a = s_a1[ii][q];
+          c2 |= (__dadd_rn(a, gl[u]) > hi_[u]) | (__dadd_rn(a, gh[u]) < lo_[u]);
+        }
+      }
+      if (__any_sync(0xffffffffu, c2)) continue;
+      bool ok = jok && jreg && (i0 + ii != j);
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        if ((q & 1) == 0 && q > 0) {
+          if (!__any_sync(0xffffffffu, ok)) break;
+        }
+        const double s = __dadd_rn(s_a1[ii][q], a2[q]);
+        ok = ok && (s <= bd.hi[q]) && (s >= bd.lo[q]);
+      }
+      const unsigned mk = __ballot_sync(0xffffffffu, ok);
+      if (mk) {
+        const long long row = (long long)s_orig[ii] - r0;
+        if (ok) atomicOr(bits + row * W + (orig_j >> 5), 1u << (orig_j & 31));
+        if (lane == 0) atomicAdd(rowcnt + row, (unsigned long long)__popc(mk));
+      }
     }
   }
 }
@@ -971,7 +1130,37 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
          sok.as<uint8_t>(), tmin.as<double>(), tmax.as<double>());
   launch(c, "k_group_bounds", k_group_bounds, dim3(div_up(ng * Kpad, 256)), dim3(256), 0, a2t.as<double>(), 1, V, Kpad,
          dok.as<uint8_t>(), gmin.as<double>(), gmax.as<double>());
-  if (!never && rows > 0) {
+  const bool use_list = (double)ng * (double)ng * 8.0 <= 1.0e9;  // worst-case list fits 1 GB
+  if (!never && rows > 0 && use_list) {
+    // culls over every (tile, group) into a compact list, then one warp per survivor
+    DevBuf& list = c->ws[WS_PAIRLIST];
+    list.alloc((size_t)ng * ng * sizeof(unsigned long long), c->stream);
+    DevBuf nlist;
+    nlist.alloc(sizeof(unsigned long long), c->stream);
+    BZG_CHECK_CUDA(cudaMemsetAsync(nlist.ptr, 0, sizeof(unsigned long long), c->stream));
+    const bool reg = R > 0;
+    launch(c, "k_tile_group_cull", k_tile_group_cull, dim3(div_up(ng, 256), (unsigned)ng), dim3(256), 0, bd,
+           tmin.as<double>(), tmax.as<double>(), gmin.as<double>(), gmax.as<double>(), ng, Kpad, rm, (int)reg,
+           list.as<unsigned long long>(), nlist.as<unsigned long long>());
+    auto go = [&](auto kern, size_t smem) {
+      BZG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      launch(c, "k_pair_list", kern, dim3((unsigned)(c->num_sms * 3)), dim3(kPairThreads), smem, bd,
+             a1c.as<double>(), a2t.as<double>(), sok.as<uint8_t>(), dok.as<uint8_t>(), perm.as<int>(),
+             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>(), rm,
+             list.as<unsigned long long>(), nlist.as<unsigned long long>());
+    };
+#define BZG_K(k)                                                                                        \
+  case k:                                                                                               \
+    if (reg) go(k_pair_list<k, true>, pair_list_smem<k, true>()); else go(k_pair_list<k, false>, pair_list_smem<k, false>()); \
+    break;
+    switch (Kpad) {
+      BZG_K(4) BZG_K(8) BZG_K(12) BZG_K(16) BZG_K(24) BZG_K(32) BZG_K(48)
+      default:
+        if (reg) go(k_pair_list<64, true>, pair_list_smem<64, true>()); else go(k_pair_list<64, false>, pair_list_smem<64, false>());
+        break;
+    }
+#undef BZG_K
+  } else if (!never && rows > 0) {
     dim3 grid(div_up(V, kPairThreads), (unsigned)ng);
     auto go = [&](auto kern) {
       launch(c, "k_pair_tiles", kern, grid, dim3(kPairThreads), 0, bd, a1c.as<double>(), a2t.as<double>(),
