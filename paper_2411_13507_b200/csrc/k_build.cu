@@ -691,12 +691,19 @@ struct DParams {
 // One warp per source row: ordered expansion of the row's bit words into
 // (src, dst) in ascending dst (np.nonzero order, graph.py:187-190) and the edge cost
 // (graph.py:192-197) computed from the two endpoint states.
+constexpr int kExpandThreads = 256;
+
 template <int G, int M>
-__global__ void k_expand(DParams dp, const double* __restrict__ Vx, long long r0, long long r1, long long W,
+__global__ void __launch_bounds__(kExpandThreads) k_expand(DParams dp, const double* __restrict__ Vx, long long r0,
+                                                           long long r1, long long W,
                          const uint32_t* __restrict__ bits, const long long* __restrict__ rptr,
                          int* __restrict__ src, int* __restrict__ dst, double* __restrict__ cost) {
+  // The set bits of 32 words are first listed in ascending (word, bit) order in the warp's
+  // shared slice, then the lanes take one edge each, so a word with many edges does not
+  // serialise its lane while the others idle.
   constexpr int N = G * M;
-  const int lane = threadIdx.x & 31;
+  __shared__ int s_j[kExpandThreads / 32][32 * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long i = r0 + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (i >= r1) return;
   long long base = rptr[i - r0];
@@ -706,27 +713,45 @@ __global__ void k_expand(DParams dp, const double* __restrict__ Vx, long long r0
 #pragma unroll
   for (int k = 0; k < N; ++k) xi[k] = Vx[i * N + k];
   const uint32_t* row = bits + (i - r0) * W;
+  int* lst = s_j[warp];
   for (long long w0 = 0; w0 < W && base < end; w0 += 32) {
+    if ((w0 & 127) == 0) {  // skip 128 empty words at a time (sparse rows of large graphs)
+      uint32_t any = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const long long wq = w0 + 32 * q + lane;
+        any |= wq < W ? row[wq] : 0u;
+      }
+      if (!__any_sync(0xffffffffu, any != 0)) {
+        w0 += 96;
+        continue;
+      }
+    }
     const long long w = w0 + lane;
     uint32_t word = w < W ? row[w] : 0u;
     const int c = __popc(word);
     const int incl = warp_incl_scan(c);
-    long long off = base + incl - c;
-    while (word) {
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    for (int k = incl - c; word; ++k) {
       const int b = __ffs(word) - 1;
       word &= word - 1;
-      const long long jv = w * 32 + b;
+      lst[k] = (int)(w * 32 + b);
+    }
+    __syncwarp();
+    for (int t = lane; t < total; t += 32) {
+      const long long jv = lst[t];
       double xj[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) xj[k] = Vx[jv * N + k];
       double P[M][2 * G];
       control_points<G, M>(xi, xj, dp.D, P);
-      src[off] = (int)i;
-      dst[off] = (int)jv;
-      cost[off] = polygon_length<G, M>(P);
-      ++off;
+      src[base + t] = (int)i;
+      dst[base + t] = (int)jv;
+      cost[base + t] = polygon_length<G, M>(P);
     }
-    base += __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    base += total;
   }
 }
 
@@ -1200,7 +1225,7 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
   if (E > 0) {
     dispatch_gm(g->gamma, g->m, [&](auto G_, auto M_) {
       constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
-      launch(c, "k_expand", k_expand<Gc, Mc>, dim3(div_up(rows * 32, 256)), dim3(256), 0, dp,
+      launch(c, "k_expand", k_expand<Gc, Mc>, dim3(div_up(rows * 32, kExpandThreads)), dim3(kExpandThreads), 0, dp,
              g->vertices.as<double>(), r0, r1, W, bits.as<uint32_t>(), rptr.as<long long>(), g->src.as<int>(),
              g->dst.as<int>(), g->cost.as<double>());
     });
