@@ -65,6 +65,12 @@ __device__ __forceinline__ bool any_inside_einsum(const double (&P)[M][2 * G], c
   return hit;
 }
 
+// NaN-free max / min as one DSETP and selects (fmax/fmin carry NaN handling, ~6 instructions).
+// Equal to np.maximum / np.minimum / np.clip for non-NaN operands up to the sign of a zero
+// result, which no later comparison or square can see.
+__device__ __forceinline__ double dmax2(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double dmin2(double a, double b) { return a < b ? a : b; }
+
 // Exact certificate that box_code_canon returns 1 (safe), from the bounding box
 // [mn, mx] of the control points.  (1) No control point is inside when, for some axis,
 // every point is beyond b + eps on one side.  (2) The face the reference picks is active
@@ -73,10 +79,43 @@ __device__ __forceinline__ bool any_inside_einsum(const double (&P)[M][2 * G], c
 // likewise -k.  (3) If every possibly-active face is cleared by all points
 // (fl(P_kj - b) > margin for all j  <=>  fl(min_j P_kj - b) > margin, monotone rounding),
 // the clearance test passes whichever of them is chosen, so the code is 1.
+//
+// (4) A possibly-active face that is not cleared is harmless if it can never be chosen: when
+// some face s is active for every possible anchor (all points on its outer side: mn_k >= hi_k
+// puts clip(v_k) = hi_k exactly, residual 0) and cleared, and the largest separation face f
+// can reach, fl(max P - b_f), is below the smallest face s can have, fl(min P - b_s), then s
+// beats f at every anchor (argmax over active faces), so f is not chosen.  This certifies
+// obstacles far along one axis even when the polygon straddles the plane of a face of
+// another axis (large maps: a few percent of all pairs instead of most).
+template <int M>
+__device__ __forceinline__ bool canon_safe_cert_far(const double (&mn)[M], const double (&mx)[M], const ObsRec<M>& o,
+                                                 double margin) {  // (4), given (1)
+  double L = -INFINITY;       // best lower bound of the separation of a surely-active cleared face
+  double ub_bad = -INFINITY;  // largest upper bound of a possibly-active uncleared face
+  bool any_bad = false;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const bool thin = o.thin[k] != 0.0;
+    // face +k: sep = fl(v_k - b_k) in [fl(mn_k - b_k), fl(mx_k - b_k)]
+    const double lb_hi = __dsub_rn(mn[k], o.b[k]), ub_hi = __dsub_rn(mx[k], o.b[k]);
+    const bool pa_hi = thin | (mx[k] > o.act_hi[k]);
+    const bool clr_hi = lb_hi > margin;
+    if (clr_hi && mn[k] >= o.hi[k]) L = dmax2(L, lb_hi);
+    if (pa_hi && !clr_hi) { any_bad = true; ub_bad = dmax2(ub_bad, ub_hi); }
+    // face -k: sep = fl(-v_k - b_{M+k}) in [fl(-mx_k - b), fl(-mn_k - b)]
+    const double lb_lo = __dsub_rn(-mx[k], o.b[M + k]), ub_lo = __dsub_rn(-mn[k], o.b[M + k]);
+    const bool pa_lo = thin | (mn[k] < o.act_lo[k]);
+    const bool clr_lo = lb_lo > margin;
+    if (clr_lo && mx[k] <= o.lo[k]) L = dmax2(L, lb_lo);
+    if (pa_lo && !clr_lo) { any_bad = true; ub_bad = dmax2(ub_bad, ub_lo); }
+  }
+  return !any_bad | (ub_bad < L);
+}
+
 template <int M>
 __device__ __forceinline__ bool canon_safe_cert(const double (&mn)[M], const double (&mx)[M], const ObsRec<M>& o,
                                                 double margin) {
-  bool noin = false, ok = true;
+  bool noin = false, ok = true;  // (1)-(3): every possibly-active face cleared
 #pragma unroll
   for (int k = 0; k < M; ++k) {
     noin |= (mn[k] > o.b_eps[k]) | (-mx[k] > o.b_eps[M + k]);
@@ -87,19 +126,13 @@ __device__ __forceinline__ bool canon_safe_cert(const double (&mn)[M], const dou
     const bool clr_lo = __dsub_rn(-mx[k], o.b[M + k]) > margin;
     ok &= (!pa_hi | clr_hi) & (!pa_lo | clr_lo);
   }
-  return noin & ok;
+  return noin && (ok || canon_safe_cert_far<M>(mn, mx, o, margin));
 }
 
 struct CutScalars {
   double margin;  // CutConfig.heur_margin
   int n_obs;
 };
-
-// NaN-free max / min as one DSETP and selects (fmax/fmin carry NaN handling, ~6 instructions).
-// Equal to np.maximum / np.minimum / np.clip for non-NaN operands up to the sign of a zero
-// result, which no later comparison or square can see.
-__device__ __forceinline__ double dmax2(double a, double b) { return a > b ? a : b; }
-__device__ __forceinline__ double dmin2(double a, double b) { return a < b ? a : b; }
 
 // Heuristic code of one edge against one box obstacle: 0 unsafe, 1 safe, 2 indeterminate
 // (graph.py:232-264).  Arithmetic follows the numpy expressions term by term.
