@@ -144,12 +144,20 @@ __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_p
   const int lane = threadIdx.x & 31;
   const long long wg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const long long nw = ((long long)gridDim.x * blockDim.x) / 32;
+  // frontier sizes rotate through counts[0..2]: sweep s reads counts[(s-1)%3], appends to
+  // counts[s%3] and zeroes counts[(s+1)%3] (last read in sweep s-1, next written in sweep s+1),
+  // so one grid-wide barrier per sweep suffices
   int sweep = 1;
   for (; sweep <= max_sweeps; ++sweep) {
     const int* qin = (sweep & 1) ? qa : qb;
     int* qout = (sweep & 1) ? qb : qa;
-    const int cin = *(volatile int*)&counts[(sweep - 1) & 1];
+    const int cin = *(volatile int*)&counts[(sweep - 1) % 3];
     if (cin == 0) break;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      counts[(sweep + 1) % 3] = 0;
+      counts[4] += cin;  // frontier vertices expanded (diagnostic)
+    }
+    int* cout = counts + sweep % 3;
     for (long long k = wg; k < cin; k += nw) {
       const int u = qin[k];
       const double du = __longlong_as_double((long long)__ldcg(dist + u));
@@ -160,15 +168,13 @@ __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_p
         const unsigned long long nb = dbits(__dadd_rn(du, cost[e]));
         if (nb < __ldcg(dist + v)) {
           const unsigned long long old = atomicMin(dist + v, nb);
-          if (nb < old && atomicExch(stamp + v, sweep) != sweep) qout[atomicAdd(counts + (sweep & 1), 1)] = v;
+          if (nb < old && atomicExch(stamp + v, sweep) != sweep) qout[atomicAdd(cout, 1)] = v;
         }
       }
     }
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) counts[(sweep - 1) & 1] = 0;  // consumed; reused by sweep + 1
-    grid.sync();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) counts[2] = sweep - 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[3] = sweep - 1;
 }
 
 // parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes)
@@ -342,14 +348,16 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     DevBuf qa, qb, cnt;
     qa.alloc(std::max(V, 1ll) * sizeof(int), c->stream);
     qb.alloc(std::max(V, 1ll) * sizeof(int), c->stream);
-    cnt.alloc(4 * sizeof(int), c->stream);
-    const int init[4] = {1, 0, 0, 0};
+    cnt.alloc(8 * sizeof(int), c->stream);
+    const int init[8] = {1, 0, 0, 0, 0, 0, 0, 0};
     const int v0i = (int)v0;
     BZG_CHECK_CUDA(cudaMemcpyAsync(cnt.ptr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     BZG_CHECK_CUDA(cudaMemcpyAsync(qa.ptr, &v0i, sizeof(int), cudaMemcpyHostToDevice, c->stream));
     int per_sm = 0;
     BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bf_persistent, 256, 0));
-    const int blocks = std::max(1, std::min(per_sm, 4) * c->num_sms);
+    static const int bf_per_sm_env =
+        std::getenv("BZG_BF_BLOCKS_PER_SM") ? std::atoi(std::getenv("BZG_BF_BLOCKS_PER_SM")) : 0;
+    const int blocks = std::max(1, std::min(per_sm, bf_per_sm_env > 0 ? bf_per_sm_env : 4) * c->num_sms);
     long long Vl = V;
     const long long* rp = g->row_ptr.as<long long>();
     const int* dd = g->dst.as<int>();
@@ -361,6 +369,13 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     int maxs = (int)std::min<long long>(V + 2, 1 << 30);
     void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &st, &pa, &pb, &pc, &maxs};
     launch_coop(c, "k_bf_persistent", (const void*)k_bf_persistent, dim3(blocks), dim3(256), args);
+    if (c->trace_on) {
+      int hc[8];
+      BZG_CHECK_CUDA(cudaMemcpyAsync(hc, cnt.ptr, sizeof(hc), cudaMemcpyDeviceToHost, c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      std::fprintf(stderr, "[bzg path] Bellman-Ford sweeps %d, frontier vertices expanded %d (V = %lld)\n", hc[3],
+                   hc[4], V);
+    }
     launch(c, "k_parent_dist", k_parent_dist, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(),
            g->dst.as<int>(), g->cost.as<double>(), alive, dist, t_pd.as<unsigned long long>());
     launch(c, "k_parent_idx", k_parent_idx, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(), g->dst.as<int>(),
