@@ -35,13 +35,27 @@ __device__ __forceinline__ void control_points(const double* __restrict__ xi, co
   for (int k = 0; k < M; ++k) {
 #pragma unroll
     for (int j = 0; j < 2 * G; ++j) {
-      double acc = 0.0;
+      if (M == 1) {
+        // m = 1 makes both einsum operands contiguous along q, and numpy's contiguous kernel
+        // accumulates in two lanes (even q, odd q) and adds them at the end (measured)
+        double ev = 0.0, od = 0.0;
 #pragma unroll
-      for (int q = 0; q < 2 * G; ++q) {
-        const double bq = q < G ? xi[q * M + k] : xj[(q - G) * M + k];
-        acc = __dadd_rn(acc, __dmul_rn(D[j * 2 * G + q], bq));
+        for (int q = 0; q < 2 * G; q += 2) {
+          const double b0 = q < G ? xi[q] : xj[q - G];
+          const double b1 = q + 1 < G ? xi[q + 1] : xj[q + 1 - G];
+          ev = __dadd_rn(ev, __dmul_rn(D[j * 2 * G + q], b0));
+          od = __dadd_rn(od, __dmul_rn(D[j * 2 * G + q + 1], b1));
+        }
+        P[k][j] = __dadd_rn(ev, od);
+      } else {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 2 * G; ++q) {
+          const double bq = q < G ? xi[q * M + k] : xj[(q - G) * M + k];
+          acc = __dadd_rn(acc, __dmul_rn(D[j * 2 * G + q], bq));
+        }
+        P[k][j] = acc;
       }
-      P[k][j] = acc;
     }
   }
 }
