@@ -416,6 +416,21 @@ def case_heur_general3():
     print("heur_general3:", np.bincount(np.array(code_l), minlength=3))
 
 
+def case_m1():
+    """One output dimension (m=1, gamma=3): numpy's contiguous einsum kernel in the control-point map."""
+    spec = bg.BezierSpec(m=1, gamma=3, T=1.0)
+    xd = rgeo.Box(np.array([0.0, -1.5, -4.0]), np.array([5.0, 1.5, 4.0])).to_polytope()
+    u = rgeo.Box(np.array([-30.0]), np.array([30.0]))
+    tube = rsim.design_tube(spec, (6.0, 11.0, 6.0), 0.02)
+    oracle = bg.build_oracle(spec, xd, u, tube)
+    sample = rgeo.Box(np.array([0.0, -0.6, -1.0]), np.array([5.0, 0.6, 1.0]))
+    obs = [rgeo.inflate(rgeo.Box(np.array([c - w / 2]), np.array([c + w / 2])).to_polytope(), tube.position_box(1))
+           for c, w in ((1.3, 0.2), (2.6, 0.15), (3.9, 0.3))]
+    start = np.array([0.2, 0.0, 0.0])
+    goal = np.array([4.8, 0.0, 0.0])
+    capture("m1_300", 300, spec, oracle, sample, 6, np.array([start, goal]), obs, start, goal, full=True, detail=True)
+
+
 def case_m3():
     """Three output dimensions (m=3, gamma=2): 3-D boxes through the whole path."""
     spec = bg.BezierSpec(m=3, gamma=2, T=1.0)
@@ -437,7 +452,7 @@ def case_m3():
 
 
 CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general, "knn": case_knn,
-         "m3": case_m3, "heur_general3": case_heur_general3,
+         "m3": case_m3, "m1": case_m1, "heur_general3": case_heur_general3,
          "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
                                                               ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
                                                               ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,

@@ -18,7 +18,7 @@ from tests.helpers import compare_cut, digest, inputs_from_golden
 
 pytestmark = pytest.mark.gpu
 
-FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600"]
+FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600", "m1_300"]
 
 
 @pytest.fixture(scope="module")
