@@ -320,6 +320,10 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
     const int nd = nob * (int)(sizeof(ObsRec<M>) / sizeof(double));
     for (int t = threadIdx.x; t < nd; t += blockDim.x) dstp[t] = srcp[t];
   }
+  __shared__ unsigned long long s_cnt[3];
+  __shared__ int s_done;
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) s_done = 0;
   __syncthreads();
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = e < E;
@@ -414,18 +418,25 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
     __syncwarp();
   }
   if (valid) first_kill[e] = s_kill[lane];
-  // block reduction of the three counters
-  typedef cub::BlockReduce<unsigned long long, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  unsigned long long t0 = BR(tmp).Sum((unsigned long long)c0);
-  __syncthreads();
-  unsigned long long t1 = BR(tmp).Sum((unsigned long long)c1);
-  __syncthreads();
-  unsigned long long t2 = BR(tmp).Sum((unsigned long long)c2);
-  if (threadIdx.x == 0) {
-    atomicAdd(counters + 0, t0);
-    atomicAdd(counters + 1, t1);
-    atomicAdd(counters + 2, t2);
+  // counters without a block barrier (warps finish pass 2 at different times): warp sums into
+  // shared memory, and the block's last warp to finish adds them to the global counters
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    c0 += __shfl_down_sync(0xffffffffu, c0, d);
+    c1 += __shfl_down_sync(0xffffffffu, c1, d);
+    c2 += __shfl_down_sync(0xffffffffu, c2, d);
+  }
+  if (lane == 0) {
+    atomicAdd(s_cnt + 0, (unsigned long long)c0);
+    atomicAdd(s_cnt + 1, (unsigned long long)c1);
+    atomicAdd(s_cnt + 2, (unsigned long long)c2);
+    __threadfence_block();
+    if (atomicAdd(&s_done, 1) == kHeurWarps - 1) {
+      __threadfence_block();
+      atomicAdd(counters + 0, atomicAdd(s_cnt + 0, 0ull));
+      atomicAdd(counters + 1, atomicAdd(s_cnt + 1, 0ull));
+      atomicAdd(counters + 2, atomicAdd(s_cnt + 2, 0ull));
+    }
   }
 }
 
