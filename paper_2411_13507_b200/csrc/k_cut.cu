@@ -129,11 +129,6 @@ __device__ __forceinline__ bool canon_safe_cert(const double (&mn)[M], const dou
   return noin && (ok || canon_safe_cert_far<M>(mn, mx, o, margin));
 }
 
-struct CutScalars {
-  double margin;  // CutConfig.heur_margin
-  int n_obs;
-};
-
 // Heuristic code of one edge against one box obstacle: 0 unsafe, 1 safe, 2 indeterminate
 // (graph.py:232-264).  Arithmetic follows the numpy expressions term by term.
 template <int G, int M>

@@ -1,4 +1,4 @@
-// Cut-QP verdict selection and active-set polish (one warp per instance).  Included by k_cut.cu.
+// Cut-QP verdict selection and active-set polish (one thread per instance).  Included by k_cut.cu.
 #pragma once
 
 namespace bzg {
