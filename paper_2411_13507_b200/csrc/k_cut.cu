@@ -657,13 +657,21 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
   const long long n_list = (long long)*hn;
   mk->n_polished = n_list;
   if (c->trace_on) std::fprintf(stderr, "[bzg cut] qp instances %lld, polished %lld\n", n_inst, n_list);
-  constexpr int NR = polish_dim<G, M, C>();
-  const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
-  BZG_CHECK_CUDA(cudaFuncSetAttribute(k_qp_polish<G, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
-  launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
-         dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
-         cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
-         mk->qp_status.as<int8_t>());
+  static const bool polish_lu = std::getenv("BZG_POLISH_IMPL") && std::string(std::getenv("BZG_POLISH_IMPL")) == "lu";
+  if (polish_lu) {  // the shared-memory core LU (kept for A/B checks)
+    constexpr int NR = polish_dim<G, M, C>();
+    const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
+    BZG_CHECK_CUDA(cudaFuncSetAttribute(k_qp_polish<G, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
+           dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
+           cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
+           mk->qp_status.as<int8_t>());
+  } else {
+    launch(c, "k_qp_polish", k_qp_polish_reg<G, M, C>, dim3(div_up(n_list, 128)), dim3(128), 0, dp,
+           g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
+           cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
+           mk->qp_status.as<int8_t>());
+  }
   trace("select+polish");
 }
 

@@ -354,5 +354,220 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
   safe_out[inst] = (uint8_t)(st[inst] == BZG_SOLVED && dl > eps_cut);
 }
 
+// Register-resident polish: the same regularised KKT system and two refinement steps, solved
+// through a Schur complement on the multipliers of the active obstacle rows and the sum row
+// (at most C + 1 unknowns) instead of a dense LU on the 11-slot core in shared memory.
+//   delta_c = (rx_dc + nu_c) / (2 + d)                       (delta pivot, as above)
+//   lambda_j = alpha_j - beta_j u_j,  u_j = sum_i g_i(j) nu_i  (g: Q rows, the sum row's ones)
+//     free j:   alpha_j = rx_j / d,                       beta_j = 1 / d
+//     bound j:  alpha_j = rn_j + e (rx_j - d rn_j),        beta_j = e = d / (1 + d^2)
+//               (nu_j = (rx_j - d rn_j - u_j) / (1 + d^2), the 2x2 bound pivot)
+//   S nu = t,   S_ik = sum_j beta_j g_i(j) g_k(j) + d_i [i = k],  t_i = sum_j g_i(j) alpha_j - rhs_i
+// S is symmetric positive definite (beta, d_i > 0): Cholesky, no pivoting.  K has condition
+// ~1/d either way, so this solve and the reference's LU reach the regularised solution to the
+// same forward accuracy after the refinement steps (residuals against the full K, as above).
+template <int G, int M, int C>
+__global__ void __launch_bounds__(128) k_qp_polish_reg(
+    DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
+    const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
+    long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ res,
+    double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
+  constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NS = C + 1;
+  const long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= n_list) return;
+  const long long inst = list[li];
+  double x[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) x[t] = x_io[inst * NV + t];
+  const double rp = res[inst * 2], rd = res[inst * 2 + 1];
+  double Q[C][J], b[C];
+  load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[inst], Q, b);
+  auto Gl = [&](int i, int j) -> double {  // lambda part of constraint row i (compile-time i, j)
+    return i < C ? Q[i < C ? i : 0][j] : (i < C + J ? (i - C == j ? 1.0 : 0.0) : 1.0);
+  };
+  auto a_dot = [&](int i, const double (&v)[NV]) -> double {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const double g = Gl(i, j);
+      if (g != 0.0) acc = __fma_rn(g, v[j], acc);
+    }
+    if (i < C) acc = __fma_rn(-1.0, v[J + (i < C ? i : 0)], acc);
+    return acc;
+  };
+  auto lo_of = [&](int i) -> double { return i < C ? -INFINITY : (i < C + J ? 0.0 : 1.0); };
+  auto hi_of = [&](int i) -> double { return i < C ? b[i < C ? i : 0] : (i < C + J ? INFINITY : 1.0); };
+  const double tol = fmax(1e-7, 10.0 * rp);
+  unsigned act = 0, atlo = 0;
+#pragma unroll
+  for (int i = 0; i < MC; ++i) {
+    const double zi = a_dot(i, x);
+    const bool l_ = __dsub_rn(zi, lo_of(i)) <= tol, u_ = __dsub_rn(hi_of(i), zi) <= tol;
+    act |= (unsigned)(l_ || u_) << i;
+    atlo |= (unsigned)l_ << i;
+  }
+  bool accept = false;
+  double xp[NV];
+  if (act) {
+    const double reg = 1e-8, i2 = 1.0 / (2.0 + reg), e2 = reg / (1.0 + reg * reg), r2 = 1.0 / (1.0 + reg * reg);
+    const double ireg = 1.0 / reg;
+    auto a_on = [&](int i) -> bool { return act >> i & 1u; };
+    auto bound = [&](int j) -> bool { return a_on(C + j); };
+    auto used = [&](int s) -> bool { return s < C ? a_on(s) : a_on(C + J); };  // nu slot s: obstacle row / sum row
+    auto gs = [&](int s, int j) -> double { return s < C ? Q[s < C ? s : 0][j] : 1.0; };
+    // ---- S = sum_j beta_j g g' + diag(d), Cholesky (compile-time indices: registers only)
+    double L[NS][NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i)
+#pragma unroll
+      for (int k = 0; k <= i; ++k) {
+        double v;
+        if (!used(i) || !used(k)) {
+          v = i == k ? 1.0 : 0.0;
+        } else {
+          v = 0.0;
+#pragma unroll
+          for (int j = 0; j < J; ++j) v = __fma_rn(__dmul_rn(bound(j) ? e2 : ireg, gs(i, j)), gs(k, j), v);
+          if (i == k) v = __dadd_rn(v, i < C ? i2 + reg : reg);
+        }
+        L[i][k] = v;
+      }
+    double Ld[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+#pragma unroll
+      for (int k = 0; k < i; ++k) {
+        double t = L[i][k];
+#pragma unroll
+        for (int q = 0; q < k; ++q) t = __fma_rn(-L[i][q], L[k][q], t);
+        L[i][k] = t * Ld[k];
+      }
+      double dd = L[i][i];
+#pragma unroll
+      for (int q = 0; q < i; ++q) dd = __fma_rn(-L[i][q], L[i][q], dd);
+      L[i][i] = sqrt(dd);
+      Ld[i] = 1.0 / L[i][i];
+    }
+    auto solve = [&](const double (&rx)[NV], const double (&rn)[MC], double (&wx)[NV], double (&wn)[MC]) {
+      double alpha[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        alpha[j] = bound(j) ? __fma_rn(e2, __fma_rn(-reg, rn[C + j], rx[j]), rn[C + j]) : __dmul_rn(rx[j], ireg);
+      double t[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        double acc = 0.0;
+        if (used(s)) {
+          const double rhs = s < C ? __fma_rn(rx[J + (s < C ? s : 0)], i2, rn[s < C ? s : 0]) : rn[C + J];
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc = __fma_rn(gs(s, j), alpha[j], acc);
+          acc = __dsub_rn(acc, rhs);
+        }
+        t[s] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {  // L y = t
+        double v = t[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) v = __fma_rn(-L[i][k], t[k], v);
+        t[i] = v * Ld[i];
+      }
+#pragma unroll
+      for (int i = NS - 1; i >= 0; --i) {  // L' nu = y
+        double v = t[i];
+#pragma unroll
+        for (int k = i + 1; k < NS; ++k) v = __fma_rn(-L[k][i], t[k], v);
+        t[i] = v * Ld[i];
+      }
+#pragma unroll
+      for (int i = 0; i < MC; ++i) wn[i] = 0.0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+        if (used(s)) wn[s < C ? s : C + J] = t[s];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        double u = 0.0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (used(s)) u = __fma_rn(gs(s, j), t[s], u);
+        if (bound(j)) {
+          wn[C + j] = __dmul_rn(__dsub_rn(__fma_rn(-reg, rn[C + j], rx[j]), u), r2);
+          wx[j] = __fma_rn(reg, wn[C + j], rn[C + j]);
+        } else {
+          wx[j] = __fma_rn(-ireg, u, alpha[j]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) wx[J + c] = __dmul_rn(__dadd_rn(rx[J + c], a_on(c) ? wn[c] : 0.0), i2);
+    };
+    auto kmul = [&](const double (&wx)[NV], const double (&wn)[MC], double (&ox)[NV], double (&on)[MC]) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        double acc = __dmul_rn(reg, wx[j]);
+#pragma unroll
+        for (int i = 0; i < MC; ++i)
+          if (a_on(i)) acc = __fma_rn(Gl(i, j), wn[i], acc);
+        ox[j] = acc;
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) ox[J + c] = __fma_rn(2.0 + reg, wx[J + c], a_on(c) ? -wn[c] : 0.0);
+#pragma unroll
+      for (int i = 0; i < MC; ++i) on[i] = a_on(i) ? __fma_rn(-reg, wn[i], a_dot(i, wx)) : 0.0;
+    };
+    double bx[NV], bn[MC], wx[NV], wn[MC];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) bx[t] = 0.0;  // -q = 0
+#pragma unroll
+    for (int i = 0; i < MC; ++i) bn[i] = a_on(i) ? ((atlo >> i & 1u) ? lo_of(i) : hi_of(i)) : 0.0;
+    solve(bx, bn, wx, wn);
+#pragma unroll 1
+    for (int rep = 0; rep < 2; ++rep) {
+      double kx[NV], kn[MC], rx[NV], rn[MC], dx[NV], dn[MC];
+      kmul(wx, wn, kx, kn);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) rx[t] = __dsub_rn(bx[t], kx[t]);
+#pragma unroll
+      for (int i = 0; i < MC; ++i) rn[i] = __dsub_rn(bn[i], kn[i]);
+      solve(rx, rn, dx, dn);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) wx[t] = __dadd_rn(wx[t], dx[t]);
+#pragma unroll
+      for (int i = 0; i < MC; ++i) wn[i] = __dadd_rn(wn[i], dn[i]);
+    }
+    // acceptance (qpsolver.py:271-279)
+    double upv = 0.0, lov = 0.0;
+#pragma unroll
+    for (int i = 0; i < MC; ++i) {
+      const double zi = a_dot(i, wx);
+      upv = fmax(upv, fmax(__dsub_rn(zi, hi_of(i)), 0.0));
+      lov = fmax(lov, fmax(__dsub_rn(lo_of(i), zi), 0.0));
+    }
+    double rdt = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {  // |P x + A' y| with y = nu on active slots
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < MC; ++i) acc = __fma_rn(Gl(i, j), wn[i], acc);
+      rdt = fmax(rdt, fabs(acc));
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) rdt = fmax(rdt, fabs(__fma_rn(-1.0, wn[c], __dmul_rn(2.0, wx[J + c]))));
+    if (fmax(__dadd_rn(upv, lov), rdt) < fmax(rp, rd)) {
+      accept = true;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) xp[t] = wx[t];
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const double dc = accept ? xp[J + c] : x[J + c];
+    s = __fma_rn(dc, dc, s);
+  }
+  const double dl = sqrt(s);
+  delta_out[inst] = dl;
+  safe_out[inst] = (uint8_t)(st[inst] == BZG_SOLVED && dl > eps_cut);
+}
+
 }  // namespace
 }  // namespace bzg
