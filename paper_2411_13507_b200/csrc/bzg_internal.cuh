@@ -10,6 +10,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <mutex>
 #include <unordered_map>
 #include <vector>
 
@@ -74,7 +75,7 @@ struct DevBuf {
 enum WsSlot {
   WS_CAND, WS_FLAG, WS_POS,                                          // samplers
   WS_BITS, WS_A1C, WS_A2T, WS_ROWCNT, WS_RPTR, WS_PAIRLIST,          // pair test
-  WS_KILL, WS_QKILL, WS_SAVED, WS_PEND, WS_GEN,                      // cut screen
+  WS_KILL, WS_QKILL, WS_SAVED, WS_PEND, WS_GEN, WS_OBSGRID,          // cut screen
   WS_QX, WS_QZY, WS_QRES, WS_QSAFE, WS_QLIST, WS_QCONST,             // Cut-QP
   kWsSlots
 };
@@ -115,6 +116,10 @@ struct Ctx {
   // cuts do not refragment the stream-ordered pool (a fresh 1 GB bit matrix per step made the
   // pool map new memory at random steps, milliseconds each).
   DevBuf ws[kWsSlots];
+  // last obstacle-grid decision (k_cut.cu): obstacle count and xy bounds -> grid sparse enough
+  int grid_nobs = -1;
+  double grid_key[4] = {0, 0, 0, 0};
+  bool grid_sparse = false;
   void* pinned = nullptr;  // small pinned host staging area
   size_t pinned_bytes = 0;
 
@@ -148,6 +153,21 @@ struct Ctx {
     return pinned;
   }
 };
+
+// Raise a kernel's dynamic shared-memory limit only when a launch needs more than before: the
+// driver call costs tens of microseconds, which shows up as a gap whenever the stream is empty.
+inline void ensure_dyn_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<unsigned long long, size_t> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long key = (unsigned long long)(uintptr_t)kern ^ ((unsigned long long)dev << 56);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return;
+  BZG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done[key] = bytes;
+}
 
 // Launch a kernel on the context stream, counting it and (when profiling) timing it
 // with a pair of CUDA events recorded on the same stream.

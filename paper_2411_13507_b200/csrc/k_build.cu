@@ -1168,7 +1168,7 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
            tmin.as<double>(), tmax.as<double>(), gmin.as<double>(), gmax.as<double>(), ng, Kpad, rm, (int)reg,
            list.as<unsigned long long>(), nlist.as<unsigned long long>());
     auto go = [&](auto kern, size_t smem) {
-      BZG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ensure_dyn_smem((const void*)kern, smem);
       launch(c, "k_pair_list", kern, dim3((unsigned)(c->num_sms * 3)), dim3(kPairThreads), smem, bd,
              a1c.as<double>(), a2t.as<double>(), sok.as<uint8_t>(), dok.as<uint8_t>(), perm.as<int>(),
              gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>(), rm,

@@ -289,6 +289,88 @@ __device__ __forceinline__ void warp_append(bool want_me, unsigned long long ite
 }
 
 constexpr int kHeurThreads = 256, kHeurWarps = kHeurThreads / 32;  // (128 x 5 blocks measured slower)
+
+// ---- spatial pre-screen for canonical boxes (large maps): a uniform grid over the first two
+// output axes holds, per cell and obstacle chunk, the mask of obstacles whose box grown by R
+// meets the cell.  If an edge's control-polygon bounding box B has extent ext <= R - 0.01
+// (max over axes of mx - mn), an obstacle whose grown box misses every cell B touches is more
+// than R >= ext + 0.01 away from B along some axis, say below B on axis x: every point has
+// P_x - hi_x > ext + 0.01, so no point is inside (1), face +x is active at every anchor and
+// cleared, and every other face that could be active and is not cleared has separation at
+// most ext + 1e-6 < mn_x - hi_x -- canon_safe_cert (4) holds: code 1 without evaluating it.
+constexpr int kGridCells = 64;  // per axis
+struct ObsGrid {
+  double x0, y0, inv_cx, inv_cy, R;  // grid origin, 1 / cell size, growth radius
+  unsigned long long ext_bits;       // max sampled edge extent (double bits)
+  unsigned long long pop, bits;      // set mask bits / all mask bits: the grid is used when sparse
+};
+
+// Strided sample of edge control-polygon extents (at most 64 k edges), max into ext_bits.
+template <int G, int M>
+__global__ void k_obs_grid_extent(DParams dp, const double* __restrict__ Vx, long long E,
+                                  const int* __restrict__ src, const int* __restrict__ dst, ObsGrid* __restrict__ gp) {
+  constexpr int N = G * M;
+  const long long stride = E > 65536 ? E / 65536 : 1;
+  const long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * stride;
+  double ext = 0.0;
+  if (e < E) {
+    double xi[N], xj[N], P[M][2 * G];
+    const long long a = src[e], b = dst[e];
+#pragma unroll
+    for (int k = 0; k < N; ++k) { xi[k] = Vx[a * N + k]; xj[k] = Vx[b * N + k]; }
+    control_points<G, M>(xi, xj, dp.D, P);
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      double mn = P[k][0], mx = P[k][0];
+#pragma unroll
+      for (int j = 1; j < 2 * G; ++j) { mn = fmin(mn, P[k][j]); mx = fmax(mx, P[k][j]); }
+      ext = fmax(ext, mx - mn);
+    }
+  }
+  for (int d = 16; d > 0; d >>= 1) ext = fmax(ext, __shfl_down_sync(0xffffffffu, ext, d));
+  // non-negative doubles order like their bit patterns
+  if ((threadIdx.x & 31) == 0) atomicMax(&gp->ext_bits, (unsigned long long)__double_as_longlong(ext));
+}
+
+// masks[chunk][cell]: bit oi set when obstacle o0 + oi, grown by R, meets the cell.  The grid
+// spans the obstacles' box bounds (lo0, lo1)-(hi0, hi1) (host) grown by R = 1.25 max sampled
+// extent + 0.02 (edges above R - 0.01 test every obstacle); thread 0 publishes it in gpp.
+template <int M>
+__global__ void k_obs_grid_masks(const ObsRec<M>* __restrict__ obs, int n_obs, int chunk, double lo0, double lo1,
+                                 double hi0, double hi1, ObsGrid* __restrict__ gpp,
+                                 unsigned long long* __restrict__ masks) {
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x, ch = blockIdx.y;
+  if (cell >= kGridCells * kGridCells) return;
+  ObsGrid gp;
+  gp.R = 1.25 * __longlong_as_double((long long)gpp->ext_bits) + 0.02;
+  gp.x0 = lo0 - gp.R;
+  gp.y0 = lo1 - gp.R;
+  gp.inv_cx = kGridCells / fmax(hi0 - lo0 + 2 * gp.R, 1e-300);
+  gp.inv_cy = kGridCells / fmax(hi1 - lo1 + 2 * gp.R, 1e-300);
+  if (cell == 0 && ch == 0) {
+    gpp->R = gp.R;
+    gpp->x0 = gp.x0;
+    gpp->y0 = gp.y0;
+    gpp->inv_cx = gp.inv_cx;
+    gpp->inv_cy = gp.inv_cy;
+    gpp->bits = (unsigned long long)kGridCells * kGridCells * n_obs;
+  }
+  const int cx = cell % kGridCells, cy = cell / kGridCells;
+  const double x0 = gp.x0 + cx / gp.inv_cx, x1 = gp.x0 + (cx + 1) / gp.inv_cx;
+  const double y0 = gp.y0 + cy / gp.inv_cy, y1 = gp.y0 + (cy + 1) / gp.inv_cy;
+  unsigned long long m = 0;
+  const int o0 = ch * chunk, o1 = min(n_obs, o0 + chunk);
+  for (int o = o0; o < o1; ++o) {
+    const ObsRec<M>& r = obs[o];
+    const bool meet = r.canon == 0.0 ||  // the argument above covers canonical boxes only
+                      (r.lo[0] - gp.R <= x1 && r.hi[0] + gp.R >= x0 && r.lo[1] - gp.R <= y1 && r.hi[1] + gp.R >= y0);
+    m |= (unsigned long long)meet << (o - o0);
+  }
+  masks[(size_t)ch * kGridCells * kGridCells + cell] = m;
+  unsigned long long p = __popcll(m);
+  for (int d = 16; d > 0; d >>= 1) p += __shfl_down_sync(0xffffffffu, p, d);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&gpp->pop, p);
+}
 constexpr int kHeurRound = 8;  // pass-2 pairs per edge per round
 
 // dynamic shared memory of k_cut_heuristic: obstacles, per-warp control points, pair lists, kills
@@ -304,10 +386,12 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
                                 double margin, int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                                 unsigned long long* __restrict__ n_pend, unsigned long long cap,
                                 unsigned long long* __restrict__ pend, unsigned long long* __restrict__ n_gen,
-                                unsigned long long gen_cap, unsigned long long* __restrict__ gen_pend) {
+                                unsigned long long gen_cap, unsigned long long* __restrict__ gen_pend,
+                                const ObsGrid* __restrict__ grid, const unsigned long long* __restrict__ gmask) {
   constexpr int N = G * M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ObsRec<M>* s_obs = reinterpret_cast<ObsRec<M>*>(smem_raw);
+  const bool use_grid = grid != nullptr;  // the host passes the grid only when it is sparse
   const int nob = o1 - o0;
   {
     const double* srcp = reinterpret_cast<const double*>(obs + o0);
@@ -347,10 +431,42 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
 #pragma unroll
       for (int j = 1; j < 2 * G; ++j) { mn[k] = dmin2(mn[k], P[k][j]); mx[k] = dmax2(mx[k], P[k][j]); }
     }
-    for (int oi = 0; oi < nob; ++oi) {
-      const ObsRec<M>& o = s_obs[oi];
-      if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
-      else hard |= 1ull << oi;
+    const unsigned long long all = nob >= 64 ? ~0ull : ((1ull << nob) - 1ull);
+    unsigned long long cand = all;
+    // spatial pre-screen (ObsGrid): far obstacles are code 1; used when the grown obstacles
+    // leave most cells empty (large maps; small maps skip it)
+    if (M >= 2 && use_grid) {
+      const ObsGrid gp = *grid;
+      double ext = 0.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) ext = dmax2(ext, __dsub_rn(mx[k], mn[k]));
+      if (__dadd_rn(ext, 0.01) <= gp.R) {
+        auto cell = [](double v, double o, double s) -> int {  // one cell of slack for rounding
+          const double c = floor((v - o) * s);
+          return (int)fmin(fmax(c, -1.0), (double)kGridCells);
+        };
+        const int cx0 = max(cell(mn[0], gp.x0, gp.inv_cx) - 1, 0), cx1 = min(cell(mx[0], gp.x0, gp.inv_cx) + 1, kGridCells - 1);
+        const int cy0 = max(cell(mn[1], gp.y0, gp.inv_cy) - 1, 0), cy1 = min(cell(mx[1], gp.y0, gp.inv_cy) + 1, kGridCells - 1);
+        unsigned long long m = 0;
+        for (int cy = cy0; cy <= cy1; ++cy)
+          for (int cx = cx0; cx <= cx1; ++cx) m |= gmask[cy * kGridCells + cx];
+        cand &= m;
+      }
+    }
+    if (cand == all) {
+      for (int oi = 0; oi < nob; ++oi) {
+        const ObsRec<M>& o = s_obs[oi];
+        if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
+        else hard |= 1ull << oi;
+      }
+    } else {
+      c1 += __popcll(all & ~cand);
+      for (unsigned long long rest = cand; rest; rest &= rest - 1ull) {
+        const int oi = __ffsll((long long)rest) - 1;
+        const ObsRec<M>& o = s_obs[oi];
+        if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
+        else hard |= 1ull << oi;
+      }
     }
   }
   // pass 2 (warp-cooperative): the uncertified (edge, obstacle) pairs of the warp's 32 edges
@@ -382,6 +498,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
     }
     const int total = __shfl_sync(0xffffffffu, off, 31);
     off -= cnt;
+    if (lane == 0) atomicAdd(counters + 8, (unsigned long long)total);
     for (int q = 0; q < cnt; ++q) {
       const int oi = __ffsll((long long)hard) - 1;
       hard &= hard - 1;
@@ -661,7 +778,7 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
   if (polish_lu) {  // the shared-memory core LU (kept for A/B checks)
     constexpr int NR = polish_dim<G, M, C>();
     const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
-    BZG_CHECK_CUDA(cudaFuncSetAttribute(k_qp_polish<G, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+    ensure_dyn_smem((const void*)k_qp_polish<G, M, C>, psmem);
     launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
            dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
            cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
@@ -740,8 +857,8 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     d_kill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_qkill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_saved.alloc(std::max(E, 1ll), c->stream);
-    d_cnt.alloc(8 * sizeof(unsigned long long), c->stream);
-    BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 8 * sizeof(unsigned long long), c->stream));
+    d_cnt.alloc(16 * sizeof(unsigned long long), c->stream);  // [8]: pass-2 pairs (diagnostic)
+    BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 16 * sizeof(unsigned long long), c->stream));
     BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
     launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
     launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
@@ -757,6 +874,56 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     unsigned long long* dcnt = d_cnt.as<unsigned long long>();
     // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
     const int chunk = std::min(64, std::max(1, (int)(96 * 1024 / sizeof(Rec))));
+    // spatial pre-screen grid (ObsGrid) for maps with enough obstacles to pay for it
+    const int n_chunks = (n_obs + chunk - 1) / chunk;
+    const bool grid_off = std::getenv("BZG_NO_OBS_GRID") != nullptr;  // read per call (tests toggle it)
+    bool use_grid = Mc >= 2 && n_obs >= 8 && E > 0 && !grid_off;
+    DevBuf d_grid;
+    DevBuf& d_gmask = c->ws[WS_OBSGRID];
+    if (use_grid) {
+      double blo[2] = {INFINITY, INFINITY}, bhi[2] = {-INFINITY, -INFINITY};
+      for (int o = 0; o < n_obs; ++o)
+        for (int k = 0; k < 2; ++k) {
+          blo[k] = std::min(blo[k], h[o].lo[k]);
+          bhi[k] = std::max(bhi[k], h[o].hi[k]);
+        }
+      // The grid pays only when the grown obstacles leave most cells empty (large maps); a
+      // dense grid costs more per edge than it saves.  That is known after building it (the
+      // fill count needs a host round trip), so the decision is kept per context for the same
+      // obstacle count and bounds: repeated cuts of one map decide once.
+      const bool known = c->grid_nobs == n_obs && c->grid_key[0] == blo[0] && c->grid_key[1] == blo[1] &&
+                         c->grid_key[2] == bhi[0] && c->grid_key[3] == bhi[1];
+      if (known && !c->grid_sparse) {
+        use_grid = false;
+      } else {
+        d_grid.alloc(sizeof(ObsGrid), c->stream);
+        BZG_CHECK_CUDA(cudaMemsetAsync(d_grid.ptr, 0, sizeof(ObsGrid), c->stream));
+        d_gmask.alloc((size_t)n_chunks * kGridCells * kGridCells * sizeof(unsigned long long), c->stream);
+        launch(c, "k_obs_grid_extent", k_obs_grid_extent<Gc, Mc>, dim3(div_up(std::min(E, 65536ll), 256)), dim3(256),
+               0, dp, g->vertices.as<double>(), E, g->src.as<int>(), g->dst.as<int>(), d_grid.as<ObsGrid>());
+        launch(c, "k_obs_grid_masks", k_obs_grid_masks<Mc>, dim3(kGridCells * kGridCells / 256, (unsigned)n_chunks),
+               dim3(256), 0, d_obs.as<Rec>(), n_obs, chunk, blo[0], blo[1], bhi[0], bhi[1], d_grid.as<ObsGrid>(),
+               d_gmask.as<unsigned long long>());
+        if (!known) {
+          ObsGrid* hg = static_cast<ObsGrid*>(c->host_scratch(sizeof(ObsGrid) + 8 * sizeof(unsigned long long)));
+          BZG_CHECK_CUDA(cudaMemcpyAsync(hg, d_grid.ptr, sizeof(ObsGrid), cudaMemcpyDeviceToHost, c->stream));
+          BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+          // sparse: under 15% of (cell, obstacle) bits set (cfg3's 5 x 5 map is denser and runs
+          // faster without the lookups; cfg5's large maps are far sparser)
+          use_grid = hg->pop * 20 < hg->bits * 3;
+          if (c->trace_on)
+            std::fprintf(stderr, "[bzg cut] obstacle grid fill %.3f, R %.3f -> %s\n", (double)hg->pop / (double)hg->bits,
+                         hg->R, use_grid ? "used" : "not used");
+          c->grid_nobs = n_obs;
+          c->grid_key[0] = blo[0];
+          c->grid_key[1] = blo[1];
+          c->grid_key[2] = bhi[0];
+          c->grid_key[3] = bhi[1];
+          c->grid_sparse = use_grid;
+          hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
+        }
+      }
+    }
     for (int attempt = 0; attempt < 3; ++attempt) {
       d_pend.alloc(cap * sizeof(unsigned long long), c->stream);
       d_gen.alloc(gen_cap * sizeof(unsigned long long), c->stream);
@@ -764,10 +931,13 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
         const int o1 = std::min(n_obs, o0 + chunk);
         const size_t smem = heur_smem<Gc, Mc>(o1 - o0);
         auto kern = k_cut_heuristic<Gc, Mc>;
-        BZG_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_dyn_smem((const void*)kern, smem);
+        const unsigned long long* gm =
+            use_grid ? d_gmask.as<unsigned long long>() + (size_t)(o0 / chunk) * kGridCells * kGridCells : nullptr;
         launch(c, "k_cut_heuristic", kern, dim3(div_up(E, kHeurThreads)), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(), E,
                g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), o0, o1, cfg->heur_margin, d_kill.as<int>(), dcnt,
-               dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>());
+               dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>(),
+               use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm);
       }
       BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
       BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
@@ -786,10 +956,16 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       // a work list overflowed: grow it and rerun the screen from a clean state
       cap = std::max(cap, hcnt[5] + 1024);
       if (n_gen > gen_cap) gen_cap = n_gen + 1024;
-      BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 8 * sizeof(unsigned long long), c->stream));
+      BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 16 * sizeof(unsigned long long), c->stream));
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
     }
     trace("heuristic");
+    if (c->trace_on) {
+      unsigned long long h8 = 0;
+      BZG_CHECK_CUDA(cudaMemcpy(&h8, d_cnt.as<unsigned long long>() + 8, sizeof(h8), cudaMemcpyDeviceToHost));
+      std::fprintf(stderr, "[bzg cut] pairs %lld, exact codes (pass 2) %llu, code0 %llu code1 %llu code2 %llu\n",
+                   E * (long long)n_obs, h8, hcnt[0], hcnt[1], hcnt[2]);
+    }
     const long long n_inst = (long long)hcnt[5];
     mk->counters[1] = (long long)hcnt[0];
     mk->counters[2] = (long long)hcnt[1];

@@ -231,3 +231,22 @@ def test_knn_prefilter(ctx, golden):
     assert gr.num_edges == 0
     with pytest.raises(ValueError):
         G.build_graph(int(g["N"]), spec, orc, bounds, int(g["seed"]), k_nearest=-1, ctx=ctx)
+
+
+def test_obstacle_grid_prescreen_is_exact(ctx, monkeypatch):
+    """The spatial obstacle pre-screen (ObsGrid, large maps) leaves every cut outcome unchanged:
+    cfg5's 10 k-node keep-in map (50 boxes on a ~11 x 11 map, where the grid is used) cut with
+    and without it."""
+    from paper_2411_13507_b200 import configs
+    from paper_2411_13507_b200 import regions as R
+
+    w = configs.scaling_sweep(10000)
+    g = R.build_region_graph(w.extra["per_region"], w.spec, w.oracle, w.extra["regions"], w.sample_bounds, w.seed,
+                             include=w.include, ctx=ctx)
+    m_grid = G.cut_graph(g, w.obstacles)
+    monkeypatch.setenv("BZG_NO_OBS_GRID", "1")
+    m_full = G.cut_graph(g, w.obstacles)
+    cnt = lambda m: [m.pairs_total, m.pairs_point_hit, m.pairs_hyperplane, m.pairs_qp, m.qp_safe, m.qp_unsafe]  # noqa: E731
+    assert cnt(m_grid) == cnt(m_full)
+    assert np.array_equal(m_grid.alive, m_full.alive)
+    assert np.array_equal(m_grid.provenance_codes, m_full.provenance_codes)
