@@ -162,13 +162,29 @@ __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_p
       const int u = qin[k];
       const double du = __longlong_as_double((long long)__ldcg(dist + u));
       const long long e1 = row_ptr[u + 1];
-      for (long long e = row_ptr[u] + lane; e < e1; e += 32) {
-        if (alive && !alive[e]) continue;
-        const int v = dst[e];
-        const unsigned long long nb = dbits(__dadd_rn(du, cost[e]));
-        if (nb < __ldcg(dist + v)) {
-          const unsigned long long old = atomicMin(dist + v, nb);
-          if (nb < old && atomicExch(stamp + v, sweep) != sweep) qout[atomicAdd(cout, 1)] = v;
+      // four edges per lane per pass, their loads issued together (the sweep is latency-bound)
+      for (long long eb = row_ptr[u] + lane; eb < e1; eb += 128) {
+        int vv[4];
+        double cc[4];
+        bool ok[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const long long e = eb + 32 * q;
+          ok[q] = e < e1 && (!alive || alive[e]);
+          vv[q] = ok[q] ? dst[e] : 0;
+          cc[q] = ok[q] ? cost[e] : 0.0;
+        }
+        unsigned long long dv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dv[q] = ok[q] ? __ldcg(dist + vv[q]) : 0ull;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!ok[q]) continue;
+          const unsigned long long nb = dbits(__dadd_rn(du, cc[q]));
+          if (nb < dv[q]) {
+            const unsigned long long old = atomicMin(dist + vv[q], nb);
+            if (nb < old && atomicExch(stamp + vv[q], sweep) != sweep) qout[atomicAdd(cout, 1)] = vv[q];
+          }
         }
       }
     }
