@@ -393,7 +393,10 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
   ObsRec<M>* s_obs = reinterpret_cast<ObsRec<M>*>(smem_raw);
   const bool use_grid = grid != nullptr;  // the host passes the grid only when it is sparse
   const int nob = o1 - o0;
-  {
+  // with the grid, each edge touches a few obstacles: read them through L1 instead of staging
+  // every record into every block's shared memory
+  const ObsRec<M>* ob = use_grid ? obs + o0 : s_obs;
+  if (!use_grid) {
     const double* srcp = reinterpret_cast<const double*>(obs + o0);
     double* dstp = reinterpret_cast<double*>(s_obs);
     const int nd = nob * (int)(sizeof(ObsRec<M>) / sizeof(double));
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
     }
     if (cand == all) {
       for (int oi = 0; oi < nob; ++oi) {
-        const ObsRec<M>& o = s_obs[oi];
+        const ObsRec<M>& o = ob[oi];
         if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
         else hard |= 1ull << oi;
       }
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
       c1 += __popcll(all & ~cand);
       for (unsigned long long rest = cand; rest; rest &= rest - 1ull) {
         const int oi = __ffsll((long long)rest) - 1;
-        const ObsRec<M>& o = s_obs[oi];
+        const ObsRec<M>& o = ob[oi];
         if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
         else hard |= 1ull << oi;
       }
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
         for (int k = 0; k < M; ++k)
 #pragma unroll
           for (int j = 0; j < 2 * G; ++j) Pq[k][j] = s_P[owner * NP + k * 2 * G + j];
-        const ObsRec<M>& o = s_obs[oi];
+        const ObsRec<M>& o = ob[oi];
         if (o.is_box == 0.0) code = any_inside_einsum<G, M>(Pq, o) ? 0 : 3;  // 3: decided by k_cut_general
         else code = o.canon != 0.0 ? box_code_canon<G, M>(Pq, o, margin) : box_code<G, M>(Pq, o, margin);
         c0 += code == 0;
