@@ -771,13 +771,16 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
          g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, polish_mode, screen,
          cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(), d_zy.as<double>(), d_res.as<double>(),
          mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
-  unsigned long long* hn = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long))) + 7;
-  BZG_CHECK_CUDA(cudaMemcpyAsync(hn, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-  const long long n_list = (long long)*hn;
-  mk->n_polished = n_list;
-  if (c->trace_on) std::fprintf(stderr, "[bzg cut] qp instances %lld, polished %lld\n", n_inst, n_list);
   static const bool polish_lu = std::getenv("BZG_POLISH_IMPL") && std::string(std::getenv("BZG_POLISH_IMPL")) == "lu";
+  long long n_list = -1;  // known on the host only when it is read back (LU path, tracing)
+  if (polish_lu || c->trace_on) {
+    unsigned long long* hn = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long))) + 7;
+    BZG_CHECK_CUDA(cudaMemcpyAsync(hn, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    n_list = (long long)*hn;
+    if (c->trace_on) std::fprintf(stderr, "[bzg cut] qp instances %lld, polished %lld\n", n_inst, n_list);
+  }
+  mk->n_polished = n_list;
   if (polish_lu) {  // the shared-memory core LU (kept for A/B checks)
     constexpr int NR = polish_dim<G, M, C>();
     const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
@@ -787,10 +790,12 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
            cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
            mk->qp_status.as<int8_t>());
   } else {
-    launch(c, "k_qp_polish", k_qp_polish_reg<G, M, C>, dim3(div_up(n_list, 128)), dim3(128), 0, dp,
-           g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
-           cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
-           mk->qp_status.as<int8_t>());
+    // persistent grid over the device-side list length (at most n_inst entries)
+    const long long pblocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 8);
+    launch(c, "k_qp_polish", k_qp_polish_reg<G, M, C>, dim3((unsigned)pblocks), dim3(128), 0, dp,
+           g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(),
+           d_next.as<unsigned long long>(), cfg->eps_cut, d_x.as<double>(), d_res.as<double>(),
+           mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), mk->qp_status.as<int8_t>());
   }
   trace("select+polish");
 }

@@ -367,15 +367,12 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
 // ~1/d either way, so this solve and the reference's LU reach the regularised solution to the
 // same forward accuracy after the refinement steps (residuals against the full K, as above).
 template <int G, int M, int C>
-__global__ void __launch_bounds__(128) k_qp_polish_reg(
-    DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
-    const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
-    long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ res,
-    double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
+__device__ __forceinline__ void polish_one_reg(
+    long long inst, const DParams& dp, const double* __restrict__ Vx, const int* __restrict__ src,
+    const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend,
+    double eps_cut, double* __restrict__ x_io, const double* __restrict__ res, double* __restrict__ delta_out,
+    uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NS = C + 1;
-  const long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (li >= n_list) return;
-  const long long inst = list[li];
   double x[NV];
 #pragma unroll
   for (int t = 0; t < NV; ++t) x[t] = x_io[inst * NV + t];
@@ -567,6 +564,20 @@ __global__ void __launch_bounds__(128) k_qp_polish_reg(
   const double dl = sqrt(s);
   delta_out[inst] = dl;
   safe_out[inst] = (uint8_t)(st[inst] == BZG_SOLVED && dl > eps_cut);
+}
+
+// Grid-stride over the work list, its length read on the device (no host round trip between
+// k_qp_select and the polish).
+template <int G, int M, int C>
+__global__ void __launch_bounds__(128) k_qp_polish_reg(
+    DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
+    const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
+    const unsigned long long* __restrict__ n_list, double eps_cut, double* __restrict__ x_io,
+    const double* __restrict__ res, double* __restrict__ delta_out, uint8_t* __restrict__ safe_out,
+    const int8_t* __restrict__ st) {
+  const long long n = (long long)*n_list;
+  for (long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x; li < n; li += (long long)gridDim.x * blockDim.x)
+    polish_one_reg<G, M, C>(list[li], dp, Vx, src, dst, obs, pend, eps_cut, x_io, res, delta_out, safe_out, st);
 }
 
 }  // namespace
