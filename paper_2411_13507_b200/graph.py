@@ -20,6 +20,7 @@ this package's host mirrors.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -283,6 +284,18 @@ class CutMask:
 
 def _pcg_words(seed) -> tuple[int, int, int, int]:
     """numpy PCG64 (state, inc) for ``default_rng(seed)`` split into 64-bit halves."""
+    if isinstance(seed, (int, np.integer)) or (isinstance(seed, (list, tuple)) and
+                                                all(isinstance(s, (int, np.integer)) for s in seed)):
+        return _pcg_words_cached(int(seed) if not isinstance(seed, (list, tuple)) else tuple(int(s) for s in seed))
+    return _pcg_words_uncached(seed)
+
+
+@functools.lru_cache(maxsize=512)
+def _pcg_words_cached(seed) -> tuple[int, int, int, int]:
+    return _pcg_words_uncached(list(seed) if isinstance(seed, tuple) else seed)
+
+
+def _pcg_words_uncached(seed) -> tuple[int, int, int, int]:
     st = np.random.default_rng(seed).bit_generator.state["state"]
     s, inc = int(st["state"]), int(st["inc"])
     mask = (1 << 64) - 1
@@ -375,7 +388,31 @@ def check_edge(oracle, x1, x2, eps: float = EPS_GEO, *, ctx=None) -> bool:
     return bool(check_edges(oracle, x1[None], x2[None], eps, ctx=ctx)[0])
 
 
+_OBS_CACHE: dict = {}
+_OBS_CACHE_SIZE = 8
+
+
 def _obstacle_arrays(obstacles, m):
+    """``_obstacle_arrays_uncached`` with a small identity cache: a replanning loop or a
+    benchmark cuts the same obstacle objects again and again.  Only lists whose arrays are all
+    read-only (both the reference's and this package's Polytope freeze them) are cached, and an
+    entry keeps its obstacles alive so the identities in its key stay unique."""
+    obstacles = list(obstacles)
+    key = (m,) + tuple((id(ob), id(ob.A), id(ob.b)) for ob in obstacles)
+    hit = _OBS_CACHE.get(key)
+    if hit is not None:
+        return hit[1]
+    out = _obstacle_arrays_uncached(obstacles, m)
+    frozen = all(not np.asarray(ob.A).flags.writeable and not np.asarray(ob.b).flags.writeable
+                 for ob in obstacles if isinstance(getattr(ob, "A", None), np.ndarray))
+    if frozen and all(isinstance(getattr(ob, "A", None), np.ndarray) for ob in obstacles):
+        if len(_OBS_CACHE) >= _OBS_CACHE_SIZE:
+            _OBS_CACHE.pop(next(iter(_OBS_CACHE)))
+        _OBS_CACHE[key] = (obstacles, out)
+    return out
+
+
+def _obstacle_arrays_uncached(obstacles, m):
     """Normalised rows (Polytope.normalized, geometry.py:135-137) and box recovery (as_box,
     geometry.py:155-185), vectorised over obstacles of 2m rows (the box shape)."""
     if not obstacles:
