@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <vector>
 
@@ -87,46 +88,43 @@ __device__ __forceinline__ double dmin2(double a, double b) { return a < b ? a :
 // beats f at every anchor (argmax over active faces), so f is not chosen.  This certifies
 // obstacles far along one axis even when the polygon straddles the plane of a face of
 // another axis (large maps: a few percent of all pairs instead of most).
+// The pass-1 fields of one obstacle, packed for shared memory (16 doubles at m = 2, read
+// as broadcast LDS.128 by every lane).  Built on the host from the ObsRec (fill_cert):
+//   be_hi = b_eps[k], nbe_lo = -b_eps[M+k]   (-P > b_eps  <=>  P < -b_eps, negation exact)
+//   ahi = hi - 1e-6 (act_hi), or -inf for a thin axis (face +k then always possibly active)
+//   alo = lo + 1e-6 (act_lo), or +inf for a thin axis
+//   bh = b[k], bl = b[M+k], hi, lo = as_box bounds
+// A non-canonical obstacle gets be_hi = +inf and nbe_lo = -inf: test (1) then never passes
+// and the pair goes to pass 2 without a separate canon branch.
 template <int M>
-__device__ __forceinline__ bool canon_safe_cert_far(const double (&mn)[M], const double (&mx)[M], const ObsRec<M>& o,
-                                                 double margin) {  // (4), given (1)
-  double L = -INFINITY;       // best lower bound of the separation of a surely-active cleared face
-  double ub_bad = -INFINITY;  // largest upper bound of a possibly-active uncleared face
-  bool any_bad = false;
-#pragma unroll
-  for (int k = 0; k < M; ++k) {
-    const bool thin = o.thin[k] != 0.0;
-    // face +k: sep = fl(v_k - b_k) in [fl(mn_k - b_k), fl(mx_k - b_k)]
-    const double lb_hi = __dsub_rn(mn[k], o.b[k]), ub_hi = __dsub_rn(mx[k], o.b[k]);
-    const bool pa_hi = thin | (mx[k] > o.act_hi[k]);
-    const bool clr_hi = lb_hi > margin;
-    if (clr_hi && mn[k] >= o.hi[k]) L = dmax2(L, lb_hi);
-    if (pa_hi && !clr_hi) { any_bad = true; ub_bad = dmax2(ub_bad, ub_hi); }
-    // face -k: sep = fl(-v_k - b_{M+k}) in [fl(-mx_k - b), fl(-mn_k - b)]
-    const double lb_lo = __dsub_rn(-mx[k], o.b[M + k]), ub_lo = __dsub_rn(-mn[k], o.b[M + k]);
-    const bool pa_lo = thin | (mn[k] < o.act_lo[k]);
-    const bool clr_lo = lb_lo > margin;
-    if (clr_lo && mx[k] <= o.lo[k]) L = dmax2(L, lb_lo);
-    if (pa_lo && !clr_lo) { any_bad = true; ub_bad = dmax2(ub_bad, ub_lo); }
-  }
-  return !any_bad | (ub_bad < L);
-}
+struct __align__(16) CertRec {
+  double be_hi[M], nbe_lo[M], ahi[M], alo[M], bh[M], bl[M], hi[M], lo[M];
+};
 
 template <int M>
-__device__ __forceinline__ bool canon_safe_cert(const double (&mn)[M], const double (&mx)[M], const ObsRec<M>& o,
+__device__ __forceinline__ bool canon_safe_cert(const double (&mn)[M], const double (&mx)[M], const CertRec<M>& o,
                                                 double margin) {
   bool noin = false, ok = true;  // (1)-(3): every possibly-active face cleared
+  double L = -INFINITY;          // (4): best lower bound of the separation of a surely-active cleared face
+  double ub_bad = -INFINITY;     //      largest upper bound of a possibly-active uncleared face
 #pragma unroll
   for (int k = 0; k < M; ++k) {
-    noin |= (mn[k] > o.b_eps[k]) | (-mx[k] > o.b_eps[M + k]);
-    const bool thin = o.thin[k] != 0.0;
-    const bool pa_hi = thin | (mx[k] > o.act_hi[k]);
-    const bool pa_lo = thin | (mn[k] < o.act_lo[k]);
-    const bool clr_hi = __dsub_rn(mn[k], o.b[k]) > margin;
-    const bool clr_lo = __dsub_rn(-mx[k], o.b[M + k]) > margin;
+    noin |= (mn[k] > o.be_hi[k]) | (mx[k] < o.nbe_lo[k]);
+    // face +k: sep = fl(v_k - b_k) in [fl(mn_k - b_k), fl(mx_k - b_k)]
+    const double lb_hi = __dsub_rn(mn[k], o.bh[k]);
+    const bool pa_hi = mx[k] > o.ahi[k], clr_hi = lb_hi > margin;
+    // face -k: sep = fl(-v_k - b_{M+k}) in [fl(-mx_k - b), fl(-mn_k - b)]
+    const double lb_lo = __dsub_rn(-mx[k], o.bl[k]);
+    const bool pa_lo = mn[k] < o.alo[k], clr_lo = lb_lo > margin;
     ok &= (!pa_hi | clr_hi) & (!pa_lo | clr_lo);
+    if (clr_hi && mn[k] >= o.hi[k]) L = dmax2(L, lb_hi);
+    if (clr_lo && mx[k] <= o.lo[k]) L = dmax2(L, lb_lo);
+    if (pa_hi && !clr_hi) ub_bad = dmax2(ub_bad, __dsub_rn(mx[k], o.bh[k]));
+    if (pa_lo && !clr_lo) ub_bad = dmax2(ub_bad, __dsub_rn(-mn[k], o.bl[k]));
   }
-  return noin && (ok || canon_safe_cert_far<M>(mn, mx, o, margin));
+  // with (1): ok, or every uncleared possibly-active face loses to a surely-active cleared one
+  // (no uncleared face leaves ub_bad = -inf < L only when L is finite; ok covers that case)
+  return noin && (ok || ub_bad < L);
 }
 
 // Heuristic code of one edge against one box obstacle: 0 unsafe, 1 safe, 2 indeterminate
@@ -376,13 +374,14 @@ constexpr int kHeurRound = 8;  // pass-2 pairs per edge per round
 // dynamic shared memory of k_cut_heuristic: obstacles, per-warp control points, pair lists, kills
 template <int G, int M>
 size_t heur_smem(int nob) {
-  return sizeof(ObsRec<M>) * nob + (size_t)kHeurWarps * 32 * (M * 2 * G) * sizeof(double) +
+  return (sizeof(ObsRec<M>) + sizeof(CertRec<M>)) * nob + (size_t)kHeurWarps * 32 * (M * 2 * G) * sizeof(double) +
          (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t) + (size_t)kHeurWarps * 32 * sizeof(int);
 }
 
 template <int G, int M>
 __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
-                                const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs, int o0, int o1,
+                                const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
+                                const CertRec<M>* __restrict__ certs, int o0, int o1,
                                 double margin, int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                                 unsigned long long* __restrict__ n_pend, unsigned long long cap,
                                 unsigned long long* __restrict__ pend, unsigned long long* __restrict__ n_gen,
@@ -390,16 +389,24 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
                                 const ObsGrid* __restrict__ grid, const unsigned long long* __restrict__ gmask) {
   constexpr int N = G * M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ObsRec<M>* s_obs = reinterpret_cast<ObsRec<M>*>(smem_raw);
   const bool use_grid = grid != nullptr;  // the host passes the grid only when it is sparse
   const int nob = o1 - o0;
-  // with the grid, each edge touches a few obstacles: read them through L1 instead of staging
-  // every record into every block's shared memory
-  const ObsRec<M>* ob = use_grid ? obs + o0 : s_obs;
+  // shared memory: [CertRec x nob][ObsRec x nob][per-warp pass-2 staging]
+  CertRec<M>* s_cert = reinterpret_cast<CertRec<M>*>(smem_raw);
+  ObsRec<M>* s_obs = reinterpret_cast<ObsRec<M>*>(smem_raw + sizeof(CertRec<M>) * nob);
+  // with the grid, each edge touches a few obstacles: pass 2 reads their full records through
+  // L1 instead of staging every record into every block's shared memory
   if (!use_grid) {
     const double* srcp = reinterpret_cast<const double*>(obs + o0);
     double* dstp = reinterpret_cast<double*>(s_obs);
     const int nd = nob * (int)(sizeof(ObsRec<M>) / sizeof(double));
+    for (int t = threadIdx.x; t < nd; t += blockDim.x) dstp[t] = srcp[t];
+  }
+  // pass-1 records, always staged (compact): the hot loop reads them with broadcast LDS
+  {
+    const double* srcp = reinterpret_cast<const double*>(certs + o0);
+    double* dstp = reinterpret_cast<double*>(s_cert);
+    const int nd = nob * (int)(sizeof(CertRec<M>) / sizeof(double));
     for (int t = threadIdx.x; t < nd; t += blockDim.x) dstp[t] = srcp[t];
   }
   __shared__ unsigned long long s_cnt[3];
@@ -458,16 +465,14 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
     }
     if (cand == all) {
       for (int oi = 0; oi < nob; ++oi) {
-        const ObsRec<M>& o = ob[oi];
-        if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
+        if (canon_safe_cert<M>(mn, mx, s_cert[oi], margin)) ++c1;
         else hard |= 1ull << oi;
       }
     } else {
       c1 += __popcll(all & ~cand);
       for (unsigned long long rest = cand; rest; rest &= rest - 1ull) {
         const int oi = __ffsll((long long)rest) - 1;
-        const ObsRec<M>& o = ob[oi];
-        if (o.canon != 0.0 && canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
+        if (canon_safe_cert<M>(mn, mx, s_cert[oi], margin)) ++c1;
         else hard |= 1ull << oi;
       }
     }
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
   // Each lane's control points are staged in shared memory for the lanes that take its pairs.
   constexpr int NP = M * 2 * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* base = smem_raw + sizeof(ObsRec<M>) * nob;
+  unsigned char* base = smem_raw + (sizeof(ObsRec<M>) + sizeof(CertRec<M>)) * nob;
   double* s_P = reinterpret_cast<double*>(base) + (size_t)warp * 32 * NP;
   base += (size_t)kHeurWarps * 32 * NP * sizeof(double);
   uint16_t* s_it = reinterpret_cast<uint16_t*>(base) + warp * 32 * kHeurRound;
@@ -518,9 +523,12 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
         for (int k = 0; k < M; ++k)
 #pragma unroll
           for (int j = 0; j < 2 * G; ++j) Pq[k][j] = s_P[owner * NP + k * 2 * G + j];
-        const ObsRec<M>& o = ob[oi];
-        if (o.is_box == 0.0) code = any_inside_einsum<G, M>(Pq, o) ? 0 : 3;  // 3: decided by k_cut_general
-        else code = o.canon != 0.0 ? box_code_canon<G, M>(Pq, o, margin) : box_code<G, M>(Pq, o, margin);
+        auto eval = [&](const ObsRec<M>& o) -> int {
+          if (o.is_box == 0.0) return any_inside_einsum<G, M>(Pq, o) ? 0 : 3;  // 3: decided by k_cut_general
+          return o.canon != 0.0 ? box_code_canon<G, M>(Pq, o, margin) : box_code<G, M>(Pq, o, margin);
+        };
+        // two call sites so each reads its records with the address space known (LDS / LDG)
+        code = use_grid ? eval(obs[o0 + oi]) : eval(s_obs[oi]);
         c0 += code == 0;
         c1 += code == 1;
         c2 += code == 2;
@@ -712,6 +720,27 @@ std::vector<ObsRec<M>> fill_obs(int n_obs, const int32_t* row_off, const double*
   return h;
 }
 
+template <int M>
+std::vector<CertRec<M>> fill_cert(const std::vector<ObsRec<M>>& h) {
+  std::vector<CertRec<M>> out(h.size());
+  for (size_t o = 0; o < h.size(); ++o) {
+    const ObsRec<M>& r = h[o];
+    CertRec<M>& q = out[o];
+    const bool canon = r.canon != 0.0;
+    for (int k = 0; k < M; ++k) {
+      q.be_hi[k] = canon ? r.b_eps[k] : INFINITY;
+      q.nbe_lo[k] = canon ? -r.b_eps[M + k] : -INFINITY;
+      q.ahi[k] = r.thin[k] != 0.0 ? -INFINITY : r.act_hi[k];
+      q.alo[k] = r.thin[k] != 0.0 ? INFINITY : r.act_lo[k];
+      q.bh[k] = r.b[k];
+      q.bl[k] = r.b[M + k];
+      q.hi[k] = r.hi[k];
+      q.lo[k] = r.lo[k];
+    }
+  }
+  return out;
+}
+
 // Batched Cut-QP over the work list pend[0 .. n_inst) (graph.py:320-337 / cut_qp 285-299):
 // ADMM, verdict selection, polish.  Fills mk->qp_status / qp_iters / qp_delta / n_polished
 // and d_safe (n_inst verdicts).  polish_mode: 0 none, 1 SOLVED, 2 SOLVED and MAX_ITER.
@@ -858,10 +887,17 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
     using Rec = ObsRec<Mc>;
     const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
+    const std::vector<CertRec<Mc>> hc = fill_cert<Mc>(h);
     DevBuf d_obs, d_cnt;
     DevBuf &d_kill = c->ws[WS_KILL], &d_qkill = c->ws[WS_QKILL], &d_saved = c->ws[WS_SAVED];
-    d_obs.alloc(sizeof(Rec) * h.size(), c->stream);
-    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, h.data(), sizeof(Rec) * h.size(), cudaMemcpyHostToDevice, c->stream));
+    // one upload: [ObsRec x n][CertRec x n] (sizeof(ObsRec) is a multiple of 8)
+    std::vector<unsigned char> hb(sizeof(Rec) * h.size() + sizeof(CertRec<Mc>) * hc.size());
+    std::memcpy(hb.data(), h.data(), sizeof(Rec) * h.size());
+    std::memcpy(hb.data() + sizeof(Rec) * h.size(), hc.data(), sizeof(CertRec<Mc>) * hc.size());
+    d_obs.alloc(hb.size(), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, hb.data(), hb.size(), cudaMemcpyHostToDevice, c->stream));
+    const CertRec<Mc>* d_cert =
+        reinterpret_cast<const CertRec<Mc>*>(static_cast<const unsigned char*>(d_obs.ptr) + sizeof(Rec) * h.size());
     d_kill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_qkill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_saved.alloc(std::max(E, 1ll), c->stream);
@@ -943,7 +979,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
         const unsigned long long* gm =
             use_grid ? d_gmask.as<unsigned long long>() + (size_t)(o0 / chunk) * kGridCells * kGridCells : nullptr;
         launch(c, "k_cut_heuristic", kern, dim3(div_up(E, kHeurThreads)), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(), E,
-               g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), o0, o1, cfg->heur_margin, d_kill.as<int>(), dcnt,
+               g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), d_cert, o0, o1, cfg->heur_margin, d_kill.as<int>(), dcnt,
                dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>(),
                use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm);
       }
