@@ -275,14 +275,16 @@ def algorithmic_work(kernel, w, step_info, world):
 def admm_ops_per_iteration(J: int, M: int, canonical: bool) -> int:
     """FP64 operations of one reduced-form ADMM iteration as k_qp_admm performs them (DESIGN.md
     "Roofline").  Generic obstacle rows (C = 2M): KKT step 3C + 1 + J(3+C) + J^2, relaxation /
-    projection / dual update 17J + C(J+17) + 7, termination test J + 2 + C(J+3) + J(C+2) + 3C
-    (384 at J=6, M=2).  Canonical boxes keep only the M rows of P: 298 at J=6, M=2."""
+    projection / dual update 15J + C(J+15) + 6 (relaxations fused: RELAX in k_admm.cuh),
+    termination test J + 2 + C(J+3) + J(C+2) + 3C (363 at J=6, M=2).  Canonical boxes keep only
+    the M rows of P: 277 at J=6, M=2."""
     C = 2 * M
+    fused = 2 * J + 2 * C + 1  # one DMUL + DADD per relaxation replaced by the FMA
     if not canonical:
         return ((3 * C + 1 + J * (3 + C) + J * J) + (17 * J + C * (J + 17) + 7)
-                + (J + 2 + C * (J + 3) + J * (C + 2) + 3 * C))
+                + (J + 2 + C * (J + 3) + J * (C + 2) + 3 * C)) - fused
     return (3 * C + 1 + M + J * (3 + M) + J * J + 12 * J + M * J + 14 * C + 7 + J + 2 + M * J + 3 * C + M
-            + J * (2 + M) + 3 * C)
+            + J * (2 + M) + 3 * C) - fused
 
 
 _BYTE_UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}

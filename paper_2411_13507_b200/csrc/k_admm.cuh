@@ -9,8 +9,8 @@
 //   S = (sigma + rho) I + (rho - rho^2/kdd) Q'Q + rho_eq 11',
 // inverted once per instance.  Relaxation, projection, dual update, the termination test
 // (rp <= eps_p and rd <= eps_d), the primal-infeasibility certificate and MAX_ITER follow
-// qpsolver.py:164-231 operation by operation; only the linear solve differs from the
-// reference by rounding.
+// qpsolver.py:164-231 operation by operation; only the linear solve and the fused
+// relaxation (RELAX) differ from the reference by rounding.
 //
 // Scheduling: persistent lanes.  Each lane owns one instance; between batches of
 // kAdmmBatch iterations, lanes whose instance terminated fetch the next one with one
@@ -21,6 +21,12 @@
 
 namespace bzg {
 namespace {
+
+// Relaxation alpha*xt + (1-alpha)*x as one FMA over the rounded second product.  The
+// reference rounds both products and the sum; the fused form differs by at most an ulp, the
+// order of the linear-solve difference, and saves 21 FP64 instructions per iteration (4% of
+// k_qp_admm).  Golden QP verdicts, statuses and counters are unchanged (tests/test_gpu_parity.py).
+#define RELAX(a, b) __fma_rn(al, (a), __dmul_rn(oma, (b)))
 
 constexpr int kAdmmBatch = 16;  // default of QpParams::batch (BZG_ADMM_BATCH overrides; 4..32 within 2%)
 
@@ -260,12 +266,12 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         sa += a[j];
-        const double zr = __dadd_rn(__dmul_rn(al, a[j]), __dmul_rn(oma, zl[j]));
+        const double zr = RELAX(a[j], zl[j]);
         const double zn = clip_nonneg(__dadd_rn(zr, RI_MUL(yl[j])));
         const double yn = __dadd_rn(yl[j], RHO_MUL(__dsub_rn(zr, zn)));
         dyl[j] = __dsub_rn(yn, yl[j]);
         sign_ok &= not_pos(dyl[j]);
-        lam[j] = __dadd_rn(__dmul_rn(al, a[j]), __dmul_rn(oma, lam[j]));
+        lam[j] = RELAX(a[j], lam[j]);
         zl[j] = zn;
         yl[j] = yn;
         const double r = __dsub_rn(lam[j], zn);
@@ -280,18 +286,18 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const double d = __fma_rn(rdel[c], ikdd, kp * qa[c]);
-        const double zr = __dadd_rn(__dmul_rn(al, __dsub_rn(qa[c], d)), __dmul_rn(oma, zc[c]));
+        const double zr = RELAX(__dsub_rn(qa[c], d), zc[c]);
         const double zn = clip_upper(__dadd_rn(zr, RI_MUL(yc[c])), b[c]);
         const double yn = __dadd_rn(yc[c], RHO_MUL(__dsub_rn(zr, zn)));
         dyc[c] = __dsub_rn(yn, yc[c]);
         sign_ok &= not_neg(dyc[c]);
-        del[c] = __dadd_rn(__dmul_rn(al, d), __dmul_rn(oma, del[c]));
+        del[c] = RELAX(d, del[c]);
         zc[c] = zn;
         yc[c] = yn;
       }
       double dye;
       {
-        const double zr = __dadd_rn(__dmul_rn(al, sa), __dmul_rn(oma, ze));
+        const double zr = RELAX(sa, ze);
         const double yn = __dadd_rn(ye, __dmul_rn(req, __dsub_rn(zr, 1.0)));  // z clipped to [1, 1]
         dye = __dsub_rn(yn, ye);
         ze = 1.0;
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
     }
   }
 #undef SI
+#undef RELAX
 #undef RHO_MUL
 #undef RI_MUL
 }
