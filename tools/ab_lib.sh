@@ -1,3 +1,6 @@
+# Same-box A/B of two builds of libbzg: the current build vs paper_2411_13507_b200/libbzg_v000.so
+# (built by hand with the variant flags), alternating twice.  CFG=cfg3 by default.
+#   gpurun -- bash tools/ab_lib.sh
 cd $GRAFT_REPO_ROOT
 L=paper_2411_13507_b200
 cp $L/libbzg.so $L/libbzg_new.so
