@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -177,13 +178,26 @@ __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_p
         unsigned long long dv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) dv[q] = ok[q] ? __ldcg(dist + vv[q]) : 0ull;
+        const unsigned am = __activemask();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          if (!ok[q]) continue;
-          const unsigned long long nb = dbits(__dadd_rn(du, cc[q]));
-          if (nb < dv[q]) {
-            const unsigned long long old = atomicMin(dist + vv[q], nb);
-            if (nb < old && atomicExch(stamp + vv[q], sweep) != sweep) qout[atomicAdd(cout, 1)] = vv[q];
+          bool push = false;
+          if (ok[q]) {
+            const unsigned long long nb = dbits(__dadd_rn(du, cc[q]));
+            if (nb < dv[q]) {
+              const unsigned long long old = atomicMin(dist + vv[q], nb);
+              push = nb < old && atomicExch(stamp + vv[q], sweep) != sweep;
+            }
+          }
+          // warp-aggregated enqueue: one atomic on the frontier counter per warp and round
+          // (a per-lane atomicAdd on the single counter serialised the sweep at large V)
+          const unsigned want = __ballot_sync(am, push);
+          if (want) {
+            const int leader = __ffs(want) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(cout, __popc(want));
+            base = __shfl_sync(am, base, leader);
+            if (push) qout[base + __popc(want & ((1u << lane) - 1u))] = vv[q];
           }
         }
       }
@@ -191,6 +205,82 @@ __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_p
     grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[3] = sweep - 1;
+}
+
+// Same frontier Bellman-Ford with the improvement detection moved out of the relax loop:
+// the relax phase issues fire-and-forget atomicMin (RED) on the distance bits, and after a
+// grid barrier a scan over all vertices enqueues those whose distance dropped since the last
+// scan (prev[]), deduplicated by construction.  The queue variant above waits on two
+// returning atomics (atomicMin, then the stamp exchange) per improvement, which at large V
+// made every sweep latency-bound.  Two barriers per sweep; same fixpoint.
+__global__ void k_bf_scan(long long V, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
+                          const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                          unsigned long long* __restrict__ dist, unsigned long long* __restrict__ prev,
+                          int* __restrict__ qa, int* __restrict__ qb, int* __restrict__ counts, int max_sweeps) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  const long long wg = tid / 32, nw = nt / 32;
+  int sweep = 1;
+  for (; sweep <= max_sweeps; ++sweep) {
+    const int* qin = (sweep & 1) ? qa : qb;
+    int* qout = (sweep & 1) ? qb : qa;
+    const int cin = *(volatile int*)&counts[(sweep - 1) % 3];
+    if (cin == 0) break;
+    if (tid == 0) {
+      counts[(sweep + 1) % 3] = 0;
+      counts[4] += cin;
+    }
+    for (long long k = wg; k < cin; k += nw) {
+      const int u = qin[k];
+      const double du = __longlong_as_double((long long)__ldcg(dist + u));
+      const long long e1 = row_ptr[u + 1];
+      for (long long eb = row_ptr[u] + lane; eb < e1; eb += 128) {
+        int vv[4];
+        double cc[4];
+        bool ok[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const long long e = eb + 32 * q;
+          ok[q] = e < e1 && (!alive || alive[e]);
+          vv[q] = ok[q] ? dst[e] : 0;
+          cc[q] = ok[q] ? cost[e] : 0.0;
+        }
+        unsigned long long dv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dv[q] = ok[q] ? __ldcg(dist + vv[q]) : 0ull;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const unsigned long long nb = dbits(__dadd_rn(du, cc[q]));
+          if (ok[q] && nb < dv[q]) atomicMin(dist + vv[q], nb);
+        }
+      }
+    }
+    grid.sync();
+    int* cout = counts + sweep % 3;
+    for (long long v0 = tid - lane; v0 < V; v0 += nt) {  // warp-uniform trip count
+      const long long v = v0 + lane;
+      bool push = false;
+      if (v < V) {
+        const unsigned long long d = __ldcg(dist + v);
+        if (d != prev[v]) {
+          prev[v] = d;
+          push = true;
+        }
+      }
+      const unsigned want = __ballot_sync(0xffffffffu, push);
+      if (want) {
+        const int leader = __ffs(want) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(cout, __popc(want));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (push) qout[base + __popc(want & ((1u << lane) - 1u))] = (int)v;
+      }
+    }
+    grid.sync();
+  }
+  if (tid == 0) counts[3] = sweep - 1;
 }
 
 // parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes)
@@ -238,6 +328,11 @@ __global__ void k_backtrack(long long V, long long v0, long long vg, const int* 
   }
   *len = n;
   *dout = __longlong_as_double((long long)dist[vg]);
+}
+
+__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
 }
 
 __global__ void k_init_sssp(long long V, long long v0, unsigned long long* dist, int* stamp, int* parent,
@@ -369,8 +464,14 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     const int v0i = (int)v0;
     BZG_CHECK_CUDA(cudaMemcpyAsync(cnt.ptr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
     BZG_CHECK_CUDA(cudaMemcpyAsync(qa.ptr, &v0i, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    // the scan variant's second barrier and V-wide scan cost more than the queue's returning
+    // atomics on small graphs (cfg5 10k: 0.22 vs 0.19 ms); from ~16 k vertices it wins
+    // (cfg3 0.33 -> 0.24 ms, cfg5 100k 1.18 -> 0.80 ms).  BZG_BF_IMPL=queue|scan overrides.
+    static const char* bf_env = std::getenv("BZG_BF_IMPL");
+    const bool bf_queue = bf_env ? std::string(bf_env) == "queue" : V < 16384;
+    const void* bf_kern = bf_queue ? (const void*)k_bf_persistent : (const void*)k_bf_scan;
     int per_sm = 0;
-    BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bf_persistent, 256, 0));
+    BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_kern, 256, 0));
     static const int bf_per_sm_env =
         std::getenv("BZG_BF_BLOCKS_PER_SM") ? std::atoi(std::getenv("BZG_BF_BLOCKS_PER_SM")) : 0;
     const int blocks = std::max(1, std::min(per_sm, bf_per_sm_env > 0 ? bf_per_sm_env : 4) * c->num_sms);
@@ -383,8 +484,17 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     int* pb = qb.as<int>();
     int* pc = cnt.as<int>();
     int maxs = (int)std::min<long long>(V + 2, 1 << 30);
-    void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &st, &pa, &pb, &pc, &maxs};
-    launch_coop(c, "k_bf_persistent", (const void*)k_bf_persistent, dim3(blocks), dim3(256), args);
+    if (bf_queue) {
+      void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &st, &pa, &pb, &pc, &maxs};
+      launch_coop(c, "k_bf_persistent", bf_kern, dim3(blocks), dim3(256), args);
+    } else {
+      // prev = dist at init (v0 = 0, others +inf), so the first scan sees only v0's improvements
+      unsigned long long* pv = t_pd.as<unsigned long long>();
+      BZG_CHECK_CUDA(cudaMemcpyAsync(pv, dist, V * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
+      void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &pv, &pa, &pb, &pc, &maxs};
+      launch_coop(c, "k_bf_scan", bf_kern, dim3(blocks), dim3(256), args);
+      launch(c, "k_fill_pd", k_fill_u64, dim3(div_up(V, 256)), dim3(256), 0, pv, V, ~0ull);  // k_parent_dist's init
+    }
     if (c->trace_on) {
       int hc[8];
       BZG_CHECK_CUDA(cudaMemcpyAsync(hc, cnt.ptr, sizeof(hc), cudaMemcpyDeviceToHost, c->stream));
