@@ -99,6 +99,7 @@ __device__ __forceinline__ double dmin2(double a, double b) { return a < b ? a :
 template <int M>
 struct __align__(16) CertRec {
   double be_hi[M], nbe_lo[M], ahi[M], alo[M], bh[M], bl[M], hi[M], lo[M];
+  int idx;  // obstacle index within its launch chunk (records are sorted by lo[0] per chunk)
 };
 
 template <int M>
@@ -374,14 +375,15 @@ constexpr int kHeurRound = 8;  // pass-2 pairs per edge per round
 // dynamic shared memory of k_cut_heuristic: obstacles, per-warp control points, pair lists, kills
 template <int G, int M>
 size_t heur_smem(int nob) {
-  return (sizeof(ObsRec<M>) + sizeof(CertRec<M>)) * nob + (size_t)kHeurWarps * 32 * (M * 2 * G) * sizeof(double) +
+  return (sizeof(ObsRec<M>) + sizeof(CertRec<M>) + 2 * sizeof(double)) * nob +
+         (size_t)kHeurWarps * 32 * (M * 2 * G) * sizeof(double) +
          (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t) + (size_t)kHeurWarps * 32 * sizeof(int);
 }
 
 template <int G, int M>
 __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
                                 const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
-                                const CertRec<M>* __restrict__ certs, int o0, int o1,
+                                const CertRec<M>* __restrict__ certs, int o0, int o1, double wmax,
                                 double margin, int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                                 unsigned long long* __restrict__ n_pend, unsigned long long cap,
                                 unsigned long long* __restrict__ pend, unsigned long long* __restrict__ n_gen,
@@ -391,9 +393,11 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const bool use_grid = grid != nullptr;  // the host passes the grid only when it is sparse
   const int nob = o1 - o0;
-  // shared memory: [CertRec x nob][ObsRec x nob][per-warp pass-2 staging]
+  // shared memory: [CertRec x nob][sorted lo[0] x nob][pos x nob][ObsRec x nob][per-warp pass-2 staging]
   CertRec<M>* s_cert = reinterpret_cast<CertRec<M>*>(smem_raw);
-  ObsRec<M>* s_obs = reinterpret_cast<ObsRec<M>*>(smem_raw + sizeof(CertRec<M>) * nob);
+  double* s_lo = reinterpret_cast<double*>(smem_raw + sizeof(CertRec<M>) * nob);
+  int* s_pos = reinterpret_cast<int*>(s_lo + nob);  // original chunk index -> sorted position
+  ObsRec<M>* s_obs = reinterpret_cast<ObsRec<M>*>(smem_raw + (sizeof(CertRec<M>) + 2 * sizeof(double)) * nob);
   // with the grid, each edge touches a few obstacles: pass 2 reads their full records through
   // L1 instead of staging every record into every block's shared memory
   if (!use_grid) {
@@ -408,6 +412,10 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
     double* dstp = reinterpret_cast<double*>(s_cert);
     const int nd = nob * (int)(sizeof(CertRec<M>) / sizeof(double));
     for (int t = threadIdx.x; t < nd; t += blockDim.x) dstp[t] = srcp[t];
+    for (int t = threadIdx.x; t < nob; t += blockDim.x) {
+      s_lo[t] = certs[o0 + t].lo[0];
+      s_pos[certs[o0 + t].idx] = t;
+    }
   }
   __shared__ unsigned long long s_cnt[3];
   __shared__ int s_done;
@@ -464,15 +472,35 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
       }
     }
     if (cand == all) {
-      for (int oi = 0; oi < nob; ++oi) {
-        if (canon_safe_cert<M>(mn, mx, s_cert[oi], margin)) ++c1;
-        else hard |= 1ull << oi;
+      // x-window over the lo[0]-sorted records: a canonical box farther than T = ext + 0.02
+      // from the bounding box along x is certified code 1 by the ObsGrid argument above
+      // (separation > ext + 0.01 along one axis; the 0.01 slack absorbs the rounding of T and
+      // of the window bounds).  Boxes with lo_x > mx_x + T lie right of it, boxes with
+      // lo_x < mn_x - T - wmax have hi_x <= lo_x + wmax < mn_x - T and lie left of it.
+      int i0 = 0, i1 = nob;
+      if (wmax >= 0.0) {
+        double ext = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) ext = dmax2(ext, __dsub_rn(mx[k], mn[k]));
+        const double T = ext + 0.02, wl = mn[0] - T - wmax, wh = mx[0] + T;
+        int lo = 0, hi = nob;  // first sorted lo >= wl
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lo[mid] < wl) lo = mid + 1; else hi = mid; }
+        i0 = lo;
+        hi = nob;  // first sorted lo > wh
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lo[mid] <= wh) lo = mid + 1; else hi = mid; }
+        i1 = lo;
+        c1 += nob - (i1 - i0);
+      }
+      for (int i = i0; i < i1; ++i) {
+        const CertRec<M>& o = s_cert[i];
+        if (canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
+        else hard |= 1ull << o.idx;
       }
     } else {
       c1 += __popcll(all & ~cand);
       for (unsigned long long rest = cand; rest; rest &= rest - 1ull) {
         const int oi = __ffsll((long long)rest) - 1;
-        if (canon_safe_cert<M>(mn, mx, s_cert[oi], margin)) ++c1;
+        if (canon_safe_cert<M>(mn, mx, s_cert[s_pos[oi]], margin)) ++c1;
         else hard |= 1ull << oi;
       }
     }
@@ -483,7 +511,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
   // Each lane's control points are staged in shared memory for the lanes that take its pairs.
   constexpr int NP = M * 2 * G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* base = smem_raw + (sizeof(ObsRec<M>) + sizeof(CertRec<M>)) * nob;
+  unsigned char* base = smem_raw + (sizeof(ObsRec<M>) + sizeof(CertRec<M>) + 2 * sizeof(double)) * nob;
   double* s_P = reinterpret_cast<double*>(base) + (size_t)warp * 32 * NP;
   base += (size_t)kHeurWarps * 32 * NP * sizeof(double);
   uint16_t* s_it = reinterpret_cast<uint16_t*>(base) + warp * 32 * kHeurRound;
@@ -720,12 +748,16 @@ std::vector<ObsRec<M>> fill_obs(int n_obs, const int32_t* row_off, const double*
   return h;
 }
 
+// Pass-1 records, sorted by lo[0] within each launch chunk, and per chunk the widest box
+// along axis 0 (the x-window of k_cut_heuristic), or -1 when the chunk has a non-canonical
+// obstacle (every such pair must reach pass 2, so no obstacle may be skipped).
 template <int M>
-std::vector<CertRec<M>> fill_cert(const std::vector<ObsRec<M>>& h) {
+std::vector<CertRec<M>> fill_cert(const std::vector<ObsRec<M>>& h, int n_obs, int chunk, std::vector<double>& wmax) {
   std::vector<CertRec<M>> out(h.size());
+  std::vector<CertRec<M>> flat(h.size());
   for (size_t o = 0; o < h.size(); ++o) {
     const ObsRec<M>& r = h[o];
-    CertRec<M>& q = out[o];
+    CertRec<M>& q = flat[o];
     const bool canon = r.canon != 0.0;
     for (int k = 0; k < M; ++k) {
       q.be_hi[k] = canon ? r.b_eps[k] : INFINITY;
@@ -737,6 +769,24 @@ std::vector<CertRec<M>> fill_cert(const std::vector<ObsRec<M>>& h) {
       q.hi[k] = r.hi[k];
       q.lo[k] = r.lo[k];
     }
+  }
+  wmax.clear();
+  for (int o0 = 0; o0 < std::max(n_obs, 1); o0 += chunk) {
+    const int o1 = std::min(std::max(n_obs, 1), o0 + chunk);
+    std::vector<int> ord(o1 - o0);
+    for (int i = 0; i < o1 - o0; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return flat[o0 + a].lo[0] < flat[o0 + b].lo[0]; });
+    double w = 0.0;
+    bool all_canon = n_obs > 0;
+    for (int i = 0; i < o1 - o0; ++i) {
+      out[o0 + i] = flat[o0 + ord[i]];
+      out[o0 + i].idx = ord[i];
+      if (o0 + ord[i] < n_obs) {
+        all_canon = all_canon && h[o0 + ord[i]].canon != 0.0;
+        w = std::max(w, flat[o0 + ord[i]].hi[0] - flat[o0 + ord[i]].lo[0]);
+      }
+    }
+    wmax.push_back(all_canon && std::isfinite(w) ? w : -1.0);
   }
   return out;
 }
@@ -887,17 +937,24 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
     using Rec = ObsRec<Mc>;
     const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
-    const std::vector<CertRec<Mc>> hc = fill_cert<Mc>(h);
-    DevBuf d_obs, d_cnt;
+    // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
+    const int chunk = std::min(64, std::max(1, (int)(96 * 1024 / sizeof(Rec))));
+    std::vector<double> wmax;
+    const std::vector<CertRec<Mc>> hc = fill_cert<Mc>(h, n_obs, chunk, wmax);
+    if (std::getenv("BZG_NO_OBS_WINDOW"))  // read per call (tests toggle it): test every obstacle
+      for (double& w : wmax) w = -1.0;
+    DevBuf d_cnt;
     DevBuf &d_kill = c->ws[WS_KILL], &d_qkill = c->ws[WS_QKILL], &d_saved = c->ws[WS_SAVED];
-    // one upload: [ObsRec x n][CertRec x n] (sizeof(ObsRec) is a multiple of 8)
-    std::vector<unsigned char> hb(sizeof(Rec) * h.size() + sizeof(CertRec<Mc>) * hc.size());
-    std::memcpy(hb.data(), h.data(), sizeof(Rec) * h.size());
-    std::memcpy(hb.data() + sizeof(Rec) * h.size(), hc.data(), sizeof(CertRec<Mc>) * hc.size());
-    d_obs.alloc(hb.size(), c->stream);
-    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, hb.data(), hb.size(), cudaMemcpyHostToDevice, c->stream));
-    const CertRec<Mc>* d_cert =
-        reinterpret_cast<const CertRec<Mc>*>(static_cast<const unsigned char*>(d_obs.ptr) + sizeof(Rec) * h.size());
+    // one upload: [CertRec x n][ObsRec x n] (CertRec is 16-byte aligned and sized; ObsRec needs 8)
+    const size_t cert_bytes = sizeof(CertRec<Mc>) * hc.size();
+    std::vector<unsigned char> hb(cert_bytes + sizeof(Rec) * h.size());
+    std::memcpy(hb.data(), hc.data(), cert_bytes);
+    std::memcpy(hb.data() + cert_bytes, h.data(), sizeof(Rec) * h.size());
+    DevBuf d_obs_all;
+    d_obs_all.alloc(hb.size(), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs_all.ptr, hb.data(), hb.size(), cudaMemcpyHostToDevice, c->stream));
+    const CertRec<Mc>* d_cert = d_obs_all.as<CertRec<Mc>>();
+    const Rec* d_recs = reinterpret_cast<const Rec*>(static_cast<const unsigned char*>(d_obs_all.ptr) + cert_bytes);
     d_kill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_qkill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_saved.alloc(std::max(E, 1ll), c->stream);
@@ -916,8 +973,6 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     DevBuf &d_pend = c->ws[WS_PEND], &d_gen = c->ws[WS_GEN];
     unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
     unsigned long long* dcnt = d_cnt.as<unsigned long long>();
-    // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
-    const int chunk = std::min(64, std::max(1, (int)(96 * 1024 / sizeof(Rec))));
     // spatial pre-screen grid (ObsGrid) for maps with enough obstacles to pay for it
     const int n_chunks = (n_obs + chunk - 1) / chunk;
     const bool grid_off = std::getenv("BZG_NO_OBS_GRID") != nullptr;  // read per call (tests toggle it)
@@ -946,7 +1001,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
         launch(c, "k_obs_grid_extent", k_obs_grid_extent<Gc, Mc>, dim3(div_up(std::min(E, 65536ll), 256)), dim3(256),
                0, dp, g->vertices.as<double>(), E, g->src.as<int>(), g->dst.as<int>(), d_grid.as<ObsGrid>());
         launch(c, "k_obs_grid_masks", k_obs_grid_masks<Mc>, dim3(kGridCells * kGridCells / 256, (unsigned)n_chunks),
-               dim3(256), 0, d_obs.as<Rec>(), n_obs, chunk, blo[0], blo[1], bhi[0], bhi[1], d_grid.as<ObsGrid>(),
+               dim3(256), 0, d_recs, n_obs, chunk, blo[0], blo[1], bhi[0], bhi[1], d_grid.as<ObsGrid>(),
                d_gmask.as<unsigned long long>());
         if (!known) {
           ObsGrid* hg = static_cast<ObsGrid*>(c->host_scratch(sizeof(ObsGrid) + 8 * sizeof(unsigned long long)));
@@ -979,7 +1034,8 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
         const unsigned long long* gm =
             use_grid ? d_gmask.as<unsigned long long>() + (size_t)(o0 / chunk) * kGridCells * kGridCells : nullptr;
         launch(c, "k_cut_heuristic", kern, dim3(div_up(E, kHeurThreads)), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(), E,
-               g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(), d_cert, o0, o1, cfg->heur_margin, d_kill.as<int>(), dcnt,
+               g->src.as<int>(), g->dst.as<int>(), d_recs, d_cert, o0, o1, wmax[o0 / chunk], cfg->heur_margin,
+               d_kill.as<int>(), dcnt,
                dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>(),
                use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm);
       }
@@ -989,7 +1045,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       if (n_gen > 0 && n_gen <= gen_cap) {
         // general obstacles: cut_heuristic past branch 1, appending to the same QP work list
         launch(c, "k_cut_general", k_cut_general<Gc, Mc>, dim3(div_up((long long)n_gen, 64)), dim3(64), 0, dp,
-               g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs.as<Rec>(),
+               g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs,
                d_gen.as<unsigned long long>(), (long long)n_gen, cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5,
                cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr);
         BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
@@ -1022,7 +1078,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     auto run_qp = [&](auto C_) {
       constexpr int Cc = decltype(C_)::value;
       DevBuf &d_safe = c->ws[WS_QSAFE];
-      qp_solve<Gc, Mc, Cc>(c, g, dp, d_obs.as<Rec>(), canon_all, d_pend.as<unsigned long long>(), n_inst, cfg,
+      qp_solve<Gc, Mc, Cc>(c, g, dp, d_recs, canon_all, d_pend.as<unsigned long long>(), n_inst, cfg,
                            cfg->qp_polish ? 1 : 0, polish_screen(), mk, d_safe, trace);
       launch(c, "k_qp_verdicts", k_qp_verdicts, dim3(div_up(n_inst, 256)), dim3(256), 0,
              d_pend.as<unsigned long long>(), n_inst, d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(),

@@ -250,3 +250,18 @@ def test_obstacle_grid_prescreen_is_exact(ctx, monkeypatch):
     assert cnt(m_grid) == cnt(m_full)
     assert np.array_equal(m_grid.alive, m_full.alive)
     assert np.array_equal(m_grid.provenance_codes, m_full.provenance_codes)
+
+
+@pytest.mark.parametrize("name", ["cfg2_rf2000", "maze", "hop1500"])
+def test_obstacle_window_is_exact(ctx, golden, name, monkeypatch):
+    """The sorted x-window of heuristic pass 1 (obstacles farther than the edge's extent
+    along x certified code 1 without a test) leaves every cut outcome unchanged."""
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+    m_win = G.cut_graph(gr, obstacles)
+    monkeypatch.setenv("BZG_NO_OBS_WINDOW", "1")
+    m_all = G.cut_graph(gr, obstacles)
+    cnt = lambda m: [m.pairs_total, m.pairs_point_hit, m.pairs_hyperplane, m.pairs_qp, m.qp_safe, m.qp_unsafe]  # noqa: E731
+    assert cnt(m_win) == cnt(m_all)
+    assert np.array_equal(m_win.alive, m_all.alive)
+    assert np.array_equal(m_win.provenance_codes, m_all.provenance_codes)
