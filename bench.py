@@ -290,16 +290,19 @@ def admm_ops_per_iteration(J: int, M: int, canonical: bool) -> int:
 _BYTE_UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, config: str):
     """dram read+write bytes per launch of `kernel` from the newest committed `ncu --set full`
-    summary (profiles/r*_ncu_full_<kernel>.json, tools/summarize_ncu.py), else None."""
-    files = sorted((ROOT / "profiles").glob(f"r*_ncu_full_{kernel}.json"))
+    capture of this config (profiles/r*_ncu_full_<config>.json, tools/summarize_ncu.py; one
+    step, so one launch per kernel), else None."""
+    files = sorted((ROOT / "profiles").glob(f"r*_ncu_full_{config}.json"))
     if not files:
         return None, None
-    rec = json.loads(files[-1].read_text())["kernels"][0]
+    recs = [r for r in json.loads(files[-1].read_text())["kernels"] if r.get("kernel") == kernel]
+    if not recs:
+        return None, None
     tot = 0.0
     for key in ("dram_read_bytes", "dram_write_bytes"):
-        v = rec.get(key)
+        v = recs[0].get(key)
         if not isinstance(v, dict):
             return None, None
         tot += float(v["value"]) * _BYTE_UNITS.get(v["unit"], 1.0)
@@ -422,7 +425,7 @@ def main():
     if work is not None and dom_n > 0:
         avg_launch_s = dom_ms / dom_n * 1e-3
         achieved = work / dom_n / avg_launch_s
-        traffic, tsrc = ncu_traffic(dom)
+        traffic, tsrc = ncu_traffic(dom, args.config)
         roof.update(bound=bound, achieved=achieved / 1e9, peak=fp64_rate / 1e9, unit="Gop/s (FP64 instr)",
                     frac=achieved / fp64_rate, traffic=traffic, traffic_source=tsrc,
                     algorithmic_ops_per_launch=work / dom_n, avg_launch_ms=dom_ms / dom_n,
