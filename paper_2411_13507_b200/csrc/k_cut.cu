@@ -478,11 +478,17 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
       // of the window bounds).  Boxes with lo_x > mx_x + T lie right of it, boxes with
       // lo_x < mn_x - T - wmax have hi_x <= lo_x + wmax < mn_x - T and lie left of it.
       int i0 = 0, i1 = nob;
+      // y-band: inside the x-window, a box farther than T along y is certified the same way
+      double yl = -INFINITY, yh = INFINITY;
       if (wmax >= 0.0) {
         double ext = 0.0;
 #pragma unroll
         for (int k = 0; k < M; ++k) ext = dmax2(ext, __dsub_rn(mx[k], mn[k]));
         const double T = ext + 0.02, wl = mn[0] - T - wmax, wh = mx[0] + T;
+        if (M >= 2) {
+          yl = mn[M >= 2 ? 1 : 0] - T;  // hi_y < yl: below the band
+          yh = mx[M >= 2 ? 1 : 0] + T;  // lo_y > yh: above it
+        }
         int lo = 0, hi = nob;  // first sorted lo >= wl
         while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lo[mid] < wl) lo = mid + 1; else hi = mid; }
         i0 = lo;
@@ -493,8 +499,11 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
       }
       for (int i = i0; i < i1; ++i) {
         const CertRec<M>& o = s_cert[i];
-        if (canon_safe_cert<M>(mn, mx, o, margin)) ++c1;
-        else hard |= 1ull << o.idx;
+        if ((M >= 2 && (o.hi[M >= 2 ? 1 : 0] < yl || o.lo[M >= 2 ? 1 : 0] > yh)) ||
+            canon_safe_cert<M>(mn, mx, o, margin))
+          ++c1;
+        else
+          hard |= 1ull << o.idx;
       }
     } else {
       c1 += __popcll(all & ~cand);
