@@ -811,10 +811,9 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
   mk->qp_status.alloc(n_inst, c->stream);
   mk->qp_iters.alloc(n_inst * sizeof(int), c->stream);
   mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
-  DevBuf &d_x = c->ws[WS_QX], &d_res = c->ws[WS_QRES], &d_zy = c->ws[WS_QZY], &d_list = c->ws[WS_QLIST];
+  DevBuf &d_x = c->ws[WS_QX], &d_zy = c->ws[WS_QZY], &d_list = c->ws[WS_QLIST];
   DevBuf d_next;
   d_x.alloc(n_inst * NV * sizeof(double), c->stream);
-  d_res.alloc(n_inst * 2 * sizeof(double), c->stream);
   d_safe.alloc(n_inst, c->stream);
   d_next.alloc(sizeof(unsigned long long), c->stream);
   d_zy.alloc(n_inst * 2 * MCc * sizeof(double), c->stream);
@@ -855,10 +854,9 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
          d_zy.as<double>());
   trace("admm");
   BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
-  launch(c, "k_qp_select", k_qp_select<G, M, C>, dim3(div_up(n_inst, 256)), dim3(256), 0, dp,
-         g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, polish_mode, screen,
-         cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(), d_zy.as<double>(), d_res.as<double>(),
-         mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
+  launch(c, "k_qp_select", k_qp_select<G, M, C>, dim3(div_up(n_inst, 256)), dim3(256), 0, n_inst, polish_mode,
+         screen, cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(), mk->qp_delta.as<double>(),
+         d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
   static const bool polish_lu = std::getenv("BZG_POLISH_IMPL") && std::string(std::getenv("BZG_POLISH_IMPL")) == "lu";
   long long n_list = -1;  // known on the host only when it is read back (LU path, tracing)
   if (polish_lu || c->trace_on) {
@@ -875,14 +873,14 @@ void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs,
     ensure_dyn_smem((const void*)k_qp_polish<G, M, C>, psmem);
     launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
            dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
-           cfg->eps_cut, d_x.as<double>(), d_res.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
+           cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
            mk->qp_status.as<int8_t>());
   } else {
     // persistent grid over the device-side list length (at most n_inst entries)
     const long long pblocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 8);
     launch(c, "k_qp_polish", k_qp_polish_reg<G, M, C>, dim3((unsigned)pblocks), dim3(128), 0, dp,
            g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(),
-           d_next.as<unsigned long long>(), cfg->eps_cut, d_x.as<double>(), d_res.as<double>(),
+           d_next.as<unsigned long long>(), cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(),
            mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), mk->qp_status.as<int8_t>());
   }
   trace("select+polish");

@@ -12,19 +12,13 @@ namespace {
 // one is 1e-7-KKT with exact complementarity, so both norms are within ~1e-3 of the
 // optimal ||delta*||).  screen <= 0 polishes every SOLVED instance, as the reference does.
 //
-// For the selected instances the residual maxima rp = max|A x - z|, rd = max|P x + A'y|
-// (qpsolver.py:179-180) are recomputed here from the stored terminal (x, z, y), exactly as
-// the reference records them with the snapshot (qpsolver.py:191).
+// The residual maxima of the selected instances are formed by the polish (qp_residuals).
 template <int G, int M, int C>
-__global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int* __restrict__ src,
-                            const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
-                            const unsigned long long* __restrict__ pend, long long n_inst, int polish,
-                            double screen, double eps_cut, const int8_t* __restrict__ st,
-                            const double* __restrict__ x, const double* __restrict__ zy,
-                            double* __restrict__ res_out, double* __restrict__ delta_out,
-                            uint8_t* __restrict__ safe_out, int* __restrict__ list,
+__global__ void k_qp_select(long long n_inst, int polish, double screen, double eps_cut,
+                            const int8_t* __restrict__ st, const double* __restrict__ x,
+                            double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, int* __restrict__ list,
                             unsigned long long* __restrict__ n_list) {
-  constexpr int J = 2 * G, NV = J + C, MC = C + J + 1;
+  constexpr int J = 2 * G, NV = J + C;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   bool need = false;
   if (t < n_inst) {
@@ -38,34 +32,6 @@ __global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int
     // polish 1: SOLVED only (the verdict is all cut_graph uses); 2: also MAX_ITER, whose
     // polished x the reference returns from solve() (cut_qp's ||delta||)
     need = polish && (solved || (polish == 2 && st[t] == BZG_MAX_ITER)) && (screen <= 0.0 || dl < screen);
-    if (need) {
-      double Q[C][J], b[C];
-      load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[t], Q, b);
-      const double* xv = x + t * NV;
-      const double* z = zy + t * 2 * MC;
-      const double* y = z + MC;
-      double rp = 0.0, rd = 0.0, sl = 0.0;
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        sl = __dadd_rn(sl, xv[j]);
-        rp = fmax(rp, fabs(__dsub_rn(xv[j], z[C + j])));
-        double acc = __dadd_rn(y[C + j], y[MC - 1]);
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], y[c], acc);
-        rd = fmax(rd, fabs(acc));
-      }
-      rp = fmax(rp, fabs(__dsub_rn(sl, z[MC - 1])));
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < J; ++j) acc = __fma_rn(Q[c][j], xv[j], acc);
-        rp = fmax(rp, fabs(__dsub_rn(__dsub_rn(acc, xv[J + c]), z[c])));
-        rd = fmax(rd, fabs(__dsub_rn(__dmul_rn(2.0, xv[J + c]), y[c])));
-      }
-      res_out[t * 2] = rp;
-      res_out[t * 2 + 1] = rd;
-    }
   }
   const unsigned m = __ballot_sync(0xffffffffu, need);
   if (m) {
@@ -74,6 +40,38 @@ __global__ void k_qp_select(DParams dp, const double* __restrict__ Vx, const int
     if (lane == leader) base = atomicAdd(n_list, (unsigned long long)__popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (need) list[base + __popc(m & ((1u << lane) - 1u))] = (int)t;
+  }
+}
+
+// rp = max |A x - z|, rd = max |P x + q + A'y| (qpsolver.py:179-180) at the terminal ADMM
+// iterate (x, z, y): recorded with the snapshot in the reference (qpsolver.py:191), formed
+// here by the polish for its own instances (dense lanes) instead of by k_qp_select, where only
+// the polish candidates among each warp's 32 instances needed them.
+template <int G, int M, int C>
+__device__ __forceinline__ void qp_residuals(const double (&Q)[C][2 * G], const double* __restrict__ xv,
+                                             const double* __restrict__ z, double& rp, double& rd) {
+  constexpr int J = 2 * G, MC = C + J + 1;
+  const double* y = z + MC;
+  double sl = 0.0;
+  rp = 0.0;
+  rd = 0.0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    sl = __dadd_rn(sl, xv[j]);
+    rp = fmax(rp, fabs(__dsub_rn(xv[j], z[C + j])));
+    double acc = __dadd_rn(y[C + j], y[MC - 1]);
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc = __fma_rn(Q[c][j], y[c], acc);
+    rd = fmax(rd, fabs(acc));
+  }
+  rp = fmax(rp, fabs(__dsub_rn(sl, z[MC - 1])));
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc = __fma_rn(Q[c][j], xv[j], acc);
+    rp = fmax(rp, fabs(__dsub_rn(__dsub_rn(acc, xv[J + c]), z[c])));
+    rd = fmax(rd, fabs(__dsub_rn(__dmul_rn(2.0, xv[J + c]), y[c])));
   }
 }
 
@@ -101,7 +99,7 @@ template <int G, int M, int C>
 __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
     DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
     const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
-    long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ res,
+    long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ zy,
     double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NC = J + C + 1;
   constexpr int BS = kPolishThreads;
@@ -117,9 +115,10 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
   double x[NV];
 #pragma unroll
   for (int t = 0; t < NV; ++t) x[t] = x_io[inst * NV + t];
-  const double rp = res[inst * 2], rd = res[inst * 2 + 1];
   double Q[C][J], b[C];
   load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[inst], Q, b);
+  double rp, rd;
+  qp_residuals<G, M, C>(Q, x_io + inst * NV, zy + inst * 2 * MC, rp, rd);
   // constraint slot i of A (graph.py:275-281): i < C obstacle row [Q_i, -e_i];
   // C <= i < C+J lambda bound [e_{i-C}, 0]; i = C+J the sum row [1..1, 0]
   auto Gl = [&](int i, int j) -> double {  // lambda part of row i (compile-time i, j)
@@ -370,15 +369,16 @@ template <int G, int M, int C>
 __device__ __forceinline__ void polish_one_reg(
     long long inst, const DParams& dp, const double* __restrict__ Vx, const int* __restrict__ src,
     const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend,
-    double eps_cut, double* __restrict__ x_io, const double* __restrict__ res, double* __restrict__ delta_out,
+    double eps_cut, double* __restrict__ x_io, const double* __restrict__ zy, double* __restrict__ delta_out,
     uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NS = C + 1;
   double x[NV];
 #pragma unroll
   for (int t = 0; t < NV; ++t) x[t] = x_io[inst * NV + t];
-  const double rp = res[inst * 2], rd = res[inst * 2 + 1];
   double Q[C][J], b[C];
   load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[inst], Q, b);
+  double rp, rd;
+  qp_residuals<G, M, C>(Q, x_io + inst * NV, zy + inst * 2 * MC, rp, rd);
   auto Gl = [&](int i, int j) -> double {  // lambda part of constraint row i (compile-time i, j)
     return i < C ? Q[i < C ? i : 0][j] : (i < C + J ? (i - C == j ? 1.0 : 0.0) : 1.0);
   };
@@ -573,11 +573,11 @@ __global__ void __launch_bounds__(128) k_qp_polish_reg(
     DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
     const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
     const unsigned long long* __restrict__ n_list, double eps_cut, double* __restrict__ x_io,
-    const double* __restrict__ res, double* __restrict__ delta_out, uint8_t* __restrict__ safe_out,
+    const double* __restrict__ zy, double* __restrict__ delta_out, uint8_t* __restrict__ safe_out,
     const int8_t* __restrict__ st) {
   const long long n = (long long)*n_list;
   for (long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x; li < n; li += (long long)gridDim.x * blockDim.x)
-    polish_one_reg<G, M, C>(list[li], dp, Vx, src, dst, obs, pend, eps_cut, x_io, res, delta_out, safe_out, st);
+    polish_one_reg<G, M, C>(list[li], dp, Vx, src, dst, obs, pend, eps_cut, x_io, zy, delta_out, safe_out, st);
 }
 
 }  // namespace
