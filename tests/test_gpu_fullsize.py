@@ -1,0 +1,122 @@
+"""Parity at BASELINE.json's full cfg3 size (20,002 vertices, 4.0e8 ordered pairs, 50 boxes).
+
+The CPU oracle cannot build or cut the whole graph in test time (~1,200 s on one core), so
+the full-size run is checked through what does not depend on size:
+* vertices bitwise (the oracle sampler is cheap at any size);
+* CSR structure: rows non-decreasing, columns strictly increasing inside a row, no self loops;
+* bitwise edges, control points and costs on sampled source-row blocks. The oracle's
+  ``pair_edges(rows=...)`` restricts the pair test to those rows (the multi-GPU row-block cut);
+* the cut on those rows' edges against ``oracle.cut_graph``. The heuristic's pending set is
+  bitwise. QP verdict differences must fall in the solver-sensitive class.
+  alive/provenance must match on every edge no such difference touches;
+* the shortest path: the oracle's heapq Dijkstra on the device's full graph and mask gives the
+  same node sequence and the same cost, bitwise.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_13507_b200 import _native as nat
+from paper_2411_13507_b200 import configs
+from paper_2411_13507_b200 import graph as G
+from paper_2411_13507_b200.bezier import boundary_matrix
+from tests.helpers import qp_solver_sensitive
+
+pytestmark = pytest.mark.gpu
+
+ROW_BLOCKS = [(0, 24), (9_990, 10_014), (19_978, 20_002)]  # the last block holds start and goal
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    ctx = nat.Context(0)
+    nat.set_default_context(ctx)
+    w = configs.BUILDERS["cfg3"]()
+    g = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, w.include, ctx=ctx)
+    mask = G.cut_graph(g, w.obstacles)
+    path = G.find_path(g, mask, w.start, w.goal)
+    yield w, g, mask, path
+    nat.set_default_context(None)
+
+
+def _oracle_vertices(w):
+    return oracle.sample_states(w.N, w.sample_bounds.lo, w.sample_bounds.hi, w.oracle.Xd.A, w.oracle.Xd.b, w.seed,
+                                w.include)
+
+
+def test_cfg3_vertices_and_csr(cfg3):
+    w, g, _, _ = cfg3
+    assert g.num_vertices == 20_002 and g.num_edges > 4_000_000
+    assert g.vertices.tobytes() == _oracle_vertices(w).tobytes()
+    rp, col = g.csr()
+    assert rp[0] == 0 and rp[-1] == g.num_edges and np.all(np.diff(rp) >= 0)
+    src = np.repeat(np.arange(g.num_vertices), np.diff(rp))
+    assert not np.any(src == col)
+    same_row = src[1:] == src[:-1]
+    assert np.all(col[1:][same_row] > col[:-1][same_row])
+    assert np.array_equal(g.edges[:, 0], src) and np.array_equal(g.edges[:, 1], col)
+
+
+def _block(w, g, V, r0, r1):
+    n = w.spec.m * w.spec.gamma
+    A1, A2 = oracle.project(V, w.oracle.F, n)
+    E = oracle.pair_edges(A1, A2, w.oracle.G, rows=(r0, r1))
+    rp, _ = g.csr()
+    lo, hi = int(rp[r0]), int(rp[r1])
+    return E, lo, hi
+
+
+@pytest.mark.parametrize("r0,r1", ROW_BLOCKS)
+def test_cfg3_row_block_edges_points_costs_bitwise(cfg3, r0, r1):
+    w, g, _, _ = cfg3
+    V = g.vertices
+    E, lo, hi = _block(w, g, V, r0, r1)
+    assert E.shape[0] == hi - lo > 0
+    assert np.array_equal(g.edges[lo:hi], E)
+    pts = oracle.edge_points(V, E, boundary_matrix(w.spec), w.spec.gamma, w.spec.m)
+    assert g.edge_points[lo:hi].tobytes() == pts.tobytes()
+    assert g.costs[lo:hi].tobytes() == oracle.edge_costs(pts).tobytes()
+
+
+def test_cfg3_cut_on_row_blocks(cfg3):
+    w, g, mask, _ = cfg3
+    V = g.vertices
+    idx = np.concatenate([np.arange(*_block(w, g, V, r0, r1)[1:]) for r0, r1 in ROW_BLOCKS])
+    obstacles = [(o.A, o.b) for o in w.obstacles]
+    ref = oracle.cut_graph(g.edge_points[idx], obstacles, record=True)
+    # per-(edge, obstacle) QP outcomes of both sides, keyed by (global edge, obstacle)
+    keys_r, st_r, it_r, dl_r = [], [], [], []
+    for oi, entry in enumerate(ref["log"]):
+        if entry["pending"].size:
+            keys_r.append(idx[entry["pending"]] * 64 + oi)
+            st_r.append(entry["status"]); it_r.append(entry["iters"]); dl_r.append(entry["delta"])
+    keys_r = np.concatenate(keys_r)
+    rec = mask.qp_records()
+    keys_d = rec["edge"].astype(np.int64) * 64 + rec["obstacle"]
+    sel = np.isin(rec["edge"], idx)
+    keys_d = keys_d[sel]
+    od, orr = np.argsort(keys_d), np.argsort(keys_r)
+    assert np.array_equal(keys_d[od], keys_r[orr]), "heuristic pending sets differ"
+    st_d, it_d, dl_d = (np.asarray(rec[k])[sel][od] for k in ("status", "iterations", "delta"))
+    st_r, it_r, dl_r = (np.concatenate(a)[orr] for a in (st_r, it_r, dl_r))
+    v_d = (st_d == 0) & (dl_d > 1e-7)
+    v_r = (st_r == 0) & (dl_r > 1e-7)
+    diff = v_d != v_r
+    sens = qp_solver_sensitive(st_d, it_d, dl_d, st_r, it_r, dl_r)
+    print(f"cfg3 row blocks: {idx.size} edges, {keys_r.size} QPs, {int(diff.sum())} verdict differences "
+          f"({int((diff & sens).sum())} solver-sensitive)")
+    assert not np.any(diff & ~sens)
+    touched = np.isin(idx, keys_r[orr][diff] // 64)
+    assert np.array_equal(mask.alive[idx][~touched], ref["alive"][~touched])
+    assert np.array_equal(mask.provenance_codes[idx][~touched], ref["provenance"][~touched])
+
+
+def test_cfg3_path_matches_oracle_dijkstra(cfg3):
+    w, g, mask, path = cfg3
+    tube = w.oracle.tube.error
+    ref_path, ref_dist = oracle.find_path(g.vertices, g.edges, g.costs, mask.alive, w.start, w.goal, w.spec.m,
+                                          tube.lo, tube.hi)
+    assert path is not None and ref_path is not None
+    assert path == list(ref_path)
+    assert G.path_cost(g, path) == float(ref_dist)
