@@ -422,162 +422,168 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
   if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) s_done = 0;
   __syncthreads();
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const bool valid = e < E;
-  double P[M][2 * G] = {};
-  int kill = 0x7fffffff;
-  if (valid) {
-    double xi[N], xj[N];
-    const long long a = src[e], b = dst[e];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      xi[k] = Vx[a * N + k];
-      xj[k] = Vx[b * N + k];
-    }
-    control_points<G, M>(xi, xj, dp.D, P);
-    kill = first_kill[e];
-  }
   unsigned c0 = 0, c1 = 0, c2 = 0;
-  // pass 1 (coherent across the warp): certify code 1 from the control-polygon bounding box
-  unsigned long long hard = 0;
-  if (valid) {
-    double mn[M], mx[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k) {
-      mn[k] = P[k][0];
-      mx[k] = P[k][0];
-#pragma unroll
-      for (int j = 1; j < 2 * G; ++j) { mn[k] = dmin2(mn[k], P[k][j]); mx[k] = dmax2(mx[k], P[k][j]); }
-    }
-    const unsigned long long all = nob >= 64 ? ~0ull : ((1ull << nob) - 1ull);
-    unsigned long long cand = all;
-    // spatial pre-screen (ObsGrid): far obstacles are code 1; used when the grown obstacles
-    // leave most cells empty (large maps; small maps skip it)
-    if (M >= 2 && use_grid) {
-      const ObsGrid gp = *grid;
-      double ext = 0.0;
-#pragma unroll
-      for (int k = 0; k < M; ++k) ext = dmax2(ext, __dsub_rn(mx[k], mn[k]));
-      if (__dadd_rn(ext, 0.01) <= gp.R) {
-        auto cell = [](double v, double o, double s) -> int {  // one cell of slack for rounding
-          const double c = floor((v - o) * s);
-          return (int)fmin(fmax(c, -1.0), (double)kGridCells);
-        };
-        const int cx0 = max(cell(mn[0], gp.x0, gp.inv_cx) - 1, 0), cx1 = min(cell(mx[0], gp.x0, gp.inv_cx) + 1, kGridCells - 1);
-        const int cy0 = max(cell(mn[1], gp.y0, gp.inv_cy) - 1, 0), cy1 = min(cell(mx[1], gp.y0, gp.inv_cy) + 1, kGridCells - 1);
-        unsigned long long m = 0;
-        for (int cy = cy0; cy <= cy1; ++cy)
-          for (int cx = cx0; cx <= cx1; ++cx) m |= gmask[cy * kGridCells + cx];
-        cand &= m;
-      }
-    }
-    if (cand == all) {
-      // x-window over the lo[0]-sorted records: a canonical box farther than T = ext + 0.02
-      // from the bounding box along x is certified code 1 by the ObsGrid argument above
-      // (separation > ext + 0.01 along one axis; the 0.01 slack absorbs the rounding of T and
-      // of the window bounds).  Boxes with lo_x > mx_x + T lie right of it, boxes with
-      // lo_x < mn_x - T - wmax have hi_x <= lo_x + wmax < mn_x - T and lie left of it.
-      int i0 = 0, i1 = nob;
-      // y-band: inside the x-window, a box farther than T along y is certified the same way
-      double yl = -INFINITY, yh = INFINITY;
-      if (wmax >= 0.0) {
-        double ext = 0.0;
-#pragma unroll
-        for (int k = 0; k < M; ++k) ext = dmax2(ext, __dsub_rn(mx[k], mn[k]));
-        const double T = ext + 0.02, wl = mn[0] - T - wmax, wh = mx[0] + T;
-        if (M >= 2) {
-          yl = mn[M >= 2 ? 1 : 0] - T;  // hi_y < yl: below the band
-          yh = mx[M >= 2 ? 1 : 0] + T;  // lo_y > yh: above it
-        }
-        int lo = 0, hi = nob;  // first sorted lo >= wl
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lo[mid] < wl) lo = mid + 1; else hi = mid; }
-        i0 = lo;
-        hi = nob;  // first sorted lo > wh
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lo[mid] <= wh) lo = mid + 1; else hi = mid; }
-        i1 = lo;
-        c1 += nob - (i1 - i0);
-      }
-      for (int i = i0; i < i1; ++i) {
-        const CertRec<M>& o = s_cert[i];
-        if ((M >= 2 && (o.hi[M >= 2 ? 1 : 0] < yl || o.lo[M >= 2 ? 1 : 0] > yh)) ||
-            canon_safe_cert<M>(mn, mx, o, margin))
-          ++c1;
-        else
-          hard |= 1ull << o.idx;
-      }
-    } else {
-      c1 += __popcll(all & ~cand);
-      for (unsigned long long rest = cand; rest; rest &= rest - 1ull) {
-        const int oi = __ffsll((long long)rest) - 1;
-        if (canon_safe_cert<M>(mn, mx, s_cert[s_pos[oi]], margin)) ++c1;
-        else hard |= 1ull << oi;
-      }
-    }
-  }
-  // pass 2 (warp-cooperative): the uncertified (edge, obstacle) pairs of the warp's 32 edges
-  // are dealt out to all 32 lanes, a round of at most kHeurRound pairs per edge at a time, so
-  // lanes whose edge has few hard obstacles do not idle while others work through theirs.
-  // Each lane's control points are staged in shared memory for the lanes that take its pairs.
-  constexpr int NP = M * 2 * G;
+  // persistent blocks: the records above are staged once per block, which then walks 256-edge
+  // tiles (one block per tile restaged ~30 KB of records for every 256 edges)
+  const long long n_tiles = (E + kHeurThreads - 1) / kHeurThreads;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* base = smem_raw + (sizeof(ObsRec<M>) + sizeof(CertRec<M>) + 2 * sizeof(double)) * nob;
-  double* s_P = reinterpret_cast<double*>(base) + (size_t)warp * 32 * NP;
-  base += (size_t)kHeurWarps * 32 * NP * sizeof(double);
-  uint16_t* s_it = reinterpret_cast<uint16_t*>(base) + warp * 32 * kHeurRound;
-  base += (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t);
-  int* s_kill = reinterpret_cast<int*>(base) + warp * 32;
-#pragma unroll
-  for (int k = 0; k < M; ++k)
-#pragma unroll
-    for (int j = 0; j < 2 * G; ++j) s_P[lane * NP + k * 2 * G + j] = P[k][j];
-  s_kill[lane] = kill;
-  const long long e0 = e - lane;
-  __syncwarp();
-  while (__any_sync(0xffffffffu, hard != 0)) {
-    const int cnt = min(__popcll(hard), kHeurRound);
-    int off = cnt;  // inclusive warp scan of cnt
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, off, d);
-      if (lane >= d) off += t;
-    }
-    const int total = __shfl_sync(0xffffffffu, off, 31);
-    off -= cnt;
-    if (lane == 0) atomicAdd(counters + 8, (unsigned long long)total);
-    for (int q = 0; q < cnt; ++q) {
-      const int oi = __ffsll((long long)hard) - 1;
-      hard &= hard - 1;
-      s_it[off + q] = (uint16_t)((lane << 8) | oi);
-    }
-    __syncwarp();
-    for (int b0 = 0; b0 < total; b0 += 32) {
-      int code = -1;
-      unsigned long long item = 0;
-      if (b0 + lane < total) {
-        const int it = s_it[b0 + lane], owner = it >> 8, oi = it & 255;
-        double Pq[M][2 * G];
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-#pragma unroll
-          for (int j = 0; j < 2 * G; ++j) Pq[k][j] = s_P[owner * NP + k * 2 * G + j];
-        auto eval = [&](const ObsRec<M>& o) -> int {
-          if (o.is_box == 0.0) return any_inside_einsum<G, M>(Pq, o) ? 0 : 3;  // 3: decided by k_cut_general
-          return o.canon != 0.0 ? box_code_canon<G, M>(Pq, o, margin) : box_code<G, M>(Pq, o, margin);
-        };
-        // two call sites so each reads its records with the address space known (LDS / LDG)
-        code = use_grid ? eval(obs[o0 + oi]) : eval(s_obs[oi]);
-        c0 += code == 0;
-        c1 += code == 1;
-        c2 += code == 2;
-        if (code == 0) atomicMin(s_kill + owner, o0 + oi);
-        item = ((unsigned long long)(e0 + owner) << 20) | (unsigned long long)(o0 + oi);
+  for (long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const long long e = tile * kHeurThreads + threadIdx.x;
+    const bool valid = e < E;
+    double P[M][2 * G] = {};
+    int kill = 0x7fffffff;
+    if (valid) {
+      double xi[N], xj[N];
+      const long long a = src[e], b = dst[e];
+  #pragma unroll
+      for (int k = 0; k < N; ++k) {
+        xi[k] = Vx[a * N + k];
+        xj[k] = Vx[b * N + k];
       }
-      warp_append(code == 2, item, n_pend, cap, pend);
-      warp_append(code == 3, item, n_gen, gen_cap, gen_pend);
+      control_points<G, M>(xi, xj, dp.D, P);
+      kill = first_kill[e];
     }
+    // pass 1 (coherent across the warp): certify code 1 from the control-polygon bounding box
+    unsigned long long hard = 0;
+    if (valid) {
+      double mn[M], mx[M];
+  #pragma unroll
+      for (int k = 0; k < M; ++k) {
+        mn[k] = P[k][0];
+        mx[k] = P[k][0];
+  #pragma unroll
+        for (int j = 1; j < 2 * G; ++j) { mn[k] = dmin2(mn[k], P[k][j]); mx[k] = dmax2(mx[k], P[k][j]); }
+      }
+      const unsigned long long all = nob >= 64 ? ~0ull : ((1ull << nob) - 1ull);
+      unsigned long long cand = all;
+      // spatial pre-screen (ObsGrid): far obstacles are code 1; used when the grown obstacles
+      // leave most cells empty (large maps; small maps skip it)
+      if (M >= 2 && use_grid) {
+        const ObsGrid gp = *grid;
+        double ext = 0.0;
+  #pragma unroll
+        for (int k = 0; k < M; ++k) ext = dmax2(ext, __dsub_rn(mx[k], mn[k]));
+        if (__dadd_rn(ext, 0.01) <= gp.R) {
+          auto cell = [](double v, double o, double s) -> int {  // one cell of slack for rounding
+            const double c = floor((v - o) * s);
+            return (int)fmin(fmax(c, -1.0), (double)kGridCells);
+          };
+          const int cx0 = max(cell(mn[0], gp.x0, gp.inv_cx) - 1, 0), cx1 = min(cell(mx[0], gp.x0, gp.inv_cx) + 1, kGridCells - 1);
+          const int cy0 = max(cell(mn[1], gp.y0, gp.inv_cy) - 1, 0), cy1 = min(cell(mx[1], gp.y0, gp.inv_cy) + 1, kGridCells - 1);
+          unsigned long long m = 0;
+          for (int cy = cy0; cy <= cy1; ++cy)
+            for (int cx = cx0; cx <= cx1; ++cx) m |= gmask[cy * kGridCells + cx];
+          cand &= m;
+        }
+      }
+      if (cand == all) {
+        // x-window over the lo[0]-sorted records: a canonical box farther than T = ext + 0.02
+        // from the bounding box along x is certified code 1 by the ObsGrid argument above
+        // (separation > ext + 0.01 along one axis; the 0.01 slack absorbs the rounding of T and
+        // of the window bounds).  Boxes with lo_x > mx_x + T lie right of it, boxes with
+        // lo_x < mn_x - T - wmax have hi_x <= lo_x + wmax < mn_x - T and lie left of it.
+        int i0 = 0, i1 = nob;
+        // y-band: inside the x-window, a box farther than T along y is certified the same way
+        double yl = -INFINITY, yh = INFINITY;
+        if (wmax >= 0.0) {
+          double ext = 0.0;
+  #pragma unroll
+          for (int k = 0; k < M; ++k) ext = dmax2(ext, __dsub_rn(mx[k], mn[k]));
+          const double T = ext + 0.02, wl = mn[0] - T - wmax, wh = mx[0] + T;
+          if (M >= 2) {
+            yl = mn[M >= 2 ? 1 : 0] - T;  // hi_y < yl: below the band
+            yh = mx[M >= 2 ? 1 : 0] + T;  // lo_y > yh: above it
+          }
+          int lo = 0, hi = nob;  // first sorted lo >= wl
+          while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lo[mid] < wl) lo = mid + 1; else hi = mid; }
+          i0 = lo;
+          hi = nob;  // first sorted lo > wh
+          while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_lo[mid] <= wh) lo = mid + 1; else hi = mid; }
+          i1 = lo;
+          c1 += nob - (i1 - i0);
+        }
+        for (int i = i0; i < i1; ++i) {
+          const CertRec<M>& o = s_cert[i];
+          if ((M >= 2 && (o.hi[M >= 2 ? 1 : 0] < yl || o.lo[M >= 2 ? 1 : 0] > yh)) ||
+              canon_safe_cert<M>(mn, mx, o, margin))
+            ++c1;
+          else
+            hard |= 1ull << o.idx;
+        }
+      } else {
+        c1 += __popcll(all & ~cand);
+        for (unsigned long long rest = cand; rest; rest &= rest - 1ull) {
+          const int oi = __ffsll((long long)rest) - 1;
+          if (canon_safe_cert<M>(mn, mx, s_cert[s_pos[oi]], margin)) ++c1;
+          else hard |= 1ull << oi;
+        }
+      }
+    }
+    // pass 2 (warp-cooperative): the uncertified (edge, obstacle) pairs of the warp's 32 edges
+    // are dealt out to all 32 lanes, a round of at most kHeurRound pairs per edge at a time, so
+    // lanes whose edge has few hard obstacles do not idle while others work through theirs.
+    // Each lane's control points are staged in shared memory for the lanes that take its pairs.
+    constexpr int NP = M * 2 * G;
+    unsigned char* base = smem_raw + (sizeof(ObsRec<M>) + sizeof(CertRec<M>) + 2 * sizeof(double)) * nob;
+    double* s_P = reinterpret_cast<double*>(base) + (size_t)warp * 32 * NP;
+    base += (size_t)kHeurWarps * 32 * NP * sizeof(double);
+    uint16_t* s_it = reinterpret_cast<uint16_t*>(base) + warp * 32 * kHeurRound;
+    base += (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t);
+    int* s_kill = reinterpret_cast<int*>(base) + warp * 32;
+  #pragma unroll
+    for (int k = 0; k < M; ++k)
+  #pragma unroll
+      for (int j = 0; j < 2 * G; ++j) s_P[lane * NP + k * 2 * G + j] = P[k][j];
+    s_kill[lane] = kill;
+    const long long e0 = e - lane;
     __syncwarp();
+    while (__any_sync(0xffffffffu, hard != 0)) {
+      const int cnt = min(__popcll(hard), kHeurRound);
+      int off = cnt;  // inclusive warp scan of cnt
+  #pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, off, d);
+        if (lane >= d) off += t;
+      }
+      const int total = __shfl_sync(0xffffffffu, off, 31);
+      off -= cnt;
+      if (lane == 0) atomicAdd(counters + 8, (unsigned long long)total);
+      for (int q = 0; q < cnt; ++q) {
+        const int oi = __ffsll((long long)hard) - 1;
+        hard &= hard - 1;
+        s_it[off + q] = (uint16_t)((lane << 8) | oi);
+      }
+      __syncwarp();
+      for (int b0 = 0; b0 < total; b0 += 32) {
+        int code = -1;
+        unsigned long long item = 0;
+        if (b0 + lane < total) {
+          const int it = s_it[b0 + lane], owner = it >> 8, oi = it & 255;
+          double Pq[M][2 * G];
+  #pragma unroll
+          for (int k = 0; k < M; ++k)
+  #pragma unroll
+            for (int j = 0; j < 2 * G; ++j) Pq[k][j] = s_P[owner * NP + k * 2 * G + j];
+          auto eval = [&](const ObsRec<M>& o) -> int {
+            if (o.is_box == 0.0) return any_inside_einsum<G, M>(Pq, o) ? 0 : 3;  // 3: decided by k_cut_general
+            return o.canon != 0.0 ? box_code_canon<G, M>(Pq, o, margin) : box_code<G, M>(Pq, o, margin);
+          };
+          // two call sites so each reads its records with the address space known (LDS / LDG)
+          code = use_grid ? eval(obs[o0 + oi]) : eval(s_obs[oi]);
+          c0 += code == 0;
+          c1 += code == 1;
+          c2 += code == 2;
+          if (code == 0) atomicMin(s_kill + owner, o0 + oi);
+          item = ((unsigned long long)(e0 + owner) << 20) | (unsigned long long)(o0 + oi);
+        }
+        warp_append(code == 2, item, n_pend, cap, pend);
+        warp_append(code == 3, item, n_gen, gen_cap, gen_pend);
+      }
+      __syncwarp();
+    }
+    if (valid) first_kill[e] = s_kill[lane];
+    __syncwarp();  // the warp's staging slices are rewritten by the next tile
   }
-  if (valid) first_kill[e] = s_kill[lane];
   // counters without a block barrier (warps finish pass 2 at different times): warp sums into
   // shared memory, and the block's last warp to finish adds them to the global counters
 #pragma unroll
@@ -1040,7 +1046,8 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
         ensure_dyn_smem((const void*)kern, smem);
         const unsigned long long* gm =
             use_grid ? d_gmask.as<unsigned long long>() + (size_t)(o0 / chunk) * kGridCells * kGridCells : nullptr;
-        launch(c, "k_cut_heuristic", kern, dim3(div_up(E, kHeurThreads)), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(), E,
+        const long long hblocks = std::min<long long>(div_up(E, kHeurThreads), (long long)c->num_sms * 3);
+        launch(c, "k_cut_heuristic", kern, dim3((unsigned)hblocks), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(), E,
                g->src.as<int>(), g->dst.as<int>(), d_recs, d_cert, o0, o1, wmax[o0 / chunk], cfg->heur_margin,
                d_kill.as<int>(), dcnt,
                dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>(),
