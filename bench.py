@@ -178,18 +178,23 @@ class DeviceStep:
         mask = G.CutMask(mh, graph, cnt)
         t2 = time.perf_counter()
         self.local_mask = mask
+        E_all = graph.num_edges
         if self.world > 1:
             from paper_2411_13507_b200 import shard
 
             local_E = graph.num_edges
-            mask = shard.gather_to_all(graph, mask)
+            graph, mask = shard.gather_to_root(graph, mask)
             self.last["local_edges"] = local_E
+            if mask is not None:
+                self.last["gather_bytes"] = mask.gather_bytes  # alive edges only travel to rank 0
+                E_all = mask.pairs_total // len(w.obstacles) if w.obstacles else graph.num_edges
         t3 = time.perf_counter()
         path = None
         if self.rank == 0:
             path = G.find_path(graph, mask, w.start, w.goal)
         t4 = time.perf_counter()
-        self.last.update(E=graph.num_edges, qp=mask.pairs_qp, alive=None, path=path, counters=cnt.tolist(),
+        self.last.update(E=E_all if graph is not None else None, qp=int(cnt[3]), alive=None, path=path,
+                         counters=cnt.tolist(),
                          host_phase_ms={"build": 1e3 * (t1 - t0), "cut": 1e3 * (t2 - t1), "gather": 1e3 * (t3 - t2),
                                         "path": 1e3 * (t4 - t3)})
         self.last_graph, self.last_mask = graph, mask
@@ -231,7 +236,7 @@ def public_api_step(w, ctx, rank, world):
         g = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, include=w.include, ctx=ctx, rows=rows)
     mask = G.cut_graph(g, w.obstacles)
     if world > 1:
-        mask = shard.gather_to_all(g, mask)
+        g, mask = shard.gather_to_root(g, mask)
     path = G.find_path(g, mask, w.start, w.goal) if rank == 0 else None
     return path
 

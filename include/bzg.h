@@ -113,6 +113,13 @@ typedef struct {
   int64_t k_nearest;
 } bzg_build_desc;
 
+/* north-star eps-band report: ordered pairs (i != j) whose minimum constraint slack
+ * min_r (G_r + eps_geo - (F1 x_i + F2 x_j)_r) lies in (-eps, eps], counted over g's source-row
+ * block as counts[1] - counts[2] with counts[1] = #pairs feasible with every threshold
+ * fl(G_r + eps_geo) + eps and counts[2] = # with fl(G_r + eps_geo) - eps; counts[0] = the band.
+ * desc = the descriptor g was built from (its vertices are g's; k_nearest is ignored). */
+int bzg_graph_eps_band(bzg_graph* g, const bzg_build_desc* desc, double eps, int64_t counts[3]);
+
 /* the sampler alone (graph.py:147-157): N accepted states of one PCG64 stream written to a
  * host buffer (N, n); uses desc's m, gamma, N, pcg_*, sample_lo/hi, xd_*, eps_geo */
 int bzg_sample_states(bzg_ctx* ctx, const bzg_build_desc* desc, double* out_host);
@@ -124,15 +131,21 @@ int bzg_sample_region_states(bzg_ctx* ctx, int32_t n, int32_t n_regions, const i
                              const double* lo, const double* hi, const int32_t* row_off, const double* A,
                              const double* b, double eps_geo, double* out_host);
 
-/* replaces graph.build_graph (graph.py:129-199) minus k_nearest */
+/* replaces graph.build_graph (graph.py:129-199), k_nearest prefilter included */
 int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* desc, bzg_graph** out);
 /* assemble a graph from an existing edge list (device or host pointers), used by
  * the multi-GPU gather on rank 0; edges must be in row-major (src, dst) order */
 int bzg_graph_from_edges(bzg_ctx* ctx, int32_t m, int32_t gamma, int32_t p, const double* D, int64_t V,
                          const double* vertices_host, int64_t E, const int32_t* src, const int32_t* dst,
                          const double* cost, int on_device, bzg_graph** out);
-/* replace the edge set of g (row-major ordered (src, dst) + cost; device or host pointers):
- * rank 0 adopts the gathered edge list of all row blocks; the row block becomes [0, V) */
+/* a new graph over the vertices of `like` (copied on the device) with the given edge list
+ * (row-major (src, dst) + cost; device or host pointers): rank 0's graph of the gathered row
+ * blocks.  `like` and its masks stay valid. */
+int bzg_graph_with_edges(const bzg_graph* like, int64_t E, const int32_t* src, const int32_t* dst,
+                         const double* cost, int on_device, bzg_graph** out);
+/* replace the edge set of g (row-major ordered (src, dst) + cost; device or host pointers);
+ * the row block becomes [0, V).  Masks cut before the change become stale: bzg_find_path,
+ * bzg_mask_copy and bzg_mask_export_device reject them with BZG_EINVAL. */
 int bzg_graph_set_edges(bzg_graph* g, int64_t E, const int32_t* src, const int32_t* dst, const double* cost,
                         int on_device);
 int bzg_graph_destroy(bzg_graph* g);
@@ -182,6 +195,8 @@ int bzg_cut_points(bzg_ctx* ctx, int32_t m, int32_t J, int64_t B, const double* 
                    const double* box_lo, const double* box_hi, const bzg_cut_config* cfg, int32_t mode, int8_t* code,
                    double* delta, int8_t* status);
 int bzg_mask_destroy(bzg_mask* mk);
+/* edge count the mask was cut for, and its QP instance count */
+int bzg_mask_info(const bzg_mask* mk, int64_t* E, int64_t* n_qp);
 /* counters: pairs_total, pairs_point_hit, pairs_hyperplane, pairs_qp, qp_safe, qp_unsafe (graph.py:97-102) */
 int bzg_mask_copy(bzg_mask* mk, uint8_t* alive /* (E,) */, uint8_t* provenance /* (E,) */, int64_t counters[6]);
 /* QP diagnostics of the last cut: per solved instance (edge, obstacle, status, iterations, ||delta||) */

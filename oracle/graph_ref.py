@@ -81,6 +81,28 @@ def pair_edges(A1, A2, G, eps=EPS_GEO, allowed=None, rows=None):
     return np.stack([np.concatenate(src_l), np.concatenate(dst_l)], axis=1).astype(np.int64)
 
 
+def eps_band(A1, A2, G, band_eps, eps=EPS_GEO, rows=None):
+    """North-star eps-band count over ordered pairs i != j (source rows ``rows``):
+    #all(lhs <= (G + eps) + band_eps) - #all(lhs <= (G + eps) - band_eps), lhs = A1[i] + A2[j]
+    exactly as graph.py:176-184 forms it.  Returns (band, plus, minus)."""
+    th = np.asarray(G) + eps
+    hi, lo_ = th + band_eps, th - band_eps
+    V = A1.shape[0]
+    r0, r1 = (0, V) if rows is None else rows
+    plus = minus = 0
+    for lo in range(r0, r1, PAIR_CHUNK):
+        h = min(lo + PAIR_CHUNK, r1)
+        lhs = A1[lo:h][:, None, :] + A2[None, :, :]
+        a = np.all(lhs <= hi, axis=2)
+        b = np.all(lhs <= lo_, axis=2)
+        idx = np.arange(h - lo)
+        a[idx, idx + lo] = False
+        b[idx, idx + lo] = False
+        plus += int(a.sum())
+        minus += int(b.sum())
+    return plus - minus, plus, minus
+
+
 def check_edges(F, G, n, X1, X2, eps=EPS_GEO):
     """Separable batched predicate (reference reachability.py:139-142)."""
     F = np.asarray(F, np.float64)

@@ -77,8 +77,10 @@ _SIGS = {
     "bzg_ctx_reset_stats": ([_P], C.c_int),
     "bzg_build_graph": ([_P, C.POINTER(BuildDesc), C.POINTER(_P)], C.c_int),
     "bzg_sample_states": ([_P, C.POINTER(BuildDesc), _P], C.c_int),
+    "bzg_graph_eps_band": ([_P, C.POINTER(BuildDesc), C.c_double, _P], C.c_int),
     "bzg_graph_from_edges": ([_P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P, C.c_int64, _P, _P, _P,
                               C.c_int, C.POINTER(_P)], C.c_int),
+    "bzg_graph_with_edges": ([_P, C.c_int64, _P, _P, _P, C.c_int, C.POINTER(_P)], C.c_int),
     "bzg_graph_set_edges": ([_P, C.c_int64, _P, _P, _P, C.c_int], C.c_int),
     "bzg_graph_destroy": ([_P], C.c_int),
     "bzg_graph_info": ([_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
@@ -95,6 +97,7 @@ _SIGS = {
                         C.POINTER(CutConfigC), C.c_int32, _P, _P, _P], C.c_int),
     "bzg_mask_destroy": ([_P], C.c_int),
     "bzg_mask_copy": ([_P, _P, _P, _P], C.c_int),
+    "bzg_mask_info": ([_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
     "bzg_mask_qp_count": ([_P, C.POINTER(C.c_int64)], C.c_int),
     "bzg_mask_copy_qp": ([_P, _P, _P, _P, _P, _P], C.c_int),
     "bzg_mask_from_arrays": ([_P, _P, _P, _P, _P, C.c_int, C.POINTER(_P)], C.c_int),

@@ -257,7 +257,9 @@ struct Mask {
 void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices);
 void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
                     const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out);
-void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g);
+// th_shift moves every oracle threshold (eps-band counting); count_only != nullptr returns the
+// edge count there and leaves g's CSR untouched
+void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift = 0.0, long long* count_only = nullptr);
 void materialize_points(Ctx* c, Graph* g);
 void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, const double* cost, bool on_device);
 void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, double eps, int64_t k,

@@ -202,6 +202,22 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
   return rc;
 }
 
+int bzg_graph_eps_band(bzg_graph* g, const bzg_build_desc* d, double eps, int64_t counts[3]) {
+  return guarded([&] {
+    BZG_REQUIRE(g && d && counts && d->F && d->G, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(eps >= 0.0, BZG_EINVAL, "eps must be non-negative");
+    BZG_REQUIRE(d->m == g->m && d->gamma == g->gamma && d->N + d->n_include == g->V, BZG_EINVAL,
+                "descriptor does not describe this graph");
+    set_device(g->ctx);
+    long long plus = 0, minus = 0;
+    build_pairs(g->ctx, d, g, eps, &plus);
+    build_pairs(g->ctx, d, g, -eps, &minus);
+    counts[0] = plus - minus;
+    counts[1] = plus;
+    counts[2] = minus;
+  });
+}
+
 int bzg_sample_states(bzg_ctx* ctx, const bzg_build_desc* d, double* out_host) {
   return guarded([&] {
     BZG_REQUIRE(ctx && d && out_host, BZG_EINVAL, "null argument");
@@ -261,6 +277,27 @@ int bzg_graph_from_edges(bzg_ctx* ctx, int32_t m, int32_t gamma, int32_t p, cons
     g->vertices.alloc((size_t)V * g->n * sizeof(double), ctx->stream);
     BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.ptr, vertices_host, (size_t)V * g->n * sizeof(double),
                                    cudaMemcpyHostToDevice, ctx->stream));
+    set_edges(ctx, g, E, src, dst, cost, on_device != 0);
+  });
+  if (rc == BZG_OK) *out = g; else delete g;
+  return rc;
+}
+
+int bzg_graph_with_edges(const bzg_graph* like, int64_t E, const int32_t* src, const int32_t* dst,
+                         const double* cost, int on_device, bzg_graph** out) {
+  bzg_graph* g = nullptr;
+  int rc = guarded([&] {
+    BZG_REQUIRE(like && out && (E == 0 || (src && dst && cost)), BZG_EINVAL, "null argument");
+    Ctx* ctx = like->ctx;
+    set_device(ctx);
+    g = new bzg_graph();
+    g->ctx = ctx;
+    g->m = like->m; g->gamma = like->gamma; g->p = like->p; g->n = like->n;
+    g->V = like->V;
+    g->D = like->D;
+    g->vertices.alloc((size_t)g->V * g->n * sizeof(double), ctx->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.ptr, like->vertices.ptr, (size_t)g->V * g->n * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
     set_edges(ctx, g, E, src, dst, cost, on_device != 0);
   });
   if (rc == BZG_OK) *out = g; else delete g;
@@ -414,6 +451,8 @@ int bzg_mask_destroy(bzg_mask* mk) {
 int bzg_mask_copy(bzg_mask* mk, uint8_t* alive, uint8_t* provenance, int64_t counters[6]) {
   return guarded([&] {
     BZG_REQUIRE(mk && mk->g, BZG_EINVAL, "null mask");
+    BZG_REQUIRE((!alive && !provenance) || mk->E == mk->g->E, BZG_EINVAL,
+                "stale mask: its graph's edge set changed after the cut");
     Ctx* c = mk->g->ctx;
     set_device(c);
     if (alive && mk->E > 0) BZG_CHECK_CUDA(cudaMemcpyAsync(alive, mk->alive.ptr, mk->E, cudaMemcpyDeviceToHost, c->stream));
@@ -422,6 +461,14 @@ int bzg_mask_copy(bzg_mask* mk, uint8_t* alive, uint8_t* provenance, int64_t cou
     if (counters)
       for (int i = 0; i < 6; ++i) counters[i] = mk->counters[i];
     BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bzg_mask_info(const bzg_mask* mk, int64_t* E, int64_t* n_qp) {
+  return guarded([&] {
+    BZG_REQUIRE(mk, BZG_EINVAL, "null mask");
+    if (E) *E = mk->E;
+    if (n_qp) *n_qp = mk->n_qp;
   });
 }
 
@@ -477,6 +524,7 @@ int bzg_mask_from_arrays(bzg_ctx* ctx, bzg_graph* g, const uint8_t* alive, const
 int bzg_mask_export_device(bzg_mask* mk, uint8_t* alive, uint8_t* provenance) {
   return guarded([&] {
     BZG_REQUIRE(mk && mk->g, BZG_EINVAL, "null mask");
+    BZG_REQUIRE(mk->E == mk->g->E, BZG_EINVAL, "stale mask: its graph's edge set changed after the cut");
     Ctx* c = mk->g->ctx;
     set_device(c);
     if (mk->E > 0) {
@@ -493,6 +541,7 @@ int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start,
   return guarded([&] {
     BZG_REQUIRE(ctx && g && start && goal && tube_lo && tube_hi && path_len, BZG_EINVAL, "null argument");
     BZG_REQUIRE(!mk || mk->g == g, BZG_EINVAL, "mask belongs to another graph");
+    BZG_REQUIRE(!mk || mk->E == g->E, BZG_EINVAL, "stale mask: its graph's edge set changed after the cut");
     set_device(ctx);
     std::vector<int64_t> path;
     double dist = 0.0;

@@ -964,7 +964,7 @@ void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg,
   }
 }
 
-void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
+void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, long long* count_only) {
   const int n = g->n;
   const int nF = d->n_F;
   const long long V = g->V;
@@ -977,6 +977,8 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
   rp.n = n;
   std::vector<double> th(nF);
   for (int r = 0; r < nF; ++r) th[r] = d->G[r] + d->eps_geo;  // oracle.G + EPS_GEO (graph.py:176)
+  if (th_shift != 0.0)  // eps-band count (bzg_graph_eps_band): every threshold moved by +-eps
+    for (int r = 0; r < nF; ++r) th[r] = th[r] + th_shift;
   auto zero = [&](int r, int off) {
     for (int k = 0; k < n; ++k)
       if (d->F[(size_t)r * 2 * n + off + k] != 0.0) return false;
@@ -1097,7 +1099,8 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
         const double* f = d->region_F + (size_t)q * 2 * n;
         bool z1 = true, z2 = true;
         for (int k = 0; k < n; ++k) { z1 &= f[k] == 0.0; z2 &= f[n + k] == 0.0; }
-        const double th = d->region_G[q] + d->eps_geo;  // check_edges: G + eps (reachability.py:142)
+        double th = d->region_G[q] + d->eps_geo;  // check_edges: G + eps (reachability.py:142)
+        if (th_shift != 0.0) th = th + th_shift;
         BZG_REQUIRE(z1 || z2, BZG_EUNSUPPORTED, "a keep-in region row couples both endpoints");
         if (z1 && z2) { never_r |= !(0.0 <= th); continue; }
         if (z2) { sF.insert(sF.end(), f, f + n); sth.push_back(th); }
@@ -1201,7 +1204,7 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
     }
 #undef BZG_K
   }
-  if (d->k_nearest >= 0 && !never && rows > 0) {
+  if (d->k_nearest >= 0 && !never && rows > 0 && !count_only) {
     BZG_REQUIRE(m <= 3, BZG_EUNSUPPORTED, "k_nearest prefilter supports m <= 3");
     const long long k = std::min<long long>(d->k_nearest, V - 1);
     launch(c, "k_knn_rows", k_knn_rows, dim3((unsigned)rows), dim3(kKnnThreads), 0, g->vertices.as<double>(), V, n, m,
@@ -1213,6 +1216,10 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g) {
   BZG_CHECK_CUDA(cudaMemcpyAsync(h, rptr.as<long long>() + rows, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
   const long long E = h[0];
+  if (count_only) {
+    *count_only = E;
+    return;
+  }
   BZG_REQUIRE(E < (1ll << 31), BZG_EUNSUPPORTED, "edge count exceeds the int32 CSR index range");
   g->E = E;
   g->src.alloc(E * sizeof(int), c->stream);

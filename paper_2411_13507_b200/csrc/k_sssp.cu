@@ -36,12 +36,32 @@ struct SnapParams {
 // norm of (v - target) over the first m_norm components, numpy order (graph.py:375/379):
 // sqrt of the sequential sum of squares.
 __device__ __forceinline__ double snap_norm(const double* v, const SnapParams& sp) {
-  double d0 = __dsub_rn(v[0], sp.target[0]);
-  double s = __dmul_rn(d0, d0);
-  for (int k = 1; k < sp.m_norm; ++k) {
+  // np.linalg.norm(axis=1) = sqrt(add.reduce(d*d)) over each contiguous row: numpy's pairwise
+  // sum, which is a left fold below 8 terms and, from 8 to 128 terms, eight interleaved
+  // partial sums combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a left-folded tail
+  // (checked against numpy for n = 4, 6, 8, 9, 12 on 200k rows).
+  const int n = sp.m_norm;
+  double sq[16];
+  for (int k = 0; k < n; ++k) {
     const double dk = __dsub_rn(v[k], sp.target[k]);
-    s = __dadd_rn(s, __dmul_rn(dk, dk));
+    sq[k] = __dmul_rn(dk, dk);
   }
+  double s;
+  int k0;
+  if (n < 8) {
+    s = sq[0];
+    k0 = 1;
+  } else {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = sq[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sq[i + j]);
+    s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                  __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    k0 = i;
+  }
+  for (int k = k0; k < n; ++k) s = __dadd_rn(s, sq[k]);
   return __dsqrt_rn(s);
 }
 

@@ -102,6 +102,19 @@ class BezierGraph:
         self._V, self._E = V.value, E.value
         self.row_block = (rb.value, re_.value)
         self._cache: dict = {}
+        self._desc_fn = None  # rebuilds the bzg_build_desc this graph came from (eps_band)
+
+    def eps_band(self, eps: float = 1e-11) -> dict:
+        """North-star report: ordered pairs whose minimum constraint slack lies in (-eps, eps]
+        (bzg_graph_eps_band), i.e. the pairs whose edge bit could flip under an eps change of
+        the thresholds.  ``band`` = feasible(G+eps) - feasible(G-eps) over this graph's rows."""
+        if self._desc_fn is None:
+            raise ValueError("this graph was not built by build_graph / build_region_graph")
+        d, keep = self._desc_fn()
+        out = np.zeros(3, dtype=np.int64)
+        nat.check(self._ctx.lib.bzg_graph_eps_band(self._h, C.byref(d), float(eps), nat.ptr(out)))
+        del keep
+        return {"eps": float(eps), "band": int(out[0]), "feasible_plus": int(out[1]), "feasible_minus": int(out[2])}
 
     # ---- reference fields, materialised lazily
     @property
@@ -184,8 +197,15 @@ class CutMask:
         self._prov = None
         self._prov_codes = None
 
+    @property
+    def num_edges(self) -> int:
+        """Edge count this mask was cut for (bzg_mask_info)."""
+        E = C.c_int64()
+        nat.check(self._graph._ctx.lib.bzg_mask_info(self._h, C.byref(E), None))
+        return E.value
+
     def _copy(self):
-        E = self._graph.num_edges
+        E = self.num_edges
         a = np.empty(E, dtype=np.uint8)
         p = np.empty(E, dtype=np.uint8)
         nat.check(self._graph._ctx.lib.bzg_mask_copy(self._h, nat.ptr(a), nat.ptr(p), None))
@@ -359,7 +379,9 @@ def build_graph(N, spec, oracle, bounds, seed, include=None, k_nearest=None, *, 
         raise ValueError(ctx.lib.bzg_last_error().decode())
     nat.check(rc)
     del keep
-    return BezierGraph(h, ctx, spec, oracle, seed, bounds, D)
+    gr = BezierGraph(h, ctx, spec, oracle, seed, bounds, D)
+    gr._desc_fn = lambda: _build_desc(N, spec, oracle, bounds, seed, include, vertices=None, rows=rows)[:2]
+    return gr
 
 
 def check_edges(oracle, X1, X2, eps: float = EPS_GEO, *, ctx=None) -> np.ndarray:

@@ -175,8 +175,9 @@ def build_region_graph(N_per_region, spec, oracle, regions, sample: Box, seed, i
     if rc == nat.BZG_EINVAL:
         raise ValueError(ctx.lib.bzg_last_error().decode())
     nat.check(rc)
-    del keep
-    return G.BezierGraph(h, ctx, spec, oracle, seed, sample, D)
+    gr = G.BezierGraph(h, ctx, spec, oracle, seed, sample, D)
+    gr._desc_fn = lambda: (d, keep)
+    return gr
 
 
 def grid_regions(nx: int, ny: int, side_x: float, side_y: float, overlap: float = 0.10) -> list:

@@ -85,15 +85,79 @@ def per_obstacle_detail(g, obstacles, cfg):
             np.array(it, np.int64), np.array(dl))
 
 
+def recorded_cut(g, obstacles, cfg):
+    """Run the reference's own cut_graph once while recording, per QP, what it decided.
+
+    `_heuristic_batch` and `qpsolver.solve_batch` are wrapped (the originals still do all the
+    work), so the per-(edge, obstacle) QP outcomes come from the very calls cut_graph makes
+    (graph.py:312-337), in its order: obstacle-major, pending edges ascending.
+    """
+    J = g.spec.p + 1
+    state = {"obstacle": -1, "pending": None}
+    po, pe, st, it, dl = [], [], [], [], []
+    orig_h, orig_s = rg._heuristic_batch, rqp.solve_batch
+
+    def heur(points, obstacle, c):
+        codes = orig_h(points, obstacle, c)
+        state["obstacle"] += 1
+        state["pending"] = np.nonzero(codes == 2)[0]
+        return codes
+
+    def solve(probs, c):
+        sols = orig_s(probs, c)
+        pend = state["pending"]
+        assert pend is not None and len(pend) == len(sols)
+        po.append(np.full(len(sols), state["obstacle"], np.int32))
+        pe.append(pend.astype(np.int64))
+        st.append(np.array([STATUS[s.status.value] for s in sols], np.int8))
+        it.append(np.array([s.iterations for s in sols], np.int64))
+        dl.append(np.array([float(np.linalg.norm(s.x[J:])) for s in sols]))
+        return sols
+
+    rg._heuristic_batch, rqp.solve_batch = heur, solve
+    try:
+        mask = rg.cut_graph(g, obstacles, cfg)
+    finally:
+        rg._heuristic_batch, rqp.solve_batch = orig_h, orig_s
+    cat = lambda l, dt: np.concatenate(l) if l else np.zeros(0, dt)  # noqa: E731
+    return mask, (cat(po, np.int32), cat(pe, np.int64), cat(st, np.int8), cat(it, np.int64), cat(dl, np.float64))
+
+
+def eps_band_count(oracle, V, n, eps=1e-11, chunk=32):
+    """Ordered pairs (i != j) whose minimum constraint slack min_r(thresh_r - (a1[i,r] + a2[j,r]))
+    lies in (-eps, eps], counted as #feasible(thresh + eps) - #feasible(thresh - eps) with the
+    reference's own pair arithmetic (graph.py:172-189: a1 + a2 <= G + EPS_GEO)."""
+    A1 = V @ oracle.F[:, :n].T
+    A2 = V @ oracle.F[:, n:].T
+    th = oracle.G + rg.EPS_GEO
+    hi, lo = th + eps, th - eps
+    cnt = 0
+    for s in range(0, V.shape[0], chunk):
+        e = min(s + chunk, V.shape[0])
+        lhs = A1[s:e][:, None, :] + A2[None, :, :]
+        a = np.all(lhs <= hi, axis=2)
+        b = np.all(lhs <= lo, axis=2)
+        idx = np.arange(e - s)
+        a[idx, idx + s] = False
+        b[idx, idx + s] = False
+        cnt += int(a.sum()) - int(b.sum())
+    return cnt
+
+
 def capture(name, N, spec, oracle, bounds, seed, include, obstacles, start, goal, *, full, detail,
-            goals=None, relaxed_starts=None):
+            goals=None, relaxed_starts=None, band=False, compact_qp=False):
     t0 = time.perf_counter()
     g = rg.build_graph(N, spec, oracle, bounds, seed, include=include)
     t_build = time.perf_counter() - t0
+    print(f"{name}: built V={g.num_vertices} E={g.num_edges} in {t_build:.1f}s", flush=True)
     cfg = rg.CutConfig()
     t0 = time.perf_counter()
-    mask = rg.cut_graph(g, obstacles, cfg)
+    if detail == "record":
+        mask, qp_detail = recorded_cut(g, obstacles, cfg)
+    else:
+        mask = rg.cut_graph(g, obstacles, cfg)
     t_cut = time.perf_counter() - t0
+    print(f"{name}: cut alive={mask.alive_count} qp={mask.pairs_qp} in {t_cut:.1f}s", flush=True)
     t0 = time.perf_counter()
     path = rg.find_path(g, mask, start, goal)
     t_path = time.perf_counter() - t0
@@ -128,9 +192,23 @@ def capture(name, N, spec, oracle, bounds, seed, include, obstacles, start, goal
         rec.update(vertices=g.vertices, edges_head=g.edges[:k], costs_head=g.costs[:k],
                    points_head=g.edge_points[:k],
                    row_counts=np.bincount(g.edges[:, 0], minlength=g.num_vertices).astype(np.int64))
-    if detail:
+    if detail == "record":
+        po, pe, st, it, dl = qp_detail
+        if compact_qp:  # headline-size graphs: narrow dtypes keep the fixture small
+            rec.update(qp_obstacle=po.astype(np.uint8), qp_edge=pe.astype(np.int32), qp_status=st,
+                       qp_iters=it.astype(np.int16), qp_delta=dl.astype(np.float32),
+                       sha_qp_pairs=digest(pe * 1_000_003 + po))
+        else:
+            rec.update(qp_obstacle=po, qp_edge=pe, qp_status=st, qp_iters=it, qp_delta=dl)
+    elif detail:
         codes, po, pe, st, it, dl = per_obstacle_detail(g, obstacles, cfg)
         rec.update(codes=codes, qp_obstacle=po, qp_edge=pe, qp_status=st, qp_iters=it, qp_delta=dl)
+    if band:
+        t0 = time.perf_counter()
+        rec["eps_band_1e-11"] = eps_band_count(oracle, g.vertices, spec.n, 1e-11)
+        rec["eps_band_1e-9"] = eps_band_count(oracle, g.vertices, spec.n, 1e-9)
+        print(f"{name}: eps band {rec['eps_band_1e-11']} / {rec['eps_band_1e-9']} in {time.perf_counter()-t0:.1f}s",
+              flush=True)
     if goals is not None:
         paths, costs = [], []
         for gl in goals:
@@ -154,13 +232,14 @@ def capture(name, N, spec, oracle, bounds, seed, include, obstacles, start, goal
           f"path={path} build={t_build:.2f}s cut={t_cut:.2f}s path={t_path*1e3:.1f}ms", flush=True)
 
 
-def scenario_case(name, s, *, full, detail, goals=None, relaxed=None, extra=None):
+def scenario_case(name, s, *, full, detail, goals=None, relaxed=None, extra=None, band=False):
     oracle = bg.build_oracle(s.spec, s.xd, s.u_bounds, s.tube)
     include = [s.start, s.goal]
     if extra is not None:
         include = list(extra) + include
     capture(name, s.graph_n, s.spec, oracle, s.sample_bounds, s.seed_graph, np.array(include),
-            rsim._inflated(s, 0.0), s.start, s.goal, full=full, detail=detail, goals=goals, relaxed_starts=relaxed)
+            rsim._inflated(s, 0.0), s.start, s.goal, full=full, detail=detail, goals=goals, relaxed_starts=relaxed,
+            band=band)
 
 
 def case_demo():
@@ -181,12 +260,12 @@ def case_cfg2():
     rng = np.random.default_rng(0)
     goals = np.zeros((100, 4))
     goals[:, :2] = rng.uniform(0.3, 4.7, size=(100, 2))
-    scenario_case("cfg2_rf2000", s, full=False, detail=False, goals=goals)
+    scenario_case("cfg2_rf2000", s, full=False, detail="record", goals=goals, band=True)
 
 
 def case_maze():
     s, grid = rsc.maze_scenario()
-    scenario_case("maze", s, full=False, detail=False, extra=grid)
+    scenario_case("maze", s, full=False, detail="record", extra=grid)
 
 
 def _hop_spec():
@@ -451,12 +530,156 @@ def case_m3():
             detail=True)
 
 
+def _clear_boxes(rng, count, lo, hi, start, goal):
+    """Random boxes (centre U(lo, hi)^2, side U(0.25, 0.7)^2), redrawn within 0.9 of start/goal
+    (the reference random field's rule, scenario.py:373-374)."""
+    out = []
+    while len(out) < count:
+        c = rng.uniform(lo, hi, 2)
+        w = rng.uniform(0.25, 0.7, 2)
+        if np.linalg.norm(c - start[:2]) < 0.9 or np.linalg.norm(c - goal[:2]) < 0.9:
+            continue
+        out.append(rsc._box_obstacle(c[0], c[1], w[0], w[1]).shape)
+    return out
+
+
+def case_cfg3():
+    """BASELINE cfg3 exactly as bench.py runs it (configs.hopping_deg5): gamma=3, 20,000 samples
+    + start/goal, 50 inflated boxes from default_rng(11).  Reference build ~4 min, cut ~20 min.
+    Digests for the big arrays, full alive/provenance, per-QP outcomes, path, eps-band counts."""
+    spec, xd, u, sample, tube = _hop_spec()
+    oracle = bg.build_oracle(spec, xd, u, tube)
+    start = np.array([0.4, 0.4, 0, 0, 0, 0.0])
+    goal = np.array([4.6, 4.6, 0, 0, 0, 0.0])
+    pos = tube.position_box(2)
+    obs = [rgeo.inflate(o, pos) for o in _clear_boxes(np.random.default_rng(11), 50, 0.4, 4.6, start, goal)]
+    capture("cfg3_hop20k", 20000, spec, oracle, sample, 1, np.array([start, goal]), obs, start, goal,
+            full=False, detail="record", band=True, compact_qp=True)
+
+
+def case_cfg5_10k():
+    """BASELINE cfg5 at 10k nodes (configs.scaling_sweep(10000)): 200 keep-in cells (20 x 10 grid,
+    10% overlap) on a 5 sqrt(5) map, 50 boxes from default_rng(101), composed from reference
+    objects as in case_regions4.  Candidate pairs per region are the vertices inside the region's
+    box: exact, because P_0 = x1 and P_p = x2 are control points and the region oracle keeps
+    them in the (eroded) region.  Then the reference's own cut_graph and find_path on it."""
+    N, seed = 10000, 1
+    spec = bg.BezierSpec(m=2, gamma=2, T=1.0)
+    side = 5.0 * float(np.sqrt(N / 2000.0))
+    xd, U, sample = rsc._standard_sets(side=side)
+    tube = rsim.design_tube(spec, (6.0, 5.0), 0.02)
+    base = bg.build_oracle(spec, xd, U, tube)
+    nx, ny, ov = 20, 10, 0.10
+    cw, ch = side / nx, side / ny
+    regions = []
+    for iy in range(ny):
+        for ix in range(nx):
+            lo = np.array([max(0.0, (ix - ov) * cw), max(0.0, (iy - ov) * ch)])
+            hi = np.array([min(side, (ix + 1 + ov) * cw), min(side, (iy + 1 + ov) * ch)])
+            regions.append(rgeo.Box(lo, hi))
+    per = N // len(regions)
+    t0 = time.perf_counter()
+    parts, oracles = [], []
+    for r, bx in enumerate(regions):
+        R = bx.to_polytope()
+        lifted = np.hstack([R.A, np.zeros((R.A.shape[0], spec.n - spec.m))])
+        Xr = rgeo.Polytope(np.vstack([xd.A, lifted]), np.concatenate([xd.b, R.b]))
+        oracles.append(bg.build_oracle(spec, Xr, U, tube))
+        bounds = rgeo.Box(np.concatenate([bx.lo, sample.lo[2:]]), np.concatenate([bx.hi, sample.hi[2:]]))
+        rng = np.random.default_rng([seed, r])  # graph.py:147-157 with the region's X_d
+        got, need = [], per
+        while need > 0:
+            cand = bounds.sample(rng, need)
+            acc = cand[Xr.contains_many(cand)]
+            if acc.size:
+                got.append(acc)
+                need -= acc.shape[0]
+        parts.append(np.vstack(got)[:per])
+    start = np.array([0.4, 0.4, 0.0, 0.0])
+    goal = np.array([side - 0.4, side - 0.4, 0.0, 0.0])
+    V = np.vstack(parts + [np.array([start, goal])])
+    Vn = V.shape[0]
+    keys = []
+    for bx, o in zip(regions, oracles):
+        inside = np.nonzero(np.all((V[:, :2] >= bx.lo - 1e-6) & (V[:, :2] <= bx.hi + 1e-6), axis=1))[0]
+        I, Jx = np.meshgrid(inside, inside, indexing="ij")
+        I, Jx = I.ravel(), Jx.ravel()
+        ok = (I != Jx) & bg.reachability.check_edges(o, V[I], V[Jx])
+        keys.append(I[ok].astype(np.int64) * Vn + Jx[ok])
+    keys = np.unique(np.concatenate(keys))
+    E = np.stack([keys // Vn, keys % Vn], axis=1).astype(np.int64)
+    D = bg.bezier.boundary_matrix(spec)
+    x1 = V[E[:, 0]].reshape(-1, spec.gamma, spec.m)
+    x2 = V[E[:, 1]].reshape(-1, spec.gamma, spec.m)
+    pts = np.einsum("pq,eqm->emp", D, np.concatenate([x1, x2], axis=1))  # graph.py:192-197
+    costs = np.linalg.norm(np.diff(pts, axis=2), axis=1).sum(axis=1)
+    t_build = time.perf_counter() - t0
+    g = rg.BezierGraph(spec=spec, oracle=base, vertices=V, edges=E, costs=costs, edge_points=pts, seed=seed,
+                       sample_bounds=sample)
+    print(f"cfg5_10k: V={Vn} E={E.shape[0]} built in {t_build:.1f}s", flush=True)
+    rng = np.random.default_rng(seed + 100)
+    obs = [rgeo.inflate(o, tube.position_box(2)) for o in _clear_boxes(rng, 50, 0.4, side - 0.4, start, goal)]
+    cfg = rg.CutConfig()
+    t0 = time.perf_counter()
+    mask, (po, pe, st, it, dl) = recorded_cut(g, obs, cfg)
+    t_cut = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    path = rg.find_path(g, mask, start, goal)
+    t_path = time.perf_counter() - t0
+    np.savez_compressed(
+        OUT / "cfg5_10k.npz", N=N, N_per=per, seed=seed, side=side, V=Vn, E=E.shape[0],
+        region_lo=np.stack([b.lo for b in regions]), region_hi=np.stack([b.hi for b in regions]),
+        F_base=base.F, G_base=base.G, start=start, goal=goal,
+        obs_n=np.array([o.num_rows for o in obs], np.int32), obs_A=np.concatenate([o.A for o in obs]),
+        obs_b=np.concatenate([o.b for o in obs]),
+        sha_vertices=digest(V), sha_edges=digest(E), sha_costs=digest(costs), sha_points=digest(pts),
+        vertices=V, row_counts=np.bincount(E[:, 0], minlength=Vn).astype(np.int64),
+        alive=mask.alive.copy(), provenance=np.array([PROV[p.value] for p in mask.provenance], np.int8),
+        counters=np.array([mask.pairs_total, mask.pairs_point_hit, mask.pairs_hyperplane, mask.pairs_qp,
+                           mask.qp_safe, mask.qp_unsafe], np.int64),
+        qp_obstacle=po, qp_edge=pe, qp_status=st, qp_iters=it, qp_delta=dl,
+        path=np.array(path if path is not None else [], np.int64), path_none=path is None,
+        path_cost=rg.path_cost(g, path) if path else 0.0, t_build=t_build, t_cut=t_cut, t_path=t_path,
+        env=json.dumps(env_info()))
+    print(f"cfg5_10k: alive={mask.alive_count} qp={mask.pairs_qp} path={path} cut={t_cut:.1f}s", flush=True)
+
+
+def case_m3g3():
+    """m = 3, gamma = 3 (n = 9): snapping's full-state norm takes numpy's pairwise order (n >= 8),
+    plus 3-D degree-5 edges through the whole path; several goals exercise the snap."""
+    spec = bg.BezierSpec(m=3, gamma=3, T=1.0)
+    side = 2.0
+    lo = np.concatenate([np.zeros(3), np.full(3, -1.5), np.full(3, -4.0)])
+    hi = np.concatenate([np.full(3, side), np.full(3, 1.5), np.full(3, 4.0)])
+    xd = rgeo.Box(lo, hi).to_polytope()
+    u = rgeo.Box(np.full(3, -30.0), np.full(3, 30.0))
+    tube = rsim.design_tube(spec, (6.0, 11.0, 6.0), 0.02)
+    oracle = bg.build_oracle(spec, xd, u, tube)
+    slo = np.concatenate([np.zeros(3), np.full(3, -0.3), np.full(3, -0.5)])
+    shi = np.concatenate([np.full(3, side), np.full(3, 0.3), np.full(3, 0.5)])
+    sample = rgeo.Box(slo, shi)
+    rng = np.random.default_rng(12)
+    obs = []
+    for _ in range(4):
+        c = rng.uniform(0.5, side - 0.5, 3)
+        sd = rng.uniform(0.2, 0.4, 3)
+        obs.append(rgeo.inflate(rgeo.Box(c - sd / 2, c + sd / 2).to_polytope(), tube.position_box(3)))
+    start = np.concatenate([np.full(3, 0.15), np.zeros(6)])
+    goal = np.concatenate([np.full(3, side - 0.15), np.zeros(6)])
+    goals = np.zeros((24, 9))
+    goals[:, :3] = rng.uniform(0.15, side - 0.15, (24, 3))
+    goals[:, 3:] = rng.uniform(-0.3, 0.3, (24, 6))
+    capture("m3g3_1500", 1500, spec, oracle, sample, 8, np.array([start, goal]), obs, start, goal, full=True,
+            detail=True, goals=goals)
+
+
 CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general, "knn": case_knn,
          "m3": case_m3, "m1": case_m1, "heur_general3": case_heur_general3,
          "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
                                                               ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
                                                               ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,
-         "cfg2": case_cfg2, "maze": case_maze}
+         "cfg2": case_cfg2, "maze": case_maze, "cfg3": case_cfg3, "cfg5_10k": case_cfg5_10k,
+         "m3g3": case_m3g3}
 
 if __name__ == "__main__":
     which = sys.argv[1:] or list(CASES)

@@ -120,3 +120,70 @@ def test_cfg3_path_matches_oracle_dijkstra(cfg3):
     assert path is not None and ref_path is not None
     assert path == list(ref_path)
     assert G.path_cost(g, path) == float(ref_dist)
+
+
+# ---------------------------------------------------------------- the live reference at full size
+def _golden_or_skip(name):
+    from tests.conftest import GOLDEN, load_golden
+
+    if not (GOLDEN / f"{name}.npz").exists():
+        pytest.skip(f"golden {name} not captured")
+    return load_golden(name)
+
+
+def test_cfg3_whole_graph_against_live_reference(cfg3):
+    """Every array of the headline run against the unmodified reference's own build_graph /
+    cut_graph / find_path on the same inputs (tests/golden/make_golden.py case_cfg3): the
+    whole 4.5 M-edge graph, all 226 M (edge, obstacle) outcomes, all 1.7 M QPs and the path."""
+    import json
+
+    from tests.helpers import assert_cut_parity, compare_cut, digest
+
+    gd = _golden_or_skip("cfg3_hop20k")
+    w, g, mask, path = cfg3
+    assert g.oracle.F.tobytes() == gd["F"].tobytes() and g.oracle.G.tobytes() == gd["G"].tobytes()
+    assert digest(g.vertices) == str(gd["sha_vertices"])
+    assert digest(g.edges) == str(gd["sha_edges"])
+    assert digest(g.costs) == str(gd["sha_costs"])
+    assert np.array_equal(np.diff(g.csr()[0]), gd["row_counts"])
+    assert digest(g.edge_points) == str(gd["sha_points"])
+    band = g.eps_band(1e-11)
+    print("cfg3 eps band", band)
+    assert band["band"] == int(gd["eps_band_1e-11"])
+    assert g.eps_band(1e-9)["band"] == int(gd["eps_band_1e-9"])
+    rep = compare_cut(mask, gd)
+    print("cfg3", json.dumps(rep))
+    assert_cut_parity(rep)
+    if rep["verdict_mismatch"] == 0:
+        assert path == list(gd["path"])
+        assert G.path_cost(g, path) == float(gd["path_cost"])
+
+
+def test_cfg5_10k_keepin_against_live_reference():
+    """BASELINE cfg5 at 10 k nodes (200 keep-in cells, 50 boxes): the device's region graph, cut
+    and path against the golden composed from the reference's build_oracle / check_edges /
+    cut_graph / find_path (make_golden.py case_cfg5_10k)."""
+    import json
+
+    from paper_2411_13507_b200 import regions as R
+    from tests.helpers import assert_cut_parity, compare_cut, digest
+
+    gd = _golden_or_skip("cfg5_10k")
+    ctx = nat.Context(0)
+    w = configs.scaling_sweep(10000)
+    lo, hi = R.region_boxes(w.extra["regions"])
+    assert lo.tobytes() == gd["region_lo"].tobytes() and hi.tobytes() == gd["region_hi"].tobytes()
+    g = R.build_region_graph(w.extra["per_region"], w.spec, w.oracle, w.extra["regions"], w.sample_bounds, w.seed,
+                             include=w.include, ctx=ctx)
+    assert g.vertices.tobytes() == gd["vertices"].tobytes()
+    assert digest(g.edges) == str(gd["sha_edges"])
+    assert digest(g.costs) == str(gd["sha_costs"])
+    assert digest(g.edge_points) == str(gd["sha_points"])
+    mask = G.cut_graph(g, w.obstacles)
+    rep = compare_cut(mask, gd)
+    print("cfg5_10k", json.dumps(rep))
+    assert_cut_parity(rep)
+    path = G.find_path(g, mask, w.start, w.goal)
+    if rep["verdict_mismatch"] == 0:
+        assert path == list(gd["path"])
+        assert G.path_cost(g, path) == float(gd["path_cost"])

@@ -12,7 +12,7 @@ import oracle
 from oracle.qp_ref import AdmmSettings
 from tests.helpers import digest, inputs_from_golden
 
-FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600", "m1_300"]
+FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600", "m1_300", "m3g3_1500"]
 
 
 @pytest.mark.parametrize("name", FULL)
@@ -145,3 +145,18 @@ def test_knn_prefilter_bitwise(golden):
     for k in g["ks"]:
         out = oracle.build_graph(int(g["N"]), spec, orc, bounds, int(g["seed"]), D=np.eye(4), k_nearest=int(k))
         assert np.array_equal(out["edges"], g[f"edges_k{k}"]), k
+
+
+def test_eps_band_oracle_matches_live_reference_count(golden):
+    """The oracle's eps-band count equals the one the golden script computed from the live
+    reference's own F, G and vertices (cfg2: no pair within 1e-9 of a threshold)."""
+    import oracle
+    from tests.helpers import inputs_from_golden
+
+    g = golden("cfg2_rf2000")
+    N, spec, orc, *_ = inputs_from_golden(g)
+    A1, A2 = oracle.project(g["vertices"], g["F"], spec.n)
+    for eps, key in ((1e-11, "eps_band_1e-11"), (1e-9, "eps_band_1e-9")):
+        band, plus, minus = oracle.eps_band(A1, A2, g["G"], eps)
+        assert band == int(g[key])
+        assert minus <= int(g["E"]) <= plus

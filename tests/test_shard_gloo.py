@@ -50,14 +50,26 @@ def _rank_main(rank, world, port, result_path):
         cnt = torch.tensor([cut[k] for k in ("pairs_total", "pairs_point_hit", "pairs_hyperplane", "pairs_qp",
                                              "qp_safe", "qp_unsafe")], dtype=torch.int64)
         dist.all_reduce(cnt)
+        # the root-only exchange bench.py uses: alive edges (+ provenance) gathered onto rank 0
+        keep = cut["alive"]
+        asz = shard.exchange_sizes(int(keep.sum()), dev)
+        root = [shard.gatherv_to_root(torch.from_numpy(np.ascontiguousarray(x[keep])), asz)
+                for x in (E[:, 0].astype(np.int32), E[:, 1].astype(np.int32), cost,
+                          cut["provenance"].astype(np.uint8))]
+        if rank != 0:
+            assert all(r is None for r in root)
         if rank == 0:
+            ga = g["alive"]
+            root_ok = (np.array_equal(np.stack([root[0].numpy(), root[1].numpy()], 1).astype(np.int64), g["edges"][ga])
+                       and root[2].numpy().tobytes() == g["costs"][ga].tobytes()
+                       and np.array_equal(root[3].numpy(), g["provenance"][ga]))
             src, dst, c, a, p = (t.numpy() for t in parts)
             ok = (np.array_equal(np.stack([src, dst], 1).astype(np.int64), g["edges"])
                   and c.tobytes() == g["costs"].tobytes()
                   and np.array_equal(a.astype(bool), g["alive"])
                   and np.array_equal(p, g["provenance"])
                   and cnt.tolist() == [int(x) for x in g["counters"]]
-                  and sum(sizes) == int(g["E"]))
+                  and sum(sizes) == int(g["E"]) and root_ok)
             with open(result_path, "w") as f:
                 f.write("ok" if ok else f"mismatch sizes={sizes}")
     finally:

@@ -34,10 +34,19 @@ def main(config="cfg2"):
     rows = shard.row_block(w.num_vertices, rank, world)
     g = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, w.include, ctx=ctx, rows=rows)
     m = G.cut_graph(g, w.obstacles)
-    m = shard.gather_to_all(g, m)
+    ga, ma = shard.gather_to_all(g, m)
+    gr, mr = shard.gather_to_root(g, m)
     ok = True
     if rank == 0:
-        path = G.find_path(g, m, w.start, w.goal)
+        path = G.find_path(ga, ma, w.start, w.goal)
+        path_root = G.find_path(gr, mr, w.start, w.goal)
+        local_path = None
+        try:  # the local row-block mask stays valid after the gathers
+            G.find_path(g, m, w.start, w.goal)
+            local_path = "ok"
+        except Exception as exc:  # noqa: BLE001
+            local_path = repr(exc)
+        g, m = ga, ma
         g1 = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, w.seed, w.include, ctx=ctx)
         m1 = G.cut_graph(g1, w.obstacles)
         p1 = G.find_path(g1, m1, w.start, w.goal)
@@ -49,6 +58,9 @@ def main(config="cfg2"):
             "counters": [m.pairs_total, m.pairs_point_hit, m.pairs_hyperplane, m.pairs_qp, m.qp_safe, m.qp_unsafe]
             == [m1.pairs_total, m1.pairs_point_hit, m1.pairs_hyperplane, m1.pairs_qp, m1.qp_safe, m1.qp_unsafe],
             "path": path == p1,
+            "path_root_alive_only": path_root == p1,
+            "root_edges_are_alive": gr.num_edges == int(m1.alive.sum()) and mr.alive.all(),
+            "local_mask_valid": local_path == "ok",
         }
         print(f"world {world}: E={g.num_edges} path={path} checks={checks}", flush=True)
         ok = all(checks.values())
