@@ -17,35 +17,12 @@
 
 #include "bzg_internal.cuh"
 #include "bzg_math.cuh"
+#include "k_cut_types.cuh"
 
 namespace bzg {
 
 namespace {
 
-
-struct DParams {
-  double D[64];
-};
-
-// Rows an obstacle may have on device (boxes have 2m; general polytopes up to this).
-constexpr int kObsRows = 8;
-
-// Per-obstacle record staged in shared memory.  Rows past `rows` are padding (A = 0,
-// b = 1e300): inert in every test and in the Cut-QP (k_qp_common.cuh).
-template <int M>
-struct ObsRec {
-  double A[kObsRows][M];   // normalised rows (geometry.py:135-137)
-  double b[kObsRows];
-  double b_eps[kObsRows];  // fl(b + eps_geo)   (graph.py:234)
-  double norm2[kObsRows];  // row norms of the normalised rows (Polytope._row_norms of O)
-  double lo[M], hi[M];     // Polytope.as_box bounds (geometry.py:155-185)
-  double canon;            // 1 when A == [I; -I] exactly (Box.to_polytope row order)
-  double act_hi[M];        // hi - 1e-6: a point below it cannot make face +k active
-  double act_lo[M];        // lo + 1e-6
-  double thin[M];          // 1 when hi - lo <= 1e-6 (both faces of axis k may be active)
-  double rows;             // constraint rows
-  double is_box;           // 1 when as_box() recovers a box (the closed-form branch applies)
-};
 
 // Branch 1 of _heuristic_batch (graph.py:236-239): einsum("cm,emj->ecj"), sequential from 0.
 template <int G, int M>
@@ -609,9 +586,6 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
 }  // namespace
 }  // namespace bzg
 
-#include "k_qp_common.cuh"
-#include "k_admm.cuh"
-#include "k_polish.cuh"
 #include "k_general.cuh"
 
 namespace bzg {
@@ -714,6 +688,7 @@ double polish_screen() {
   return s ? std::atof(s) : 1e-2;
 }
 
+
 template <typename F>
 void dispatch_cut(int G, int M, F&& f) {
 #define BZG_GM(g, m) \
@@ -804,92 +779,6 @@ std::vector<CertRec<M>> fill_cert(const std::vector<ObsRec<M>>& h, int n_obs, in
     wmax.push_back(all_canon && std::isfinite(w) ? w : -1.0);
   }
   return out;
-}
-
-// Batched Cut-QP over the work list pend[0 .. n_inst) (graph.py:320-337 / cut_qp 285-299):
-// ADMM, verdict selection, polish.  Fills mk->qp_status / qp_iters / qp_delta / n_polished
-// and d_safe (n_inst verdicts).  polish_mode: 0 none, 1 SOLVED, 2 SOLVED and MAX_ITER.
-template <int G, int M, int C, typename Trace>
-void qp_solve(Ctx* c, const Graph* g, const DParams& dp, const ObsRec<M>* d_obs, bool canon,
-              const unsigned long long* d_pend, long long n_inst, const bzg_cut_config* cfg, int polish_mode,
-              double screen, Mask* mk, DevBuf& d_safe, Trace&& trace) {
-  constexpr int NV = 2 * G + C, MCc = C + 2 * G + 1;
-  mk->qp_status.alloc(n_inst, c->stream);
-  mk->qp_iters.alloc(n_inst * sizeof(int), c->stream);
-  mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
-  DevBuf &d_x = c->ws[WS_QX], &d_zy = c->ws[WS_QZY], &d_list = c->ws[WS_QLIST];
-  DevBuf d_next;
-  d_x.alloc(n_inst * NV * sizeof(double), c->stream);
-  d_safe.alloc(n_inst, c->stream);
-  d_next.alloc(sizeof(unsigned long long), c->stream);
-  d_zy.alloc(n_inst * 2 * MCc * sizeof(double), c->stream);
-  d_list.alloc(n_inst * sizeof(int), c->stream);
-  BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
-  QpParams qp{};
-  qp.rho = cfg->qp_rho;
-  qp.rho_eq = cfg->qp_rho * 1e3;  // equality rows (qpsolver.py:100-103, 137)
-  qp.sigma = cfg->qp_sigma;
-  qp.alpha = cfg->qp_alpha;
-  qp.one_m_alpha = 1.0 - cfg->qp_alpha;
-  qp.eps_abs = cfg->qp_eps_abs;
-  qp.eps_rel = cfg->qp_eps_rel;
-  qp.eps_pinf = cfg->qp_eps_pinf;
-  qp.max_iter = cfg->qp_max_iter;
-  static const int batch_env = std::getenv("BZG_ADMM_BATCH") ? std::atoi(std::getenv("BZG_ADMM_BATCH")) : 0;
-  qp.batch = batch_env > 0 ? batch_env : kAdmmBatch;
-  // persistent grid: enough resident warps to cover the SMs several times
-  const long long blocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 16);
-  const bool rel = cfg->qp_eps_rel != 0.0, unit = cfg->qp_rho == 1.0;
-  auto admm = rel ? (unit ? k_qp_admm<G, M, C, true, true, false> : k_qp_admm<G, M, C, true, false, false>)
-                  : (unit ? k_qp_admm<G, M, C, false, true, false> : k_qp_admm<G, M, C, false, false, false>);
-  auto setup = k_qp_setup<G, M, C, false>;
-  size_t nconst = QpConsts<G, M, C, false>::N;
-  if constexpr (C == 2 * M)
-    if (canon && unit && !rel) {
-      admm = k_qp_admm<G, M, C, false, true, true>;
-      setup = k_qp_setup<G, M, C, true>;
-      nconst = QpConsts<G, M, C, true>::N;
-    }
-  DevBuf& d_consts = c->ws[WS_QCONST];
-  d_consts.alloc(n_inst * nconst * sizeof(double), c->stream);
-  trace("qp alloc");
-  launch(c, "k_qp_setup", setup, dim3(div_up(n_inst, 128)), dim3(128), 0, qp, dp, g->vertices.as<double>(),
-         g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, d_consts.as<double>());
-  launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, d_consts.as<double>(), n_inst,
-         d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
-         d_zy.as<double>());
-  trace("admm");
-  BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
-  launch(c, "k_qp_select", k_qp_select<G, M, C>, dim3(div_up(n_inst, 256)), dim3(256), 0, n_inst, polish_mode,
-         screen, cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(), mk->qp_delta.as<double>(),
-         d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
-  static const bool polish_lu = std::getenv("BZG_POLISH_IMPL") && std::string(std::getenv("BZG_POLISH_IMPL")) == "lu";
-  long long n_list = -1;  // known on the host only when it is read back (LU path, tracing)
-  if (polish_lu || c->trace_on) {
-    unsigned long long* hn = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long))) + 7;
-    BZG_CHECK_CUDA(cudaMemcpyAsync(hn, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-    n_list = (long long)*hn;
-    if (c->trace_on) std::fprintf(stderr, "[bzg cut] qp instances %lld, polished %lld\n", n_inst, n_list);
-  }
-  mk->n_polished = n_list;
-  if (polish_lu) {  // the shared-memory core LU (kept for A/B checks)
-    constexpr int NR = polish_dim<G, M, C>();
-    const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
-    ensure_dyn_smem((const void*)k_qp_polish<G, M, C>, psmem);
-    launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
-           dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
-           cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
-           mk->qp_status.as<int8_t>());
-  } else {
-    // persistent grid over the device-side list length (at most n_inst entries)
-    const long long pblocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 8);
-    launch(c, "k_qp_polish", k_qp_polish_reg<G, M, C>, dim3((unsigned)pblocks), dim3(128), 0, dp,
-           g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(),
-           d_next.as<unsigned long long>(), cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(),
-           mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), mk->qp_status.as<int8_t>());
-  }
-  trace("select+polish");
 }
 
 // Validates the obstacle list; returns the padded row count of a Cut-QP launch
@@ -1092,8 +981,11 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
     auto run_qp = [&](auto C_) {
       constexpr int Cc = decltype(C_)::value;
       DevBuf &d_safe = c->ws[WS_QSAFE];
-      qp_solve<Gc, Mc, Cc>(c, g, dp, d_recs, canon_all, d_pend.as<unsigned long long>(), n_inst, cfg,
-                           cfg->qp_polish ? 1 : 0, polish_screen(), mk, d_safe, trace);
+      QpJob job{g, {}, d_recs, canon_all, d_pend.as<unsigned long long>(), n_inst, cfg, cfg->qp_polish ? 1 : 0,
+                polish_screen(), mk, &d_safe};
+      for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
+      qp_solve(c, Gc, Mc, Cc, job);
+      trace("qp");
       launch(c, "k_qp_verdicts", k_qp_verdicts, dim3(div_up(n_inst, 256)), dim3(256), 0,
              d_pend.as<unsigned long long>(), n_inst, d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(),
              d_cnt.as<unsigned long long>());
@@ -1196,10 +1088,11 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
     mk.g = &g;
     mk.E = B;
     DevBuf &d_safe = c->ws[WS_QSAFE];
-    auto no_trace = [](const char*) {};
     dispatch_rows<Mc>(qp_rows, [&](auto C_) {
-      qp_solve<Gc, Mc, decltype(C_)::value>(c, &g, dp, d_obs.as<Rec>(), canon_all, d_items.as<unsigned long long>(), B,
-                                            cfg, cfg->qp_polish ? 2 : 0, 0.0, &mk, d_safe, no_trace);
+      QpJob job{&g, {}, d_obs.ptr, canon_all, d_items.as<unsigned long long>(), B, cfg, cfg->qp_polish ? 2 : 0, 0.0,
+                &mk, &d_safe};
+      for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
+      qp_solve(c, Gc, Mc, decltype(C_)::value, job);
     });
     if (code_out) BZG_CHECK_CUDA(cudaMemcpyAsync(code_out, d_safe.ptr, B, cudaMemcpyDeviceToHost, c->stream));
     if (delta_out)

@@ -1,0 +1,64 @@
+// Types shared by the cut translation units (k_cut.cu: screen + aggregation; k_qp_g*.cu:
+// the Cut-QP per gamma).  Kept in an anonymous namespace like the kernels that use them;
+// across translation units the obstacle records travel as raw device pointers.
+#pragma once
+
+#include "bzg_internal.cuh"
+
+namespace bzg {
+
+// Everything the batched Cut-QP of one cut needs (k_qp_impl.cuh qp_solve_t).
+struct QpJob {
+  const Graph* g;
+  double D[64];                       // boundary matrix (p+1) x 2*gamma, row-major
+  const void* d_obs;                  // ObsRec<M>[n_obs] on the device
+  bool canon;                         // every obstacle a canonical box (A = [I; -I])
+  const unsigned long long* d_pend;   // work list (e << 20 | o), n_inst entries
+  long long n_inst;
+  const bzg_cut_config* cfg;
+  int polish_mode;                    // 0 none, 1 SOLVED, 2 SOLVED and MAX_ITER
+  double screen;                      // polish screen (k_qp_select)
+  Mask* mk;                           // receives qp_status / qp_iters / qp_delta / n_polished
+  DevBuf* d_safe;                     // receives n_inst verdicts
+};
+// C = padded obstacle rows of the launch (2m or kObsRows); defined in k_qp_g<gamma>.cu
+void qp_solve_g1(Ctx* c, int M, int C, const QpJob& j);
+void qp_solve_g2(Ctx* c, int M, int C, const QpJob& j);
+void qp_solve_g3(Ctx* c, int M, int C, const QpJob& j);
+inline void qp_solve(Ctx* c, int G, int M, int C, const QpJob& j) {
+  switch (G) {
+    case 1: qp_solve_g1(c, M, C, j); return;
+    case 2: qp_solve_g2(c, M, C, j); return;
+    case 3: qp_solve_g3(c, M, C, j); return;
+    default: throw Error(BZG_EUNSUPPORTED, "device cut supports gamma in 1..3");
+  }
+}
+
+namespace {
+
+struct DParams {
+  double D[64];
+};
+
+// Rows an obstacle may have on device (boxes have 2m; general polytopes up to this).
+constexpr int kObsRows = 8;
+
+// Per-obstacle record staged in shared memory.  Rows past `rows` are padding (A = 0,
+// b = 1e300): inert in every test and in the Cut-QP (k_qp_common.cuh).
+template <int M>
+struct ObsRec {
+  double A[kObsRows][M];   // normalised rows (geometry.py:135-137)
+  double b[kObsRows];
+  double b_eps[kObsRows];  // fl(b + eps_geo)   (graph.py:234)
+  double norm2[kObsRows];  // row norms of the normalised rows (Polytope._row_norms of O)
+  double lo[M], hi[M];     // Polytope.as_box bounds (geometry.py:155-185)
+  double canon;            // 1 when A == [I; -I] exactly (Box.to_polytope row order)
+  double act_hi[M];        // hi - 1e-6: a point below it cannot make face +k active
+  double act_lo[M];        // lo + 1e-6
+  double thin[M];          // 1 when hi - lo <= 1e-6 (both faces of axis k may be active)
+  double rows;             // constraint rows
+  double is_box;           // 1 when as_box() recovers a box (the closed-form branch applies)
+};
+
+}  // namespace
+}  // namespace bzg

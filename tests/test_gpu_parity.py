@@ -292,3 +292,24 @@ def test_full_state_snapping_pairwise_norm(ctx, golden):
         p = G.find_path(gr, RefMask(), start, gl)
         assert (p or []) == list(flat[off:off + lens[k]]), k
         off += lens[k]
+
+
+@pytest.mark.parametrize("name", ["rf300_s5", "hop1500", "general60", "m3_600", "m1_300", "cfg2_rf2000"])
+def test_admm_two_lane_iterates_bitwise(ctx, golden, name, monkeypatch):
+    """k_qp_admm2 (two lanes per instance) reproduces k_qp_admm's iterates exactly: the same
+    status, iteration count and ||delta|| bits for every QP, hence the same mask.  Covers the
+    canonical box (m = 1, 2, 3 -- odd stored-row count at m = 3), general polygons (C = 8)
+    and gamma = 2, 3."""
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+    out = {}
+    for lanes in ("1", "2"):
+        monkeypatch.setenv("BZG_ADMM_LANES", lanes)
+        m = G.cut_graph(gr, obstacles)
+        out[lanes] = (m, m.qp_records())
+    (m1, r1), (m2, r2) = out["1"], out["2"]
+    assert r1["status"].size == r2["status"].size > 0
+    for k in ("edge", "obstacle", "status", "iterations"):
+        assert np.array_equal(r1[k], r2[k]), k
+    assert r1["delta"].tobytes() == r2["delta"].tobytes()
+    assert np.array_equal(m1.alive, m2.alive) and np.array_equal(m1.provenance_codes, m2.provenance_codes)
