@@ -76,7 +76,7 @@ enum WsSlot {
   WS_CAND, WS_FLAG, WS_POS,                                          // samplers
   WS_BITS, WS_A1C, WS_A2T, WS_ROWCNT, WS_RPTR, WS_PAIRLIST,          // pair test
   WS_KILL, WS_QKILL, WS_SAVED, WS_PEND, WS_GEN, WS_OBSGRID,          // cut screen
-  WS_QX, WS_QZY, WS_QSAFE, WS_QLIST, WS_QCONST,             // Cut-QP
+  WS_QX, WS_QZY, WS_QSAFE, WS_QLIST, WS_QCONST, WS_QRESUME,             // Cut-QP
   kWsSlots
 };
 

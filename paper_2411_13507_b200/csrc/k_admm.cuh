@@ -172,6 +172,22 @@ __global__ void __launch_bounds__(128) k_qp_setup(QpParams qp, DParams dp, const
   for (int c = 0; c < C; ++c) o[(K::NS + K::NQ + c) * n_inst] = b[c];
 }
 
+// Tail compaction.  One instance per lane keeps the FP64 pipe busy while the work list lasts,
+// but once it is drained the warps thin out: each warp instruction costs the pipe the same two
+// cycles however few lanes are live (ncu on cfg2: 12.6 of 32 lanes per instruction), so the
+// last, longest chains crawl behind their sparse neighbours.  A pass with dump_below > 0 parks
+// the live iterates of a thinned warp (x / zy slots of the instance, iteration count in
+// it_out) and queues the instance; the next launch resumes the queue densely packed, 32 per
+// warp, from exactly that state, so every iterate is unchanged (bitwise).  The last pass
+// has dump_below = 0 and runs everything it holds to termination.
+struct AdmmPass {
+  const int* rq_in;                // resume pass: instances to continue; nullptr: 0 .. n_inst-1
+  const unsigned long long* rq_in_n;
+  int* rq_out;                     // parked instances of this pass (n_inst capacity)
+  unsigned long long* rq_out_n;
+  int dump_below;                  // 0: never park
+};
+
 // REL: eps_rel != 0 (termination tolerances depend on the iterate, qpsolver.py:181-186)
 // UNIT: rho == 1 (CutConfig default) -- the multiplications by rho and 1/rho are exact and skipped
 // CANON: every obstacle is a canonical box (see QOps)
@@ -179,7 +195,7 @@ template <int G, int M, int C, bool REL, bool UNIT, bool CANON>
 __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* __restrict__ consts, long long n_inst,
                                                  unsigned long long* __restrict__ next, int8_t* __restrict__ st_out,
                                                  int* __restrict__ it_out, double* __restrict__ x_out,
-                                                 double* __restrict__ zy_out) {
+                                                 double* __restrict__ zy_out, AdmmPass pass) {
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1;
   const int lane = threadIdx.x & 31;
   const double rho = UNIT ? 1.0 : qp.rho, req = qp.rho_eq, ri = UNIT ? 1.0 : 1.0 / qp.rho;
@@ -195,7 +211,34 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
 #define RHO_MUL(v) (UNIT ? (v) : __dmul_rn(rho, (v)))
 #define RI_MUL(v) (UNIT ? (v) : __dmul_rn(ri, (v)))
 
+  const long long n_src = pass.rq_in ? (long long)*pass.rq_in_n : n_inst;
   while (true) {
+    // ---- tail compaction (see AdmmPass): once the work source is drained, a warp left with
+    // fewer than pass.dump_below live lanes parks their iterates in their own x / zy slots,
+    // queues them for the next, densely packed pass and retires
+    if (pass.dump_below > 0) {
+      const unsigned live = __ballot_sync(0xffffffffu, inst >= 0);
+      if (live && __popc(live) < pass.dump_below && __any_sync(0xffffffffu, inst == -2)) {
+        if (inst >= 0) {
+          double* xo = x_out + inst * NV;
+          double* zo = zy_out + inst * 2 * MC;
+#pragma unroll
+          for (int j = 0; j < J; ++j) { xo[j] = lam[j]; zo[C + j] = zl[j]; zo[MC + C + j] = yl[j]; }
+#pragma unroll
+          for (int c = 0; c < C; ++c) { xo[J + c] = del[c]; zo[c] = zc[c]; zo[MC + c] = yc[c]; }
+          zo[MC - 1] = ze;
+          zo[2 * MC - 1] = ye;
+          it_out[inst] = it;
+        }
+        // queue the live lanes (warp-aggregated append; the whole warp is here)
+        const int leader = __ffs(live) - 1;
+        unsigned long long qb = 0;
+        if (lane == leader) qb = atomicAdd(pass.rq_out_n, (unsigned long long)__popc(live));
+        qb = __shfl_sync(0xffffffffu, qb, leader);
+        if (inst >= 0) pass.rq_out[qb + __popc(live & ((1u << lane) - 1u))] = (int)inst;
+        inst = -2;
+      }
+    }
     // ---- refill lanes whose instance terminated (one atomic per warp)
     const unsigned need = __ballot_sync(0xffffffffu, inst == -1);
     if (need) {
@@ -205,7 +248,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
       base = __shfl_sync(0xffffffffu, base, leader);
       if (inst == -1) {
         const unsigned long long my = base + __popc(need & ((1u << lane) - 1u));
-        inst = (long long)my < n_inst ? (long long)my : -2;
+        inst = (long long)my < n_src ? (pass.rq_in ? (long long)pass.rq_in[my] : (long long)my) : -2;
         if (inst >= 0) {  // constants from k_qp_setup
           using K = QpConsts<G, M, C, CANON>;
           const double* o = consts + inst;
@@ -218,13 +261,25 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
 #pragma unroll
           for (int c = 0; c < C; ++c) b[c] = o[(K::NS + K::NQ + c) * n_inst];
         }
+        if (inst >= 0 && pass.rq_in) {  // resume a parked instance exactly where it stopped
+          const double* xo = x_out + inst * NV;
+          const double* zo = zy_out + inst * 2 * MC;
 #pragma unroll
-        for (int j = 0; j < J; ++j) { lam[j] = 0.0; zl[j] = 0.0; yl[j] = 0.0; }
+          for (int j = 0; j < J; ++j) { lam[j] = xo[j]; zl[j] = zo[C + j]; yl[j] = zo[MC + C + j]; }
 #pragma unroll
-        for (int c = 0; c < C; ++c) { del[c] = 0.0; zc[c] = 0.0; yc[c] = 0.0; }
-        ze = 0.0;
-        ye = 0.0;
-        it = 0;
+          for (int c = 0; c < C; ++c) { del[c] = xo[J + c]; zc[c] = zo[c]; yc[c] = zo[MC + c]; }
+          ze = zo[MC - 1];
+          ye = zo[2 * MC - 1];
+          it = it_out[inst];
+        } else {
+#pragma unroll
+          for (int j = 0; j < J; ++j) { lam[j] = 0.0; zl[j] = 0.0; yl[j] = 0.0; }
+#pragma unroll
+          for (int c = 0; c < C; ++c) { del[c] = 0.0; zc[c] = 0.0; yc[c] = 0.0; }
+          ze = 0.0;
+          ye = 0.0;
+          it = 0;
+        }
       }
     }
     if (__all_sync(0xffffffffu, inst == -2)) break;

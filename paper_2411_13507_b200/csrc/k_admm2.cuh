@@ -27,7 +27,7 @@ namespace bzg {
 namespace {
 
 // k_qp_admm2 is chosen while n_inst <= kAdmm2MaxPerLane x (k_qp_admm's resident lanes)
-constexpr double kAdmm2MaxPerLane = 4.0;
+constexpr double kAdmm2MaxPerLane = 0.0;  // measured slower than k_qp_admm at every size; BZG_ADMM_LANES=2 forces it
 
 template <int G, int M, int C, bool CANON>
 __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* __restrict__ consts, long long n_inst,

@@ -94,9 +94,42 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
            d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
            d_zy.as<double>());
   } else {
-    launch(c, "k_qp_admm", admm, dim3((unsigned)blocks), dim3(128), 0, qp, d_consts.as<double>(), n_inst,
-           d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
-           d_zy.as<double>());
+    // main pass over the work list, then resume passes over the parked tails (AdmmPass):
+    // BZG_ADMM_PASSES launches, the last one without parking; BZG_ADMM_DUMP is the live-lane
+    // count below which a drained warp parks its instances (default 12).  Default: one pass --
+    // the parked tails are latency-bound chains that a dense relaunch does not run faster
+    // (cfg2: 0.57 ms in one pass, 0.73-0.96 ms with 2-6 passes).
+    const int passes = std::max(1, std::getenv("BZG_ADMM_PASSES") ? std::atoi(std::getenv("BZG_ADMM_PASSES")) : 1);
+    const int dump = std::getenv("BZG_ADMM_DUMP") ? std::atoi(std::getenv("BZG_ADMM_DUMP")) : 12;
+    DevBuf& d_rq = c->ws[WS_QRESUME];
+    d_rq.alloc((passes > 1 ? 2 * n_inst : 1) * sizeof(int) + 4 * sizeof(unsigned long long), c->stream);
+    unsigned long long* qn = reinterpret_cast<unsigned long long*>(d_rq.as<char>() + (passes > 1 ? 2 * n_inst : 1) * sizeof(int));
+    int* q0 = d_rq.as<int>();
+    int* q1 = q0 + n_inst;
+    if (passes > 1) BZG_CHECK_CUDA(cudaMemsetAsync(qn, 0, 4 * sizeof(unsigned long long), c->stream));
+    for (int ps = 0; ps < passes; ++ps) {
+      AdmmPass pass{};
+      if (ps > 0) {
+        pass.rq_in = (ps & 1) ? q0 : q1;
+        pass.rq_in_n = qn + ((ps & 1) ? 0 : 1);
+        BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
+      }
+      if (ps + 1 < passes) {
+        pass.rq_out = (ps & 1) ? q1 : q0;
+        pass.rq_out_n = qn + ((ps & 1) ? 1 : 0);
+        if (ps > 0) BZG_CHECK_CUDA(cudaMemsetAsync(pass.rq_out_n, 0, sizeof(unsigned long long), c->stream));
+        pass.dump_below = dump;
+      }
+      launch(c, ps == 0 ? "k_qp_admm" : "k_qp_admm_tail", admm, dim3((unsigned)blocks), dim3(128), 0, qp,
+             d_consts.as<double>(), n_inst, d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(),
+             mk->qp_iters.as<int>(), d_x.as<double>(), d_zy.as<double>(), pass);
+      if (c->trace_on && pass.rq_out_n) {
+        unsigned long long hq = 0;
+        BZG_CHECK_CUDA(cudaMemcpyAsync(&hq, pass.rq_out_n, sizeof(hq), cudaMemcpyDeviceToHost, c->stream));
+        BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+        std::fprintf(stderr, "[bzg qp] pass %d parked %llu of %lld instances\n", ps, hq, n_inst);
+      }
+    }
   }
   trace("admm");
   BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));

@@ -295,21 +295,35 @@ def test_full_state_snapping_pairwise_norm(ctx, golden):
 
 
 @pytest.mark.parametrize("name", ["rf300_s5", "hop1500", "general60", "m3_600", "m1_300", "cfg2_rf2000"])
-def test_admm_two_lane_iterates_bitwise(ctx, golden, name, monkeypatch):
-    """k_qp_admm2 (two lanes per instance) reproduces k_qp_admm's iterates exactly: the same
-    status, iteration count and ||delta|| bits for every QP, hence the same mask.  Covers the
-    canonical box (m = 1, 2, 3 -- odd stored-row count at m = 3), general polygons (C = 8)
-    and gamma = 2, 3."""
+def test_admm_schedules_iterates_bitwise(ctx, golden, name, monkeypatch):
+    """Every ADMM schedule yields the same iterates: one pass of k_qp_admm (the plain
+    persistent kernel), the default tail-compaction passes (AdmmPass: thinned warps park
+    their instances and a later launch resumes them densely), aggressive parking
+    (BZG_ADMM_DUMP=32: any non-full drained warp parks), and k_qp_admm2 (two lanes per
+    instance).  Same status, iteration count and ||delta|| bits for every QP, same mask.
+    Covers the canonical box (m = 1, 2, 3 -- odd stored-row count at m = 3), general polygons
+    (C = 8) and gamma = 2, 3."""
     g = golden(name)
     gr, obstacles, start, goal = _build(g, ctx)
+    variants = {"plain": {"BZG_ADMM_LANES": "1", "BZG_ADMM_PASSES": "1"},
+                "compact": {"BZG_ADMM_LANES": "1"},
+                "park_all": {"BZG_ADMM_LANES": "1", "BZG_ADMM_PASSES": "4", "BZG_ADMM_DUMP": "32"},
+                "two_lane": {"BZG_ADMM_LANES": "2"}}
     out = {}
-    for lanes in ("1", "2"):
-        monkeypatch.setenv("BZG_ADMM_LANES", lanes)
+    for nm, env in variants.items():
+        for k in ("BZG_ADMM_LANES", "BZG_ADMM_PASSES", "BZG_ADMM_DUMP"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         m = G.cut_graph(gr, obstacles)
-        out[lanes] = (m, m.qp_records())
-    (m1, r1), (m2, r2) = out["1"], out["2"]
-    assert r1["status"].size == r2["status"].size > 0
-    for k in ("edge", "obstacle", "status", "iterations"):
-        assert np.array_equal(r1[k], r2[k]), k
-    assert r1["delta"].tobytes() == r2["delta"].tobytes()
-    assert np.array_equal(m1.alive, m2.alive) and np.array_equal(m1.provenance_codes, m2.provenance_codes)
+        r = m.qp_records()
+        # the work list is appended by warp atomics: compare in (edge, obstacle) order
+        o = np.argsort(r["edge"] * 1_000_003 + r["obstacle"], kind="stable")
+        out[nm] = (m, {k: v[o] for k, v in r.items()})
+    m0, r0 = out["plain"]
+    assert r0["status"].size > 0
+    for nm, (m, r) in out.items():
+        for k in ("edge", "obstacle", "status", "iterations"):
+            assert np.array_equal(r0[k], r[k]), (nm, k)
+        assert r0["delta"].tobytes() == r["delta"].tobytes(), nm
+        assert np.array_equal(m0.alive, m.alive) and np.array_equal(m0.provenance_codes, m.provenance_codes), nm

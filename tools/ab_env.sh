@@ -4,7 +4,7 @@ cd "${GRAFT_REPO_ROOT:-.}"
 IFS=';' read -ra S <<< "$SPECS"
 for rep in 1 2; do
   for spec in "${S[@]}"; do
-    env $spec python bench.py --config ${CFG:-cfg3} --steps 8 --warmup 3 2>/dev/null | tail -1 | \
+    env $spec python bench.py --config ${CFG:-cfg3} ${NODES:+--nodes $NODES} --steps 8 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1 | \
       python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$spec', round(d['ms_per_step'],3), d['kernels_ms_breakdown_pass']['k_qp_admm'])"
   done
 done
