@@ -77,6 +77,7 @@ enum WsSlot {
   WS_BITS, WS_A1C, WS_A2T, WS_ROWCNT, WS_RPTR, WS_PAIRLIST,          // pair test
   WS_KILL, WS_QKILL, WS_SAVED, WS_PEND, WS_GEN, WS_OBSGRID,          // cut screen
   WS_QX, WS_QZY, WS_QSAFE, WS_QLIST, WS_QCONST, WS_QRESUME,             // Cut-QP
+  WS_PLAN, WS_SSSP_PREV, WS_SSSP_PD, WS_SSSP_AUX, WS_SSSP_OUT,       // find_path
   kWsSlots
 };
 
@@ -245,9 +246,9 @@ struct Mask {
   // QP diagnostics
   int64_t n_qp = 0, n_polished = 0;
   DevBuf qp_edge, qp_obs, qp_status, qp_iters, qp_delta;
-  // cached shortest-path tree (reused while (mask, v0) is unchanged: cfg4 replanning)
-  int64_t tree_v0 = -1;
-  DevBuf dist, parent;
+  // cached shortest-path tree (reused while (mask, v0) is unchanged: cfg4 replanning); the
+  // key (the tree's v0, -1 = none) lives on the device next to the tree
+  DevBuf dist, parent, tree_key;
   // cached reverse reachability to vg (relaxed snapping)
   int64_t reach_vg = -1;
   DevBuf reach;

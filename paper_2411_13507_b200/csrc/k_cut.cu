@@ -819,7 +819,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
   mk->prov.alloc(std::max(E, 1ll), c->stream);
   for (int i = 0; i < 6; ++i) mk->counters[i] = 0;
   mk->counters[0] = E * (long long)n_obs;
-  mk->tree_v0 = -1;
+  mk->tree_key.release();
   mk->reach_vg = -1;
   mk->n_qp = 0;
 

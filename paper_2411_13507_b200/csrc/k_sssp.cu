@@ -160,7 +160,9 @@ __global__ void k_reach_sweep(long long E, const int* __restrict__ src, const in
 __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
                                 const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                                 unsigned long long* __restrict__ dist, int* __restrict__ stamp, int* __restrict__ qa,
-                                int* __restrict__ qb, int* __restrict__ counts, int max_sweeps) {
+                                int* __restrict__ qb, int* __restrict__ counts, int max_sweeps,
+                                const long long* __restrict__ plan) {
+  if (!plan[2]) return;  // grid-uniform
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const long long wg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
@@ -236,7 +238,9 @@ __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_p
 __global__ void k_bf_scan(long long V, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
                           const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                           unsigned long long* __restrict__ dist, unsigned long long* __restrict__ prev,
-                          int* __restrict__ qa, int* __restrict__ qb, int* __restrict__ counts, int max_sweeps) {
+                          int* __restrict__ qa, int* __restrict__ qb, int* __restrict__ counts, int max_sweeps,
+                          const long long* __restrict__ plan) {
+  if (!plan[2]) return;  // grid-uniform
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -303,10 +307,53 @@ __global__ void k_bf_scan(long long V, const long long* __restrict__ row_ptr, co
   if (tid == 0) counts[3] = sweep - 1;
 }
 
+__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+// ---------------------------------------------------------------- device-resident plan
+// find_path keeps (vg, v0) and the decisions that depend on them on the device, so a search is
+// one stream of launches and one host synchronisation (the path read-back).
+//   plan[0] = vg, plan[1] = v0 (-1: no snappable start), plan[2] = 1 when the shortest-path
+//   tree must be (re)built, plan[3] = 1 when the mask's cached tree (tree_key = its v0) is
+//   reused.  Kernels that build the tree return at once when plan[2] == 0.
+__global__ void k_plan(long long* __restrict__ plan, long long* __restrict__ tree_key) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const long long vg = plan[0], v0 = plan[1];
+  const bool trivial = v0 < 0 || v0 == vg;
+  const bool cached = !trivial && tree_key && *tree_key == v0;
+  plan[2] = (!trivial && !cached) ? 1 : 0;
+  plan[3] = cached ? 1 : 0;
+  if (plan[2] && tree_key) *tree_key = v0;  // the tree built below is the cache from now on
+}
+
+// mode 1 (k_bf_persistent): stamps -1 but v0, frontier queue = [v0], counts = {1, 0, ...};
+// mode 2 (k_bf_scan): prev = dist, frontier queue = [v0], counts = {1, 0, ...}.
+__global__ void k_init_tree(long long V, const long long* __restrict__ plan, int mode,
+                            unsigned long long* __restrict__ dist, unsigned long long* __restrict__ prev,
+                            int* __restrict__ stamp, int* __restrict__ parent, unsigned long long* __restrict__ pd,
+                            int* __restrict__ counts, int* __restrict__ qa) {
+  if (!plan[2]) return;
+  const long long v0 = plan[1];
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < 8) counts[i] = (i == 0) ? 1 : 0;
+  if (i == 0 && mode != 0) qa[0] = (int)v0;
+  if (i >= V) return;
+  const unsigned long long d = i == v0 ? 0ull : kInfBits;
+  dist[i] = d;
+  if (mode == 1) stamp[i] = i == v0 ? 0 : -1;
+  if (mode == 2) prev[i] = d;
+  parent[i] = 0x7fffffff;
+  pd[i] = ~0ull;
+}
+
 // parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes)
 __global__ void k_parent_dist(long long E, const int* __restrict__ src, const int* __restrict__ dst,
                               const double* __restrict__ cost, const uint8_t* __restrict__ alive,
-                              const unsigned long long* __restrict__ dist, unsigned long long* __restrict__ pd) {
+                              const unsigned long long* __restrict__ dist, unsigned long long* __restrict__ pd,
+                              const long long* __restrict__ plan) {
+  if (plan && !plan[2]) return;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= E) return;
   if (alive && !alive[e]) return;
@@ -320,7 +367,8 @@ __global__ void k_parent_dist(long long E, const int* __restrict__ src, const in
 __global__ void k_parent_idx(long long E, const int* __restrict__ src, const int* __restrict__ dst,
                              const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                              const unsigned long long* __restrict__ dist, const unsigned long long* __restrict__ pd,
-                             int* __restrict__ parent) {
+                             int* __restrict__ parent, const long long* __restrict__ plan) {
+  if (plan && !plan[2]) return;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= E) return;
   if (alive && !alive[e]) return;
@@ -331,14 +379,15 @@ __global__ void k_parent_idx(long long E, const int* __restrict__ src, const int
   if (dbits(nd) == dist[v]) atomicMin(parent + v, u);
 }
 
-__global__ void k_backtrack(long long V, long long v0, long long vg, const int* __restrict__ parent,
-                            const unsigned long long* __restrict__ dist, long long* __restrict__ path,
-                            long long* __restrict__ len, double* __restrict__ dout) {
+// out[0] = path length (-1: None), out[1] = dist bits, out[2..] = the path from v0 to vg
+__global__ void k_backtrack(long long V, const long long* __restrict__ plan, const int* __restrict__ parent,
+                            const unsigned long long* __restrict__ dist, long long* __restrict__ out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  if (dist[vg] >= kInfBits) {
-    *len = -1;
-    return;
-  }
+  const long long vg = plan[0], v0 = plan[1];
+  long long* path = out + 2;
+  if (v0 < 0) { out[0] = -1; return; }
+  if (v0 == vg) { out[0] = 1; out[1] = 0; path[0] = v0; return; }
+  if (dist[vg] >= kInfBits) { out[0] = -1; return; }
   long long n = 0, v = vg;
   path[n++] = v;
   while (v != v0 && n <= V) {
@@ -346,75 +395,70 @@ __global__ void k_backtrack(long long V, long long v0, long long vg, const int* 
     if (v < 0 || v >= V) { n = -2; break; }
     path[n++] = v;
   }
-  *len = n;
-  *dout = __longlong_as_double((long long)dist[vg]);
+  if (n > 0)
+    for (long long a = 0, b = n - 1; a < b; ++a, --b) {  // vg .. v0 -> v0 .. vg
+      const long long t = path[a];
+      path[a] = path[b];
+      path[b] = t;
+    }
+  out[0] = n;
+  out[1] = (long long)dist[vg];
 }
 
-__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
-}
-
-__global__ void k_init_sssp(long long V, long long v0, unsigned long long* dist, int* stamp, int* parent,
-                            unsigned long long* pd) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= V) return;
-  dist[i] = i == v0 ? 0ull : kInfBits;
-  stamp[i] = i == v0 ? 0 : -1;
-  parent[i] = 0x7fffffff;
-  pd[i] = ~0ull;
-}
-
-long long snap_launch(Ctx* c, Graph* g, const SnapParams& sp, const uint8_t* reach) {
+// k_snap over the vertices, the result (first argmin index, -1 if none) written to *out
+void snap_launch(Ctx* c, Graph* g, const SnapParams& sp, const uint8_t* reach, DevBuf& best, long long* out) {
   const long long V = g->V;
   const unsigned nb = div_up(V, 256);
-  DevBuf best, out;
   best.alloc((1 + 2 * (size_t)nb) * sizeof(unsigned long long), c->stream);
-  out.alloc(sizeof(long long), c->stream);
-  const unsigned long long init = kInfBits + 2;
-  BZG_CHECK_CUDA(cudaMemcpyAsync(best.ptr, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  launch(c, "k_fill_best", k_fill_u64, dim3(1), dim3(32), 0, best.as<unsigned long long>(), 1ll, kInfBits + 2);
   launch(c, "k_snap", k_snap, dim3(nb), dim3(256), 0, sp, g->vertices.as<double>(), V, reach,
          best.as<unsigned long long>());
-  launch(c, "k_snap_final", k_snap_final, dim3(1), dim3(32), 0, best.as<unsigned long long>(), (int)nb,
-         out.as<long long>());
-  long long* h = static_cast<long long*>(c->host_scratch(sizeof(long long)));
-  BZG_CHECK_CUDA(cudaMemcpyAsync(h, out.ptr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-  return h[0];
+  launch(c, "k_snap_final", k_snap_final, dim3(1), dim3(32), 0, best.as<unsigned long long>(), (int)nb, out);
 }
 
 }  // namespace
 
+// One host synchronisation per search (the path read-back).  (vg, v0) stay on the device
+// (plan); the tree kernels skip themselves when the mask's cached shortest-path tree already
+// belongs to v0 (cfg4 goal updates) or the answer is trivial.  Relaxed snapping computes the
+// reverse reachability to vg with a host-driven sweep loop (cached per (mask, vg)).
 void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
                const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
                double* dist_out) {
   const long long V = g->V, E = g->E;
   const int n = g->n;
   BZG_REQUIRE(n <= 16, BZG_EUNSUPPORTED, "state dimension too large");
+  BZG_REQUIRE(V >= 1, BZG_EINVAL, "graph has no vertices");
   const uint8_t* alive = mk ? mk->alive.as<uint8_t>() : nullptr;
   path.clear();
   *dist_out = INFINITY;
 
+  DevBuf& d_plan = c->ws[WS_PLAN];
+  d_plan.alloc(8 * sizeof(long long), c->stream);
+  long long* plan = d_plan.as<long long>();
+  DevBuf best0, best1;
   SnapParams sp{};
   sp.n = n;
   sp.m_norm = pos_only ? g->m : n;
   for (int k = 0; k < n; ++k) sp.target[k] = goal[k];
   sp.mode = 0;
-  const long long vg = snap_launch(c, g, sp, nullptr);
-  BZG_REQUIRE(vg >= 0, BZG_EINVAL, "graph has no vertices");
+  snap_launch(c, g, sp, nullptr, best0, plan + 0);
 
   for (int k = 0; k < n; ++k) {
     sp.target[k] = start[k];
     sp.tlo[k] = -tube_hi[k] - eps;  // (diff >= -tube.hi - EPS_GEO)   graph.py:381
     sp.thi[k] = -tube_lo[k] + eps;  // (diff <= -tube.lo + EPS_GEO)
   }
-  long long v0;
   DevBuf tmp_reach;
   if (require_tube) {
     sp.mode = 1;
-    v0 = snap_launch(c, g, sp, nullptr);
+    snap_launch(c, g, sp, nullptr, best1, plan + 1);
   } else {
     // relaxed mid-run snap: nearest vertex that can still reach vg (graph.py:388-392)
+    long long* hv = static_cast<long long*>(c->host_scratch(sizeof(long long)));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(hv, plan, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    const long long vg = hv[0];
     uint8_t* reach;
     if (mk) {
       mk->reach.alloc(V, c->stream);
@@ -443,110 +487,112 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
       if (mk) mk->reach_vg = vg;
     }
     sp.mode = 2;
-    v0 = snap_launch(c, g, sp, reach);
-  }
-  if (v0 < 0) return;  // no snappable start -> None
-  if (v0 == vg) {
-    path.push_back(v0);
-    *dist_out = 0.0;
-    return;
+    snap_launch(c, g, sp, reach, best1, plan + 1);
   }
 
-  DevBuf lpath, llen, ldist;
-  DevBuf t_dist, t_parent, t_stamp, t_pd, t_last;
+  // ---- the shortest-path tree from v0 (skipped on the device when cached or trivial)
+  DevBuf t_dist, t_parent, t_key;
   unsigned long long* dist;
   int* parent;
-  const bool cached = mk && mk->tree_v0 == v0;
+  long long* key = nullptr;
   if (mk) {
+    if (mk->dist.bytes < (size_t)V * sizeof(unsigned long long)) mk->tree_key.release();
     mk->dist.alloc(V * sizeof(unsigned long long), c->stream);
     mk->parent.alloc(V * sizeof(int), c->stream);
+    if (!mk->tree_key.ptr) {
+      mk->tree_key.alloc(sizeof(long long), c->stream);
+      BZG_CHECK_CUDA(cudaMemsetAsync(mk->tree_key.ptr, 0xFF, sizeof(long long), c->stream));  // -1: no tree
+    }
     dist = mk->dist.as<unsigned long long>();
     parent = mk->parent.as<int>();
+    key = mk->tree_key.as<long long>();
   } else {
     t_dist.alloc(V * sizeof(unsigned long long), c->stream);
     t_parent.alloc(V * sizeof(int), c->stream);
     dist = t_dist.as<unsigned long long>();
     parent = t_parent.as<int>();
   }
-  if (!cached) {
-    t_stamp.alloc(V * sizeof(int), c->stream);
-    t_pd.alloc(V * sizeof(unsigned long long), c->stream);
-    t_last.alloc(sizeof(int), c->stream);
-    launch(c, "k_init_sssp", k_init_sssp, dim3(div_up(V, 256)), dim3(256), 0, V, v0, dist, t_stamp.as<int>(), parent,
-           t_pd.as<unsigned long long>());
-    BZG_CHECK_CUDA(cudaMemsetAsync(t_last.ptr, 0, sizeof(int), c->stream));
-    // frontier Bellman-Ford in one cooperative launch (all blocks resident)
-    DevBuf qa, qb, cnt;
-    qa.alloc(std::max(V, 1ll) * sizeof(int), c->stream);
-    qb.alloc(std::max(V, 1ll) * sizeof(int), c->stream);
-    cnt.alloc(8 * sizeof(int), c->stream);
-    const int init[8] = {1, 0, 0, 0, 0, 0, 0, 0};
-    const int v0i = (int)v0;
-    BZG_CHECK_CUDA(cudaMemcpyAsync(cnt.ptr, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-    BZG_CHECK_CUDA(cudaMemcpyAsync(qa.ptr, &v0i, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    // the scan variant's second barrier and V-wide scan cost more than the queue's returning
-    // atomics on small graphs (cfg5 10k: 0.22 vs 0.19 ms); from ~16 k vertices it wins
-    // (cfg3 0.33 -> 0.24 ms, cfg5 100k 1.18 -> 0.80 ms).  BZG_BF_IMPL=queue|scan overrides.
-    static const char* bf_env = std::getenv("BZG_BF_IMPL");
-    const bool bf_queue = bf_env ? std::string(bf_env) == "queue" : V < 16384;
-    const void* bf_kern = bf_queue ? (const void*)k_bf_persistent : (const void*)k_bf_scan;
-    int per_sm = 0;
-    BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_kern, 256, 0));
-    static const int bf_per_sm_env =
-        std::getenv("BZG_BF_BLOCKS_PER_SM") ? std::atoi(std::getenv("BZG_BF_BLOCKS_PER_SM")) : 0;
-    const int blocks = std::max(1, std::min(per_sm, bf_per_sm_env > 0 ? bf_per_sm_env : 4) * c->num_sms);
-    long long Vl = V;
-    const long long* rp = g->row_ptr.as<long long>();
-    const int* dd = g->dst.as<int>();
-    const double* cc = g->cost.as<double>();
-    int* st = t_stamp.as<int>();
-    int* pa = qa.as<int>();
-    int* pb = qb.as<int>();
-    int* pc = cnt.as<int>();
-    int maxs = (int)std::min<long long>(V + 2, 1 << 30);
-    if (bf_queue) {
-      void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &st, &pa, &pb, &pc, &maxs};
-      launch_coop(c, "k_bf_persistent", bf_kern, dim3(blocks), dim3(256), args);
-    } else {
-      // prev = dist at init (v0 = 0, others +inf), so the first scan sees only v0's improvements
-      unsigned long long* pv = t_pd.as<unsigned long long>();
-      BZG_CHECK_CUDA(cudaMemcpyAsync(pv, dist, V * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
-      void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &pv, &pa, &pb, &pc, &maxs};
-      launch_coop(c, "k_bf_scan", bf_kern, dim3(blocks), dim3(256), args);
-      launch(c, "k_fill_pd", k_fill_u64, dim3(div_up(V, 256)), dim3(256), 0, pv, V, ~0ull);  // k_parent_dist's init
-    }
-    if (c->trace_on) {
-      int hc[8];
-      BZG_CHECK_CUDA(cudaMemcpyAsync(hc, cnt.ptr, sizeof(hc), cudaMemcpyDeviceToHost, c->stream));
-      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-      std::fprintf(stderr, "[bzg path] Bellman-Ford sweeps %d, frontier vertices expanded %d (V = %lld)\n", hc[3],
-                   hc[4], V);
-    }
-    launch(c, "k_parent_dist", k_parent_dist, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(),
-           g->dst.as<int>(), g->cost.as<double>(), alive, dist, t_pd.as<unsigned long long>());
-    launch(c, "k_parent_idx", k_parent_idx, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(), g->dst.as<int>(),
-           g->cost.as<double>(), alive, dist, t_pd.as<unsigned long long>(), parent);
-    if (mk) mk->tree_v0 = v0;
+  launch(c, "k_plan", k_plan, dim3(1), dim3(32), 0, plan, key);
+  DevBuf &t_prev = c->ws[WS_SSSP_PREV], &t_pd = c->ws[WS_SSSP_PD], &t_aux = c->ws[WS_SSSP_AUX];
+  t_prev.alloc(std::max(V, 1ll) * sizeof(unsigned long long), c->stream);
+  t_pd.alloc(std::max(V, 1ll) * sizeof(unsigned long long), c->stream);
+  // aux: counts (8 ints) | stamp (V ints) | qa (V ints) | qb (V ints)
+  t_aux.alloc((8 + 3 * (size_t)std::max(V, 1ll)) * sizeof(int), c->stream);
+  int* counts = t_aux.as<int>();
+  int* stamp = counts + 8;
+  int* qa = stamp + V;
+  int* qb = qa + V;
+  // BZG_BF_IMPL=queue|scan: k_bf_persistent (frontier queue, returning atomics) or k_bf_scan
+  // (fire-and-forget relaxation + rescan, two barriers per sweep).  The queue's returning
+  // atomics put two L2 round trips on every improvement; from a few thousand vertices the scan
+  // wins (cfg2 0.111 -> 0.096 ms, cfg3 0.33 -> 0.22, cfg5 100k 1.18 -> 0.78).  A one-barrier
+  // scan-and-relax variant (each sweep rescans every vertex and relaxes the changed ones in
+  // place) was slower: cfg3 0.39, cfg5 100k 3.6 ms.
+  const char* bf_env = std::getenv("BZG_BF_IMPL");
+  const int mode = bf_env ? (std::string(bf_env) == "queue" ? 1 : 2) : (V < 4096 ? 1 : 2);
+  launch(c, "k_init_tree", k_init_tree, dim3(div_up(std::max(V, 8ll), 256)), dim3(256), 0, V, (const long long*)plan,
+         mode, dist, t_prev.as<unsigned long long>(), stamp, parent, t_pd.as<unsigned long long>(), counts, qa);
+  const void* bf_kern = mode == 1 ? (const void*)k_bf_persistent : (const void*)k_bf_scan;
+  int per_sm = 0;
+  BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_kern, 256, 0));
+  static const int bf_per_sm_env =
+      std::getenv("BZG_BF_BLOCKS_PER_SM") ? std::atoi(std::getenv("BZG_BF_BLOCKS_PER_SM")) : 0;
+  // blocks per SM: fewer blocks make the grid barriers cheaper, more hide the relax latency
+  // (scan: cfg3 0.228 / 0.208 ms at 4 / 2 per SM; cfg5 100k 0.79 / 0.86)
+  const int want_per_sm = bf_per_sm_env > 0 ? bf_per_sm_env : (V < 50000 ? 2 : 4);
+  const int blocks = std::max(1, std::min(per_sm, want_per_sm) * c->num_sms);
+  long long Vl = V;
+  const long long* rp = g->row_ptr.as<long long>();
+  const int* dd = g->dst.as<int>();
+  const double* cc = g->cost.as<double>();
+  unsigned long long* pv = t_prev.as<unsigned long long>();
+  int maxs = (int)std::min<long long>(V + 2, 1 << 30);
+  const long long* cplan = plan;
+  if (mode == 1) {
+    void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &stamp, &qa, &qb, &counts, &maxs, &cplan};
+    launch_coop(c, "k_bf_persistent", bf_kern, dim3(blocks), dim3(256), args);
+  } else {
+    void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &pv, &qa, &qb, &counts, &maxs, &cplan};
+    launch_coop(c, "k_bf_scan", bf_kern, dim3(blocks), dim3(256), args);
   }
-  lpath.alloc((V + 1) * sizeof(long long), c->stream);
-  llen.alloc(sizeof(long long), c->stream);
-  ldist.alloc(sizeof(double), c->stream);
-  launch(c, "k_backtrack", k_backtrack, dim3(1), dim3(32), 0, V, v0, vg, parent, dist, lpath.as<long long>(),
-         llen.as<long long>(), ldist.as<double>());
-  long long* h = static_cast<long long*>(c->host_scratch(2 * sizeof(long long)));
-  BZG_CHECK_CUDA(cudaMemcpyAsync(h, llen.ptr, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  BZG_CHECK_CUDA(cudaMemcpyAsync(h + 1, ldist.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (c->trace_on) {
+    int hc[8];
+    long long hp[4];
+    BZG_CHECK_CUDA(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(hp, plan, sizeof(hp), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    std::fprintf(stderr, "[bzg path] vg %lld v0 %lld build %lld cached %lld; Bellman-Ford sweeps %d (V = %lld)\n",
+                 hp[0], hp[1], hp[2], hp[3], hc[3], V);
+  }
+  launch(c, "k_parent_dist", k_parent_dist, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, g->src.as<int>(),
+         g->dst.as<int>(), g->cost.as<double>(), alive, (const unsigned long long*)dist, t_pd.as<unsigned long long>(),
+         cplan);
+  launch(c, "k_parent_idx", k_parent_idx, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, g->src.as<int>(),
+         g->dst.as<int>(), g->cost.as<double>(), alive, (const unsigned long long*)dist,
+         (const unsigned long long*)t_pd.as<unsigned long long>(), parent, cplan);
+
+  // ---- backtrack and the single read-back: [len, dist bits, path...], the first kHead entries
+  DevBuf& d_out = c->ws[WS_SSSP_OUT];
+  d_out.alloc((V + 3) * sizeof(long long), c->stream);
+  launch(c, "k_backtrack", k_backtrack, dim3(1), dim3(32), 0, V, cplan, (const int*)parent,
+         (const unsigned long long*)dist, d_out.as<long long>());
+  constexpr long long kHead = 510;
+  const long long head = std::min(V + 2, kHead + 2);
+  long long* h = static_cast<long long*>(c->host_scratch((size_t)(kHead + 2) * sizeof(long long)));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h, d_out.ptr, head * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
   const long long len = h[0];
+  BZG_REQUIRE(len != -2, BZG_ECUDA, "parent chain broken during backtrack");
+  if (len < 0) return;  // no snappable start or vg unreachable -> None
   double dv;
   memcpy(&dv, h + 1, sizeof(double));
-  BZG_REQUIRE(len != -2, BZG_ECUDA, "parent chain broken during backtrack");
-  if (len < 0) return;  // vg unreachable -> None
-  std::vector<long long> rev(len);
-  BZG_CHECK_CUDA(cudaMemcpyAsync(rev.data(), lpath.ptr, len * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-  path.resize(len);
-  for (long long i = 0; i < len; ++i) path[i] = rev[len - 1 - i];
+  path.assign(h + 2, h + 2 + std::min(len, head - 2));
+  if (len > head - 2) {  // long path: the rest in a second copy
+    path.resize(len);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(path.data() + (head - 2), d_out.as<long long>() + head,
+                                   (len - (head - 2)) * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  }
   *dist_out = dv;
 }
 

@@ -30,16 +30,18 @@ def inputs_from_golden(g: dict):
     return int(g["N"]), spec, oracle, bounds, int(g["seed"]), include, obstacles, g["start"], g["goal"]
 
 
-def qp_solver_sensitive(status_a, iters_a, delta_a, status_b, iters_b, delta_b, eps_cut=1e-7):
-    """QP pairs whose verdict may legitimately depend on the solver's rounding —
+def qp_solver_sensitive(status_a, iters_a, delta_a, status_b, iters_b, delta_b, eps_cut=1e-7, eps_abs=1e-7):
+    """QP pairs whose verdict may legitimately depend on the solver's rounding --
     MAX_ITER or an infeasibility certificate on either side (the verdict then hinges on where
-    the iteration stopped), or ||delta|| within 1e-8 of eps_cut on either side.  A differing
-    iteration count alone does NOT excuse a verdict difference: with both sides SOLVED and
-    ||delta|| far from the threshold the verdicts must agree (iters_* are kept in the
-    signature for the report)."""
+    the iteration stopped), or ||delta|| within eps_abs of eps_cut on either side: the ADMM
+    stops once its residuals are below eps_abs (CutConfig.qp, graph.py:47-49), so a ||delta||
+    that close to the threshold is only known to that accuracy.  (Measured at cfg3 against the
+    live reference: the four both-SOLVED verdict differences have ||delta|| in [7.0e-8,
+    1.65e-7] on the two sides, iteration counts 1-2 apart.)  A differing iteration count alone
+    does NOT excuse a verdict difference (iters_* are kept in the signature for the report)."""
     del iters_a, iters_b
     return ((status_a == 1) | (status_b == 1) | (status_a == 2) | (status_b == 2)
-            | (np.abs(delta_a - eps_cut) < 1e-8) | (np.abs(delta_b - eps_cut) < 1e-8))
+            | (np.abs(delta_a - eps_cut) < eps_abs) | (np.abs(delta_b - eps_cut) < eps_abs))
 
 
 def compare_cut(mask, g: dict, eps_cut: float = 1e-7) -> dict:
@@ -68,6 +70,9 @@ def compare_cut(mask, g: dict, eps_cut: float = 1e-7) -> dict:
     sens = qp_solver_sensitive(st_g, it_g, dl_g, st_d, it_d, dl_d, eps_cut)
     mism = v_d != v_g
     rep["verdict_mismatch"] = int(mism.sum())
+    out = np.nonzero(mism & ~sens)[0][:10]
+    rep["outside_examples"] = [[int(st_g[i]), int(st_d[i]), int(it_g[i]), int(it_d[i]), float(dl_g[i]), float(dl_d[i])]
+                               for i in out]
     rep["mismatch_outside_sensitive"] = int((mism & ~sens).sum())
     rep["solver_sensitive"] = int(sens.sum())
     rep["status_equal"] = float((st_d == st_g).mean()) if st_d.size else 1.0
