@@ -76,7 +76,7 @@ enum WsSlot {
   WS_CAND, WS_FLAG, WS_POS,                                          // samplers
   WS_BITS, WS_A1C, WS_A2T, WS_ROWCNT, WS_RPTR, WS_PAIRLIST,          // pair test
   WS_KILL, WS_QKILL, WS_SAVED, WS_PEND, WS_GEN, WS_OBSGRID,          // cut screen
-  WS_QX, WS_QZY, WS_QSAFE, WS_QLIST, WS_QCONST, WS_QRESUME,             // Cut-QP
+  WS_QX, WS_QZY, WS_QSAFE, WS_QLIST, WS_QCONST, WS_QRESUME, WS_QSTATUS, WS_QITERS, WS_QDELTA,             // Cut-QP
   WS_PLAN, WS_SSSP_PREV, WS_SSSP_PD, WS_SSSP_AUX, WS_SSSP_OUT,       // find_path
   kWsSlots
 };
@@ -121,6 +121,10 @@ struct Ctx {
   int grid_nobs = -1;
   double grid_key[4] = {0, 0, 0, 0};
   bool grid_sparse = false;
+  long long qp_hint = 0;   // QP instances of the last cut: sizes the next cut's QP buffers
+  double sample_est = 1.0; // acceptance rate of the last sampler run (sizes a single round)
+  int* sample_check = nullptr;  // pending single-round sampler count (device), need, candidates
+  long long sample_need = 0, sample_count = 0;
   void* pinned = nullptr;  // small pinned host staging area
   size_t pinned_bytes = 0;
 
@@ -255,12 +259,14 @@ struct Mask {
 };
 
 // Kernel-family entry points (defined in the k_*.cu translation units).
-void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices);
+// single_round: one round sized from Ctx::sample_est, its acceptance checked by build_pairs
+void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool single_round = false);
 void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
                     const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out);
 // th_shift moves every oracle threshold (eps-band counting); count_only != nullptr returns the
-// edge count there and leaves g's CSR untouched
-void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift = 0.0, long long* count_only = nullptr);
+// edge count there and leaves g's CSR untouched.  Returns false (CSR untouched) when the
+// preceding single-round sampler (Ctx::sample_check) accepted fewer than N states.
+bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift = 0.0, long long* count_only = nullptr);
 void materialize_points(Ctx* c, Graph* g);
 void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, const double* cost, bool on_device);
 void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, double eps, int64_t k,

@@ -165,6 +165,7 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
     BZG_REQUIRE(d->F && d->G && d->D, BZG_EINVAL, "oracle F, G and boundary matrix D are required");
     BZG_REQUIRE(d->n_include >= 0 && (d->n_include == 0 || d->include), BZG_EINVAL, "include rows missing");
     const int n = d->m * d->gamma;
+    ctx->sample_check = nullptr;
     ctx->trace("build: enter");
     g = new bzg_graph();
     g->ctx = ctx;
@@ -185,13 +186,17 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
                                      cudaMemcpyHostToDevice, ctx->stream));
     } else {
       BZG_REQUIRE(d->sample_lo && d->sample_hi && d->xd_A && d->xd_b, BZG_EINVAL, "sampler inputs missing");
-      sample_states(ctx, d, g->vertices.as<double>());
+      sample_states(ctx, d, g->vertices.as<double>(), /*single_round=*/true);
     }
     if (d->n_include > 0)
       BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)d->N * n, d->include,
                                      (size_t)d->n_include * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     ctx->trace("build: vertices");
-    build_pairs(ctx, d, g);
+    if (!build_pairs(ctx, d, g)) {  // the one sampler round fell short: checked rounds, then again
+      ctx->trace("build: resample");
+      sample_states(ctx, d, g->vertices.as<double>());
+      build_pairs(ctx, d, g);
+    }
     ctx->trace("build: pairs+csr");
   });
   if (rc == BZG_OK) {
@@ -209,6 +214,7 @@ int bzg_graph_eps_band(bzg_graph* g, const bzg_build_desc* d, double eps, int64_
     BZG_REQUIRE(d->m == g->m && d->gamma == g->gamma && d->N + d->n_include == g->V, BZG_EINVAL,
                 "descriptor does not describe this graph");
     set_device(g->ctx);
+    g->ctx->sample_check = nullptr;
     long long plus = 0, minus = 0;
     build_pairs(g->ctx, d, g, eps, &plus);
     build_pairs(g->ctx, d, g, -eps, &minus);

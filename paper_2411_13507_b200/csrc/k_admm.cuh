@@ -152,24 +152,28 @@ __global__ void __launch_bounds__(128) k_qp_setup(QpParams qp, DParams dp, const
                                                   const int* __restrict__ src, const int* __restrict__ dst,
                                                   const ObsRec<M>* __restrict__ obs,
                                                   const unsigned long long* __restrict__ pend, long long n_inst,
+                                                  const unsigned long long* __restrict__ d_n,
                                                   double* __restrict__ consts) {
   using K = QpConsts<G, M, C, CANON>;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= n_inst) return;
+  const long long n = dev_count(n_inst, d_n);
   const double rho = qp.rho, req = qp.rho_eq, sig = qp.sigma;
   const double kdd = 2.0 + sig + rho, ikdd = 1.0 / kdd;
-  double Qf[C][2 * G], b[C], Si[K::NS];
-  load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[t], Qf, b);
-  admm_setup<G, M, C>(Qf, Si, rho, req, sig, ikdd);
-  double* o = consts + t;  // field-major: field k of instance t at consts[k * n_inst + t] (coalesced)
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    double Qf[C][2 * G], b[C], Si[K::NS];
+    load_instance<G, M, C>(dp, Vx, src, dst, obs, pend[t], Qf, b);
+    admm_setup<G, M, C>(Qf, Si, rho, req, sig, ikdd);
+    // field-major: field k of instance t at consts[k * n_inst + t] (coalesced); n_inst is the
+    // capacity of the work list, the stride every reader uses
+    double* o = consts + t;
 #pragma unroll
-  for (int k = 0; k < K::NS; ++k) o[k * n_inst] = Si[k];
+    for (int k = 0; k < K::NS; ++k) o[k * n_inst] = Si[k];
 #pragma unroll
-  for (int r = 0; r < K::R; ++r)
+    for (int r = 0; r < K::R; ++r)
 #pragma unroll
-    for (int j = 0; j < K::J; ++j) o[(K::NS + r * K::J + j) * n_inst] = Qf[r][j];
+      for (int j = 0; j < K::J; ++j) o[(K::NS + r * K::J + j) * n_inst] = Qf[r][j];
 #pragma unroll
-  for (int c = 0; c < C; ++c) o[(K::NS + K::NQ + c) * n_inst] = b[c];
+    for (int c = 0; c < C; ++c) o[(K::NS + K::NQ + c) * n_inst] = b[c];
+  }
 }
 
 // Tail compaction.  One instance per lane keeps the FP64 pipe busy while the work list lasts,
@@ -195,7 +199,8 @@ template <int G, int M, int C, bool REL, bool UNIT, bool CANON>
 __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* __restrict__ consts, long long n_inst,
                                                  unsigned long long* __restrict__ next, int8_t* __restrict__ st_out,
                                                  int* __restrict__ it_out, double* __restrict__ x_out,
-                                                 double* __restrict__ zy_out, AdmmPass pass) {
+                                                 double* __restrict__ zy_out, AdmmPass pass,
+                                                 const unsigned long long* __restrict__ d_n) {
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1;
   const int lane = threadIdx.x & 31;
   const double rho = UNIT ? 1.0 : qp.rho, req = qp.rho_eq, ri = UNIT ? 1.0 : 1.0 / qp.rho;
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
 #define RHO_MUL(v) (UNIT ? (v) : __dmul_rn(rho, (v)))
 #define RI_MUL(v) (UNIT ? (v) : __dmul_rn(ri, (v)))
 
-  const long long n_src = pass.rq_in ? (long long)*pass.rq_in_n : n_inst;
+  const long long n_src = pass.rq_in ? (long long)*pass.rq_in_n : dev_count(n_inst, d_n);
   while (true) {
     // ---- tail compaction (see AdmmPass): once the work source is drained, a warp left with
     // fewer than pass.dump_below live lanes parks their iterates in their own x / zy slots,

@@ -33,7 +33,8 @@ template <int G, int M, int C, bool CANON>
 __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* __restrict__ consts, long long n_inst,
                                                   unsigned long long* __restrict__ next, int8_t* __restrict__ st_out,
                                                   int* __restrict__ it_out, double* __restrict__ x_out,
-                                                  double* __restrict__ zy_out) {
+                                                  double* __restrict__ zy_out,
+                                                  const unsigned long long* __restrict__ d_n) {
   using K = QpConsts<G, M, C, CANON>;
   constexpr int J = 2 * G, JH = G, NV = J + C, MC = C + J + 1;
   constexpr int R = K::R;          // stored Q rows
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
 #define RELAX(a, b) __fma_rn(al, (a), __dmul_rn(oma, (b)))
 #define XCH(v) __shfl_xor_sync(FULL, (v), 1)
 
+  const long long n_lim = dev_count(n_inst, d_n);
   long long inst = -1;  // pair-uniform: -1 needs work, -2 exhausted
   int it = 0;
   double si[JH][J];              // S^-1 rows of the owned lambda rows
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
       base = __shfl_sync(FULL, base, leader);
       if (inst == -1) {
         const unsigned long long my = base + (__popc(need & ((1u << pair0) - 1u)) >> 1);
-        inst = (long long)my < n_inst ? (long long)my : -2;
+        inst = (long long)my < n_lim ? (long long)my : -2;
         if (inst >= 0) {
           const double* o = consts + inst;
 #pragma unroll

@@ -840,7 +840,7 @@ void exclusive_scan_i(Ctx* c, const int* in, int* out, long long count) {
 }  // namespace
 
 // ------------------------------------------------------------------ host side
-void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices) {
+void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool single_round) {
   const int n = d->m * d->gamma;
   BZG_REQUIRE(n <= kMaxN, BZG_EUNSUPPORTED, "state dimension too large for the device sampler");
   BZG_REQUIRE(d->xd_rows >= 1 && d->xd_rows <= kMaxRows, BZG_EUNSUPPORTED, "state polytope row count unsupported");
@@ -856,12 +856,14 @@ void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices) {
     sp.b_eps[r] = d->xd_b[r] + d->eps_geo;
   }
   long long need = d->N, row0 = 0, got = 0;
-  double est = 1.0;
+  // acceptance estimate: the last build's on this context (single_round: its one round is sized
+  // from it and checked later, at build_pairs' read-back, instead of synchronising here)
+  double est = single_round ? c->sample_est : 1.0;
   DevBuf &cand = c->ws[WS_CAND], &flag = c->ws[WS_FLAG], &pos = c->ws[WS_POS];
   int* h = static_cast<int*>(c->host_scratch(2 * sizeof(int)));
   for (int round = 0; need > 0; ++round) {
     BZG_REQUIRE(round < 10000, BZG_EINVAL, "sampler made no progress: state polytope misses the sampling box");
-    long long count = (long long)std::ceil((double)need / std::max(est, 1e-3) * 1.05) + 256;
+    long long count = (long long)std::ceil((double)need / std::max(est, 1e-3) * (single_round ? 1.10 : 1.05)) + 256;
     count = std::min<long long>(count, 1ll << 26);
     cand.alloc(count * n * sizeof(double), c->stream);
     flag.alloc((count + 1) * sizeof(int), c->stream);
@@ -874,6 +876,12 @@ void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices) {
     exclusive_scan_i(c, flag.as<int>(), pos.as<int>(), count + 1);
     launch(c, "k_sample_scatter", k_sample_scatter, dim3(div_up(count, 256)), dim3(256), 0, cand.as<double>(),
            flag.as<int>(), pos.as<int>(), count, n, need, d_vertices + got * n);
+    if (single_round) {  // accepted count checked by build_pairs (Ctx::sample_check)
+      c->sample_check = pos.as<int>() + count;
+      c->sample_need = need;
+      c->sample_count = count;
+      return;
+    }
     BZG_CHECK_CUDA(cudaMemcpyAsync(h, pos.as<int>() + count, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
     const long long acc = h[0];
@@ -886,6 +894,7 @@ void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices) {
     row0 += count;
     est = std::max(1e-3, (double)acc / (double)count);
   }
+  c->sample_est = est;
 }
 
 void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
@@ -964,7 +973,7 @@ void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg,
   }
 }
 
-void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, long long* count_only) {
+bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, long long* count_only) {
   const int n = g->n;
   const int nF = d->n_F;
   const long long V = g->V;
@@ -1212,13 +1221,24 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   }
   c->trace("pairs: tiles(+knn)");
   exclusive_scan_ll(c, rowcnt.as<unsigned long long>(), rptr.as<long long>(), rows + 1);
-  long long* h = static_cast<long long*>(c->host_scratch(sizeof(long long)));
+  long long* h = static_cast<long long*>(c->host_scratch(2 * sizeof(long long)));
   BZG_CHECK_CUDA(cudaMemcpyAsync(h, rptr.as<long long>() + rows, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  int* sampled = c->sample_check;
+  if (sampled) {
+    h[1] = 0;
+    BZG_CHECK_CUDA(cudaMemcpyAsync(h + 1, sampled, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  }
   BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  if (sampled) {  // the single sampler round of this build (sample_states): enough acceptances?
+    c->sample_check = nullptr;
+    const long long acc = (long long)(int)h[1];
+    c->sample_est = std::max(1e-3, (double)acc / (double)c->sample_count);
+    if (acc < c->sample_need) return false;  // the caller resamples with the checked loop
+  }
   const long long E = h[0];
   if (count_only) {
     *count_only = E;
-    return;
+    return true;
   }
   BZG_REQUIRE(E < (1ll << 31), BZG_EUNSUPPORTED, "edge count exceeds the int32 CSR index range");
   g->E = E;
@@ -1239,6 +1259,7 @@ void build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   }
   launch(c, "k_row_ptr_global", k_row_ptr_global, dim3(div_up(V + 1, 256)), dim3(256), 0, rptr.as<long long>(),
          V, r0, r1, g->row_ptr.as<long long>());
+  return true;
 }
 
 void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, const double* cost, bool on_device) {

@@ -600,53 +600,60 @@ constexpr double kEpsGeo = 1e-9;  // geometry.EPS_GEO (geometry.py:14), closest_
 template <int G, int M>
 __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const int* __restrict__ src,
                               const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
-                              const unsigned long long* __restrict__ gen, long long n, double margin,
+                              const unsigned long long* __restrict__ gen, long long n_cap,
+                              const unsigned long long* __restrict__ d_n, double margin,
                               int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                               unsigned long long* __restrict__ n_pend, unsigned long long cap,
                               unsigned long long* __restrict__ pend, int8_t* __restrict__ code_out) {
   constexpr int N = G * M;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  int code = -2;
-  unsigned long long item = 0;
-  if (t < n) {
-    item = gen[t];
-    const long long e = (long long)(item >> 20);
-    const int oi = (int)(item & 0xFFFFF);
-    double xi[N], xj[N], P[M][2 * G];
-    const long long a = src[e], c = dst[e];
+  // n = min(*d_n, n_cap): the pair count of the screen, known on the device only
+  const long long n = d_n ? ((long long)*d_n < n_cap ? (long long)*d_n : n_cap) : n_cap;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < n; t0 += stride) {  // warp-uniform
+    const long long t = t0 + threadIdx.x;
+    int code = -2;
+    unsigned long long item = 0;
+    if (t < n) {
+      item = gen[t];
+      const long long e = (long long)(item >> 20);
+      const int oi = (int)(item & 0xFFFFF);
+      double xi[N], xj[N], P[M][2 * G];
+      const long long a = src[e], c = dst[e];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      xi[k] = Vx[a * N + k];
-      xj[k] = Vx[c * N + k];
+      for (int k = 0; k < N; ++k) {
+        xi[k] = Vx[a * N + k];
+        xj[k] = Vx[c * N + k];
+      }
+      control_points<G, M>(xi, xj, dp.D, P);
+      code = general_code<G, M>(P, obs[oi], margin, kEpsGeo);
+      if (code == 0) atomicMin(first_kill + e, oi);
+      if (code >= 0) atomicAdd(counters + code, 1ull);
+      if (code == -1) atomicOr(counters + 7, 1ull);
+      if (code_out) code_out[t] = (int8_t)code;
     }
-    control_points<G, M>(xi, xj, dp.D, P);
-    code = general_code<G, M>(P, obs[oi], margin, kEpsGeo);
-    if (code == 0) atomicMin(first_kill + e, oi);
-    if (code >= 0) atomicAdd(counters + code, 1ull);
-    if (code == -1) atomicOr(counters + 7, 1ull);
-    if (code_out) code_out[t] = (int8_t)code;
+    warp_append(code == 2, item, n_pend, cap, pend);
   }
-  warp_append(code == 2, item, n_pend, cap, pend);
 }
 
 // ------------------------------------------------------------------ aggregation
-__global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long long n_inst,
-                              const uint8_t* __restrict__ safe, int* __restrict__ qp_kill,
-                              uint8_t* __restrict__ qp_saved, unsigned long long* __restrict__ counters) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned s = 0, u = 0;
-  if (t < n_inst) {
+__global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long long n_cap,
+                              const unsigned long long* __restrict__ d_n, const uint8_t* __restrict__ safe,
+                              int* __restrict__ qp_kill, uint8_t* __restrict__ qp_saved,
+                              unsigned long long* __restrict__ counters) {
+  const long long n = (long long)*d_n < n_cap ? (long long)*d_n : n_cap;
+  unsigned long long s = 0, u = 0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
     const unsigned long long pk = pend[t];
     const long long e = (long long)(pk >> 20);
     const int o = (int)(pk & 0xFFFFF);
-    if (safe[t]) { qp_saved[e] = 1; s = 1; }
-    else { atomicMin(qp_kill + e, o); u = 1; }
+    if (safe[t]) { qp_saved[e] = 1; ++s; }
+    else { atomicMin(qp_kill + e, o); ++u; }
   }
   typedef cub::BlockReduce<unsigned long long, 256> BR;
   __shared__ typename BR::TempStorage tmp;
-  unsigned long long ts = BR(tmp).Sum((unsigned long long)s);
+  unsigned long long ts = BR(tmp).Sum(s);
   __syncthreads();
-  unsigned long long tu = BR(tmp).Sum((unsigned long long)u);
+  unsigned long long tu = BR(tmp).Sum(u);
   if (threadIdx.x == 0) {
     if (ts) atomicAdd(counters + 3, ts);
     if (tu) atomicAdd(counters + 4, tu);
@@ -925,7 +932,47 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
         }
       }
     }
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    // One stream of launches and ONE host synchronisation: the screen's pending count stays on
+    // the device (dcnt[5]) and every QP kernel reads it there; the per-instance buffers are sized
+    // by a capacity (the previous cut's count with headroom).  The read-back at the end checks
+    // the capacities; an overflow (rare: a first cut much larger than the hint) reruns the
+    // affected stage with exact sizes.
+    bool canon_all = true;
+    for (int o = 0; o < n_obs; ++o) canon_all = canon_all && h[o].canon != 0.0;
+    DevBuf &d_safe = c->ws[WS_QSAFE], &d_qst = c->ws[WS_QSTATUS], &d_qit = c->ws[WS_QITERS],
+           &d_qdl = c->ws[WS_QDELTA];
+    const bool any_pairs = E > 0 && n_obs > 0;
+    // first cut on this context: half the screen's list capacity; afterwards the last count + 25%
+    long long qcap = c->qp_hint > 0 ? std::min<long long>((long long)cap, c->qp_hint + c->qp_hint / 4 + 1024)
+                                    : (long long)cap / 2;
+    auto run_qp_stage = [&]() {
+      if (!any_pairs) return;
+      d_safe.alloc(qcap, c->stream);
+      d_qst.alloc(qcap, c->stream);
+      d_qit.alloc(qcap * sizeof(int), c->stream);
+      d_qdl.alloc(qcap * sizeof(double), c->stream);
+      dispatch_rows<Mc>(qp_rows, [&](auto C_) {
+        constexpr int Cc = decltype(C_)::value;
+        QpJob job{g, {}, d_recs, canon_all, d_pend.as<unsigned long long>(), qcap, dcnt + 5, cfg,
+                  cfg->qp_polish ? 1 : 0, polish_screen(), mk, &d_safe, d_qst.as<int8_t>(), d_qit.as<int>(),
+                  d_qdl.as<double>()};
+        for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
+        qp_solve(c, Gc, Mc, Cc, job);
+      });
+      trace("qp");
+      launch(c, "k_qp_verdicts", k_qp_verdicts, dim3((unsigned)std::min<long long>(div_up(qcap, 256), c->num_sms * 8ll)),
+             dim3(256), 0, d_pend.as<unsigned long long>(), qcap, (const unsigned long long*)(dcnt + 5),
+             d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), dcnt);
+    };
+    auto finalize_and_read = [&]() {
+      launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, n_obs,
+             d_kill.as<int>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), mk->alive.as<uint8_t>(),
+             mk->prov.as<uint8_t>());
+      BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    };
+    for (int attempt = 0;; ++attempt) {
+      BZG_REQUIRE(attempt < 4, BZG_ECUDA, "cut work lists kept overflowing");
       d_pend.alloc(cap * sizeof(unsigned long long), c->stream);
       d_gen.alloc(gen_cap * sizeof(unsigned long long), c->stream);
       for (int o0 = 0; o0 < n_obs; o0 += chunk) {
@@ -942,65 +989,68 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
                dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>(),
                use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm);
       }
-      BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-      const unsigned long long n_gen = hcnt[6];
-      if (n_gen > 0 && n_gen <= gen_cap) {
-        // general obstacles: cut_heuristic past branch 1, appending to the same QP work list
-        launch(c, "k_cut_general", k_cut_general<Gc, Mc>, dim3(div_up((long long)n_gen, 64)), dim3(64), 0, dp,
-               g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs,
-               d_gen.as<unsigned long long>(), (long long)n_gen, cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5,
-               cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr);
-        BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-        BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      if (any_general) {
+        // general obstacles: cut_heuristic past branch 1 over the device-side list, appending
+        // to the same QP work list
+        launch(c, "k_cut_general", k_cut_general<Gc, Mc>,
+               dim3((unsigned)std::min<long long>(div_up((long long)gen_cap, 64), c->num_sms * 16ll)), dim3(64), 0, dp,
+               g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs, d_gen.as<unsigned long long>(),
+               (long long)gen_cap, (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt,
+               dcnt + 5, cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr);
       }
+      trace("heuristic");
+      run_qp_stage();
+      finalize_and_read();
       BZG_REQUIRE(hcnt[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
+      const unsigned long long n_gen = hcnt[6];
       if (hcnt[5] <= cap && n_gen <= gen_cap) break;
-      // a work list overflowed: grow it and rerun the screen from a clean state
+      // a screen work list overflowed: grow it and rerun the cut from a clean state
       cap = std::max(cap, hcnt[5] + 1024);
       if (n_gen > gen_cap) gen_cap = n_gen + 1024;
       BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 16 * sizeof(unsigned long long), c->stream));
+      BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
+      launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
     }
-    trace("heuristic");
+    long long n_inst = (long long)hcnt[5];
+    if (n_inst > qcap) {
+      // the QP buffers were too small for this cut: rerun the QP stage (and the mask) exactly
+      qcap = n_inst;
+      unsigned long long zero2[2] = {0, 0};
+      BZG_CHECK_CUDA(cudaMemcpyAsync(dcnt + 3, zero2, sizeof(zero2), cudaMemcpyHostToDevice, c->stream));
+      BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
+      launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
+      run_qp_stage();
+      finalize_and_read();
+    }
+    c->qp_hint = n_inst;
     if (c->trace_on) {
       unsigned long long h8 = 0;
       BZG_CHECK_CUDA(cudaMemcpy(&h8, d_cnt.as<unsigned long long>() + 8, sizeof(h8), cudaMemcpyDeviceToHost));
       std::fprintf(stderr, "[bzg cut] pairs %lld, exact codes (pass 2) %llu, code0 %llu code1 %llu code2 %llu\n",
                    E * (long long)n_obs, h8, hcnt[0], hcnt[1], hcnt[2]);
     }
-    const long long n_inst = (long long)hcnt[5];
     mk->counters[1] = (long long)hcnt[0];
     mk->counters[2] = (long long)hcnt[1];
     mk->counters[3] = (long long)hcnt[2];
-
-    // ---- QP fallback on every indeterminate pair (graph.py:320-337)
-    mk->n_qp = n_inst;
-    bool canon_all = true;
-    for (int o = 0; o < n_obs; ++o) canon_all = canon_all && h[o].canon != 0.0;
-    auto run_qp = [&](auto C_) {
-      constexpr int Cc = decltype(C_)::value;
-      DevBuf &d_safe = c->ws[WS_QSAFE];
-      QpJob job{g, {}, d_recs, canon_all, d_pend.as<unsigned long long>(), n_inst, cfg, cfg->qp_polish ? 1 : 0,
-                polish_screen(), mk, &d_safe};
-      for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
-      qp_solve(c, Gc, Mc, Cc, job);
-      trace("qp");
-      launch(c, "k_qp_verdicts", k_qp_verdicts, dim3(div_up(n_inst, 256)), dim3(256), 0,
-             d_pend.as<unsigned long long>(), n_inst, d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(),
-             d_cnt.as<unsigned long long>());
-      mk->qp_edge.alloc(n_inst * sizeof(long long), c->stream);
-      mk->qp_obs.alloc(n_inst * sizeof(int), c->stream);
-      launch(c, "k_unpack_pend", k_unpack_pend, dim3(div_up(n_inst, 256)), dim3(256), 0,
-             d_pend.as<unsigned long long>(), n_inst, mk->qp_edge.as<long long>(), mk->qp_obs.as<int>());
-    };
-    if (n_inst > 0) dispatch_rows<Mc>(qp_rows, run_qp);
-    launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(E, 256)), dim3(256), 0, E, n_obs, d_kill.as<int>(),
-           d_qkill.as<int>(), d_saved.as<uint8_t>(), mk->alive.as<uint8_t>(), mk->prov.as<uint8_t>());
-    BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
     mk->counters[4] = (long long)hcnt[3];
     mk->counters[5] = (long long)hcnt[4];
+    // per-QP records of the mask, exact size, filled asynchronously after the read-back
+    mk->n_qp = n_inst;
+    if (n_inst > 0) {
+      mk->qp_status.alloc(n_inst, c->stream);
+      mk->qp_iters.alloc(n_inst * sizeof(int), c->stream);
+      mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
+      mk->qp_edge.alloc(n_inst * sizeof(long long), c->stream);
+      mk->qp_obs.alloc(n_inst * sizeof(int), c->stream);
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_status.ptr, d_qst.ptr, n_inst, cudaMemcpyDeviceToDevice, c->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_iters.ptr, d_qit.ptr, n_inst * sizeof(int), cudaMemcpyDeviceToDevice,
+                                     c->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_delta.ptr, d_qdl.ptr, n_inst * sizeof(double), cudaMemcpyDeviceToDevice,
+                                     c->stream));
+      launch(c, "k_unpack_pend", k_unpack_pend, dim3(div_up(n_inst, 256)), dim3(256), 0,
+             d_pend.as<unsigned long long>(), n_inst, mk->qp_edge.as<long long>(), mk->qp_obs.as<int>());
+    }
   });
 }
 
@@ -1072,9 +1122,9 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(B, 256)), dim3(256), 0, d_kill.as<int>(), B, n_obs);
       unsigned long long* dcnt = d_cnt.as<unsigned long long>();
       launch(c, "k_cut_general", k_cut_general<Gc, Mc>, dim3(div_up(B, 64)), dim3(64), 0, dp, g.vertices.as<double>(),
-             g.src.as<int>(), g.dst.as<int>(), d_obs.as<Rec>(), d_items.as<unsigned long long>(), B, cfg->heur_margin,
-             d_kill.as<int>(), dcnt, dcnt + 5, (unsigned long long)B, d_pend.as<unsigned long long>(),
-             d_code.as<int8_t>());
+             g.src.as<int>(), g.dst.as<int>(), d_obs.as<Rec>(), d_items.as<unsigned long long>(), B,
+             (const unsigned long long*)nullptr, cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5,
+             (unsigned long long)B, d_pend.as<unsigned long long>(), d_code.as<int8_t>());
       unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
       BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
       BZG_CHECK_CUDA(cudaMemcpyAsync(code_out, d_code.ptr, B, cudaMemcpyDeviceToHost, c->stream));
@@ -1089,8 +1139,12 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
     mk.E = B;
     DevBuf &d_safe = c->ws[WS_QSAFE];
     dispatch_rows<Mc>(qp_rows, [&](auto C_) {
-      QpJob job{&g, {}, d_obs.ptr, canon_all, d_items.as<unsigned long long>(), B, cfg, cfg->qp_polish ? 2 : 0, 0.0,
-                &mk, &d_safe};
+      mk.qp_status.alloc(B, c->stream);
+      mk.qp_iters.alloc(B * sizeof(int), c->stream);
+      mk.qp_delta.alloc(B * sizeof(double), c->stream);
+      d_safe.alloc(B, c->stream);
+      QpJob job{&g, {}, d_obs.ptr, canon_all, d_items.as<unsigned long long>(), B, nullptr, cfg, cfg->qp_polish ? 2 : 0,
+                0.0, &mk, &d_safe, mk.qp_status.as<int8_t>(), mk.qp_iters.as<int>(), mk.qp_delta.as<double>()};
       for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
       qp_solve(c, Gc, Mc, decltype(C_)::value, job);
     });

@@ -13,13 +13,17 @@ struct QpJob {
   double D[64];                       // boundary matrix (p+1) x 2*gamma, row-major
   const void* d_obs;                  // ObsRec<M>[n_obs] on the device
   bool canon;                         // every obstacle a canonical box (A = [I; -I])
-  const unsigned long long* d_pend;   // work list (e << 20 | o), n_inst entries
-  long long n_inst;
+  const unsigned long long* d_pend;   // work list (e << 20 | o)
+  long long n_inst;                   // capacity of the work list and of every per-instance buffer
+  const unsigned long long* d_n;      // device-side instance count (nullptr: n_inst itself)
   const bzg_cut_config* cfg;
   int polish_mode;                    // 0 none, 1 SOLVED, 2 SOLVED and MAX_ITER
   double screen;                      // polish screen (k_qp_select)
-  Mask* mk;                           // receives qp_status / qp_iters / qp_delta / n_polished
-  DevBuf* d_safe;                     // receives n_inst verdicts
+  Mask* mk;                           // receives n_polished (-1 unless read back)
+  DevBuf* d_safe;                     // receives the verdicts (n_inst capacity)
+  int8_t* st_out;                     // solver status, iterations, ||delta|| per instance
+  int* it_out;
+  double* delta_out;
 };
 // C = padded obstacle rows of the launch (2m or kObsRows); defined in k_qp_g<gamma>.cu
 void qp_solve_g1(Ctx* c, int M, int C, const QpJob& j);

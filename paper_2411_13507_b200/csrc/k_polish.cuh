@@ -14,32 +14,36 @@ namespace {
 //
 // The residual maxima of the selected instances are formed by the polish (qp_residuals).
 template <int G, int M, int C>
-__global__ void k_qp_select(long long n_inst, int polish, double screen, double eps_cut,
-                            const int8_t* __restrict__ st, const double* __restrict__ x,
+__global__ void k_qp_select(long long n_inst, const unsigned long long* __restrict__ d_n, int polish, double screen,
+                            double eps_cut, const int8_t* __restrict__ st, const double* __restrict__ x,
                             double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, int* __restrict__ list,
                             unsigned long long* __restrict__ n_list) {
   constexpr int J = 2 * G, NV = J + C;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  bool need = false;
-  if (t < n_inst) {
-    double s = 0.0;
+  const long long n = dev_count(n_inst, d_n);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t0 = (long long)blockIdx.x * blockDim.x; t0 < n; t0 += stride) {  // warp-uniform
+    const long long t = t0 + threadIdx.x;
+    bool need = false;
+    if (t < n) {
+      double s = 0.0;
 #pragma unroll
-    for (int c = J; c < NV; ++c) s = __fma_rn(x[t * NV + c], x[t * NV + c], s);
-    const double dl = sqrt(s);
-    const bool solved = st[t] == BZG_SOLVED;
-    delta_out[t] = dl;
-    safe_out[t] = (uint8_t)(solved && dl > eps_cut);
-    // polish 1: SOLVED only (the verdict is all cut_graph uses); 2: also MAX_ITER, whose
-    // polished x the reference returns from solve() (cut_qp's ||delta||)
-    need = polish && (solved || (polish == 2 && st[t] == BZG_MAX_ITER)) && (screen <= 0.0 || dl < screen);
-  }
-  const unsigned m = __ballot_sync(0xffffffffu, need);
-  if (m) {
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) base = atomicAdd(n_list, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (need) list[base + __popc(m & ((1u << lane) - 1u))] = (int)t;
+      for (int c = J; c < NV; ++c) s = __fma_rn(x[t * NV + c], x[t * NV + c], s);
+      const double dl = sqrt(s);
+      const bool solved = st[t] == BZG_SOLVED;
+      delta_out[t] = dl;
+      safe_out[t] = (uint8_t)(solved && dl > eps_cut);
+      // polish 1: SOLVED only (the verdict is all cut_graph uses); 2: also MAX_ITER, whose
+      // polished x the reference returns from solve() (cut_qp's ||delta||)
+      need = polish && (solved || (polish == 2 && st[t] == BZG_MAX_ITER)) && (screen <= 0.0 || dl < screen);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (m) {
+      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(n_list, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) list[base + __popc(m & ((1u << lane) - 1u))] = (int)t;
+    }
   }
 }
 

@@ -15,6 +15,14 @@
 namespace bzg {
 namespace {
 
+// Work-list length known only on the device (cut_graph keeps the heuristic's pending count
+// there): n = min(*d_n, cap); d_n == nullptr means n = cap (the host knows it).
+__device__ __forceinline__ long long dev_count(long long cap, const unsigned long long* __restrict__ d_n) {
+  if (!d_n) return cap;
+  const unsigned long long n = *d_n;
+  return (long long)n < cap ? (long long)n : cap;
+}
+
 struct QpParams {
   double rho, rho_eq, sigma, alpha, one_m_alpha, eps_abs, eps_rel, eps_pinf;
   int max_iter;

@@ -18,9 +18,10 @@
 namespace bzg {
 namespace {
 
-// Batched Cut-QP over the work list pend[0 .. n_inst) (graph.py:320-337 / cut_qp 285-299):
-// ADMM, verdict selection, polish.  Fills mk->qp_status / qp_iters / qp_delta / n_polished
-// and d_safe (n_inst verdicts).  polish_mode: 0 none, 1 SOLVED, 2 SOLVED and MAX_ITER.
+// Batched Cut-QP over the work list pend[0 .. n) (graph.py:320-337 / cut_qp 285-299), n =
+// min(*job.d_n, job.n_inst) read on the device (job.n_inst = the buffers' capacity): ADMM,
+// verdict selection, polish.  Fills job.st_out / it_out / delta_out, mk->n_polished and d_safe
+// (n verdicts).  polish_mode: 0 none, 1 SOLVED, 2 SOLVED and MAX_ITER.  No host round trip.
 template <int G, int M, int C>
 void qp_solve_t(Ctx* c, const QpJob& job) {
   const Graph* g = job.g;
@@ -37,9 +38,10 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
   DevBuf& d_safe = *job.d_safe;
   auto trace = [&](const char* what) { c->trace(what); };
   constexpr int NV = 2 * G + C, MCc = C + 2 * G + 1;
-  mk->qp_status.alloc(n_inst, c->stream);
-  mk->qp_iters.alloc(n_inst * sizeof(int), c->stream);
-  mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
+  const unsigned long long* d_n = job.d_n;
+  int8_t* st_out = job.st_out;
+  int* it_out = job.it_out;
+  double* delta_out = job.delta_out;
   DevBuf &d_x = c->ws[WS_QX], &d_zy = c->ws[WS_QZY], &d_list = c->ws[WS_QLIST];
   DevBuf d_next;
   d_x.alloc(n_inst * NV * sizeof(double), c->stream);
@@ -76,8 +78,9 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
   DevBuf& d_consts = c->ws[WS_QCONST];
   d_consts.alloc(n_inst * nconst * sizeof(double), c->stream);
   trace("qp alloc");
-  launch(c, "k_qp_setup", setup, dim3(div_up(n_inst, 128)), dim3(128), 0, qp, dp, g->vertices.as<double>(),
-         g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, d_consts.as<double>());
+  launch(c, "k_qp_setup", setup, dim3((unsigned)std::min<long long>(div_up(n_inst, 128), c->num_sms * 8ll)),
+         dim3(128), 0, qp, dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, d_n,
+         d_consts.as<double>());
   // Lanes per instance: two when the work list is short against the resident lanes (the
   // 500-iteration chains then set the time, and k_qp_admm2 halves them), else one.
   // BZG_ADMM_LANES=1|2 forces a variant (A/B runs).
@@ -91,8 +94,7 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
       if (canon) admm2 = k_qp_admm2<G, M, C, true>;
     const long long blocks2 = std::min<long long>(div_up(2 * n_inst, 128), (long long)c->num_sms * 16);
     launch(c, "k_qp_admm", admm2, dim3((unsigned)blocks2), dim3(128), 0, qp, d_consts.as<double>(), n_inst,
-           d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(), mk->qp_iters.as<int>(), d_x.as<double>(),
-           d_zy.as<double>());
+           d_next.as<unsigned long long>(), st_out, it_out, d_x.as<double>(), d_zy.as<double>(), d_n);
   } else {
     // main pass over the work list, then resume passes over the parked tails (AdmmPass):
     // BZG_ADMM_PASSES launches, the last one without parking; BZG_ADMM_DUMP is the live-lane
@@ -121,8 +123,8 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
         pass.dump_below = dump;
       }
       launch(c, ps == 0 ? "k_qp_admm" : "k_qp_admm_tail", admm, dim3((unsigned)blocks), dim3(128), 0, qp,
-             d_consts.as<double>(), n_inst, d_next.as<unsigned long long>(), mk->qp_status.as<int8_t>(),
-             mk->qp_iters.as<int>(), d_x.as<double>(), d_zy.as<double>(), pass);
+             d_consts.as<double>(), n_inst, d_next.as<unsigned long long>(), st_out, it_out, d_x.as<double>(),
+             d_zy.as<double>(), pass, d_n);
       if (c->trace_on && pass.rq_out_n) {
         unsigned long long hq = 0;
         BZG_CHECK_CUDA(cudaMemcpyAsync(&hq, pass.rq_out_n, sizeof(hq), cudaMemcpyDeviceToHost, c->stream));
@@ -133,9 +135,10 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
   }
   trace("admm");
   BZG_CHECK_CUDA(cudaMemsetAsync(d_next.ptr, 0, sizeof(unsigned long long), c->stream));
-  launch(c, "k_qp_select", k_qp_select<G, M, C>, dim3(div_up(n_inst, 256)), dim3(256), 0, n_inst, polish_mode,
-         screen, cfg->eps_cut, mk->qp_status.as<int8_t>(), d_x.as<double>(), mk->qp_delta.as<double>(),
-         d_safe.as<uint8_t>(), d_list.as<int>(), d_next.as<unsigned long long>());
+  launch(c, "k_qp_select", k_qp_select<G, M, C>,
+         dim3((unsigned)std::min<long long>(div_up(n_inst, 256), c->num_sms * 8ll)), dim3(256), 0, n_inst, d_n,
+         polish_mode, screen, cfg->eps_cut, (const int8_t*)st_out, d_x.as<double>(), delta_out, d_safe.as<uint8_t>(),
+         d_list.as<int>(), d_next.as<unsigned long long>());
   static const bool polish_lu = std::getenv("BZG_POLISH_IMPL") && std::string(std::getenv("BZG_POLISH_IMPL")) == "lu";
   long long n_list = -1;  // known on the host only when it is read back (LU path, tracing)
   if (polish_lu || c->trace_on) {
@@ -152,15 +155,14 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
     ensure_dyn_smem((const void*)k_qp_polish<G, M, C>, psmem);
     launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
            dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
-           cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(), mk->qp_delta.as<double>(), d_safe.as<uint8_t>(),
-           mk->qp_status.as<int8_t>());
+           cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(), delta_out, d_safe.as<uint8_t>(), st_out);
   } else {
     // persistent grid over the device-side list length (at most n_inst entries)
     const long long pblocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 8);
     launch(c, "k_qp_polish", k_qp_polish_reg<G, M, C>, dim3((unsigned)pblocks), dim3(128), 0, dp,
            g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(),
-           d_next.as<unsigned long long>(), cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(),
-           mk->qp_delta.as<double>(), d_safe.as<uint8_t>(), mk->qp_status.as<int8_t>());
+           d_next.as<unsigned long long>(), cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(), delta_out,
+           d_safe.as<uint8_t>(), st_out);
   }
   trace("select+polish");
 }
