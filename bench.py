@@ -168,6 +168,7 @@ class DeviceStep:
         h = C.c_void_p()
         nat.check(lib.bzg_build_graph(ctx.handle, C.byref(self.desc), C.byref(h)))
         graph = G.BezierGraph(h, ctx, w.spec, w.oracle, w.seed, w.sample_bounds, self.D)
+        graph._desc_fn = lambda: (self.desc, self._keep)
         t1 = time.perf_counter()
         offs, A, b, is_box, lo, hi = self.obs
         mh = C.c_void_p()
@@ -474,6 +475,8 @@ def main():
     if args.breakdown and rank == 0:
         for k, (ms, n) in sorted(breakdown.items(), key=lambda kv: -kv[1][0]):
             print(f"{k:28s} {ms:9.4f} ms/step  {n:7d} launches/step", file=sys.stderr)
+    if rank == 0 and world == 1:
+        out["parity"] = parity_block(w, step)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(w, step, args.cpu_rows)
     if rank == 0:
@@ -575,17 +578,48 @@ def _cpu_sample_rows(w, rows):
 
 
 def cpu_baseline(w, step, rows_opt):
-    """Single-core oracle (numpy restatement of the reference) on a bounded row sample."""
-    import oracle
+    """One host core on a bounded row sample: the unmodified reference package where the config
+    has a reference generator (cfg2, cfg3: build_graph's pair test + cut_graph's own
+    _heuristic_batch / solve_batch, _ref_live_rows; its own find_path on the full graph the device
+    produced), else the oracle port (numpy restatement of the reference)."""
+    import types
 
     V = w.num_vertices
     S = rows_opt or max(8, min(V, int(round(V * 0.005))))  # ~0.5% of the source rows
+    g, mk = step.last_graph, step.last_mask
+    if _import_reference() is not None and w.name.startswith(("cfg2", "cfg3")):
+        from beziergraph import graph as rg
+
+        name = "cfg3" if w.name.startswith("cfg3") else "cfg2"
+        t0 = time.perf_counter()
+        _ref_live_init(name)  # scene + sampler (graph.py:147-159) on reference objects
+        t_sample = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        e_s, q_s = _ref_live_rows((0, S))
+        t_rows = time.perf_counter() - t0
+        spec, oracle = _REF_SCENE[0], _REF_SCENE[1]
+        gref = types.SimpleNamespace(vertices=g.vertices, edges=g.edges, costs=g.costs, spec=spec, oracle=oracle,
+                                     num_vertices=g.num_vertices)
+        mref = types.SimpleNamespace(alive=mk.alive)
+        t0 = time.perf_counter()
+        rg.find_path(gref, mref, w.start, w.goal)
+        t_path = time.perf_counter() - t0
+        t_full = t_sample + t_rows * (V / S) + t_path
+        return {"value": V * V / t_full, "unit": UNIT, "cores": 1, "kind": "reference",
+                "ms_per_step_extrapolated": t_full * 1e3,
+                "sample": (f"unmodified reference package (baseline/_ref) in one process: scene + sampler "
+                           f"({t_sample:.2f}s), build_graph's pair test + points + costs and cut_graph's "
+                           f"_heuristic_batch + solve_batch on source rows [0,{S}) ({S * V} pairs, {e_s} edges, "
+                           f"{q_s} QPs, {t_rows:.2f}s) extrapolated x{V / S:.1f}, the reference's find_path on the "
+                           f"full {g.num_edges}-edge graph ({t_path:.2f}s)"),
+                "cpu_model": _cpu_model()}
+    import oracle
+
     t0 = time.perf_counter()
     oracle.sample_states(w.N, w.sample_bounds.lo, w.sample_bounds.hi, w.oracle.Xd.A, w.oracle.Xd.b, w.seed, w.include)
     t_sample = time.perf_counter() - t0
     tb, tc, e_s, q_s = _cpu_sample_rows(w, (0, S))
     # Dijkstra (heapq) on the full graph the device produced (same arrays the reference would search)
-    g, mk = step.last_graph, step.last_mask
     t0 = time.perf_counter()
     oracle.find_path(g.vertices, g.edges, g.costs, mk.alive, w.start, w.goal, w.spec.m, w.oracle.tube.error.lo,
                      w.oracle.tube.error.hi)
@@ -600,6 +634,36 @@ def cpu_baseline(w, step, rows_opt):
             "cpu_model": _cpu_model()}
 
 
+def parity_block(w, step):
+    """The step's outputs against the live-reference golden of this workload (tests/golden,
+    captured by make_golden.py from the unmodified reference on the same inputs): outside the
+    timed region.  None when no golden exists for the config."""
+    import hashlib
+
+    name = {"cfg3-hop-deg5-20k": "cfg3_hop20k", "cfg2-random-field-1": "cfg2_rf2000"}.get(w.name)
+    path = ROOT / "tests" / "golden" / f"{name}.npz"
+    if name is None or not path.exists() or step.world > 1:
+        return None
+    gd = np.load(path)
+    g, mk = step.last_graph, step.last_mask
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    alive = mk.alive
+    cnt = [mk.pairs_total, mk.pairs_point_hit, mk.pairs_hyperplane, mk.pairs_qp, mk.qp_safe, mk.qp_unsafe]
+    ref_cnt = [int(x) for x in gd["counters"]]
+    band = g.eps_band(1e-11)["band"] if g._desc_fn is not None else None
+    return {"golden": f"tests/golden/{name}.npz (live reference, {str(gd['env'])[:60]}...)",
+            "vertices_bitwise": sha(g.vertices) == str(gd["sha_vertices"]),
+            "edges_bitwise": sha(g.edges) == str(gd["sha_edges"]),
+            "costs_bitwise": sha(g.costs) == str(gd["sha_costs"]),
+            "heuristic_counters_equal": cnt[:4] == ref_cnt[:4],
+            "qp_counters": {"device": cnt[4:], "reference": ref_cnt[4:]},
+            "alive_mismatch": int((alive != gd["alive"]).sum()),
+            "provenance_mismatch": int((mk.provenance_codes != gd["provenance"]).sum()),
+            "path_equal": step.last["path"] == [int(x) for x in gd["path"]],
+            "eps_band_1e-11": {"device": band, "reference": int(gd["eps_band_1e-11"])} if "eps_band_1e-11" in gd else None,
+            "note": "QP verdict differences are solver-sensitive (tests/helpers.py qp_solver_sensitive)"}
+
+
 def _cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -610,6 +674,119 @@ def _cpu_model():
     return "unknown"
 
 
+def _import_reference():
+    """The unmodified reference package: baseline/_ref (pip-installed by __graft_entry__.build(),
+    travels to the GPU box) or /root/reference/pkg/src (the build container); None if absent."""
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "beziergraph" / "__init__.py").exists():
+            if str(p) not in sys.path:
+                sys.path.insert(0, str(p))
+            import beziergraph
+
+            return beziergraph
+    return None
+
+
+_REF_SCENE = None
+
+
+def _ref_scene(name):
+    """Reference objects of a BASELINE workload built with the reference's own generators:
+    (spec, oracle, V, inflated obstacles, CutConfig).  cfg2 = random_field_scenario(1, 20, 2000)
+    through sim.build_pipeline's inputs; cfg3 = the recipe of tests/golden/make_golden.py
+    case_cfg3.  Vertices by build_graph's own sampler loop (graph.py:147-159) on reference
+    Box/Polytope objects.  None for the keep-in configs (no reference function)."""
+    bg = _import_reference()
+    if bg is None or name not in ("cfg2", "cfg3"):
+        return None
+    from beziergraph import geometry as rgeo
+    from beziergraph import graph as rg
+    from beziergraph import scenario as rsc
+    from beziergraph import sim as rsim
+
+    if name == "cfg2":
+        s = rsc.random_field_scenario(1, n_obstacles=20, graph_n=2000)
+        spec, oracle = s.spec, bg.build_oracle(s.spec, s.xd, s.u_bounds, s.tube)
+        N, bounds, seed, include = s.graph_n, s.sample_bounds, s.seed_graph, np.array([s.start, s.goal])
+        obstacles = rsim._inflated(s, 0.0)
+    else:
+        spec = bg.BezierSpec(m=2, gamma=3, T=1.0)
+        xd = rgeo.Box(np.array([0.0, 0.0, -1.5, -1.5, -4.0, -4.0]), np.array([5.0, 5.0, 1.5, 1.5, 4.0, 4.0])).to_polytope()
+        u = rgeo.Box(np.array([-30.0, -30.0]), np.array([30.0, 30.0]))
+        bounds = rgeo.Box(np.array([0.0, 0.0, -0.6, -0.6, -1.0, -1.0]), np.array([5.0, 5.0, 0.6, 0.6, 1.0, 1.0]))
+        tube = rsim.design_tube(spec, (6.0, 11.0, 6.0), 0.02)
+        oracle = bg.build_oracle(spec, xd, u, tube)
+        start = np.array([0.4, 0.4, 0, 0, 0, 0.0])
+        goal = np.array([4.6, 4.6, 0, 0, 0, 0.0])
+        rng = np.random.default_rng(11)
+        obs = []
+        while len(obs) < 50:
+            c = rng.uniform(0.4, 4.6, 2)
+            w_ = rng.uniform(0.25, 0.7, 2)
+            if np.linalg.norm(c - start[:2]) < 0.9 or np.linalg.norm(c - goal[:2]) < 0.9:
+                continue
+            obs.append(rsc._box_obstacle(c[0], c[1], w_[0], w_[1]).shape)
+        obstacles = [rgeo.inflate(o, tube.position_box(2)) for o in obs]
+        N, seed, include = 20000, 1, np.array([start, goal])
+    rng = np.random.default_rng(seed)  # graph.py:147-159
+    got, need = [], N
+    while need > 0:
+        cand = bounds.sample(rng, need)
+        ok = oracle.Xd.contains_many(cand)
+        if ok.any():
+            got.append(cand[ok])
+            need -= int(ok.sum())
+    V = np.vstack([np.vstack(got)[:N], include])
+    return spec, oracle, V, obstacles, rg.CutConfig()
+
+
+def _ref_live_init(name):
+    global _REF_SCENE
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    _REF_SCENE = _ref_scene(name)
+
+
+def _ref_live_rows(payload):
+    """Source rows [r0, r1) through the reference: the pair test as build_graph evaluates it
+    (graph.py:172-197, its own projections and 32-row chunks), then the reference's own
+    _heuristic_batch and qpsolver.solve_batch on those edges, as cut_graph calls them
+    (graph.py:312-337).  Returns (edges, QPs)."""
+    from beziergraph import bezier as rbz
+    from beziergraph import graph as rg
+    from beziergraph import qpsolver as rqp
+
+    r0, r1 = payload
+    spec, oracle, V, obstacles, cfg = _REF_SCENE
+    n = spec.n
+    A1 = V[r0:r1] @ oracle.F1.T
+    A2 = V @ oracle.F2.T
+    thresh = oracle.G + rg.EPS_GEO
+    src_l, dst_l = [], []
+    for lo in range(0, r1 - r0, rg._PAIR_CHUNK):
+        hi = min(lo + rg._PAIR_CHUNK, r1 - r0)
+        feas = np.all(A1[lo:hi][:, None, :] + A2[None, :, :] <= thresh, axis=2)
+        feas[np.arange(hi - lo), np.arange(r0 + lo, r0 + hi)] = False
+        s_, d_ = np.nonzero(feas)
+        src_l.append(s_ + r0 + lo)
+        dst_l.append(d_)
+    E = np.stack([np.concatenate(src_l), np.concatenate(dst_l)], axis=1).astype(np.int64)
+    D = rbz.boundary_matrix(spec)
+    x1 = V[E[:, 0]].reshape(-1, spec.gamma, spec.m)
+    x2 = V[E[:, 1]].reshape(-1, spec.gamma, spec.m)
+    pts = np.einsum("pq,eqm->emp", D, np.concatenate([x1, x2], axis=1))
+    np.linalg.norm(np.diff(pts, axis=2), axis=1).sum(axis=1)
+    del n
+    n_qp = 0
+    for ob in obstacles:
+        codes = rg._heuristic_batch(pts, ob, cfg)
+        pending = np.nonzero(codes == 2)[0]
+        n_qp += pending.size
+        if pending.size:
+            O = ob.normalized()
+            rqp.solve_batch([rg._cut_qp_problem(pts[e], O) for e in pending], cfg.qp)
+    return E.shape[0], n_qp
+
+
 def _ref_worker(payload):
     name, r0, r1 = payload
     w = workload(name)
@@ -617,7 +794,14 @@ def _ref_worker(payload):
 
 
 def reference_arm(args, rank, world):
-    """`--impl reference`: the oracle port of the reference CPU path on all host cores (rank 0 only)."""
+    """`--impl reference`: the reference's CPU path on all host cores (rank 0 only).
+
+    cfg2 / cfg3: the unmodified reference package (baseline/_ref) in a pool of one process per
+    host core, each running the reference's own build arithmetic and its _heuristic_batch /
+    solve_batch on a block of source rows (SURVEY.md §8(d) "ref-Np").  A step is a bounded
+    row sample, extrapolated linearly to all rows (the whole reference step at cfg3 is
+    ~2,900 s on one core: tests/golden/cfg3_hop20k.npz t_build + t_cut).  Keep-in configs have
+    no reference function: the oracle port stands in there."""
     if rank != 0:
         return
     import multiprocessing as mp
@@ -626,30 +810,52 @@ def reference_arm(args, rank, world):
     w = workload(args.config)
     V = w.num_vertices
     cores = len(os.sched_getaffinity(0))
-    S = args.cpu_rows or min(V, cores * 48)
-    chunks = [(args.config, S * k // cores, S * (k + 1) // cores) for k in range(cores)]
+    live = _import_reference() is not None and args.config in ("cfg2", "cfg3")
+    S = args.cpu_rows or min(V, cores * (48 if args.config == "cfg3" else 64))
     times = []
-    with mp.get_context("spawn").Pool(cores) as pool:
+    if live:
+        chunks = [(S * k // cores, S * (k + 1) // cores) for k in range(cores)]
+        pool = mp.get_context("spawn").Pool(cores, initializer=_ref_live_init, initargs=(args.config,))
+        fn = _ref_live_rows
+    else:
+        chunks = [(args.config, S * k // cores, S * (k + 1) // cores) for k in range(cores)]
+        pool = mp.get_context("spawn").Pool(cores)
+        fn = _ref_worker
+    with pool:
         for k in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            res = pool.map(_ref_worker, chunks)
+            res = pool.map(fn, chunks)
             t = time.perf_counter() - t0
             if k >= args.warmup:
                 times.append(t)
     ms_sample = statistics.mean(times) * 1e3
     ms_full = ms_sample * V / S
     value = V * V / (ms_full * 1e-3)
-    e_s = sum(r[2] for r in res)
-    q_s = sum(r[3] for r in res)
-    sample = (f"oracle port (numpy restatement of reference graph.py/qpsolver.py) in a {cores}-process pool: each "
-              f"step = pair test + control points + costs + box cut + Cut-QP on source rows [0,{S}) of {w.name} "
-              f"({S * V} pairs, {e_s} edges, {q_s} QPs), extrapolated x{V / S:.1f} to all rows; Dijkstra excluded")
+    if live:
+        e_s = sum(r[0] for r in res)
+        q_s = sum(r[1] for r in res)
+        kind = "reference"
+        sample = (f"unmodified reference package (baseline/_ref beziergraph) in a {cores}-process pool: each step "
+                  f"= build_graph's pair test + control points + costs (graph.py:172-197) and cut_graph's "
+                  f"_heuristic_batch + qpsolver.solve_batch (graph.py:312-337) on source rows [0,{S}) of {w.name} "
+                  f"({S * V} pairs, {e_s} edges, {q_s} QPs), extrapolated x{V / S:.1f} to all rows; Dijkstra "
+                  f"excluded (the reference's heapq search: 1.2 s of its 2,902 s single-core step at cfg3, 93 ms "
+                  f"of 76 s at cfg2)")
+    else:
+        e_s = sum(r[2] for r in res)
+        q_s = sum(r[3] for r in res)
+        kind = "port"
+        sample = (f"oracle port (numpy restatement of reference graph.py/qpsolver.py; the keep-in regions have no "
+                  f"reference function) in a {cores}-process pool: each step = pair test + control points + costs + "
+                  f"box cut + Cut-QP on source rows [0,{S}) of {w.name} ({S * V} pairs, {e_s} edges, {q_s} QPs), "
+                  f"extrapolated x{V / S:.1f} to all rows; Dijkstra excluded")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_full, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": w.name, "vertices": V, "ordered_pairs": V * V, "obstacles": len(w.obstacles),
-                      "gamma": w.spec.gamma, "parallelism": f"cpu x{cores}"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                      "gamma": w.spec.gamma, "degree": w.spec.p, "parallelism": f"cpu x{cores}",
+                      "seed": w.seed},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
                             "cpu_model": _cpu_model()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
