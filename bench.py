@@ -168,7 +168,8 @@ class DeviceStep:
         h = C.c_void_p()
         nat.check(lib.bzg_build_graph(ctx.handle, C.byref(self.desc), C.byref(h)))
         graph = G.BezierGraph(h, ctx, w.spec, w.oracle, w.seed, w.sample_bounds, self.D)
-        graph._desc_fn = lambda: (self.desc, self._keep)
+        desc, keep = self.desc, self._keep  # no reference back to self: graph <-> step would be a cycle
+        graph._desc_fn = lambda: (desc, keep)
         t1 = time.perf_counter()
         offs, A, b, is_box, lo, hi = self.obs
         mh = C.c_void_p()

@@ -242,6 +242,7 @@ struct Graph {
 
 struct Mask {
   Graph* g = nullptr;
+  Ctx* ctx = nullptr;  // kept here so a mask can be released after its graph (Python GC order)
   int64_t E = 0;
   int32_t n_obs = 0;
   DevBuf alive;                   // E uint8

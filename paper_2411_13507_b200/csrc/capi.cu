@@ -449,7 +449,7 @@ int bzg_cut_points(bzg_ctx* ctx, int32_t m, int32_t J, int64_t B, const double* 
 int bzg_mask_destroy(bzg_mask* mk) {
   return guarded([&] {
     if (!mk) return;
-    if (mk->g) set_device(mk->g->ctx);
+    if (mk->ctx) set_device(mk->ctx);  // not via mk->g: the graph may already be released
     delete mk;
   });
 }
@@ -510,6 +510,7 @@ int bzg_mask_from_arrays(bzg_ctx* ctx, bzg_graph* g, const uint8_t* alive, const
     set_device(ctx);
     mk = new bzg_mask();
     mk->g = g;
+    mk->ctx = ctx;
     mk->E = g->E;
     const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     mk->alive.alloc(std::max<long long>(g->E, 1), ctx->stream);

@@ -204,6 +204,28 @@ __global__ void k_project_sorted(RowPlan rp, const double* __restrict__ F, const
   dst_ok[s] = (uint8_t)ok;
 }
 
+// A row block's own sources, in the Morton order of the full sort: sorted positions whose
+// vertex lies in [r0, r1) (flag + exclusive scan -> pos), then gathered so source tiles are
+// dense in the block (a tile of the full order would hold ~32 / G of them).
+__global__ void k_src_flags(const int* __restrict__ perm, long long V, long long r0, long long r1, int* __restrict__ flag) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s < V) flag[s] = (perm[s] >= r0 && perm[s] < r1) ? 1 : 0;
+}
+
+__global__ void k_src_gather(const int* __restrict__ perm, const int* __restrict__ flag, const int* __restrict__ pos,
+                             long long V, int Kpad, const double* __restrict__ a1c, const uint8_t* __restrict__ src_ok,
+                             const unsigned long long* __restrict__ smask, int RW, int* __restrict__ perm_src,
+                             double* __restrict__ a1c_src, uint8_t* __restrict__ ok_src,
+                             unsigned long long* __restrict__ smask_src) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= V || !flag[s]) return;
+  const long long t = pos[s];
+  perm_src[t] = perm[s];
+  ok_src[t] = src_ok[s];
+  for (int q = 0; q < Kpad; ++q) a1c_src[t * Kpad + q] = a1c[s * Kpad + q];
+  for (int w = 0; w < RW; ++w) smask_src[t * RW + w] = smask[s * RW + w];
+}
+
 // [min, max] per (32-vertex group, interval) over the group's valid vertices
 __global__ void k_group_bounds(const double* __restrict__ a, int transposed, long long V, int Kpad,
                                const uint8_t* __restrict__ ok, double* __restrict__ gmin, double* __restrict__ gmax) {
@@ -308,7 +330,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_tiles(
     const uint8_t* __restrict__ dst_ok, const int* __restrict__ perm, const double* __restrict__ tmin,
     const double* __restrict__ tmax, const double* __restrict__ gmin, const double* __restrict__ gmax, long long V,
     long long r0, long long W, uint32_t* __restrict__ bits, unsigned long long* __restrict__ rowcnt,
-    RegionMasks rm) {
+    RegionMasks rm, const int* __restrict__ perm_src, long long V_src) {
   __shared__ double s_a1[kTile][K];
   __shared__ uint8_t s_ok[kTile];
   __shared__ int s_orig[kTile];
@@ -316,7 +338,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_tiles(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long tile = blockIdx.y;
   const long long i0 = tile * kTile;
-  const int rows = (int)min((long long)kTile, V - i0);
+  const int rows = (int)min((long long)kTile, V_src - i0);
   const long long g = (long long)blockIdx.x * (kPairThreads / 32) + warp;
   // ---- (tile, group) culls first: a block whose eight groups all fail skips the staging
   bool live = g * kTile < V;
@@ -354,7 +376,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_tiles(
   }
   if (tid < rows) {
     s_ok[tid] = src_ok[i0 + tid];
-    s_orig[tid] = perm[i0 + tid];
+    s_orig[tid] = perm_src[i0 + tid];
     if (REG)
       for (int w = 0; w < kMaxRegionWords; ++w) s_sm[tid][w] = w < rm.RW ? rm.smask[(i0 + tid) * rm.RW + w] : 0ull;
   }
@@ -400,7 +422,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_tiles(
       }
     }
     if (__any_sync(0xffffffffu, c2)) continue;
-    bool ok = jok && jreg && (i0 + ii != j);
+    bool ok = jok && jreg && (s_orig[ii] != orig_j);  // by original index
 #pragma unroll
     for (int q = 0; q < K; ++q) {
       if ((q & 1) == 0 && q > 0) {
@@ -467,7 +489,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_list(
     const uint8_t* __restrict__ dst_ok, const int* __restrict__ perm, const double* __restrict__ gmin,
     const double* __restrict__ gmax, long long V, long long r0, long long W, uint32_t* __restrict__ bits,
     unsigned long long* __restrict__ rowcnt, RegionMasks rm, const unsigned long long* __restrict__ list,
-    const unsigned long long* __restrict__ n_list) {
+    const unsigned long long* __restrict__ n_list, const int* __restrict__ perm_src, long long V_src) {
   constexpr int NW = kPairThreads / 32, QL = (K + 31) / 32;
   // dynamic shared memory (pair_list_smem): per warp a1 tile, region masks, original ids, flags
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -486,7 +508,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_list(
     const unsigned long long it = list[e];
     const long long tile = (long long)(it >> 32), g = (long long)(it & 0xffffffffull);
     const long long i0 = tile * kTile;
-    const int rows = (int)min((long long)kTile, V - i0);
+    const int rows = (int)min((long long)kTile, V_src - i0);
     __syncwarp();
     for (int t = lane; t < rows * K; t += 32) {
       const int ii = t / K, q = t - ii * K;
@@ -494,7 +516,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_list(
     }
     if (lane < rows) {
       s_ok[lane] = src_ok[i0 + lane];
-      s_orig[lane] = perm[i0 + lane];
+      s_orig[lane] = perm_src[i0 + lane];
       if (REG)
         for (int w = 0; w < kMaxRegionWords; ++w)
           s_sm_all[warp][lane][w] = w < rm.RW ? rm.smask[(i0 + lane) * rm.RW + w] : 0ull;
@@ -555,7 +577,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_list(
         }
       }
       if (__any_sync(0xffffffffu, c2)) continue;
-      bool ok = jok && jreg && (i0 + ii != j);
+      bool ok = jok && jreg && (s_orig[ii] != orig_j);  // by original index
 #pragma unroll
       for (int q = 0; q < K; ++q) {
         if ((q & 1) == 0 && q > 0) {
@@ -1158,33 +1180,69 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
                      gor.as<unsigned long long>(), rr.RW};
   }
   c->trace("pairs: morton+proj+regions");
+  // ---- the row block's sources, densely tiled in Morton order (multi-GPU row split: with the
+  // full order a 32-source tile would hold ~32 / G sources of this block, and the cull, list
+  // and staging work would not shrink with G); destinations stay the full sorted order
+  const bool split = rows < V && rows > 0;
+  const long long Vs = split ? rows : V;
+  const long long ngs = (Vs + kTile - 1) / kTile;
+  DevBuf s_perm, s_a1c, s_ok, s_smask, s_flag, s_pos, s_tor;
+  const int* perm_src = perm.as<int>();
+  const double* a1c_src = a1c.as<double>();
+  const uint8_t* ok_src = sok.as<uint8_t>();
+  RegionMasks rms = rm;
+  if (split) {
+    s_flag.alloc((V + 1) * sizeof(int), c->stream);
+    s_pos.alloc((V + 1) * sizeof(int), c->stream);
+    launch(c, "k_src_flags", k_src_flags, dim3(div_up(V, 256)), dim3(256), 0, perm.as<int>(), V, r0, r1,
+           s_flag.as<int>());
+    BZG_CHECK_CUDA(cudaMemsetAsync(s_flag.as<int>() + V, 0, sizeof(int), c->stream));
+    exclusive_scan_i(c, s_flag.as<int>(), s_pos.as<int>(), V + 1);
+    s_perm.alloc(Vs * sizeof(int), c->stream);
+    s_a1c.alloc((size_t)Vs * Kpad * sizeof(double), c->stream);
+    s_ok.alloc(Vs, c->stream);
+    s_smask.alloc(std::max<long long>(R > 0 ? Vs * rm.RW : 1, 1) * sizeof(unsigned long long), c->stream);
+    launch(c, "k_src_gather", k_src_gather, dim3(div_up(V, 256)), dim3(256), 0, perm.as<int>(), s_flag.as<int>(),
+           s_pos.as<int>(), V, Kpad, a1c.as<double>(), sok.as<uint8_t>(), rm.smask, R > 0 ? rm.RW : 0,
+           s_perm.as<int>(), s_a1c.as<double>(), s_ok.as<uint8_t>(), s_smask.as<unsigned long long>());
+    perm_src = s_perm.as<int>();
+    a1c_src = s_a1c.as<double>();
+    ok_src = s_ok.as<uint8_t>();
+    if (R > 0) {
+      s_tor.alloc(ngs * rm.RW * sizeof(unsigned long long), c->stream);
+      launch(c, "k_mask_or", k_mask_or, dim3(div_up(ngs * rm.RW, 256)), dim3(256), 0, s_smask.as<unsigned long long>(),
+             ok_src, Vs, rm.RW, s_tor.as<unsigned long long>());
+      rms.smask = s_smask.as<unsigned long long>();
+      rms.tile_or = s_tor.as<unsigned long long>();
+    }
+  }
   DevBuf tmin, tmax, gmin, gmax;
-  tmin.alloc(ng * Kpad * sizeof(double), c->stream);
-  tmax.alloc(ng * Kpad * sizeof(double), c->stream);
+  tmin.alloc(ngs * Kpad * sizeof(double), c->stream);
+  tmax.alloc(ngs * Kpad * sizeof(double), c->stream);
   gmin.alloc(ng * Kpad * sizeof(double), c->stream);
   gmax.alloc(ng * Kpad * sizeof(double), c->stream);
-  launch(c, "k_group_bounds", k_group_bounds, dim3(div_up(ng * Kpad, 256)), dim3(256), 0, a1c.as<double>(), 0, V, Kpad,
-         sok.as<uint8_t>(), tmin.as<double>(), tmax.as<double>());
+  launch(c, "k_group_bounds", k_group_bounds, dim3(div_up(ngs * Kpad, 256)), dim3(256), 0, a1c_src, 0, Vs, Kpad,
+         ok_src, tmin.as<double>(), tmax.as<double>());
   launch(c, "k_group_bounds", k_group_bounds, dim3(div_up(ng * Kpad, 256)), dim3(256), 0, a2t.as<double>(), 1, V, Kpad,
          dok.as<uint8_t>(), gmin.as<double>(), gmax.as<double>());
-  const bool use_list = (double)ng * (double)ng * 8.0 <= 1.0e9;  // worst-case list fits 1 GB
+  const bool use_list = (double)ngs * (double)ng * 8.0 <= 1.0e9;  // worst-case list fits 1 GB
   if (!never && rows > 0 && use_list) {
     // culls over every (tile, group) into a compact list, then one warp per survivor
     DevBuf& list = c->ws[WS_PAIRLIST];
-    list.alloc((size_t)ng * ng * sizeof(unsigned long long), c->stream);
+    list.alloc((size_t)ngs * ng * sizeof(unsigned long long), c->stream);
     DevBuf nlist;
     nlist.alloc(sizeof(unsigned long long), c->stream);
     BZG_CHECK_CUDA(cudaMemsetAsync(nlist.ptr, 0, sizeof(unsigned long long), c->stream));
     const bool reg = R > 0;
-    launch(c, "k_tile_group_cull", k_tile_group_cull, dim3(div_up(ng, 256), (unsigned)ng), dim3(256), 0, bd,
-           tmin.as<double>(), tmax.as<double>(), gmin.as<double>(), gmax.as<double>(), ng, Kpad, rm, (int)reg,
+    launch(c, "k_tile_group_cull", k_tile_group_cull, dim3(div_up(ng, 256), (unsigned)ngs), dim3(256), 0, bd,
+           tmin.as<double>(), tmax.as<double>(), gmin.as<double>(), gmax.as<double>(), ng, Kpad, rms, (int)reg,
            list.as<unsigned long long>(), nlist.as<unsigned long long>());
     auto go = [&](auto kern, size_t smem) {
       ensure_dyn_smem((const void*)kern, smem);
       launch(c, "k_pair_list", kern, dim3((unsigned)(c->num_sms * 3)), dim3(kPairThreads), smem, bd,
-             a1c.as<double>(), a2t.as<double>(), sok.as<uint8_t>(), dok.as<uint8_t>(), perm.as<int>(),
-             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>(), rm,
-             list.as<unsigned long long>(), nlist.as<unsigned long long>());
+             a1c_src, a2t.as<double>(), ok_src, dok.as<uint8_t>(), perm.as<int>(),
+             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>(), rms,
+             list.as<unsigned long long>(), nlist.as<unsigned long long>(), perm_src, Vs);
     };
 #define BZG_K(k)                                                                                        \
   case k:                                                                                               \
@@ -1198,11 +1256,12 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     }
 #undef BZG_K
   } else if (!never && rows > 0) {
-    dim3 grid(div_up(V, kPairThreads), (unsigned)ng);
+    dim3 grid(div_up(V, kPairThreads), (unsigned)ngs);
     auto go = [&](auto kern) {
-      launch(c, "k_pair_tiles", kern, grid, dim3(kPairThreads), 0, bd, a1c.as<double>(), a2t.as<double>(),
-             sok.as<uint8_t>(), dok.as<uint8_t>(), perm.as<int>(), tmin.as<double>(), tmax.as<double>(),
-             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>(), rm);
+      launch(c, "k_pair_tiles", kern, grid, dim3(kPairThreads), 0, bd, a1c_src, a2t.as<double>(),
+             ok_src, dok.as<uint8_t>(), perm.as<int>(), tmin.as<double>(), tmax.as<double>(),
+             gmin.as<double>(), gmax.as<double>(), V, r0, W, bits.as<uint32_t>(), rowcnt.as<unsigned long long>(), rms,
+             perm_src, Vs);
     };
     const bool reg = R > 0;
 #define BZG_K(k) \

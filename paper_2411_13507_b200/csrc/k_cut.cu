@@ -820,6 +820,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
   BZG_REQUIRE(E < (1ll << 43), BZG_EUNSUPPORTED, "edge count too large for the QP work list");
   const int qp_rows = check_obstacles(n_obs, row_off, is_box, m);
   mk->g = g;
+  mk->ctx = c;
   mk->E = E;
   mk->n_obs = n_obs;
   mk->alive.alloc(std::max(E, 1ll), c->stream);
@@ -1136,6 +1137,7 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
     for (int o = 0; o < n_obs; ++o) canon_all = canon_all && h[o].canon != 0.0;
     Mask mk;
     mk.g = &g;
+    mk.ctx = c;
     mk.E = B;
     DevBuf &d_safe = c->ws[WS_QSAFE];
     dispatch_rows<Mc>(qp_rows, [&](auto C_) {
