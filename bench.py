@@ -554,7 +554,56 @@ def replanning_bench(args, ctx, stream, rank, world):
         "roofline": {"kernel": "k_bf_persistent", "bound": "latency", "achieved": None, "peak": None, "frac": None,
                      "traffic": None, "note": "a goal update is a few dependent small launches; latency-bound"},
     }
+    out["recut_moving_obstacle"] = recut_bench(ctx, stream, w, graph, steps=20)
     print(json.dumps(out), flush=True)
+
+
+def recut_bench(ctx, stream, w, graph, steps=20):
+    """Replanning with a moving obstacle (sim.py:324-330, ObstacleTrack.at): every cycle one of
+    the obstacles (round robin) is translated by a few cm and the graph is re-cut, then searched
+    (relaxed snap, as run_closed_loop mid-run).  Device ms per cycle, the full cut vs the re-cut
+    cache (BezierGraph.set_cut_cache), and whether the two masks agree on every cycle."""
+    import torch
+
+    from paper_2411_13507_b200 import graph as G
+    from paper_2411_13507_b200.geometry import Polytope
+
+    obs = list(w.obstacles)
+    m = w.spec.m
+
+    def lists():
+        cur = list(obs)
+        for k in range(steps):
+            o = k % len(obs)
+            A = np.asarray(cur[o].A, dtype=np.float64)
+            cur[o] = Polytope(A, np.asarray(cur[o].b, dtype=np.float64) + A @ np.full(m, 0.01 * (1 + k % 3)))
+            yield list(cur)
+
+    res, masks = {}, {}
+    for mode, cache in (("full", 0), ("cached", 4 * len(obs))):
+        graph.set_cut_cache(cache)
+        G.cut_graph(graph, obs)  # warm (and fill the cache with the static obstacles)
+        ms, ms_cut, ms_all = [], [], []
+        masks[mode] = []
+        for lst in lists():
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            c = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            mk = G.cut_graph(graph, lst)
+            b.record(stream)
+            G.find_path(graph, mk, w.start, w.goal, position_only_snap=True, require_tube_snap=False)
+            c.record(stream)
+            c.synchronize()
+            ms_cut.append(a.elapsed_time(b))
+            ms_all.append(a.elapsed_time(c))
+            masks[mode].append(np.packbits(mk.alive).tobytes() + mk.provenance_codes.tobytes())
+        res[mode] = {"cut_p50_ms": float(np.percentile(ms_cut, 50)), "cycle_p50_ms": float(np.percentile(ms_all, 50)),
+                     "cycle_p99_ms": float(np.percentile(ms_all, 99))}
+    graph.set_cut_cache(0)
+    res["masks_equal_every_cycle"] = masks["full"] == masks["cached"]
+    res["workload"] = f"{w.name}: one of {len(obs)} obstacles moves per cycle, {steps} cycles, cut + relaxed-snap search"
+    return res
 
 
 # ----------------------------------------------------------------------------- CPU baselines

@@ -148,6 +148,14 @@ int bzg_graph_with_edges(const bzg_graph* like, int64_t E, const int32_t* src, c
  * bzg_mask_copy and bzg_mask_export_device reject them with BZG_EINVAL. */
 int bzg_graph_set_edges(bzg_graph* g, int64_t E, const int32_t* src, const int32_t* dst, const double* cost,
                         int on_device);
+/* re-cut cache (device-resident replanning, sim.py:324-330): while max_obstacles > 0, every
+ * bzg_cut_graph on g keeps per-obstacle outcome bits (3 x E bits per obstacle) for up to
+ * max_obstacles distinct obstacles (least recently used evicted); obstacles seen before --
+ * same normalised rows, bounds and cut configuration, bit for bit -- are not screened or QP'd
+ * again, only recombined, so a replanning cycle in which a few obstacles moved costs the cut
+ * of those few.  The mask is identical to a full cut's; its QP records cover the QPs this
+ * call solved.  Lists longer than max_obstacles are cut without the cache.  0 = off. */
+int bzg_graph_set_cut_cache(bzg_graph* g, int32_t max_obstacles);
 int bzg_graph_destroy(bzg_graph* g);
 int bzg_graph_info(const bzg_graph* g, int64_t* V, int64_t* E, int64_t* row_begin, int64_t* row_end);
 /* host copies (BezierGraph fields, graph.py:61-68); any pointer may be NULL */

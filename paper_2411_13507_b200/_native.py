@@ -82,6 +82,7 @@ _SIGS = {
                               C.c_int, C.POINTER(_P)], C.c_int),
     "bzg_graph_with_edges": ([_P, C.c_int64, _P, _P, _P, C.c_int, C.POINTER(_P)], C.c_int),
     "bzg_graph_set_edges": ([_P, C.c_int64, _P, _P, _P, C.c_int], C.c_int),
+    "bzg_graph_set_cut_cache": ([_P, C.c_int32], C.c_int),
     "bzg_graph_destroy": ([_P], C.c_int),
     "bzg_graph_info": ([_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                         C.POINTER(C.c_int64)], C.c_int),

@@ -78,6 +78,7 @@ enum WsSlot {
   WS_KILL, WS_QKILL, WS_SAVED, WS_PEND, WS_GEN, WS_OBSGRID,          // cut screen
   WS_QX, WS_QZY, WS_QSAFE, WS_QLIST, WS_QCONST, WS_QRESUME, WS_QSTATUS, WS_QITERS, WS_QDELTA,             // Cut-QP
   WS_PLAN, WS_SSSP_PREV, WS_SSSP_PD, WS_SSSP_AUX, WS_SSSP_OUT,       // find_path
+  WS_CUTBITS, WS_CUTSLOTS,                                           // re-cut cache
   kWsSlots
 };
 
@@ -226,6 +227,25 @@ struct ScopedLibLaunch {
 inline unsigned div_up(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
 // ---------------------------------------------------------------- graph / mask
+// Re-cut cache of a graph (cut_graph_cached): per distinct obstacle (key = its rows, bounds and
+// the cut configuration, bit for bit) the three outcome bit rows of its last cut on this graph
+// -- heuristic kill, QP safe, QP unsafe -- and their popcounts; a re-cut then runs the screen
+// and the QPs only for obstacles it has not seen (the moved ones) and recombines the rest.
+struct CutCache {
+  int max_slots = 0;                       // 0: off
+  long long Wb = 0;                        // words per bit row = ceil(E / 32)
+  DevBuf pool;                             // max_slots x 3 x Wb uint32
+  std::unordered_map<std::string, int> slot_of;
+  std::vector<std::string> key_of;         // per slot ("" = free)
+  std::vector<long long> stamp;            // last use (LRU)
+  std::vector<long long> cnt;              // per slot: kill, qp safe, qp unsafe
+  long long clock = 0;
+  void clear() {
+    slot_of.clear();
+    for (auto& k : key_of) k.clear();
+  }
+};
+
 struct Graph {
   Ctx* ctx = nullptr;
   int m = 0, gamma = 0, p = 0, n = 0;
@@ -238,6 +258,7 @@ struct Graph {
   DevBuf cost;                    // E double
   DevBuf points;                  // lazily materialised E x m x (p+1)
   bool points_ready = false;
+  CutCache cut_cache;
 };
 
 struct Mask {

@@ -319,6 +319,19 @@ int bzg_graph_set_edges(bzg_graph* g, int64_t E, const int32_t* src, const int32
   });
 }
 
+int bzg_graph_set_cut_cache(bzg_graph* g, int32_t max_obstacles) {
+  return guarded([&] {
+    BZG_REQUIRE(g && max_obstacles >= 0, BZG_EINVAL, "bad argument");
+    set_device(g->ctx);
+    CutCache& cc = g->cut_cache;
+    cc.clear();
+    cc.max_slots = max_obstacles;
+    cc.Wb = 0;
+    cc.key_of.clear();
+    if (max_obstacles == 0) cc.pool.release();
+  });
+}
+
 int bzg_graph_destroy(bzg_graph* g) {
   return guarded([&] {
     if (!g) return;

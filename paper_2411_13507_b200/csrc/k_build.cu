@@ -1328,6 +1328,8 @@ void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, co
   g->row_begin = 0;
   g->row_end = g->V;
   g->points_ready = false;
+  g->cut_cache.clear();  // the cached cut outcomes belong to the old edge set
+  g->cut_cache.Wb = 0;
   g->src.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
   g->dst.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
   g->cost.alloc(std::max(E, 1ll) * sizeof(double), c->stream);

@@ -274,6 +274,19 @@ constexpr int kHeurThreads = 256, kHeurWarps = kHeurThreads / 32;  // (128 x 5 b
 // P_x - hi_x > ext + 0.01, so no point is inside (1), face +x is active at every anchor and
 // cleared, and every other face that could be active and is not cleared has separation at
 // most ext + 1e-6 < mn_x - hi_x -- canon_safe_cert (4) holds: code 1 without evaluating it.
+// Per-obstacle outcome bits of one cut (the re-cut cache, cut_graph_cached): bit e of row o
+// of `kill` = (edge e, obstacle o) heuristic code 0; of `qsafe` / `qunsafe` = the pair's
+// Cut-QP verdict.  kill == nullptr: not recorded.
+struct CutBits {
+  uint32_t* kill;
+  uint32_t* qsafe;
+  uint32_t* qunsafe;
+  long long Wb;  // words per obstacle row: ceil(E / 32)
+};
+__device__ __forceinline__ void set_bit(uint32_t* rowbase, long long Wb, int o, long long e) {
+  atomicOr(rowbase + (size_t)o * Wb + (e >> 5), 1u << (e & 31));
+}
+
 constexpr int kGridCells = 64;  // per axis
 struct ObsGrid {
   double x0, y0, inv_cx, inv_cy, R;  // grid origin, 1 / cell size, growth radius
@@ -365,7 +378,8 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
                                 unsigned long long* __restrict__ n_pend, unsigned long long cap,
                                 unsigned long long* __restrict__ pend, unsigned long long* __restrict__ n_gen,
                                 unsigned long long gen_cap, unsigned long long* __restrict__ gen_pend,
-                                const ObsGrid* __restrict__ grid, const unsigned long long* __restrict__ gmask) {
+                                const ObsGrid* __restrict__ grid, const unsigned long long* __restrict__ gmask,
+                                CutBits bits) {
   constexpr int N = G * M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const bool use_grid = grid != nullptr;  // the host passes the grid only when it is sparse
@@ -550,7 +564,10 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
           c0 += code == 0;
           c1 += code == 1;
           c2 += code == 2;
-          if (code == 0) atomicMin(s_kill + owner, o0 + oi);
+          if (code == 0) {
+            atomicMin(s_kill + owner, o0 + oi);
+            if (bits.kill) set_bit(bits.kill, bits.Wb, o0 + oi, e0 + owner);
+          }
           item = ((unsigned long long)(e0 + owner) << 20) | (unsigned long long)(o0 + oi);
         }
         warp_append(code == 2, item, n_pend, cap, pend);
@@ -604,7 +621,7 @@ __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const i
                               const unsigned long long* __restrict__ d_n, double margin,
                               int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                               unsigned long long* __restrict__ n_pend, unsigned long long cap,
-                              unsigned long long* __restrict__ pend, int8_t* __restrict__ code_out) {
+                              unsigned long long* __restrict__ pend, int8_t* __restrict__ code_out, CutBits bits) {
   constexpr int N = G * M;
   // n = min(*d_n, n_cap): the pair count of the screen, known on the device only
   const long long n = d_n ? ((long long)*d_n < n_cap ? (long long)*d_n : n_cap) : n_cap;
@@ -626,7 +643,10 @@ __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const i
       }
       control_points<G, M>(xi, xj, dp.D, P);
       code = general_code<G, M>(P, obs[oi], margin, kEpsGeo);
-      if (code == 0) atomicMin(first_kill + e, oi);
+      if (code == 0) {
+        atomicMin(first_kill + e, oi);
+        if (bits.kill) set_bit(bits.kill, bits.Wb, oi, e);
+      }
       if (code >= 0) atomicAdd(counters + code, 1ull);
       if (code == -1) atomicOr(counters + 7, 1ull);
       if (code_out) code_out[t] = (int8_t)code;
@@ -639,15 +659,22 @@ __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const i
 __global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long long n_cap,
                               const unsigned long long* __restrict__ d_n, const uint8_t* __restrict__ safe,
                               int* __restrict__ qp_kill, uint8_t* __restrict__ qp_saved,
-                              unsigned long long* __restrict__ counters) {
+                              unsigned long long* __restrict__ counters, CutBits bits) {
   const long long n = (long long)*d_n < n_cap ? (long long)*d_n : n_cap;
   unsigned long long s = 0, u = 0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
     const unsigned long long pk = pend[t];
     const long long e = (long long)(pk >> 20);
     const int o = (int)(pk & 0xFFFFF);
-    if (safe[t]) { qp_saved[e] = 1; ++s; }
-    else { atomicMin(qp_kill + e, o); ++u; }
+    if (safe[t]) {
+      qp_saved[e] = 1;
+      ++s;
+      if (bits.kill) set_bit(bits.qsafe, bits.Wb, o, e);
+    } else {
+      atomicMin(qp_kill + e, o);
+      ++u;
+      if (bits.kill) set_bit(bits.qunsafe, bits.Wb, o, e);
+    }
   }
   typedef cub::BlockReduce<unsigned long long, 256> BR;
   __shared__ typename BR::TempStorage tmp;
@@ -811,9 +838,11 @@ void dispatch_rows(int qp_rows, F&& f) {
 
 }  // namespace
 
-void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
-               const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
-               Mask* mk) {
+namespace {
+
+void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                    const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                    Mask* mk, CutBits cbits) {
   const long long E = g->E;
   const int m = g->m;
   BZG_REQUIRE(n_obs >= 0 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
@@ -963,7 +992,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       trace("qp");
       launch(c, "k_qp_verdicts", k_qp_verdicts, dim3((unsigned)std::min<long long>(div_up(qcap, 256), c->num_sms * 8ll)),
              dim3(256), 0, d_pend.as<unsigned long long>(), qcap, (const unsigned long long*)(dcnt + 5),
-             d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), dcnt);
+             d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), dcnt, cbits);
     };
     auto finalize_and_read = [&]() {
       launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, n_obs,
@@ -988,7 +1017,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
                g->src.as<int>(), g->dst.as<int>(), d_recs, d_cert, o0, o1, wmax[o0 / chunk], cfg->heur_margin,
                d_kill.as<int>(), dcnt,
                dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>(),
-               use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm);
+               use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm, cbits);
       }
       if (any_general) {
         // general obstacles: cut_heuristic past branch 1 over the device-side list, appending
@@ -997,7 +1026,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
                dim3((unsigned)std::min<long long>(div_up((long long)gen_cap, 64), c->num_sms * 16ll)), dim3(64), 0, dp,
                g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs, d_gen.as<unsigned long long>(),
                (long long)gen_cap, (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt,
-               dcnt + 5, cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr);
+               dcnt + 5, cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
       }
       trace("heuristic");
       run_qp_stage();
@@ -1012,6 +1041,7 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
+      if (cbits.kill) BZG_CHECK_CUDA(cudaMemsetAsync(cbits.kill, 0, (size_t)3 * n_obs * cbits.Wb * 4, c->stream));
     }
     long long n_inst = (long long)hcnt[5];
     if (n_inst > qcap) {
@@ -1021,6 +1051,8 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
       BZG_CHECK_CUDA(cudaMemcpyAsync(dcnt + 3, zero2, sizeof(zero2), cudaMemcpyHostToDevice, c->stream));
       BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
+      if (cbits.kill)  // QP verdict rows only: the kill rows of the screen stand
+        BZG_CHECK_CUDA(cudaMemsetAsync(cbits.qsafe, 0, (size_t)2 * n_obs * cbits.Wb * 4, c->stream));
       run_qp_stage();
       finalize_and_read();
     }
@@ -1053,6 +1085,202 @@ void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double
              d_pend.as<unsigned long long>(), n_inst, mk->qp_edge.as<long long>(), mk->qp_obs.as<int>());
     }
   });
+}
+
+// first obstacle (list position) whose bit row holds edge e, for the three rows of each slot
+__global__ void k_cut_combine(long long E, int n_obs, const uint32_t* __restrict__ pool, long long Wb,
+                              const int* __restrict__ slots, uint8_t* __restrict__ alive, uint8_t* __restrict__ prov) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const long long w = e >> 5;
+  const uint32_t bit = 1u << (e & 31);
+  int kh = n_obs, kq = n_obs;
+  bool saved = false;
+  for (int o = 0; o < n_obs; ++o) {
+    const uint32_t* base = pool + (size_t)slots[o] * 3 * Wb;
+    if (kh == n_obs && (base[w] & bit)) kh = o;
+    saved |= (base[Wb + w] & bit) != 0;
+    if (kq == n_obs && (base[2 * Wb + w] & bit)) kq = o;
+  }
+  const bool dead = kh < n_obs || kq < n_obs;  // as k_mask_finalize (graph.py:316-340)
+  alive[e] = dead ? 0 : 1;
+  prov[e] = dead ? (kh < kq ? BZG_HEURISTIC_UNSAFE : BZG_QP_UNSAFE) : (saved ? BZG_QP_SAFE : BZG_HEURISTIC_SAFE);
+}
+
+// popcounts of n_rows bit rows of Wb words into out[row]
+__global__ void k_row_popcount(const uint32_t* __restrict__ rows, long long Wb, unsigned long long* __restrict__ out) {
+  const uint32_t* r = rows + (size_t)blockIdx.x * Wb;
+  unsigned long long s = 0;
+  for (long long w = threadIdx.x; w < Wb; w += blockDim.x) s += __popc(r[w]);
+  typedef cub::BlockReduce<unsigned long long, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const unsigned long long t = BR(tmp).Sum(s);
+  if (threadIdx.x == 0) out[blockIdx.x] = t;
+}
+
+__global__ void k_remap_int(int* __restrict__ v, long long n, const int* __restrict__ map) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < n) v[t] = map[v[t]];
+}
+
+// The re-cut cache (CutCache, bzg_graph_set_cut_cache): obstacles already cut on this graph --
+// same rows, bounds and configuration, bit for bit -- contribute their stored outcome rows;
+// the others (moved obstacles in a replanning loop, sim.py:324-330) are cut now, as a sub-list,
+// recording their rows.  k_cut_combine then rebuilds alive / provenance in list order and the
+// counters are sums of per-obstacle popcounts, so the mask equals a full cut's.  The QP
+// records (qp_records) cover the QPs solved by this call.  Returns false when the list does
+// not fit the cache (the caller cuts without it).
+bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                      const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                      Mask* mk) {
+  CutCache& cc = g->cut_cache;
+  const long long E = g->E;
+  const int m = g->m;
+  const long long Wb = (E + 31) / 32;
+  if (n_obs > cc.max_slots || E <= 0) return false;
+  check_obstacles(n_obs, row_off, is_box, m);
+  if (cc.Wb != Wb || (int)cc.key_of.size() != cc.max_slots) {
+    cc.clear();
+    cc.Wb = Wb;
+    cc.key_of.assign(cc.max_slots, std::string());
+    cc.stamp.assign(cc.max_slots, 0);
+    cc.cnt.assign((size_t)cc.max_slots * 3, 0);
+    cc.pool.alloc((size_t)cc.max_slots * 3 * Wb * sizeof(uint32_t), c->stream);
+  }
+  // keys: the obstacle's normalised rows, bounds, box flag and the whole cut configuration
+  std::vector<std::string> keys(n_obs);
+  for (int o = 0; o < n_obs; ++o) {
+    const int r0 = row_off[o], r1 = row_off[o + 1];
+    std::string k;
+    k.append(reinterpret_cast<const char*>(cfg), sizeof(*cfg));
+    k.append(reinterpret_cast<const char*>(A + (size_t)r0 * m), (size_t)(r1 - r0) * m * sizeof(double));
+    k.append(reinterpret_cast<const char*>(b + r0), (size_t)(r1 - r0) * sizeof(double));
+    k.push_back((char)is_box[o]);
+    k.append(reinterpret_cast<const char*>(box_lo + (size_t)o * m), m * sizeof(double));
+    k.append(reinterpret_cast<const char*>(box_hi + (size_t)o * m), m * sizeof(double));
+    keys[o] = std::move(k);
+  }
+  ++cc.clock;
+  std::unordered_map<std::string, int> in_list;
+  for (int o = 0; o < n_obs; ++o) in_list.emplace(keys[o], o);
+  // misses: distinct keys not cached, in first-occurrence order
+  std::vector<int> miss;
+  {
+    std::unordered_map<std::string, int> seen;
+    for (int o = 0; o < n_obs; ++o) {
+      auto it = cc.slot_of.find(keys[o]);
+      if (it != cc.slot_of.end()) { cc.stamp[it->second] = cc.clock; continue; }
+      if (seen.emplace(keys[o], o).second) miss.push_back(o);
+    }
+  }
+  // slots for the misses: free slots first, then least recently used ones not in this list
+  std::vector<int> new_slot(miss.size());
+  for (size_t i = 0; i < miss.size(); ++i) {
+    int best = -1;
+    for (int sl = 0; sl < cc.max_slots; ++sl) {
+      const bool empty = cc.key_of[sl].empty();
+      if (!empty && (cc.stamp[sl] == cc.clock || in_list.count(cc.key_of[sl]))) continue;  // in use now
+      if (best < 0) { best = sl; continue; }
+      const bool best_empty = cc.key_of[best].empty();
+      if ((empty && !best_empty) || (empty == best_empty && cc.stamp[sl] < cc.stamp[best])) best = sl;
+    }
+    if (best < 0) return false;  // cannot happen while n_obs <= max_slots
+    if (!cc.key_of[best].empty()) cc.slot_of.erase(cc.key_of[best]);
+    cc.key_of[best] = keys[miss[i]];
+    cc.slot_of[keys[miss[i]]] = best;
+    cc.stamp[best] = cc.clock;
+    new_slot[i] = best;
+  }
+  mk->g = g;
+  mk->ctx = c;
+  mk->E = E;
+  mk->n_obs = n_obs;
+  mk->alive.alloc(std::max(E, 1ll), c->stream);
+  mk->prov.alloc(std::max(E, 1ll), c->stream);
+  mk->tree_key.release();
+  mk->reach_vg = -1;
+  mk->n_qp = 0;
+  const int nm = (int)miss.size();
+  if (nm > 0) {
+    // the misses as a sub-list, cut with their outcome rows recorded
+    std::vector<int32_t> sro(nm + 1, 0);
+    std::vector<double> sA, sb, slo, shi;
+    std::vector<uint8_t> sbox(nm);
+    for (int i = 0; i < nm; ++i) {
+      const int o = miss[i], r0 = row_off[o], r1 = row_off[o + 1];
+      sro[i + 1] = sro[i] + (r1 - r0);
+      sA.insert(sA.end(), A + (size_t)r0 * m, A + (size_t)r1 * m);
+      sb.insert(sb.end(), b + r0, b + r1);
+      sbox[i] = is_box[o];
+      slo.insert(slo.end(), box_lo + (size_t)o * m, box_lo + (size_t)(o + 1) * m);
+      shi.insert(shi.end(), box_hi + (size_t)o * m, box_hi + (size_t)(o + 1) * m);
+    }
+    DevBuf& tmp = c->ws[WS_CUTBITS];
+    tmp.alloc((size_t)3 * nm * Wb * sizeof(uint32_t), c->stream);
+    BZG_CHECK_CUDA(cudaMemsetAsync(tmp.ptr, 0, (size_t)3 * nm * Wb * sizeof(uint32_t), c->stream));
+    uint32_t* tk = tmp.as<uint32_t>();
+    CutBits bits{tk, tk + (size_t)nm * Wb, tk + (size_t)2 * nm * Wb, Wb};
+    cut_graph_impl(c, g, nm, sro.data(), sA.data(), sb.data(), sbox.data(), slo.data(), shi.data(), cfg, mk, bits);
+    // per-obstacle popcounts, the rows into their slots
+    DevBuf d_pc;
+    d_pc.alloc((size_t)3 * nm * sizeof(unsigned long long), c->stream);
+    launch(c, "k_row_popcount", k_row_popcount, dim3(3 * nm), dim3(256), 0, (const uint32_t*)tk, Wb,
+           d_pc.as<unsigned long long>());
+    for (int i = 0; i < nm; ++i)
+      for (int r = 0; r < 3; ++r)
+        BZG_CHECK_CUDA(cudaMemcpyAsync(cc.pool.as<uint32_t>() + ((size_t)new_slot[i] * 3 + r) * Wb,
+                                       tk + ((size_t)r * nm + i) * Wb, Wb * sizeof(uint32_t),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+    std::vector<unsigned long long> hpc(3 * nm);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(hpc.data(), d_pc.ptr, hpc.size() * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
+    // QP records: sub-list obstacle index -> its first position in the full list
+    if (mk->n_qp > 0) {
+      DevBuf d_map;
+      d_map.alloc(nm * sizeof(int), c->stream);
+      BZG_CHECK_CUDA(cudaMemcpyAsync(d_map.ptr, miss.data(), nm * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      launch(c, "k_remap_int", k_remap_int, dim3(div_up(mk->n_qp, 256)), dim3(256), 0, mk->qp_obs.as<int>(), mk->n_qp,
+             (const int*)d_map.as<int>());
+    }
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < nm; ++i)
+      for (int r = 0; r < 3; ++r) cc.cnt[(size_t)new_slot[i] * 3 + r] = (long long)hpc[(size_t)r * nm + i];
+  }
+  // recombine the whole list from the slots
+  std::vector<int> slots(n_obs);
+  for (int o = 0; o < n_obs; ++o) slots[o] = cc.slot_of.at(keys[o]);
+  DevBuf& d_slots = c->ws[WS_CUTSLOTS];
+  d_slots.alloc(n_obs * sizeof(int), c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(d_slots.ptr, slots.data(), n_obs * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  launch(c, "k_cut_combine", k_cut_combine, dim3(div_up(E, 256)), dim3(256), 0, E, n_obs,
+         (const uint32_t*)cc.pool.as<uint32_t>(), Wb, (const int*)d_slots.as<int>(), mk->alive.as<uint8_t>(),
+         mk->prov.as<uint8_t>());
+  long long kill = 0, qs = 0, qu = 0;
+  for (int o = 0; o < n_obs; ++o) {
+    kill += cc.cnt[(size_t)slots[o] * 3 + 0];
+    qs += cc.cnt[(size_t)slots[o] * 3 + 1];
+    qu += cc.cnt[(size_t)slots[o] * 3 + 2];
+  }
+  mk->counters[0] = E * (long long)n_obs;
+  mk->counters[1] = kill;
+  mk->counters[3] = qs + qu;
+  mk->counters[2] = mk->counters[0] - kill - (qs + qu);
+  mk->counters[4] = qs;
+  mk->counters[5] = qu;
+  // the host sync that returns counters to the caller is the mask read-back (stream-ordered)
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  return true;
+}
+
+}  // namespace
+
+void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+               const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+               Mask* mk) {
+  if (g->cut_cache.max_slots > 0 && n_obs > 0 &&
+      cut_graph_cached(c, g, n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg, mk))
+    return;
+  cut_graph_impl(c, g, n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg, mk, CutBits{});
 }
 
 // The reference's scalar entry points on explicit control-point sets: cut_heuristic
@@ -1125,7 +1353,7 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
       launch(c, "k_cut_general", k_cut_general<Gc, Mc>, dim3(div_up(B, 64)), dim3(64), 0, dp, g.vertices.as<double>(),
              g.src.as<int>(), g.dst.as<int>(), d_obs.as<Rec>(), d_items.as<unsigned long long>(), B,
              (const unsigned long long*)nullptr, cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5,
-             (unsigned long long)B, d_pend.as<unsigned long long>(), d_code.as<int8_t>());
+             (unsigned long long)B, d_pend.as<unsigned long long>(), d_code.as<int8_t>(), CutBits{});
       unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
       BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
       BZG_CHECK_CUDA(cudaMemcpyAsync(code_out, d_code.ptr, B, cudaMemcpyDeviceToHost, c->stream));

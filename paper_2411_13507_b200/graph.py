@@ -104,6 +104,13 @@ class BezierGraph:
         self._cache: dict = {}
         self._desc_fn = None  # rebuilds the bzg_build_desc this graph came from (eps_band)
 
+    def set_cut_cache(self, max_obstacles: int) -> None:
+        """Keep per-obstacle cut outcomes on the device for up to ``max_obstacles`` distinct
+        obstacles (bzg_graph_set_cut_cache): a later cut_graph on this graph screens and QPs only
+        the obstacles it has not seen -- the moved ones of a replanning loop -- and recombines the
+        rest; the mask equals a full cut's.  0 turns it off."""
+        nat.check(self._ctx.lib.bzg_graph_set_cut_cache(self._h, int(max_obstacles)))
+
     def eps_band(self, eps: float = 1e-11) -> dict:
         """North-star report: ordered pairs whose minimum constraint slack lies in (-eps, eps]
         (bzg_graph_eps_band), i.e. the pairs whose edge bit could flip under an eps change of

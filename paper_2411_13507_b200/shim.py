@@ -23,17 +23,31 @@ _PATCHED = ("build_graph", "cut_graph", "find_path", "path_cost", "cut_heuristic
 _saved: dict = {}
 
 
-def install(beziergraph_pkg) -> None:
-    """Patch ``beziergraph.graph`` (and the package re-exports) with the device functions."""
+def _build_with_cache(cut_cache):
+    def build_graph(N, spec, oracle, bounds, seed, include=None, k_nearest=None):
+        g = _dev.build_graph(N, spec, oracle, bounds, seed, include, k_nearest)
+        g.set_cut_cache(cut_cache)
+        return g
+    build_graph.__wrapped__ = _dev.build_graph
+    return build_graph
+
+
+def install(beziergraph_pkg, cut_cache: int = 0) -> None:
+    """Patch ``beziergraph.graph`` (and the package re-exports) with the device functions.
+
+    ``cut_cache`` > 0 turns on the re-cut cache of every graph built while installed
+    (BezierGraph.set_cut_cache): the simulator's re-cuts of a fixed graph (sim.py:324-330)
+    then screen and QP only the obstacles that moved.  The masks are identical either way."""
     gmod = beziergraph_pkg.graph
     if _saved:
         return
     for name in _PATCHED:
+        fn = _build_with_cache(cut_cache) if (name == "build_graph" and cut_cache > 0) else getattr(_dev, name)
         _saved[("graph", name)] = getattr(gmod, name)
-        setattr(gmod, name, getattr(_dev, name))
+        setattr(gmod, name, fn)
         if hasattr(beziergraph_pkg, name):
             _saved[("pkg", name)] = getattr(beziergraph_pkg, name)
-            setattr(beziergraph_pkg, name, getattr(_dev, name))
+            setattr(beziergraph_pkg, name, fn)
     _saved[("prov",)] = _dev._PROV_ENUM
     _dev._PROV_ENUM = gmod.CutProvenance
     _saved[("verdict",)] = _dev._VERDICT_ENUM

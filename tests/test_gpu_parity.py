@@ -327,3 +327,40 @@ def test_admm_schedules_iterates_bitwise(ctx, golden, name, monkeypatch):
             assert np.array_equal(r0[k], r[k]), (nm, k)
         assert r0["delta"].tobytes() == r["delta"].tobytes(), nm
         assert np.array_equal(m0.alive, m.alive) and np.array_equal(m0.provenance_codes, m.provenance_codes), nm
+
+
+def _moved(ob, t):
+    from paper_2411_13507_b200.geometry import Polytope
+
+    A = np.asarray(ob.A, dtype=np.float64)
+    return Polytope(A, np.asarray(ob.b, dtype=np.float64) + A @ np.asarray(t, dtype=np.float64))
+
+
+def _same_cut(a, b):
+    assert np.array_equal(a.alive, b.alive)
+    assert np.array_equal(a.provenance_codes, b.provenance_codes)
+    ca = [a.pairs_total, a.pairs_point_hit, a.pairs_hyperplane, a.pairs_qp, a.qp_safe, a.qp_unsafe]
+    cb = [b.pairs_total, b.pairs_point_hit, b.pairs_hyperplane, b.pairs_qp, b.qp_safe, b.qp_unsafe]
+    assert ca == cb, (ca, cb)
+
+
+@pytest.mark.parametrize("name", ["rf300_s5", "hop1500", "general60", "m3_600"])
+def test_recut_cache_equals_full_cut(ctx, golden, name):
+    """The re-cut cache (bzg_graph_set_cut_cache): a replanning sequence -- first cut, one obstacle
+    moved, obstacles reordered and duplicated, the first list again, a list larger than the cache
+    -- gives masks identical to uncached cuts of the same lists (alive, provenance, counters)."""
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+    ref = G.build_graph(*inputs_from_golden(g)[:6], ctx=ctx)  # same graph, no cache
+    m = gr.spec.m
+    moved = list(obstacles)
+    moved[0] = _moved(obstacles[0], np.full(m, 0.07))
+    lists = [list(obstacles), moved, moved[::-1] + moved[:1], list(obstacles)]
+    gr.set_cut_cache(len(obstacles) + 2)
+    for lst in lists:
+        _same_cut(G.cut_graph(gr, lst), G.cut_graph(ref, lst))
+    big = list(obstacles) + [_moved(o, np.full(m, -0.05)) for o in obstacles]  # larger than the cache
+    _same_cut(G.cut_graph(gr, big), G.cut_graph(ref, big))
+    _same_cut(G.cut_graph(gr, moved), G.cut_graph(ref, moved))
+    gr.set_cut_cache(0)
+    _same_cut(G.cut_graph(gr, moved), G.cut_graph(ref, moved))

@@ -38,8 +38,8 @@ def ref():
     pytest.skip("the reference package is neither at /root/reference nor in baseline/_ref")
 
 
-def _patched(ref, fn, *args, **kw):
-    shim.install(ref)
+def _patched(ref, fn, *args, cut_cache=0, **kw):
+    shim.install(ref, cut_cache=cut_cache)
     try:
         return fn(*args, **kw)
     finally:
@@ -119,6 +119,9 @@ def test_closed_loop_moving_obstacle_patched_equals_reference(ref):
     s = dataclasses.replace(base, obstacles=[base.obstacles[0], moving, base.obstacles[2]], timeout=2.0)
     t0 = ref.sim.run_closed_loop(s)
     t1 = _patched(ref, ref.sim.run_closed_loop, s)
+    t2 = _patched(ref, ref.sim.run_closed_loop, s, cut_cache=16)  # static obstacles reused
+    assert t2.cut_history == t0.cut_history and t2.states.tobytes() == t0.states.tobytes()
+    assert t2.final_path == t0.final_path
     assert len(t0.cut_history) == len(t1.cut_history) == 20
     assert t1.cut_history == t0.cut_history
     assert t1.events == t0.events
@@ -128,3 +131,30 @@ def test_closed_loop_moving_obstacle_patched_equals_reference(ref):
     assert t1.final_path == t0.final_path
     assert t1.summary() == t0.summary()
     _same_mask(t0.final_mask, t1.final_mask)
+
+
+def test_to_json_wire_formats_match_reference(ref, golden):
+    """BezierGraph.to_json / CutMask.to_json (graph.py:83-88, 115-126): the device objects'
+    wire formats equal the reference's on the same graph and mask (demo200 golden)."""
+    from paper_2411_13507_b200 import _native as nat
+    from paper_2411_13507_b200 import graph as G
+    from tests.helpers import inputs_from_golden
+
+    g = golden("demo200")
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    ctx = nat.Context(0)
+    gr = G.build_graph(N, spec, orc, bounds, seed, include, ctx=ctx)
+    mask = G.cut_graph(gr, obstacles)
+    rg = ref.graph
+    ref_spec = ref.BezierSpec(int(g["m"]), int(g["gamma"]), float(g["T"]))
+    ref_graph = rg.BezierGraph(spec=ref_spec, oracle=None, vertices=g["vertices"].copy(), edges=g["edges"].copy(),
+                               costs=g["costs"].copy(), edge_points=g["edge_points"].copy(), seed=int(g["seed"]),
+                               sample_bounds=None)
+    assert gr.to_json() == ref_graph.to_json()
+    assert gr.to_json(max_edges=100) == ref_graph.to_json(max_edges=100)
+    names = ["HEURISTIC_UNSAFE", "HEURISTIC_SAFE", "QP_SAFE", "QP_UNSAFE"]
+    prov = np.array([getattr(rg.CutProvenance, names[k]) for k in g["provenance"]], dtype=object)
+    c = [int(x) for x in g["counters"]]
+    ref_mask = rg.CutMask(alive=g["alive"].copy(), provenance=prov, pairs_total=c[0], pairs_point_hit=c[1],
+                          pairs_hyperplane=c[2], pairs_qp=c[3], qp_safe=c[4], qp_unsafe=c[5])
+    assert mask.to_json() == ref_mask.to_json()
