@@ -150,7 +150,7 @@ struct QpConsts {
 template <int G, int M, int C, bool CANON>
 __global__ void __launch_bounds__(128) k_qp_setup(QpParams qp, DParams dp, const double* __restrict__ Vx,
                                                   const int* __restrict__ src, const int* __restrict__ dst,
-                                                  const ObsRec<M>* __restrict__ obs,
+                                                  const ObsRec<M, obs_cap<C>()>* __restrict__ obs,
                                                   const unsigned long long* __restrict__ pend, long long n_inst,
                                                   const unsigned long long* __restrict__ d_n,
                                                   double* __restrict__ consts) {

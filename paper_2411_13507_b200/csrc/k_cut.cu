@@ -556,7 +556,8 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
   #pragma unroll
             for (int j = 0; j < 2 * G; ++j) Pq[k][j] = s_P[owner * NP + k * 2 * G + j];
           auto eval = [&](const ObsRec<M>& o) -> int {
-            if (o.is_box == 0.0) return any_inside_einsum<G, M>(Pq, o) ? 0 : 3;  // 3: decided by k_cut_general
+            if (o.is_box == 0.0)  // 3: decided by k_cut_general (all of it when the rows exceed the record)
+              return (o.rows <= (double)kObsRows && any_inside_einsum<G, M>(Pq, o)) ? 0 : 3;
             return o.canon != 0.0 ? box_code_canon<G, M>(Pq, o, margin) : box_code<G, M>(Pq, o, margin);
           };
           // two call sites so each reads its records with the address space known (LDS / LDG)
@@ -614,9 +615,9 @@ constexpr double kEpsGeo = 1e-9;  // geometry.EPS_GEO (geometry.py:14), closest_
 // one thread per pair.  Same bookkeeping as k_cut_heuristic: first kill by atomicMin, codes
 // counted, indeterminate pairs appended to the QP work list.  counters[7] flags an
 // obstacle whose projection QP certified it empty (the reference raises ValueError).
-template <int G, int M>
+template <int G, int M, int RC>
 __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const int* __restrict__ src,
-                              const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
+                              const int* __restrict__ dst, const ObsRec<M, RC>* __restrict__ obs,
                               const unsigned long long* __restrict__ gen, long long n_cap,
                               const unsigned long long* __restrict__ d_n, double margin,
                               int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
@@ -642,7 +643,7 @@ __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const i
         xj[k] = Vx[c * N + k];
       }
       control_points<G, M>(xi, xj, dp.D, P);
-      code = general_code<G, M>(P, obs[oi], margin, kEpsGeo);
+      code = general_code<G, M, RC>(P, obs[oi], margin, kEpsGeo);
       if (code == 0) {
         atomicMin(first_kill + e, oi);
         if (bits.kill) set_bit(bits.kill, bits.Wb, oi, e);
@@ -728,39 +729,41 @@ void dispatch_cut(int G, int M, F&& f) {
 #define BZG_GM(g, m) \
   if (G == g && M == m) { f(std::integral_constant<int, g>{}, std::integral_constant<int, m>{}); return; }
   BZG_GM(1, 1) BZG_GM(1, 2) BZG_GM(1, 3) BZG_GM(2, 1) BZG_GM(2, 2) BZG_GM(2, 3)
-  BZG_GM(3, 1) BZG_GM(3, 2) BZG_GM(3, 3)
+  BZG_GM(3, 1) BZG_GM(3, 2) BZG_GM(3, 3) BZG_GM(4, 1) BZG_GM(4, 2) BZG_GM(4, 3)
 #undef BZG_GM
-  throw Error(BZG_EUNSUPPORTED, "device cut supports gamma in 1..3 and m in 1..3");
+  throw Error(BZG_EUNSUPPORTED, "device cut supports gamma in 1..4 and m in 1..3");
 }
 
 // Device records of the obstacle list; rows normalised by the caller (geometry.py:135-137).
-template <int M>
-std::vector<ObsRec<M>> fill_obs(int n_obs, const int32_t* row_off, const double* A, const double* b,
-                                const uint8_t* is_box, const double* box_lo, const double* box_hi, double eps_geo) {
-  std::vector<ObsRec<M>> h(std::max(n_obs, 1));
+// RC = row capacity of the record (an obstacle with more rows keeps only `rows`, see ObsRec).
+template <int M, int RC = kObsRows>
+std::vector<ObsRec<M, RC>> fill_obs(int n_obs, const int32_t* row_off, const double* A, const double* b,
+                                    const uint8_t* is_box, const double* box_lo, const double* box_hi, double eps_geo) {
+  std::vector<ObsRec<M, RC>> h(std::max(n_obs, 1));
   for (int o = 0; o < n_obs; ++o) {
-    ObsRec<M>& r = h[o];
+    ObsRec<M, RC>& r = h[o];
     const int rows = row_off[o + 1] - row_off[o];
     r.rows = rows;
     r.is_box = is_box[o] ? 1.0 : 0.0;
-    for (int q = 0; q < kObsRows; ++q) {
+    const int kept = rows <= RC ? rows : 0;  // an over-capacity obstacle: rows only
+    for (int q = 0; q < RC; ++q) {
       const int row = row_off[o] + q;
       double s = 0.0;
       for (int k = 0; k < M; ++k) {
-        r.A[q][k] = q < rows ? A[(size_t)row * M + k] : 0.0;
+        r.A[q][k] = q < kept ? A[(size_t)row * M + k] : 0.0;
         const double sq = r.A[q][k] * r.A[q][k];
         s = k == 0 ? sq : s + sq;  // np.linalg.norm(axis=1): left fold of the squares
       }
-      r.norm2[q] = q < rows ? std::sqrt(s) : 1.0;
-      r.b[q] = q < rows ? b[row] : 1e300;
-      r.b_eps[q] = q < rows ? b[row] + eps_geo : 1e300;  // O.b + eps_geo (graph.py:234)
+      r.norm2[q] = q < kept ? std::sqrt(s) : 1.0;
+      r.b[q] = q < kept ? b[row] : 1e300;
+      r.b_eps[q] = q < kept ? b[row] + eps_geo : 1e300;  // O.b + eps_geo (graph.py:234)
     }
     for (int k = 0; k < M; ++k) {
       r.lo[k] = box_lo[(size_t)o * M + k];
       r.hi[k] = box_hi[(size_t)o * M + k];
     }
     bool canon = is_box[o] != 0;
-    for (int q = 0; q < 2 * M; ++q)
+    for (int q = 0; q < 2 * M && q < RC; ++q)
       for (int k = 0; k < M; ++k) canon = canon && r.A[q][k] == (k == (q % M) ? (q < M ? 1.0 : -1.0) : 0.0);
     r.canon = canon ? 1.0 : 0.0;
     for (int k = 0; k < M; ++k) {
@@ -816,24 +819,28 @@ std::vector<CertRec<M>> fill_cert(const std::vector<ObsRec<M>>& h, int n_obs, in
 }
 
 // Validates the obstacle list; returns the padded row count of a Cut-QP launch
-// (2m when every obstacle fits, else kObsRows).
+// (2m when every obstacle fits, else kObsRows, else kObsRowsBig).
 int check_obstacles(int n_obs, const int32_t* row_off, const uint8_t* is_box, int m) {
   int max_rows = 2 * m;
   for (int o = 0; o < n_obs; ++o) {
     const int rows = row_off[o + 1] - row_off[o];
-    BZG_REQUIRE(rows >= 1 && rows <= kObsRows, BZG_EUNSUPPORTED,
+    BZG_REQUIRE(rows >= 1 && rows <= kObsRowsBig, BZG_EUNSUPPORTED,
                 "obstacle " + std::to_string(o) + " has " + std::to_string(rows) + " rows; the device cut takes 1.." +
-                    std::to_string(kObsRows));
+                    std::to_string(kObsRowsBig));
     BZG_REQUIRE(!is_box[o] || rows == 2 * m, BZG_EINVAL, "box obstacle must have 2m rows");
     max_rows = std::max(max_rows, rows);
   }
-  return max_rows <= 2 * m ? 2 * m : kObsRows;
+  return max_rows <= 2 * m ? 2 * m : (max_rows <= kObsRows ? kObsRows : kObsRowsBig);
 }
 
 template <int M, typename F>
 void dispatch_rows(int qp_rows, F&& f) {
   if (qp_rows <= 2 * M) f(std::integral_constant<int, 2 * M>{});
-  else if constexpr (2 * M < kObsRows) f(std::integral_constant<int, kObsRows>{});
+  else if (qp_rows <= kObsRows) {
+    if constexpr (2 * M < kObsRows) f(std::integral_constant<int, kObsRows>{});
+  } else {
+    f(std::integral_constant<int, kObsRowsBig>{});
+  }
 }
 
 }  // namespace
@@ -894,6 +901,19 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
     BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs_all.ptr, hb.data(), hb.size(), cudaMemcpyHostToDevice, c->stream));
     const CertRec<Mc>* d_cert = d_obs_all.as<CertRec<Mc>>();
     const Rec* d_recs = reinterpret_cast<const Rec*>(static_cast<const unsigned char*>(d_obs_all.ptr) + cert_bytes);
+    // obstacles with more rows than the staged records: every obstacle also as a kObsRowsBig
+    // record, read by the general screen and by the Cut-QP (C = kObsRowsBig) of this cut
+    const bool big = qp_rows > kObsRows;
+    DevBuf d_obs_big;
+    if (big) {
+      const std::vector<ObsRec<Mc, kObsRowsBig>> hbig =
+          fill_obs<Mc, kObsRowsBig>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
+      d_obs_big.alloc(sizeof(ObsRec<Mc, kObsRowsBig>) * hbig.size(), c->stream);
+      BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs_big.ptr, hbig.data(), sizeof(ObsRec<Mc, kObsRowsBig>) * hbig.size(),
+                                     cudaMemcpyHostToDevice, c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));  // hbig leaves scope
+    }
+    const void* d_qp_obs = big ? d_obs_big.ptr : (const void*)d_recs;
     d_kill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_qkill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
     d_saved.alloc(std::max(E, 1ll), c->stream);
@@ -983,7 +1003,7 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
       d_qdl.alloc(qcap * sizeof(double), c->stream);
       dispatch_rows<Mc>(qp_rows, [&](auto C_) {
         constexpr int Cc = decltype(C_)::value;
-        QpJob job{g, {}, d_recs, canon_all, d_pend.as<unsigned long long>(), qcap, dcnt + 5, cfg,
+        QpJob job{g, {}, d_qp_obs, canon_all, d_pend.as<unsigned long long>(), qcap, dcnt + 5, cfg,
                   cfg->qp_polish ? 1 : 0, polish_screen(), mk, &d_safe, d_qst.as<int8_t>(), d_qit.as<int>(),
                   d_qdl.as<double>()};
         for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
@@ -1022,11 +1042,18 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
       if (any_general) {
         // general obstacles: cut_heuristic past branch 1 over the device-side list, appending
         // to the same QP work list
-        launch(c, "k_cut_general", k_cut_general<Gc, Mc>,
-               dim3((unsigned)std::min<long long>(div_up((long long)gen_cap, 64), c->num_sms * 16ll)), dim3(64), 0, dp,
-               g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs, d_gen.as<unsigned long long>(),
-               (long long)gen_cap, (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt,
-               dcnt + 5, cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
+        const long long gblocks = std::min<long long>(div_up((long long)gen_cap, 64), c->num_sms * 16ll);
+        if (big)
+          launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRowsBig>, dim3((unsigned)gblocks), dim3(64), 0, dp,
+                 g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(),
+                 (const ObsRec<Mc, kObsRowsBig>*)d_obs_big.ptr, d_gen.as<unsigned long long>(), (long long)gen_cap,
+                 (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5, cap,
+                 d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
+        else
+          launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRows>, dim3((unsigned)gblocks), dim3(64), 0, dp,
+                 g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs, d_gen.as<unsigned long long>(),
+                 (long long)gen_cap, (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt,
+                 dcnt + 5, cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
       }
       trace("heuristic");
       run_qp_stage();
@@ -1335,9 +1362,15 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
     using Rec = ObsRec<Mc>;
     const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
+    const bool big = qp_rows > kObsRows;
+    const std::vector<ObsRec<Mc, kObsRowsBig>> hbig =
+        big ? fill_obs<Mc, kObsRowsBig>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo)
+            : std::vector<ObsRec<Mc, kObsRowsBig>>();
     DevBuf d_obs, d_items;
-    d_obs.alloc(sizeof(Rec) * h.size(), c->stream);
-    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, h.data(), sizeof(Rec) * h.size(), cudaMemcpyHostToDevice, c->stream));
+    const size_t obytes = big ? sizeof(ObsRec<Mc, kObsRowsBig>) * hbig.size() : sizeof(Rec) * h.size();
+    d_obs.alloc(obytes, c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs.ptr, big ? (const void*)hbig.data() : (const void*)h.data(), obytes,
+                                   cudaMemcpyHostToDevice, c->stream));
     d_items.alloc(B * sizeof(unsigned long long), c->stream);
     BZG_CHECK_CUDA(cudaMemcpyAsync(d_items.ptr, items.data(), B * sizeof(unsigned long long), cudaMemcpyHostToDevice,
                                    c->stream));
@@ -1350,10 +1383,18 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
       BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 8 * sizeof(unsigned long long), c->stream));
       launch(c, "k_fill_int", k_fill_int, dim3(div_up(B, 256)), dim3(256), 0, d_kill.as<int>(), B, n_obs);
       unsigned long long* dcnt = d_cnt.as<unsigned long long>();
-      launch(c, "k_cut_general", k_cut_general<Gc, Mc>, dim3(div_up(B, 64)), dim3(64), 0, dp, g.vertices.as<double>(),
-             g.src.as<int>(), g.dst.as<int>(), d_obs.as<Rec>(), d_items.as<unsigned long long>(), B,
-             (const unsigned long long*)nullptr, cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5,
-             (unsigned long long)B, d_pend.as<unsigned long long>(), d_code.as<int8_t>(), CutBits{});
+      if (big)
+        launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRowsBig>, dim3(div_up(B, 64)), dim3(64), 0, dp,
+               g.vertices.as<double>(), g.src.as<int>(), g.dst.as<int>(), (const ObsRec<Mc, kObsRowsBig>*)d_obs.ptr,
+               d_items.as<unsigned long long>(), B, (const unsigned long long*)nullptr, cfg->heur_margin,
+               d_kill.as<int>(), dcnt, dcnt + 5, (unsigned long long)B, d_pend.as<unsigned long long>(),
+               d_code.as<int8_t>(), CutBits{});
+      else
+        launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRows>, dim3(div_up(B, 64)), dim3(64), 0, dp,
+               g.vertices.as<double>(), g.src.as<int>(), g.dst.as<int>(), d_obs.as<Rec>(),
+               d_items.as<unsigned long long>(), B, (const unsigned long long*)nullptr, cfg->heur_margin,
+               d_kill.as<int>(), dcnt, dcnt + 5, (unsigned long long)B, d_pend.as<unsigned long long>(),
+               d_code.as<int8_t>(), CutBits{});
       unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
       BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
       BZG_CHECK_CUDA(cudaMemcpyAsync(code_out, d_code.ptr, B, cudaMemcpyDeviceToHost, c->stream));

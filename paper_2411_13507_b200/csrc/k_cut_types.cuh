@@ -29,12 +29,14 @@ struct QpJob {
 void qp_solve_g1(Ctx* c, int M, int C, const QpJob& j);
 void qp_solve_g2(Ctx* c, int M, int C, const QpJob& j);
 void qp_solve_g3(Ctx* c, int M, int C, const QpJob& j);
+void qp_solve_g4(Ctx* c, int M, int C, const QpJob& j);
 inline void qp_solve(Ctx* c, int G, int M, int C, const QpJob& j) {
   switch (G) {
     case 1: qp_solve_g1(c, M, C, j); return;
     case 2: qp_solve_g2(c, M, C, j); return;
     case 3: qp_solve_g3(c, M, C, j); return;
-    default: throw Error(BZG_EUNSUPPORTED, "device cut supports gamma in 1..3");
+    case 4: qp_solve_g4(c, M, C, j); return;
+    default: throw Error(BZG_EUNSUPPORTED, "device cut supports gamma in 1..4");
   }
 }
 
@@ -44,17 +46,26 @@ struct DParams {
   double D[64];
 };
 
-// Rows an obstacle may have on device (boxes have 2m; general polytopes up to this).
+// Row capacities of the obstacle records: kObsRows for boxes and small polytopes (the records
+// the screen stages in shared memory), kObsRowsBig for the rest (convex hulls with many faces,
+// e.g. the paper's segmented obstacles): those take the general screen and a Cut-QP launch
+// with C = kObsRowsBig.  More rows: BZG_EUNSUPPORTED.
 constexpr int kObsRows = 8;
+constexpr int kObsRowsBig = 32;
+// record capacity a Cut-QP launch with C padded rows reads
+template <int C>
+constexpr int obs_cap() { return C > kObsRows ? kObsRowsBig : kObsRows; }
 
-// Per-obstacle record staged in shared memory.  Rows past `rows` are padding (A = 0,
-// b = 1e300): inert in every test and in the Cut-QP (k_qp_common.cuh).
-template <int M>
+// Per-obstacle record.  Rows past `rows` are padding (A = 0, b = 1e300): inert in every
+// test and in the Cut-QP (k_qp_common.cuh).  In an RC = kObsRows record of an obstacle with
+// more rows only `rows` (and is_box = 0) is meaningful: the screen sends its pairs to the
+// general path, which reads the kObsRowsBig record.
+template <int M, int RC = kObsRows>
 struct ObsRec {
-  double A[kObsRows][M];   // normalised rows (geometry.py:135-137)
-  double b[kObsRows];
-  double b_eps[kObsRows];  // fl(b + eps_geo)   (graph.py:234)
-  double norm2[kObsRows];  // row norms of the normalised rows (Polytope._row_norms of O)
+  double A[RC][M];         // normalised rows (geometry.py:135-137)
+  double b[RC];
+  double b_eps[RC];        // fl(b + eps_geo)   (graph.py:234)
+  double norm2[RC];        // row norms of the normalised rows (Polytope._row_norms of O)
   double lo[M], hi[M];     // Polytope.as_box bounds (geometry.py:155-185)
   double canon;            // 1 when A == [I; -I] exactly (Box.to_polytope row order)
   double act_hi[M];        // hi - 1e-6: a point below it cannot make face +k active

@@ -63,8 +63,8 @@ __device__ __forceinline__ double norm1d(const double* v) {  // np.linalg.norm o
 
 // closest_point(O, x) (geometry.py:202-230): x when inside, the clamp for boxes, else the
 // projection QP.  Returns false when the solver certifies infeasibility (the reference raises).
-template <int M>
-__device__ bool closest_point_general(const ObsRec<M>& o, const double (&x)[M], double eps, double (&y)[M]) {
+template <int M, int RC>
+__device__ bool closest_point_general(const ObsRec<M, RC>& o, const double (&x)[M], double eps, double (&y)[M]) {
   const int R = (int)o.rows;
   bool inside = true;
   for (int c = 0; c < R; ++c) inside &= gemv_row<M>(o.A[c], x) <= __dadd_rn(o.b[c], eps);
@@ -99,10 +99,10 @@ __device__ bool closest_point_general(const ObsRec<M>& o, const double (&x)[M], 
     for (int k = 0; k < r; ++k) d -= L[r][k] * L[r][k];
     L[r][r] = sqrt(d);
   }
-  double xs[M], z[kObsRows], yv[kObsRows];
+  double xs[M], z[RC], yv[RC];
 #pragma unroll
   for (int k = 0; k < M; ++k) xs[k] = 0.0;
-  for (int c = 0; c < kObsRows; ++c) { z[c] = 0.0; yv[c] = 0.0; }
+  for (int c = 0; c < RC; ++c) { z[c] = 0.0; yv[c] = 0.0; }
   double qn = 0.0;
 #pragma unroll
   for (int k = 0; k < M; ++k) qn = fmax(qn, fabs(2.0 * x[k]));
@@ -183,12 +183,12 @@ __device__ bool closest_point_general(const ObsRec<M>& o, const double (&x)[M], 
   if (status == BZG_INFEASIBLE) return false;
   // polish (qpsolver.py:236-279): equality solve on the rows with b - A x <= tol
   const double tol = fmax(1e-7, 10.0 * rp);
-  int act[kObsRows];
+  int act[RC];
   int k = 0;
   for (int c = 0; c < R; ++c)
     if (__dsub_rn(o.b[c], gemm_row<M>(o.A[c], xs)) <= tol) act[k++] = c;
   if (k > 0) {
-    constexpr int NK = M + kObsRows;
+    constexpr int NK = M + RC;
     const int nk = M + k;
     const double reg = 1e-8;
     double K0[NK][NK], U[NK][NK], rhs0[NK], w[NK];
@@ -276,8 +276,8 @@ __device__ bool closest_point_general(const ObsRec<M>& o, const double (&x)[M], 
 
 // cut_heuristic (graph.py:202-221) on the control points P (M x J): 0 unsafe, 1 safe, 2 indeterminate;
 // -1 when a projection QP certifies an empty polytope (the reference raises).
-template <int G, int M>
-__device__ int general_code(const double (&P)[M][2 * G], const ObsRec<M>& o, double margin, double eps) {
+template <int G, int M, int RC>
+__device__ int general_code(const double (&P)[M][2 * G], const ObsRec<M, RC>& o, double margin, double eps) {
   constexpr int J = 2 * G;
   const int R = (int)o.rows;
   // O.contains_many(pts.T, eps): gemm order
@@ -295,7 +295,7 @@ __device__ int general_code(const double (&P)[M][2 * G], const ObsRec<M>& o, dou
     double p[M], y[M], dv[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) p[k] = P[k][j];
-    if (!closest_point_general<M>(o, p, eps, y)) return -1;
+    if (!closest_point_general<M, RC>(o, p, eps, y)) return -1;
 #pragma unroll
     for (int k = 0; k < M; ++k) dv[k] = __dsub_rn(y[k], p[k]);
     const double dj = norm1d<M>(dv);

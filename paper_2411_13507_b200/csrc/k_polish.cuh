@@ -102,7 +102,7 @@ constexpr int polish_dim() { return 2 * G + C + 1; }  // core: J + C + 1
 template <int G, int M, int C>
 __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
     DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
-    const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
+    const ObsRec<M, obs_cap<C>()>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
     long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ zy,
     double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NC = J + C + 1;
@@ -142,19 +142,19 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
   auto hi_of = [&](int i) -> double { return i < C ? b[i < C ? i : 0] : (i < C + J ? INFINITY : 1.0); };
   // active set at z = A x (qpsolver.py:245-249)
   const double tol = fmax(1e-7, 10.0 * rp);
-  unsigned act = 0, atlo = 0;
+  unsigned long long act = 0, atlo = 0;  // MC = C + J + 1 rows: up to 41 with kObsRowsBig
 #pragma unroll
   for (int i = 0; i < MC; ++i) {
     const double zi = a_dot(i, x);
     const bool l_ = __dsub_rn(zi, lo_of(i)) <= tol, u_ = __dsub_rn(hi_of(i), zi) <= tol;
-    act |= (unsigned)(l_ || u_) << i;
-    atlo |= (unsigned)l_ << i;
+    act |= (unsigned long long)(l_ || u_) << i;
+    atlo |= (unsigned long long)l_ << i;
   }
   bool accept = false;
   double xp[NV];
   if (act) {
     const double reg = 1e-8, i2 = 1.0 / (2.0 + reg), e2 = reg / (1.0 + reg * reg), r2 = 1.0 / (1.0 + reg * reg);
-    auto a_on = [&](int i) -> bool { return act >> i & 1u; };
+    auto a_on = [&](int i) -> bool { return act >> i & 1ull; };
     // core slot of row/column r: r < J lambda_r (used iff lambda bound r inactive),
     // J <= r < J+C nu of obstacle row r-J, r = J+C nu of the sum row
     auto core_used = [&](int r) -> bool { return r < J ? !a_on(C + r) : (r < J + C ? a_on(r - J) : a_on(C + J)); };
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
 #pragma unroll
       for (int t = 0; t < NV; ++t) bx[t] = 0.0;  // -q = 0
 #pragma unroll
-      for (int i = 0; i < MC; ++i) bn[i] = a_on(i) ? ((atlo >> i & 1u) ? lo_of(i) : hi_of(i)) : 0.0;
+      for (int i = 0; i < MC; ++i) bn[i] = a_on(i) ? ((atlo >> i & 1ull) ? lo_of(i) : hi_of(i)) : 0.0;
       solve(bx, bn, wx, wn);
 #pragma unroll 1
       for (int rep = 0; rep < 2; ++rep) {
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
 template <int G, int M, int C>
 __device__ __forceinline__ void polish_one_reg(
     long long inst, const DParams& dp, const double* __restrict__ Vx, const int* __restrict__ src,
-    const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend,
+    const int* __restrict__ dst, const ObsRec<M, obs_cap<C>()>* __restrict__ obs, const unsigned long long* __restrict__ pend,
     double eps_cut, double* __restrict__ x_io, const double* __restrict__ zy, double* __restrict__ delta_out,
     uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NS = C + 1;
@@ -399,20 +399,20 @@ __device__ __forceinline__ void polish_one_reg(
   auto lo_of = [&](int i) -> double { return i < C ? -INFINITY : (i < C + J ? 0.0 : 1.0); };
   auto hi_of = [&](int i) -> double { return i < C ? b[i < C ? i : 0] : (i < C + J ? INFINITY : 1.0); };
   const double tol = fmax(1e-7, 10.0 * rp);
-  unsigned act = 0, atlo = 0;
+  unsigned long long act = 0, atlo = 0;  // MC = C + J + 1 rows: up to 41 with kObsRowsBig
 #pragma unroll
   for (int i = 0; i < MC; ++i) {
     const double zi = a_dot(i, x);
     const bool l_ = __dsub_rn(zi, lo_of(i)) <= tol, u_ = __dsub_rn(hi_of(i), zi) <= tol;
-    act |= (unsigned)(l_ || u_) << i;
-    atlo |= (unsigned)l_ << i;
+    act |= (unsigned long long)(l_ || u_) << i;
+    atlo |= (unsigned long long)l_ << i;
   }
   bool accept = false;
   double xp[NV];
   if (act) {
     const double reg = 1e-8, i2 = 1.0 / (2.0 + reg), e2 = reg / (1.0 + reg * reg), r2 = 1.0 / (1.0 + reg * reg);
     const double ireg = 1.0 / reg;
-    auto a_on = [&](int i) -> bool { return act >> i & 1u; };
+    auto a_on = [&](int i) -> bool { return act >> i & 1ull; };
     auto bound = [&](int j) -> bool { return a_on(C + j); };
     auto used = [&](int s) -> bool { return s < C ? a_on(s) : a_on(C + J); };  // nu slot s: obstacle row / sum row
     auto gs = [&](int s, int j) -> double { return s < C ? Q[s < C ? s : 0][j] : 1.0; };
@@ -519,7 +519,7 @@ __device__ __forceinline__ void polish_one_reg(
 #pragma unroll
     for (int t = 0; t < NV; ++t) bx[t] = 0.0;  // -q = 0
 #pragma unroll
-    for (int i = 0; i < MC; ++i) bn[i] = a_on(i) ? ((atlo >> i & 1u) ? lo_of(i) : hi_of(i)) : 0.0;
+    for (int i = 0; i < MC; ++i) bn[i] = a_on(i) ? ((atlo >> i & 1ull) ? lo_of(i) : hi_of(i)) : 0.0;
     solve(bx, bn, wx, wn);
 #pragma unroll 1
     for (int rep = 0; rep < 2; ++rep) {
@@ -575,7 +575,7 @@ __device__ __forceinline__ void polish_one_reg(
 template <int G, int M, int C>
 __global__ void __launch_bounds__(128) k_qp_polish_reg(
     DParams dp, const double* __restrict__ Vx, const int* __restrict__ src, const int* __restrict__ dst,
-    const ObsRec<M>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
+    const ObsRec<M, obs_cap<C>()>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
     const unsigned long long* __restrict__ n_list, double eps_cut, double* __restrict__ x_io,
     const double* __restrict__ zy, double* __restrict__ delta_out, uint8_t* __restrict__ safe_out,
     const int8_t* __restrict__ st) {

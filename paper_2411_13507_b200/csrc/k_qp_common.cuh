@@ -31,7 +31,8 @@ struct QpParams {
 
 // Q = A_O @ points (graph.py:276): BLAS product, FMA chain over the m output dimensions.
 template <int G, int M, int C>
-__device__ __forceinline__ void cut_q_matrix(const ObsRec<M>& o, const double (&P)[M][2 * G], double (&Q)[C][2 * G]) {
+__device__ __forceinline__ void cut_q_matrix(const ObsRec<M, obs_cap<C>()>& o, const double (&P)[M][2 * G],
+                                             double (&Q)[C][2 * G]) {
 #pragma unroll
   for (int c = 0; c < C; ++c)
 #pragma unroll
@@ -46,11 +47,11 @@ __device__ __forceinline__ void cut_q_matrix(const ObsRec<M>& o, const double (&
 template <int G, int M, int C>
 __device__ __forceinline__ void load_instance(const DParams& dp, const double* __restrict__ Vx,
                                               const int* __restrict__ src, const int* __restrict__ dst,
-                                              const ObsRec<M>* __restrict__ obs, unsigned long long pk,
+                                              const ObsRec<M, obs_cap<C>()>* __restrict__ obs, unsigned long long pk,
                                               double (&Q)[C][2 * G], double (&b)[C]) {
   constexpr int N = G * M;
   const long long e = (long long)(pk >> 20);
-  const ObsRec<M>& o = obs[(int)(pk & 0xFFFFF)];
+  const ObsRec<M, obs_cap<C>()>& o = obs[(int)(pk & 0xFFFFF)];
   double xi[N], xj[N], P[M][2 * G];
   const long long a = src[e], c = dst[e];
 #pragma unroll

@@ -27,7 +27,7 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
   const Graph* g = job.g;
   DParams dp{};
   for (int k = 0; k < 64; ++k) dp.D[k] = job.D[k];
-  const ObsRec<M>* d_obs = static_cast<const ObsRec<M>*>(job.d_obs);
+  const ObsRec<M, obs_cap<C>()>* d_obs = static_cast<const ObsRec<M, obs_cap<C>()>*>(job.d_obs);
   const bool canon = job.canon;
   const unsigned long long* d_pend = job.d_pend;
   const long long n_inst = job.n_inst;
@@ -86,15 +86,17 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
   // BZG_ADMM_LANES=1|2 forces a variant (A/B runs).
   const int lanes_env = std::getenv("BZG_ADMM_LANES") ? std::atoi(std::getenv("BZG_ADMM_LANES")) : 0;  // per call
   const long long resident = (long long)c->num_sms * 384;  // k_qp_admm: 3 blocks x 128 per SM
-  const bool two_ok = unit && !rel;
+  const bool two_ok = unit && !rel && C <= kObsRows;
   const bool two = two_ok && (lanes_env == 2 || (lanes_env == 0 && n_inst <= kAdmm2MaxPerLane * resident));
   if (two) {
-    auto admm2 = k_qp_admm2<G, M, C, false>;
-    if constexpr (C == 2 * M)
-      if (canon) admm2 = k_qp_admm2<G, M, C, true>;
-    const long long blocks2 = std::min<long long>(div_up(2 * n_inst, 128), (long long)c->num_sms * 16);
-    launch(c, "k_qp_admm", admm2, dim3((unsigned)blocks2), dim3(128), 0, qp, d_consts.as<double>(), n_inst,
-           d_next.as<unsigned long long>(), st_out, it_out, d_x.as<double>(), d_zy.as<double>(), d_n);
+    if constexpr (C <= kObsRows) {
+      auto admm2 = k_qp_admm2<G, M, C, false>;
+      if constexpr (C == 2 * M)
+        if (canon) admm2 = k_qp_admm2<G, M, C, true>;
+      const long long blocks2 = std::min<long long>(div_up(2 * n_inst, 128), (long long)c->num_sms * 16);
+      launch(c, "k_qp_admm", admm2, dim3((unsigned)blocks2), dim3(128), 0, qp, d_consts.as<double>(), n_inst,
+             d_next.as<unsigned long long>(), st_out, it_out, d_x.as<double>(), d_zy.as<double>(), d_n);
+    }
   } else {
     // main pass over the work list, then resume passes over the parked tails (AdmmPass):
     // BZG_ADMM_PASSES launches, the last one without parking; BZG_ADMM_DUMP is the live-lane
@@ -149,13 +151,15 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
     if (c->trace_on) std::fprintf(stderr, "[bzg cut] qp instances %lld, polished %lld\n", n_inst, n_list);
   }
   mk->n_polished = n_list;
-  if (polish_lu) {  // the shared-memory core LU (kept for A/B checks)
-    constexpr int NR = polish_dim<G, M, C>();
-    const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
-    ensure_dyn_smem((const void*)k_qp_polish<G, M, C>, psmem);
-    launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads), psmem,
-           dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(), n_list,
-           cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(), delta_out, d_safe.as<uint8_t>(), st_out);
+  if (polish_lu && C <= kObsRows) {  // the shared-memory core LU (kept for A/B checks)
+    if constexpr (C <= kObsRows) {
+      constexpr int NR = polish_dim<G, M, C>();
+      const size_t psmem = (size_t)(NR * NR + NR) * kPolishThreads * sizeof(double);
+      ensure_dyn_smem((const void*)k_qp_polish<G, M, C>, psmem);
+      launch(c, "k_qp_polish", k_qp_polish<G, M, C>, dim3(div_up(n_list, kPolishThreads)), dim3(kPolishThreads),
+             psmem, dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, d_list.as<int>(),
+             n_list, cfg->eps_cut, d_x.as<double>(), d_zy.as<double>(), delta_out, d_safe.as<uint8_t>(), st_out);
+    }
   } else {
     // persistent grid over the device-side list length (at most n_inst entries)
     const long long pblocks = std::min<long long>(div_up(n_inst, 128), (long long)c->num_sms * 8);
@@ -180,6 +184,9 @@ void BZG_QP_ENTRY(BZG_QP_G)(Ctx* c, int M, int C, const QpJob& job) {
   if (M == 2 && C == kObsRows) return qp_solve_t<G, 2, kObsRows>(c, job);
   if (M == 3 && C == 6) return qp_solve_t<G, 3, 6>(c, job);
   if (M == 3 && C == kObsRows) return qp_solve_t<G, 3, kObsRows>(c, job);
+  if (M == 1 && C == kObsRowsBig) return qp_solve_t<G, 1, kObsRowsBig>(c, job);
+  if (M == 2 && C == kObsRowsBig) return qp_solve_t<G, 2, kObsRowsBig>(c, job);
+  if (M == 3 && C == kObsRowsBig) return qp_solve_t<G, 3, kObsRowsBig>(c, job);
   throw Error(BZG_EUNSUPPORTED, "Cut-QP: unsupported (m, obstacle rows)");
 }
 

@@ -673,13 +673,90 @@ def case_m3g3():
             detail=True, goals=goals)
 
 
+def general_obstacles_big():
+    """Convex polygons with 10..32 faces (the paper's segmented obstacles are convex hulls with
+    many faces) plus one box, in the demo map."""
+    return [
+        _regular_polygon((2.5, 2.5), 0.45, 12, 0.3),
+        _regular_polygon((1.3, 3.7), 0.35, 32, 0.2),
+        _regular_polygon((3.7, 1.3), 0.40, 10, 0.1),
+        _regular_polygon((1.2, 1.6), 0.30, 20, 0.0),
+        _regular_polygon((3.6, 3.4), 0.38, 16, np.pi / 16),
+        rgeo.Box(np.array([2.2, 0.3]), np.array([2.7, 0.9])).to_polytope(),
+    ]
+
+
+def case_general_big():
+    """Graph golden with 10..32-face obstacles: the general heuristic and the Cut-QP beyond the
+    8-row records (build -> cut -> path with per-QP detail)."""
+    s = rsc.demo_scenario()
+    oracle = bg.build_oracle(s.spec, s.xd, s.u_bounds, s.tube)
+    capture("general_big60", 60, s.spec, oracle, s.sample_bounds, 11, np.array([s.start, s.goal]),
+            general_obstacles_big(), s.start, s.goal, full=True, detail=True)
+
+
+def case_heur_general_big():
+    """Scalar cut_heuristic / closest_point / adjacent_hyperplane on 10..32-face polygons."""
+    rng = np.random.default_rng(13)
+    obs = general_obstacles_big()[:5]
+    ctrs = [(2.5, 2.5), (1.3, 3.7), (3.7, 1.3), (1.2, 1.6), (3.6, 3.4)]
+    cfg = rg.CutConfig()
+    pts_l, oi_l, code_l, proj_l, hp_l = [], [], [], [], []
+    for i in range(300):
+        oi = i % len(obs)
+        O = obs[oi]
+        pts = np.asarray(ctrs[oi])[:, None] + rng.uniform(-0.9, 0.9, (2, 1)) + rng.uniform(-0.35, 0.35, (2, 4))
+        pts_l.append(pts)
+        oi_l.append(oi)
+        code_l.append({rg.CutVerdict.UNSAFE: 0, rg.CutVerdict.SAFE: 1, rg.CutVerdict.INDETERMINATE: 2}[
+            rg.cut_heuristic(pts, O, cfg)])
+        On = O.normalized()
+        proj_l.append(np.stack([rgeo.closest_point(On, p) for p in pts.T]))
+        try:
+            hp = rgeo.adjacent_hyperplane(On, pts[:, 0])
+            hp_l.append(np.concatenate([hp.normal, [hp.offset]]))
+        except ValueError:
+            hp_l.append(np.full(3, np.nan))
+    np.savez_compressed(OUT / "heur_general_big.npz", points=np.stack(pts_l), obstacle=np.array(oi_l, np.int32),
+                        codes=np.array(code_l, np.int8), projections=np.stack(proj_l), hyperplanes=np.stack(hp_l),
+                        obs_n=np.array([o.num_rows for o in obs], np.int32),
+                        obs_A=np.concatenate([o.A for o in obs]), obs_b=np.concatenate([o.b for o in obs]),
+                        env=json.dumps(env_info()))
+    print("heur_general_big:", np.bincount(np.array(code_l), minlength=3))
+
+
+def case_g4():
+    """gamma = 4 (degree 7, snap norm over n = 8 terms -> numpy's pairwise order): 2-D boxes
+    through build -> cut -> path."""
+    spec = bg.BezierSpec(m=2, gamma=4, T=1.0)
+    lo = np.array([0.0, 0.0, -1.5, -1.5, -4.0, -4.0, -20.0, -20.0])
+    hi = np.array([5.0, 5.0, 1.5, 1.5, 4.0, 4.0, 20.0, 20.0])
+    xd = rgeo.Box(lo, hi).to_polytope()
+    u = rgeo.Box(np.full(2, -200.0), np.full(2, 200.0))
+    tube = rsim.design_tube(spec, (24.0, 50.0, 35.0, 10.0), 0.02)
+    oracle = bg.build_oracle(spec, xd, u, tube)
+    sample = rgeo.Box(np.array([0.0, 0.0, -0.5, -0.5, -1.0, -1.0, -2.0, -2.0]),
+                      np.array([5.0, 5.0, 0.5, 0.5, 1.0, 1.0, 2.0, 2.0]))
+    obs = [rgeo.inflate(rsc._box_obstacle(c[0], c[1], w[0], w[1]).shape, tube.position_box(2))
+           for c, w in (((2.5, 2.5), (0.8, 0.8)), ((1.3, 3.6), (0.6, 0.5)), ((3.7, 1.4), (0.5, 0.7)))]
+    start = np.array([0.4, 0.4, 0, 0, 0, 0, 0, 0.0])
+    goal = np.array([4.6, 4.6, 0, 0, 0, 0, 0, 0.0])
+    rng = np.random.default_rng(21)
+    goals = np.zeros((16, 8))
+    goals[:, :2] = rng.uniform(0.3, 4.7, (16, 2))
+    goals[:, 2:4] = rng.uniform(-0.3, 0.3, (16, 2))
+    capture("g4_800", 800, spec, oracle, sample, 5, np.array([start, goal]), obs, start, goal, full=True,
+            detail=True, goals=goals)
+
+
 CASES = {"regions4": case_regions4, "general": case_general, "heur_general": case_heur_general, "knn": case_knn,
          "m3": case_m3, "m1": case_m1, "heur_general3": case_heur_general3,
          "regions4gap": lambda: case_regions4("regions4gap", [((0.0, 0.0), (2.4, 2.4)), ((2.6, 0.0), (5.0, 2.4)),
                                                               ((0.0, 2.6), (2.4, 5.0)), ((2.6, 2.6), (5.0, 5.0)),
                                                               ((1.5, 1.5), (3.5, 3.5))]), "demo": case_demo, "rf_small": case_rf_small, "hop_small": case_hop_small, "reject": case_reject,
          "cfg2": case_cfg2, "maze": case_maze, "cfg3": case_cfg3, "cfg5_10k": case_cfg5_10k,
-         "m3g3": case_m3g3}
+         "m3g3": case_m3g3, "general_big": case_general_big, "heur_general_big": case_heur_general_big,
+         "g4": case_g4}
 
 if __name__ == "__main__":
     which = sys.argv[1:] or list(CASES)

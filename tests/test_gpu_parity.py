@@ -18,7 +18,7 @@ from tests.helpers import assert_cut_parity, compare_cut, digest, inputs_from_go
 
 pytestmark = pytest.mark.gpu
 
-FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600", "m1_300", "m3g3_1500"]
+FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600", "m1_300", "m3g3_1500", "g4_800"]
 
 
 @pytest.fixture(scope="module")
@@ -277,10 +277,12 @@ def test_eps_band_counts(ctx, golden, name):
         assert gr.eps_band(1e-11)["band"] == int(g["eps_band_1e-11"])
 
 
-def test_full_state_snapping_pairwise_norm(ctx, golden):
-    """n = m*gamma = 9: the full-state snap norm follows numpy's pairwise summation (n >= 8),
-    so goal snapping and the resulting paths match the live reference on 24 goals."""
-    g = golden("m3g3_1500")
+@pytest.mark.parametrize("name", ["m3g3_1500", "g4_800"])
+def test_full_state_snapping_pairwise_norm(ctx, golden, name):
+    """n = m*gamma = 9 (m = 3, gamma = 3) and 8 (m = 2, gamma = 4): the full-state snap norm
+    follows numpy's pairwise summation (n >= 8), so goal snapping and the resulting paths match
+    the live reference on every goal."""
+    g = golden(name)
     gr, obstacles, start, goal = _build(g, ctx)
 
     class RefMask:

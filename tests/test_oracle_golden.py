@@ -12,7 +12,7 @@ import oracle
 from oracle.qp_ref import AdmmSettings
 from tests.helpers import digest, inputs_from_golden
 
-FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600", "m1_300", "m3g3_1500"]
+FULL = ["demo200", "rf300_s5", "hop1500", "reject400", "m3_600", "m1_300", "m3g3_1500", "g4_800"]
 
 
 @pytest.mark.parametrize("name", FULL)
