@@ -26,8 +26,11 @@
 namespace bzg {
 namespace {
 
-// k_qp_admm2 is chosen while n_inst <= kAdmm2MaxPerLane x (k_qp_admm's resident lanes)
-constexpr double kAdmm2MaxPerLane = 0.0;  // measured slower than k_qp_admm at every size; BZG_ADMM_LANES=2 forces it
+// k_qp_admm2 is chosen for work lists of at most kAdmm2MaxInst instances: every instance is
+// then a lone chain on its SM sub-partition and two lanes shorten it (cfg1: 0.195 -> 0.178 ms);
+// with more instances the extra shuffles and the redundant sums cost more than they save
+// (cfg2 0.57 -> 0.62 ms, cfg3 9.2 -> 12.7 ms).  BZG_ADMM_LANES=1|2 forces one.
+constexpr long long kAdmm2MaxInst = 4096;
 
 template <int G, int M, int C, bool CANON>
 __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* __restrict__ consts, long long n_inst,

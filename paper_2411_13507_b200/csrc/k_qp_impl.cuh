@@ -81,13 +81,11 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
   launch(c, "k_qp_setup", setup, dim3((unsigned)std::min<long long>(div_up(n_inst, 128), c->num_sms * 8ll)),
          dim3(128), 0, qp, dp, g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_obs, d_pend, n_inst, d_n,
          d_consts.as<double>());
-  // Lanes per instance: two when the work list is short against the resident lanes (the
-  // 500-iteration chains then set the time, and k_qp_admm2 halves them), else one.
-  // BZG_ADMM_LANES=1|2 forces a variant (A/B runs).
+  // Lanes per instance: two for very short work lists (kAdmm2MaxInst), else one.
   const int lanes_env = std::getenv("BZG_ADMM_LANES") ? std::atoi(std::getenv("BZG_ADMM_LANES")) : 0;  // per call
-  const long long resident = (long long)c->num_sms * 384;  // k_qp_admm: 3 blocks x 128 per SM
   const bool two_ok = unit && !rel && C <= kObsRows;
-  const bool two = two_ok && (lanes_env == 2 || (lanes_env == 0 && n_inst <= kAdmm2MaxPerLane * resident));
+  // the list length is known on the host when d_n is null, else the capacity bounds it
+  const bool two = two_ok && (lanes_env == 2 || (lanes_env == 0 && n_inst <= kAdmm2MaxInst));
   if (two) {
     if constexpr (C <= kObsRows) {
       auto admm2 = k_qp_admm2<G, M, C, false>;
