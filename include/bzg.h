@@ -223,6 +223,14 @@ int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start,
                   int require_tube_snap, int64_t* path_out, int64_t path_cap, int64_t* path_len,
                   double* dist_out);
 
+/* replaces sim._project_on_path (sim.py:220-239): the grid time tau = k h (k < (L-1) *
+ * steps_per_hop, steps_per_hop = round(T / h)) along the curve chain through the L path states
+ * (L, n) whose position is closest to state[:m]; first minimum, same arithmetic as the
+ * reference (bezier.py boundary_points / de_casteljau, 1-D norm).  L <= 1: 0. */
+int bzg_project_on_path(bzg_ctx* ctx, int32_t m, int32_t gamma, double T, const double* D, int64_t L,
+                        const double* path_states, double h, int32_t steps_per_hop, const double* state,
+                        double* best_t);
+
 /* ---- diagnostics (not a reference entry point) -------------------------- */
 /* sustained FP64 instruction issue rate (DFMA if use_fma else DADD), instructions/s:
  * the roofline denominator of the FP64-pipe-bound kernels (pair test, box cut, QP). */

@@ -79,6 +79,7 @@ enum WsSlot {
   WS_QX, WS_QZY, WS_QSAFE, WS_QLIST, WS_QCONST, WS_QRESUME, WS_QSTATUS, WS_QITERS, WS_QDELTA,             // Cut-QP
   WS_PLAN, WS_SSSP_PREV, WS_SSSP_PD, WS_SSSP_AUX, WS_SSSP_OUT,       // find_path
   WS_CUTBITS, WS_CUTSLOTS,                                           // re-cut cache
+  WS_PROJ,                                                           // project_on_path
   kWsSlots
 };
 
@@ -300,6 +301,8 @@ void cut_points(Ctx* c, int m, int J, long long B, const double* points, const i
                 const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
                 const double* box_hi, const bzg_cut_config* cfg, int mode, int8_t* code_out, double* delta_out,
                 int8_t* status_out);
+double project_on_path(Ctx* c, int m, int gamma, double T, const double* D, long long L, const double* path_states,
+                       double h, int spt, const double* state);
 void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
                const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
                double* dist);

@@ -555,6 +555,16 @@ int bzg_mask_export_device(bzg_mask* mk, uint8_t* alive, uint8_t* provenance) {
   });
 }
 
+int bzg_project_on_path(bzg_ctx* ctx, int32_t m, int32_t gamma, double T, const double* D, int64_t L,
+                        const double* path_states, double h, int32_t steps_per_hop, const double* state,
+                        double* best_t) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && D && state && best_t && (L == 0 || path_states), BZG_EINVAL, "null argument");
+    set_device(ctx);
+    *best_t = project_on_path(ctx, m, gamma, T, D, L, path_states, h, steps_per_hop, state);
+  });
+}
+
 int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start, const double* goal,
                   const double* tube_lo, const double* tube_hi, double eps_geo, int position_only_snap,
                   int require_tube_snap, int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out) {

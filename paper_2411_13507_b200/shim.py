@@ -48,6 +48,12 @@ def install(beziergraph_pkg, cut_cache: int = 0) -> None:
         if hasattr(beziergraph_pkg, name):
             _saved[("pkg", name)] = getattr(beziergraph_pkg, name)
             setattr(beziergraph_pkg, name, fn)
+    sim = getattr(beziergraph_pkg, "sim", None)
+    if sim is not None and hasattr(sim, "_project_on_path"):  # sim.py:220-239 -> device
+        from . import replan
+
+        _saved[("sim", "_project_on_path")] = sim._project_on_path
+        sim._project_on_path = replan.project_on_path
     _saved[("prov",)] = _dev._PROV_ENUM
     _dev._PROV_ENUM = gmod.CutProvenance
     _saved[("verdict",)] = _dev._VERDICT_ENUM
@@ -61,6 +67,8 @@ def uninstall(beziergraph_pkg) -> None:
             setattr(gmod, key[1], fn)
         elif key[0] == "pkg":
             setattr(beziergraph_pkg, key[1], fn)
+        elif key[0] == "sim":
+            setattr(beziergraph_pkg.sim, key[1], fn)
         elif key[0] == "prov":
             _dev._PROV_ENUM = fn
         elif key[0] == "verdict":

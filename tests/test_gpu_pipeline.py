@@ -158,3 +158,28 @@ def test_to_json_wire_formats_match_reference(ref, golden):
     ref_mask = rg.CutMask(alive=g["alive"].copy(), provenance=prov, pairs_total=c[0], pairs_point_hit=c[1],
                           pairs_hyperplane=c[2], pairs_qp=c[3], qp_safe=c[4], qp_unsafe=c[5])
     assert mask.to_json() == ref_mask.to_json()
+
+
+def test_project_on_path_matches_reference(ref, golden):
+    """replan.project_on_path (bzg_project_on_path) vs the reference's sim._project_on_path
+    (sim.py:220-239) on paths of the demo graph and random vehicle states: the same grid time,
+    bit for bit (gamma = 2 and the gamma = 3 hop1500 graph)."""
+    from paper_2411_13507_b200 import replan
+
+    rng = np.random.default_rng(3)
+    for name, spec_args, hs in (("demo200", (2, 2, 1.0), (0.1, 0.05, 0.2)), ("hop1500", (2, 3, 1.0), (0.1, 0.25))):
+        g = golden(name)
+        spec = ref.BezierSpec(*spec_args)
+        V = g["vertices"]
+        path = np.asarray(g["path"], dtype=np.int64)
+        n_cases = 0
+        for h in hs:
+            for L in (1, 2, 3, len(path)):
+                states = V[path[:L]]
+                for _ in range(12):
+                    x = V[rng.integers(0, V.shape[0])] + rng.normal(0, 0.2, V.shape[1])
+                    want = ref.sim._project_on_path(states, spec, h, x)
+                    got = replan.project_on_path(states, spec, h, x)
+                    assert got == want, (name, h, L, got, want)
+                    n_cases += 1
+        assert n_cases > 50
