@@ -190,6 +190,9 @@ struct AdmmPass {
   int* rq_out;                     // parked instances of this pass (n_inst capacity)
   unsigned long long* rq_out_n;
   int dump_below;                  // 0: never park
+  int park_after;                  // > 0: park every instance still running after this many
+                                   // iterations (longest-last schedule: the next pass runs the
+                                   // long ones together); its lane takes new work
 };
 
 // REL: eps_rel != 0 (termination tolerances depend on the iterate, qpsolver.py:181-186)
@@ -242,6 +245,31 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
         qb = __shfl_sync(0xffffffffu, qb, leader);
         if (inst >= 0) pass.rq_out[qb + __popc(live & ((1u << lane) - 1u))] = (int)inst;
         inst = -2;
+      }
+    }
+    if (pass.park_after > 0) {
+      const bool park = inst >= 0 && it >= pass.park_after;
+      const unsigned pk = __ballot_sync(0xffffffffu, park);
+      if (pk) {
+        if (park) {
+          double* xo = x_out + inst * NV;
+          double* zo = zy_out + inst * 2 * MC;
+#pragma unroll
+          for (int j = 0; j < J; ++j) { xo[j] = lam[j]; zo[C + j] = zl[j]; zo[MC + C + j] = yl[j]; }
+#pragma unroll
+          for (int c = 0; c < C; ++c) { xo[J + c] = del[c]; zo[c] = zc[c]; zo[MC + c] = yc[c]; }
+          zo[MC - 1] = ze;
+          zo[2 * MC - 1] = ye;
+          it_out[inst] = it;
+        }
+        const int leader = __ffs(pk) - 1;
+        unsigned long long qb = 0;
+        if (lane == leader) qb = atomicAdd(pass.rq_out_n, (unsigned long long)__popc(pk));
+        qb = __shfl_sync(0xffffffffu, qb, leader);
+        if (park) {
+          pass.rq_out[qb + __popc(pk & ((1u << lane) - 1u))] = (int)inst;
+          inst = -1;  // this lane takes new work
+        }
       }
     }
     // ---- refill lanes whose instance terminated (one atomic per warp)

@@ -103,6 +103,9 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
     // (cfg2: 0.57 ms in one pass, 0.73-0.96 ms with 2-6 passes).
     const int passes = std::max(1, std::getenv("BZG_ADMM_PASSES") ? std::atoi(std::getenv("BZG_ADMM_PASSES")) : 1);
     const int dump = std::getenv("BZG_ADMM_DUMP") ? std::atoi(std::getenv("BZG_ADMM_DUMP")) : 12;
+    // BZG_ADMM_BUDGET=C: the first pass parks every instance still running after C iterations
+    // (the long ones then run together in the next pass)
+    const int budget = std::getenv("BZG_ADMM_BUDGET") ? std::atoi(std::getenv("BZG_ADMM_BUDGET")) : 0;
     DevBuf& d_rq = c->ws[WS_QRESUME];
     d_rq.alloc((passes > 1 ? 2 * n_inst : 1) * sizeof(int) + 4 * sizeof(unsigned long long), c->stream);
     unsigned long long* qn = reinterpret_cast<unsigned long long*>(d_rq.as<char>() + (passes > 1 ? 2 * n_inst : 1) * sizeof(int));
@@ -120,7 +123,8 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
         pass.rq_out = (ps & 1) ? q1 : q0;
         pass.rq_out_n = qn + ((ps & 1) ? 1 : 0);
         if (ps > 0) BZG_CHECK_CUDA(cudaMemsetAsync(pass.rq_out_n, 0, sizeof(unsigned long long), c->stream));
-        pass.dump_below = dump;
+        pass.dump_below = budget > 0 ? 0 : dump;
+        if (ps == 0) pass.park_after = budget;
       }
       launch(c, ps == 0 ? "k_qp_admm" : "k_qp_admm_tail", admm, dim3((unsigned)blocks), dim3(128), 0, qp,
              d_consts.as<double>(), n_inst, d_next.as<unsigned long long>(), st_out, it_out, d_x.as<double>(),
