@@ -328,6 +328,8 @@ __global__ void k_plan(long long* __restrict__ plan, long long* __restrict__ tre
   if (plan[2] && tree_key) *tree_key = v0;  // the tree built below is the cache from now on
 }
 
+// mode 3 (k_bf_async): in-queue flags (stamp) 0 but v0, ring queue slot 0 = v0 + 1 (qa holds
+//   the Q ring slots, zeroed by the caller), 64-bit head / tail / pending counters in counts;
 // mode 1 (k_bf_persistent): stamps -1 but v0, frontier queue = [v0], counts = {1, 0, ...};
 // mode 2 (k_bf_scan): prev = dist, frontier queue = [v0], counts = {1, 0, ...}.
 __global__ void k_init_tree(long long V, const long long* __restrict__ plan, int mode,
@@ -337,15 +339,99 @@ __global__ void k_init_tree(long long V, const long long* __restrict__ plan, int
   if (!plan[2]) return;
   const long long v0 = plan[1];
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < 8) counts[i] = (i == 0) ? 1 : 0;
-  if (i == 0 && mode != 0) qa[0] = (int)v0;
+  if (mode == 3) {
+    unsigned long long* c64 = reinterpret_cast<unsigned long long*>(counts);
+    if (i == 0) { c64[0] = 0; c64[1] = 1; c64[2] = 1; c64[3] = 0; qa[0] = (int)v0 + 1; }  // head, tail, pending
+  } else {
+    if (i < 8) counts[i] = (i == 0) ? 1 : 0;
+    if (i == 0 && mode != 0) qa[0] = (int)v0;
+  }
   if (i >= V) return;
   const unsigned long long d = i == v0 ? 0ull : kInfBits;
   dist[i] = d;
   if (mode == 1) stamp[i] = i == v0 ? 0 : -1;
+  if (mode == 3) stamp[i] = i == v0 ? 1 : 0;
   if (mode == 2) prev[i] = d;
   parent[i] = 0x7fffffff;
   pd[i] = ~0ull;
+}
+
+// Bellman-Ford without barriers: the same fixed point by asynchronous relaxation.  A ring queue
+// of vertices whose distance dropped (each at most once at a time: the in-queue flag), one warp
+// per popped vertex relaxing its alive out-edges with returning atomicMin, improved targets
+// pushed back (warp-aggregated); `pending` counts pushed-but-unfinished items, and the kernel
+// ends when it reaches zero.  Relaxation order does not matter: every d[v] only ever decreases
+// to min over paths of the left-fold fl sums, which is what the sweeps reach too.
+// Ordering: a popper clears the flag, fences, then reads d[v]; a pusher lowers d[w], fences,
+// then tests the flag -- so a drop after the read always re-enqueues the vertex.
+__global__ void k_bf_async(long long V, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
+                           const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                           unsigned long long* __restrict__ dist, int* __restrict__ inq, int* __restrict__ ring,
+                           unsigned long long* __restrict__ ctr, long long Q, const long long* __restrict__ plan) {
+  if (!plan[2]) return;
+  const int lane = threadIdx.x & 31;
+  volatile int* vring = ring;
+  volatile unsigned long long* vpend = ctr + 2;
+  while (true) {
+    unsigned long long h = 0;
+    if (lane == 0) h = atomicAdd(ctr + 0, 1ull);
+    h = __shfl_sync(0xffffffffu, h, 0);
+    const long long slot = (long long)(h % (unsigned long long)Q);
+    int v = -1;
+    while (true) {  // wait for index h to be published, or for the end
+      int sv = 0;
+      if (lane == 0) sv = vring[slot];
+      sv = __shfl_sync(0xffffffffu, sv, 0);
+      if (sv != 0) { v = sv - 1; break; }
+      unsigned long long pd = 0;
+      if (lane == 0) pd = *vpend;
+      pd = __shfl_sync(0xffffffffu, pd, 0);
+      if (pd == 0) return;
+      __nanosleep(64);
+    }
+    if (lane == 0) {
+      vring[slot] = 0;
+      atomicExch(inq + v, 0);
+      __threadfence();
+    }
+    __syncwarp();
+    const double du = __longlong_as_double((long long)atomicAdd(dist + v, 0ull));
+    const long long e1 = row_ptr[v + 1];
+    for (long long e = row_ptr[v] + lane; e - lane < e1; e += 32) {
+      bool push = false;
+      int w = 0;
+      if (e < e1 && (!alive || alive[e])) {
+        w = dst[e];
+        const unsigned long long nb = dbits(__dadd_rn(du, cost[e]));
+        if (nb < __ldcg(dist + w)) {
+          const unsigned long long old = atomicMin(dist + w, nb);
+          if (nb < old) {
+            __threadfence();
+            push = atomicExch(inq + w, 1) == 0;
+          }
+        }
+      }
+      const unsigned want = __ballot_sync(0xffffffffu, push);
+      if (want) {
+        const int leader = __ffs(want) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) {
+          atomicAdd(ctr + 2, (unsigned long long)__popc(want));  // pending first, then publish
+          base = atomicAdd(ctr + 1, (unsigned long long)__popc(want));
+        }
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (push) {
+          const unsigned long long t = base + __popc(want & ((1u << lane) - 1u));
+          vring[(long long)(t % (unsigned long long)Q)] = w + 1;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(ctr + 2, ~0ull);  // this item is done (-1)
+    }
+  }
 }
 
 // parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes)
@@ -529,10 +615,20 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   // scan-and-relax variant (each sweep rescans every vertex and relaxes the changed ones in
   // place) was slower: cfg3 0.39, cfg5 100k 3.6 ms.
   const char* bf_env = std::getenv("BZG_BF_IMPL");
-  const int mode = bf_env ? (std::string(bf_env) == "queue" ? 1 : 2) : (V < 4096 ? 1 : 2);
+  const std::string bfs = bf_env ? std::string(bf_env) : std::string();
+  const int mode = bfs == "queue" ? 1 : (bfs == "scan" ? 2 : (bfs == "async" ? 3 : (V < 4096 ? 1 : 2)));
+  const long long Q = V + 8192 + 64;  // ring: <= V queued (flags) + claimed-unread (one per warp)
+  if (mode == 3) {
+    t_aux.alloc((8 + (size_t)std::max(V, 1ll) + (size_t)Q) * sizeof(int), c->stream);
+    counts = t_aux.as<int>();
+    stamp = counts + 8;
+    qa = stamp + V;
+    BZG_CHECK_CUDA(cudaMemsetAsync(qa, 0, (size_t)Q * sizeof(int), c->stream));
+  }
   launch(c, "k_init_tree", k_init_tree, dim3(div_up(std::max(V, 8ll), 256)), dim3(256), 0, V, (const long long*)plan,
          mode, dist, t_prev.as<unsigned long long>(), stamp, parent, t_pd.as<unsigned long long>(), counts, qa);
-  const void* bf_kern = mode == 1 ? (const void*)k_bf_persistent : (const void*)k_bf_scan;
+  const void* bf_kern = mode == 1 ? (const void*)k_bf_persistent
+                                  : (mode == 3 ? (const void*)k_bf_async : (const void*)k_bf_scan);
   int per_sm = 0;
   BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_kern, 256, 0));
   static const int bf_per_sm_env =
@@ -551,6 +647,9 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   if (mode == 1) {
     void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &stamp, &qa, &qb, &counts, &maxs, &cplan};
     launch_coop(c, "k_bf_persistent", bf_kern, dim3(blocks), dim3(256), args);
+  } else if (mode == 3) {
+    launch(c, "k_bf_async", k_bf_async, dim3(blocks), dim3(256), 0, Vl, rp, dd, cc, alive, dist, stamp, qa,
+           reinterpret_cast<unsigned long long*>(counts), Q, cplan);
   } else {
     void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &pv, &qa, &qb, &counts, &maxs, &cplan};
     launch_coop(c, "k_bf_scan", bf_kern, dim3(blocks), dim3(256), args);

@@ -366,3 +366,29 @@ def test_recut_cache_equals_full_cut(ctx, golden, name):
     _same_cut(G.cut_graph(gr, moved), G.cut_graph(ref, moved))
     gr.set_cut_cache(0)
     _same_cut(G.cut_graph(gr, moved), G.cut_graph(ref, moved))
+
+
+@pytest.mark.parametrize("impl", ["queue", "scan", "async"])
+@pytest.mark.parametrize("name", ["cfg2_rf2000", "maze", "hop1500"])
+def test_bellman_ford_variants_reach_the_reference_paths(ctx, golden, name, impl, monkeypatch):
+    """Every Bellman-Ford schedule (frontier queue, rescan, barrier-free asynchronous) reaches the
+    same fixed point: the paths (and costs) through the reference's own mask are the golden's,
+    and so are the cfg4 goal updates (cfg2)."""
+    monkeypatch.setenv("BZG_BF_IMPL", impl)
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+
+    class RefMask:
+        alive = g["alive"]
+
+    path = G.find_path(gr, RefMask(), start, goal)
+    assert path == (None if bool(g["path_none"]) else list(g["path"]))
+    if path:
+        assert G.path_cost(gr, path) == float(g["path_cost"])
+    if "goals" in g:
+        lens, flat = g["goal_path_len"], g["goal_paths"]
+        off = 0
+        for k, gl in enumerate(g["goals"][:40]):
+            p = G.find_path(gr, RefMask(), start, gl)
+            assert (p or []) == list(flat[off:off + lens[k]]), k
+            off += lens[k]
