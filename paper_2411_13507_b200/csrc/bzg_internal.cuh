@@ -80,6 +80,7 @@ enum WsSlot {
   WS_PLAN, WS_SSSP_PREV, WS_SSSP_PD, WS_SSSP_AUX, WS_SSSP_OUT,       // find_path
   WS_CUTBITS, WS_CUTSLOTS,                                           // re-cut cache
   WS_PROJ,                                                           // project_on_path
+  WS_REACH_FLAGS,
   kWsSlots
 };
 
@@ -276,9 +277,9 @@ struct Mask {
   // cached shortest-path tree (reused while (mask, v0) is unchanged: cfg4 replanning); the
   // key (the tree's v0, -1 = none) lives on the device next to the tree
   DevBuf dist, parent, tree_key;
-  // cached reverse reachability to vg (relaxed snapping)
+  // cached reverse reachability to vg (relaxed snapping); its key (vg, -1 = none) on the device
   int64_t reach_vg = -1;
-  DevBuf reach;
+  DevBuf reach, reach_key;
 };
 
 // Kernel-family entry points (defined in the k_*.cu translation units).

@@ -865,6 +865,7 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
   mk->counters[0] = E * (long long)n_obs;
   mk->tree_key.release();
   mk->reach_vg = -1;
+  mk->reach_key.release();
   mk->n_qp = 0;
 
   DParams dp{};
@@ -1226,6 +1227,7 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
   mk->prov.alloc(std::max(E, 1ll), c->stream);
   mk->tree_key.release();
   mk->reach_vg = -1;
+  mk->reach_key.release();
   mk->n_qp = 0;
   const int nm = (int)miss.size();
   if (nm > 0) {

@@ -152,6 +152,39 @@ __global__ void k_reach_sweep(long long E, const int* __restrict__ src, const in
   }
 }
 
+// Reverse reachability to vg (graph.py:433-450, _reaches_goal) in one cooperative launch: vg
+// from the device plan; sweeps over the alive edges mark src when dst is marked, a grid barrier
+// per sweep, until a sweep marks nothing.  Cached per (mask, vg) through `key` on the device.
+__global__ void k_reach_coop(long long E, long long V, const int* __restrict__ src, const int* __restrict__ dst,
+                             const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach,
+                             long long* __restrict__ key, const long long* __restrict__ plan, int* __restrict__ flags) {
+  cg::grid_group grid = cg::this_grid();
+  const long long vg = plan[0];
+  if (*(volatile long long*)key == vg) return;  // grid-uniform: the cached set is vg's
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < V; i += nt) reach[i] = i == vg ? 1 : 0;
+  if (tid < 3) flags[tid] = 0;
+  grid.sync();
+  for (int sweep = 0; sweep <= V + 1; ++sweep) {
+    if (tid == 0) flags[(sweep + 1) % 3] = 0;
+    bool any = false;
+    for (long long e = tid; e < E; e += nt) {
+      if (alive && !alive[e]) continue;
+      const int u = src[e];
+      if (reach[dst[e]] && !reach[u]) {
+        reach[u] = 1;
+        any = true;
+      }
+    }
+    if (any) flags[sweep % 3] = 1;
+    grid.sync();
+    if (*(volatile int*)&flags[sweep % 3] == 0) break;
+  }
+  grid.sync();
+  if (tid == 0) *key = vg;
+}
+
 // Frontier Bellman-Ford as one persistent cooperative kernel: a queue of the vertices
 // improved in the previous sweep (each enqueued once per sweep through its stamp); one warp
 // per queued vertex relaxes its alive out-edges with fl(d[u] + c) and atomicMin on the
@@ -540,38 +573,38 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     sp.mode = 1;
     snap_launch(c, g, sp, nullptr, best1, plan + 1);
   } else {
-    // relaxed mid-run snap: nearest vertex that can still reach vg (graph.py:388-392)
-    long long* hv = static_cast<long long*>(c->host_scratch(sizeof(long long)));
-    BZG_CHECK_CUDA(cudaMemcpyAsync(hv, plan, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-    const long long vg = hv[0];
+    // relaxed mid-run snap: nearest vertex that can still reach vg (graph.py:388-392); the
+    // reverse reachability runs on the device (k_reach_coop), cached per (mask, vg) there
     uint8_t* reach;
+    long long* rkey;
+    DevBuf tmp_key;
     if (mk) {
       mk->reach.alloc(V, c->stream);
       reach = mk->reach.as<uint8_t>();
+      if (!mk->reach_key.ptr) {
+        mk->reach_key.alloc(sizeof(long long), c->stream);
+        BZG_CHECK_CUDA(cudaMemsetAsync(mk->reach_key.ptr, 0xFF, sizeof(long long), c->stream));
+      }
+      rkey = mk->reach_key.as<long long>();
     } else {
       tmp_reach.alloc(V, c->stream);
       reach = tmp_reach.as<uint8_t>();
+      tmp_key.alloc(sizeof(long long), c->stream);
+      BZG_CHECK_CUDA(cudaMemsetAsync(tmp_key.ptr, 0xFF, sizeof(long long), c->stream));
+      rkey = tmp_key.as<long long>();
     }
-    if (!mk || mk->reach_vg != vg) {
-      DevBuf changed;
-      changed.alloc(sizeof(int), c->stream);
-      BZG_CHECK_CUDA(cudaMemsetAsync(reach, 0, V, c->stream));
-      const uint8_t one = 1;
-      BZG_CHECK_CUDA(cudaMemcpyAsync(reach + vg, &one, 1, cudaMemcpyHostToDevice, c->stream));
-      int* h = static_cast<int*>(c->host_scratch(sizeof(int)));
-      for (int guard = 0;; ++guard) {
-        BZG_CHECK_CUDA(cudaMemsetAsync(changed.ptr, 0, sizeof(int), c->stream));
-        for (int s = 0; s < 8; ++s)
-          launch(c, "k_reach_sweep", k_reach_sweep, dim3(div_up(E, 256)), dim3(256), 0, E, g->src.as<int>(),
-                 g->dst.as<int>(), alive, reach, changed.as<int>());
-        BZG_CHECK_CUDA(cudaMemcpyAsync(h, changed.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-        if (!h[0] || E == 0) break;
-        BZG_REQUIRE(guard < V + 8, BZG_ECUDA, "reachability sweep did not converge");
-      }
-      if (mk) mk->reach_vg = vg;
-    }
+    DevBuf& rflags = c->ws[WS_REACH_FLAGS];
+    rflags.alloc(4 * sizeof(int), c->stream);
+    int per_sm = 0;
+    BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_reach_coop, 256, 0));
+    const int rblocks = std::max(1, std::min(per_sm, 2) * c->num_sms);
+    long long El = E, Vl2 = V;
+    const int* rs = g->src.as<int>();
+    const int* rd = g->dst.as<int>();
+    const long long* cpl = plan;
+    int* rf = rflags.as<int>();
+    void* args[] = {&El, &Vl2, &rs, &rd, &alive, &reach, &rkey, &cpl, &rf};
+    launch_coop(c, "k_reach_coop", (const void*)k_reach_coop, dim3(rblocks), dim3(256), args);
     sp.mode = 2;
     snap_launch(c, g, sp, reach, best1, plan + 1);
   }
@@ -608,15 +641,14 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   int* stamp = counts + 8;
   int* qa = stamp + V;
   int* qb = qa + V;
-  // BZG_BF_IMPL=queue|scan: k_bf_persistent (frontier queue, returning atomics) or k_bf_scan
-  // (fire-and-forget relaxation + rescan, two barriers per sweep).  The queue's returning
-  // atomics put two L2 round trips on every improvement; from a few thousand vertices the scan
-  // wins (cfg2 0.111 -> 0.096 ms, cfg3 0.33 -> 0.22, cfg5 100k 1.18 -> 0.78).  A one-barrier
-  // scan-and-relax variant (each sweep rescans every vertex and relaxes the changed ones in
-  // place) was slower: cfg3 0.39, cfg5 100k 3.6 ms.
+  // BZG_BF_IMPL=queue|scan|async: k_bf_persistent (frontier queue, returning atomics), k_bf_scan
+  // (fire-and-forget relaxation + rescan, two barriers per sweep) or k_bf_async (no barriers).
   const char* bf_env = std::getenv("BZG_BF_IMPL");
   const std::string bfs = bf_env ? std::string(bf_env) : std::string();
-  const int mode = bfs == "queue" ? 1 : (bfs == "scan" ? 2 : (bfs == "async" ? 3 : (V < 4096 ? 1 : 2)));
+  // default: the rescan variant (cfg2 0.086 ms vs queue 0.098, cfg3 0.20 vs 0.30, cfg5 100k 0.80
+  // vs 1.17); the queue for tiny graphs.  The barrier-free k_bf_async reaches the same fixed
+  // point but re-relaxes far more (cfg3 0.46 ms, cfg5 100k 2.7 ms).
+  const int mode = bfs == "queue" ? 1 : (bfs == "scan" ? 2 : (bfs == "async" ? 3 : (V < 1024 ? 1 : 2)));
   const long long Q = V + 8192 + 64;  // ring: <= V queued (flags) + claimed-unread (one per warp)
   if (mode == 3) {
     t_aux.alloc((8 + (size_t)std::max(V, 1ll) + (size_t)Q) * sizeof(int), c->stream);
