@@ -1202,6 +1202,13 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
     }
   }
   // slots for the misses: free slots first, then least recently used ones not in this list
+  // (enough exist: the list's own slots are at most n_obs - misses of the max_slots >= n_obs)
+  {
+    int avail = 0;
+    for (int sl = 0; sl < cc.max_slots; ++sl)
+      avail += cc.key_of[sl].empty() || (cc.stamp[sl] != cc.clock && !in_list.count(cc.key_of[sl]));
+    if (avail < (int)miss.size()) return false;
+  }
   std::vector<int> new_slot(miss.size());
   for (size_t i = 0; i < miss.size(); ++i) {
     int best = -1;
@@ -1249,7 +1256,15 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
     BZG_CHECK_CUDA(cudaMemsetAsync(tmp.ptr, 0, (size_t)3 * nm * Wb * sizeof(uint32_t), c->stream));
     uint32_t* tk = tmp.as<uint32_t>();
     CutBits bits{tk, tk + (size_t)nm * Wb, tk + (size_t)2 * nm * Wb, Wb};
-    cut_graph_impl(c, g, nm, sro.data(), sA.data(), sb.data(), sbox.data(), slo.data(), shi.data(), cfg, mk, bits);
+    try {
+      cut_graph_impl(c, g, nm, sro.data(), sA.data(), sb.data(), sbox.data(), slo.data(), shi.data(), cfg, mk, bits);
+    } catch (...) {  // the new slots hold no outcome rows: forget them
+      for (int i = 0; i < nm; ++i) {
+        cc.slot_of.erase(cc.key_of[new_slot[i]]);
+        cc.key_of[new_slot[i]].clear();
+      }
+      throw;
+    }
     // per-obstacle popcounts, the rows into their slots
     DevBuf d_pc;
     d_pc.alloc((size_t)3 * nm * sizeof(unsigned long long), c->stream);

@@ -361,6 +361,14 @@ def test_recut_cache_equals_full_cut(ctx, golden, name):
     gr.set_cut_cache(len(obstacles) + 2)
     for lst in lists:
         _same_cut(G.cut_graph(gr, lst), G.cut_graph(ref, lst))
+    if m == 2:  # a failing cut (an empty obstacle: ValueError) leaves the cache consistent
+        from paper_2411_13507_b200.geometry import Polytope
+
+        empty = Polytope(np.array([[1.0, 0.0], [-1.0, 0.0], [0.0, 1.0]]), np.array([0.0, -1.0, 1.0]))
+        with pytest.raises(ValueError):
+            G.cut_graph(gr, [_moved(obstacles[0], np.full(m, 0.03)), empty])
+        lst = [_moved(obstacles[0], np.full(m, 0.03))] + list(obstacles[1:])
+        _same_cut(G.cut_graph(gr, lst), G.cut_graph(ref, lst))
     big = list(obstacles) + [_moved(o, np.full(m, -0.05)) for o in obstacles]  # larger than the cache
     _same_cut(G.cut_graph(gr, big), G.cut_graph(ref, big))
     _same_cut(G.cut_graph(gr, moved), G.cut_graph(ref, moved))
