@@ -257,7 +257,13 @@ class CutMask:
         return int(self.alive.sum())
 
     def qp_records(self) -> dict:
-        """Per-QP diagnostics: edge, obstacle, status (0 solved..3 error), iterations, ||delta||."""
+        """Per-QP diagnostics: edge, obstacle, status (0 solved..3 error), iterations, ||delta||.
+
+        cut_graph skips the polish of SOLVED instances whose ADMM ||delta|| is >= 1e-2
+        (BZG_POLISH_SCREEN; verdict-exact), so for those ``delta`` is the ADMM
+        iterate's norm, not the polished one the reference's solve() would return (cut_qp
+        polishes every instance).  With the re-cut cache on, the records cover the QPs solved by
+        the cut that produced this mask (obstacles seen before contribute cached outcomes)."""
         lib = self._graph._ctx.lib
         n = C.c_int64()
         nat.check(lib.bzg_mask_qp_count(self._h, C.byref(n)))
@@ -408,7 +414,12 @@ def check_edges(oracle, X1, X2, eps: float = EPS_GEO, *, ctx=None) -> np.ndarray
 
 
 def check_edge(oracle, x1, x2, eps: float = EPS_GEO, *, ctx=None) -> bool:
-    """Scalar predicate (reachability.py:130-136) through the device batch kernel."""
+    """Scalar predicate (reachability.py:130-136) through the device batch kernel.
+
+    Evaluated with check_edges' separable arithmetic fl(x1 F1' + x2 F2') -- build_graph's own
+    edge test (graph.py:172-184) -- not the reference's length-2n gemv F @ [x1; x2], whose
+    OpenBLAS summation order is not reproduced: for a pair within rounding of a threshold the
+    answer can differ from the reference's scalar check_edge (never from its graph)."""
     x1 = np.asarray(x1, dtype=np.float64)
     x2 = np.asarray(x2, dtype=np.float64)
     n = oracle.spec.n
@@ -490,7 +501,11 @@ def _cut_cfg(cfg) -> nat.CutConfigC:
 
 
 def cut_graph(graph: BezierGraph, obstacles, cfg: CutConfig | None = None) -> CutMask:
-    """Screen every (edge, obstacle) pair, QP the leftovers, keep edges safe for all (graph.py:302-350)."""
+    """Screen every (edge, obstacle) pair, QP the leftovers, keep edges safe for all (graph.py:302-350).
+
+    Obstacles: boxes (as_box) take the closed-form screen, other convex polytopes of up to 32
+    rows the general one.  The polish of SOLVED QPs with ADMM ||delta|| >= 1e-2 is skipped
+    (verdict-exact; see CutMask.qp_records).  One device synchronisation (the counters)."""
     cfg = cfg or CutConfig()
     ctx = graph._ctx
     arrs = _obstacle_arrays(list(obstacles), graph.spec.m)
