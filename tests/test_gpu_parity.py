@@ -400,3 +400,37 @@ def test_bellman_ford_variants_reach_the_reference_paths(ctx, golden, name, impl
             p = G.find_path(gr, RefMask(), start, gl)
             assert (p or []) == list(flat[off:off + lens[k]]), k
             off += lens[k]
+
+
+def test_edge_cases_round2(ctx, golden):
+    """Degenerate inputs of the round-2 entry points: empty obstacle lists under the re-cut cache,
+    an unreachable goal (None) and start == goal through the one-sync search, eps_band on a
+    row block, project_on_path on 0/1-state paths."""
+    from paper_2411_13507_b200 import replan
+
+    g = golden("demo200")
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(g)
+    gr = G.build_graph(N, spec, orc, bounds, seed, include, ctx=ctx)
+    gr.set_cut_cache(8)
+    m0 = G.cut_graph(gr, [])
+    assert m0.alive.all() and m0.pairs_total == 0
+    m1 = G.cut_graph(gr, obstacles)
+    m2 = G.cut_graph(gr, obstacles)  # all hits
+    assert np.array_equal(m1.alive, m2.alive) and m1.qp_safe == m2.qp_safe and m2.pairs_qp == m1.pairs_qp
+    assert np.array_equal(m1.alive, g["alive"])
+    # start == goal -> [v]; a goal whose snapped vertex has no alive in-edges -> None
+
+    class NoEdges:
+        alive = np.zeros(gr.num_edges, dtype=bool)
+
+    assert G.find_path(gr, NoEdges(), start, start) == [N]
+    assert G.find_path(gr, NoEdges(), start, goal) is None
+    # eps band of a row block = its share of the whole
+    rb = G.build_graph(N, spec, orc, bounds, seed, include, ctx=ctx, rows=(0, 101))
+    rb2 = G.build_graph(N, spec, orc, bounds, seed, include, ctx=ctx, rows=(101, N + 2))
+    full = gr.eps_band(1e-3)
+    a, b = rb.eps_band(1e-3), rb2.eps_band(1e-3)
+    assert a["band"] + b["band"] == full["band"] and a["feasible_plus"] + b["feasible_plus"] == full["feasible_plus"]
+    # project_on_path: no hop -> 0
+    assert replan.project_on_path(np.zeros((0, spec.n)), spec, 0.1, start) == 0.0
+    assert replan.project_on_path(start[None], spec, 0.1, start) == 0.0
