@@ -647,7 +647,9 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   const std::string bfs = bf_env ? std::string(bf_env) : std::string();
   // default: the rescan variant (cfg2 0.086 ms vs queue 0.098, cfg3 0.20 vs 0.30, cfg5 100k 0.80
   // vs 1.17); the queue for tiny graphs.  The barrier-free k_bf_async reaches the same fixed
-  // point but re-relaxes far more (cfg3 0.46 ms, cfg5 100k 2.7 ms).
+  // point but re-relaxes far more (cfg3 0.46 ms, cfg5 100k 2.7 ms), and a one-barrier rescan
+  // (relax the last frontier and rescan without waiting) measured the same as two barriers
+  // (cfg3 0.201 vs 0.208 ms): the sweeps are bound by their dependent loads.
   const int mode = bfs == "queue" ? 1 : (bfs == "scan" ? 2 : (bfs == "async" ? 3 : (V < 1024 ? 1 : 2)));
   const long long Q = V + 8192 + 64;  // ring: <= V queued (flags) + claimed-unread (one per warp)
   if (mode == 3) {
