@@ -510,7 +510,10 @@ def replanning_bench(args, ctx, stream, rank, world):
     near = np.argsort(np.linalg.norm(Vx - np.asarray(w.start), axis=1))
     start2 = Vx[int(near[1])].copy()
 
-    def timed(starts):
+    query = G.PathQuery(graph, mask)  # the same search captured as one CUDA graph
+
+    def timed(starts, fn=None):
+        fn = fn or (lambda st, gl: G.find_path(graph, mask, st, gl))
         dev, wall, paths = [], [], []
         for k, gl in enumerate(goals):
             st = starts[k % len(starts)]
@@ -518,7 +521,7 @@ def replanning_bench(args, ctx, stream, rank, world):
             b = torch.cuda.Event(enable_timing=True)
             t0 = time.perf_counter()
             a.record(stream)
-            p = G.find_path(graph, mask, st, gl)
+            p = fn(st, gl)
             b.record(stream)
             b.synchronize()
             wall.append(1e3 * (time.perf_counter() - t0))
@@ -528,14 +531,18 @@ def replanning_bench(args, ctx, stream, rank, world):
 
     for _ in range(max(args.warmup, 1)):
         timed([w.start])
+        timed([w.start, start2], query)
     ctx.reset_stats()
     clocks = ClockSampler(0)
     clocks.start()
     time.sleep(0.4)
     dev_c, wall_c, paths = timed([w.start])
-    dev_m, wall_m, _ = timed([w.start, start2])
+    dev_m, wall_m, paths_m = timed([w.start, start2])
     launches, _ = ctx.stats()
+    qdev_c, qwall_c, qpaths = timed([w.start], query)
+    qdev_m, qwall_m, qpaths_m = timed([w.start, start2], query)
     clk = clocks.stop()
+    assert qpaths == paths and qpaths_m == paths_m, "captured query differs from find_path"
     pct = lambda a, q: float(np.percentile(a, q))  # noqa: E731
     out = {
         "metric": "goal-update latency p50 (find_path on a fixed graph+mask)", "value": pct(dev_c, 50), "unit": "ms",
@@ -545,6 +552,11 @@ def replanning_bench(args, ctx, stream, rank, world):
                    "vertices": graph.num_vertices, "edges": graph.num_edges, "alive": mask.alive_count},
         "p99_ms": pct(dev_c, 99), "p50_ms": pct(dev_c, 50),
         "moving_start": {"p50_ms": pct(dev_m, 50), "p99_ms": pct(dev_m, 99)},
+        # the same updates through PathQuery (one captured CUDA graph per search; same paths)
+        "captured": {"p50_ms": pct(qdev_c, 50), "p99_ms": pct(qdev_c, 99), "moving_start_p50_ms": pct(qdev_m, 50),
+                     "moving_start_p99_ms": pct(qdev_m, 99), "wall_p50_ms": pct(qwall_c, 50),
+                     "wall_moving_start_p50_ms": pct(qwall_m, 50), "kernels_per_query": query.kernels_per_query,
+                     "api": "paper_2411_13507_b200.PathQuery"},
         "e2e": {"value": pct(wall_c, 50), "unit": "ms", "p99": pct(wall_c, 99),
                 "moving_start_p50": pct(wall_m, 50), "h2d_bytes_per_step": 2 * 8 * w.spec.n,
                 "d2h_bytes_per_step": int(np.mean([8 * (len(p or []) + 1) for p in paths])),

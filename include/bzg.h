@@ -47,6 +47,7 @@ enum { BZG_SOLVED = 0, BZG_MAX_ITER = 1, BZG_INFEASIBLE = 2, BZG_ERROR = 3 };
 typedef struct bzg_ctx bzg_ctx;
 typedef struct bzg_graph bzg_graph;
 typedef struct bzg_mask bzg_mask;
+typedef struct bzg_query bzg_query;
 
 int bzg_abi_version(void);
 const char* bzg_last_error(void);
@@ -222,6 +223,19 @@ int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start,
                   const double* tube_lo, const double* tube_hi, double eps_geo, int position_only_snap,
                   int require_tube_snap, int64_t* path_out, int64_t path_cap, int64_t* path_len,
                   double* dist_out);
+/* repeated find_path on one (graph, mask) -- the 200 Hz goal/start updates of a replanning
+ * loop (sim.py:275-408 calls graph.find_path every cycle): bzg_query_create warms the search
+ * up once and captures it as a CUDA graph; bzg_query_run(start, goal) is then one graph
+ * launch and one synchronisation, with the same result as bzg_find_path with these options.
+ * mk may be NULL (no mask).  A query is stale (BZG_EINVAL) once g's edge set changes; destroy
+ * it before its graph and mask. */
+int bzg_query_create(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* tube_lo, const double* tube_hi,
+                     double eps_geo, int position_only_snap, int require_tube_snap, bzg_query** out);
+int bzg_query_run(bzg_query* q, const double* start, const double* goal, int64_t* path_out, int64_t path_cap,
+                  int64_t* path_len, double* dist_out);
+/* kernels per bzg_query_run (the captured graph's kernel nodes) */
+int bzg_query_kernels(const bzg_query* q, int64_t* n);
+int bzg_query_destroy(bzg_query* q);
 
 /* replaces sim._project_on_path (sim.py:220-239): the grid time tau = k h (k < (L-1) *
  * steps_per_hop, steps_per_hop = round(T / h)) along the curve chain through the L path states

@@ -16,6 +16,7 @@ from .graph import (
     CutMask,
     CutProvenance,
     CutVerdict,
+    PathQuery,
     SolveConfig,
     build_graph,
     check_edge,
@@ -35,7 +36,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BezierSpec", "boundary_matrix", "derivative_matrix",
     "EPS_GEO", "Box", "Hyperplane", "Polytope", "bounding_box", "erode", "inflate",
-    "BezierGraph", "CutConfig", "CutMask", "CutProvenance", "CutVerdict", "SolveConfig",
+    "BezierGraph", "CutConfig", "CutMask", "CutProvenance", "CutVerdict", "PathQuery", "SolveConfig",
     "build_graph", "check_edge", "check_edges", "cut_graph", "cut_heuristic", "cut_heuristic_batch", "cut_qp",
     "cut_qp_batch", "find_path", "path_cost",
     "ReachOracle", "TrackingTube", "build_oracle",

@@ -105,6 +105,10 @@ _SIGS = {
     "bzg_mask_export_device": ([_P, _P, _P], C.c_int),
     "bzg_find_path": ([_P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_int, C.c_int, _P, C.c_int64,
                        C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
+    "bzg_query_create": ([_P, _P, _P, _P, _P, C.c_double, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
+    "bzg_query_run": ([_P, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
+    "bzg_query_kernels": ([_P, C.POINTER(C.c_int64)], C.c_int),
+    "bzg_query_destroy": ([_P], C.c_int),
     "bzg_project_on_path": ([_P, C.c_int32, C.c_int32, C.c_double, _P, C.c_int64, _P, C.c_double, C.c_int32, _P,
                              C.POINTER(C.c_double)], C.c_int),
     "bzg_probe_fp64": ([_P, C.c_int, C.POINTER(C.c_double)], C.c_int),

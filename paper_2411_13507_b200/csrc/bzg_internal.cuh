@@ -37,6 +37,11 @@ struct Error : std::runtime_error {
 
 struct Ctx;
 
+// Set while a stream capture (bzg_query) records work: a workspace that would have to grow
+// then is an error (the graph would bake in a fresh allocation), so captures are preceded by
+// an eager warm-up that sizes every buffer.
+inline thread_local bool g_capturing = false;
+
 // Stream-ordered device allocation owned by the library.
 struct DevBuf {
   void* ptr = nullptr;
@@ -62,6 +67,7 @@ struct DevBuf {
   }
   void alloc(size_t nbytes, cudaStream_t s) {
     if (nbytes <= bytes && ptr) return;
+    if (g_capturing) throw Error(BZG_ECUDA, "workspace grew during a stream capture");
     release();
     stream = s;
     if (nbytes == 0) nbytes = 16;
@@ -81,6 +87,7 @@ enum WsSlot {
   WS_CUTBITS, WS_CUTSLOTS,                                           // re-cut cache
   WS_PROJ,                                                           // project_on_path
   WS_REACH_FLAGS,
+  WS_SNAP, WS_BEST0, WS_BEST1, WS_NM_REACH, WS_NM_KEY, WS_NM_DIST, WS_NM_PARENT,  // find_path
   kWsSlots
 };
 
@@ -119,7 +126,9 @@ struct Ctx {
   // cut work lists, QP state): reused across calls on this stream, so repeated builds and
   // cuts do not refragment the stream-ordered pool (a fresh 1 GB bit matrix per step made the
   // pool map new memory at random steps, milliseconds each).
-  DevBuf ws[kWsSlots];
+  // ws points at ws_own except while a bzg_query warms up or captures with its own set.
+  DevBuf ws_own[kWsSlots];
+  DevBuf* ws = ws_own;
   // last obstacle-grid decision (k_cut.cu): obstacle count and xy bounds -> grid sparse enough
   int grid_nobs = -1;
   double grid_key[4] = {0, 0, 0, 0};
@@ -261,6 +270,7 @@ struct Graph {
   DevBuf points;                  // lazily materialised E x m x (p+1)
   bool points_ready = false;
   CutCache cut_cache;
+  uint64_t version = 0;           // bumped whenever the edge set is replaced (stale queries)
 };
 
 struct Mask {
@@ -307,5 +317,15 @@ double project_on_path(Ctx* c, int m, int gamma, double T, const double* D, long
 void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
                const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
                double* dist);
+
+// A find_path on a fixed (graph, mask) captured as a CUDA graph (bzg_query): start and goal go
+// through pinned host memory, so a query is one graph launch and one synchronisation.
+struct Query;
+Query* query_create(Ctx* c, Graph* g, Mask* mk, const double* tube_lo, const double* tube_hi, double eps,
+                    int pos_only, int require_tube);
+void query_run(Query* q, const double* start, const double* goal, std::vector<int64_t>& path, double* dist);
+void query_destroy(Query* q);
+long long query_kernels(const Query* q);
+Ctx* query_ctx(const Query* q);
 
 }  // namespace bzg

@@ -11,6 +11,9 @@ using namespace bzg;
 struct bzg_ctx : Ctx {};
 struct bzg_graph : Graph {};
 struct bzg_mask : Mask {};
+// bzg_query is opaque here (Query is defined with the search, k_sssp.cu)
+static Query* as_query(bzg_query* q) { return reinterpret_cast<Query*>(q); }
+static const Query* as_query(const bzg_query* q) { return reinterpret_cast<const Query*>(q); }
 
 namespace {
 
@@ -83,7 +86,7 @@ int bzg_ctx_destroy(bzg_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->scratch.release();
     ctx->flag.release();
-    for (auto& w : ctx->ws) w.release();
+    for (auto& w : ctx->ws_own) w.release();
     ctx->drain_profile();
     for (auto e : ctx->spare) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -584,6 +587,52 @@ int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start,
       std::memcpy(path_out, path.data(), path.size() * sizeof(int64_t));
     }
     if (dist_out) *dist_out = dist;
+  });
+}
+
+int bzg_query_create(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* tube_lo, const double* tube_hi,
+                     double eps_geo, int position_only_snap, int require_tube_snap, bzg_query** out) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && g && tube_lo && tube_hi && out, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(!mk || mk->g == g, BZG_EINVAL, "mask belongs to another graph");
+    BZG_REQUIRE(!mk || mk->E == g->E, BZG_EINVAL, "stale mask: its graph's edge set changed after the cut");
+    set_device(ctx);
+    *out = reinterpret_cast<bzg_query*>(
+        query_create(ctx, g, mk, tube_lo, tube_hi, eps_geo, position_only_snap, require_tube_snap));
+  });
+}
+
+int bzg_query_run(bzg_query* q, const double* start, const double* goal, int64_t* path_out, int64_t path_cap,
+                  int64_t* path_len, double* dist_out) {
+  return guarded([&] {
+    BZG_REQUIRE(q && start && goal && path_len, BZG_EINVAL, "null argument");
+    set_device(query_ctx(as_query(q)));
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    query_run(as_query(q), start, goal, path, &dist);
+    if (path.empty()) {
+      *path_len = -1;
+    } else {
+      *path_len = (int64_t)path.size();
+      BZG_REQUIRE(path_out && path_cap >= (int64_t)path.size(), BZG_EINVAL, "path buffer too small");
+      std::memcpy(path_out, path.data(), path.size() * sizeof(int64_t));
+    }
+    if (dist_out) *dist_out = dist;
+  });
+}
+
+int bzg_query_kernels(const bzg_query* q, int64_t* n) {
+  return guarded([&] {
+    BZG_REQUIRE(q && n, BZG_EINVAL, "null argument");
+    *n = query_kernels(as_query(q));
+  });
+}
+
+int bzg_query_destroy(bzg_query* q) {
+  return guarded([&] {
+    if (!q) return;
+    set_device(query_ctx(as_query(q)));
+    query_destroy(as_query(q));
   });
 }
 

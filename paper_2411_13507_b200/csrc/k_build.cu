@@ -1301,6 +1301,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   }
   BZG_REQUIRE(E < (1ll << 31), BZG_EUNSUPPORTED, "edge count exceeds the int32 CSR index range");
   g->E = E;
+  ++g->version;
   g->src.alloc(E * sizeof(int), c->stream);
   g->dst.alloc(E * sizeof(int), c->stream);
   g->cost.alloc(E * sizeof(double), c->stream);
@@ -1325,6 +1326,7 @@ void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, co
   const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   BZG_REQUIRE(E >= 0 && E < (1ll << 31), BZG_EINVAL, "edge count out of range");
   g->E = E;
+  ++g->version;
   g->row_begin = 0;
   g->row_end = g->V;
   g->points_ready = false;

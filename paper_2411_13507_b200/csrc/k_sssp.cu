@@ -67,8 +67,11 @@ __device__ __forceinline__ double snap_norm(const double* v, const SnapParams& s
 
 // first argmin (value, index) over candidates; infinite values are skipped so an
 // all-excluded set returns index -1.
-__global__ void k_snap(SnapParams sp, const double* __restrict__ Vx, long long V, const uint8_t* __restrict__ reach,
-                       unsigned long long* __restrict__ best) {
+// spd: the parameters in device memory (a captured query, whose start/goal change per launch),
+// else the by-value sp
+__global__ void k_snap(SnapParams sp_val, const SnapParams* __restrict__ spd, const double* __restrict__ Vx,
+                       long long V, const uint8_t* __restrict__ reach, unsigned long long* __restrict__ best) {
+  const SnapParams& sp = spd ? *spd : sp_val;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   double val = INFINITY;
   long long idx = -1;
@@ -340,6 +343,190 @@ __global__ void k_bf_scan(long long V, const long long* __restrict__ row_ptr, co
   if (tid == 0) counts[3] = sweep - 1;
 }
 
+// Tiny graphs (V <= kBfCtaMaxV, E <= kBfCtaMaxE): the frontier Bellman-Ford in ONE thread
+// block with the distances, stamps and both frontier queues in shared memory -- every sweep is a
+// block barrier and the relaxations are shared-memory atomics; only the edges come from L2.
+constexpr int kBfCtaThreads = 1024;
+constexpr long long kBfCtaMaxV = 4096, kBfCtaMaxE = 32768;
+__global__ void __launch_bounds__(kBfCtaThreads, 1)
+k_bf_cta(long long V, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
+         const double* __restrict__ cost, const uint8_t* __restrict__ alive, unsigned long long* __restrict__ dist,
+         int* __restrict__ counts, int max_sweeps, const long long* __restrict__ plan) {
+  if (!plan[2]) return;  // block-uniform
+  extern __shared__ unsigned long long smem_u64[];
+  unsigned long long* sd = smem_u64;               // V distances (double bits)
+  int* sstamp = reinterpret_cast<int*>(sd + V);    // V stamps: last sweep that enqueued the vertex
+  int* qa = sstamp + V;                            // two frontier queues of V entries
+  int* qb = qa + V;
+  __shared__ int scount[3];
+  const int v0 = (int)plan[1];
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    sd[i] = i == v0 ? 0ull : kInfBits;
+    sstamp[i] = i == v0 ? 0 : -1;
+  }
+  if (threadIdx.x == 0) {
+    qa[0] = v0;
+    scount[0] = 1;
+    scount[1] = 0;
+    scount[2] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int sweep = 1;
+  for (; sweep <= max_sweeps; ++sweep) {
+    const int* qin = (sweep & 1) ? qa : qb;
+    int* qout = (sweep & 1) ? qb : qa;
+    const int cin = scount[(sweep - 1) % 3];
+    if (cin == 0) break;
+    if (threadIdx.x == 0) scount[(sweep + 1) % 3] = 0;
+    int* cout = scount + sweep % 3;
+    for (int k = wid; k < cin; k += nw) {
+      const int u = qin[k];
+      const double du = __longlong_as_double((long long)sd[u]);
+      const long long e1 = row_ptr[u + 1];
+      for (long long eb = row_ptr[u] + lane; eb < e1; eb += 64) {
+        int vv[2];
+        double cc[2];
+        bool ok[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const long long e = eb + 32 * t;
+          ok[t] = e < e1 && (!alive || alive[e]);
+          vv[t] = ok[t] ? dst[e] : 0;
+          cc[t] = ok[t] ? cost[e] : 0.0;
+        }
+        const unsigned am = __activemask();
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          bool push = false;
+          if (ok[t]) {
+            const unsigned long long nb = dbits(__dadd_rn(du, cc[t]));
+            if (nb < sd[vv[t]]) {
+              const unsigned long long old = atomicMin(sd + vv[t], nb);
+              push = nb < old && atomicExch(sstamp + vv[t], sweep) != sweep;
+            }
+          }
+          const unsigned want = __ballot_sync(am, push);
+          if (want) {
+            const int leader = __ffs(want) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(cout, __popc(want));
+            base = __shfl_sync(am, base, leader);
+            if (push) qout[base + __popc(want & ((1u << lane) - 1u))] = vv[t];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < V; i += blockDim.x) dist[i] = sd[i];
+  if (threadIdx.x == 0) {
+    counts[3] = sweep - 1;
+    counts[4] = 0;
+  }
+}
+
+// Thread-block-cluster Bellman-Ford (graphs up to kBfClusterMaxV vertices): the frontier
+// Bellman-Ford of k_bf_scan on the CTAs of ONE cluster, so a sweep ends with a cluster barrier
+// (barrier.cluster, far cheaper than the cooperative grid barrier, which costs ~2 us per sweep
+// and is most of a small graph's search).  CTA r owns the vertex slice [r*chunk, (r+1)*chunk):
+// one phase per sweep, each CTA scans its slice for vertices whose distance dropped since its
+// last scan (prev, in shared memory), queues them in shared memory, relaxes their alive
+// out-edges with fire-and-forget atomicMin on the global distance bits (L2), and adds its queue
+// length to a cluster-wide counter in CTA 0's shared memory; the search ends after the barrier
+// that shows a sweep with an empty frontier everywhere.  Same fixed point as the other schedules.
+constexpr int kBfClusterThreads = 1024;
+constexpr long long kBfClusterMaxV = 16 * 16 * 1024;
+// default range of the cluster schedule: cfg2 (V = 2k, 249k edges) 0.056 ms vs 0.084 for the
+// grid rescan; cfg3 (20k, 4.5M) 0.201 vs 0.203 -- even; cfg5 100k (14M edges) 13 ms: 16 SMs are
+// far too few for the relaxations there
+constexpr long long kBfClusterDefaultV = 16384, kBfClusterDefaultE = 2ll << 20;
+__global__ void __launch_bounds__(kBfClusterThreads, 1)
+k_bf_cluster(long long V, long long chunk, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
+             const double* __restrict__ cost, const uint8_t* __restrict__ alive, unsigned long long* __restrict__ dist,
+             int* __restrict__ counts, int max_sweeps, const long long* __restrict__ plan) {
+  if (!plan[2]) return;  // cluster-uniform
+  cg::cluster_group cl = cg::this_cluster();  // barriers: barrier.cluster arrive.release / wait.acquire
+  extern __shared__ unsigned long long smem_u64[];
+  unsigned long long* sprev = smem_u64;            // chunk: the owned distances at the last scan
+  int* q = reinterpret_cast<int*>(sprev + chunk);  // the local frontier (global vertex ids)
+  __shared__ int tot[3];                           // rank 0's: frontier totals per phase (mod 3)
+  __shared__ int qn;
+  const unsigned rank = cl.block_rank();
+  const long long v_lo = (long long)rank * chunk;
+  const long long n_own = max(0ll, min(chunk, V - v_lo));
+  // k_init_tree set dist (0 at v0, +inf elsewhere); prev = +inf everywhere, so v0 shows up as
+  // dropped in the first scan
+  for (long long i = threadIdx.x; i < chunk; i += blockDim.x) sprev[i] = kInfBits;
+  if (threadIdx.x < 3) tot[threadIdx.x] = 0;
+  int* tot0 = cl.map_shared_rank(tot, 0);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  cl.sync();
+  int phase = 0;
+  for (; phase <= max_sweeps; ++phase) {
+    if (phase > 0 && *(volatile int*)&tot0[(phase - 1) % 3] == 0) break;  // last sweep relaxed nothing
+    if (rank == 0 && threadIdx.x == 0) tot[(phase + 1) % 3] = 0;
+    // scan the owned slice: vertices whose distance dropped form this sweep's frontier
+    if (threadIdx.x == 0) qn = 0;
+    __syncthreads();
+    for (long long i0 = (long long)threadIdx.x - lane; i0 < n_own; i0 += blockDim.x) {  // warp-uniform
+      const long long i = i0 + lane;
+      bool push = false;
+      if (i < n_own) {
+        const unsigned long long d = __ldcg(dist + v_lo + i);
+        if (d != sprev[i]) {
+          sprev[i] = d;
+          push = true;
+        }
+      }
+      const unsigned want = __ballot_sync(0xffffffffu, push);
+      if (want) {
+        const int leader = __ffs(want) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&qn, __popc(want));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (push) q[base + __popc(want & ((1u << lane) - 1u))] = (int)(v_lo + i);
+      }
+    }
+    __syncthreads();
+    const int cin = qn;
+    if (threadIdx.x == 0 && cin) atomicAdd(&tot0[phase % 3], cin);
+    // relax the frontier's alive out-edges (a stale, larger du only gives a larger candidate;
+    // the later drop is caught by the next scan)
+    for (int k = wid; k < cin; k += nw) {
+      const int u = q[k];
+      const double du = __longlong_as_double((long long)sprev[u - v_lo]);
+      const long long e1 = row_ptr[u + 1];
+      for (long long eb = row_ptr[u] + lane; eb < e1; eb += 128) {
+        int vv[4];
+        double cc[4];
+        bool ok[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const long long e = eb + 32 * t;
+          ok[t] = e < e1 && (!alive || alive[e]);
+          vv[t] = ok[t] ? dst[e] : 0;
+          cc[t] = ok[t] ? cost[e] : 0.0;
+        }
+        unsigned long long dv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dv[t] = ok[t] ? __ldcg(dist + vv[t]) : 0ull;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const unsigned long long nb = dbits(__dadd_rn(du, cc[t]));
+          if (ok[t] && nb < dv[t]) atomicMin(dist + vv[t], nb);
+        }
+      }
+    }
+    cl.sync();
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    counts[3] = phase;
+    counts[4] = 0;
+  }
+  cl.sync();  // no CTA leaves while others may still read CTA 0's counters
+}
+
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -524,60 +711,104 @@ __global__ void k_backtrack(long long V, const long long* __restrict__ plan, con
   out[1] = (long long)dist[vg];
 }
 
+size_t bf_cluster_smem(long long chunk) { return (size_t)chunk * (sizeof(unsigned long long) + sizeof(int)); }
+
+// cluster size for k_bf_cluster on V vertices: the smallest of 1, 2, 4, 8, 16 whose slice fits
+// the shared memory (16 needs the non-portable cluster size) -- small clusters for small graphs,
+// fewer CTAs to synchronise; 0 when V is too large or the device refuses the configuration
+int bf_cluster_size(long long V) {
+  if (V > kBfClusterMaxV) return 0;
+  const long long per_cta = 192 * 1024 / (sizeof(unsigned long long) + sizeof(int));
+  static int max_size = -1;
+  if (max_size < 0) {  // 16 CTAs at the largest slice, if the device schedules such a cluster
+    max_size = 8;
+    if (cudaFuncSetAttribute((const void*)k_bf_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+            cudaSuccess &&
+        cudaFuncSetAttribute((const void*)k_bf_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)bf_cluster_smem(per_cta)) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16);
+      cfg.blockDim = dim3(kBfClusterThreads);
+      cfg.dynamicSmemBytes = bf_cluster_smem(per_cta);
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 16;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, (const void*)k_bf_cluster, &cfg) == cudaSuccess && n > 0) max_size = 16;
+    }
+    cudaGetLastError();
+  }
+  const int env = std::getenv("BZG_BF_CLUSTER") ? std::atoi(std::getenv("BZG_BF_CLUSTER")) : 0;  // per call
+  int cs = env > 0 ? env : 16;
+  // default: 16 CTAs (the relaxation streams the edges through 16 SMs)
+  if (div_up(V, cs) > per_cta) return 0;
+  return cs <= max_size ? cs : 0;
+}
+
 // k_snap over the vertices, the result (first argmin index, -1 if none) written to *out
-void snap_launch(Ctx* c, Graph* g, const SnapParams& sp, const uint8_t* reach, DevBuf& best, long long* out) {
+void snap_launch(Ctx* c, Graph* g, const SnapParams& sp, const SnapParams* spd, const uint8_t* reach, DevBuf& best,
+                 long long* out) {
   const long long V = g->V;
   const unsigned nb = div_up(V, 256);
   best.alloc((1 + 2 * (size_t)nb) * sizeof(unsigned long long), c->stream);
   launch(c, "k_fill_best", k_fill_u64, dim3(1), dim3(32), 0, best.as<unsigned long long>(), 1ll, kInfBits + 2);
-  launch(c, "k_snap", k_snap, dim3(nb), dim3(256), 0, sp, g->vertices.as<double>(), V, reach,
+  launch(c, "k_snap", k_snap, dim3(nb), dim3(256), 0, sp, spd, g->vertices.as<double>(), V, reach,
          best.as<unsigned long long>());
   launch(c, "k_snap_final", k_snap_final, dim3(1), dim3(32), 0, best.as<unsigned long long>(), (int)nb, out);
 }
 
-}  // namespace
+constexpr long long kHead = 510;  // path entries in the first read-back
 
-// One host synchronisation per search (the path read-back).  (vg, v0) stay on the device
-// (plan); the tree kernels skip themselves when the mask's cached shortest-path tree already
-// belongs to v0 (cfg4 goal updates) or the answer is trivial.  Relaxed snapping computes the
-// reverse reachability to vg with a host-driven sweep loop (cached per (mask, vg)).
-void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
-               const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
-               double* dist_out) {
-  const long long V = g->V, E = g->E;
+// goal (mode 0) and start (mode 1 tube / 2 reach) snapping parameters of one search
+void snap_params(const Graph* g, const double* start, const double* goal, const double* tube_lo,
+                 const double* tube_hi, double eps, int pos_only, int require_tube, SnapParams sp[2]) {
   const int n = g->n;
-  BZG_REQUIRE(n <= 16, BZG_EUNSUPPORTED, "state dimension too large");
-  BZG_REQUIRE(V >= 1, BZG_EINVAL, "graph has no vertices");
-  const uint8_t* alive = mk ? mk->alive.as<uint8_t>() : nullptr;
-  path.clear();
-  *dist_out = INFINITY;
+  for (int j = 0; j < 2; ++j) {
+    sp[j] = SnapParams{};
+    sp[j].n = n;
+    sp[j].m_norm = pos_only ? g->m : n;
+  }
+  for (int k = 0; k < n; ++k) {
+    sp[0].target[k] = goal[k];
+    sp[1].target[k] = start[k];
+    sp[1].tlo[k] = -tube_hi[k] - eps;  // (diff >= -tube.hi - EPS_GEO)   graph.py:381
+    sp[1].thi[k] = -tube_lo[k] + eps;  // (diff <= -tube.lo + EPS_GEO)
+  }
+  sp[0].mode = 0;
+  sp[1].mode = require_tube ? 1 : 2;
+}
 
+// Enqueue one search on c->stream: snapping, the shortest-path tree (skipped on the device when
+// cached or trivial), parents, backtrack, and the read-back of the first kHead + 2 entries of
+// [len, dist bits, path...] into h_out (pinned).  Every buffer comes from c->ws or the mask, so
+// the same sequence can be captured (bzg_query).  h_sp (pinned, 2 SnapParams) non-null: the
+// snapping parameters are copied to the device and read there instead of sp.
+void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const SnapParams* h_sp, long long* h_out) {
+  const long long V = g->V, E = g->E;
+  const uint8_t* alive = mk ? mk->alive.as<uint8_t>() : nullptr;
   DevBuf& d_plan = c->ws[WS_PLAN];
   d_plan.alloc(8 * sizeof(long long), c->stream);
   long long* plan = d_plan.as<long long>();
-  DevBuf best0, best1;
-  SnapParams sp{};
-  sp.n = n;
-  sp.m_norm = pos_only ? g->m : n;
-  for (int k = 0; k < n; ++k) sp.target[k] = goal[k];
-  sp.mode = 0;
-  snap_launch(c, g, sp, nullptr, best0, plan + 0);
-
-  for (int k = 0; k < n; ++k) {
-    sp.target[k] = start[k];
-    sp.tlo[k] = -tube_hi[k] - eps;  // (diff >= -tube.hi - EPS_GEO)   graph.py:381
-    sp.thi[k] = -tube_lo[k] + eps;  // (diff <= -tube.lo + EPS_GEO)
+  const SnapParams* spd = nullptr;
+  if (h_sp) {
+    DevBuf& d_sp = c->ws[WS_SNAP];
+    d_sp.alloc(2 * sizeof(SnapParams), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_sp.ptr, h_sp, 2 * sizeof(SnapParams), cudaMemcpyHostToDevice, c->stream));
+    spd = d_sp.as<SnapParams>();
   }
-  DevBuf tmp_reach;
-  if (require_tube) {
-    sp.mode = 1;
-    snap_launch(c, g, sp, nullptr, best1, plan + 1);
+  snap_launch(c, g, sp[0], spd, nullptr, c->ws[WS_BEST0], plan + 0);
+
+  if (sp[1].mode == 1) {
+    snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, nullptr, c->ws[WS_BEST1], plan + 1);
   } else {
     // relaxed mid-run snap: nearest vertex that can still reach vg (graph.py:388-392); the
     // reverse reachability runs on the device (k_reach_coop), cached per (mask, vg) there
     uint8_t* reach;
     long long* rkey;
-    DevBuf tmp_key;
     if (mk) {
       mk->reach.alloc(V, c->stream);
       reach = mk->reach.as<uint8_t>();
@@ -586,12 +817,13 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
         BZG_CHECK_CUDA(cudaMemsetAsync(mk->reach_key.ptr, 0xFF, sizeof(long long), c->stream));
       }
       rkey = mk->reach_key.as<long long>();
-    } else {
-      tmp_reach.alloc(V, c->stream);
-      reach = tmp_reach.as<uint8_t>();
-      tmp_key.alloc(sizeof(long long), c->stream);
-      BZG_CHECK_CUDA(cudaMemsetAsync(tmp_key.ptr, 0xFF, sizeof(long long), c->stream));
-      rkey = tmp_key.as<long long>();
+    } else {  // no mask, no cache: the key is reset every search
+      DevBuf &t_reach = c->ws[WS_NM_REACH], &t_key = c->ws[WS_NM_KEY];
+      t_reach.alloc(V, c->stream);
+      reach = t_reach.as<uint8_t>();
+      t_key.alloc(sizeof(long long), c->stream);
+      BZG_CHECK_CUDA(cudaMemsetAsync(t_key.ptr, 0xFF, sizeof(long long), c->stream));
+      rkey = t_key.as<long long>();
     }
     DevBuf& rflags = c->ws[WS_REACH_FLAGS];
     rflags.alloc(4 * sizeof(int), c->stream);
@@ -605,12 +837,10 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     int* rf = rflags.as<int>();
     void* args[] = {&El, &Vl2, &rs, &rd, &alive, &reach, &rkey, &cpl, &rf};
     launch_coop(c, "k_reach_coop", (const void*)k_reach_coop, dim3(rblocks), dim3(256), args);
-    sp.mode = 2;
-    snap_launch(c, g, sp, reach, best1, plan + 1);
+    snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, reach, c->ws[WS_BEST1], plan + 1);
   }
 
   // ---- the shortest-path tree from v0 (skipped on the device when cached or trivial)
-  DevBuf t_dist, t_parent, t_key;
   unsigned long long* dist;
   int* parent;
   long long* key = nullptr;
@@ -626,6 +856,7 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     parent = mk->parent.as<int>();
     key = mk->tree_key.as<long long>();
   } else {
+    DevBuf &t_dist = c->ws[WS_NM_DIST], &t_parent = c->ws[WS_NM_PARENT];
     t_dist.alloc(V * sizeof(unsigned long long), c->stream);
     t_parent.alloc(V * sizeof(int), c->stream);
     dist = t_dist.as<unsigned long long>();
@@ -635,12 +866,6 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   DevBuf &t_prev = c->ws[WS_SSSP_PREV], &t_pd = c->ws[WS_SSSP_PD], &t_aux = c->ws[WS_SSSP_AUX];
   t_prev.alloc(std::max(V, 1ll) * sizeof(unsigned long long), c->stream);
   t_pd.alloc(std::max(V, 1ll) * sizeof(unsigned long long), c->stream);
-  // aux: counts (8 ints) | stamp (V ints) | qa (V ints) | qb (V ints)
-  t_aux.alloc((8 + 3 * (size_t)std::max(V, 1ll)) * sizeof(int), c->stream);
-  int* counts = t_aux.as<int>();
-  int* stamp = counts + 8;
-  int* qa = stamp + V;
-  int* qb = qa + V;
   // BZG_BF_IMPL=queue|scan|async: k_bf_persistent (frontier queue, returning atomics), k_bf_scan
   // (fire-and-forget relaxation + rescan, two barriers per sweep) or k_bf_async (no barriers).
   const char* bf_env = std::getenv("BZG_BF_IMPL");
@@ -650,21 +875,36 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   // point but re-relaxes far more (cfg3 0.46 ms, cfg5 100k 2.7 ms), and a one-barrier rescan
   // (relax the last frontier and rescan without waiting) measured the same as two barriers
   // (cfg3 0.201 vs 0.208 ms): the sweeps are bound by their dependent loads.
-  const int mode = bfs == "queue" ? 1 : (bfs == "scan" ? 2 : (bfs == "async" ? 3 : (V < 1024 ? 1 : 2)));
+  // tiny graphs: one block in shared memory (k_bf_cta); graphs up to kBfClusterDefaultV: one
+  // cluster (k_bf_cluster); larger: the grid-wide rescan (k_bf_scan)
+  const int cl_size = bf_cluster_size(V);
+  const bool cta_ok = V <= kBfCtaMaxV && E <= kBfCtaMaxE;
+  const int mode = bfs == "queue" ? 1
+                   : bfs == "scan" ? 2
+                   : bfs == "async" ? 3
+                   : bfs == "cta" && cta_ok ? 5
+                   : bfs == "cluster" && cl_size > 0 ? 4
+                   : !bfs.empty() ? 2
+                   : cta_ok ? 5
+                   : cl_size > 0 && V <= kBfClusterDefaultV && E <= kBfClusterDefaultE ? 4
+                   : 2;
   const long long Q = V + 8192 + 64;  // ring: <= V queued (flags) + claimed-unread (one per warp)
-  if (mode == 3) {
+  // aux: counts (8 ints) | stamp (V ints) | qa (V ints) | qb (V ints); async: counts | stamp | ring
+  if (mode == 3)
     t_aux.alloc((8 + (size_t)std::max(V, 1ll) + (size_t)Q) * sizeof(int), c->stream);
-    counts = t_aux.as<int>();
-    stamp = counts + 8;
-    qa = stamp + V;
-    BZG_CHECK_CUDA(cudaMemsetAsync(qa, 0, (size_t)Q * sizeof(int), c->stream));
-  }
+  else
+    t_aux.alloc((8 + 3 * (size_t)std::max(V, 1ll)) * sizeof(int), c->stream);
+  int* counts = t_aux.as<int>();
+  int* stamp = counts + 8;
+  int* qa = stamp + V;
+  int* qb = qa + V;
+  if (mode == 3) BZG_CHECK_CUDA(cudaMemsetAsync(qa, 0, (size_t)Q * sizeof(int), c->stream));
   launch(c, "k_init_tree", k_init_tree, dim3(div_up(std::max(V, 8ll), 256)), dim3(256), 0, V, (const long long*)plan,
          mode, dist, t_prev.as<unsigned long long>(), stamp, parent, t_pd.as<unsigned long long>(), counts, qa);
   const void* bf_kern = mode == 1 ? (const void*)k_bf_persistent
                                   : (mode == 3 ? (const void*)k_bf_async : (const void*)k_bf_scan);
   int per_sm = 0;
-  BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_kern, 256, 0));
+  if (mode != 4) BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bf_kern, 256, 0));
   static const int bf_per_sm_env =
       std::getenv("BZG_BF_BLOCKS_PER_SM") ? std::atoi(std::getenv("BZG_BF_BLOCKS_PER_SM")) : 0;
   // blocks per SM: fewer blocks make the grid barriers cheaper, more hide the relax latency
@@ -678,7 +918,38 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   unsigned long long* pv = t_prev.as<unsigned long long>();
   int maxs = (int)std::min<long long>(V + 2, 1 << 30);
   const long long* cplan = plan;
-  if (mode == 1) {
+  if (mode == 5) {
+    const size_t smem = (size_t)V * (sizeof(unsigned long long) + 3 * sizeof(int));
+    ensure_dyn_smem((const void*)k_bf_cta, smem);
+    launch(c, "k_bf_cta", k_bf_cta, dim3(1), dim3(kBfCtaThreads), smem, Vl, rp, dd, cc, alive, dist, counts, maxs,
+           cplan);
+  } else if (mode == 4) {
+    const long long chunk = div_up(V, cl_size);
+    const size_t smem = bf_cluster_smem(chunk);
+    ensure_dyn_smem((const void*)k_bf_cluster, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl_size);
+    cfg.blockDim = dim3(kBfClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl_size;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaEvent_t ea = nullptr;
+    const bool timed = c->timed("k_bf_cluster");
+    if (timed) { ea = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(ea, c->stream)); }
+    BZG_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_bf_cluster, Vl, chunk, rp, dd, cc, alive, dist, counts, maxs, cplan));
+    c->launches++;
+    if (timed) {
+      cudaEvent_t eb = c->take_event();
+      BZG_CHECK_CUDA(cudaEventRecord(eb, c->stream));
+      c->pending.push_back({"k_bf_cluster", ea, eb});
+    }
+  } else if (mode == 1) {
     void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &stamp, &qa, &qb, &counts, &maxs, &cplan};
     launch_coop(c, "k_bf_persistent", bf_kern, dim3(blocks), dim3(256), args);
   } else if (mode == 3) {
@@ -688,7 +959,7 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
     void* args[] = {&Vl, &rp, &dd, &cc, &alive, &dist, &pv, &qa, &qb, &counts, &maxs, &cplan};
     launch_coop(c, "k_bf_scan", bf_kern, dim3(blocks), dim3(256), args);
   }
-  if (c->trace_on) {
+  if (c->trace_on && !g_capturing) {
     int hc[8];
     long long hp[4];
     BZG_CHECK_CUDA(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, c->stream));
@@ -709,11 +980,17 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   d_out.alloc((V + 3) * sizeof(long long), c->stream);
   launch(c, "k_backtrack", k_backtrack, dim3(1), dim3(32), 0, V, cplan, (const int*)parent,
          (const unsigned long long*)dist, d_out.as<long long>());
-  constexpr long long kHead = 510;
-  const long long head = std::min(V + 2, kHead + 2);
-  long long* h = static_cast<long long*>(c->host_scratch((size_t)(kHead + 2) * sizeof(long long)));
-  BZG_CHECK_CUDA(cudaMemcpyAsync(h, d_out.ptr, head * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  const long long head = std::min<long long>(V + 2, kHead + 2);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h_out, d_out.ptr, head * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// After the stream reached the read-back: the path (empty: None) and its distance; a path
+// longer than the head is completed from d_out with a second copy.
+void path_collect(Ctx* c, const Graph* g, const long long* h, const long long* d_out, std::vector<int64_t>& path,
+                  double* dist_out) {
+  path.clear();
+  *dist_out = INFINITY;
+  const long long head = std::min<long long>(g->V + 2, kHead + 2);
   const long long len = h[0];
   BZG_REQUIRE(len != -2, BZG_ECUDA, "parent chain broken during backtrack");
   if (len < 0) return;  // no snappable start or vg unreachable -> None
@@ -722,11 +999,150 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   path.assign(h + 2, h + 2 + std::min(len, head - 2));
   if (len > head - 2) {  // long path: the rest in a second copy
     path.resize(len);
-    BZG_CHECK_CUDA(cudaMemcpyAsync(path.data() + (head - 2), d_out.as<long long>() + head,
-                                   (len - (head - 2)) * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    BZG_CHECK_CUDA(cudaMemcpyAsync(path.data() + (head - 2), d_out + head, (len - (head - 2)) * sizeof(long long),
+                                   cudaMemcpyDeviceToHost, c->stream));
     BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
   }
   *dist_out = dv;
 }
+
+}  // namespace
+
+// One host synchronisation per search (the path read-back).  (vg, v0) stay on the device
+// (plan); the tree kernels skip themselves when the mask's cached shortest-path tree already
+// belongs to v0 (cfg4 goal updates) or the answer is trivial.  Relaxed snapping computes the
+// reverse reachability to vg on the device (cached per (mask, vg)).
+void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* goal, const double* tube_lo,
+               const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
+               double* dist_out) {
+  BZG_REQUIRE(g->n <= 16, BZG_EUNSUPPORTED, "state dimension too large");
+  BZG_REQUIRE(g->V >= 1, BZG_EINVAL, "graph has no vertices");
+  SnapParams sp[2];
+  snap_params(g, start, goal, tube_lo, tube_hi, eps, pos_only, require_tube, sp);
+  long long* h = static_cast<long long*>(c->host_scratch((size_t)(kHead + 2) * sizeof(long long)));
+  path_enqueue(c, g, mk, sp, nullptr, h);
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  path_collect(c, g, h, c->ws[WS_SSSP_OUT].as<long long>(), path, dist_out);
+}
+
+// ---- bzg_query: the search above captured once per (graph, mask, snapping options)
+struct Query {
+  Ctx* c = nullptr;
+  Graph* g = nullptr;
+  Mask* mk = nullptr;
+  uint64_t version = 0;
+  int64_t E = 0;
+  int pos_only = 0, require_tube = 0;
+  double eps = 0.0;
+  std::vector<double> tube_lo, tube_hi;
+  DevBuf ws[kWsSlots];               // the query's own workspaces (the graph reads their addresses)
+  SnapParams* h_sp = nullptr;        // pinned: [goal, start] parameters, read by the graph's H2D copy
+  long long* h_out = nullptr;        // pinned: the head of the read-back
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0;             // kernel nodes per launch
+};
+
+namespace {
+// run fn with c->ws switched to the query's workspaces
+template <typename F>
+void with_query_ws(Query* q, F&& fn) {
+  Ctx* c = q->c;
+  DevBuf* saved = c->ws;
+  c->ws = q->ws;
+  try {
+    fn();
+  } catch (...) {
+    c->ws = saved;
+    throw;
+  }
+  c->ws = saved;
+}
+}  // namespace
+
+void query_destroy(Query* q) {
+  if (!q) return;
+  if (q->c) cudaStreamSynchronize(q->c->stream);
+  if (q->exec) cudaGraphExecDestroy(q->exec);
+  if (q->graph) cudaGraphDestroy(q->graph);
+  for (auto& w : q->ws) w.release();
+  if (q->h_sp) cudaFreeHost(q->h_sp);
+  if (q->h_out) cudaFreeHost(q->h_out);
+  delete q;
+}
+
+Query* query_create(Ctx* c, Graph* g, Mask* mk, const double* tube_lo, const double* tube_hi, double eps,
+                    int pos_only, int require_tube) {
+  BZG_REQUIRE(g->n <= 16, BZG_EUNSUPPORTED, "state dimension too large");
+  BZG_REQUIRE(g->V >= 1, BZG_EINVAL, "graph has no vertices");
+  Query* q = new Query();
+  try {
+    q->c = c;
+    q->g = g;
+    q->mk = mk;
+    q->version = g->version;
+    q->E = g->E;
+    q->pos_only = pos_only;
+    q->require_tube = require_tube;
+    q->eps = eps;
+    q->tube_lo.assign(tube_lo, tube_lo + g->n);
+    q->tube_hi.assign(tube_hi, tube_hi + g->n);
+    BZG_CHECK_CUDA(cudaMallocHost(&q->h_sp, 2 * sizeof(SnapParams)));
+    BZG_CHECK_CUDA(cudaMallocHost(&q->h_out, (size_t)(kHead + 2) * sizeof(long long)));
+    // warm-up: one eager search (start = goal = the first vertex's neighbourhood: any values do)
+    // sizes every workspace and initialises the mask's cache keys
+    std::vector<double> zero(g->n, 0.0);
+    snap_params(g, zero.data(), zero.data(), tube_lo, tube_hi, eps, pos_only, require_tube, q->h_sp);
+    with_query_ws(q, [&] {
+      path_enqueue(c, g, mk, q->h_sp, q->h_sp, q->h_out);
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      const bool prof = c->profiling;
+      const long long launches0 = c->launches;
+      c->profiling = false;  // no event records inside the graph
+      g_capturing = true;
+      cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        try {
+          path_enqueue(c, g, mk, q->h_sp, q->h_sp, q->h_out);
+        } catch (...) {
+          cudaGraph_t tmp = nullptr;
+          cudaStreamEndCapture(c->stream, &tmp);
+          if (tmp) cudaGraphDestroy(tmp);
+          g_capturing = false;
+          c->profiling = prof;
+          throw;
+        }
+        e = cudaStreamEndCapture(c->stream, &q->graph);
+      }
+      g_capturing = false;
+      c->profiling = prof;
+      q->kernels = c->launches - launches0;
+      c->launches = launches0;
+      BZG_CHECK_CUDA(e);
+      BZG_CHECK_CUDA(cudaGraphInstantiate(&q->exec, q->graph, 0));
+      BZG_CHECK_CUDA(cudaGraphUpload(q->exec, c->stream));
+    });
+  } catch (...) {
+    query_destroy(q);
+    throw;
+  }
+  return q;
+}
+
+void query_run(Query* q, const double* start, const double* goal, std::vector<int64_t>& path, double* dist) {
+  Ctx* c = q->c;
+  Graph* g = q->g;
+  BZG_REQUIRE(g->version == q->version && g->E == q->E && (!q->mk || (q->mk->g == g && q->mk->E == g->E)),
+              BZG_EINVAL, "stale query: the graph's edge set changed after it was captured");
+  // the previous launch finished (query_run synchronises), so the staging area is free
+  snap_params(g, start, goal, q->tube_lo.data(), q->tube_hi.data(), q->eps, q->pos_only, q->require_tube, q->h_sp);
+  BZG_CHECK_CUDA(cudaGraphLaunch(q->exec, c->stream));
+  c->launches += q->kernels;
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  path_collect(c, g, q->h_out, q->ws[WS_SSSP_OUT].as<long long>(), path, dist);
+}
+
+long long query_kernels(const Query* q) { return q->kernels; }
+Ctx* query_ctx(const Query* q) { return q->c; }
 
 }  // namespace bzg

@@ -613,6 +613,68 @@ def find_path(graph: BezierGraph, mask, start, goal, position_only_snap: bool = 
     return out
 
 
+class PathQuery:
+    """Repeated ``find_path(graph, mask, start, goal, ...)`` on one fixed graph and mask -- the
+    goal/start updates of a replanning loop (sim.py:275-408 calls graph.find_path every cycle,
+    graph.py:353-430) -- as one captured CUDA graph (bzg_query): ``q(start, goal)`` returns what
+    ``find_path`` returns with the same options, in one graph launch and one synchronisation.
+    Creating it runs one search (warm-up) and the capture; it holds the graph and mask alive and
+    becomes stale (ValueError) if the graph's edge set is replaced."""
+
+    def __init__(self, graph: BezierGraph, mask, position_only_snap: bool = False, require_tube_snap: bool = True):
+        ctx = graph._ctx
+        self._ctx, self._graph, self._mask = ctx, graph, mask
+        self._h = None
+        self._tmp = None
+        tube = graph.oracle.tube.error
+        tlo, thi = _f64(tube.lo), _f64(tube.hi)
+        mh = None
+        if isinstance(mask, CutMask):
+            mh = mask._device_handle()
+        elif mask is not None:  # a foreign CutMask: its alive bits, owned by the query
+            a = np.ascontiguousarray(mask.alive, dtype=np.uint8)
+            h = C.c_void_p()
+            nat.check(ctx.lib.bzg_mask_from_arrays(ctx.handle, graph._h, nat.ptr(a), None, None, 0, C.byref(h)))
+            mh = self._tmp = h
+        q = C.c_void_p()
+        nat.check(ctx.lib.bzg_query_create(ctx.handle, graph._h, mh, nat.ptr(tlo), nat.ptr(thi), EPS_GEO,
+                                           int(bool(position_only_snap)), int(bool(require_tube_snap)), C.byref(q)))
+        self._h = q
+        self._path = np.empty(graph.num_vertices + 1, dtype=np.int64)
+        self._plen = C.c_int64()
+        self._dist = C.c_double()
+
+    @property
+    def kernels_per_query(self) -> int:
+        n = C.c_int64()
+        nat.check(self._ctx.lib.bzg_query_kernels(self._h, C.byref(n)))
+        return n.value
+
+    def __call__(self, start, goal):
+        start, goal = _f64(start), _f64(goal)
+        nat.check(self._ctx.lib.bzg_query_run(self._h, nat.ptr(start), nat.ptr(goal), nat.ptr(self._path),
+                                              self._path.size, C.byref(self._plen), C.byref(self._dist)))
+        if self._plen.value < 0:
+            return None
+        out = [int(v) for v in self._path[: self._plen.value]]
+        self._graph._cache["last_dist"] = (tuple(out), self._dist.value)
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._ctx.lib.bzg_query_destroy(self._h)
+            self._h = None
+        if getattr(self, "_tmp", None):
+            self._ctx.lib.bzg_mask_destroy(self._tmp)
+            self._tmp = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def path_cost(graph: BezierGraph, path) -> float:
     """Total edge cost along a vertex path, left-to-right sum (graph.py:453-458)."""
     if len(path) < 2:

@@ -376,10 +376,11 @@ def test_recut_cache_equals_full_cut(ctx, golden, name):
     _same_cut(G.cut_graph(gr, moved), G.cut_graph(ref, moved))
 
 
-@pytest.mark.parametrize("impl", ["queue", "scan", "async"])
+@pytest.mark.parametrize("impl", ["queue", "scan", "async", "cluster", "cta"])
 @pytest.mark.parametrize("name", ["cfg2_rf2000", "maze", "hop1500"])
 def test_bellman_ford_variants_reach_the_reference_paths(ctx, golden, name, impl, monkeypatch):
-    """Every Bellman-Ford schedule (frontier queue, rescan, barrier-free asynchronous) reaches the
+    """Every Bellman-Ford schedule (frontier queue, rescan, barrier-free asynchronous, single
+    thread-block cluster, one block in shared memory) reaches the
     same fixed point: the paths (and costs) through the reference's own mask are the golden's,
     and so are the cfg4 goal updates (cfg2)."""
     monkeypatch.setenv("BZG_BF_IMPL", impl)
@@ -400,6 +401,26 @@ def test_bellman_ford_variants_reach_the_reference_paths(ctx, golden, name, impl
             p = G.find_path(gr, RefMask(), start, gl)
             assert (p or []) == list(flat[off:off + lens[k]]), k
             off += lens[k]
+
+
+@pytest.mark.parametrize("cs", [1, 2, 4, 8, 16])
+def test_bellman_ford_cluster_sizes(ctx, golden, cs, monkeypatch):
+    """k_bf_cluster at every cluster size (the owned slices, DSMEM relaxations and the cluster
+    barrier schedule change with it): the golden paths of cfg2 and its goal updates."""
+    monkeypatch.setenv("BZG_BF_IMPL", "cluster")
+    monkeypatch.setenv("BZG_BF_CLUSTER", str(cs))
+    g = golden("cfg2_rf2000")
+    gr, obstacles, start, goal = _build(g, ctx)
+
+    class RefMask:
+        alive = g["alive"]
+
+    assert G.find_path(gr, RefMask(), start, goal) == list(g["path"])
+    lens, flat = g["goal_path_len"], g["goal_paths"]
+    off = 0
+    for k, gl in enumerate(g["goals"][:20]):
+        assert (G.find_path(gr, RefMask(), start, gl) or []) == list(flat[off:off + lens[k]]), k
+        off += lens[k]
 
 
 def test_edge_cases_round2(ctx, golden):

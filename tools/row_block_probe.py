@@ -22,12 +22,12 @@ import bench  # noqa: E402
 from paper_2411_13507_b200 import _native as nat  # noqa: E402
 
 
-def main(cfg="cfg3", steps="5"):
+def main(cfg="cfg3", steps="5", nodes="0"):
     steps = int(steps)
     stream = torch.cuda.Stream()
     ctx = nat.Context(0, stream=stream.cuda_stream)
     nat.set_default_context(ctx)
-    w = bench.workload(cfg)
+    w = bench.workload(cfg, int(nodes))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     out = []
     for G in (1, 2, 4, 8):

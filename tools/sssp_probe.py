@@ -30,7 +30,7 @@ def main(cfg="cfg3", reps="5"):
         alive = np.ascontiguousarray(m.alive)
 
     paths = {}
-    for impl in ("scan", "queue", "async"):
+    for impl in ("cluster", "scan", "queue", "async"):
         os.environ["BZG_BF_IMPL"] = impl
         G.find_path(g, Alive(), w.start, w.goal)
         ctx.reset_stats()
@@ -44,9 +44,9 @@ def main(cfg="cfg3", reps="5"):
         ks = {k: round(v[0] / int(reps), 4) for k, v in st.items()}
         tot = round(sum(v for k, v in ks.items()), 4)
         print(f"{cfg} {impl:6s} V={g.num_vertices} E={g.num_edges} alive={int(m.alive.sum())} hops={len(p or [])} "
-              f"bf={ks.get('k_bf_' + {'scan': 'scan', 'queue': 'persistent', 'async': 'async'}[impl])} all={tot} {ks}",
+              f"bf={ks.get('k_bf_' + {"cluster": "cluster", "scan": "scan", "queue": "persistent", "async": "async"}[impl])} all={tot} {ks}",
               flush=True)
-    assert paths["scan"] == paths["queue"] == paths["async"], paths
+    assert len({str(p) for p in paths.values()}) == 1, paths
 
 
 if __name__ == "__main__":
