@@ -571,10 +571,12 @@ def replanning_bench(args, ctx, stream, rank, world):
 
 
 def recut_bench(ctx, stream, w, graph, steps=20):
-    """Replanning with a moving obstacle (sim.py:324-330, ObstacleTrack.at): every cycle one of
-    the obstacles (round robin) is translated by a few cm and the graph is re-cut, then searched
-    (relaxed snap, as run_closed_loop mid-run).  Device ms per cycle, the full cut vs the re-cut
-    cache (BezierGraph.set_cut_cache), and whether the two masks agree on every cycle."""
+    """Replanning with a moving obstacle (sim.py:324-330, ObstacleTrack.at): every cycle obstacle
+    0 moves a few cm along its track and the graph is re-cut, then searched (relaxed snap, as
+    run_closed_loop mid-run).  Device ms per cycle: the eager full cut, the eager re-cut cache
+    (BezierGraph.set_cut_cache), and the Replanner (cut + search as one captured CUDA graph),
+    re-cutting every obstacle or only the moving one (static / dynamic split); and whether all
+    masks agree on every cycle."""
     import torch
 
     from paper_2411_13507_b200 import graph as G
@@ -586,9 +588,8 @@ def recut_bench(ctx, stream, w, graph, steps=20):
     def lists():
         cur = list(obs)
         for k in range(steps):
-            o = k % len(obs)
-            A = np.asarray(cur[o].A, dtype=np.float64)
-            cur[o] = Polytope(A, np.asarray(cur[o].b, dtype=np.float64) + A @ np.full(m, 0.01 * (1 + k % 3)))
+            A = np.asarray(cur[0].A, dtype=np.float64)
+            cur[0] = Polytope(A, np.asarray(cur[0].b, dtype=np.float64) + A @ np.full(m, 0.01 * (1 + k % 3)))
             yield list(cur)
 
     res, masks = {}, {}
@@ -613,8 +614,33 @@ def recut_bench(ctx, stream, w, graph, steps=20):
         res[mode] = {"cut_p50_ms": float(np.percentile(ms_cut, 50)), "cycle_p50_ms": float(np.percentile(ms_all, 50)),
                      "cycle_p99_ms": float(np.percentile(ms_all, 99))}
     graph.set_cut_cache(0)
-    res["masks_equal_every_cycle"] = masks["full"] == masks["cached"]
-    res["workload"] = f"{w.name}: one of {len(obs)} obstacles moves per cycle, {steps} cycles, cut + relaxed-snap search"
+    # the same cycles through the Replanner: cut + search captured as one CUDA graph
+    from paper_2411_13507_b200.replan import Replanner
+
+    for mode, dyn in (("captured", None), ("captured_split", [True] + [False] * (len(obs) - 1))):
+        rp = Replanner(graph, obs, position_only_snap=True, require_tube_snap=False, dynamic=dyn)
+        rp(obs, w.start, w.goal)
+        ms_all, masks[mode], walls = [], [], []
+        for lst in lists():
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            a.record(stream)
+            rp(lst, w.start, w.goal)
+            b.record(stream)
+            b.synchronize()
+            walls.append(1e3 * (time.perf_counter() - t0))
+            ms_all.append(a.elapsed_time(b))
+            mk = rp.mask()
+            masks[mode].append(np.packbits(mk.alive).tobytes() + mk.provenance_codes.tobytes())
+        info = rp.info()
+        rp.close()
+        res[mode] = {"cycle_p50_ms": float(np.percentile(ms_all, 50)), "cycle_p99_ms": float(np.percentile(ms_all, 99)),
+                     "wall_p50_ms": float(np.percentile(walls, 50)), "kernels_per_cycle": info["kernels_per_cycle"],
+                     "eager_cycles": info["eager_cycles"], "api": "paper_2411_13507_b200.replan.Replanner"}
+    res["masks_equal_every_cycle"] = (masks["full"] == masks["cached"] == masks["captured"] ==
+                                      masks["captured_split"])
+    res["workload"] = f"{w.name}: obstacle 0 of {len(obs)} moves every cycle, {steps} cycles, cut + relaxed-snap search"
     return res
 
 

@@ -48,6 +48,7 @@ typedef struct bzg_ctx bzg_ctx;
 typedef struct bzg_graph bzg_graph;
 typedef struct bzg_mask bzg_mask;
 typedef struct bzg_query bzg_query;
+typedef struct bzg_replanner bzg_replanner;
 
 int bzg_abi_version(void);
 const char* bzg_last_error(void);
@@ -236,6 +237,33 @@ int bzg_query_run(bzg_query* q, const double* start, const double* goal, int64_t
 /* kernels per bzg_query_run (the captured graph's kernel nodes) */
 int bzg_query_kernels(const bzg_query* q, int64_t* n);
 int bzg_query_destroy(bzg_query* q);
+
+/* ---- f2: the replanning cycle as one captured CUDA graph -------------------- */
+/* A cycle of sim.run_closed_loop (sim.py:324-330: re-cut with the moved obstacles, then
+ * graph.find_path, graph.py:302-430) on a fixed graph: bzg_replanner_create runs the first cycle
+ * with the given obstacles eagerly and captures cut + search as one CUDA graph; every
+ * bzg_replanner_run is then one graph launch and one synchronisation, with the obstacle records
+ * and the snapping targets passed through pinned staging.  Results equal bzg_cut_graph +
+ * bzg_find_path on the same inputs.  The obstacle list keeps its count; when its shape (row
+ * counts, box / general kinds) changes or a work list outgrows its capacity, that cycle runs
+ * eagerly (*eager = 1) and the graph is re-captured.  counters: as bzg_mask_copy.  The
+ * replanner's mask holds no per-QP records.  dynamic (n_obs flags, NULL = all): obstacles
+ * flagged 0 are static -- cut once, their per-obstacle outcome rows kept on the device (as
+ * the re-cut cache keeps them) -- and a cycle cuts only the dynamic ones and rebuilds the mask
+ * in list order; a static obstacle passed changed to a later run is re-cut then. */
+int bzg_replanner_create(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_off, const double* A,
+                         const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                         const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps_geo,
+                         int position_only_snap, int require_tube_snap, bzg_replanner** out);
+int bzg_replanner_run(bzg_replanner* rp, int32_t n_obs, const int32_t* row_off, const double* A, const double* b,
+                      const uint8_t* is_box, const double* box_lo, const double* box_hi, const double* start,
+                      const double* goal, int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out,
+                      int64_t counters[6], int32_t* eager);
+/* a new mask (owned by the caller) holding the last cycle's alive set, provenance and counters */
+int bzg_replanner_mask(bzg_replanner* rp, bzg_mask** out);
+/* info: kernels per captured cycle, cycles run, cycles run eagerly, captures */
+int bzg_replanner_info(const bzg_replanner* rp, int64_t info[4]);
+int bzg_replanner_destroy(bzg_replanner* rp);
 
 /* replaces sim._project_on_path (sim.py:220-239): the grid time tau = k h (k < (L-1) *
  * steps_per_hop, steps_per_hop = round(T / h)) along the curve chain through the L path states

@@ -109,6 +109,13 @@ _SIGS = {
     "bzg_query_run": ([_P, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double)], C.c_int),
     "bzg_query_kernels": ([_P, C.POINTER(C.c_int64)], C.c_int),
     "bzg_query_destroy": ([_P], C.c_int),
+    "bzg_replanner_create": ([_P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_int,
+                              C.c_int, C.POINTER(_P)], C.c_int),
+    "bzg_replanner_run": ([_P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64),
+                           C.POINTER(C.c_double), _P, C.POINTER(C.c_int32)], C.c_int),
+    "bzg_replanner_mask": ([_P, C.POINTER(_P)], C.c_int),
+    "bzg_replanner_info": ([_P, _P], C.c_int),
+    "bzg_replanner_destroy": ([_P], C.c_int),
     "bzg_project_on_path": ([_P, C.c_int32, C.c_int32, C.c_double, _P, C.c_int64, _P, C.c_double, C.c_int32, _P,
                              C.POINTER(C.c_double)], C.c_int),
     "bzg_probe_fp64": ([_P, C.c_int, C.POINTER(C.c_double)], C.c_int),

@@ -88,6 +88,7 @@ enum WsSlot {
   WS_PROJ,                                                           // project_on_path
   WS_REACH_FLAGS,
   WS_SNAP, WS_BEST0, WS_BEST1, WS_NM_REACH, WS_NM_KEY, WS_NM_DIST, WS_NM_PARENT,  // find_path
+  WS_OBSGRIDHDR, WS_CUTCNT, WS_CUTOBS, WS_QNEXT,                     // cut staging, counters
   kWsSlots
 };
 
@@ -109,7 +110,7 @@ struct Ctx {
   bool trace_on = std::getenv("BZG_TRACE") != nullptr;
   std::chrono::steady_clock::time_point trace_t = std::chrono::steady_clock::now();
   void trace(const char* what) {
-    if (!trace_on) return;
+    if (!trace_on || g_capturing) return;
     cudaStreamSynchronize(stream);
     const auto now = std::chrono::steady_clock::now();
     std::fprintf(stderr, "[bzg] %-24s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - trace_t).count());
@@ -134,6 +135,7 @@ struct Ctx {
   double grid_key[4] = {0, 0, 0, 0};
   bool grid_sparse = false;
   long long qp_hint = 0;   // QP instances of the last cut: sizes the next cut's QP buffers
+  unsigned long long cut_last_pend = 0, cut_last_gen = 0;  // the last cut's work-list lengths
   double sample_est = 1.0; // acceptance rate of the last sampler run (sizes a single round)
   int* sample_check = nullptr;  // pending single-round sampler count (device), need, candidates
   long long sample_need = 0, sample_count = 0;
@@ -235,6 +237,61 @@ struct ScopedLibLaunch {
   }
 };
 
+// Record fn()'s work on c->stream into an instantiated CUDA graph (stream capture, thread-local
+// mode).  Every workspace must already be sized (g_capturing makes a growth an error) and no
+// event may be recorded (profiling is paused).  *kernels = launches counted while capturing.
+template <typename F>
+cudaGraphExec_t capture_graph(Ctx* c, F&& fn, long long* kernels, cudaGraph_t* graph_out) {
+  const bool prof = c->profiling;
+  const long long launches0 = c->launches;
+  c->profiling = false;
+  g_capturing = true;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    try {
+      fn();
+    } catch (...) {
+      cudaGraph_t tmp = nullptr;
+      cudaStreamEndCapture(c->stream, &tmp);
+      if (tmp) cudaGraphDestroy(tmp);
+      g_capturing = false;
+      c->profiling = prof;
+      c->launches = launches0;
+      throw;
+    }
+    e = cudaStreamEndCapture(c->stream, &graph);
+  }
+  g_capturing = false;
+  c->profiling = prof;
+  *kernels = c->launches - launches0;
+  c->launches = launches0;
+  BZG_CHECK_CUDA(e);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  if (ei != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    BZG_CHECK_CUDA(ei);
+  }
+  BZG_CHECK_CUDA(cudaGraphUpload(exec, c->stream));
+  *graph_out = graph;
+  return exec;
+}
+
+// run fn with c->ws switched to another workspace set (a captured plan's own buffers)
+template <typename F>
+void with_ws(Ctx* c, DevBuf* ws, F&& fn) {
+  DevBuf* saved = c->ws;
+  c->ws = ws;
+  try {
+    fn();
+  } catch (...) {
+    c->ws = saved;
+    throw;
+  }
+  c->ws = saved;
+}
+
 inline unsigned div_up(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
 // ---------------------------------------------------------------- graph / mask
@@ -318,9 +375,31 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
                const double* tube_hi, double eps, int pos_only, int require_tube, std::vector<int64_t>& path,
                double* dist);
 
+// A search whose launches read start/goal from pinned staging (PathStage): enqueue is
+// capturable; collect reads the result after the stream synchronised.
+struct PathStage;
+PathStage* path_stage_create(const Graph* g, const double* tube_lo, const double* tube_hi, double eps, int pos_only,
+                             int require_tube);
+void path_stage_set(PathStage* s, const Graph* g, const double* start, const double* goal);
+void path_stage_enqueue(Ctx* c, Graph* g, Mask* mk, PathStage* s);
+void path_stage_collect(Ctx* c, const Graph* g, PathStage* s, std::vector<int64_t>& path, double* dist);
+void path_stage_destroy(PathStage* s);
+
 // A find_path on a fixed (graph, mask) captured as a CUDA graph (bzg_query): start and goal go
 // through pinned host memory, so a query is one graph launch and one synchronisation.
 struct Query;
+struct Replanner;
+Replanner* replanner_create(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                            const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                            const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo,
+                            const double* tube_hi, double eps, int pos_only, int require_tube);
+void replanner_run(Replanner* r, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                   const uint8_t* is_box, const double* box_lo, const double* box_hi, const double* start,
+                   const double* goal, std::vector<int64_t>& path, double* dist, int* eager_out);
+void replanner_destroy(Replanner* r);
+Ctx* replanner_ctx(const Replanner* r);
+const Mask* replanner_mask(const Replanner* r);
+void replanner_info(const Replanner* r, int64_t info[4]);
 Query* query_create(Ctx* c, Graph* g, Mask* mk, const double* tube_lo, const double* tube_hi, double eps,
                     int pos_only, int require_tube);
 void query_run(Query* q, const double* start, const double* goal, std::vector<int64_t>& path, double* dist);

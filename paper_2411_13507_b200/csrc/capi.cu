@@ -14,6 +14,8 @@ struct bzg_mask : Mask {};
 // bzg_query is opaque here (Query is defined with the search, k_sssp.cu)
 static Query* as_query(bzg_query* q) { return reinterpret_cast<Query*>(q); }
 static const Query* as_query(const bzg_query* q) { return reinterpret_cast<const Query*>(q); }
+static Replanner* as_rp(bzg_replanner* r) { return reinterpret_cast<Replanner*>(r); }
+static const Replanner* as_rp(const bzg_replanner* r) { return reinterpret_cast<const Replanner*>(r); }
 
 namespace {
 
@@ -633,6 +635,89 @@ int bzg_query_destroy(bzg_query* q) {
     if (!q) return;
     set_device(query_ctx(as_query(q)));
     query_destroy(as_query(q));
+  });
+}
+
+int bzg_replanner_create(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_off, const double* A,
+                         const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                         const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps_geo,
+                         int position_only_snap, int require_tube_snap, bzg_replanner** out) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && g && cfg && tube_lo && tube_hi && out, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(row_off && A && b && is_box && box_lo && box_hi, BZG_EINVAL, "obstacle arrays missing");
+    set_device(ctx);
+    *out = reinterpret_cast<bzg_replanner*>(replanner_create(ctx, g, n_obs, row_off, A, b, is_box, box_lo, box_hi,
+                                                             dynamic, cfg, tube_lo, tube_hi, eps_geo, position_only_snap,
+                                                             require_tube_snap));
+  });
+}
+
+int bzg_replanner_run(bzg_replanner* rp, int32_t n_obs, const int32_t* row_off, const double* A, const double* b,
+                      const uint8_t* is_box, const double* box_lo, const double* box_hi, const double* start,
+                      const double* goal, int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out,
+                      int64_t counters[6], int32_t* eager) {
+  return guarded([&] {
+    BZG_REQUIRE(rp && start && goal && path_len, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(row_off && A && b && is_box && box_lo && box_hi, BZG_EINVAL, "obstacle arrays missing");
+    Replanner* r = as_rp(rp);
+    set_device(replanner_ctx(r));
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    int eg = 0;
+    replanner_run(r, n_obs, row_off, A, b, is_box, box_lo, box_hi, start, goal, path, &dist, &eg);
+    if (path.empty()) {
+      *path_len = -1;
+    } else {
+      *path_len = (int64_t)path.size();
+      BZG_REQUIRE(path_out && path_cap >= (int64_t)path.size(), BZG_EINVAL, "path buffer too small");
+      std::memcpy(path_out, path.data(), path.size() * sizeof(int64_t));
+    }
+    if (dist_out) *dist_out = dist;
+    if (counters)
+      for (int i = 0; i < 6; ++i) counters[i] = replanner_mask(r)->counters[i];
+    if (eager) *eager = eg;
+  });
+}
+
+int bzg_replanner_mask(bzg_replanner* rp, bzg_mask** out) {
+  bzg_mask* mk = nullptr;
+  int rc = guarded([&] {
+    BZG_REQUIRE(rp && out, BZG_EINVAL, "null argument");
+    const Replanner* r = as_rp(rp);
+    Ctx* c = replanner_ctx(r);
+    set_device(c);
+    const Mask* src = replanner_mask(r);
+    mk = new bzg_mask();
+    mk->g = src->g;
+    mk->ctx = c;
+    mk->E = src->E;
+    mk->n_obs = src->n_obs;
+    for (int i = 0; i < 6; ++i) mk->counters[i] = src->counters[i];
+    mk->alive.alloc(std::max<long long>(src->E, 1), c->stream);
+    mk->prov.alloc(std::max<long long>(src->E, 1), c->stream);
+    if (src->E > 0) {
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->alive.ptr, src->alive.ptr, src->E, cudaMemcpyDeviceToDevice, c->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->prov.ptr, src->prov.ptr, src->E, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+  if (rc == BZG_OK) *out = mk; else delete mk;
+  return rc;
+}
+
+int bzg_replanner_info(const bzg_replanner* rp, int64_t info[4]) {
+  return guarded([&] {
+    BZG_REQUIRE(rp && info, BZG_EINVAL, "null argument");
+    replanner_info(as_rp(rp), info);
+  });
+}
+
+int bzg_replanner_destroy(bzg_replanner* rp) {
+  return guarded([&] {
+    if (!rp) return;
+    Replanner* r = as_rp(rp);
+    set_device(replanner_ctx(r));
+    replanner_destroy(r);
   });
 }
 

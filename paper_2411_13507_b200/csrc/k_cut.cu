@@ -281,10 +281,11 @@ struct CutBits {
   uint32_t* kill;
   uint32_t* qsafe;
   uint32_t* qunsafe;
-  long long Wb;  // words per obstacle row: ceil(E / 32)
+  long long Wb;      // words per obstacle row: ceil(E / 32)
+  long long stride;  // words from one obstacle's row to the next (Wb, or 3 Wb in a slot-major pool)
 };
-__device__ __forceinline__ void set_bit(uint32_t* rowbase, long long Wb, int o, long long e) {
-  atomicOr(rowbase + (size_t)o * Wb + (e >> 5), 1u << (e & 31));
+__device__ __forceinline__ void set_bit(uint32_t* rowbase, long long stride, int o, long long e) {
+  atomicOr(rowbase + (size_t)o * stride + (e >> 5), 1u << (e & 31));
 }
 
 constexpr int kGridCells = 64;  // per axis
@@ -325,9 +326,10 @@ __global__ void k_obs_grid_extent(DParams dp, const double* __restrict__ Vx, lon
 // spans the obstacles' box bounds (lo0, lo1)-(hi0, hi1) (host) grown by R = 1.25 max sampled
 // extent + 0.02 (edges above R - 0.01 test every obstacle); thread 0 publishes it in gpp.
 template <int M>
-__global__ void k_obs_grid_masks(const ObsRec<M>* __restrict__ obs, int n_obs, int chunk, double lo0, double lo1,
-                                 double hi0, double hi1, ObsGrid* __restrict__ gpp,
+__global__ void k_obs_grid_masks(const ObsRec<M>* __restrict__ obs, int n_obs, int chunk,
+                                 const double* __restrict__ bnd, ObsGrid* __restrict__ gpp,
                                  unsigned long long* __restrict__ masks) {
+  const double lo0 = bnd[0], lo1 = bnd[1], hi0 = bnd[2], hi1 = bnd[3];  // the obstacles' xy bounds
   const int cell = blockIdx.x * blockDim.x + threadIdx.x, ch = blockIdx.y;
   if (cell >= kGridCells * kGridCells) return;
   ObsGrid gp;
@@ -373,7 +375,7 @@ size_t heur_smem(int nob) {
 template <int G, int M>
 __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
                                 const int* __restrict__ dst, const ObsRec<M>* __restrict__ obs,
-                                const CertRec<M>* __restrict__ certs, int o0, int o1, double wmax,
+                                const CertRec<M>* __restrict__ certs, int o0, int o1, const double* __restrict__ wmaxp,
                                 double margin, int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                                 unsigned long long* __restrict__ n_pend, unsigned long long cap,
                                 unsigned long long* __restrict__ pend, unsigned long long* __restrict__ n_gen,
@@ -382,6 +384,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
                                 CutBits bits) {
   constexpr int N = G * M;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const double wmax = *wmaxp;  // the chunk's x-window width (-1: no window), from the staged obstacles
   const bool use_grid = grid != nullptr;  // the host passes the grid only when it is sparse
   const int nob = o1 - o0;
   // shared memory: [CertRec x nob][sorted lo[0] x nob][pos x nob][ObsRec x nob][per-warp pass-2 staging]
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
           c2 += code == 2;
           if (code == 0) {
             atomicMin(s_kill + owner, o0 + oi);
-            if (bits.kill) set_bit(bits.kill, bits.Wb, o0 + oi, e0 + owner);
+            if (bits.kill) set_bit(bits.kill, bits.stride, o0 + oi, e0 + owner);
           }
           item = ((unsigned long long)(e0 + owner) << 20) | (unsigned long long)(o0 + oi);
         }
@@ -646,7 +649,7 @@ __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const i
       code = general_code<G, M, RC>(P, obs[oi], margin, kEpsGeo);
       if (code == 0) {
         atomicMin(first_kill + e, oi);
-        if (bits.kill) set_bit(bits.kill, bits.Wb, oi, e);
+        if (bits.kill) set_bit(bits.kill, bits.stride, oi, e);
       }
       if (code >= 0) atomicAdd(counters + code, 1ull);
       if (code == -1) atomicOr(counters + 7, 1ull);
@@ -670,11 +673,11 @@ __global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long 
     if (safe[t]) {
       qp_saved[e] = 1;
       ++s;
-      if (bits.kill) set_bit(bits.qsafe, bits.Wb, o, e);
+      if (bits.kill) set_bit(bits.qsafe, bits.stride, o, e);
     } else {
       atomicMin(qp_kill + e, o);
       ++u;
-      if (bits.kill) set_bit(bits.qunsafe, bits.Wb, o, e);
+      if (bits.kill) set_bit(bits.qunsafe, bits.stride, o, e);
     }
   }
   typedef cub::BlockReduce<unsigned long long, 256> BR;
@@ -847,14 +850,196 @@ void dispatch_rows(int qp_rows, F&& f) {
 
 namespace {
 
-void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
-                    const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
-                    Mask* mk, CutBits cbits) {
+// ---- a cut in three steps: host preparation (cut_prepare: obstacle records, pass-1
+// certificates, per-chunk x-windows and the xy bounds, staged in ONE blob uploaded with one
+// copy), the launches (cut_enqueue: no host round trip, every buffer from c->ws or the mask,
+// so a replanner can capture it), and the host finish after the stream synchronised.
+struct CutPrep {
+  std::vector<unsigned char> blob;
+  int n_obs = 0, qp_rows = 0, chunk = 1, n_chunks = 1;
+  bool big = false, canon_all = true, any_general = false, grid_cand = false;
+  double blo[2] = {INFINITY, INFINITY}, bhi[2] = {-INFINITY, -INFINITY};
+  size_t off_rec = 0, off_wmax = 0, off_bnd = 0, off_big = 0;
+  // everything a captured launch sequence depends on besides the blob's contents
+  bool same_shape(const CutPrep& o) const {
+    return blob.size() == o.blob.size() && n_obs == o.n_obs && qp_rows == o.qp_rows && chunk == o.chunk &&
+           n_chunks == o.n_chunks && big == o.big && canon_all == o.canon_all && any_general == o.any_general &&
+           grid_cand == o.grid_cand;
+  }
+};
+
+inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+template <int Mc>
+void cut_prepare_t(const Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                   const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                   int qp_rows, CutPrep& p) {
+  using Rec = ObsRec<Mc>;
+  const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
+  // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
+  p.chunk = std::min(64, std::max(1, (int)(96 * 1024 / sizeof(Rec))));
+  std::vector<double> wmax;
+  const std::vector<CertRec<Mc>> hc = fill_cert<Mc>(h, n_obs, p.chunk, wmax);
+  if (std::getenv("BZG_NO_OBS_WINDOW"))  // read per call (tests toggle it): test every obstacle
+    for (double& w : wmax) w = -1.0;
+  p.n_obs = n_obs;
+  p.qp_rows = qp_rows;
+  p.n_chunks = (int)wmax.size();
+  p.big = qp_rows > kObsRows;
+  p.canon_all = true;
+  p.any_general = false;
+  for (int o = 0; o < n_obs; ++o) {
+    p.canon_all = p.canon_all && h[o].canon != 0.0;
+    p.any_general = p.any_general || h[o].is_box == 0.0;
+    for (int k = 0; k < 2 && k < Mc; ++k) {
+      p.blo[k] = std::min(p.blo[k], h[o].lo[k]);
+      p.bhi[k] = std::max(p.bhi[k], h[o].hi[k]);
+    }
+  }
+  p.grid_cand = Mc >= 2 && n_obs >= 8 && g->E > 0 && std::getenv("BZG_NO_OBS_GRID") == nullptr;  // per call
+  // [CertRec x n][ObsRec x n][wmax x chunks][xy bounds][ObsRec<M, kObsRowsBig> x n when big]
+  const size_t cert_bytes = sizeof(CertRec<Mc>) * hc.size();  // CertRec is 16-byte aligned and sized
+  p.off_rec = align16(cert_bytes);
+  p.off_wmax = align16(p.off_rec + sizeof(Rec) * h.size());
+  p.off_bnd = align16(p.off_wmax + sizeof(double) * wmax.size());
+  p.off_big = align16(p.off_bnd + 4 * sizeof(double));
+  std::vector<ObsRec<Mc, kObsRowsBig>> hbig;
+  if (p.big) hbig = fill_obs<Mc, kObsRowsBig>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
+  p.blob.assign(p.off_big + sizeof(ObsRec<Mc, kObsRowsBig>) * hbig.size(), 0);
+  std::memcpy(p.blob.data(), hc.data(), cert_bytes);
+  std::memcpy(p.blob.data() + p.off_rec, h.data(), sizeof(Rec) * h.size());
+  std::memcpy(p.blob.data() + p.off_wmax, wmax.data(), sizeof(double) * wmax.size());
+  const double bnd[4] = {p.blo[0], Mc >= 2 ? p.blo[1] : 0.0, p.bhi[0], Mc >= 2 ? p.bhi[1] : 0.0};
+  std::memcpy(p.blob.data() + p.off_bnd, bnd, sizeof(bnd));
+  if (p.big) std::memcpy(p.blob.data() + p.off_big, hbig.data(), sizeof(ObsRec<Mc, kObsRowsBig>) * hbig.size());
+}
+
+// Work-list capacities and the obstacle-grid mode of one cut_enqueue: grid 0 = no grid,
+// 1 = build it (k_obs_grid_extent / k_obs_grid_masks) and use it, 2 = use the one built
+// earlier on this stream.
+struct CutCaps {
+  unsigned long long cap = 0, gen_cap = 1;
+  long long qcap = 0;
+  int grid = 0;
+};
+
+template <int Gc, int Mc>
+void grid_build(Ctx* c, Graph* g, const CutPrep& p, const unsigned char* d_blob) {
   const long long E = g->E;
-  const int m = g->m;
-  BZG_REQUIRE(n_obs >= 0 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
-  BZG_REQUIRE(E < (1ll << 43), BZG_EUNSUPPORTED, "edge count too large for the QP work list");
-  const int qp_rows = check_obstacles(n_obs, row_off, is_box, m);
+  DParams dp{};
+  for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
+  DevBuf &d_grid = c->ws[WS_OBSGRIDHDR], &d_gmask = c->ws[WS_OBSGRID];
+  d_grid.alloc(sizeof(ObsGrid), c->stream);
+  BZG_CHECK_CUDA(cudaMemsetAsync(d_grid.ptr, 0, sizeof(ObsGrid), c->stream));
+  d_gmask.alloc((size_t)p.n_chunks * kGridCells * kGridCells * sizeof(unsigned long long), c->stream);
+  launch(c, "k_obs_grid_extent", k_obs_grid_extent<Gc, Mc>, dim3(div_up(std::min(E, 65536ll), 256)), dim3(256), 0, dp,
+         g->vertices.as<double>(), E, g->src.as<int>(), g->dst.as<int>(), d_grid.as<ObsGrid>());
+  launch(c, "k_obs_grid_masks", k_obs_grid_masks<Mc>, dim3(kGridCells * kGridCells / 256, (unsigned)p.n_chunks),
+         dim3(256), 0, reinterpret_cast<const ObsRec<Mc>*>(d_blob + p.off_rec), p.n_obs, p.chunk,
+         reinterpret_cast<const double*>(d_blob + p.off_bnd), d_grid.as<ObsGrid>(),
+         d_gmask.as<unsigned long long>());
+}
+
+// The cut's launches: reset, (grid), screen per obstacle chunk, general pairs, Cut-QP stage,
+// verdicts, mask, and the counters' read-back into h_cnt (8 words: codes 0/1/2, QP safe /
+// unsafe, QP work-list length, general-list length, empty-polytope flag).  Also resets the
+// mask's cached search keys (its alive set changes).  No host synchronisation.
+template <int Gc, int Mc>
+void cut_enqueue(Ctx* c, Graph* g, const CutPrep& p, const unsigned char* d_blob, const bzg_cut_config* cfg, Mask* mk,
+                 CutBits cbits, const CutCaps& cc, unsigned long long* h_cnt) {
+  const long long E = g->E;
+  const int n_obs = p.n_obs;
+  DParams dp{};
+  for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
+  const CertRec<Mc>* d_cert = reinterpret_cast<const CertRec<Mc>*>(d_blob);
+  const ObsRec<Mc>* d_recs = reinterpret_cast<const ObsRec<Mc>*>(d_blob + p.off_rec);
+  const double* d_wmax = reinterpret_cast<const double*>(d_blob + p.off_wmax);
+  const void* d_qp_obs = p.big ? (const void*)(d_blob + p.off_big) : (const void*)d_recs;
+  DevBuf &d_kill = c->ws[WS_KILL], &d_qkill = c->ws[WS_QKILL], &d_saved = c->ws[WS_SAVED], &d_cnt = c->ws[WS_CUTCNT];
+  DevBuf &d_pend = c->ws[WS_PEND], &d_gen = c->ws[WS_GEN];
+  d_kill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
+  d_qkill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
+  d_saved.alloc(std::max(E, 1ll), c->stream);
+  d_cnt.alloc(16 * sizeof(unsigned long long), c->stream);  // [8]: pass-2 pairs (diagnostic)
+  d_pend.alloc(cc.cap * sizeof(unsigned long long), c->stream);
+  d_gen.alloc(cc.gen_cap * sizeof(unsigned long long), c->stream);
+  unsigned long long* dcnt = d_cnt.as<unsigned long long>();
+  BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 16 * sizeof(unsigned long long), c->stream));
+  BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
+  launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
+  launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
+  if (cbits.kill && n_obs > 0)  // the recorded outcome rows (n_obs rows of Wb words, stride apart)
+    for (uint32_t* rows : {cbits.kill, cbits.qsafe, cbits.qunsafe})
+      BZG_CHECK_CUDA(cudaMemset2DAsync(rows, cbits.stride * sizeof(uint32_t), 0, cbits.Wb * sizeof(uint32_t), n_obs,
+                                       c->stream));
+  for (DevBuf* key : {&mk->tree_key, &mk->reach_key})  // the mask's alive set changes: no cached tree
+    if (key->ptr) BZG_CHECK_CUDA(cudaMemsetAsync(key->ptr, 0xFF, sizeof(long long), c->stream));
+  if (cc.grid == 1) grid_build<Gc, Mc>(c, g, p, d_blob);
+  const bool use_grid = cc.grid != 0;
+  DevBuf &d_grid = c->ws[WS_OBSGRIDHDR], &d_gmask = c->ws[WS_OBSGRID];
+
+  // ---- heuristic screen (obstacle chunks sized to shared memory)
+  for (int o0 = 0; o0 < n_obs; o0 += p.chunk) {
+    const int o1 = std::min(n_obs, o0 + p.chunk);
+    const size_t smem = heur_smem<Gc, Mc>(o1 - o0);
+    auto kern = k_cut_heuristic<Gc, Mc>;
+    ensure_dyn_smem((const void*)kern, smem);
+    const unsigned long long* gm =
+        use_grid ? d_gmask.as<unsigned long long>() + (size_t)(o0 / p.chunk) * kGridCells * kGridCells : nullptr;
+    const long long hblocks = std::min<long long>(div_up(E, kHeurThreads), (long long)c->num_sms * 3);
+    launch(c, "k_cut_heuristic", kern, dim3((unsigned)hblocks), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(),
+           E, g->src.as<int>(), g->dst.as<int>(), d_recs, d_cert, o0, o1, d_wmax + o0 / p.chunk, cfg->heur_margin,
+           d_kill.as<int>(), dcnt, dcnt + 5, cc.cap, d_pend.as<unsigned long long>(), dcnt + 6, cc.gen_cap,
+           d_gen.as<unsigned long long>(), use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm, cbits);
+  }
+  if (p.any_general) {
+    // general obstacles: cut_heuristic past branch 1 over the device-side list, appending
+    // to the same QP work list
+    const long long gblocks = std::min<long long>(div_up((long long)cc.gen_cap, 64), c->num_sms * 16ll);
+    if (p.big)
+      launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRowsBig>, dim3((unsigned)gblocks), dim3(64), 0, dp,
+             g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(),
+             reinterpret_cast<const ObsRec<Mc, kObsRowsBig>*>(d_blob + p.off_big), d_gen.as<unsigned long long>(),
+             (long long)cc.gen_cap, (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt,
+             dcnt + 5, cc.cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
+    else
+      launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRows>, dim3((unsigned)gblocks), dim3(64), 0, dp,
+             g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs, d_gen.as<unsigned long long>(),
+             (long long)cc.gen_cap, (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt,
+             dcnt + 5, cc.cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
+  }
+  c->trace("cut: heuristic");
+
+  // ---- Cut-QP over the device-side work list (its length stays on the device, dcnt[5]); the
+  // per-instance buffers have capacity qcap, checked after the read-back
+  DevBuf &d_safe = c->ws[WS_QSAFE], &d_qst = c->ws[WS_QSTATUS], &d_qit = c->ws[WS_QITERS], &d_qdl = c->ws[WS_QDELTA];
+  if (E > 0 && n_obs > 0) {
+    const long long qcap = cc.qcap;
+    d_safe.alloc(qcap, c->stream);
+    d_qst.alloc(qcap, c->stream);
+    d_qit.alloc(qcap * sizeof(int), c->stream);
+    d_qdl.alloc(qcap * sizeof(double), c->stream);
+    dispatch_rows<Mc>(p.qp_rows, [&](auto C_) {
+      constexpr int Cc = decltype(C_)::value;
+      QpJob job{g, {}, d_qp_obs, p.canon_all, d_pend.as<unsigned long long>(), qcap, dcnt + 5, cfg,
+                cfg->qp_polish ? 1 : 0, polish_screen(), mk, &d_safe, d_qst.as<int8_t>(), d_qit.as<int>(),
+                d_qdl.as<double>()};
+      for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
+      qp_solve(c, Gc, Mc, Cc, job);
+    });
+    c->trace("cut: qp");
+    launch(c, "k_qp_verdicts", k_qp_verdicts, dim3((unsigned)std::min<long long>(div_up(qcap, 256), c->num_sms * 8ll)),
+           dim3(256), 0, d_pend.as<unsigned long long>(), qcap, (const unsigned long long*)(dcnt + 5),
+           d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), dcnt, cbits);
+  }
+  launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, n_obs,
+         d_kill.as<int>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), mk->alive.as<uint8_t>(), mk->prov.as<uint8_t>());
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h_cnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+}
+
+// the mask fields a cut sets on the host before its launches
+void mask_begin(Ctx* c, Graph* g, Mask* mk, int n_obs) {
+  const long long E = g->E;
   mk->g = g;
   mk->ctx = c;
   mk->E = E;
@@ -863,239 +1048,102 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
   mk->prov.alloc(std::max(E, 1ll), c->stream);
   for (int i = 0; i < 6; ++i) mk->counters[i] = 0;
   mk->counters[0] = E * (long long)n_obs;
-  mk->tree_key.release();
   mk->reach_vg = -1;
-  mk->reach_key.release();
   mk->n_qp = 0;
+}
 
-  DParams dp{};
-  for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
-  // BZG_TRACE=1: host wall time of each cut phase (synchronising), for diagnosing launch gaps
-  static const bool trace_on = std::getenv("BZG_TRACE") != nullptr;
-  auto t_prev = std::chrono::steady_clock::now();
-  auto trace = [&](const char* what) {
-    if (!trace_on) return;
-    cudaStreamSynchronize(c->stream);
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[bzg cut] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t_prev).count());
-    t_prev = now;
-  };
+// counters of a finished cut from its read-back
+void mask_counters(Mask* mk, const unsigned long long* hcnt) {
+  for (int i = 0; i < 5; ++i) mk->counters[1 + i] = (long long)hcnt[i];
+}
+
+// first cut on this context: half the screen's list capacity; afterwards the last count + 25%
+CutCaps default_caps(Ctx* c, const Graph* g, const CutPrep& p) {
+  CutCaps cc;
+  cc.cap = (unsigned long long)std::max<long long>(1 << 20, g->E * (long long)p.n_obs / 32);
+  cc.gen_cap = p.any_general ? cc.cap : 1;
+  cc.qcap = c->qp_hint > 0 ? std::min<long long>((long long)cc.cap, c->qp_hint + c->qp_hint / 4 + 1024)
+                           : (long long)cc.cap / 2;
+  return cc;
+}
+
+// The grid decision: the grid pays only when the grown obstacles leave most cells empty (large
+// maps); a dense grid costs more per edge than it saves.  That is known after building it (the
+// fill count needs a host round trip), so the decision is kept per context for the same obstacle
+// count and bounds: repeated cuts of one map decide once.  Returns the CutCaps grid mode.
+template <int Gc, int Mc>
+int grid_decide(Ctx* c, Graph* g, const CutPrep& p, const unsigned char* d_blob) {
+  if (!p.grid_cand) return 0;
+  const bool known = c->grid_nobs == p.n_obs && c->grid_key[0] == p.blo[0] && c->grid_key[1] == p.blo[1] &&
+                     c->grid_key[2] == p.bhi[0] && c->grid_key[3] == p.bhi[1];
+  if (known) return c->grid_sparse ? 1 : 0;
+  grid_build<Gc, Mc>(c, g, p, d_blob);
+  ObsGrid* hg = static_cast<ObsGrid*>(c->host_scratch(sizeof(ObsGrid) + 8 * sizeof(unsigned long long)));
+  BZG_CHECK_CUDA(cudaMemcpyAsync(hg, c->ws[WS_OBSGRIDHDR].ptr, sizeof(ObsGrid), cudaMemcpyDeviceToHost, c->stream));
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  // sparse: under 15% of (cell, obstacle) bits set (cfg3's 5 x 5 map is denser and runs faster
+  // without the lookups; cfg5's large maps are far sparser)
+  const bool sparse = hg->pop * 20 < hg->bits * 3;
+  if (c->trace_on)
+    std::fprintf(stderr, "[bzg cut] obstacle grid fill %.3f, R %.3f -> %s\n", (double)hg->pop / (double)hg->bits,
+                 hg->R, sparse ? "used" : "not used");
+  c->grid_nobs = p.n_obs;
+  c->grid_key[0] = p.blo[0];
+  c->grid_key[1] = p.blo[1];
+  c->grid_key[2] = p.bhi[0];
+  c->grid_key[3] = p.bhi[1];
+  c->grid_sparse = sparse;
+  return sparse ? 2 : 0;  // built above
+}
+
+// One stream of launches and ONE host synchronisation: the screen's pending count stays on the
+// device and every QP kernel reads it there; the per-instance buffers are sized by a capacity
+// (the previous cut's count with headroom).  The read-back at the end checks the capacities; an
+// overflow (rare: a first cut much larger than the hint) reruns the cut with exact sizes.
+void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                    const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                    Mask* mk, CutBits cbits) {
+  const long long E = g->E;
+  const int m = g->m;
+  BZG_REQUIRE(n_obs >= 0 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
+  BZG_REQUIRE(E < (1ll << 43), BZG_EUNSUPPORTED, "edge count too large for the QP work list");
+  const int qp_rows = check_obstacles(n_obs, row_off, is_box, m);
+  mask_begin(c, g, mk, n_obs);
   dispatch_cut(g->gamma, m, [&](auto G_, auto M_) {
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
-    using Rec = ObsRec<Mc>;
-    const std::vector<Rec> h = fill_obs<Mc>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
-    // obstacles per launch: fits shared memory and the 64-bit per-edge "hard" mask
-    const int chunk = std::min(64, std::max(1, (int)(96 * 1024 / sizeof(Rec))));
-    std::vector<double> wmax;
-    const std::vector<CertRec<Mc>> hc = fill_cert<Mc>(h, n_obs, chunk, wmax);
-    if (std::getenv("BZG_NO_OBS_WINDOW"))  // read per call (tests toggle it): test every obstacle
-      for (double& w : wmax) w = -1.0;
-    DevBuf d_cnt;
-    DevBuf &d_kill = c->ws[WS_KILL], &d_qkill = c->ws[WS_QKILL], &d_saved = c->ws[WS_SAVED];
-    // one upload: [CertRec x n][ObsRec x n] (CertRec is 16-byte aligned and sized; ObsRec needs 8)
-    const size_t cert_bytes = sizeof(CertRec<Mc>) * hc.size();
-    std::vector<unsigned char> hb(cert_bytes + sizeof(Rec) * h.size());
-    std::memcpy(hb.data(), hc.data(), cert_bytes);
-    std::memcpy(hb.data() + cert_bytes, h.data(), sizeof(Rec) * h.size());
-    DevBuf d_obs_all;
-    d_obs_all.alloc(hb.size(), c->stream);
-    BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs_all.ptr, hb.data(), hb.size(), cudaMemcpyHostToDevice, c->stream));
-    const CertRec<Mc>* d_cert = d_obs_all.as<CertRec<Mc>>();
-    const Rec* d_recs = reinterpret_cast<const Rec*>(static_cast<const unsigned char*>(d_obs_all.ptr) + cert_bytes);
-    // obstacles with more rows than the staged records: every obstacle also as a kObsRowsBig
-    // record, read by the general screen and by the Cut-QP (C = kObsRowsBig) of this cut
-    const bool big = qp_rows > kObsRows;
-    DevBuf d_obs_big;
-    if (big) {
-      const std::vector<ObsRec<Mc, kObsRowsBig>> hbig =
-          fill_obs<Mc, kObsRowsBig>(n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg->eps_geo);
-      d_obs_big.alloc(sizeof(ObsRec<Mc, kObsRowsBig>) * hbig.size(), c->stream);
-      BZG_CHECK_CUDA(cudaMemcpyAsync(d_obs_big.ptr, hbig.data(), sizeof(ObsRec<Mc, kObsRowsBig>) * hbig.size(),
-                                     cudaMemcpyHostToDevice, c->stream));
-      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));  // hbig leaves scope
-    }
-    const void* d_qp_obs = big ? d_obs_big.ptr : (const void*)d_recs;
-    d_kill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
-    d_qkill.alloc(std::max(E, 1ll) * sizeof(int), c->stream);
-    d_saved.alloc(std::max(E, 1ll), c->stream);
-    d_cnt.alloc(16 * sizeof(unsigned long long), c->stream);  // [8]: pass-2 pairs (diagnostic)
-    BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 16 * sizeof(unsigned long long), c->stream));
-    BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
-    launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
-    launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
-    trace("setup");
-
-    // ---- heuristic screen (obstacle chunks sized to shared memory)
-    unsigned long long cap = (unsigned long long)std::max<long long>(1 << 20, E * (long long)n_obs / 32);
-    bool any_general = false;
-    for (int o = 0; o < n_obs; ++o) any_general |= h[o].is_box == 0.0;
-    unsigned long long gen_cap = any_general ? cap : 1;
-    DevBuf &d_pend = c->ws[WS_PEND], &d_gen = c->ws[WS_GEN];
+    CutPrep p;
+    cut_prepare_t<Mc>(g, n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg, qp_rows, p);
+    DevBuf& d_blob = c->ws[WS_CUTOBS];
+    d_blob.alloc(p.blob.size(), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(d_blob.ptr, p.blob.data(), p.blob.size(), cudaMemcpyHostToDevice, c->stream));
+    const unsigned char* db = d_blob.as<unsigned char>();
+    CutCaps cc = default_caps(c, g, p);
+    cc.grid = grid_decide<Gc, Mc>(c, g, p, db);
     unsigned long long* hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
-    unsigned long long* dcnt = d_cnt.as<unsigned long long>();
-    // spatial pre-screen grid (ObsGrid) for maps with enough obstacles to pay for it
-    const int n_chunks = (n_obs + chunk - 1) / chunk;
-    const bool grid_off = std::getenv("BZG_NO_OBS_GRID") != nullptr;  // read per call (tests toggle it)
-    bool use_grid = Mc >= 2 && n_obs >= 8 && E > 0 && !grid_off;
-    DevBuf d_grid;
-    DevBuf& d_gmask = c->ws[WS_OBSGRID];
-    if (use_grid) {
-      double blo[2] = {INFINITY, INFINITY}, bhi[2] = {-INFINITY, -INFINITY};
-      for (int o = 0; o < n_obs; ++o)
-        for (int k = 0; k < 2; ++k) {
-          blo[k] = std::min(blo[k], h[o].lo[k]);
-          bhi[k] = std::max(bhi[k], h[o].hi[k]);
-        }
-      // The grid pays only when the grown obstacles leave most cells empty (large maps); a
-      // dense grid costs more per edge than it saves.  That is known after building it (the
-      // fill count needs a host round trip), so the decision is kept per context for the same
-      // obstacle count and bounds: repeated cuts of one map decide once.
-      const bool known = c->grid_nobs == n_obs && c->grid_key[0] == blo[0] && c->grid_key[1] == blo[1] &&
-                         c->grid_key[2] == bhi[0] && c->grid_key[3] == bhi[1];
-      if (known && !c->grid_sparse) {
-        use_grid = false;
-      } else {
-        d_grid.alloc(sizeof(ObsGrid), c->stream);
-        BZG_CHECK_CUDA(cudaMemsetAsync(d_grid.ptr, 0, sizeof(ObsGrid), c->stream));
-        d_gmask.alloc((size_t)n_chunks * kGridCells * kGridCells * sizeof(unsigned long long), c->stream);
-        launch(c, "k_obs_grid_extent", k_obs_grid_extent<Gc, Mc>, dim3(div_up(std::min(E, 65536ll), 256)), dim3(256),
-               0, dp, g->vertices.as<double>(), E, g->src.as<int>(), g->dst.as<int>(), d_grid.as<ObsGrid>());
-        launch(c, "k_obs_grid_masks", k_obs_grid_masks<Mc>, dim3(kGridCells * kGridCells / 256, (unsigned)n_chunks),
-               dim3(256), 0, d_recs, n_obs, chunk, blo[0], blo[1], bhi[0], bhi[1], d_grid.as<ObsGrid>(),
-               d_gmask.as<unsigned long long>());
-        if (!known) {
-          ObsGrid* hg = static_cast<ObsGrid*>(c->host_scratch(sizeof(ObsGrid) + 8 * sizeof(unsigned long long)));
-          BZG_CHECK_CUDA(cudaMemcpyAsync(hg, d_grid.ptr, sizeof(ObsGrid), cudaMemcpyDeviceToHost, c->stream));
-          BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-          // sparse: under 15% of (cell, obstacle) bits set (cfg3's 5 x 5 map is denser and runs
-          // faster without the lookups; cfg5's large maps are far sparser)
-          use_grid = hg->pop * 20 < hg->bits * 3;
-          if (c->trace_on)
-            std::fprintf(stderr, "[bzg cut] obstacle grid fill %.3f, R %.3f -> %s\n", (double)hg->pop / (double)hg->bits,
-                         hg->R, use_grid ? "used" : "not used");
-          c->grid_nobs = n_obs;
-          c->grid_key[0] = blo[0];
-          c->grid_key[1] = blo[1];
-          c->grid_key[2] = bhi[0];
-          c->grid_key[3] = bhi[1];
-          c->grid_sparse = use_grid;
-          hcnt = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long)));
-        }
-      }
-    }
-    // One stream of launches and ONE host synchronisation: the screen's pending count stays on
-    // the device (dcnt[5]) and every QP kernel reads it there; the per-instance buffers are sized
-    // by a capacity (the previous cut's count with headroom).  The read-back at the end checks
-    // the capacities; an overflow (rare: a first cut much larger than the hint) reruns the
-    // affected stage with exact sizes.
-    bool canon_all = true;
-    for (int o = 0; o < n_obs; ++o) canon_all = canon_all && h[o].canon != 0.0;
-    DevBuf &d_safe = c->ws[WS_QSAFE], &d_qst = c->ws[WS_QSTATUS], &d_qit = c->ws[WS_QITERS],
-           &d_qdl = c->ws[WS_QDELTA];
-    const bool any_pairs = E > 0 && n_obs > 0;
-    // first cut on this context: half the screen's list capacity; afterwards the last count + 25%
-    long long qcap = c->qp_hint > 0 ? std::min<long long>((long long)cap, c->qp_hint + c->qp_hint / 4 + 1024)
-                                    : (long long)cap / 2;
-    auto run_qp_stage = [&]() {
-      if (!any_pairs) return;
-      d_safe.alloc(qcap, c->stream);
-      d_qst.alloc(qcap, c->stream);
-      d_qit.alloc(qcap * sizeof(int), c->stream);
-      d_qdl.alloc(qcap * sizeof(double), c->stream);
-      dispatch_rows<Mc>(qp_rows, [&](auto C_) {
-        constexpr int Cc = decltype(C_)::value;
-        QpJob job{g, {}, d_qp_obs, canon_all, d_pend.as<unsigned long long>(), qcap, dcnt + 5, cfg,
-                  cfg->qp_polish ? 1 : 0, polish_screen(), mk, &d_safe, d_qst.as<int8_t>(), d_qit.as<int>(),
-                  d_qdl.as<double>()};
-        for (int k = 0; k < 64; ++k) job.D[k] = dp.D[k];
-        qp_solve(c, Gc, Mc, Cc, job);
-      });
-      trace("qp");
-      launch(c, "k_qp_verdicts", k_qp_verdicts, dim3((unsigned)std::min<long long>(div_up(qcap, 256), c->num_sms * 8ll)),
-             dim3(256), 0, d_pend.as<unsigned long long>(), qcap, (const unsigned long long*)(dcnt + 5),
-             d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), dcnt, cbits);
-    };
-    auto finalize_and_read = [&]() {
-      launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, n_obs,
-             d_kill.as<int>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), mk->alive.as<uint8_t>(),
-             mk->prov.as<uint8_t>());
-      BZG_CHECK_CUDA(cudaMemcpyAsync(hcnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-    };
     for (int attempt = 0;; ++attempt) {
       BZG_REQUIRE(attempt < 4, BZG_ECUDA, "cut work lists kept overflowing");
-      d_pend.alloc(cap * sizeof(unsigned long long), c->stream);
-      d_gen.alloc(gen_cap * sizeof(unsigned long long), c->stream);
-      for (int o0 = 0; o0 < n_obs; o0 += chunk) {
-        const int o1 = std::min(n_obs, o0 + chunk);
-        const size_t smem = heur_smem<Gc, Mc>(o1 - o0);
-        auto kern = k_cut_heuristic<Gc, Mc>;
-        ensure_dyn_smem((const void*)kern, smem);
-        const unsigned long long* gm =
-            use_grid ? d_gmask.as<unsigned long long>() + (size_t)(o0 / chunk) * kGridCells * kGridCells : nullptr;
-        const long long hblocks = std::min<long long>(div_up(E, kHeurThreads), (long long)c->num_sms * 3);
-        launch(c, "k_cut_heuristic", kern, dim3((unsigned)hblocks), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(), E,
-               g->src.as<int>(), g->dst.as<int>(), d_recs, d_cert, o0, o1, wmax[o0 / chunk], cfg->heur_margin,
-               d_kill.as<int>(), dcnt,
-               dcnt + 5, cap, d_pend.as<unsigned long long>(), dcnt + 6, gen_cap, d_gen.as<unsigned long long>(),
-               use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm, cbits);
-      }
-      if (any_general) {
-        // general obstacles: cut_heuristic past branch 1 over the device-side list, appending
-        // to the same QP work list
-        const long long gblocks = std::min<long long>(div_up((long long)gen_cap, 64), c->num_sms * 16ll);
-        if (big)
-          launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRowsBig>, dim3((unsigned)gblocks), dim3(64), 0, dp,
-                 g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(),
-                 (const ObsRec<Mc, kObsRowsBig>*)d_obs_big.ptr, d_gen.as<unsigned long long>(), (long long)gen_cap,
-                 (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt, dcnt + 5, cap,
-                 d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
-        else
-          launch(c, "k_cut_general", k_cut_general<Gc, Mc, kObsRows>, dim3((unsigned)gblocks), dim3(64), 0, dp,
-                 g->vertices.as<double>(), g->src.as<int>(), g->dst.as<int>(), d_recs, d_gen.as<unsigned long long>(),
-                 (long long)gen_cap, (const unsigned long long*)(dcnt + 6), cfg->heur_margin, d_kill.as<int>(), dcnt,
-                 dcnt + 5, cap, d_pend.as<unsigned long long>(), (int8_t*)nullptr, cbits);
-      }
-      trace("heuristic");
-      run_qp_stage();
-      finalize_and_read();
+      cut_enqueue<Gc, Mc>(c, g, p, db, cfg, mk, cbits, cc, hcnt);
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
       BZG_REQUIRE(hcnt[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
-      const unsigned long long n_gen = hcnt[6];
-      if (hcnt[5] <= cap && n_gen <= gen_cap) break;
-      // a screen work list overflowed: grow it and rerun the cut from a clean state
-      cap = std::max(cap, hcnt[5] + 1024);
-      if (n_gen > gen_cap) gen_cap = n_gen + 1024;
-      BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 16 * sizeof(unsigned long long), c->stream));
-      BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
-      launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
-      launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
-      if (cbits.kill) BZG_CHECK_CUDA(cudaMemsetAsync(cbits.kill, 0, (size_t)3 * n_obs * cbits.Wb * 4, c->stream));
+      const unsigned long long n_pend = hcnt[5], n_gen = hcnt[6];
+      if (n_pend <= cc.cap && n_gen <= cc.gen_cap && (long long)n_pend <= cc.qcap) break;
+      // a work list overflowed: grow it and rerun the cut from a clean state
+      if (n_pend > cc.cap) cc.cap = n_pend + 1024;
+      if (n_gen > cc.gen_cap) cc.gen_cap = n_gen + 1024;
+      cc.qcap = std::max<long long>(cc.qcap, (long long)n_pend);
+      if (cc.grid == 1) cc.grid = 2;  // built by the first attempt
     }
-    long long n_inst = (long long)hcnt[5];
-    if (n_inst > qcap) {
-      // the QP buffers were too small for this cut: rerun the QP stage (and the mask) exactly
-      qcap = n_inst;
-      unsigned long long zero2[2] = {0, 0};
-      BZG_CHECK_CUDA(cudaMemcpyAsync(dcnt + 3, zero2, sizeof(zero2), cudaMemcpyHostToDevice, c->stream));
-      BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
-      launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
-      if (cbits.kill)  // QP verdict rows only: the kill rows of the screen stand
-        BZG_CHECK_CUDA(cudaMemsetAsync(cbits.qsafe, 0, (size_t)2 * n_obs * cbits.Wb * 4, c->stream));
-      run_qp_stage();
-      finalize_and_read();
-    }
+    const long long n_inst = (long long)hcnt[5];
     c->qp_hint = n_inst;
+    c->cut_last_pend = hcnt[5];
+    c->cut_last_gen = hcnt[6];
     if (c->trace_on) {
       unsigned long long h8 = 0;
-      BZG_CHECK_CUDA(cudaMemcpy(&h8, d_cnt.as<unsigned long long>() + 8, sizeof(h8), cudaMemcpyDeviceToHost));
+      BZG_CHECK_CUDA(cudaMemcpy(&h8, c->ws[WS_CUTCNT].as<unsigned long long>() + 8, sizeof(h8), cudaMemcpyDeviceToHost));
       std::fprintf(stderr, "[bzg cut] pairs %lld, exact codes (pass 2) %llu, code0 %llu code1 %llu code2 %llu\n",
                    E * (long long)n_obs, h8, hcnt[0], hcnt[1], hcnt[2]);
     }
-    mk->counters[1] = (long long)hcnt[0];
-    mk->counters[2] = (long long)hcnt[1];
-    mk->counters[3] = (long long)hcnt[2];
-    mk->counters[4] = (long long)hcnt[3];
-    mk->counters[5] = (long long)hcnt[4];
+    mask_counters(mk, hcnt);
     // per-QP records of the mask, exact size, filled asynchronously after the read-back
     mk->n_qp = n_inst;
     if (n_inst > 0) {
@@ -1104,13 +1152,14 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
       mk->qp_delta.alloc(n_inst * sizeof(double), c->stream);
       mk->qp_edge.alloc(n_inst * sizeof(long long), c->stream);
       mk->qp_obs.alloc(n_inst * sizeof(int), c->stream);
-      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_status.ptr, d_qst.ptr, n_inst, cudaMemcpyDeviceToDevice, c->stream));
-      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_iters.ptr, d_qit.ptr, n_inst * sizeof(int), cudaMemcpyDeviceToDevice,
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_status.ptr, c->ws[WS_QSTATUS].ptr, n_inst, cudaMemcpyDeviceToDevice,
                                      c->stream));
-      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_delta.ptr, d_qdl.ptr, n_inst * sizeof(double), cudaMemcpyDeviceToDevice,
-                                     c->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_iters.ptr, c->ws[WS_QITERS].ptr, n_inst * sizeof(int),
+                                     cudaMemcpyDeviceToDevice, c->stream));
+      BZG_CHECK_CUDA(cudaMemcpyAsync(mk->qp_delta.ptr, c->ws[WS_QDELTA].ptr, n_inst * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, c->stream));
       launch(c, "k_unpack_pend", k_unpack_pend, dim3(div_up(n_inst, 256)), dim3(256), 0,
-             d_pend.as<unsigned long long>(), n_inst, mk->qp_edge.as<long long>(), mk->qp_obs.as<int>());
+             c->ws[WS_PEND].as<unsigned long long>(), n_inst, mk->qp_edge.as<long long>(), mk->qp_obs.as<int>());
     }
   });
 }
@@ -1226,16 +1275,9 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
     cc.stamp[best] = cc.clock;
     new_slot[i] = best;
   }
-  mk->g = g;
-  mk->ctx = c;
-  mk->E = E;
-  mk->n_obs = n_obs;
-  mk->alive.alloc(std::max(E, 1ll), c->stream);
-  mk->prov.alloc(std::max(E, 1ll), c->stream);
-  mk->tree_key.release();
-  mk->reach_vg = -1;
-  mk->reach_key.release();
-  mk->n_qp = 0;
+  mask_begin(c, g, mk, n_obs);
+  for (DevBuf* key : {&mk->tree_key, &mk->reach_key})  // the mask's alive set changes: no cached tree
+    if (key->ptr) BZG_CHECK_CUDA(cudaMemsetAsync(key->ptr, 0xFF, sizeof(long long), c->stream));
   const int nm = (int)miss.size();
   if (nm > 0) {
     // the misses as a sub-list, cut with their outcome rows recorded
@@ -1255,7 +1297,7 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
     tmp.alloc((size_t)3 * nm * Wb * sizeof(uint32_t), c->stream);
     BZG_CHECK_CUDA(cudaMemsetAsync(tmp.ptr, 0, (size_t)3 * nm * Wb * sizeof(uint32_t), c->stream));
     uint32_t* tk = tmp.as<uint32_t>();
-    CutBits bits{tk, tk + (size_t)nm * Wb, tk + (size_t)2 * nm * Wb, Wb};
+    CutBits bits{tk, tk + (size_t)nm * Wb, tk + (size_t)2 * nm * Wb, Wb, Wb};
     try {
       cut_graph_impl(c, g, nm, sro.data(), sA.data(), sb.data(), sbox.data(), slo.data(), shi.data(), cfg, mk, bits);
     } catch (...) {  // the new slots hold no outcome rows: forget them
@@ -1317,6 +1359,302 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
 }
 
 }  // namespace
+
+// ---- Replanner (bzg_replanner): cut + find_path on a fixed graph as ONE captured CUDA graph.
+// A replanning cycle (sim.py:324-330 re-cuts with the moved obstacles, then graph.find_path) on
+// the device is ~20-30 launches whose inputs change only through the obstacle blob and the
+// snapping parameters; both go through pinned staging, so a cycle is one memcpy into pinned
+// memory, one graph launch and one synchronisation.  With a static / dynamic split, the static
+// obstacles are cut once (their per-obstacle outcome rows kept in a slot-major pool, as the
+// re-cut cache keeps them) and a cycle cuts only the dynamic ones, writing their rows into the
+// pool, and rebuilds alive / provenance in list order (k_cut_combine).  The capture is valid
+// while the dynamic list keeps its shape (count, rows, box / canonical / general kinds:
+// CutPrep::same_shape) and the work lists fit their capacities; otherwise the cycle runs
+// eagerly and is re-captured.
+struct Replanner {
+  Ctx* c = nullptr;
+  Graph* g = nullptr;
+  uint64_t version = 0;
+  int64_t E = 0, Wb = 0;
+  int n_obs = 0;
+  bzg_cut_config cfg{};
+  Mask mk;                                 // the replanner's mask (rewritten every cycle)
+  bool split = false;                      // static / dynamic split
+  std::vector<int> stat, dyn;              // list positions of the static / dynamic obstacles
+  std::string static_key;                  // the static obstacles as last cut (change check)
+  long long static_cnt[5] = {0, 0, 0, 0, 0};  // their code-0 / code-1 / QP pairs, QP safe / unsafe
+  DevBuf pool;                             // slot-major outcome rows, 3 Wb words per obstacle
+  DevBuf slots;                            // list position -> pool slot (static first, then dynamic)
+  CutPrep shape;                           // the captured layout (of the dynamic list)
+  CutCaps caps;
+  unsigned char* h_blob = nullptr;         // pinned: the obstacle blob the graph uploads
+  size_t h_blob_bytes = 0;
+  unsigned long long* h_cnt = nullptr;     // pinned: the cut's counters
+  PathStage* ps = nullptr;
+  DevBuf ws[kWsSlots];                     // own workspaces (the graph reads their addresses)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0, runs = 0, eager = 0, captures = 0;
+};
+
+namespace {
+
+// obstacles [idx...] of a list as a list of their own
+struct SubList {
+  std::vector<int32_t> ro{0};
+  std::vector<double> A, b, lo, hi;
+  std::vector<uint8_t> box;
+  int n() const { return (int)box.size(); }
+};
+SubList sublist(const std::vector<int>& idx, int m, const int32_t* row_off, const double* A, const double* b,
+                const uint8_t* is_box, const double* box_lo, const double* box_hi) {
+  SubList s;
+  for (int o : idx) {
+    const int r0 = row_off[o], r1 = row_off[o + 1];
+    s.ro.push_back(s.ro.back() + (r1 - r0));
+    s.A.insert(s.A.end(), A + (size_t)r0 * m, A + (size_t)r1 * m);
+    s.b.insert(s.b.end(), b + r0, b + r1);
+    s.box.push_back(is_box[o]);
+    s.lo.insert(s.lo.end(), box_lo + (size_t)o * m, box_lo + (size_t)(o + 1) * m);
+    s.hi.insert(s.hi.end(), box_hi + (size_t)o * m, box_hi + (size_t)(o + 1) * m);
+  }
+  return s;
+}
+std::string sublist_key(const SubList& s) {
+  std::string k;
+  auto add = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  add(s.ro.data(), s.ro.size() * sizeof(int32_t));
+  add(s.A.data(), s.A.size() * sizeof(double));
+  add(s.b.data(), s.b.size() * sizeof(double));
+  add(s.box.data(), s.box.size());
+  add(s.lo.data(), s.lo.size() * sizeof(double));
+  add(s.hi.data(), s.hi.size() * sizeof(double));
+  return k;
+}
+
+// pool rows of the dynamic obstacles (slots n_static ..)
+CutBits dyn_bits(Replanner* r) {
+  uint32_t* base = r->pool.as<uint32_t>() + (size_t)r->stat.size() * 3 * r->Wb;
+  return CutBits{base, base + r->Wb, base + 2 * r->Wb, r->Wb, 3 * r->Wb};
+}
+
+// the static obstacles' outcome rows and counts (eager; on creation and when they change)
+void replanner_cut_static(Replanner* r, const SubList& st) {
+  Ctx* c = r->c;
+  Mask tmp;
+  uint32_t* base = r->pool.as<uint32_t>();
+  with_ws(c, r->ws, [&] {
+    cut_graph_impl(c, r->g, st.n(), st.ro.data(), st.A.data(), st.b.data(), st.box.data(), st.lo.data(),
+                   st.hi.data(), &r->cfg, &tmp, CutBits{base, base + r->Wb, base + 2 * r->Wb, r->Wb, 3 * r->Wb});
+  });
+  for (int i = 0; i < 5; ++i) r->static_cnt[i] = tmp.counters[1 + i];
+  r->static_key = sublist_key(st);
+}
+
+// the whole list's counters from the static ones and a dynamic cut's codes (h: its read-back)
+void replanner_counters(Replanner* r, const unsigned long long* h) {
+  r->mk.counters[0] = r->E * (long long)r->n_obs;
+  for (int i = 0; i < 5; ++i) r->mk.counters[1 + i] = r->static_cnt[i] + (long long)h[i];
+}
+
+void replanner_combine(Replanner* r) {
+  Ctx* c = r->c;
+  launch(c, "k_cut_combine", k_cut_combine, dim3(div_up(r->E, 256)), dim3(256), 0, r->E, r->n_obs,
+         (const uint32_t*)r->pool.as<uint32_t>(), r->Wb, (const int*)r->slots.as<int>(), r->mk.alive.as<uint8_t>(),
+         r->mk.prov.as<uint8_t>());
+}
+
+void replanner_drop_graph(Replanner* r) {
+  if (r->exec) cudaGraphExecDestroy(r->exec);
+  if (r->graph) cudaGraphDestroy(r->graph);
+  r->exec = nullptr;
+  r->graph = nullptr;
+}
+
+// one cycle's launches: upload the staged blob, cut (the dynamic obstacles when split, then the
+// combination with the static rows), search
+template <int Gc, int Mc>
+void replanner_enqueue(Replanner* r) {
+  Ctx* c = r->c;
+  DevBuf& d_blob = c->ws[WS_CUTOBS];
+  d_blob.alloc(r->shape.blob.size(), c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(d_blob.ptr, r->h_blob, r->shape.blob.size(), cudaMemcpyHostToDevice, c->stream));
+  cut_enqueue<Gc, Mc>(c, r->g, r->shape, d_blob.as<unsigned char>(), &r->cfg, &r->mk,
+                      r->split ? dyn_bits(r) : CutBits{}, r->caps, r->h_cnt);
+  if (r->split) replanner_combine(r);
+  path_stage_enqueue(c, r->g, &r->mk, r->ps);
+}
+
+// (re)capture for the layout of p, after an eager cycle on the same obstacles (c->qp_hint and
+// the grid decision are this list's)
+template <int Gc, int Mc>
+void replanner_capture(Replanner* r, const CutPrep& p, unsigned long long seen_pend, unsigned long long seen_gen) {
+  Ctx* c = r->c;
+  replanner_drop_graph(r);
+  r->shape = p;
+  CutCaps cc = default_caps(c, r->g, p);
+  cc.cap = std::max(cc.cap, seen_pend + seen_pend / 4 + 1024);
+  if (p.any_general) cc.gen_cap = std::max(cc.gen_cap, seen_gen + seen_gen / 4 + 1024);
+  cc.qcap = std::max<long long>(cc.qcap, (long long)(seen_pend + seen_pend / 4 + 1024));
+  cc.qcap = std::min<long long>(cc.qcap, (long long)cc.cap);
+  cc.grid = p.grid_cand && c->grid_sparse && c->grid_nobs == p.n_obs ? 1 : 0;
+  r->caps = cc;
+  if (r->h_blob_bytes < p.blob.size()) {
+    if (r->h_blob) cudaFreeHost(r->h_blob);
+    r->h_blob = nullptr;
+    r->h_blob_bytes = 0;
+    BZG_CHECK_CUDA(cudaMallocHost(&r->h_blob, p.blob.size()));
+    r->h_blob_bytes = p.blob.size();
+  }
+  std::memcpy(r->h_blob, p.blob.data(), p.blob.size());
+  const long long counters[6] = {r->mk.counters[0], r->mk.counters[1], r->mk.counters[2], r->mk.counters[3],
+                                 r->mk.counters[4], r->mk.counters[5]};
+  with_ws(c, r->ws, [&] {
+    replanner_enqueue<Gc, Mc>(r);  // sizes every workspace for these capacities
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    r->exec = capture_graph(c, [&] { replanner_enqueue<Gc, Mc>(r); }, &r->kernels, &r->graph);
+  });
+  for (int i = 0; i < 6; ++i) r->mk.counters[i] = counters[i];  // (the warm-up rewrote them)
+  ++r->captures;
+}
+
+}  // namespace
+
+void replanner_destroy(Replanner* r) {
+  if (!r) return;
+  if (r->c) cudaStreamSynchronize(r->c->stream);
+  replanner_drop_graph(r);
+  for (auto& w : r->ws) w.release();
+  path_stage_destroy(r->ps);
+  if (r->h_blob) cudaFreeHost(r->h_blob);
+  if (r->h_cnt) cudaFreeHost(r->h_cnt);
+  delete r;
+}
+
+// One cycle: the cut of the obstacle list and the search from start to goal.  *eager_out = 1
+// when the cycle could not use the captured graph (shape change, work-list overflow) and ran
+// eagerly (then it was re-captured).
+void replanner_run(Replanner* r, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                   const uint8_t* is_box, const double* box_lo, const double* box_hi, const double* start,
+                   const double* goal, std::vector<int64_t>& path, double* dist, int* eager_out) {
+  Ctx* c = r->c;
+  Graph* g = r->g;
+  const int m = g->m;
+  BZG_REQUIRE(g->version == r->version && g->E == r->E, BZG_EINVAL,
+              "stale replanner: the graph's edge set changed after it was created");
+  BZG_REQUIRE(n_obs == r->n_obs, BZG_EINVAL, "a replanner keeps its obstacle count");
+  check_obstacles(n_obs, row_off, is_box, m);
+  ++r->runs;
+  *eager_out = 0;
+  // the list the cycle cuts: the dynamic obstacles (split) or all of them
+  SubList dl;
+  if (r->split) {
+    const SubList st = sublist(r->stat, m, row_off, A, b, is_box, box_lo, box_hi);
+    if (sublist_key(st) != r->static_key) replanner_cut_static(r, st);  // rows are data: the graph stays valid
+    dl = sublist(r->dyn, m, row_off, A, b, is_box, box_lo, box_hi);
+  }
+  const int nc = r->split ? dl.n() : n_obs;
+  const int32_t* ro = r->split ? dl.ro.data() : row_off;
+  const double* cA = r->split ? dl.A.data() : A;
+  const double* cb = r->split ? dl.b.data() : b;
+  const uint8_t* cbox = r->split ? dl.box.data() : is_box;
+  const double* clo = r->split ? dl.lo.data() : box_lo;
+  const double* chi = r->split ? dl.hi.data() : box_hi;
+  const int qp_rows = check_obstacles(nc, ro, cbox, m);
+  dispatch_cut(g->gamma, m, [&](auto G_, auto M_) {
+    constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+    CutPrep p;
+    cut_prepare_t<Mc>(g, nc, ro, cA, cb, cbox, clo, chi, &r->cfg, qp_rows, p);
+    path_stage_set(r->ps, g, start, goal);  // no launch of this replanner is pending
+    if (r->exec && p.same_shape(r->shape)) {
+      std::memcpy(r->h_blob, p.blob.data(), p.blob.size());
+      BZG_CHECK_CUDA(cudaGraphLaunch(r->exec, c->stream));
+      c->launches += r->kernels;
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      const unsigned long long* h = r->h_cnt;
+      BZG_REQUIRE(h[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
+      if (h[5] <= r->caps.cap && h[6] <= r->caps.gen_cap && (long long)h[5] <= r->caps.qcap) {
+        if (r->split) replanner_counters(r, h); else mask_counters(&r->mk, h);
+        r->mk.n_qp = 0;
+        with_ws(c, r->ws, [&] { path_stage_collect(c, g, r->ps, path, dist); });
+        return;
+      }
+    }
+    // eager cycle on the replanner's workspaces, then a capture for this layout
+    *eager_out = 1;
+    ++r->eager;
+    with_ws(c, r->ws, [&] {
+      cut_graph_impl(c, g, nc, ro, cA, cb, cbox, clo, chi, &r->cfg, &r->mk, r->split ? dyn_bits(r) : CutBits{});
+      if (r->split) {
+        const unsigned long long h[5] = {(unsigned long long)r->mk.counters[1], (unsigned long long)r->mk.counters[2],
+                                         (unsigned long long)r->mk.counters[3], (unsigned long long)r->mk.counters[4],
+                                         (unsigned long long)r->mk.counters[5]};
+        r->mk.n_obs = n_obs;
+        replanner_counters(r, h);
+        replanner_combine(r);
+      }
+      path_stage_enqueue(c, g, &r->mk, r->ps);
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      path_stage_collect(c, g, r->ps, path, dist);
+    });
+    replanner_capture<Gc, Mc>(r, p, c->cut_last_pend, c->cut_last_gen);
+  });
+}
+
+Ctx* replanner_ctx(const Replanner* r) { return r->c; }
+const Mask* replanner_mask(const Replanner* r) { return &r->mk; }
+void replanner_info(const Replanner* r, int64_t info[4]) {
+  info[0] = r->kernels;
+  info[1] = r->runs;
+  info[2] = r->eager;
+  info[3] = r->captures;
+}
+
+Replanner* replanner_create(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                            const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                            const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo,
+                            const double* tube_hi, double eps, int pos_only, int require_tube) {
+  BZG_REQUIRE(n_obs >= 1 && n_obs < (1 << 20), BZG_EINVAL, "a replanner needs at least one obstacle");
+  BZG_REQUIRE(g->E >= 1, BZG_EINVAL, "a replanner needs a graph with edges");
+  check_obstacles(n_obs, row_off, is_box, g->m);
+  Replanner* r = new Replanner();
+  try {
+    r->c = c;
+    r->g = g;
+    r->version = g->version;
+    r->E = g->E;
+    r->Wb = (g->E + 31) / 32;
+    r->n_obs = n_obs;
+    r->cfg = *cfg;
+    for (int o = 0; o < n_obs; ++o) (dynamic && !dynamic[o] ? r->stat : r->dyn).push_back(o);
+    BZG_REQUIRE(!r->dyn.empty(), BZG_EINVAL, "a replanner needs at least one dynamic obstacle");
+    r->split = !r->stat.empty();
+    r->ps = path_stage_create(g, tube_lo, tube_hi, eps, pos_only, require_tube);
+    BZG_CHECK_CUDA(cudaMallocHost(&r->h_cnt, 8 * sizeof(unsigned long long)));
+    if (r->split) {
+      r->pool.alloc((size_t)3 * n_obs * r->Wb * sizeof(uint32_t), c->stream);
+      std::vector<int> slot(n_obs);
+      for (size_t k = 0; k < r->stat.size(); ++k) slot[r->stat[k]] = (int)k;
+      for (size_t k = 0; k < r->dyn.size(); ++k) slot[r->dyn[k]] = (int)(r->stat.size() + k);
+      r->slots.alloc(n_obs * sizeof(int), c->stream);
+      BZG_CHECK_CUDA(cudaMemcpyAsync(r->slots.ptr, slot.data(), n_obs * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));  // (slot leaves scope)
+      replanner_cut_static(r, sublist(r->stat, g->m, row_off, A, b, is_box, box_lo, box_hi));
+    }
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    int eager = 0;
+    std::vector<double> zero(g->n, 0.0);
+    // the first cycle runs eagerly (sizing, grid decision, QP count) and captures
+    replanner_run(r, n_obs, row_off, A, b, is_box, box_lo, box_hi, zero.data(), zero.data(), path, &dist, &eager);
+    r->runs = 0;
+    r->eager = 0;
+  } catch (...) {
+    replanner_destroy(r);
+    throw;
+  }
+  return r;
+}
 
 void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
                const uint8_t* is_box, const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,

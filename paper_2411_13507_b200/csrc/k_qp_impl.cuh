@@ -42,8 +42,7 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
   int8_t* st_out = job.st_out;
   int* it_out = job.it_out;
   double* delta_out = job.delta_out;
-  DevBuf &d_x = c->ws[WS_QX], &d_zy = c->ws[WS_QZY], &d_list = c->ws[WS_QLIST];
-  DevBuf d_next;
+  DevBuf &d_x = c->ws[WS_QX], &d_zy = c->ws[WS_QZY], &d_list = c->ws[WS_QLIST], &d_next = c->ws[WS_QNEXT];
   d_x.alloc(n_inst * NV * sizeof(double), c->stream);
   d_safe.alloc(n_inst, c->stream);
   d_next.alloc(sizeof(unsigned long long), c->stream);
@@ -129,7 +128,7 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
       launch(c, ps == 0 ? "k_qp_admm" : "k_qp_admm_tail", admm, dim3((unsigned)blocks), dim3(128), 0, qp,
              d_consts.as<double>(), n_inst, d_next.as<unsigned long long>(), st_out, it_out, d_x.as<double>(),
              d_zy.as<double>(), pass, d_n);
-      if (c->trace_on && pass.rq_out_n) {
+      if (c->trace_on && pass.rq_out_n && !g_capturing) {
         unsigned long long hq = 0;
         BZG_CHECK_CUDA(cudaMemcpyAsync(&hq, pass.rq_out_n, sizeof(hq), cudaMemcpyDeviceToHost, c->stream));
         BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
@@ -145,7 +144,7 @@ void qp_solve_t(Ctx* c, const QpJob& job) {
          d_list.as<int>(), d_next.as<unsigned long long>());
   static const bool polish_lu = std::getenv("BZG_POLISH_IMPL") && std::string(std::getenv("BZG_POLISH_IMPL")) == "lu";
   long long n_list = -1;  // known on the host only when it is read back (LU path, tracing)
-  if (polish_lu || c->trace_on) {
+  if ((polish_lu || c->trace_on) && !g_capturing) {
     unsigned long long* hn = static_cast<unsigned long long*>(c->host_scratch(8 * sizeof(unsigned long long))) + 7;
     BZG_CHECK_CUDA(cudaMemcpyAsync(hn, d_next.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));

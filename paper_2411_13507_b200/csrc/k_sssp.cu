@@ -1025,6 +1025,53 @@ void find_path(Ctx* c, Graph* g, Mask* mk, const double* start, const double* go
   path_collect(c, g, h, c->ws[WS_SSSP_OUT].as<long long>(), path, dist_out);
 }
 
+// ---- PathStage: the search with start/goal in pinned staging (capturable enqueue)
+struct PathStage {
+  int pos_only = 0, require_tube = 0;
+  double eps = 0.0;
+  std::vector<double> tube_lo, tube_hi;
+  SnapParams* h_sp = nullptr;  // pinned: [goal, start] parameters, read by the enqueued H2D copy
+  long long* h_out = nullptr;  // pinned: the head of the read-back
+};
+
+PathStage* path_stage_create(const Graph* g, const double* tube_lo, const double* tube_hi, double eps, int pos_only,
+                             int require_tube) {
+  BZG_REQUIRE(g->n <= 16, BZG_EUNSUPPORTED, "state dimension too large");
+  BZG_REQUIRE(g->V >= 1, BZG_EINVAL, "graph has no vertices");
+  PathStage* s = new PathStage();
+  s->pos_only = pos_only;
+  s->require_tube = require_tube;
+  s->eps = eps;
+  s->tube_lo.assign(tube_lo, tube_lo + g->n);
+  s->tube_hi.assign(tube_hi, tube_hi + g->n);
+  if (cudaMallocHost(&s->h_sp, 2 * sizeof(SnapParams)) != cudaSuccess ||
+      cudaMallocHost(&s->h_out, (size_t)(kHead + 2) * sizeof(long long)) != cudaSuccess) {
+    path_stage_destroy(s);
+    throw Error(BZG_ECUDA, "pinned staging allocation failed");
+  }
+  std::vector<double> zero(g->n, 0.0);
+  path_stage_set(s, g, zero.data(), zero.data());
+  return s;
+}
+
+// (the caller guarantees that no launch reading the staging is still pending)
+void path_stage_set(PathStage* s, const Graph* g, const double* start, const double* goal) {
+  snap_params(g, start, goal, s->tube_lo.data(), s->tube_hi.data(), s->eps, s->pos_only, s->require_tube, s->h_sp);
+}
+
+void path_stage_enqueue(Ctx* c, Graph* g, Mask* mk, PathStage* s) { path_enqueue(c, g, mk, s->h_sp, s->h_sp, s->h_out); }
+
+void path_stage_collect(Ctx* c, const Graph* g, PathStage* s, std::vector<int64_t>& path, double* dist) {
+  path_collect(c, g, s->h_out, c->ws[WS_SSSP_OUT].as<long long>(), path, dist);
+}
+
+void path_stage_destroy(PathStage* s) {
+  if (!s) return;
+  if (s->h_sp) cudaFreeHost(s->h_sp);
+  if (s->h_out) cudaFreeHost(s->h_out);
+  delete s;
+}
+
 // ---- bzg_query: the search above captured once per (graph, mask, snapping options)
 struct Query {
   Ctx* c = nullptr;
@@ -1032,33 +1079,12 @@ struct Query {
   Mask* mk = nullptr;
   uint64_t version = 0;
   int64_t E = 0;
-  int pos_only = 0, require_tube = 0;
-  double eps = 0.0;
-  std::vector<double> tube_lo, tube_hi;
-  DevBuf ws[kWsSlots];               // the query's own workspaces (the graph reads their addresses)
-  SnapParams* h_sp = nullptr;        // pinned: [goal, start] parameters, read by the graph's H2D copy
-  long long* h_out = nullptr;        // pinned: the head of the read-back
+  PathStage* st = nullptr;
+  DevBuf ws[kWsSlots];  // the query's own workspaces (the graph reads their addresses)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  long long kernels = 0;             // kernel nodes per launch
+  long long kernels = 0;  // kernel nodes per launch
 };
-
-namespace {
-// run fn with c->ws switched to the query's workspaces
-template <typename F>
-void with_query_ws(Query* q, F&& fn) {
-  Ctx* c = q->c;
-  DevBuf* saved = c->ws;
-  c->ws = q->ws;
-  try {
-    fn();
-  } catch (...) {
-    c->ws = saved;
-    throw;
-  }
-  c->ws = saved;
-}
-}  // namespace
 
 void query_destroy(Query* q) {
   if (!q) return;
@@ -1066,15 +1092,12 @@ void query_destroy(Query* q) {
   if (q->exec) cudaGraphExecDestroy(q->exec);
   if (q->graph) cudaGraphDestroy(q->graph);
   for (auto& w : q->ws) w.release();
-  if (q->h_sp) cudaFreeHost(q->h_sp);
-  if (q->h_out) cudaFreeHost(q->h_out);
+  path_stage_destroy(q->st);
   delete q;
 }
 
 Query* query_create(Ctx* c, Graph* g, Mask* mk, const double* tube_lo, const double* tube_hi, double eps,
                     int pos_only, int require_tube) {
-  BZG_REQUIRE(g->n <= 16, BZG_EUNSUPPORTED, "state dimension too large");
-  BZG_REQUIRE(g->V >= 1, BZG_EINVAL, "graph has no vertices");
   Query* q = new Query();
   try {
     q->c = c;
@@ -1082,45 +1105,12 @@ Query* query_create(Ctx* c, Graph* g, Mask* mk, const double* tube_lo, const dou
     q->mk = mk;
     q->version = g->version;
     q->E = g->E;
-    q->pos_only = pos_only;
-    q->require_tube = require_tube;
-    q->eps = eps;
-    q->tube_lo.assign(tube_lo, tube_lo + g->n);
-    q->tube_hi.assign(tube_hi, tube_hi + g->n);
-    BZG_CHECK_CUDA(cudaMallocHost(&q->h_sp, 2 * sizeof(SnapParams)));
-    BZG_CHECK_CUDA(cudaMallocHost(&q->h_out, (size_t)(kHead + 2) * sizeof(long long)));
-    // warm-up: one eager search (start = goal = the first vertex's neighbourhood: any values do)
-    // sizes every workspace and initialises the mask's cache keys
-    std::vector<double> zero(g->n, 0.0);
-    snap_params(g, zero.data(), zero.data(), tube_lo, tube_hi, eps, pos_only, require_tube, q->h_sp);
-    with_query_ws(q, [&] {
-      path_enqueue(c, g, mk, q->h_sp, q->h_sp, q->h_out);
+    q->st = path_stage_create(g, tube_lo, tube_hi, eps, pos_only, require_tube);
+    // warm-up: one eager search sizes every workspace and initialises the mask's cache keys
+    with_ws(c, q->ws, [&] {
+      path_stage_enqueue(c, g, mk, q->st);
       BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-      const bool prof = c->profiling;
-      const long long launches0 = c->launches;
-      c->profiling = false;  // no event records inside the graph
-      g_capturing = true;
-      cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
-      if (e == cudaSuccess) {
-        try {
-          path_enqueue(c, g, mk, q->h_sp, q->h_sp, q->h_out);
-        } catch (...) {
-          cudaGraph_t tmp = nullptr;
-          cudaStreamEndCapture(c->stream, &tmp);
-          if (tmp) cudaGraphDestroy(tmp);
-          g_capturing = false;
-          c->profiling = prof;
-          throw;
-        }
-        e = cudaStreamEndCapture(c->stream, &q->graph);
-      }
-      g_capturing = false;
-      c->profiling = prof;
-      q->kernels = c->launches - launches0;
-      c->launches = launches0;
-      BZG_CHECK_CUDA(e);
-      BZG_CHECK_CUDA(cudaGraphInstantiate(&q->exec, q->graph, 0));
-      BZG_CHECK_CUDA(cudaGraphUpload(q->exec, c->stream));
+      q->exec = capture_graph(c, [&] { path_stage_enqueue(c, g, mk, q->st); }, &q->kernels, &q->graph);
     });
   } catch (...) {
     query_destroy(q);
@@ -1134,12 +1124,11 @@ void query_run(Query* q, const double* start, const double* goal, std::vector<in
   Graph* g = q->g;
   BZG_REQUIRE(g->version == q->version && g->E == q->E && (!q->mk || (q->mk->g == g && q->mk->E == g->E)),
               BZG_EINVAL, "stale query: the graph's edge set changed after it was captured");
-  // the previous launch finished (query_run synchronises), so the staging area is free
-  snap_params(g, start, goal, q->tube_lo.data(), q->tube_hi.data(), q->eps, q->pos_only, q->require_tube, q->h_sp);
+  path_stage_set(q->st, g, start, goal);  // the previous launch finished (query_run synchronises)
   BZG_CHECK_CUDA(cudaGraphLaunch(q->exec, c->stream));
   c->launches += q->kernels;
   BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
-  path_collect(c, g, q->h_out, q->ws[WS_SSSP_OUT].as<long long>(), path, dist);
+  with_ws(c, q->ws, [&] { path_stage_collect(c, g, q->st, path, dist); });
 }
 
 long long query_kernels(const Query* q) { return q->kernels; }
