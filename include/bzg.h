@@ -250,7 +250,9 @@ int bzg_query_destroy(bzg_query* q);
  * replanner's mask holds no per-QP records.  dynamic (n_obs flags, NULL = all): obstacles
  * flagged 0 are static -- cut once, their per-obstacle outcome rows kept on the device (as
  * the re-cut cache keeps them) -- and a cycle cuts only the dynamic ones and rebuilds the mask
- * in list order; a static obstacle passed changed to a later run is re-cut then. */
+ * in list order; a static obstacle passed changed to a later run is re-cut then.  A run may
+ * pass the dynamic obstacles alone (n_obs = their count, in list order): the static ones then
+ * stand as last given. */
 int bzg_replanner_create(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_off, const double* A,
                          const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
                          const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps_geo,

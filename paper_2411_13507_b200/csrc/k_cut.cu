@@ -1542,24 +1542,29 @@ void replanner_run(Replanner* r, int n_obs, const int32_t* row_off, const double
   const int m = g->m;
   BZG_REQUIRE(g->version == r->version && g->E == r->E, BZG_EINVAL,
               "stale replanner: the graph's edge set changed after it was created");
-  BZG_REQUIRE(n_obs == r->n_obs, BZG_EINVAL, "a replanner keeps its obstacle count");
+  // n_obs == the dynamic count (split): the arrays hold the dynamic obstacles only, in list
+  // order, and the static ones stand as last given
+  const bool dyn_only = r->split && n_obs == (int)r->dyn.size();
+  BZG_REQUIRE(n_obs == r->n_obs || dyn_only, BZG_EINVAL,
+              "a replanner keeps its obstacle count (or takes its dynamic obstacles alone)");
   check_obstacles(n_obs, row_off, is_box, m);
   ++r->runs;
   *eager_out = 0;
   // the list the cycle cuts: the dynamic obstacles (split) or all of them
   SubList dl;
-  if (r->split) {
+  if (r->split && !dyn_only) {
     const SubList st = sublist(r->stat, m, row_off, A, b, is_box, box_lo, box_hi);
     if (sublist_key(st) != r->static_key) replanner_cut_static(r, st);  // rows are data: the graph stays valid
     dl = sublist(r->dyn, m, row_off, A, b, is_box, box_lo, box_hi);
   }
-  const int nc = r->split ? dl.n() : n_obs;
-  const int32_t* ro = r->split ? dl.ro.data() : row_off;
-  const double* cA = r->split ? dl.A.data() : A;
-  const double* cb = r->split ? dl.b.data() : b;
-  const uint8_t* cbox = r->split ? dl.box.data() : is_box;
-  const double* clo = r->split ? dl.lo.data() : box_lo;
-  const double* chi = r->split ? dl.hi.data() : box_hi;
+  const bool sub = r->split && !dyn_only;
+  const int nc = sub ? dl.n() : n_obs;
+  const int32_t* ro = sub ? dl.ro.data() : row_off;
+  const double* cA = sub ? dl.A.data() : A;
+  const double* cb = sub ? dl.b.data() : b;
+  const uint8_t* cbox = sub ? dl.box.data() : is_box;
+  const double* clo = sub ? dl.lo.data() : box_lo;
+  const double* chi = sub ? dl.hi.data() : box_hi;
   const int qp_rows = check_obstacles(nc, ro, cbox, m);
   dispatch_cut(g->gamma, m, [&](auto G_, auto M_) {
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;

@@ -442,7 +442,7 @@ def _obstacle_arrays(obstacles, m):
     hit = _OBS_CACHE.get(key)
     if hit is not None:
         return hit[1]
-    out = _obstacle_arrays_uncached(obstacles, m)
+    out = _obstacle_arrays_rows(obstacles, m)
     frozen = all(not np.asarray(ob.A).flags.writeable and not np.asarray(ob.b).flags.writeable
                  for ob in obstacles if isinstance(getattr(ob, "A", None), np.ndarray))
     if frozen and all(isinstance(getattr(ob, "A", None), np.ndarray) for ob in obstacles):
@@ -450,6 +450,97 @@ def _obstacle_arrays(obstacles, m):
             _OBS_CACHE.pop(next(iter(_OBS_CACHE)))
         _OBS_CACHE[key] = (obstacles, out)
     return out
+
+
+# Per-A-matrix constants of the obstacle preparation (row norms, normalised rows, and for 2m-row
+# matrices the box-recovery structure), keyed by the identity of a read-only A: a moving
+# obstacle is usually Polytope(A, b + A @ shift) with the same frozen A, so a replanning cycle
+# recomputes only b-dependent values.  Entries pin their A so the identities stay unique.
+_A_CACHE: dict = {}
+_A_CACHE_SIZE = 4096
+
+
+def _a_constants(A: np.ndarray, m: int):
+    hit = _A_CACHE.get(id(A))
+    if hit is not None and hit[0] is A:
+        return hit[1]
+    nrm = np.linalg.norm(A, axis=1)
+    An = A / nrm[:, None]
+    box = None
+    if A.shape[0] == 2 * m:  # recover_boxes(An, bn) on one obstacle, the b-independent part
+        n2 = np.linalg.norm(An, axis=1)
+        rows = []
+        ok = True
+        for i in range(2 * m):
+            row = An[i] / n2[i]
+            ax = int(np.argmax(np.abs(row)))
+            unit = np.zeros(m)
+            unit[ax] = np.sign(row[ax])
+            ok = ok and bool(np.all(np.abs(row - unit) <= 1e-12 + 1e-5 * np.abs(unit)))
+            rows.append((ax, bool(row[ax] > 0), float(n2[i])))
+        box = (ok, rows)
+    const = (nrm, _ro(An), box)
+    if not A.flags.writeable:
+        if len(_A_CACHE) >= _A_CACHE_SIZE:
+            _A_CACHE.pop(next(iter(_A_CACHE)))
+        _A_CACHE[id(A)] = (A, const)
+    return const
+
+
+_OB_CACHE: dict = {}
+_OB_CACHE_SIZE = 8192
+
+
+def _one_obstacle(ob, m):
+    """(An, bn, is_box, lo, hi) of one obstacle, cached by the identities of its read-only A, b."""
+    A = np.asarray(ob.A, dtype=np.float64)
+    b = np.asarray(ob.b, dtype=np.float64)
+    key = (id(A), id(b))
+    hit = _OB_CACHE.get(key)
+    if hit is not None and hit[0] is A and hit[1] is b:
+        return hit[2]
+    if A.ndim != 2 or A.shape[1] != m:
+        raise ValueError(f"obstacles must live in the {m}-d output space")
+    nrm, An, box = _a_constants(A, m)
+    bn = b / nrm
+    isb, lo, hi = 0, (0.0,) * m, (0.0,) * m
+    if box is not None:
+        ok, info = box
+        lo_l = [float("nan")] * m
+        hi_l = [float("nan")] * m
+        for i, (ax, pos, n2) in enumerate(info):
+            val = float(bn[i]) / n2
+            if pos:
+                hi_l[ax] = val
+            else:
+                lo_l[ax] = -val
+        if ok and not any(v != v for v in lo_l + hi_l) and not any(lo_l[j] > hi_l[j] for j in range(m)):
+            isb, lo, hi = 1, tuple(lo_l), tuple(hi_l)
+    out = (An, bn, isb, lo, hi)
+    if not A.flags.writeable and not b.flags.writeable:
+        if len(_OB_CACHE) >= _OB_CACHE_SIZE:
+            _OB_CACHE.pop(next(iter(_OB_CACHE)))
+        _OB_CACHE[key] = (A, b, out)
+    return out
+
+
+def _obstacle_arrays_rows(obstacles, m):
+    """``_obstacle_arrays_uncached`` obstacle by obstacle with per-obstacle results cached (a
+    replanning cycle recomputes only the moved obstacles): the same float operations in the
+    same order (row norm, division, box recovery), so the arrays are bitwise the vectorised
+    ones (tests/test_host_obstacles.py)."""
+    if not obstacles:
+        return _obstacle_arrays_uncached(obstacles, m)
+    parts = [_one_obstacle(ob, m) for ob in obstacles]
+    rows = [p[0].shape[0] for p in parts]
+    offs = np.zeros(len(parts) + 1, np.int32)
+    np.cumsum(rows, out=offs[1:])
+    An = np.concatenate([p[0] for p in parts])
+    bn = np.concatenate([p[1] for p in parts])
+    is_box = np.fromiter((p[2] for p in parts), np.uint8, len(parts))
+    lo = np.array([p[3] for p in parts], dtype=np.float64).reshape(len(parts), m)
+    hi = np.array([p[4] for p in parts], dtype=np.float64).reshape(len(parts), m)
+    return offs, An, bn, is_box, lo, hi
 
 
 def _obstacle_arrays_uncached(obstacles, m):

@@ -61,13 +61,18 @@ class Replanner:
         self._cc = _cut_cfg(cfg or CutConfig())
         tube = graph.oracle.tube.error
         tlo, thi = _f64(tube.lo), _f64(tube.hi)
-        offs, A, b, is_box, lo, hi = _obstacle_arrays(list(obstacles), self._m)
+        obstacles = list(obstacles)
+        offs, A, b, is_box, lo, hi = _obstacle_arrays(obstacles, self._m)
         self._n_obs = len(is_box)
         dyn = None
+        self._dyn_idx = None
         if dynamic is not None:
             dyn = np.ascontiguousarray(np.asarray(dynamic, dtype=bool).astype(np.uint8))
             if dyn.shape != (self._n_obs,):
                 raise ValueError("dynamic needs one flag per obstacle")
+            if not dyn.all():
+                self._dyn_idx = [int(i) for i in np.nonzero(dyn)[0]]
+        self._static = [ob for i, ob in enumerate(obstacles) if dyn is not None and not dyn[i]]
         h = C.c_void_p()
         nat.check(ctx.lib.bzg_replanner_create(ctx.handle, graph._h, self._n_obs, nat.ptr(offs), nat.ptr(A), nat.ptr(b),
                                                nat.ptr(is_box), nat.ptr(lo), nat.ptr(hi), nat.ptr(dyn),
@@ -75,6 +80,7 @@ class Replanner:
                                                nat.ptr(tlo), nat.ptr(thi), EPS_GEO, int(bool(position_only_snap)),
                                                int(bool(require_tube_snap)), C.byref(h)))
         self._h = h
+        self._dyn_set = set(self._dyn_idx or [])
         self._path = np.empty(graph.num_vertices + 1, dtype=np.int64)
         self._plen = C.c_int64()
         self._dist = C.c_double()
@@ -83,12 +89,21 @@ class Replanner:
         self.last_eager = False
 
     def __call__(self, obstacles, start, goal):
-        offs, A, b, is_box, lo, hi = self._arrays(list(obstacles), self._m)
-        if len(is_box) != self._n_obs:
+        obstacles = list(obstacles)
+        if len(obstacles) != self._n_obs:
             raise ValueError(f"a Replanner keeps its obstacle count ({self._n_obs})")
+        lst, n = obstacles, self._n_obs
+        if self._dyn_idx is not None:
+            static = [ob for i, ob in enumerate(obstacles) if i not in self._dyn_set]
+            if all(a is b for a, b in zip(static, self._static)):  # unchanged: pass the dynamic ones alone
+                lst = [obstacles[i] for i in self._dyn_idx]
+                n = len(lst)
+            else:
+                self._static = static
+        offs, A, b, is_box, lo, hi = self._arrays(lst, self._m)
         s = np.ascontiguousarray(start, dtype=np.float64)
         g = np.ascontiguousarray(goal, dtype=np.float64)
-        nat.check(self._ctx.lib.bzg_replanner_run(self._h, self._n_obs, nat.ptr(offs), nat.ptr(A), nat.ptr(b),
+        nat.check(self._ctx.lib.bzg_replanner_run(self._h, n, nat.ptr(offs), nat.ptr(A), nat.ptr(b),
                                                   nat.ptr(is_box), nat.ptr(lo), nat.ptr(hi), nat.ptr(s), nat.ptr(g),
                                                   nat.ptr(self._path), self._path.size, C.byref(self._plen),
                                                   C.byref(self._dist), nat.ptr(self.counters), C.byref(self._eager)))
