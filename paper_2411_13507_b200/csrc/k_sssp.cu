@@ -140,21 +140,6 @@ __global__ void k_snap_final(unsigned long long* __restrict__ best, int nblocks,
   if (lane == 0) *out = idx;
 }
 
-// reverse reachability sweep over alive edges: reach[u] |= reach[v] for u -> v
-__global__ void k_reach_sweep(long long E, const int* __restrict__ src, const int* __restrict__ dst,
-                              const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach, int* __restrict__ changed) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  if (alive && !alive[e]) return;
-  const int v = dst[e];
-  if (!reach[v]) return;
-  const int u = src[e];
-  if (!reach[u]) {
-    reach[u] = 1;
-    *changed = 1;
-  }
-}
-
 // Reverse reachability to vg (graph.py:433-450, _reaches_goal) in one cooperative launch: vg
 // from the device plan; sweeps over the alive edges mark src when dst is marked, a grid barrier
 // per sweep, until a sweep marks nothing.  Cached per (mask, vg) through `key` on the device.
