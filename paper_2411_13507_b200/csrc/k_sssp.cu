@@ -143,17 +143,22 @@ __global__ void k_snap_final(unsigned long long* __restrict__ best, int nblocks,
 // Reverse reachability to vg (graph.py:433-450, _reaches_goal) in one cooperative launch: vg
 // from the device plan; sweeps over the alive edges mark src when dst is marked, a grid barrier
 // per sweep, until a sweep marks nothing.  Cached per (mask, vg) through `key` on the device.
-__global__ void k_reach_coop(long long E, long long V, const int* __restrict__ src, const int* __restrict__ dst,
-                             const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach,
-                             long long* __restrict__ key, const long long* __restrict__ plan, int* __restrict__ flags) {
-  cg::grid_group grid = cg::this_grid();
+// GRID: one cooperative grid and grid barriers; else ONE thread-block cluster (the launch's
+// whole grid) and cluster barriers -- far cheaper per sweep for small graphs (k_bf_cluster).
+template <bool GRID>
+__global__ void k_reach_sweeps(long long E, long long V, const int* __restrict__ src, const int* __restrict__ dst,
+                               const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach,
+                               long long* __restrict__ key, const long long* __restrict__ plan, int* __restrict__ flags) {
   const long long vg = plan[0];
-  if (*(volatile long long*)key == vg) return;  // grid-uniform: the cached set is vg's
+  if (*(volatile long long*)key == vg) return;  // uniform: the cached set is vg's
+  auto sync = [] {
+    if constexpr (GRID) cg::this_grid().sync(); else cg::this_cluster().sync();
+  };
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nt = (long long)gridDim.x * blockDim.x;
   for (long long i = tid; i < V; i += nt) reach[i] = i == vg ? 1 : 0;
   if (tid < 3) flags[tid] = 0;
-  grid.sync();
+  sync();
   for (int sweep = 0; sweep <= V + 1; ++sweep) {
     if (tid == 0) flags[(sweep + 1) % 3] = 0;
     bool any = false;
@@ -166,10 +171,10 @@ __global__ void k_reach_coop(long long E, long long V, const int* __restrict__ s
       }
     }
     if (any) flags[sweep % 3] = 1;
-    grid.sync();
+    sync();
     if (*(volatile int*)&flags[sweep % 3] == 0) break;
   }
-  grid.sync();
+  sync();
   if (tid == 0) *key = vg;
 }
 
@@ -812,16 +817,53 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
     }
     DevBuf& rflags = c->ws[WS_REACH_FLAGS];
     rflags.alloc(4 * sizeof(int), c->stream);
-    int per_sm = 0;
-    BZG_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_reach_coop, 256, 0));
-    const int rblocks = std::max(1, std::min(per_sm, 2) * c->num_sms);
     long long El = E, Vl2 = V;
     const int* rs = g->src.as<int>();
     const int* rd = g->dst.as<int>();
     const long long* cpl = plan;
     int* rf = rflags.as<int>();
-    void* args[] = {&El, &Vl2, &rs, &rd, &alive, &reach, &rkey, &cpl, &rf};
-    launch_coop(c, "k_reach_coop", (const void*)k_reach_coop, dim3(rblocks), dim3(256), args);
+    // small graphs: one cluster (BZG_REACH_IMPL=grid|cluster forces a schedule)
+    const char* re = std::getenv("BZG_REACH_IMPL");
+    const std::string rs_env = re ? std::string(re) : std::string();
+    const int rcs = bf_cluster_size(V) > 0 ? (E <= kBfCtaMaxE ? 1 : 16) : 0;
+    const bool rcl = rcs > 0 && (rs_env == "cluster" || (rs_env.empty() && V <= kBfClusterDefaultV &&
+                                                         E <= kBfClusterDefaultE));
+    if (rcl) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(rcs);
+      cfg.blockDim = dim3(1024);
+      cfg.stream = c->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = rcs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      static bool attr_set = false;
+      if (!attr_set) {
+        BZG_CHECK_CUDA(cudaFuncSetAttribute((const void*)k_reach_sweeps<false>,
+                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr_set = true;
+      }
+      cudaEvent_t ea = nullptr;
+      const bool timed = c->timed("k_reach_cluster");
+      if (timed) { ea = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(ea, c->stream)); }
+      BZG_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_reach_sweeps<false>, El, Vl2, rs, rd, alive, reach, rkey, cpl, rf));
+      c->launches++;
+      if (timed) {
+        cudaEvent_t eb = c->take_event();
+        BZG_CHECK_CUDA(cudaEventRecord(eb, c->stream));
+        c->pending.push_back({"k_reach_cluster", ea, eb});
+      }
+    } else {
+      int per_sm = 0;
+      BZG_CHECK_CUDA(
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_reach_sweeps<true>, 256, 0));
+      const int rblocks = std::max(1, std::min(per_sm, 2) * c->num_sms);
+      void* args[] = {&El, &Vl2, &rs, &rd, &alive, &reach, &rkey, &cpl, &rf};
+      launch_coop(c, "k_reach_coop", (const void*)k_reach_sweeps<true>, dim3(rblocks), dim3(256), args);
+    }
     snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, reach, c->ws[WS_BEST1], plan + 1);
   }
 

@@ -455,3 +455,26 @@ def test_edge_cases_round2(ctx, golden):
     # project_on_path: no hop -> 0
     assert replan.project_on_path(np.zeros((0, spec.n)), spec, 0.1, start) == 0.0
     assert replan.project_on_path(start[None], spec, 0.1, start) == 0.0
+
+
+@pytest.mark.parametrize("name", ["demo200", "maze", "cfg2_rf2000", "hop1500"])
+def test_reverse_reachability_schedules(ctx, golden, name, monkeypatch):
+    """Relaxed mid-run snapping (graph.py:388-392, _reaches_goal 433-450): the reverse
+    reachability by cooperative grid sweeps and by one thread-block cluster give the same
+    snapped starts and paths, for many starts and goals."""
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+
+    class RefMask:
+        alive = g["alive"]
+
+    rng = np.random.default_rng(17)
+    V = gr.vertices
+    cases = [(start, goal)] + [(V[rng.integers(0, len(V))], V[rng.integers(0, len(V))]) for _ in range(12)]
+    out = {}
+    for impl in ("grid", "cluster"):
+        monkeypatch.setenv("BZG_REACH_IMPL", impl)
+        out[impl] = [G.find_path(gr, RefMask(), s, t, position_only_snap=True, require_tube_snap=False)
+                     for s, t in cases]
+    assert out["grid"] == out["cluster"]
+    assert sum(p is not None for p in out["grid"]) >= 2

@@ -5,7 +5,7 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 R=${R:-r02}
 mkdir -p gpurun_out
-for c in cfg1 cfg2 cfg3 cfg4; do
+for c in cfg1 cfg1-demo cfg2 cfg3 cfg4; do
   python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/${R}_bench_$c.json 2> gpurun_out/err_$c.txt
 done
 for n in 10000 20000 50000 100000; do
@@ -13,6 +13,13 @@ for n in 10000 20000 50000 100000; do
 done
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${R}_bench_reference_arm_cfg3.json 2>&1
 python tools/row_block_probe.py cfg3 5 > gpurun_out/${R}_row_blocks_cfg3.jsonl 2> gpurun_out/err_rbp.txt
+# replanning cycles (eager vs captured) and the launch list of captured cfg1-demo / cfg2 cycles
+python tools/replan_probe.py cfg1-demo cfg2 cfg3 > gpurun_out/${R}_replan_cycles.jsonl 2> gpurun_out/err_replan.txt
+for c in cfg1-demo cfg2; do
+  python tools/replan_cycle.py $c 3 > /dev/null 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/replan_launches_$c.csv \
+      python tools/replan_cycle.py $c 3 > /dev/null 2>&1
+done
 # launch list of the same bench command (cold-cache, serialised: compare shares, not times)
 python bench.py --config cfg3 --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
