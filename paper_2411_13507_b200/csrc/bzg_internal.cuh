@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -92,6 +93,34 @@ enum WsSlot {
   kWsSlots
 };
 
+// Per-call device temporaries without a cudaMallocAsync / cudaFreeAsync pair each (a small
+// scene's build did ~25 of them, tens of microseconds of host time): grow-only chunks handed
+// out bump-style and reused by the next call.  Like the ws slots this is safe because every
+// use is stream-ordered on the context's one stream; reset() at the start of each user.
+struct Arena {
+  std::vector<DevBuf> chunks;
+  size_t cur = 0, off = 0;
+  void reset() {
+    cur = 0;
+    off = 0;
+  }
+  void* take(size_t bytes, cudaStream_t s) {
+    bytes = std::max<size_t>((bytes + 255) & ~(size_t)255, 256);
+    while (true) {
+      if (cur == chunks.size()) chunks.emplace_back();
+      DevBuf& ch = chunks[cur];
+      if (off == 0 && ch.bytes < bytes) ch.alloc(std::max<size_t>(bytes, (size_t)1 << 20), s);
+      if (off + bytes <= ch.bytes) {
+        void* p = static_cast<char*>(ch.ptr) + off;
+        off += bytes;
+        return p;
+      }
+      ++cur;
+      off = 0;
+    }
+  }
+};
+
 struct KernelStat {
   double ms = 0.0;
   long long count = 0;
@@ -130,6 +159,7 @@ struct Ctx {
   // ws points at ws_own except while a bzg_query warms up or captures with its own set.
   DevBuf ws_own[kWsSlots];
   DevBuf* ws = ws_own;
+  Arena arena;  // per-call temporaries (TmpBuf)
   // last obstacle-grid decision (k_cut.cu): obstacle count and xy bounds -> grid sparse enough
   int grid_nobs = -1;
   double grid_key[4] = {0, 0, 0, 0};
@@ -171,6 +201,20 @@ struct Ctx {
     }
     return pinned;
   }
+};
+
+// A DevBuf-like view of arena memory, valid until the next Arena::reset of its context.
+struct TmpBuf {
+  Ctx* c;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  explicit TmpBuf(Ctx* c_) : c(c_) {}
+  void alloc(size_t n, cudaStream_t s) {
+    if (ptr && n <= bytes) return;
+    ptr = c->arena.take(n, s);
+    bytes = n;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
 };
 
 // Raise a kernel's dynamic shared-memory limit only when a launch needs more than before: the

@@ -89,6 +89,7 @@ int bzg_ctx_destroy(bzg_ctx* ctx) {
     ctx->scratch.release();
     ctx->flag.release();
     for (auto& w : ctx->ws_own) w.release();
+    ctx->arena.chunks.clear();
     ctx->drain_profile();
     for (auto e : ctx->spare) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);

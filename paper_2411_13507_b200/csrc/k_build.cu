@@ -926,9 +926,10 @@ void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg,
   std::vector<double> range((size_t)R * n), beps(row_off[R]);
   for (size_t k = 0; k < range.size(); ++k) range[k] = hi[k] - lo[k];  // np.subtract(high, low)
   for (int q = 0; q < row_off[R]; ++q) beps[q] = b[q] + eps_geo;
-  DevBuf d_pcg, d_lo, d_rng, d_off, d_A, d_b, d_coff, d_row0, d_dest, d_need, d_acc;
+  c->arena.reset();
+  TmpBuf d_pcg(c), d_lo(c), d_rng(c), d_off(c), d_A(c), d_b(c), d_coff(c), d_row0(c), d_dest(c), d_need(c), d_acc(c);
   DevBuf &cand = c->ws[WS_CAND], &flag = c->ws[WS_FLAG], &pos = c->ws[WS_POS];
-  auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+  auto up = [&](TmpBuf& buf, const void* src, size_t bytes) {
     buf.alloc(std::max<size_t>(bytes, 8), c->stream);
     if (bytes) BZG_CHECK_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, c->stream));
   };
@@ -1057,11 +1058,12 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     }
   }
 
-  DevBuf dF;
+  c->arena.reset();
+  TmpBuf dF(c);
   dF.alloc((size_t)nF * 2 * n * sizeof(double), c->stream);
   BZG_CHECK_CUDA(cudaMemcpyAsync(dF.ptr, d->F, (size_t)nF * 2 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   DevBuf &a1c = c->ws[WS_A1C], &a2t = c->ws[WS_A2T];
-  DevBuf sok, dok;
+  TmpBuf sok(c), dok(c);
   a1c.alloc((size_t)V * Kpad * sizeof(double), c->stream);
   a2t.alloc((size_t)V * Kpad * sizeof(double), c->stream);
   sok.alloc(V, c->stream);
@@ -1094,7 +1096,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     phi[k] = hi > lo ? hi : lo + 1.0;
   }
   const double cells = m == 1 ? 1073741823.0 : (m == 2 ? 65535.0 : 1023.0);
-  DevBuf key, key2, idx, perm;
+  TmpBuf key(c), key2(c), idx(c), perm(c);
   key.alloc(V * sizeof(unsigned), c->stream);
   key2.alloc(V * sizeof(unsigned), c->stream);
   idx.alloc(V * sizeof(int), c->stream);
@@ -1117,7 +1119,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   const long long ng = (V + kTile - 1) / kTile;
   // ---- keep-in regions: per-vertex membership masks from the one-sided added rows
   RegionMasks rm{nullptr, nullptr, nullptr, nullptr, 0};
-  DevBuf r_soff, r_sF, r_sth, r_doff, r_dF, r_dth, smask, dmask, tor, gor;
+  TmpBuf r_soff(c), r_sF(c), r_sth(c), r_doff(c), r_dF(c), r_dth(c), smask(c), dmask(c), tor(c), gor(c);
   const int R = d->n_regions;
   if (R > 0) {
     BZG_REQUIRE(R <= 64 * kMaxRegionWords, BZG_EUNSUPPORTED, "at most 256 keep-in regions");
@@ -1144,7 +1146,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
       soff.push_back((int)sth.size());
       doff.push_back((int)dth.size());
     }
-    auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+    auto up = [&](TmpBuf& buf, const void* src, size_t bytes) {
       buf.alloc(std::max<size_t>(bytes, 8), c->stream);
       if (bytes) BZG_CHECK_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, c->stream));
     };
@@ -1162,7 +1164,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     gor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
     BZG_CHECK_CUDA(cudaMemsetAsync(smask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
     BZG_CHECK_CUDA(cudaMemsetAsync(dmask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
-    DevBuf rblo, rbhi;
+    TmpBuf rblo(c), rbhi(c);
     if (d->region_box_lo && d->region_box_hi) {
       up(rblo, d->region_box_lo, (size_t)R * m * sizeof(double));
       up(rbhi, d->region_box_hi, (size_t)R * m * sizeof(double));
@@ -1186,7 +1188,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   const bool split = rows < V && rows > 0;
   const long long Vs = split ? rows : V;
   const long long ngs = (Vs + kTile - 1) / kTile;
-  DevBuf s_perm, s_a1c, s_ok, s_smask, s_flag, s_pos, s_tor;
+  TmpBuf s_perm(c), s_a1c(c), s_ok(c), s_smask(c), s_flag(c), s_pos(c), s_tor(c);
   const int* perm_src = perm.as<int>();
   const double* a1c_src = a1c.as<double>();
   const uint8_t* ok_src = sok.as<uint8_t>();
@@ -1216,7 +1218,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
       rms.tile_or = s_tor.as<unsigned long long>();
     }
   }
-  DevBuf tmin, tmax, gmin, gmax;
+  TmpBuf tmin(c), tmax(c), gmin(c), gmax(c);
   tmin.alloc(ngs * Kpad * sizeof(double), c->stream);
   tmax.alloc(ngs * Kpad * sizeof(double), c->stream);
   gmin.alloc(ng * Kpad * sizeof(double), c->stream);
@@ -1230,7 +1232,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     // culls over every (tile, group) into a compact list, then one warp per survivor
     DevBuf& list = c->ws[WS_PAIRLIST];
     list.alloc((size_t)ngs * ng * sizeof(unsigned long long), c->stream);
-    DevBuf nlist;
+    TmpBuf nlist(c);
     nlist.alloc(sizeof(unsigned long long), c->stream);
     BZG_CHECK_CUDA(cudaMemsetAsync(nlist.ptr, 0, sizeof(unsigned long long), c->stream));
     const bool reg = R > 0;
@@ -1367,7 +1369,8 @@ void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, doubl
   if (k <= 0) return;
   std::vector<double> th(n_F);
   for (int r = 0; r < n_F; ++r) th[r] = G[r] + eps;
-  DevBuf dF, dT, d1, d2, dout;
+  c->arena.reset();
+  TmpBuf dF(c), dT(c), d1(c), d2(c), dout(c);
   dF.alloc((size_t)n_F * 2 * n * 8, c->stream);
   dT.alloc((size_t)n_F * 8, c->stream);
   d1.alloc((size_t)k * n * 8, c->stream);

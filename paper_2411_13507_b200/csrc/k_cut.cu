@@ -1308,7 +1308,8 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
       throw;
     }
     // per-obstacle popcounts, the rows into their slots
-    DevBuf d_pc;
+    c->arena.reset();
+    TmpBuf d_pc(c);
     d_pc.alloc((size_t)3 * nm * sizeof(unsigned long long), c->stream);
     launch(c, "k_row_popcount", k_row_popcount, dim3(3 * nm), dim3(256), 0, (const uint32_t*)tk, Wb,
            d_pc.as<unsigned long long>());
@@ -1322,7 +1323,7 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
                                    cudaMemcpyDeviceToHost, c->stream));
     // QP records: sub-list obstacle index -> its first position in the full list
     if (mk->n_qp > 0) {
-      DevBuf d_map;
+      TmpBuf d_map(c);
       d_map.alloc(nm * sizeof(int), c->stream);
       BZG_CHECK_CUDA(cudaMemcpyAsync(d_map.ptr, miss.data(), nm * sizeof(int), cudaMemcpyHostToDevice, c->stream));
       launch(c, "k_remap_int", k_remap_int, dim3(div_up(mk->n_qp, 256)), dim3(256), 0, mk->qp_obs.as<int>(), mk->n_qp,
