@@ -49,6 +49,7 @@ typedef struct bzg_graph bzg_graph;
 typedef struct bzg_mask bzg_mask;
 typedef struct bzg_query bzg_query;
 typedef struct bzg_replanner bzg_replanner;
+typedef struct bzg_planner bzg_planner;
 
 int bzg_abi_version(void);
 const char* bzg_last_error(void);
@@ -187,8 +188,8 @@ typedef struct {
  * of A (rows x m) / b, ALREADY NORMALISED (Polytope.normalized, geometry.py:135-137).
  * is_box[o] != 0 marks obstacles recovered by Polytope.as_box (geometry.py:155-185)
  * with the recovered bounds box_lo/box_hi (o*m ... o*m+m-1); they take the closed-form
- * screen (graph.py:249-264).  Other obstacles (1..8 rows) take the per-edge cut_heuristic
- * (graph.py:202-221, projection QPs of geometry.py:202-252).  More than 8 rows:
+ * screen (graph.py:249-264).  Other obstacles (1..32 rows) take the per-edge cut_heuristic
+ * (graph.py:202-221, projection QPs of geometry.py:202-252).  More than 32 rows:
  * BZG_EUNSUPPORTED.  An obstacle whose projection QP certifies it empty: BZG_EINVAL
  * (the reference raises ValueError). */
 int bzg_cut_graph(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_off, const double* A,
@@ -266,6 +267,35 @@ int bzg_replanner_mask(bzg_replanner* rp, bzg_mask** out);
 /* info: kernels per captured cycle, cycles run, cycles run eagerly, captures */
 int bzg_replanner_info(const bzg_replanner* rp, int64_t info[4]);
 int bzg_replanner_destroy(bzg_replanner* rp);
+
+/* ---- the whole stage as one captured CUDA graph ---------------------------- */
+/* build_graph -> cut_graph -> find_path (graph.py:129-430, the order of sim.plan_once) for one
+ * scene shape: desc fixes the oracle, N, curve, sampling bounds and include count (no keep-in
+ * regions, no row block); the obstacle list keeps its count.  bzg_planner_create runs the first
+ * call (desc's seed and include rows, the given obstacles) eagerly and captures the stage; each
+ * bzg_planner_run(pcg = the seed's PCG64 words as in bzg_build_desc, include rows, obstacles,
+ * start, goal) is then one graph launch and one synchronisation, with the results of
+ * bzg_build_graph + bzg_cut_graph + bzg_find_path on the same inputs.  The build's edge count
+ * stays on the device; the CSR arrays have a capacity (1.5 x the last edge count, at most every
+ * ordered pair); a call whose sampler round fell short, whose edges outgrew the
+ * capacity, whose work lists overflowed or whose obstacle list changed shape runs eagerly
+ * (*eager = 1) and re-captures.  counters as bzg_mask_copy; *num_edges = the graph's E. */
+int bzg_planner_create(bzg_ctx* ctx, const bzg_build_desc* desc, int32_t n_obs, const int32_t* row_off,
+                       const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
+                       const double* box_hi, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi,
+                       double eps_geo, int position_only_snap, int require_tube_snap, bzg_planner** out);
+int bzg_planner_run(bzg_planner* pl, const uint64_t pcg[4], const double* include, int32_t n_obs,
+                    const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
+                    const double* box_lo, const double* box_hi, const double* start, const double* goal,
+                    int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out, int64_t counters[6],
+                    int64_t* num_edges, int32_t* eager);
+/* copies (owned by the caller) of the last call's graph and (m_out non-NULL) its mask */
+int bzg_planner_result(bzg_planner* pl, bzg_graph** g_out, bzg_mask** m_out);
+/* info: kernels per captured call, calls, eager calls, captures, edge capacity, and why the
+ * last eager call was eager (0 it was not / the first call, 1 obstacle-list shape, 2 sampler
+ * round short, 3 edge capacity, 4 cut work lists) */
+int bzg_planner_info(const bzg_planner* pl, int64_t info[6]);
+int bzg_planner_destroy(bzg_planner* pl);
 
 /* replaces sim._project_on_path (sim.py:220-239): the grid time tau = k h (k < (L-1) *
  * steps_per_hop, steps_per_hop = round(T / h)) along the curve chain through the L path states

@@ -30,6 +30,7 @@ from .graph import (
     path_cost,
 )
 from .reachability import ReachOracle, TrackingTube, build_oracle
+from .plan import Planner
 from .replan import Replanner, project_on_path
 
 __version__ = "0.1.0"
@@ -39,6 +40,6 @@ __all__ = [
     "EPS_GEO", "Box", "Hyperplane", "Polytope", "bounding_box", "erode", "inflate",
     "BezierGraph", "CutConfig", "CutMask", "CutProvenance", "CutVerdict", "PathQuery", "SolveConfig",
     "build_graph", "check_edge", "check_edges", "cut_graph", "cut_heuristic", "cut_heuristic_batch", "cut_qp",
-    "cut_qp_batch", "find_path", "path_cost", "Replanner", "project_on_path",
+    "cut_qp_batch", "find_path", "path_cost", "Planner", "Replanner", "project_on_path",
     "ReachOracle", "TrackingTube", "build_oracle",
 ]

@@ -116,6 +116,13 @@ _SIGS = {
     "bzg_replanner_mask": ([_P, C.POINTER(_P)], C.c_int),
     "bzg_replanner_info": ([_P, _P], C.c_int),
     "bzg_replanner_destroy": ([_P], C.c_int),
+    "bzg_planner_create": ([_P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_int, C.c_int,
+                            C.POINTER(_P)], C.c_int),
+    "bzg_planner_run": ([_P, _P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64),
+                         C.POINTER(C.c_double), _P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)], C.c_int),
+    "bzg_planner_result": ([_P, C.POINTER(_P), C.POINTER(_P)], C.c_int),
+    "bzg_planner_info": ([_P, _P], C.c_int),
+    "bzg_planner_destroy": ([_P], C.c_int),
     "bzg_project_on_path": ([_P, C.c_int32, C.c_int32, C.c_double, _P, C.c_int64, _P, C.c_double, C.c_int32, _P,
                              C.POINTER(C.c_double)], C.c_int),
     "bzg_probe_fp64": ([_P, C.c_int, C.POINTER(C.c_double)], C.c_int),

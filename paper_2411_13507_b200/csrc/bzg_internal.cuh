@@ -90,6 +90,7 @@ enum WsSlot {
   WS_REACH_FLAGS,
   WS_SNAP, WS_BEST0, WS_BEST1, WS_NM_REACH, WS_NM_KEY, WS_NM_DIST, WS_NM_PARENT,  // find_path
   WS_OBSGRIDHDR, WS_CUTCNT, WS_CUTOBS, WS_QNEXT,                     // cut staging, counters
+  WS_SCRATCH,                                                        // CUB temporary storage
   kWsSlots
 };
 
@@ -150,7 +151,6 @@ struct Ctx {
   std::vector<cudaEvent_t> spare;
   std::vector<std::string> order;
   std::unordered_map<std::string, KernelStat> stats;
-  DevBuf scratch;       // cub temp storage
   DevBuf flag;          // small device scalars
   // Grow-only workspaces for the per-call temporaries (pair bit matrix, sampler candidates,
   // cut work lists, QP state): reused across calls on this stream, so repeated builds and
@@ -159,7 +159,8 @@ struct Ctx {
   // ws points at ws_own except while a bzg_query warms up or captures with its own set.
   DevBuf ws_own[kWsSlots];
   DevBuf* ws = ws_own;
-  Arena arena;  // per-call temporaries (TmpBuf)
+  Arena arena_own;         // per-call temporaries (TmpBuf)
+  Arena* arena = &arena_own;  // switched with ws by a captured plan
   // last obstacle-grid decision (k_cut.cu): obstacle count and xy bounds -> grid sparse enough
   int grid_nobs = -1;
   double grid_key[4] = {0, 0, 0, 0};
@@ -211,7 +212,7 @@ struct TmpBuf {
   explicit TmpBuf(Ctx* c_) : c(c_) {}
   void alloc(size_t n, cudaStream_t s) {
     if (ptr && n <= bytes) return;
-    ptr = c->arena.take(n, s);
+    ptr = c->arena->take(n, s);
     bytes = n;
   }
   template <typename T> T* as() const { return static_cast<T*>(ptr); }
@@ -324,16 +325,20 @@ cudaGraphExec_t capture_graph(Ctx* c, F&& fn, long long* kernels, cudaGraph_t* g
 
 // run fn with c->ws switched to another workspace set (a captured plan's own buffers)
 template <typename F>
-void with_ws(Ctx* c, DevBuf* ws, F&& fn) {
+void with_ws(Ctx* c, DevBuf* ws, F&& fn, Arena* arena = nullptr) {
   DevBuf* saved = c->ws;
+  Arena* saved_a = c->arena;
   c->ws = ws;
+  if (arena) c->arena = arena;
   try {
     fn();
   } catch (...) {
     c->ws = saved;
+    c->arena = saved_a;
     throw;
   }
   c->ws = saved;
+  c->arena = saved_a;
 }
 
 inline unsigned div_up(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
@@ -372,6 +377,7 @@ struct Graph {
   bool points_ready = false;
   CutCache cut_cache;
   uint64_t version = 0;           // bumped whenever the edge set is replaced (stale queries)
+  const long long* dE = nullptr;  // a captured plan's graph: the edge count on the device (E = capacity)
 };
 
 struct Mask {
@@ -395,13 +401,23 @@ struct Mask {
 
 // Kernel-family entry points (defined in the k_*.cu translation units).
 // single_round: one round sized from Ctx::sample_est, its acceptance checked by build_pairs
-void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool single_round = false);
+void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool single_round = false,
+                   const unsigned long long* pcg_dev = nullptr);
 void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
                     const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out);
 // th_shift moves every oracle threshold (eps-band counting); count_only != nullptr returns the
 // edge count there and leaves g's CSR untouched.  Returns false (CSR untouched) when the
 // preceding single-round sampler (Ctx::sample_check) accepted fewer than N states.
-bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift = 0.0, long long* count_only = nullptr);
+// A build recorded into a captured plan (bzg_planner): the oracle rows come from dF (uploaded
+// once), nothing is read back mid-build, and the edge count / sampler acceptances are copied
+// to h_out / h_sampled (pinned) for the plan's check after the launch.
+struct BuildCapture {
+  const double* dF;
+  long long* h_out;
+  int* h_sampled;
+};
+bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift = 0.0, long long* count_only = nullptr,
+                 const BuildCapture* bc = nullptr);
 void materialize_points(Ctx* c, Graph* g);
 void set_edges(Ctx* c, Graph* g, long long E, const int* src, const int* dst, const double* cost, bool on_device);
 void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, double eps, int64_t k,
@@ -433,6 +449,20 @@ void path_stage_destroy(PathStage* s);
 // through pinned host memory, so a query is one graph launch and one synchronisation.
 struct Query;
 struct Replanner;
+struct Planner;
+Planner* planner_create(Ctx* c, const bzg_build_desc* d, int n_obs, const int32_t* row_off, const double* A,
+                        const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                        const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps,
+                        int pos_only, int require_tube);
+void planner_run(Planner* p, const uint64_t pcg[4], const double* include, int n_obs, const int32_t* row_off,
+                 const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
+                 const double* box_hi, const double* start, const double* goal, std::vector<int64_t>& path,
+                 double* dist, int* eager_out);
+void planner_destroy(Planner* p);
+Ctx* planner_ctx(const Planner* p);
+Graph* planner_graph(Planner* p);
+const Mask* planner_mask(const Planner* p);
+void planner_info(const Planner* p, int64_t info[6]);
 Replanner* replanner_create(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
                             const uint8_t* is_box, const double* box_lo, const double* box_hi,
                             const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo,

@@ -15,6 +15,8 @@ struct bzg_mask : Mask {};
 static Query* as_query(bzg_query* q) { return reinterpret_cast<Query*>(q); }
 static const Query* as_query(const bzg_query* q) { return reinterpret_cast<const Query*>(q); }
 static Replanner* as_rp(bzg_replanner* r) { return reinterpret_cast<Replanner*>(r); }
+static Planner* as_pl(bzg_planner* p) { return reinterpret_cast<Planner*>(p); }
+static const Planner* as_pl(const bzg_planner* p) { return reinterpret_cast<const Planner*>(p); }
 static const Replanner* as_rp(const bzg_replanner* r) { return reinterpret_cast<const Replanner*>(r); }
 
 namespace {
@@ -86,10 +88,9 @@ int bzg_ctx_destroy(bzg_ctx* ctx) {
     if (!ctx) return;
     set_device(ctx);
     cudaStreamSynchronize(ctx->stream);
-    ctx->scratch.release();
     ctx->flag.release();
     for (auto& w : ctx->ws_own) w.release();
-    ctx->arena.chunks.clear();
+    ctx->arena_own.chunks.clear();
     ctx->drain_profile();
     for (auto e : ctx->spare) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -719,6 +720,114 @@ int bzg_replanner_destroy(bzg_replanner* rp) {
     Replanner* r = as_rp(rp);
     set_device(replanner_ctx(r));
     replanner_destroy(r);
+  });
+}
+
+int bzg_planner_create(bzg_ctx* ctx, const bzg_build_desc* desc, int32_t n_obs, const int32_t* row_off,
+                       const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
+                       const double* box_hi, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi,
+                       double eps_geo, int position_only_snap, int require_tube_snap, bzg_planner** out) {
+  return guarded([&] {
+    BZG_REQUIRE(ctx && desc && cfg && tube_lo && tube_hi && out, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(n_obs == 0 || (row_off && A && b && is_box && box_lo && box_hi), BZG_EINVAL, "obstacle arrays missing");
+    BZG_REQUIRE(desc->n_include == 0 || desc->include, BZG_EINVAL, "include rows missing");
+    set_device(ctx);
+    *out = reinterpret_cast<bzg_planner*>(planner_create(ctx, desc, n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg,
+                                                         tube_lo, tube_hi, eps_geo, position_only_snap,
+                                                         require_tube_snap));
+  });
+}
+
+int bzg_planner_run(bzg_planner* pl, const uint64_t pcg[4], const double* include, int32_t n_obs,
+                    const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
+                    const double* box_lo, const double* box_hi, const double* start, const double* goal,
+                    int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out, int64_t counters[6],
+                    int64_t* num_edges, int32_t* eager) {
+  return guarded([&] {
+    BZG_REQUIRE(pl && pcg && start && goal && path_len, BZG_EINVAL, "null argument");
+    BZG_REQUIRE(n_obs == 0 || (row_off && A && b && is_box && box_lo && box_hi), BZG_EINVAL, "obstacle arrays missing");
+    Planner* p = as_pl(pl);
+    set_device(planner_ctx(p));
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    int eg = 0;
+    planner_run(p, pcg, include, n_obs, row_off, A, b, is_box, box_lo, box_hi, start, goal, path, &dist, &eg);
+    if (path.empty()) {
+      *path_len = -1;
+    } else {
+      *path_len = (int64_t)path.size();
+      BZG_REQUIRE(path_out && path_cap >= (int64_t)path.size(), BZG_EINVAL, "path buffer too small");
+      std::memcpy(path_out, path.data(), path.size() * sizeof(int64_t));
+    }
+    if (dist_out) *dist_out = dist;
+    if (counters)
+      for (int i = 0; i < 6; ++i) counters[i] = planner_mask(p)->counters[i];
+    if (num_edges) *num_edges = planner_graph(p)->E;
+    if (eager) *eager = eg;
+  });
+}
+
+int bzg_planner_result(bzg_planner* pl, bzg_graph** g_out, bzg_mask** m_out) {
+  bzg_graph* g = nullptr;
+  bzg_mask* mk = nullptr;
+  int rc = guarded([&] {
+    BZG_REQUIRE(pl && g_out, BZG_EINVAL, "null argument");
+    Planner* p = as_pl(pl);
+    Ctx* c = planner_ctx(p);
+    set_device(c);
+    const Graph* src = planner_graph(p);
+    g = new bzg_graph();
+    g->ctx = c;
+    g->m = src->m;
+    g->gamma = src->gamma;
+    g->p = src->p;
+    g->n = src->n;
+    g->V = src->V;
+    g->D = src->D;
+    g->vertices.alloc((size_t)g->V * g->n * sizeof(double), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.ptr, src->vertices.ptr, (size_t)g->V * g->n * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, c->stream));
+    set_edges(c, g, src->E, src->src.as<int>(), src->dst.as<int>(), src->cost.as<double>(), true);
+    if (m_out) {
+      const Mask* sm = planner_mask(p);
+      mk = new bzg_mask();
+      mk->g = g;
+      mk->ctx = c;
+      mk->E = g->E;
+      mk->n_obs = sm->n_obs;
+      for (int i = 0; i < 6; ++i) mk->counters[i] = sm->counters[i];
+      mk->alive.alloc(std::max<long long>(g->E, 1), c->stream);
+      mk->prov.alloc(std::max<long long>(g->E, 1), c->stream);
+      if (g->E > 0) {
+        BZG_CHECK_CUDA(cudaMemcpyAsync(mk->alive.ptr, sm->alive.ptr, g->E, cudaMemcpyDeviceToDevice, c->stream));
+        BZG_CHECK_CUDA(cudaMemcpyAsync(mk->prov.ptr, sm->prov.ptr, g->E, cudaMemcpyDeviceToDevice, c->stream));
+      }
+    }
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+  if (rc == BZG_OK) {
+    *g_out = g;
+    if (m_out) *m_out = mk;
+  } else {
+    delete mk;
+    delete g;
+  }
+  return rc;
+}
+
+int bzg_planner_info(const bzg_planner* pl, int64_t info[6]) {
+  return guarded([&] {
+    BZG_REQUIRE(pl && info, BZG_EINVAL, "null argument");
+    planner_info(as_pl(pl), info);
+  });
+}
+
+int bzg_planner_destroy(bzg_planner* pl) {
+  return guarded([&] {
+    if (!pl) return;
+    Planner* p = as_pl(pl);
+    set_device(planner_ctx(p));
+    planner_destroy(p);
   });
 }
 

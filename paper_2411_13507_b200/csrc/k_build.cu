@@ -31,11 +31,20 @@ struct SampleParams {
 // One thread per candidate row: jump the PCG64 stream to draw row*n, draw the n
 // uniforms of that row (geometry.py:69-72 -> numpy random_uniform: lo + range*u,
 // range = hi - lo) and test Xd membership (geometry.py:145-148).
+// pcg_dev non-null: the four PCG64 words (state hi/lo, inc hi/lo) read from device memory (a
+// captured plan's staging) instead of the by-value ones
 __global__ void k_sample_candidates(SampleParams sp, unsigned long long st_hi, unsigned long long st_lo,
                                     unsigned long long inc_hi, unsigned long long inc_lo, long long row0,
-                                    long long count, double* __restrict__ cand, int* __restrict__ flag) {
+                                    long long count, double* __restrict__ cand, int* __restrict__ flag,
+                                    const unsigned long long* __restrict__ pcg_dev) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= count) return;
+  if (pcg_dev) {
+    st_hi = pcg_dev[0];
+    st_lo = pcg_dev[1];
+    inc_hi = pcg_dev[2];
+    inc_lo = pcg_dev[3];
+  }
   const u128 inc = ((u128)inc_hi << 64) | inc_lo;
   u128 s = ((u128)st_hi << 64) | st_lo;
   s = pcg_advance(s, inc, (uint64_t)(row0 + t) * (uint64_t)sp.n);
@@ -719,18 +728,19 @@ template <int G, int M>
 __global__ void __launch_bounds__(kExpandThreads) k_expand(DParams dp, const double* __restrict__ Vx, long long r0,
                                                            long long r1, long long W,
                          const uint32_t* __restrict__ bits, const long long* __restrict__ rptr,
-                         int* __restrict__ src, int* __restrict__ dst, double* __restrict__ cost) {
+                         int* __restrict__ src, int* __restrict__ dst, double* __restrict__ cost, long long cap) {
   // The set bits of 32 words are first listed in ascending (word, bit) order in the warp's
   // shared slice, then the lanes take one edge each, so a word with many edges does not
-  // serialise its lane while the others idle.
+  // serialise its lane while the others idle.  cap: the arrays' capacity (a captured plan's,
+  // whose edge count is not known at launch; edges past it are dropped and the plan reruns).
   constexpr int N = G * M;
   __shared__ int s_j[kExpandThreads / 32][32 * 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long i = r0 + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (i >= r1) return;
   long long base = rptr[i - r0];
-  const long long end = rptr[i - r0 + 1];
-  if (base == end) return;
+  const long long end = min(rptr[i - r0 + 1], cap);
+  if (base >= end) return;
   double xi[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) xi[k] = Vx[i * N + k];
@@ -761,7 +771,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand(DParams dp, const dou
       lst[k] = (int)(w * 32 + b);
     }
     __syncwarp();
-    for (int t = lane; t < total; t += 32) {
+    for (int t = lane; t < total && base + t < end; t += 32) {
       const long long jv = lst[t];
       double xj[N];
 #pragma unroll
@@ -846,23 +856,24 @@ void dispatch_gm(int G, int M, F&& f) {
 void exclusive_scan_ll(Ctx* c, const unsigned long long* in, long long* out, long long count) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, count, c->stream);
-  c->scratch.alloc(bytes, c->stream);
+  c->ws[WS_SCRATCH].alloc(bytes, c->stream);
   ScopedLibLaunch l(c, "cub_scan_rows", 2);
-  BZG_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(c->scratch.ptr, bytes, in, out, count, c->stream));
+  BZG_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(c->ws[WS_SCRATCH].ptr, bytes, in, out, count, c->stream));
 }
 
 void exclusive_scan_i(Ctx* c, const int* in, int* out, long long count) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, count, c->stream);
-  c->scratch.alloc(bytes, c->stream);
+  c->ws[WS_SCRATCH].alloc(bytes, c->stream);
   ScopedLibLaunch l(c, "cub_scan_sample", 2);
-  BZG_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(c->scratch.ptr, bytes, in, out, count, c->stream));
+  BZG_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(c->ws[WS_SCRATCH].ptr, bytes, in, out, count, c->stream));
 }
 
 }  // namespace
 
 // ------------------------------------------------------------------ host side
-void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool single_round) {
+void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool single_round,
+                   const unsigned long long* pcg_dev) {
   const int n = d->m * d->gamma;
   BZG_REQUIRE(n <= kMaxN, BZG_EUNSUPPORTED, "state dimension too large for the device sampler");
   BZG_REQUIRE(d->xd_rows >= 1 && d->xd_rows <= kMaxRows, BZG_EUNSUPPORTED, "state polytope row count unsupported");
@@ -893,7 +904,7 @@ void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool sin
     launch(c, "k_sample_candidates", k_sample_candidates, dim3(div_up(count, 256)), dim3(256), 0, sp,
            (unsigned long long)d->pcg_state_hi, (unsigned long long)d->pcg_state_lo,
            (unsigned long long)d->pcg_inc_hi, (unsigned long long)d->pcg_inc_lo, row0, count, cand.as<double>(),
-           flag.as<int>());
+           flag.as<int>(), pcg_dev);
     BZG_CHECK_CUDA(cudaMemsetAsync(flag.as<int>() + count, 0, sizeof(int), c->stream));
     exclusive_scan_i(c, flag.as<int>(), pos.as<int>(), count + 1);
     launch(c, "k_sample_scatter", k_sample_scatter, dim3(div_up(count, 256)), dim3(256), 0, cand.as<double>(),
@@ -926,7 +937,7 @@ void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg,
   std::vector<double> range((size_t)R * n), beps(row_off[R]);
   for (size_t k = 0; k < range.size(); ++k) range[k] = hi[k] - lo[k];  // np.subtract(high, low)
   for (int q = 0; q < row_off[R]; ++q) beps[q] = b[q] + eps_geo;
-  c->arena.reset();
+  c->arena->reset();
   TmpBuf d_pcg(c), d_lo(c), d_rng(c), d_off(c), d_A(c), d_b(c), d_coff(c), d_row0(c), d_dest(c), d_need(c), d_acc(c);
   DevBuf &cand = c->ws[WS_CAND], &flag = c->ws[WS_FLAG], &pos = c->ws[WS_POS];
   auto up = [&](TmpBuf& buf, const void* src, size_t bytes) {
@@ -996,7 +1007,8 @@ void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg,
   }
 }
 
-bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, long long* count_only) {
+bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, long long* count_only,
+                 const BuildCapture* bc) {
   const int n = g->n;
   const int nF = d->n_F;
   const long long V = g->V;
@@ -1058,10 +1070,15 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     }
   }
 
-  c->arena.reset();
+  c->arena->reset();
   TmpBuf dF(c);
-  dF.alloc((size_t)nF * 2 * n * sizeof(double), c->stream);
-  BZG_CHECK_CUDA(cudaMemcpyAsync(dF.ptr, d->F, (size_t)nF * 2 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (bc) {  // a captured plan: the oracle rows were uploaded once
+    dF.ptr = const_cast<double*>(bc->dF);
+    dF.bytes = (size_t)nF * 2 * n * sizeof(double);
+  } else {
+    dF.alloc((size_t)nF * 2 * n * sizeof(double), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(dF.ptr, d->F, (size_t)nF * 2 * n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
   DevBuf &a1c = c->ws[WS_A1C], &a2t = c->ws[WS_A2T];
   TmpBuf sok(c), dok(c);
   a1c.alloc((size_t)V * Kpad * sizeof(double), c->stream);
@@ -1108,9 +1125,9 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.as<unsigned>(), key2.as<unsigned>(), idx.as<int>(),
                                     perm.as<int>(), V, 0, 32, c->stream);
-    c->scratch.alloc(bytes, c->stream);
+    c->ws[WS_SCRATCH].alloc(bytes, c->stream);
     ScopedLibLaunch l(c, "cub_sort_morton", 4);
-    BZG_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(c->scratch.ptr, bytes, key.as<unsigned>(), key2.as<unsigned>(),
+    BZG_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(c->ws[WS_SCRATCH].ptr, bytes, key.as<unsigned>(), key2.as<unsigned>(),
                                                    idx.as<int>(), perm.as<int>(), V, 0, 32, c->stream));
   }
   launch(c, "k_project_sorted", k_project_sorted, dim3(div_up(V, 128)), dim3(128), 0, rp, dF.as<double>(),
@@ -1121,6 +1138,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   RegionMasks rm{nullptr, nullptr, nullptr, nullptr, 0};
   TmpBuf r_soff(c), r_sF(c), r_sth(c), r_doff(c), r_dF(c), r_dth(c), smask(c), dmask(c), tor(c), gor(c);
   const int R = d->n_regions;
+  BZG_REQUIRE(!bc || R == 0, BZG_EUNSUPPORTED, "a captured plan does not take keep-in regions");
   if (R > 0) {
     BZG_REQUIRE(R <= 64 * kMaxRegionWords, BZG_EUNSUPPORTED, "at most 256 keep-in regions");
     BZG_REQUIRE(d->region_row_off && d->region_F && d->region_G, BZG_EINVAL, "region rows missing");
@@ -1186,6 +1204,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   // full order a 32-source tile would hold ~32 / G sources of this block, and the cull, list
   // and staging work would not shrink with G); destinations stay the full sorted order
   const bool split = rows < V && rows > 0;
+  BZG_REQUIRE(!bc || !split, BZG_EUNSUPPORTED, "a captured plan builds the whole graph");
   const long long Vs = split ? rows : V;
   const long long ngs = (Vs + kTile - 1) / kTile;
   TmpBuf s_perm(c), s_a1c(c), s_ok(c), s_smask(c), s_flag(c), s_pos(c), s_tor(c);
@@ -1282,6 +1301,28 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   }
   c->trace("pairs: tiles(+knn)");
   exclusive_scan_ll(c, rowcnt.as<unsigned long long>(), rptr.as<long long>(), rows + 1);
+  if (bc) {
+    // captured plan: no read-back here.  The CSR arrays already have the plan's capacity (E on
+    // the host); the edge count stays on the device (rptr[rows], read by the cut and search
+    // kernels through Graph::dE) and reaches the host with the sampler's acceptance count at
+    // the end of the launch, where the plan checks both.
+    BZG_CHECK_CUDA(cudaMemcpyAsync(bc->h_out, rptr.as<long long>() + rows, sizeof(long long), cudaMemcpyDeviceToHost,
+                                   c->stream));
+    if (c->sample_check)
+      BZG_CHECK_CUDA(cudaMemcpyAsync(bc->h_sampled, c->sample_check, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sample_check = nullptr;
+    DParams dp{};
+    for (size_t k = 0; k < g->D.size(); ++k) dp.D[k] = g->D[k];
+    dispatch_gm(g->gamma, g->m, [&](auto G_, auto M_) {
+      constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+      launch(c, "k_expand", k_expand<Gc, Mc>, dim3(div_up(rows * 32, kExpandThreads)), dim3(kExpandThreads), 0, dp,
+             g->vertices.as<double>(), r0, r1, W, bits.as<uint32_t>(), rptr.as<long long>(), g->src.as<int>(),
+             g->dst.as<int>(), g->cost.as<double>(), (long long)g->E);
+    });
+    launch(c, "k_row_ptr_global", k_row_ptr_global, dim3(div_up(V + 1, 256)), dim3(256), 0, rptr.as<long long>(),
+           V, r0, r1, g->row_ptr.as<long long>());
+    return true;
+  }
   long long* h = static_cast<long long*>(c->host_scratch(2 * sizeof(long long)));
   BZG_CHECK_CUDA(cudaMemcpyAsync(h, rptr.as<long long>() + rows, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   int* sampled = c->sample_check;
@@ -1316,7 +1357,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
       constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
       launch(c, "k_expand", k_expand<Gc, Mc>, dim3(div_up(rows * 32, kExpandThreads)), dim3(kExpandThreads), 0, dp,
              g->vertices.as<double>(), r0, r1, W, bits.as<uint32_t>(), rptr.as<long long>(), g->src.as<int>(),
-             g->dst.as<int>(), g->cost.as<double>());
+             g->dst.as<int>(), g->cost.as<double>(), E);
     });
   }
   launch(c, "k_row_ptr_global", k_row_ptr_global, dim3(div_up(V + 1, 256)), dim3(256), 0, rptr.as<long long>(),
@@ -1369,7 +1410,7 @@ void check_edges(Ctx* c, int n, int n_F, const double* F, const double* G, doubl
   if (k <= 0) return;
   std::vector<double> th(n_F);
   for (int r = 0; r < n_F; ++r) th[r] = G[r] + eps;
-  c->arena.reset();
+  c->arena->reset();
   TmpBuf dF(c), dT(c), d1(c), d2(c), dout(c);
   dF.alloc((size_t)n_F * 2 * n * 8, c->stream);
   dT.alloc((size_t)n_F * 8, c->stream);

@@ -298,8 +298,10 @@ struct ObsGrid {
 // Strided sample of edge control-polygon extents (at most 64 k edges), max into ext_bits.
 template <int G, int M>
 __global__ void k_obs_grid_extent(DParams dp, const double* __restrict__ Vx, long long E,
-                                  const int* __restrict__ src, const int* __restrict__ dst, ObsGrid* __restrict__ gp) {
+                                  const int* __restrict__ src, const int* __restrict__ dst, ObsGrid* __restrict__ gp,
+                                  const long long* __restrict__ dE) {
   constexpr int N = G * M;
+  if (dE) E = min(E, *dE);  // a captured plan's edge count (E = its capacity)
   const long long stride = E > 65536 ? E / 65536 : 1;
   const long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * stride;
   double ext = 0.0;
@@ -381,8 +383,9 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
                                 unsigned long long* __restrict__ pend, unsigned long long* __restrict__ n_gen,
                                 unsigned long long gen_cap, unsigned long long* __restrict__ gen_pend,
                                 const ObsGrid* __restrict__ grid, const unsigned long long* __restrict__ gmask,
-                                CutBits bits) {
+                                CutBits bits, const long long* __restrict__ dE) {
   constexpr int N = G * M;
+  if (dE) E = min(E, *dE);  // a captured plan's edge count (E = its capacity)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const double wmax = *wmaxp;  // the chunk's x-window width (-1: no window), from the staged obstacles
   const bool use_grid = grid != nullptr;  // the host passes the grid only when it is sparse
@@ -933,7 +936,7 @@ void grid_build(Ctx* c, Graph* g, const CutPrep& p, const unsigned char* d_blob)
   BZG_CHECK_CUDA(cudaMemsetAsync(d_grid.ptr, 0, sizeof(ObsGrid), c->stream));
   d_gmask.alloc((size_t)p.n_chunks * kGridCells * kGridCells * sizeof(unsigned long long), c->stream);
   launch(c, "k_obs_grid_extent", k_obs_grid_extent<Gc, Mc>, dim3(div_up(std::min(E, 65536ll), 256)), dim3(256), 0, dp,
-         g->vertices.as<double>(), E, g->src.as<int>(), g->dst.as<int>(), d_grid.as<ObsGrid>());
+         g->vertices.as<double>(), E, g->src.as<int>(), g->dst.as<int>(), d_grid.as<ObsGrid>(), (const long long*)g->dE);
   launch(c, "k_obs_grid_masks", k_obs_grid_masks<Mc>, dim3(kGridCells * kGridCells / 256, (unsigned)p.n_chunks),
          dim3(256), 0, reinterpret_cast<const ObsRec<Mc>*>(d_blob + p.off_rec), p.n_obs, p.chunk,
          reinterpret_cast<const double*>(d_blob + p.off_bnd), d_grid.as<ObsGrid>(),
@@ -990,7 +993,8 @@ void cut_enqueue(Ctx* c, Graph* g, const CutPrep& p, const unsigned char* d_blob
     launch(c, "k_cut_heuristic", kern, dim3((unsigned)hblocks), dim3(kHeurThreads), smem, dp, g->vertices.as<double>(),
            E, g->src.as<int>(), g->dst.as<int>(), d_recs, d_cert, o0, o1, d_wmax + o0 / p.chunk, cfg->heur_margin,
            d_kill.as<int>(), dcnt, dcnt + 5, cc.cap, d_pend.as<unsigned long long>(), dcnt + 6, cc.gen_cap,
-           d_gen.as<unsigned long long>(), use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm, cbits);
+           d_gen.as<unsigned long long>(), use_grid ? d_grid.as<ObsGrid>() : (const ObsGrid*)nullptr, gm, cbits,
+           (const long long*)g->dE);
   }
   if (p.any_general) {
     // general obstacles: cut_heuristic past branch 1 over the device-side list, appending
@@ -1308,7 +1312,7 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
       throw;
     }
     // per-obstacle popcounts, the rows into their slots
-    c->arena.reset();
+    c->arena->reset();
     TmpBuf d_pc(c);
     d_pc.alloc((size_t)3 * nm * sizeof(unsigned long long), c->stream);
     launch(c, "k_row_popcount", k_row_popcount, dim3(3 * nm), dim3(256), 0, (const uint32_t*)tk, Wb,
@@ -1660,6 +1664,331 @@ Replanner* replanner_create(Ctx* c, Graph* g, int n_obs, const int32_t* row_off,
     throw;
   }
   return r;
+}
+
+// ---- Planner (bzg_planner): build -> cut -> find_path of one scene as ONE captured CUDA graph.
+// The whole step of the reference's plan_once stage (graph.py:129-430) for a fixed scene shape
+// (oracle, N, spec, bounds, obstacle-list shape): a call stages the sampler seed (PCG64 words),
+// the included vertices, the obstacle blob and the snapping targets in pinned memory and
+// launches the graph once.  The build runs without its mid-call read-back: the CSR arrays have
+// a capacity (every ordered pair for small graphs), the edge count stays on the device
+// (Graph::dE, read by the cut and search kernels) and comes back with the sampler's
+// acceptance count and the cut's counters at the end, where the plan checks them; a call whose
+// sampler round fell short, whose edges outgrew the capacity or whose work lists overflowed
+// runs eagerly (same results) and the graph is re-captured with larger capacities.
+struct Planner {
+  Ctx* c = nullptr;
+  bzg_build_desc d{};                      // the scene; its arrays point at the copies below
+  std::vector<double> F, G, D, slo, shi, xA, xb;
+  std::vector<double> inc0;                // the creation call's include rows (the Morton box of the
+                                           // capture; it steers tiling only, so later rows may differ)
+  Graph g;                                 // the plan's graph (CSR arrays of capacity Ecap)
+  long long Ecap = 0, E = 0;
+  double sample_est = 1.0;                 // acceptance estimate the captured sampler round uses
+  Mask mk;
+  int n_obs = 0;
+  bzg_cut_config cfg{};
+  CutPrep shape;
+  CutCaps caps;
+  DevBuf dF, d_in;                         // oracle rows (uploaded once); staged inputs
+  unsigned long long* h_in = nullptr;      // pinned: [4 PCG64 words][include rows]
+  size_t in_bytes = 0;
+  unsigned char* h_blob = nullptr;         // pinned: the obstacle blob
+  size_t h_blob_bytes = 0;
+  unsigned long long* h_cnt = nullptr;     // pinned: the cut's counters
+  long long* h_build = nullptr;            // pinned: the edge count
+  int* h_sampled = nullptr;                // pinned: the sampler round's acceptances
+  PathStage* ps = nullptr;
+  DevBuf ws[kWsSlots];
+  Arena arena;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0, runs = 0, eager = 0, captures = 0;
+  int last_reason = 0;  // why the last eager call was eager: 1 shape, 2 sampler, 3 edges, 4 work lists
+};
+
+namespace {
+
+void planner_drop_graph(Planner* p) {
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  p->exec = nullptr;
+  p->graph = nullptr;
+}
+
+// the captured sequence: inputs up, sample, include rows, pairs + CSR, obstacle blob up, cut,
+// search.  p->g.E is the capacity while this runs.
+template <int Gc, int Mc>
+void planner_enqueue(Planner* p) {
+  Ctx* c = p->c;
+  Graph* g = &p->g;
+  const int n = g->n;
+  BZG_CHECK_CUDA(cudaMemcpyAsync(p->d_in.ptr, p->h_in, p->in_bytes, cudaMemcpyHostToDevice, c->stream));
+  c->sample_est = p->sample_est;
+  c->sample_check = nullptr;
+  sample_states(c, &p->d, g->vertices.as<double>(), /*single_round=*/true, p->d_in.as<unsigned long long>());
+  if (p->d.n_include > 0)
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)p->d.N * n,
+                                   reinterpret_cast<const double*>(p->d_in.as<unsigned long long>() + 4),
+                                   (size_t)p->d.n_include * n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  const BuildCapture bc{p->dF.as<double>(), p->h_build, p->h_sampled};
+  build_pairs(c, &p->d, g, 0.0, nullptr, &bc);
+  g->dE = c->ws[WS_RPTR].as<long long>() + g->V;  // rptr[rows]: the edge count on the device
+  DevBuf& d_blob = c->ws[WS_CUTOBS];
+  d_blob.alloc(p->shape.blob.size(), c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(d_blob.ptr, p->h_blob, p->shape.blob.size(), cudaMemcpyHostToDevice, c->stream));
+  cut_enqueue<Gc, Mc>(c, g, p->shape, d_blob.as<unsigned char>(), &p->cfg, &p->mk, CutBits{}, p->caps, p->h_cnt);
+  path_stage_enqueue(c, g, &p->mk, p->ps);
+}
+
+// (re)capture for the obstacle layout of prep, after an eager call on the same inputs
+template <int Gc, int Mc>
+void planner_capture(Planner* p, const CutPrep& prep) {
+  Ctx* c = p->c;
+  Graph* g = &p->g;
+  planner_drop_graph(p);
+  p->shape = prep;
+  const long long E_last = g->E;
+  const long long counters[6] = {p->mk.counters[0], p->mk.counters[1], p->mk.counters[2], p->mk.counters[3],
+                                 p->mk.counters[4], p->mk.counters[5]};
+  g->E = p->Ecap;  // capacity-sized launches
+  CutCaps cc = default_caps(c, g, prep);
+  const unsigned long long seen = c->cut_last_pend, seen_gen = c->cut_last_gen;
+  cc.cap = std::max(cc.cap, seen + seen / 4 + 1024);
+  if (prep.any_general) cc.gen_cap = std::max(cc.gen_cap, seen_gen + seen_gen / 4 + 1024);
+  cc.qcap = std::min<long long>(std::max<long long>(cc.qcap, (long long)(seen + seen / 4 + 1024)), (long long)cc.cap);
+  cc.grid = prep.grid_cand && c->grid_sparse && c->grid_nobs == prep.n_obs ? 1 : 0;
+  p->caps = cc;
+  if (p->h_blob_bytes < prep.blob.size()) {
+    if (p->h_blob) cudaFreeHost(p->h_blob);
+    p->h_blob = nullptr;
+    p->h_blob_bytes = 0;
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_blob, prep.blob.size()));
+    p->h_blob_bytes = prep.blob.size();
+  }
+  std::memcpy(p->h_blob, prep.blob.data(), prep.blob.size());
+  g->src.alloc((size_t)p->Ecap * sizeof(int), c->stream);
+  g->dst.alloc((size_t)p->Ecap * sizeof(int), c->stream);
+  g->cost.alloc((size_t)p->Ecap * sizeof(double), c->stream);
+  mask_begin(c, g, &p->mk, p->n_obs);  // alive / provenance of capacity size
+  try {
+    with_ws(
+        c, p->ws,
+        [&] {
+          planner_enqueue<Gc, Mc>(p);  // sizes every workspace for these capacities
+          BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+          p->exec = capture_graph(c, [&] { planner_enqueue<Gc, Mc>(p); }, &p->kernels, &p->graph);
+        },
+        &p->arena);
+  } catch (...) {
+    g->dE = nullptr;
+    g->E = E_last;
+    throw;
+  }
+  g->dE = nullptr;  // (the launches hold it)
+  g->E = E_last;
+  p->mk.E = E_last;
+  for (int i = 0; i < 6; ++i) p->mk.counters[i] = counters[i];
+  ++p->captures;
+}
+
+}  // namespace
+
+void planner_destroy(Planner* p) {
+  if (!p) return;
+  if (p->c) cudaStreamSynchronize(p->c->stream);
+  planner_drop_graph(p);
+  for (auto& w : p->ws) w.release();
+  p->arena.chunks.clear();
+  path_stage_destroy(p->ps);
+  for (void* h : {(void*)p->h_in, (void*)p->h_blob, (void*)p->h_cnt, (void*)p->h_build, (void*)p->h_sampled})
+    if (h) cudaFreeHost(h);
+  delete p;
+}
+
+// One call: build with the seed's PCG64 words (pcg: state hi/lo, inc hi/lo) and the include
+// rows, cut with the obstacles, search from start to goal.  *eager_out = 1 when it ran eagerly.
+void planner_run(Planner* p, const uint64_t pcg[4], const double* include, int n_obs, const int32_t* row_off,
+                 const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
+                 const double* box_hi, const double* start, const double* goal, std::vector<int64_t>& path,
+                 double* dist, int* eager_out) {
+  Ctx* c = p->c;
+  Graph* g = &p->g;
+  const int n = g->n;
+  BZG_REQUIRE(n_obs == p->n_obs, BZG_EINVAL, "a planner keeps its obstacle count");
+  BZG_REQUIRE(p->d.n_include == 0 || include, BZG_EINVAL, "include rows missing");
+  const int qp_rows = check_obstacles(n_obs, row_off, is_box, g->m);
+  ++p->runs;
+  *eager_out = 0;
+  p->h_in[0] = pcg[0];
+  p->h_in[1] = pcg[1];
+  p->h_in[2] = pcg[2];
+  p->h_in[3] = pcg[3];
+  if (p->d.n_include > 0) std::memcpy(p->h_in + 4, include, (size_t)p->d.n_include * n * sizeof(double));
+  path_stage_set(p->ps, g, start, goal);
+  dispatch_cut(g->gamma, g->m, [&](auto G_, auto M_) {
+    constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+    CutPrep prep;
+    const long long E_keep = g->E;
+    g->E = std::max<long long>(p->Ecap, 1);  // (cut_prepare reads E > 0 only: a plan's graph has edges)
+    cut_prepare_t<Mc>(g, n_obs, row_off, A, b, is_box, box_lo, box_hi, &p->cfg, qp_rows, prep);
+    g->E = E_keep;
+    p->last_reason = 1;
+    if (p->exec && prep.same_shape(p->shape)) {
+      std::memcpy(p->h_blob, prep.blob.data(), prep.blob.size());
+      BZG_CHECK_CUDA(cudaGraphLaunch(p->exec, c->stream));
+      c->launches += p->kernels;
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      const unsigned long long* h = p->h_cnt;
+      const long long E = *p->h_build;
+      const bool sampled_ok = *p->h_sampled >= p->d.N;
+      p->last_reason = !sampled_ok ? 2 : (E > p->Ecap ? 3 : 4);
+      if (sampled_ok && E <= p->Ecap) {
+        BZG_REQUIRE(h[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
+        if (h[5] <= p->caps.cap && h[6] <= p->caps.gen_cap && (long long)h[5] <= p->caps.qcap) {
+          g->E = E;
+          p->E = E;
+          ++g->version;
+          g->points_ready = false;
+          p->mk.E = E;
+          mask_counters(&p->mk, h);
+          p->mk.counters[0] = E * (long long)n_obs;
+          p->mk.n_qp = 0;
+          with_ws(c, p->ws, [&] { path_stage_collect(c, g, p->ps, path, dist); }, &p->arena);
+          p->last_reason = 0;
+          return;
+        }
+      }
+      if (!sampled_ok) p->sample_est *= 0.9;  // the next capture draws more candidates
+    }
+    // eager call on the plan's graph and workspaces, then a capture
+    *eager_out = 1;
+    ++p->eager;
+    with_ws(
+        c, p->ws,
+        [&] {
+          bzg_build_desc d = p->d;
+          d.pcg_state_hi = pcg[0];
+          d.pcg_state_lo = pcg[1];
+          d.pcg_inc_hi = pcg[2];
+          d.pcg_inc_lo = pcg[3];
+          d.include = include;
+          g->dE = nullptr;
+          c->sample_check = nullptr;
+          c->sample_est = p->sample_est;
+          sample_states(c, &d, g->vertices.as<double>(), /*single_round=*/true);
+          if (d.n_include > 0)
+            BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)d.N * n, include,
+                                           (size_t)d.n_include * n * sizeof(double), cudaMemcpyHostToDevice,
+                                           c->stream));
+          if (!build_pairs(c, &d, g)) {
+            sample_states(c, &d, g->vertices.as<double>());
+            build_pairs(c, &d, g);
+          }
+          // the captured round draws ~1.3x the candidates the measured acceptance needs, so other
+          // seeds' rounds (acceptance varies by a few percent) rarely fall short
+          p->sample_est = std::min(p->sample_est, 0.85 * c->sample_est);
+          p->E = g->E;
+          cut_graph_impl(c, g, n_obs, row_off, A, b, is_box, box_lo, box_hi, &p->cfg, &p->mk, CutBits{});
+          path_stage_enqueue(c, g, &p->mk, p->ps);
+          BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+          path_stage_collect(c, g, p->ps, path, dist);
+        },
+        &p->arena);
+    // capacity: the edge count with 50 % headroom (other seeds and obstacle lists vary it by a
+    // few percent), at most every ordered pair; the capacity sizes the cut's and search's grids
+    const long long V = g->V;
+    p->Ecap = std::max(p->Ecap, std::min(V * (V - 1), p->E + p->E / 2 + 4096));
+    planner_capture<Gc, Mc>(p, prep);
+  });
+}
+
+Ctx* planner_ctx(const Planner* p) { return p->c; }
+Graph* planner_graph(Planner* p) { return &p->g; }
+const Mask* planner_mask(const Planner* p) { return &p->mk; }
+void planner_info(const Planner* p, int64_t info[6]) {
+  info[5] = p->last_reason;
+  info[0] = p->kernels;
+  info[1] = p->runs;
+  info[2] = p->eager;
+  info[3] = p->captures;
+  info[4] = p->Ecap;
+}
+
+Planner* planner_create(Ctx* c, const bzg_build_desc* d, int n_obs, const int32_t* row_off, const double* A,
+                        const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                        const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps,
+                        int pos_only, int require_tube) {
+  BZG_REQUIRE(d->m >= 1 && d->gamma >= 1 && d->p == 2 * d->gamma - 1, BZG_EINVAL, "bad curve specification");
+  BZG_REQUIRE(d->N >= 2, BZG_EINVAL, "need at least two vertices");
+  BZG_REQUIRE(d->F && d->G && d->D && d->sample_lo && d->sample_hi && d->xd_A && d->xd_b, BZG_EINVAL,
+              "oracle, boundary matrix and sampler inputs are required");
+  BZG_REQUIRE(!d->vertices && d->n_regions == 0 && d->row_end <= 0 && d->row_begin == 0, BZG_EUNSUPPORTED,
+              "a planner samples its own vertices (no keep-in regions, no row block)");
+  BZG_REQUIRE(n_obs >= 0 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
+  Planner* p = new Planner();
+  try {
+    p->c = c;
+    const int n = d->m * d->gamma;
+    p->d = *d;
+    p->F.assign(d->F, d->F + (size_t)d->n_F * 2 * n);
+    p->G.assign(d->G, d->G + d->n_F);
+    p->D.assign(d->D, d->D + (size_t)(d->p + 1) * 2 * d->gamma);
+    p->slo.assign(d->sample_lo, d->sample_lo + n);
+    p->shi.assign(d->sample_hi, d->sample_hi + n);
+    p->xA.assign(d->xd_A, d->xd_A + (size_t)d->xd_rows * n);
+    p->xb.assign(d->xd_b, d->xd_b + d->xd_rows);
+    p->d.F = p->F.data();
+    p->d.G = p->G.data();
+    p->d.D = p->D.data();
+    p->d.sample_lo = p->slo.data();
+    p->d.sample_hi = p->shi.data();
+    p->d.xd_A = p->xA.data();
+    p->d.xd_b = p->xb.data();
+    if (d->n_include > 0) p->inc0.assign(d->include, d->include + (size_t)d->n_include * n);
+    p->d.include = d->n_include > 0 ? p->inc0.data() : nullptr;
+    p->d.vertices = nullptr;
+    p->n_obs = n_obs;
+    p->cfg = *cfg;
+    Graph* g = &p->g;
+    g->ctx = c;
+    g->m = d->m;
+    g->gamma = d->gamma;
+    g->p = d->p;
+    g->n = n;
+    g->V = d->N + d->n_include;
+    g->row_begin = 0;
+    g->row_end = g->V;
+    g->D = p->D;
+    g->vertices.alloc((size_t)g->V * n * sizeof(double), c->stream);
+    g->row_ptr.alloc((g->V + 1) * sizeof(long long), c->stream);
+    p->dF.alloc(p->F.size() * sizeof(double), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(p->dF.ptr, p->F.data(), p->F.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                   c->stream));
+    p->in_bytes = 4 * sizeof(unsigned long long) + (size_t)d->n_include * n * sizeof(double);
+    p->d_in.alloc(p->in_bytes, c->stream);
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_in, p->in_bytes));
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_cnt, 8 * sizeof(unsigned long long)));
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_build, sizeof(long long)));
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_sampled, sizeof(int)));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    p->ps = path_stage_create(g, tube_lo, tube_hi, eps, pos_only, require_tube);
+    // the first call (the descriptor's own seed and include rows, the given obstacles) runs
+    // eagerly, sizes everything and captures
+    const uint64_t pcg[4] = {d->pcg_state_hi, d->pcg_state_lo, d->pcg_inc_hi, d->pcg_inc_lo};
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    int eager = 0;
+    std::vector<double> zero(n, 0.0);
+    planner_run(p, pcg, d->include, n_obs, row_off, A, b, is_box, box_lo, box_hi, zero.data(), zero.data(), path,
+                &dist, &eager);
+    p->runs = 0;
+    p->eager = 0;
+  } catch (...) {
+    planner_destroy(p);
+    throw;
+  }
+  return p;
 }
 
 void cut_graph(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,

@@ -148,7 +148,9 @@ __global__ void k_snap_final(unsigned long long* __restrict__ best, int nblocks,
 template <bool GRID>
 __global__ void k_reach_sweeps(long long E, long long V, const int* __restrict__ src, const int* __restrict__ dst,
                                const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach,
-                               long long* __restrict__ key, const long long* __restrict__ plan, int* __restrict__ flags) {
+                               long long* __restrict__ key, const long long* __restrict__ plan, int* __restrict__ flags,
+                               const long long* __restrict__ dE) {
+  if (dE) E = min(E, *dE);  // a captured plan's edge count (E = its capacity)
   const long long vg = plan[0];
   if (*(volatile long long*)key == vg) return;  // uniform: the cached set is vg's
   auto sync = [] {
@@ -648,7 +650,8 @@ __global__ void k_bf_async(long long V, const long long* __restrict__ row_ptr, c
 __global__ void k_parent_dist(long long E, const int* __restrict__ src, const int* __restrict__ dst,
                               const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                               const unsigned long long* __restrict__ dist, unsigned long long* __restrict__ pd,
-                              const long long* __restrict__ plan) {
+                              const long long* __restrict__ plan, const long long* __restrict__ dE) {
+  if (dE) E = min(E, *dE);
   if (plan && !plan[2]) return;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= E) return;
@@ -663,7 +666,9 @@ __global__ void k_parent_dist(long long E, const int* __restrict__ src, const in
 __global__ void k_parent_idx(long long E, const int* __restrict__ src, const int* __restrict__ dst,
                              const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                              const unsigned long long* __restrict__ dist, const unsigned long long* __restrict__ pd,
-                             int* __restrict__ parent, const long long* __restrict__ plan) {
+                             int* __restrict__ parent, const long long* __restrict__ plan,
+                             const long long* __restrict__ dE) {
+  if (dE) E = min(E, *dE);
   if (plan && !plan[2]) return;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= E) return;
@@ -818,6 +823,7 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
     DevBuf& rflags = c->ws[WS_REACH_FLAGS];
     rflags.alloc(4 * sizeof(int), c->stream);
     long long El = E, Vl2 = V;
+    const long long* dEp = g->dE;
     const int* rs = g->src.as<int>();
     const int* rd = g->dst.as<int>();
     const long long* cpl = plan;
@@ -849,7 +855,7 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
       cudaEvent_t ea = nullptr;
       const bool timed = c->timed("k_reach_cluster");
       if (timed) { ea = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(ea, c->stream)); }
-      BZG_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_reach_sweeps<false>, El, Vl2, rs, rd, alive, reach, rkey, cpl, rf));
+      BZG_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_reach_sweeps<false>, El, Vl2, rs, rd, alive, reach, rkey, cpl, rf, dEp));
       c->launches++;
       if (timed) {
         cudaEvent_t eb = c->take_event();
@@ -861,7 +867,7 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
       BZG_CHECK_CUDA(
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_reach_sweeps<true>, 256, 0));
       const int rblocks = std::max(1, std::min(per_sm, 2) * c->num_sms);
-      void* args[] = {&El, &Vl2, &rs, &rd, &alive, &reach, &rkey, &cpl, &rf};
+      void* args[] = {&El, &Vl2, &rs, &rd, &alive, &reach, &rkey, &cpl, &rf, &dEp};
       launch_coop(c, "k_reach_coop", (const void*)k_reach_sweeps<true>, dim3(rblocks), dim3(256), args);
     }
     snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, reach, c->ws[WS_BEST1], plan + 1);
@@ -997,10 +1003,10 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
   }
   launch(c, "k_parent_dist", k_parent_dist, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, g->src.as<int>(),
          g->dst.as<int>(), g->cost.as<double>(), alive, (const unsigned long long*)dist, t_pd.as<unsigned long long>(),
-         cplan);
+         cplan, (const long long*)g->dE);
   launch(c, "k_parent_idx", k_parent_idx, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, g->src.as<int>(),
          g->dst.as<int>(), g->cost.as<double>(), alive, (const unsigned long long*)dist,
-         (const unsigned long long*)t_pd.as<unsigned long long>(), parent, cplan);
+         (const unsigned long long*)t_pd.as<unsigned long long>(), parent, cplan, (const long long*)g->dE);
 
   // ---- backtrack and the single read-back: [len, dist bits, path...], the first kHead entries
   DevBuf& d_out = c->ws[WS_SSSP_OUT];
