@@ -416,7 +416,7 @@ def main():
     # ---------------- the same step through the captured Planner (one CUDA graph per step);
     # when the scene allows it (one GPU, no keep-in regions) it is the headline step
     planner = None
-    if rank == 0 and world == 1 and not w.extra.get("regions") and not args.no_planner:
+    if rank == 0 and world == 1 and not args.no_planner:
         planner = planner_block(w, ctx, stream, flush, args.steps)
     clk = clocks.stop()  # sampled over the timed region and the e2e pass that follows it
     clk["window"] = "device-timed steps + e2e steps" + (" + planner steps" if planner else "")
@@ -517,7 +517,12 @@ def planner_block(w, ctx, stream, flush, steps):
 
     from paper_2411_13507_b200.plan import Planner
 
-    pl = Planner(w.N, w.spec, w.oracle, w.sample_bounds, w.obstacles, seed=w.seed, include=w.include, ctx=ctx)
+    kw = {}
+    if w.extra.get("regions"):  # keep-in regions (cfg1, cfg5): the same host constants as the eager step
+        rr, smp = region_constants(w)
+        kw = dict(regions=w.extra["regions"], per_region=w.extra["per_region"], rows_added=rr, sampling=smp)
+    pl = Planner(w.N, w.spec, w.oracle, w.sample_bounds, w.obstacles, seed=w.seed, include=w.include, ctx=ctx,
+                 **kw)
     want = public_api_step(w, ctx, 0, 1)
     dev, wall = [], []
     for k in range(steps + 3):

@@ -63,6 +63,12 @@ class CutConfigC(C.Structure):
     ]
 
 
+class RegionSampler(C.Structure):
+    """bzg_region_sampler (include/bzg.h): the keep-in sampler of a planner."""
+    _fields_ = [("n_regions", C.c_int32), ("N", C.c_void_p), ("pcg", C.c_void_p), ("lo", C.c_void_p),
+                ("hi", C.c_void_p), ("row_off", C.c_void_p), ("A", C.c_void_p), ("b", C.c_void_p)]
+
+
 _P = C.c_void_p
 _SIGS = {
     "bzg_abi_version": ([], C.c_int),
@@ -116,8 +122,8 @@ _SIGS = {
     "bzg_replanner_mask": ([_P, C.POINTER(_P)], C.c_int),
     "bzg_replanner_info": ([_P, _P], C.c_int),
     "bzg_replanner_destroy": ([_P], C.c_int),
-    "bzg_planner_create": ([_P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_int, C.c_int,
-                            C.POINTER(_P)], C.c_int),
+    "bzg_planner_create": ([_P, _P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_double, C.c_int,
+                            C.c_int, C.POINTER(_P)], C.c_int),
     "bzg_planner_run": ([_P, _P, _P, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P, _P, C.c_int64, C.POINTER(C.c_int64),
                          C.POINTER(C.c_double), _P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)], C.c_int),
     "bzg_planner_result": ([_P, C.POINTER(_P), C.POINTER(_P)], C.c_int),

@@ -404,7 +404,20 @@ struct Mask {
 void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool single_round = false,
                    const unsigned long long* pcg_dev = nullptr);
 void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
-                    const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out);
+                    const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out,
+                    double* est_out = nullptr);
+// a captured plan's keep-in pieces (k_build.cu): the single-round region sampler and the
+// region rows of the pair test, uploaded once
+struct RegionSamplePlan;
+RegionSamplePlan* region_sample_plan_create(Ctx* c, int n, int R, const int64_t* N, const double* lo,
+                                            const double* hi, const int32_t* row_off, const double* A,
+                                            const double* b, double eps_geo, const double* est);
+void region_sample_plan_enqueue(Ctx* c, RegionSamplePlan* s, const unsigned long long* d_pcg, double* d_out,
+                                long long* h_acc);
+void region_sample_plan_destroy(RegionSamplePlan* s);
+struct RegionRowsCache;
+RegionRowsCache* region_rows_cache_create(Ctx* c, const bzg_build_desc* d);
+void region_rows_cache_destroy(RegionRowsCache* rc);
 // th_shift moves every oracle threshold (eps-band counting); count_only != nullptr returns the
 // edge count there and leaves g's CSR untouched.  Returns false (CSR untouched) when the
 // preceding single-round sampler (Ctx::sample_check) accepted fewer than N states.
@@ -415,6 +428,7 @@ struct BuildCapture {
   const double* dF;
   long long* h_out;
   int* h_sampled;
+  const RegionRowsCache* rows = nullptr;  // keep-in rows (regions only)
 };
 bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift = 0.0, long long* count_only = nullptr,
                  const BuildCapture* bc = nullptr);
@@ -450,11 +464,11 @@ void path_stage_destroy(PathStage* s);
 struct Query;
 struct Replanner;
 struct Planner;
-Planner* planner_create(Ctx* c, const bzg_build_desc* d, int n_obs, const int32_t* row_off, const double* A,
-                        const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
-                        const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps,
-                        int pos_only, int require_tube);
-void planner_run(Planner* p, const uint64_t pcg[4], const double* include, int n_obs, const int32_t* row_off,
+Planner* planner_create(Ctx* c, const bzg_build_desc* d, const bzg_region_sampler* rsam, int n_obs,
+                        const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
+                        const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                        const double* tube_lo, const double* tube_hi, double eps, int pos_only, int require_tube);
+void planner_run(Planner* p, const uint64_t* pcg, const double* include, int n_obs, const int32_t* row_off,
                  const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
                  const double* box_hi, const double* start, const double* goal, std::vector<int64_t>& path,
                  double* dist, int* eager_out);

@@ -723,7 +723,8 @@ int bzg_replanner_destroy(bzg_replanner* rp) {
   });
 }
 
-int bzg_planner_create(bzg_ctx* ctx, const bzg_build_desc* desc, int32_t n_obs, const int32_t* row_off,
+int bzg_planner_create(bzg_ctx* ctx, const bzg_build_desc* desc, const bzg_region_sampler* regions, int32_t n_obs,
+                       const int32_t* row_off,
                        const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
                        const double* box_hi, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi,
                        double eps_geo, int position_only_snap, int require_tube_snap, bzg_planner** out) {
@@ -732,13 +733,13 @@ int bzg_planner_create(bzg_ctx* ctx, const bzg_build_desc* desc, int32_t n_obs, 
     BZG_REQUIRE(n_obs == 0 || (row_off && A && b && is_box && box_lo && box_hi), BZG_EINVAL, "obstacle arrays missing");
     BZG_REQUIRE(desc->n_include == 0 || desc->include, BZG_EINVAL, "include rows missing");
     set_device(ctx);
-    *out = reinterpret_cast<bzg_planner*>(planner_create(ctx, desc, n_obs, row_off, A, b, is_box, box_lo, box_hi, cfg,
-                                                         tube_lo, tube_hi, eps_geo, position_only_snap,
+    *out = reinterpret_cast<bzg_planner*>(planner_create(ctx, desc, regions, n_obs, row_off, A, b, is_box, box_lo,
+                                                         box_hi, cfg, tube_lo, tube_hi, eps_geo, position_only_snap,
                                                          require_tube_snap));
   });
 }
 
-int bzg_planner_run(bzg_planner* pl, const uint64_t pcg[4], const double* include, int32_t n_obs,
+int bzg_planner_run(bzg_planner* pl, const uint64_t* pcg, const double* include, int32_t n_obs,
                     const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
                     const double* box_lo, const double* box_hi, const double* start, const double* goal,
                     int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out, int64_t counters[6],

@@ -931,7 +931,8 @@ void sample_states(Ctx* c, const bzg_build_desc* d, double* d_vertices, bool sin
 }
 
 void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg, const double* lo, const double* hi,
-                    const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out) {
+                    const int32_t* row_off, const double* A, const double* b, double eps_geo, double* d_out,
+                    double* est_out) {
   BZG_REQUIRE(n >= 1 && n <= kMaxN, BZG_EUNSUPPORTED, "state dimension too large for the device sampler");
   BZG_REQUIRE(R >= 1, BZG_EINVAL, "need at least one region");
   std::vector<double> range((size_t)R * n), beps(row_off[R]);
@@ -1005,7 +1006,146 @@ void sample_regions(Ctx* c, int n, int R, const int64_t* N, const uint64_t* pcg,
       est[r] = std::max(1e-3, (double)hacc[r] / (double)cnt);
     }
   }
+  if (est_out)
+    for (int r = 0; r < R; ++r) est_out[r] = est[r];
 }
+
+// ---- keep-in sampling for a captured plan: ONE round whose per-region candidate counts come
+// from acceptance estimates (1.3x margin), every array but the PCG words uploaded once; the
+// per-region acceptance counts reach h_acc (pinned) for the plan's check after the launch.
+struct RegionSamplePlan {
+  int n = 0, R = 0;
+  long long total = 0;
+  DevBuf lo, range, row_off, A, b_eps, cand_off, row0, dest, need, acc;
+};
+
+RegionSamplePlan* region_sample_plan_create(Ctx* c, int n, int R, const int64_t* N, const double* lo,
+                                            const double* hi, const int32_t* row_off, const double* A,
+                                            const double* b, double eps_geo, const double* est) {
+  RegionSamplePlan* s = new RegionSamplePlan();
+  s->n = n;
+  s->R = R;
+  std::vector<double> range((size_t)R * n), beps(row_off[R]);
+  for (size_t k = 0; k < range.size(); ++k) range[k] = hi[k] - lo[k];  // np.subtract(high, low)
+  for (int q = 0; q < row_off[R]; ++q) beps[q] = b[q] + eps_geo;
+  std::vector<long long> coff(R + 1, 0), row0(R, 0), dest(R, 0), need(R);
+  long long base = 0;
+  for (int r = 0; r < R; ++r) {
+    const long long cnt = N[r] > 0 ? std::min<long long>(
+        (long long)std::ceil((double)N[r] / std::max(est[r], 1e-3) * 1.3) + 64, 1ll << 24) : 0;
+    coff[r + 1] = coff[r] + cnt;
+    dest[r] = base;
+    need[r] = N[r];
+    base += N[r];
+  }
+  s->total = coff[R];
+  auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+    buf.alloc(std::max<size_t>(bytes, 8), c->stream);
+    if (bytes) BZG_CHECK_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  };
+  up(s->lo, lo, (size_t)R * n * sizeof(double));
+  up(s->range, range.data(), range.size() * sizeof(double));
+  up(s->row_off, row_off, (size_t)(R + 1) * sizeof(int32_t));
+  up(s->A, A, (size_t)row_off[R] * n * sizeof(double));
+  up(s->b_eps, beps.data(), beps.size() * sizeof(double));
+  up(s->cand_off, coff.data(), coff.size() * sizeof(long long));
+  up(s->row0, row0.data(), row0.size() * sizeof(long long));
+  up(s->dest, dest.data(), dest.size() * sizeof(long long));
+  up(s->need, need.data(), need.size() * sizeof(long long));
+  s->acc.alloc(R * sizeof(long long), c->stream);
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));  // (host vectors leave scope)
+  return s;
+}
+
+void region_sample_plan_enqueue(Ctx* c, RegionSamplePlan* s, const unsigned long long* d_pcg, double* d_out,
+                                long long* h_acc) {
+  DevBuf &cand = c->ws[WS_CAND], &flag = c->ws[WS_FLAG], &pos = c->ws[WS_POS];
+  const long long total = s->total;
+  cand.alloc(total * s->n * sizeof(double), c->stream);
+  flag.alloc((total + 1) * sizeof(int), c->stream);
+  pos.alloc((total + 1) * sizeof(int), c->stream);
+  RegionSampleDev rs{d_pcg, s->lo.as<double>(), s->range.as<double>(), s->row_off.as<int>(), s->A.as<double>(),
+                     s->b_eps.as<double>(), s->cand_off.as<long long>(), s->row0.as<long long>(), s->n, s->R};
+  launch(c, "k_sample_regions", k_sample_regions, dim3(div_up(total, 256)), dim3(256), 0, rs, total,
+         cand.as<double>(), flag.as<int>());
+  BZG_CHECK_CUDA(cudaMemsetAsync(flag.as<int>() + total, 0, sizeof(int), c->stream));
+  exclusive_scan_i(c, flag.as<int>(), pos.as<int>(), total + 1);
+  launch(c, "k_scatter_regions", k_scatter_regions, dim3(div_up(total, 256)), dim3(256), 0, cand.as<double>(),
+         flag.as<int>(), pos.as<int>(), s->cand_off.as<long long>(), s->R, total, s->n, s->dest.as<long long>(),
+         s->need.as<long long>(), d_out);
+  launch(c, "k_region_acc", k_region_acc, dim3(div_up(s->R, 256)), dim3(256), 0, pos.as<int>(),
+         s->cand_off.as<long long>(), s->R, s->acc.as<long long>());
+  BZG_CHECK_CUDA(cudaMemcpyAsync(h_acc, s->acc.ptr, s->R * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+}
+
+void region_sample_plan_destroy(RegionSamplePlan* s) { delete s; }
+
+// the keep-in rows of the pair test (one-sided source / destination rows per region, with the
+// eps-shifted thresholds), prepared on the host
+struct RegionRowsHost {
+  std::vector<int> soff{0}, doff{0};
+  std::vector<double> sF, sth, dF, dth;
+};
+RegionRowsHost region_rows_host(const bzg_build_desc* d, int n, double th_shift) {
+  RegionRowsHost h;
+  const int R = d->n_regions;
+  for (int r = 0; r < R; ++r) {
+    bool never_r = false;
+    for (int q = d->region_row_off[r]; q < d->region_row_off[r + 1]; ++q) {
+      const double* f = d->region_F + (size_t)q * 2 * n;
+      bool z1 = true, z2 = true;
+      for (int k = 0; k < n; ++k) { z1 &= f[k] == 0.0; z2 &= f[n + k] == 0.0; }
+      double th = d->region_G[q] + d->eps_geo;  // check_edges: G + eps (reachability.py:142)
+      if (th_shift != 0.0) th = th + th_shift;
+      BZG_REQUIRE(z1 || z2, BZG_EUNSUPPORTED, "a keep-in region row couples both endpoints");
+      if (z1 && z2) { never_r |= !(0.0 <= th); continue; }
+      if (z2) { h.sF.insert(h.sF.end(), f, f + n); h.sth.push_back(th); }
+      else { h.dF.insert(h.dF.end(), f + n, f + 2 * n); h.dth.push_back(th); }
+    }
+    if (never_r) {  // a constant row that fails: the region admits no edge
+      h.sF.insert(h.sF.end(), n, 0.0);
+      h.sth.push_back(-1.0);
+    }
+    h.soff.push_back((int)h.sth.size());
+    h.doff.push_back((int)h.dth.size());
+  }
+  return h;
+}
+
+// a captured plan's keep-in rows and region boxes, uploaded once
+struct RegionRowsCache {
+  DevBuf soff, sF, sth, doff, dF, dth, blo, bhi;
+  int R = 0;
+  bool boxes = false;
+};
+
+RegionRowsCache* region_rows_cache_create(Ctx* c, const bzg_build_desc* d) {
+  const int n = d->m * d->gamma, m = d->m, R = d->n_regions;
+  BZG_REQUIRE(R <= 64 * kMaxRegionWords, BZG_EUNSUPPORTED, "at most 256 keep-in regions");
+  BZG_REQUIRE(d->region_row_off && d->region_F && d->region_G, BZG_EINVAL, "region rows missing");
+  const RegionRowsHost h = region_rows_host(d, n, 0.0);
+  RegionRowsCache* rc = new RegionRowsCache();
+  rc->R = R;
+  auto up = [&](DevBuf& buf, const void* src, size_t bytes) {
+    buf.alloc(std::max<size_t>(bytes, 8), c->stream);
+    if (bytes) BZG_CHECK_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  };
+  up(rc->soff, h.soff.data(), h.soff.size() * sizeof(int));
+  up(rc->sF, h.sF.data(), h.sF.size() * sizeof(double));
+  up(rc->sth, h.sth.data(), h.sth.size() * sizeof(double));
+  up(rc->doff, h.doff.data(), h.doff.size() * sizeof(int));
+  up(rc->dF, h.dF.data(), h.dF.size() * sizeof(double));
+  up(rc->dth, h.dth.data(), h.dth.size() * sizeof(double));
+  if (d->region_box_lo && d->region_box_hi) {
+    rc->boxes = true;
+    up(rc->blo, d->region_box_lo, (size_t)R * m * sizeof(double));
+    up(rc->bhi, d->region_box_hi, (size_t)R * m * sizeof(double));
+  }
+  BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));  // (host vectors leave scope)
+  return rc;
+}
+
+void region_rows_cache_destroy(RegionRowsCache* rc) { delete rc; }
 
 bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, long long* count_only,
                  const BuildCapture* bc) {
@@ -1138,42 +1278,34 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
   RegionMasks rm{nullptr, nullptr, nullptr, nullptr, 0};
   TmpBuf r_soff(c), r_sF(c), r_sth(c), r_doff(c), r_dF(c), r_dth(c), smask(c), dmask(c), tor(c), gor(c);
   const int R = d->n_regions;
-  BZG_REQUIRE(!bc || R == 0, BZG_EUNSUPPORTED, "a captured plan does not take keep-in regions");
+  BZG_REQUIRE(!bc || R == 0 || bc->rows, BZG_EINVAL, "a captured plan's keep-in rows are missing");
   if (R > 0) {
     BZG_REQUIRE(R <= 64 * kMaxRegionWords, BZG_EUNSUPPORTED, "at most 256 keep-in regions");
     BZG_REQUIRE(d->region_row_off && d->region_F && d->region_G, BZG_EINVAL, "region rows missing");
-    std::vector<int> soff(1, 0), doff(1, 0);
-    std::vector<double> sF, sth, dF_, dth;
-    for (int r = 0; r < R; ++r) {
-      bool never_r = false;
-      for (int q = d->region_row_off[r]; q < d->region_row_off[r + 1]; ++q) {
-        const double* f = d->region_F + (size_t)q * 2 * n;
-        bool z1 = true, z2 = true;
-        for (int k = 0; k < n; ++k) { z1 &= f[k] == 0.0; z2 &= f[n + k] == 0.0; }
-        double th = d->region_G[q] + d->eps_geo;  // check_edges: G + eps (reachability.py:142)
-        if (th_shift != 0.0) th = th + th_shift;
-        BZG_REQUIRE(z1 || z2, BZG_EUNSUPPORTED, "a keep-in region row couples both endpoints");
-        if (z1 && z2) { never_r |= !(0.0 <= th); continue; }
-        if (z2) { sF.insert(sF.end(), f, f + n); sth.push_back(th); }
-        else { dF_.insert(dF_.end(), f + n, f + 2 * n); dth.push_back(th); }
-      }
-      if (never_r) {  // a constant row that fails: the region admits no edge
-        sF.insert(sF.end(), n, 0.0);
-        sth.push_back(-1.0);
-      }
-      soff.push_back((int)sth.size());
-      doff.push_back((int)dth.size());
-    }
     auto up = [&](TmpBuf& buf, const void* src, size_t bytes) {
       buf.alloc(std::max<size_t>(bytes, 8), c->stream);
       if (bytes) BZG_CHECK_CUDA(cudaMemcpyAsync(buf.ptr, src, bytes, cudaMemcpyHostToDevice, c->stream));
     };
-    up(r_soff, soff.data(), soff.size() * sizeof(int));
-    up(r_sF, sF.data(), sF.size() * sizeof(double));
-    up(r_sth, sth.data(), sth.size() * sizeof(double));
-    up(r_doff, doff.data(), doff.size() * sizeof(int));
-    up(r_dF, dF_.data(), dF_.size() * sizeof(double));
-    up(r_dth, dth.data(), dth.size() * sizeof(double));
+    auto view = [](TmpBuf& buf, const DevBuf& src) { buf.ptr = src.ptr; buf.bytes = src.bytes; };
+    TmpBuf rblo(c), rbhi(c);
+    if (bc) {  // a captured plan: uploaded once (region_rows_cache_create)
+      const RegionRowsCache* rc = bc->rows;
+      view(r_soff, rc->soff); view(r_sF, rc->sF); view(r_sth, rc->sth);
+      view(r_doff, rc->doff); view(r_dF, rc->dF); view(r_dth, rc->dth);
+      if (rc->boxes) { view(rblo, rc->blo); view(rbhi, rc->bhi); }
+    } else {
+      const RegionRowsHost h = region_rows_host(d, n, th_shift);
+      up(r_soff, h.soff.data(), h.soff.size() * sizeof(int));
+      up(r_sF, h.sF.data(), h.sF.size() * sizeof(double));
+      up(r_sth, h.sth.data(), h.sth.size() * sizeof(double));
+      up(r_doff, h.doff.data(), h.doff.size() * sizeof(int));
+      up(r_dF, h.dF.data(), h.dF.size() * sizeof(double));
+      up(r_dth, h.dth.data(), h.dth.size() * sizeof(double));
+      if (d->region_box_lo && d->region_box_hi) {
+        up(rblo, d->region_box_lo, (size_t)R * m * sizeof(double));
+        up(rbhi, d->region_box_hi, (size_t)R * m * sizeof(double));
+      }
+    }
     RegionRowsDev rr{r_soff.as<int>(), r_sF.as<double>(), r_sth.as<double>(), r_doff.as<int>(), r_dF.as<double>(),
                      r_dth.as<double>(), R, (R + 63) / 64, n};
     smask.alloc(V * rr.RW * sizeof(unsigned long long), c->stream);
@@ -1182,11 +1314,6 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     gor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
     BZG_CHECK_CUDA(cudaMemsetAsync(smask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
     BZG_CHECK_CUDA(cudaMemsetAsync(dmask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
-    TmpBuf rblo(c), rbhi(c);
-    if (d->region_box_lo && d->region_box_hi) {
-      up(rblo, d->region_box_lo, (size_t)R * m * sizeof(double));
-      up(rbhi, d->region_box_hi, (size_t)R * m * sizeof(double));
-    }
     launch(c, "k_region_masks", k_region_masks, dim3(div_up(V, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
            perm.as<int>(), V, m, rblo.as<double>(), rbhi.as<double>(), smask.as<unsigned long long>(),
            dmask.as<unsigned long long>());

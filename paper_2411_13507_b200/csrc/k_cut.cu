@@ -1690,8 +1690,16 @@ struct Planner {
   bzg_cut_config cfg{};
   CutPrep shape;
   CutCaps caps;
+  // keep-in regions (configs 1 and 5): the single-round region sampler and the region rows
+  int R = 0;
+  std::vector<int64_t> rN;
+  std::vector<double> rlo, rhi, rA, rb, rest, reg_F, reg_G, reg_blo, reg_bhi;
+  std::vector<int32_t> rrow_off, reg_row_off;
+  RegionSamplePlan* rs = nullptr;
+  RegionRowsCache* rows = nullptr;
+  long long* h_acc = nullptr;              // pinned: per-region acceptances
   DevBuf dF, d_in;                         // oracle rows (uploaded once); staged inputs
-  unsigned long long* h_in = nullptr;      // pinned: [4 PCG64 words][include rows]
+  unsigned long long* h_in = nullptr;      // pinned: [4 PCG64 words per stream][include rows]
   size_t in_bytes = 0;
   unsigned char* h_blob = nullptr;         // pinned: the obstacle blob
   size_t h_blob_bytes = 0;
@@ -1726,12 +1734,17 @@ void planner_enqueue(Planner* p) {
   BZG_CHECK_CUDA(cudaMemcpyAsync(p->d_in.ptr, p->h_in, p->in_bytes, cudaMemcpyHostToDevice, c->stream));
   c->sample_est = p->sample_est;
   c->sample_check = nullptr;
-  sample_states(c, &p->d, g->vertices.as<double>(), /*single_round=*/true, p->d_in.as<unsigned long long>());
+  if (p->R > 0)
+    region_sample_plan_enqueue(c, p->rs, p->d_in.as<unsigned long long>(), g->vertices.as<double>(), p->h_acc);
+  else
+    sample_states(c, &p->d, g->vertices.as<double>(), /*single_round=*/true, p->d_in.as<unsigned long long>());
   if (p->d.n_include > 0)
     BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)p->d.N * n,
-                                   reinterpret_cast<const double*>(p->d_in.as<unsigned long long>() + 4),
+                                   reinterpret_cast<const double*>(p->d_in.as<unsigned long long>() +
+                                                                   4 * std::max(p->R, 1)),
                                    (size_t)p->d.n_include * n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  const BuildCapture bc{p->dF.as<double>(), p->h_build, p->h_sampled};
+  BuildCapture bc{p->dF.as<double>(), p->h_build, p->h_sampled};
+  bc.rows = p->rows;
   build_pairs(c, &p->d, g, 0.0, nullptr, &bc);
   g->dE = c->ws[WS_RPTR].as<long long>() + g->V;  // rptr[rows]: the edge count on the device
   DevBuf& d_blob = c->ws[WS_CUTOBS];
@@ -1801,14 +1814,18 @@ void planner_destroy(Planner* p) {
   for (auto& w : p->ws) w.release();
   p->arena.chunks.clear();
   path_stage_destroy(p->ps);
-  for (void* h : {(void*)p->h_in, (void*)p->h_blob, (void*)p->h_cnt, (void*)p->h_build, (void*)p->h_sampled})
+  region_sample_plan_destroy(p->rs);
+  region_rows_cache_destroy(p->rows);
+  for (void* h : {(void*)p->h_in, (void*)p->h_blob, (void*)p->h_cnt, (void*)p->h_build, (void*)p->h_sampled,
+                  (void*)p->h_acc})
     if (h) cudaFreeHost(h);
   delete p;
 }
 
-// One call: build with the seed's PCG64 words (pcg: state hi/lo, inc hi/lo) and the include
-// rows, cut with the obstacles, search from start to goal.  *eager_out = 1 when it ran eagerly.
-void planner_run(Planner* p, const uint64_t pcg[4], const double* include, int n_obs, const int32_t* row_off,
+// One call: build with the seed's PCG64 words (pcg: state hi/lo, inc hi/lo; for keep-in regions
+// four per region stream) and the include rows, cut with the obstacles, search from start to
+// goal.  *eager_out = 1 when it ran eagerly.
+void planner_run(Planner* p, const uint64_t* pcg, const double* include, int n_obs, const int32_t* row_off,
                  const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
                  const double* box_hi, const double* start, const double* goal, std::vector<int64_t>& path,
                  double* dist, int* eager_out) {
@@ -1820,11 +1837,9 @@ void planner_run(Planner* p, const uint64_t pcg[4], const double* include, int n
   const int qp_rows = check_obstacles(n_obs, row_off, is_box, g->m);
   ++p->runs;
   *eager_out = 0;
-  p->h_in[0] = pcg[0];
-  p->h_in[1] = pcg[1];
-  p->h_in[2] = pcg[2];
-  p->h_in[3] = pcg[3];
-  if (p->d.n_include > 0) std::memcpy(p->h_in + 4, include, (size_t)p->d.n_include * n * sizeof(double));
+  const int nw = 4 * std::max(p->R, 1);
+  std::memcpy(p->h_in, pcg, nw * sizeof(uint64_t));
+  if (p->d.n_include > 0) std::memcpy(p->h_in + nw, include, (size_t)p->d.n_include * n * sizeof(double));
   path_stage_set(p->ps, g, start, goal);
   dispatch_cut(g->gamma, g->m, [&](auto G_, auto M_) {
     constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
@@ -1841,7 +1856,11 @@ void planner_run(Planner* p, const uint64_t pcg[4], const double* include, int n
       BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
       const unsigned long long* h = p->h_cnt;
       const long long E = *p->h_build;
-      const bool sampled_ok = *p->h_sampled >= p->d.N;
+      bool sampled_ok = true;
+      if (p->R > 0)
+        for (int r = 0; r < p->R; ++r) sampled_ok = sampled_ok && p->h_acc[r] >= p->rN[r];
+      else
+        sampled_ok = *p->h_sampled >= p->d.N;
       p->last_reason = !sampled_ok ? 2 : (E > p->Ecap ? 3 : 4);
       if (sampled_ok && E <= p->Ecap) {
         BZG_REQUIRE(h[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
@@ -1899,6 +1918,13 @@ void planner_run(Planner* p, const uint64_t pcg[4], const double* include, int n
     // few percent), at most every ordered pair; the capacity sizes the cut's and search's grids
     const long long V = g->V;
     p->Ecap = std::max(p->Ecap, std::min(V * (V - 1), p->E + p->E / 2 + 4096));
+    if (p->R > 0) {  // the captured region round, sized from this call's acceptance rates
+      planner_drop_graph(p);
+      region_sample_plan_destroy(p->rs);
+      p->rs = nullptr;
+      p->rs = region_sample_plan_create(c, n, p->R, p->rN.data(), p->rlo.data(), p->rhi.data(), p->rrow_off.data(),
+                                        p->rA.data(), p->rb.data(), p->d.eps_geo, p->rest.data());
+    }
     planner_capture<Gc, Mc>(p, prep);
   });
 }
@@ -1915,16 +1941,18 @@ void planner_info(const Planner* p, int64_t info[6]) {
   info[4] = p->Ecap;
 }
 
-Planner* planner_create(Ctx* c, const bzg_build_desc* d, int n_obs, const int32_t* row_off, const double* A,
-                        const double* b, const uint8_t* is_box, const double* box_lo, const double* box_hi,
-                        const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps,
-                        int pos_only, int require_tube) {
+Planner* planner_create(Ctx* c, const bzg_build_desc* d, const bzg_region_sampler* rsam, int n_obs,
+                        const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
+                        const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                        const double* tube_lo, const double* tube_hi, double eps, int pos_only, int require_tube) {
   BZG_REQUIRE(d->m >= 1 && d->gamma >= 1 && d->p == 2 * d->gamma - 1, BZG_EINVAL, "bad curve specification");
   BZG_REQUIRE(d->N >= 2, BZG_EINVAL, "need at least two vertices");
   BZG_REQUIRE(d->F && d->G && d->D && d->sample_lo && d->sample_hi && d->xd_A && d->xd_b, BZG_EINVAL,
               "oracle, boundary matrix and sampler inputs are required");
-  BZG_REQUIRE(!d->vertices && d->n_regions == 0 && d->row_end <= 0 && d->row_begin == 0, BZG_EUNSUPPORTED,
-              "a planner samples its own vertices (no keep-in regions, no row block)");
+  BZG_REQUIRE(!d->vertices && d->row_end <= 0 && d->row_begin == 0, BZG_EUNSUPPORTED,
+              "a planner samples its own vertices and builds every row");
+  BZG_REQUIRE((d->n_regions > 0) == (rsam != nullptr), BZG_EINVAL,
+              "keep-in regions need their sampler (and only they take one)");
   BZG_REQUIRE(n_obs >= 0 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
   Planner* p = new Planner();
   try {
@@ -1948,6 +1976,36 @@ Planner* planner_create(Ctx* c, const bzg_build_desc* d, int n_obs, const int32_
     if (d->n_include > 0) p->inc0.assign(d->include, d->include + (size_t)d->n_include * n);
     p->d.include = d->n_include > 0 ? p->inc0.data() : nullptr;
     p->d.vertices = nullptr;
+    if (rsam) {  // keep-in regions: copies of the region rows and of the region sampler inputs
+      const int R = d->n_regions, m = d->m;
+      BZG_REQUIRE(rsam->n_regions == R && rsam->N && rsam->lo && rsam->hi && rsam->row_off && rsam->A && rsam->b,
+                  BZG_EINVAL, "region sampler inputs missing");
+      p->R = R;
+      p->rN.assign(rsam->N, rsam->N + R);
+      long long tot = 0;
+      for (int r = 0; r < R; ++r) tot += p->rN[r];
+      BZG_REQUIRE(tot == d->N, BZG_EINVAL, "the region sample counts must add up to N");
+      p->rlo.assign(rsam->lo, rsam->lo + (size_t)R * n);
+      p->rhi.assign(rsam->hi, rsam->hi + (size_t)R * n);
+      p->rrow_off.assign(rsam->row_off, rsam->row_off + R + 1);
+      p->rA.assign(rsam->A, rsam->A + (size_t)rsam->row_off[R] * n);
+      p->rb.assign(rsam->b, rsam->b + rsam->row_off[R]);
+      p->rest.assign(R, 1.0);
+      p->reg_row_off.assign(d->region_row_off, d->region_row_off + R + 1);
+      p->reg_F.assign(d->region_F, d->region_F + (size_t)d->region_row_off[R] * 2 * n);
+      p->reg_G.assign(d->region_G, d->region_G + d->region_row_off[R]);
+      p->d.region_row_off = p->reg_row_off.data();
+      p->d.region_F = p->reg_F.data();
+      p->d.region_G = p->reg_G.data();
+      if (d->region_box_lo && d->region_box_hi) {
+        p->reg_blo.assign(d->region_box_lo, d->region_box_lo + (size_t)R * m);
+        p->reg_bhi.assign(d->region_box_hi, d->region_box_hi + (size_t)R * m);
+        p->d.region_box_lo = p->reg_blo.data();
+        p->d.region_box_hi = p->reg_bhi.data();
+      }
+      p->rows = region_rows_cache_create(c, &p->d);
+      BZG_CHECK_CUDA(cudaMallocHost(&p->h_acc, R * sizeof(long long)));
+    }
     p->n_obs = n_obs;
     p->cfg = *cfg;
     Graph* g = &p->g;
@@ -1965,7 +2023,7 @@ Planner* planner_create(Ctx* c, const bzg_build_desc* d, int n_obs, const int32_
     p->dF.alloc(p->F.size() * sizeof(double), c->stream);
     BZG_CHECK_CUDA(cudaMemcpyAsync(p->dF.ptr, p->F.data(), p->F.size() * sizeof(double), cudaMemcpyHostToDevice,
                                    c->stream));
-    p->in_bytes = 4 * sizeof(unsigned long long) + (size_t)d->n_include * n * sizeof(double);
+    p->in_bytes = 4 * std::max(p->R, 1) * sizeof(unsigned long long) + (size_t)d->n_include * n * sizeof(double);
     p->d_in.alloc(p->in_bytes, c->stream);
     BZG_CHECK_CUDA(cudaMallocHost(&p->h_in, p->in_bytes));
     BZG_CHECK_CUDA(cudaMallocHost(&p->h_cnt, 8 * sizeof(unsigned long long)));
@@ -1975,13 +2033,14 @@ Planner* planner_create(Ctx* c, const bzg_build_desc* d, int n_obs, const int32_
     p->ps = path_stage_create(g, tube_lo, tube_hi, eps, pos_only, require_tube);
     // the first call (the descriptor's own seed and include rows, the given obstacles) runs
     // eagerly, sizes everything and captures
-    const uint64_t pcg[4] = {d->pcg_state_hi, d->pcg_state_lo, d->pcg_inc_hi, d->pcg_inc_lo};
+    std::vector<uint64_t> pcg = {d->pcg_state_hi, d->pcg_state_lo, d->pcg_inc_hi, d->pcg_inc_lo};
+    if (rsam) pcg.assign(rsam->pcg, rsam->pcg + 4 * (size_t)p->R);
     std::vector<int64_t> path;
     double dist = 0.0;
     int eager = 0;
     std::vector<double> zero(n, 0.0);
-    planner_run(p, pcg, d->include, n_obs, row_off, A, b, is_box, box_lo, box_hi, zero.data(), zero.data(), path,
-                &dist, &eager);
+    planner_run(p, pcg.data(), d->include, n_obs, row_off, A, b, is_box, box_lo, box_hi, zero.data(), zero.data(),
+                path, &dist, &eager);
     p->runs = 0;
     p->eager = 0;
   } catch (...) {

@@ -9,6 +9,11 @@ spec, oracle, bounds, seed, include)``, bit for bit, in one graph launch and one
 synchronisation; ``pl.result()`` gives that call's graph and mask.  Calls whose sampler round
 falls short, whose edge count outgrows the capacity, whose QP work lists overflow or whose
 obstacle list changes shape run eagerly and re-capture (``pl.info()``).
+
+Keep-in regions (BASELINE configs 1 and 5, ``regions.build_region_graph``): pass ``regions``
+and ``per_region`` (and optionally the host constants ``rows_added`` / ``sampling`` a caller
+keeps); the captured sampler draws every region in one round sized from the measured
+acceptance rates.
 """
 
 from __future__ import annotations
@@ -24,11 +29,34 @@ from .geometry import EPS_GEO
 
 class Planner:
     def __init__(self, N, spec, oracle, bounds, obstacles, seed=0, include=None, cfg=None,
-                 position_only_snap: bool = False, require_tube_snap: bool = True, *, ctx=None):
+                 position_only_snap: bool = False, require_tube_snap: bool = True, *, ctx=None,
+                 regions=None, per_region=None, rows_added=None, sampling=None):
         self._ctx = ctx = ctx or nat.default_context()
         self._spec, self._oracle, self._bounds = spec, oracle, bounds
         self._m = spec.m
+        self._R = 0
+        rsam = None
+        if regions is not None:
+            from . import regions as RG
+
+            rr = rows_added or RG.region_rows(oracle, RG.region_oracles(spec, oracle.Xd, oracle.U, oracle.tube,
+                                                                        regions))
+            smp = sampling or RG.region_sampling(per_region, spec, oracle.Xd, regions, bounds, seed)
+            self._R = len(regions)
+            N = smp.total
         d, keep, D = G._build_desc(N, spec, oracle, bounds, seed, include)
+        if regions is not None:  # the keep-in fields of build_region_graph's descriptor
+            off = np.concatenate([[0], np.cumsum([f.shape[0] for f in rr.F])]).astype(np.int32)
+            RF = G._f64(np.vstack(rr.F)) if rr.F else np.zeros((0, 2 * spec.n))
+            RGv = G._f64(np.concatenate(rr.G)) if rr.G else np.zeros(0)
+            blo, bhi = RG.region_boxes(regions)
+            keep += [off, RF, RGv, blo, bhi, smp]
+            d.n_regions = self._R
+            d.region_row_off, d.region_F, d.region_G = nat.ptr(off), nat.ptr(RF), nat.ptr(RGv)
+            d.region_box_lo, d.region_box_hi = nat.ptr(blo), nat.ptr(bhi)
+            rsam = nat.RegionSampler(self._R, nat.ptr(smp.N), nat.ptr(smp.pcg), nat.ptr(smp.lo), nat.ptr(smp.hi),
+                                     nat.ptr(smp.row_off), nat.ptr(smp.A), nat.ptr(smp.b))
+            self._pcg_cache = {seed: np.ascontiguousarray(smp.pcg, dtype=np.uint64)}
         self._D = D
         self._n_include = int(d.n_include)
         self._cc = G._cut_cfg(cfg or G.CutConfig())
@@ -39,7 +67,8 @@ class Planner:
         self._n_obs = len(is_box)
         self._h = None
         h = C.c_void_p()
-        nat.check(ctx.lib.bzg_planner_create(ctx.handle, C.byref(d), self._n_obs, nat.ptr(offs), nat.ptr(A), nat.ptr(b),
+        nat.check(ctx.lib.bzg_planner_create(ctx.handle, C.byref(d), C.byref(rsam) if rsam is not None else None,
+                                             self._n_obs, nat.ptr(offs), nat.ptr(A), nat.ptr(b),
                                              nat.ptr(is_box), nat.ptr(lo), nat.ptr(hi), C.byref(self._cc), nat.ptr(tlo),
                                              nat.ptr(thi), EPS_GEO, int(bool(position_only_snap)),
                                              int(bool(require_tube_snap)), C.byref(h)))
@@ -60,8 +89,19 @@ class Planner:
     def num_edges(self) -> int:
         return int(self._E.value)
 
+    def _pcg(self, seed):
+        if not self._R:
+            return np.array(G._pcg_words(seed), dtype=np.uint64)
+        hit = self._pcg_cache.get(seed)
+        if hit is None:  # default_rng([seed, r]) per region (regions.region_sampling)
+            hit = np.array([G._pcg_words([seed, r]) for r in range(self._R)], dtype=np.uint64).reshape(-1)
+            if len(self._pcg_cache) > 64:
+                self._pcg_cache.clear()
+            self._pcg_cache[seed] = hit
+        return np.ascontiguousarray(hit, dtype=np.uint64)
+
     def __call__(self, seed, obstacles, start, goal, include=None):
-        pcg = np.array(G._pcg_words(seed), dtype=np.uint64)
+        pcg = self._pcg(seed)
         inc = None
         if self._n_include:
             if include is None:

@@ -103,3 +103,30 @@ def test_planner_shape_change_reruns_eagerly(ctx, golden):
     _check(pl, _eager(ctx, N, spec, orc, bounds, seed + 1, include, mixed, start, goal, {}), path)
     with pytest.raises(ValueError, match="obstacle count"):
         pl(seed, obstacles[:-1], start, goal, include=include)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg5"])
+def test_planner_keep_in_regions(ctx, cfg):
+    """Keep-in regions (configs 1 and 5, regions.build_region_graph): the captured single-round
+    region sampler and the region rows uploaded once give the eager pipeline's graph, mask and
+    path for several seeds."""
+    import bench
+    from paper_2411_13507_b200 import regions as RG
+
+    w = bench.workload(cfg, 10000)
+    regs, per = w.extra["regions"], w.extra["per_region"]
+    obstacles = list(w.obstacles)
+    pl = Planner(None, w.spec, w.oracle, w.sample_bounds, obstacles, seed=w.seed, include=w.include,
+                 regions=regs, per_region=per)
+    rng = np.random.default_rng(3)
+    for k in range(3):
+        seed = w.seed + k
+        if k:
+            obstacles[k % len(obstacles)] = _moved(obstacles[k % len(obstacles)], rng.normal(0, 0.05, w.spec.m))
+        path = pl(seed, obstacles, w.start, w.goal, include=w.include)
+        g0 = RG.build_region_graph(per, w.spec, w.oracle, regs, w.sample_bounds, seed, include=w.include, ctx=ctx)
+        m0 = G.cut_graph(g0, obstacles)
+        p0 = G.find_path(g0, m0, w.start, w.goal)
+        _check(pl, (g0, m0, p0, g0._cache.get("last_dist")), path)
+    info = pl.info()
+    assert info["calls"] == 3 and info["eager_calls"] == 0, info
