@@ -1,7 +1,6 @@
 # Refresh the round's bench lines, the cfg3 launch list, the cfg3 `ncu --set full` capture and the
 # row-block table on a GPU box (one GPU):   gpurun --timeout 3600 -- 'R=r02 bash tools/refresh_profiles.sh'
-# then locally:  python tools/summarize_ncu.py launches gpurun_out/launches.csv profiles/${R}_launches_cfg3.json
-#                python tools/summarize_ncu.py full gpurun_out/prof_${R}_full.ncu-rep profiles/${R}_ncu_full_cfg3.json
+# (the ncu summaries are written on the box: gpurun_out/${R}_ncu_full_cfg3.json, ${R}_launches_cfg3.json)
 cd "${GRAFT_REPO_ROOT:-.}"
 R=${R:-r02}
 mkdir -p gpurun_out
@@ -28,5 +27,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 python tools/run_once.py cfg3 1 > /dev/null 2>&1 && \
 ncu --set full --clock-control none --import-source on \
     -k 'regex:k_qp_admm|k_cut_heuristic|k_pair_list|k_qp_polish|k_bf_scan|k_expand' -c 6 -f \
-    -o gpurun_out/prof_${R}_full python tools/run_once.py cfg3 1 > gpurun_out/ncu_full.log 2>&1
+    -o /tmp/prof_${R}_full python tools/run_once.py cfg3 1 > gpurun_out/ncu_full.log 2>&1
+# summaries on the box (the report itself exceeds what gpurun copies back)
+python tools/summarize_ncu.py full /tmp/prof_${R}_full.ncu-rep gpurun_out/${R}_ncu_full_cfg3.json > /dev/null 2>&1
+python tools/summarize_ncu.py launches gpurun_out/launches.csv gpurun_out/${R}_launches_cfg3.json > /dev/null 2>&1
+for c in cfg1-demo cfg2; do
+  python tools/summarize_ncu.py launches gpurun_out/replan_launches_$c.csv gpurun_out/${R}_replan_launches_$c.json > /dev/null 2>&1
+done
 echo done
