@@ -130,3 +130,22 @@ def test_planner_keep_in_regions(ctx, cfg):
         _check(pl, (g0, m0, p0, g0._cache.get("last_dist")), path)
     info = pl.info()
     assert info["calls"] == 3 and info["eager_calls"] == 0, info
+
+
+def test_planner_edge_cases(ctx, golden):
+    """No obstacles, no included vertices, an unreachable goal (None), start == goal."""
+    gd = golden("demo200")
+    N, spec, orc, bounds, seed, include, obstacles, start, goal = inputs_from_golden(gd)
+    pl = Planner(N, spec, orc, bounds, [], seed=seed)  # no include rows, no obstacles
+    path = pl(seed + 3, [], start, goal)
+    g0 = G.build_graph(N, spec, orc, bounds, seed + 3, None, ctx=ctx)
+    m0 = G.cut_graph(g0, [])
+    _check(pl, (g0, m0, G.find_path(g0, m0, start, goal), g0._cache.get("last_dist")), path)
+    far = np.asarray(goal, float) + 1e3  # snaps to the farthest corner vertex; compare with eager
+    path = pl(seed + 3, [], start, far)
+    assert path == G.find_path(g0, m0, start, far)
+    same = pl(seed + 3, [], start, start)
+    assert same == G.find_path(g0, m0, start, start)
+    with pytest.raises(ValueError, match="includes"):
+        Planner(N, spec, orc, bounds, obstacles, seed=seed, include=include)(seed, obstacles, start, goal)
+    assert pl.info()["eager_calls"] == 0
