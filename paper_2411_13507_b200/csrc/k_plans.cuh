@@ -1,0 +1,693 @@
+// Captured plans on top of the cut (included by k_cut.cu, whose cut_prepare / cut_enqueue /
+// mask helpers they use): the Replanner (re-cut + search per replanning cycle) and the Planner
+// (build -> cut -> search of one scene), each one CUDA graph per call.  See DESIGN.md section 5.
+#pragma once
+
+namespace bzg {
+
+// ---- Replanner (bzg_replanner): cut + find_path on a fixed graph as ONE captured CUDA graph.
+// A replanning cycle (sim.py:324-330 re-cuts with the moved obstacles, then graph.find_path) on
+// the device is ~20-30 launches whose inputs change only through the obstacle blob and the
+// snapping parameters; both go through pinned staging, so a cycle is one memcpy into pinned
+// memory, one graph launch and one synchronisation.  With a static / dynamic split, the static
+// obstacles are cut once (their per-obstacle outcome rows kept in a slot-major pool, as the
+// re-cut cache keeps them) and a cycle cuts only the dynamic ones, writing their rows into the
+// pool, and rebuilds alive / provenance in list order (k_cut_combine).  The capture is valid
+// while the dynamic list keeps its shape (count, rows, box / canonical / general kinds:
+// CutPrep::same_shape) and the work lists fit their capacities; otherwise the cycle runs
+// eagerly and is re-captured.
+struct Replanner {
+  Ctx* c = nullptr;
+  Graph* g = nullptr;
+  uint64_t version = 0;
+  int64_t E = 0, Wb = 0;
+  int n_obs = 0;
+  bzg_cut_config cfg{};
+  Mask mk;                                 // the replanner's mask (rewritten every cycle)
+  bool split = false;                      // static / dynamic split
+  std::vector<int> stat, dyn;              // list positions of the static / dynamic obstacles
+  std::string static_key;                  // the static obstacles as last cut (change check)
+  long long static_cnt[5] = {0, 0, 0, 0, 0};  // their code-0 / code-1 / QP pairs, QP safe / unsafe
+  DevBuf pool;                             // slot-major outcome rows, 3 Wb words per obstacle
+  DevBuf slots;                            // list position -> pool slot (static first, then dynamic)
+  CutPrep shape;                           // the captured layout (of the dynamic list)
+  CutCaps caps;
+  unsigned char* h_blob = nullptr;         // pinned: the obstacle blob the graph uploads
+  size_t h_blob_bytes = 0;
+  unsigned long long* h_cnt = nullptr;     // pinned: the cut's counters
+  PathStage* ps = nullptr;
+  DevBuf ws[kWsSlots];                     // own workspaces (the graph reads their addresses)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0, runs = 0, eager = 0, captures = 0;
+};
+
+namespace {
+
+// obstacles [idx...] of a list as a list of their own
+struct SubList {
+  std::vector<int32_t> ro{0};
+  std::vector<double> A, b, lo, hi;
+  std::vector<uint8_t> box;
+  int n() const { return (int)box.size(); }
+};
+SubList sublist(const std::vector<int>& idx, int m, const int32_t* row_off, const double* A, const double* b,
+                const uint8_t* is_box, const double* box_lo, const double* box_hi) {
+  SubList s;
+  for (int o : idx) {
+    const int r0 = row_off[o], r1 = row_off[o + 1];
+    s.ro.push_back(s.ro.back() + (r1 - r0));
+    s.A.insert(s.A.end(), A + (size_t)r0 * m, A + (size_t)r1 * m);
+    s.b.insert(s.b.end(), b + r0, b + r1);
+    s.box.push_back(is_box[o]);
+    s.lo.insert(s.lo.end(), box_lo + (size_t)o * m, box_lo + (size_t)(o + 1) * m);
+    s.hi.insert(s.hi.end(), box_hi + (size_t)o * m, box_hi + (size_t)(o + 1) * m);
+  }
+  return s;
+}
+std::string sublist_key(const SubList& s) {
+  std::string k;
+  auto add = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  add(s.ro.data(), s.ro.size() * sizeof(int32_t));
+  add(s.A.data(), s.A.size() * sizeof(double));
+  add(s.b.data(), s.b.size() * sizeof(double));
+  add(s.box.data(), s.box.size());
+  add(s.lo.data(), s.lo.size() * sizeof(double));
+  add(s.hi.data(), s.hi.size() * sizeof(double));
+  return k;
+}
+
+// pool rows of the dynamic obstacles (slots n_static ..)
+CutBits dyn_bits(Replanner* r) {
+  uint32_t* base = r->pool.as<uint32_t>() + (size_t)r->stat.size() * 3 * r->Wb;
+  return CutBits{base, base + r->Wb, base + 2 * r->Wb, r->Wb, 3 * r->Wb};
+}
+
+// the static obstacles' outcome rows and counts (eager; on creation and when they change)
+void replanner_cut_static(Replanner* r, const SubList& st) {
+  Ctx* c = r->c;
+  Mask tmp;
+  uint32_t* base = r->pool.as<uint32_t>();
+  with_ws(c, r->ws, [&] {
+    cut_graph_impl(c, r->g, st.n(), st.ro.data(), st.A.data(), st.b.data(), st.box.data(), st.lo.data(),
+                   st.hi.data(), &r->cfg, &tmp, CutBits{base, base + r->Wb, base + 2 * r->Wb, r->Wb, 3 * r->Wb});
+  });
+  for (int i = 0; i < 5; ++i) r->static_cnt[i] = tmp.counters[1 + i];
+  r->static_key = sublist_key(st);
+}
+
+// the whole list's counters from the static ones and a dynamic cut's codes (h: its read-back)
+void replanner_counters(Replanner* r, const unsigned long long* h) {
+  r->mk.counters[0] = r->E * (long long)r->n_obs;
+  for (int i = 0; i < 5; ++i) r->mk.counters[1 + i] = r->static_cnt[i] + (long long)h[i];
+}
+
+void replanner_combine(Replanner* r) {
+  Ctx* c = r->c;
+  launch(c, "k_cut_combine", k_cut_combine, dim3(div_up(r->E, 256)), dim3(256), 0, r->E, r->n_obs,
+         (const uint32_t*)r->pool.as<uint32_t>(), r->Wb, (const int*)r->slots.as<int>(), r->mk.alive.as<uint8_t>(),
+         r->mk.prov.as<uint8_t>());
+}
+
+void replanner_drop_graph(Replanner* r) {
+  if (r->exec) cudaGraphExecDestroy(r->exec);
+  if (r->graph) cudaGraphDestroy(r->graph);
+  r->exec = nullptr;
+  r->graph = nullptr;
+}
+
+// one cycle's launches: upload the staged blob, cut (the dynamic obstacles when split, then the
+// combination with the static rows), search
+template <int Gc, int Mc>
+void replanner_enqueue(Replanner* r) {
+  Ctx* c = r->c;
+  DevBuf& d_blob = c->ws[WS_CUTOBS];
+  d_blob.alloc(r->shape.blob.size(), c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(d_blob.ptr, r->h_blob, r->shape.blob.size(), cudaMemcpyHostToDevice, c->stream));
+  cut_enqueue<Gc, Mc>(c, r->g, r->shape, d_blob.as<unsigned char>(), &r->cfg, &r->mk,
+                      r->split ? dyn_bits(r) : CutBits{}, r->caps, r->h_cnt);
+  if (r->split) replanner_combine(r);
+  path_stage_enqueue(c, r->g, &r->mk, r->ps);
+}
+
+// (re)capture for the layout of p, after an eager cycle on the same obstacles (c->qp_hint and
+// the grid decision are this list's)
+template <int Gc, int Mc>
+void replanner_capture(Replanner* r, const CutPrep& p, unsigned long long seen_pend, unsigned long long seen_gen) {
+  Ctx* c = r->c;
+  replanner_drop_graph(r);
+  r->shape = p;
+  CutCaps cc = default_caps(c, r->g, p);
+  cc.cap = std::max(cc.cap, seen_pend + seen_pend / 4 + 1024);
+  if (p.any_general) cc.gen_cap = std::max(cc.gen_cap, seen_gen + seen_gen / 4 + 1024);
+  cc.qcap = std::max<long long>(cc.qcap, (long long)(seen_pend + seen_pend / 4 + 1024));
+  cc.qcap = std::min<long long>(cc.qcap, (long long)cc.cap);
+  cc.grid = p.grid_cand && c->grid_sparse && c->grid_nobs == p.n_obs ? 1 : 0;
+  r->caps = cc;
+  if (r->h_blob_bytes < p.blob.size()) {
+    if (r->h_blob) cudaFreeHost(r->h_blob);
+    r->h_blob = nullptr;
+    r->h_blob_bytes = 0;
+    BZG_CHECK_CUDA(cudaMallocHost(&r->h_blob, p.blob.size()));
+    r->h_blob_bytes = p.blob.size();
+  }
+  std::memcpy(r->h_blob, p.blob.data(), p.blob.size());
+  const long long counters[6] = {r->mk.counters[0], r->mk.counters[1], r->mk.counters[2], r->mk.counters[3],
+                                 r->mk.counters[4], r->mk.counters[5]};
+  with_ws(c, r->ws, [&] {
+    replanner_enqueue<Gc, Mc>(r);  // sizes every workspace for these capacities
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    r->exec = capture_graph(c, [&] { replanner_enqueue<Gc, Mc>(r); }, &r->kernels, &r->graph);
+  });
+  for (int i = 0; i < 6; ++i) r->mk.counters[i] = counters[i];  // (the warm-up rewrote them)
+  ++r->captures;
+}
+
+}  // namespace
+
+void replanner_destroy(Replanner* r) {
+  if (!r) return;
+  if (r->c) cudaStreamSynchronize(r->c->stream);
+  replanner_drop_graph(r);
+  for (auto& w : r->ws) w.release();
+  path_stage_destroy(r->ps);
+  if (r->h_blob) cudaFreeHost(r->h_blob);
+  if (r->h_cnt) cudaFreeHost(r->h_cnt);
+  delete r;
+}
+
+// One cycle: the cut of the obstacle list and the search from start to goal.  *eager_out = 1
+// when the cycle could not use the captured graph (shape change, work-list overflow) and ran
+// eagerly (then it was re-captured).
+void replanner_run(Replanner* r, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                   const uint8_t* is_box, const double* box_lo, const double* box_hi, const double* start,
+                   const double* goal, std::vector<int64_t>& path, double* dist, int* eager_out) {
+  Ctx* c = r->c;
+  Graph* g = r->g;
+  const int m = g->m;
+  BZG_REQUIRE(g->version == r->version && g->E == r->E, BZG_EINVAL,
+              "stale replanner: the graph's edge set changed after it was created");
+  // n_obs == the dynamic count (split): the arrays hold the dynamic obstacles only, in list
+  // order, and the static ones stand as last given
+  const bool dyn_only = r->split && n_obs == (int)r->dyn.size();
+  BZG_REQUIRE(n_obs == r->n_obs || dyn_only, BZG_EINVAL,
+              "a replanner keeps its obstacle count (or takes its dynamic obstacles alone)");
+  check_obstacles(n_obs, row_off, is_box, m);
+  ++r->runs;
+  *eager_out = 0;
+  // the list the cycle cuts: the dynamic obstacles (split) or all of them
+  SubList dl;
+  if (r->split && !dyn_only) {
+    const SubList st = sublist(r->stat, m, row_off, A, b, is_box, box_lo, box_hi);
+    if (sublist_key(st) != r->static_key) replanner_cut_static(r, st);  // rows are data: the graph stays valid
+    dl = sublist(r->dyn, m, row_off, A, b, is_box, box_lo, box_hi);
+  }
+  const bool sub = r->split && !dyn_only;
+  const int nc = sub ? dl.n() : n_obs;
+  const int32_t* ro = sub ? dl.ro.data() : row_off;
+  const double* cA = sub ? dl.A.data() : A;
+  const double* cb = sub ? dl.b.data() : b;
+  const uint8_t* cbox = sub ? dl.box.data() : is_box;
+  const double* clo = sub ? dl.lo.data() : box_lo;
+  const double* chi = sub ? dl.hi.data() : box_hi;
+  const int qp_rows = check_obstacles(nc, ro, cbox, m);
+  dispatch_cut(g->gamma, m, [&](auto G_, auto M_) {
+    constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+    CutPrep p;
+    cut_prepare_t<Mc>(g, nc, ro, cA, cb, cbox, clo, chi, &r->cfg, qp_rows, p);
+    path_stage_set(r->ps, g, start, goal);  // no launch of this replanner is pending
+    if (r->exec && p.same_shape(r->shape)) {
+      std::memcpy(r->h_blob, p.blob.data(), p.blob.size());
+      BZG_CHECK_CUDA(cudaGraphLaunch(r->exec, c->stream));
+      c->launches += r->kernels;
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      const unsigned long long* h = r->h_cnt;
+      BZG_REQUIRE(h[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
+      if (h[5] <= r->caps.cap && h[6] <= r->caps.gen_cap && (long long)h[5] <= r->caps.qcap) {
+        if (r->split) replanner_counters(r, h); else mask_counters(&r->mk, h);
+        r->mk.n_qp = 0;
+        with_ws(c, r->ws, [&] { path_stage_collect(c, g, r->ps, path, dist); });
+        return;
+      }
+    }
+    // eager cycle on the replanner's workspaces, then a capture for this layout
+    *eager_out = 1;
+    ++r->eager;
+    with_ws(c, r->ws, [&] {
+      cut_graph_impl(c, g, nc, ro, cA, cb, cbox, clo, chi, &r->cfg, &r->mk, r->split ? dyn_bits(r) : CutBits{});
+      if (r->split) {
+        const unsigned long long h[5] = {(unsigned long long)r->mk.counters[1], (unsigned long long)r->mk.counters[2],
+                                         (unsigned long long)r->mk.counters[3], (unsigned long long)r->mk.counters[4],
+                                         (unsigned long long)r->mk.counters[5]};
+        r->mk.n_obs = n_obs;
+        replanner_counters(r, h);
+        replanner_combine(r);
+      }
+      path_stage_enqueue(c, g, &r->mk, r->ps);
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      path_stage_collect(c, g, r->ps, path, dist);
+    });
+    replanner_capture<Gc, Mc>(r, p, c->cut_last_pend, c->cut_last_gen);
+  });
+}
+
+Ctx* replanner_ctx(const Replanner* r) { return r->c; }
+const Mask* replanner_mask(const Replanner* r) { return &r->mk; }
+void replanner_info(const Replanner* r, int64_t info[4]) {
+  info[0] = r->kernels;
+  info[1] = r->runs;
+  info[2] = r->eager;
+  info[3] = r->captures;
+}
+
+Replanner* replanner_create(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const double* A, const double* b,
+                            const uint8_t* is_box, const double* box_lo, const double* box_hi,
+                            const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo,
+                            const double* tube_hi, double eps, int pos_only, int require_tube) {
+  BZG_REQUIRE(n_obs >= 1 && n_obs < (1 << 20), BZG_EINVAL, "a replanner needs at least one obstacle");
+  BZG_REQUIRE(g->E >= 1, BZG_EINVAL, "a replanner needs a graph with edges");
+  check_obstacles(n_obs, row_off, is_box, g->m);
+  Replanner* r = new Replanner();
+  try {
+    r->c = c;
+    r->g = g;
+    r->version = g->version;
+    r->E = g->E;
+    r->Wb = (g->E + 31) / 32;
+    r->n_obs = n_obs;
+    r->cfg = *cfg;
+    for (int o = 0; o < n_obs; ++o) (dynamic && !dynamic[o] ? r->stat : r->dyn).push_back(o);
+    BZG_REQUIRE(!r->dyn.empty(), BZG_EINVAL, "a replanner needs at least one dynamic obstacle");
+    r->split = !r->stat.empty();
+    r->ps = path_stage_create(g, tube_lo, tube_hi, eps, pos_only, require_tube);
+    BZG_CHECK_CUDA(cudaMallocHost(&r->h_cnt, 8 * sizeof(unsigned long long)));
+    if (r->split) {
+      r->pool.alloc((size_t)3 * n_obs * r->Wb * sizeof(uint32_t), c->stream);
+      std::vector<int> slot(n_obs);
+      for (size_t k = 0; k < r->stat.size(); ++k) slot[r->stat[k]] = (int)k;
+      for (size_t k = 0; k < r->dyn.size(); ++k) slot[r->dyn[k]] = (int)(r->stat.size() + k);
+      r->slots.alloc(n_obs * sizeof(int), c->stream);
+      BZG_CHECK_CUDA(cudaMemcpyAsync(r->slots.ptr, slot.data(), n_obs * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));  // (slot leaves scope)
+      replanner_cut_static(r, sublist(r->stat, g->m, row_off, A, b, is_box, box_lo, box_hi));
+    }
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    int eager = 0;
+    std::vector<double> zero(g->n, 0.0);
+    // the first cycle runs eagerly (sizing, grid decision, QP count) and captures
+    replanner_run(r, n_obs, row_off, A, b, is_box, box_lo, box_hi, zero.data(), zero.data(), path, &dist, &eager);
+    r->runs = 0;
+    r->eager = 0;
+  } catch (...) {
+    replanner_destroy(r);
+    throw;
+  }
+  return r;
+}
+
+// ---- Planner (bzg_planner): build -> cut -> find_path of one scene as ONE captured CUDA graph.
+// The whole step of the reference's plan_once stage (graph.py:129-430) for a fixed scene shape
+// (oracle, N, spec, bounds, obstacle-list shape): a call stages the sampler seed (PCG64 words),
+// the included vertices, the obstacle blob and the snapping targets in pinned memory and
+// launches the graph once.  The build runs without its mid-call read-back: the CSR arrays have
+// a capacity (every ordered pair for small graphs), the edge count stays on the device
+// (Graph::dE, read by the cut and search kernels) and comes back with the sampler's
+// acceptance count and the cut's counters at the end, where the plan checks them; a call whose
+// sampler round fell short, whose edges outgrew the capacity or whose work lists overflowed
+// runs eagerly (same results) and the graph is re-captured with larger capacities.
+struct Planner {
+  Ctx* c = nullptr;
+  bzg_build_desc d{};                      // the scene; its arrays point at the copies below
+  std::vector<double> F, G, D, slo, shi, xA, xb;
+  std::vector<double> inc0;                // the creation call's include rows (the Morton box of the
+                                           // capture; it steers tiling only, so later rows may differ)
+  Graph g;                                 // the plan's graph (CSR arrays of capacity Ecap)
+  long long Ecap = 0, E = 0;
+  double sample_est = 1.0;                 // acceptance estimate the captured sampler round uses
+  Mask mk;
+  int n_obs = 0;
+  bzg_cut_config cfg{};
+  CutPrep shape;
+  CutCaps caps;
+  // keep-in regions (configs 1 and 5): the single-round region sampler and the region rows
+  int R = 0;
+  std::vector<int64_t> rN;
+  std::vector<double> rlo, rhi, rA, rb, rest, reg_F, reg_G, reg_blo, reg_bhi;
+  std::vector<int32_t> rrow_off, reg_row_off;
+  RegionSamplePlan* rs = nullptr;
+  RegionRowsCache* rows = nullptr;
+  long long* h_acc = nullptr;              // pinned: per-region acceptances
+  DevBuf dF, d_in;                         // oracle rows (uploaded once); staged inputs
+  unsigned long long* h_in = nullptr;      // pinned: [4 PCG64 words per stream][include rows]
+  size_t in_bytes = 0;
+  unsigned char* h_blob = nullptr;         // pinned: the obstacle blob
+  size_t h_blob_bytes = 0;
+  unsigned long long* h_cnt = nullptr;     // pinned: the cut's counters
+  long long* h_build = nullptr;            // pinned: the edge count
+  int* h_sampled = nullptr;                // pinned: the sampler round's acceptances
+  PathStage* ps = nullptr;
+  DevBuf ws[kWsSlots];
+  Arena arena;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0, runs = 0, eager = 0, captures = 0;
+  int last_reason = 0;  // why the last eager call was eager: 1 shape, 2 sampler, 3 edges, 4 work lists
+};
+
+namespace {
+
+void planner_drop_graph(Planner* p) {
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  p->exec = nullptr;
+  p->graph = nullptr;
+}
+
+// the captured sequence: inputs up, sample, include rows, pairs + CSR, obstacle blob up, cut,
+// search.  p->g.E is the capacity while this runs.
+template <int Gc, int Mc>
+void planner_enqueue(Planner* p) {
+  Ctx* c = p->c;
+  Graph* g = &p->g;
+  const int n = g->n;
+  BZG_CHECK_CUDA(cudaMemcpyAsync(p->d_in.ptr, p->h_in, p->in_bytes, cudaMemcpyHostToDevice, c->stream));
+  c->sample_est = p->sample_est;
+  c->sample_check = nullptr;
+  if (p->R > 0)
+    region_sample_plan_enqueue(c, p->rs, p->d_in.as<unsigned long long>(), g->vertices.as<double>(), p->h_acc);
+  else
+    sample_states(c, &p->d, g->vertices.as<double>(), /*single_round=*/true, p->d_in.as<unsigned long long>());
+  if (p->d.n_include > 0)
+    BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)p->d.N * n,
+                                   reinterpret_cast<const double*>(p->d_in.as<unsigned long long>() +
+                                                                   4 * std::max(p->R, 1)),
+                                   (size_t)p->d.n_include * n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  BuildCapture bc{p->dF.as<double>(), p->h_build, p->h_sampled};
+  bc.rows = p->rows;
+  build_pairs(c, &p->d, g, 0.0, nullptr, &bc);
+  g->dE = c->ws[WS_RPTR].as<long long>() + g->V;  // rptr[rows]: the edge count on the device
+  DevBuf& d_blob = c->ws[WS_CUTOBS];
+  d_blob.alloc(p->shape.blob.size(), c->stream);
+  BZG_CHECK_CUDA(cudaMemcpyAsync(d_blob.ptr, p->h_blob, p->shape.blob.size(), cudaMemcpyHostToDevice, c->stream));
+  cut_enqueue<Gc, Mc>(c, g, p->shape, d_blob.as<unsigned char>(), &p->cfg, &p->mk, CutBits{}, p->caps, p->h_cnt);
+  path_stage_enqueue(c, g, &p->mk, p->ps);
+}
+
+// (re)capture for the obstacle layout of prep, after an eager call on the same inputs
+template <int Gc, int Mc>
+void planner_capture(Planner* p, const CutPrep& prep) {
+  Ctx* c = p->c;
+  Graph* g = &p->g;
+  planner_drop_graph(p);
+  p->shape = prep;
+  const long long E_last = g->E;
+  const long long counters[6] = {p->mk.counters[0], p->mk.counters[1], p->mk.counters[2], p->mk.counters[3],
+                                 p->mk.counters[4], p->mk.counters[5]};
+  g->E = p->Ecap;  // capacity-sized launches
+  CutCaps cc = default_caps(c, g, prep);
+  const unsigned long long seen = c->cut_last_pend, seen_gen = c->cut_last_gen;
+  cc.cap = std::max(cc.cap, seen + seen / 4 + 1024);
+  if (prep.any_general) cc.gen_cap = std::max(cc.gen_cap, seen_gen + seen_gen / 4 + 1024);
+  cc.qcap = std::min<long long>(std::max<long long>(cc.qcap, (long long)(seen + seen / 4 + 1024)), (long long)cc.cap);
+  cc.grid = prep.grid_cand && c->grid_sparse && c->grid_nobs == prep.n_obs ? 1 : 0;
+  p->caps = cc;
+  if (p->h_blob_bytes < prep.blob.size()) {
+    if (p->h_blob) cudaFreeHost(p->h_blob);
+    p->h_blob = nullptr;
+    p->h_blob_bytes = 0;
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_blob, prep.blob.size()));
+    p->h_blob_bytes = prep.blob.size();
+  }
+  std::memcpy(p->h_blob, prep.blob.data(), prep.blob.size());
+  g->src.alloc((size_t)p->Ecap * sizeof(int), c->stream);
+  g->dst.alloc((size_t)p->Ecap * sizeof(int), c->stream);
+  g->cost.alloc((size_t)p->Ecap * sizeof(double), c->stream);
+  mask_begin(c, g, &p->mk, p->n_obs);  // alive / provenance of capacity size
+  try {
+    with_ws(
+        c, p->ws,
+        [&] {
+          planner_enqueue<Gc, Mc>(p);  // sizes every workspace for these capacities
+          BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+          p->exec = capture_graph(c, [&] { planner_enqueue<Gc, Mc>(p); }, &p->kernels, &p->graph);
+        },
+        &p->arena);
+  } catch (...) {
+    g->dE = nullptr;
+    g->E = E_last;
+    throw;
+  }
+  g->dE = nullptr;  // (the launches hold it)
+  g->E = E_last;
+  p->mk.E = E_last;
+  for (int i = 0; i < 6; ++i) p->mk.counters[i] = counters[i];
+  ++p->captures;
+}
+
+}  // namespace
+
+void planner_destroy(Planner* p) {
+  if (!p) return;
+  if (p->c) cudaStreamSynchronize(p->c->stream);
+  planner_drop_graph(p);
+  for (auto& w : p->ws) w.release();
+  p->arena.chunks.clear();
+  path_stage_destroy(p->ps);
+  region_sample_plan_destroy(p->rs);
+  region_rows_cache_destroy(p->rows);
+  for (void* h : {(void*)p->h_in, (void*)p->h_blob, (void*)p->h_cnt, (void*)p->h_build, (void*)p->h_sampled,
+                  (void*)p->h_acc})
+    if (h) cudaFreeHost(h);
+  delete p;
+}
+
+// One call: build with the seed's PCG64 words (pcg: state hi/lo, inc hi/lo; for keep-in regions
+// four per region stream) and the include rows, cut with the obstacles, search from start to
+// goal.  *eager_out = 1 when it ran eagerly.
+void planner_run(Planner* p, const uint64_t* pcg, const double* include, int n_obs, const int32_t* row_off,
+                 const double* A, const double* b, const uint8_t* is_box, const double* box_lo,
+                 const double* box_hi, const double* start, const double* goal, std::vector<int64_t>& path,
+                 double* dist, int* eager_out) {
+  Ctx* c = p->c;
+  Graph* g = &p->g;
+  const int n = g->n;
+  BZG_REQUIRE(n_obs == p->n_obs, BZG_EINVAL, "a planner keeps its obstacle count");
+  BZG_REQUIRE(p->d.n_include == 0 || include, BZG_EINVAL, "include rows missing");
+  const int qp_rows = check_obstacles(n_obs, row_off, is_box, g->m);
+  ++p->runs;
+  *eager_out = 0;
+  const int nw = 4 * std::max(p->R, 1);
+  std::memcpy(p->h_in, pcg, nw * sizeof(uint64_t));
+  if (p->d.n_include > 0) std::memcpy(p->h_in + nw, include, (size_t)p->d.n_include * n * sizeof(double));
+  path_stage_set(p->ps, g, start, goal);
+  dispatch_cut(g->gamma, g->m, [&](auto G_, auto M_) {
+    constexpr int Gc = decltype(G_)::value, Mc = decltype(M_)::value;
+    CutPrep prep;
+    const long long E_keep = g->E;
+    g->E = std::max<long long>(p->Ecap, 1);  // (cut_prepare reads E > 0 only: a plan's graph has edges)
+    cut_prepare_t<Mc>(g, n_obs, row_off, A, b, is_box, box_lo, box_hi, &p->cfg, qp_rows, prep);
+    g->E = E_keep;
+    p->last_reason = 1;
+    if (p->exec && prep.same_shape(p->shape)) {
+      std::memcpy(p->h_blob, prep.blob.data(), prep.blob.size());
+      BZG_CHECK_CUDA(cudaGraphLaunch(p->exec, c->stream));
+      c->launches += p->kernels;
+      BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+      const unsigned long long* h = p->h_cnt;
+      const long long E = *p->h_build;
+      bool sampled_ok = true;
+      if (p->R > 0)
+        for (int r = 0; r < p->R; ++r) sampled_ok = sampled_ok && p->h_acc[r] >= p->rN[r];
+      else
+        sampled_ok = *p->h_sampled >= p->d.N;
+      p->last_reason = !sampled_ok ? 2 : (E > p->Ecap ? 3 : 4);
+      if (sampled_ok && E <= p->Ecap) {
+        BZG_REQUIRE(h[7] == 0, BZG_EINVAL, "cannot project onto an empty polytope (geometry.py:226-229)");
+        if (h[5] <= p->caps.cap && h[6] <= p->caps.gen_cap && (long long)h[5] <= p->caps.qcap) {
+          g->E = E;
+          p->E = E;
+          ++g->version;
+          g->points_ready = false;
+          p->mk.E = E;
+          mask_counters(&p->mk, h);
+          p->mk.counters[0] = E * (long long)n_obs;
+          p->mk.n_qp = 0;
+          with_ws(c, p->ws, [&] { path_stage_collect(c, g, p->ps, path, dist); }, &p->arena);
+          p->last_reason = 0;
+          return;
+        }
+      }
+      if (!sampled_ok) p->sample_est *= 0.9;  // the next capture draws more candidates
+    }
+    // eager call on the plan's graph and workspaces, then a capture
+    *eager_out = 1;
+    ++p->eager;
+    with_ws(
+        c, p->ws,
+        [&] {
+          bzg_build_desc d = p->d;
+          d.pcg_state_hi = pcg[0];
+          d.pcg_state_lo = pcg[1];
+          d.pcg_inc_hi = pcg[2];
+          d.pcg_inc_lo = pcg[3];
+          d.include = include;
+          g->dE = nullptr;
+          c->sample_check = nullptr;
+          c->sample_est = p->sample_est;
+          sample_states(c, &d, g->vertices.as<double>(), /*single_round=*/true);
+          if (d.n_include > 0)
+            BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)d.N * n, include,
+                                           (size_t)d.n_include * n * sizeof(double), cudaMemcpyHostToDevice,
+                                           c->stream));
+          if (!build_pairs(c, &d, g)) {
+            sample_states(c, &d, g->vertices.as<double>());
+            build_pairs(c, &d, g);
+          }
+          // the captured round draws ~1.3x the candidates the measured acceptance needs, so other
+          // seeds' rounds (acceptance varies by a few percent) rarely fall short
+          p->sample_est = std::min(p->sample_est, 0.85 * c->sample_est);
+          p->E = g->E;
+          cut_graph_impl(c, g, n_obs, row_off, A, b, is_box, box_lo, box_hi, &p->cfg, &p->mk, CutBits{});
+          path_stage_enqueue(c, g, &p->mk, p->ps);
+          BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+          path_stage_collect(c, g, p->ps, path, dist);
+        },
+        &p->arena);
+    // capacity: the edge count with 50 % headroom (other seeds and obstacle lists vary it by a
+    // few percent), at most every ordered pair; the capacity sizes the cut's and search's grids
+    const long long V = g->V;
+    p->Ecap = std::max(p->Ecap, std::min(V * (V - 1), p->E + p->E / 2 + 4096));
+    if (p->R > 0) {  // the captured region round, sized from this call's acceptance rates
+      planner_drop_graph(p);
+      region_sample_plan_destroy(p->rs);
+      p->rs = nullptr;
+      p->rs = region_sample_plan_create(c, n, p->R, p->rN.data(), p->rlo.data(), p->rhi.data(), p->rrow_off.data(),
+                                        p->rA.data(), p->rb.data(), p->d.eps_geo, p->rest.data());
+    }
+    planner_capture<Gc, Mc>(p, prep);
+  });
+}
+
+Ctx* planner_ctx(const Planner* p) { return p->c; }
+Graph* planner_graph(Planner* p) { return &p->g; }
+const Mask* planner_mask(const Planner* p) { return &p->mk; }
+void planner_info(const Planner* p, int64_t info[6]) {
+  info[5] = p->last_reason;
+  info[0] = p->kernels;
+  info[1] = p->runs;
+  info[2] = p->eager;
+  info[3] = p->captures;
+  info[4] = p->Ecap;
+}
+
+Planner* planner_create(Ctx* c, const bzg_build_desc* d, const bzg_region_sampler* rsam, int n_obs,
+                        const int32_t* row_off, const double* A, const double* b, const uint8_t* is_box,
+                        const double* box_lo, const double* box_hi, const bzg_cut_config* cfg,
+                        const double* tube_lo, const double* tube_hi, double eps, int pos_only, int require_tube) {
+  BZG_REQUIRE(d->m >= 1 && d->gamma >= 1 && d->p == 2 * d->gamma - 1, BZG_EINVAL, "bad curve specification");
+  BZG_REQUIRE(d->N >= 2, BZG_EINVAL, "need at least two vertices");
+  BZG_REQUIRE(d->F && d->G && d->D && d->sample_lo && d->sample_hi && d->xd_A && d->xd_b, BZG_EINVAL,
+              "oracle, boundary matrix and sampler inputs are required");
+  BZG_REQUIRE(!d->vertices && d->row_end <= 0 && d->row_begin == 0, BZG_EUNSUPPORTED,
+              "a planner samples its own vertices and builds every row");
+  BZG_REQUIRE((d->n_regions > 0) == (rsam != nullptr), BZG_EINVAL,
+              "keep-in regions need their sampler (and only they take one)");
+  BZG_REQUIRE(n_obs >= 0 && n_obs < (1 << 20), BZG_EINVAL, "obstacle count out of range");
+  Planner* p = new Planner();
+  try {
+    p->c = c;
+    const int n = d->m * d->gamma;
+    p->d = *d;
+    p->F.assign(d->F, d->F + (size_t)d->n_F * 2 * n);
+    p->G.assign(d->G, d->G + d->n_F);
+    p->D.assign(d->D, d->D + (size_t)(d->p + 1) * 2 * d->gamma);
+    p->slo.assign(d->sample_lo, d->sample_lo + n);
+    p->shi.assign(d->sample_hi, d->sample_hi + n);
+    p->xA.assign(d->xd_A, d->xd_A + (size_t)d->xd_rows * n);
+    p->xb.assign(d->xd_b, d->xd_b + d->xd_rows);
+    p->d.F = p->F.data();
+    p->d.G = p->G.data();
+    p->d.D = p->D.data();
+    p->d.sample_lo = p->slo.data();
+    p->d.sample_hi = p->shi.data();
+    p->d.xd_A = p->xA.data();
+    p->d.xd_b = p->xb.data();
+    if (d->n_include > 0) p->inc0.assign(d->include, d->include + (size_t)d->n_include * n);
+    p->d.include = d->n_include > 0 ? p->inc0.data() : nullptr;
+    p->d.vertices = nullptr;
+    if (rsam) {  // keep-in regions: copies of the region rows and of the region sampler inputs
+      const int R = d->n_regions, m = d->m;
+      BZG_REQUIRE(rsam->n_regions == R && rsam->N && rsam->lo && rsam->hi && rsam->row_off && rsam->A && rsam->b,
+                  BZG_EINVAL, "region sampler inputs missing");
+      p->R = R;
+      p->rN.assign(rsam->N, rsam->N + R);
+      long long tot = 0;
+      for (int r = 0; r < R; ++r) tot += p->rN[r];
+      BZG_REQUIRE(tot == d->N, BZG_EINVAL, "the region sample counts must add up to N");
+      p->rlo.assign(rsam->lo, rsam->lo + (size_t)R * n);
+      p->rhi.assign(rsam->hi, rsam->hi + (size_t)R * n);
+      p->rrow_off.assign(rsam->row_off, rsam->row_off + R + 1);
+      p->rA.assign(rsam->A, rsam->A + (size_t)rsam->row_off[R] * n);
+      p->rb.assign(rsam->b, rsam->b + rsam->row_off[R]);
+      p->rest.assign(R, 1.0);
+      p->reg_row_off.assign(d->region_row_off, d->region_row_off + R + 1);
+      p->reg_F.assign(d->region_F, d->region_F + (size_t)d->region_row_off[R] * 2 * n);
+      p->reg_G.assign(d->region_G, d->region_G + d->region_row_off[R]);
+      p->d.region_row_off = p->reg_row_off.data();
+      p->d.region_F = p->reg_F.data();
+      p->d.region_G = p->reg_G.data();
+      if (d->region_box_lo && d->region_box_hi) {
+        p->reg_blo.assign(d->region_box_lo, d->region_box_lo + (size_t)R * m);
+        p->reg_bhi.assign(d->region_box_hi, d->region_box_hi + (size_t)R * m);
+        p->d.region_box_lo = p->reg_blo.data();
+        p->d.region_box_hi = p->reg_bhi.data();
+      }
+      p->rows = region_rows_cache_create(c, &p->d);
+      BZG_CHECK_CUDA(cudaMallocHost(&p->h_acc, R * sizeof(long long)));
+    }
+    p->n_obs = n_obs;
+    p->cfg = *cfg;
+    Graph* g = &p->g;
+    g->ctx = c;
+    g->m = d->m;
+    g->gamma = d->gamma;
+    g->p = d->p;
+    g->n = n;
+    g->V = d->N + d->n_include;
+    g->row_begin = 0;
+    g->row_end = g->V;
+    g->D = p->D;
+    g->vertices.alloc((size_t)g->V * n * sizeof(double), c->stream);
+    g->row_ptr.alloc((g->V + 1) * sizeof(long long), c->stream);
+    p->dF.alloc(p->F.size() * sizeof(double), c->stream);
+    BZG_CHECK_CUDA(cudaMemcpyAsync(p->dF.ptr, p->F.data(), p->F.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                   c->stream));
+    p->in_bytes = 4 * std::max(p->R, 1) * sizeof(unsigned long long) + (size_t)d->n_include * n * sizeof(double);
+    p->d_in.alloc(p->in_bytes, c->stream);
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_in, p->in_bytes));
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_cnt, 8 * sizeof(unsigned long long)));
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_build, sizeof(long long)));
+    BZG_CHECK_CUDA(cudaMallocHost(&p->h_sampled, sizeof(int)));
+    BZG_CHECK_CUDA(cudaStreamSynchronize(c->stream));
+    p->ps = path_stage_create(g, tube_lo, tube_hi, eps, pos_only, require_tube);
+    // the first call (the descriptor's own seed and include rows, the given obstacles) runs
+    // eagerly, sizes everything and captures
+    std::vector<uint64_t> pcg = {d->pcg_state_hi, d->pcg_state_lo, d->pcg_inc_hi, d->pcg_inc_lo};
+    if (rsam) pcg.assign(rsam->pcg, rsam->pcg + 4 * (size_t)p->R);
+    std::vector<int64_t> path;
+    double dist = 0.0;
+    int eager = 0;
+    std::vector<double> zero(n, 0.0);
+    planner_run(p, pcg.data(), d->include, n_obs, row_off, A, b, is_box, box_lo, box_hi, zero.data(), zero.data(),
+                path, &dist, &eager);
+    p->runs = 0;
+    p->eager = 0;
+  } catch (...) {
+    planner_destroy(p);
+    throw;
+  }
+  return p;
+}
+
+}  // namespace bzg
