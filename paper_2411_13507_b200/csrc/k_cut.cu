@@ -440,6 +440,21 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
       control_points<G, M>(xi, xj, dp.D, P);
       kill = first_kill[e];
     }
+    // pass-2 staging: each lane's control points in shared memory for the lanes that take its
+    // pairs.  Stored before pass 1 so P is dead during pass 1 and the bounding box (mn, mx)
+    // stays in registers there (with P live the compiler rebuilt mn / mx from P for every
+    // obstacle of the window: ~60 compare / select instructions per pass-1 test).
+    constexpr int NP = M * 2 * G;
+    unsigned char* base = smem_raw + (sizeof(ObsRec<M>) + sizeof(CertRec<M>) + 2 * sizeof(double)) * nob;
+    double* s_P = reinterpret_cast<double*>(base) + (size_t)warp * 32 * NP;
+    base += (size_t)kHeurWarps * 32 * NP * sizeof(double);
+    uint16_t* s_it = reinterpret_cast<uint16_t*>(base) + warp * 32 * kHeurRound;
+    base += (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t);
+    int* s_kill = reinterpret_cast<int*>(base) + warp * 32;
+  #pragma unroll
+    for (int k = 0; k < M; ++k)
+  #pragma unroll
+      for (int j = 0; j < 2 * G; ++j) s_P[lane * NP + k * 2 * G + j] = P[k][j];
     // pass 1 (coherent across the warp): certify code 1 from the control-polygon bounding box
     unsigned long long hard = 0;
     if (valid) {
@@ -520,17 +535,6 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
     // are dealt out to all 32 lanes, a round of at most kHeurRound pairs per edge at a time, so
     // lanes whose edge has few hard obstacles do not idle while others work through theirs.
     // Each lane's control points are staged in shared memory for the lanes that take its pairs.
-    constexpr int NP = M * 2 * G;
-    unsigned char* base = smem_raw + (sizeof(ObsRec<M>) + sizeof(CertRec<M>) + 2 * sizeof(double)) * nob;
-    double* s_P = reinterpret_cast<double*>(base) + (size_t)warp * 32 * NP;
-    base += (size_t)kHeurWarps * 32 * NP * sizeof(double);
-    uint16_t* s_it = reinterpret_cast<uint16_t*>(base) + warp * 32 * kHeurRound;
-    base += (size_t)kHeurWarps * 32 * kHeurRound * sizeof(uint16_t);
-    int* s_kill = reinterpret_cast<int*>(base) + warp * 32;
-  #pragma unroll
-    for (int k = 0; k < M; ++k)
-  #pragma unroll
-      for (int j = 0; j < 2 * G; ++j) s_P[lane * NP + k * 2 * G + j] = P[k][j];
     s_kill[lane] = kill;
     const long long e0 = e - lane;
     __syncwarp();
