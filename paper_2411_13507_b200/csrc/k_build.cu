@@ -808,12 +808,15 @@ __global__ void k_points(DParams dp, const double* __restrict__ Vx, long long E,
     for (int j = 0; j < 2 * G; ++j) out[e * M * 2 * G + k * 2 * G + j] = P[k][j];
 }
 
+// cap: the CSR arrays' capacity (a captured plan's; offsets past it are clipped so the search
+// never reads beyond the arrays of a build whose edges overflowed -- the plan reruns it)
 __global__ void k_row_ptr_global(const long long* __restrict__ local, long long V, long long r0, long long r1,
-                                 long long* __restrict__ out) {
+                                 long long* __restrict__ out, long long cap) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i > V) return;
   const long long E = local[r1 - r0];
-  out[i] = i <= r0 ? 0 : (i >= r1 ? E : local[i - r0]);
+  const long long v = i <= r0 ? 0 : (i >= r1 ? E : local[i - r0]);
+  out[i] = v < cap ? v : cap;
 }
 
 // row_ptr[i] = lower_bound(src, i) over a source-sorted edge list (gathered row blocks)
@@ -1447,7 +1450,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
              g->dst.as<int>(), g->cost.as<double>(), (long long)g->E);
     });
     launch(c, "k_row_ptr_global", k_row_ptr_global, dim3(div_up(V + 1, 256)), dim3(256), 0, rptr.as<long long>(),
-           V, r0, r1, g->row_ptr.as<long long>());
+           V, r0, r1, g->row_ptr.as<long long>(), (long long)g->E);
     return true;
   }
   long long* h = static_cast<long long*>(c->host_scratch(2 * sizeof(long long)));
@@ -1488,7 +1491,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     });
   }
   launch(c, "k_row_ptr_global", k_row_ptr_global, dim3(div_up(V + 1, 256)), dim3(256), 0, rptr.as<long long>(),
-         V, r0, r1, g->row_ptr.as<long long>());
+         V, r0, r1, g->row_ptr.as<long long>(), E);
   return true;
 }
 

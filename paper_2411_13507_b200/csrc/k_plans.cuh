@@ -535,7 +535,12 @@ void planner_run(Planner* p, const uint64_t* pcg, const double* include, int n_o
           g->dE = nullptr;
           c->sample_check = nullptr;
           c->sample_est = p->sample_est;
-          sample_states(c, &d, g->vertices.as<double>(), /*single_round=*/true);
+          if (p->R > 0) {  // the checked multi-round region sampler, straight into the vertices
+            sample_regions(c, n, p->R, p->rN.data(), pcg, p->rlo.data(), p->rhi.data(), p->rrow_off.data(),
+                           p->rA.data(), p->rb.data(), d.eps_geo, g->vertices.as<double>(), p->rest.data());
+          } else {
+            sample_states(c, &d, g->vertices.as<double>(), /*single_round=*/true);
+          }
           if (d.n_include > 0)
             BZG_CHECK_CUDA(cudaMemcpyAsync(g->vertices.as<double>() + (size_t)d.N * n, include,
                                            (size_t)d.n_include * n * sizeof(double), cudaMemcpyHostToDevice,
@@ -546,7 +551,12 @@ void planner_run(Planner* p, const uint64_t* pcg, const double* include, int n_o
           }
           // the captured round draws ~1.3x the candidates the measured acceptance needs, so other
           // seeds' rounds (acceptance varies by a few percent) rarely fall short
-          p->sample_est = std::min(p->sample_est, 0.85 * c->sample_est);
+          if (p->R == 0) {
+            p->sample_est = std::min(p->sample_est, 0.85 * c->sample_est);
+            // BZG_PLAN_STRESS=1 (tests): capture with a sampler round and an edge capacity far
+            // too small, so every call takes the checked eager path
+            if (std::getenv("BZG_PLAN_STRESS")) p->sample_est = 4.0 * c->sample_est;
+          }
           p->E = g->E;
           cut_graph_impl(c, g, n_obs, row_off, A, b, is_box, box_lo, box_hi, &p->cfg, &p->mk, CutBits{});
           path_stage_enqueue(c, g, &p->mk, p->ps);
@@ -558,12 +568,16 @@ void planner_run(Planner* p, const uint64_t* pcg, const double* include, int n_o
     // few percent), at most every ordered pair; the capacity sizes the cut's and search's grids
     const long long V = g->V;
     p->Ecap = std::max(p->Ecap, std::min(V * (V - 1), p->E + p->E / 2 + 4096));
+    if (std::getenv("BZG_PLAN_STRESS")) p->Ecap = std::max(1ll, p->E / 4);  // (tests: overflow)
     if (p->R > 0) {  // the captured region round, sized from this call's acceptance rates
       planner_drop_graph(p);
       region_sample_plan_destroy(p->rs);
       p->rs = nullptr;
+      std::vector<double> est = p->rest;
+      if (std::getenv("BZG_PLAN_STRESS"))  // (tests: a region round far too small)
+        for (double& e : est) e *= 4.0;
       p->rs = region_sample_plan_create(c, n, p->R, p->rN.data(), p->rlo.data(), p->rhi.data(), p->rrow_off.data(),
-                                        p->rA.data(), p->rb.data(), p->d.eps_geo, p->rest.data());
+                                        p->rA.data(), p->rb.data(), p->d.eps_geo, est.data());
     }
     planner_capture<Gc, Mc>(p, prep);
   });

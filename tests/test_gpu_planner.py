@@ -149,3 +149,33 @@ def test_planner_edge_cases(ctx, golden):
     with pytest.raises(ValueError, match="includes"):
         Planner(N, spec, orc, bounds, obstacles, seed=seed, include=include)(seed, obstacles, start, goal)
     assert pl.info()["eager_calls"] == 0
+
+
+@pytest.mark.parametrize("cfg", ["cfg1-demo", "cfg1"])
+def test_planner_fallbacks_equal_eager(ctx, cfg, monkeypatch):
+    """BZG_PLAN_STRESS=1 captures with a sampler round and an edge capacity far too small: every
+    call's check fails (sampler short / edge capacity), runs the checked eager path on the
+    plan's own objects and re-captures -- with the eager API's results."""
+    import bench
+    from paper_2411_13507_b200 import regions as RG
+
+    monkeypatch.setenv("BZG_PLAN_STRESS", "1")
+    w = bench.workload(cfg)
+    kw = {}
+    if w.extra.get("regions"):
+        kw = dict(regions=w.extra["regions"], per_region=w.extra["per_region"])
+    obstacles = list(w.obstacles)
+    pl = Planner(w.N, w.spec, w.oracle, w.sample_bounds, obstacles, seed=w.seed, include=w.include, **kw)
+    for k in range(3):
+        seed = w.seed + k
+        path = pl(seed, obstacles, w.start, w.goal, include=w.include)
+        assert pl.last_eager
+        if kw:
+            g0 = RG.build_region_graph(kw["per_region"], w.spec, w.oracle, kw["regions"], w.sample_bounds, seed,
+                                       include=w.include, ctx=ctx)
+        else:
+            g0 = G.build_graph(w.N, w.spec, w.oracle, w.sample_bounds, seed, w.include, ctx=ctx)
+        m0 = G.cut_graph(g0, obstacles)
+        _check(pl, (g0, m0, G.find_path(g0, m0, w.start, w.goal), g0._cache.get("last_dist")), path)
+    info = pl.info()
+    assert info["eager_calls"] == 3 and info["last_eager_reason"] in ("sampler round short", "edge capacity"), info
