@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/bzg.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace bzg {
 
@@ -37,6 +38,15 @@ struct Error : std::runtime_error {
   } while (0)
 
 struct Ctx;
+
+// NVTX range around a public entry point (header-only NVTX v3: a no-op unless a profiler such as
+// ncu --nvtx or nsys attaches), so captures can be filtered by call.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Set while a stream capture (bzg_query) records work: a workspace that would have to grow
 // then is an error (the graph would bake in a fresh allocation), so captures are preceded by

@@ -164,6 +164,7 @@ int bzg_ctx_reset_stats(bzg_ctx* ctx) {
 int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
   bzg_graph* g = nullptr;
   int rc = guarded([&] {
+    NvtxRange nvtx_range("bzg_build_graph");
     BZG_REQUIRE(ctx && d && out, BZG_EINVAL, "null argument");
     set_device(ctx);
     BZG_REQUIRE(d->m >= 1 && d->gamma >= 1, BZG_EINVAL, "require m >= 1 and gamma >= 1");
@@ -216,6 +217,7 @@ int bzg_build_graph(bzg_ctx* ctx, const bzg_build_desc* d, bzg_graph** out) {
 
 int bzg_graph_eps_band(bzg_graph* g, const bzg_build_desc* d, double eps, int64_t counts[3]) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_graph_eps_band");
     BZG_REQUIRE(g && d && counts && d->F && d->G, BZG_EINVAL, "null argument");
     BZG_REQUIRE(eps >= 0.0, BZG_EINVAL, "eps must be non-negative");
     BZG_REQUIRE(d->m == g->m && d->gamma == g->gamma && d->N + d->n_include == g->V, BZG_EINVAL,
@@ -252,6 +254,7 @@ int bzg_sample_region_states(bzg_ctx* ctx, int32_t n, int32_t n_regions, const i
                              const double* lo, const double* hi, const int32_t* row_off, const double* A,
                              const double* b, double eps_geo, double* out_host) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_sample_region_states");
     BZG_REQUIRE(ctx && N && pcg && lo && hi && row_off && A && b && out_host, BZG_EINVAL, "null argument");
     BZG_REQUIRE(n_regions >= 1, BZG_EINVAL, "need at least one region");
     long long total = 0;
@@ -370,6 +373,7 @@ int bzg_graph_copy_vertices(bzg_graph* g, double* vertices) {
 
 int bzg_graph_copy_edges(bzg_graph* g, int64_t* edges, double* costs) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_graph_copy_edges");
     BZG_REQUIRE(g, BZG_EINVAL, "null graph");
     set_device(g->ctx);
     const long long E = g->E;
@@ -391,6 +395,7 @@ int bzg_graph_copy_edges(bzg_graph* g, int64_t* edges, double* costs) {
 
 int bzg_graph_copy_points(bzg_graph* g, double* points) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_graph_copy_points");
     BZG_REQUIRE(g, BZG_EINVAL, "null graph");
     set_device(g->ctx);
     materialize_points(g->ctx, g);
@@ -431,6 +436,7 @@ int bzg_graph_export_device(bzg_graph* g, int32_t* src, int32_t* dst, double* co
 int bzg_check_edges(bzg_ctx* ctx, int32_t n, int32_t n_F, const double* F, const double* G, double eps, int64_t k,
                     const double* X1, const double* X2, uint8_t* out) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_check_edges");
     BZG_REQUIRE(ctx && F && G && (k == 0 || (X1 && X2 && out)), BZG_EINVAL, "null argument");
     set_device(ctx);
     check_edges(ctx, n, n_F, F, G, eps, k, X1, X2, out);
@@ -442,6 +448,7 @@ int bzg_cut_graph(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_t* row_
                   bzg_mask** out) {
   bzg_mask* mk = nullptr;
   int rc = guarded([&] {
+    NvtxRange nvtx_range("bzg_cut_graph");
     BZG_REQUIRE(ctx && g && cfg && out, BZG_EINVAL, "null argument");
     BZG_REQUIRE(n_obs == 0 || (row_off && A && b && is_box && box_lo && box_hi), BZG_EINVAL, "obstacle arrays missing");
     set_device(ctx);
@@ -457,6 +464,7 @@ int bzg_cut_points(bzg_ctx* ctx, int32_t m, int32_t J, int64_t B, const double* 
                    const double* box_lo, const double* box_hi, const bzg_cut_config* cfg, int32_t mode, int8_t* code,
                    double* delta, int8_t* status) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_cut_points");
     BZG_REQUIRE(ctx && cfg && code && (B == 0 || (points && obs_index)), BZG_EINVAL, "null argument");
     BZG_REQUIRE(row_off && A && b && is_box && box_lo && box_hi, BZG_EINVAL, "obstacle arrays missing");
     BZG_REQUIRE(m >= 1 && m <= 3, BZG_EUNSUPPORTED, "device cut supports m in 1..3");
@@ -476,6 +484,7 @@ int bzg_mask_destroy(bzg_mask* mk) {
 
 int bzg_mask_copy(bzg_mask* mk, uint8_t* alive, uint8_t* provenance, int64_t counters[6]) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_mask_copy");
     BZG_REQUIRE(mk && mk->g, BZG_EINVAL, "null mask");
     BZG_REQUIRE((!alive && !provenance) || mk->E == mk->g->E, BZG_EINVAL,
                 "stale mask: its graph's edge set changed after the cut");
@@ -566,6 +575,7 @@ int bzg_project_on_path(bzg_ctx* ctx, int32_t m, int32_t gamma, double T, const 
                         const double* path_states, double h, int32_t steps_per_hop, const double* state,
                         double* best_t) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_project_on_path");
     BZG_REQUIRE(ctx && D && state && best_t && (L == 0 || path_states), BZG_EINVAL, "null argument");
     set_device(ctx);
     *best_t = project_on_path(ctx, m, gamma, T, D, L, path_states, h, steps_per_hop, state);
@@ -576,6 +586,7 @@ int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start,
                   const double* tube_lo, const double* tube_hi, double eps_geo, int position_only_snap,
                   int require_tube_snap, int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_find_path");
     BZG_REQUIRE(ctx && g && start && goal && tube_lo && tube_hi && path_len, BZG_EINVAL, "null argument");
     BZG_REQUIRE(!mk || mk->g == g, BZG_EINVAL, "mask belongs to another graph");
     BZG_REQUIRE(!mk || mk->E == g->E, BZG_EINVAL, "stale mask: its graph's edge set changed after the cut");
@@ -597,6 +608,7 @@ int bzg_find_path(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* start,
 int bzg_query_create(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* tube_lo, const double* tube_hi,
                      double eps_geo, int position_only_snap, int require_tube_snap, bzg_query** out) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_query_create");
     BZG_REQUIRE(ctx && g && tube_lo && tube_hi && out, BZG_EINVAL, "null argument");
     BZG_REQUIRE(!mk || mk->g == g, BZG_EINVAL, "mask belongs to another graph");
     BZG_REQUIRE(!mk || mk->E == g->E, BZG_EINVAL, "stale mask: its graph's edge set changed after the cut");
@@ -609,6 +621,7 @@ int bzg_query_create(bzg_ctx* ctx, bzg_graph* g, bzg_mask* mk, const double* tub
 int bzg_query_run(bzg_query* q, const double* start, const double* goal, int64_t* path_out, int64_t path_cap,
                   int64_t* path_len, double* dist_out) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_query_run");
     BZG_REQUIRE(q && start && goal && path_len, BZG_EINVAL, "null argument");
     set_device(query_ctx(as_query(q)));
     std::vector<int64_t> path;
@@ -645,6 +658,7 @@ int bzg_replanner_create(bzg_ctx* ctx, bzg_graph* g, int32_t n_obs, const int32_
                          const uint8_t* dynamic, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi, double eps_geo,
                          int position_only_snap, int require_tube_snap, bzg_replanner** out) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_replanner_create");
     BZG_REQUIRE(ctx && g && cfg && tube_lo && tube_hi && out, BZG_EINVAL, "null argument");
     BZG_REQUIRE(row_off && A && b && is_box && box_lo && box_hi, BZG_EINVAL, "obstacle arrays missing");
     set_device(ctx);
@@ -659,6 +673,7 @@ int bzg_replanner_run(bzg_replanner* rp, int32_t n_obs, const int32_t* row_off, 
                       const double* goal, int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out,
                       int64_t counters[6], int32_t* eager) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_replanner_run");
     BZG_REQUIRE(rp && start && goal && path_len, BZG_EINVAL, "null argument");
     BZG_REQUIRE(row_off && A && b && is_box && box_lo && box_hi, BZG_EINVAL, "obstacle arrays missing");
     Replanner* r = as_rp(rp);
@@ -729,6 +744,7 @@ int bzg_planner_create(bzg_ctx* ctx, const bzg_build_desc* desc, const bzg_regio
                        const double* box_hi, const bzg_cut_config* cfg, const double* tube_lo, const double* tube_hi,
                        double eps_geo, int position_only_snap, int require_tube_snap, bzg_planner** out) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_planner_create");
     BZG_REQUIRE(ctx && desc && cfg && tube_lo && tube_hi && out, BZG_EINVAL, "null argument");
     BZG_REQUIRE(n_obs == 0 || (row_off && A && b && is_box && box_lo && box_hi), BZG_EINVAL, "obstacle arrays missing");
     BZG_REQUIRE(desc->n_include == 0 || desc->include, BZG_EINVAL, "include rows missing");
@@ -745,6 +761,7 @@ int bzg_planner_run(bzg_planner* pl, const uint64_t* pcg, const double* include,
                     int64_t* path_out, int64_t path_cap, int64_t* path_len, double* dist_out, int64_t counters[6],
                     int64_t* num_edges, int32_t* eager) {
   return guarded([&] {
+    NvtxRange nvtx_range("bzg_planner_run");
     BZG_REQUIRE(pl && pcg && start && goal && path_len, BZG_EINVAL, "null argument");
     BZG_REQUIRE(n_obs == 0 || (row_off && A && b && is_box && box_lo && box_hi), BZG_EINVAL, "obstacle arrays missing");
     Planner* p = as_pl(pl);
