@@ -270,17 +270,17 @@ int bzg_replanner_destroy(bzg_replanner* rp);
 
 /* ---- the whole stage as one captured CUDA graph ---------------------------- */
 /* build_graph -> cut_graph -> find_path (graph.py:129-430, the order of sim.plan_once) for one
- * scene shape: desc fixes the oracle, N, curve, sampling bounds and include count (no keep-in
- * regions take a bzg_region_sampler; no row block); the obstacle list keeps its count.  bzg_planner_create runs the first
- * call (desc's seed and include rows, the given obstacles) eagerly and captures the stage; each
- * bzg_planner_run(pcg = the seed's PCG64 words as in bzg_build_desc -- 4 per region with keep-in
- * regions -- include rows, obstacles,
- * start, goal) is then one graph launch and one synchronisation, with the results of
- * bzg_build_graph + bzg_cut_graph + bzg_find_path on the same inputs.  The build's edge count
- * stays on the device; the CSR arrays have a capacity (1.5 x the last edge count, at most every
- * ordered pair); a call whose sampler round fell short, whose edges outgrew the
- * capacity, whose work lists overflowed or whose obstacle list changed shape runs eagerly
- * (*eager = 1) and re-captures.  counters as bzg_mask_copy; *num_edges = the graph's E. */
+ * scene shape: desc fixes the oracle, N, curve, sampling bounds and include count (keep-in
+ * regions take a bzg_region_sampler; no row block); the obstacle list keeps its count.
+ * bzg_planner_create runs the first call (desc's seed and include rows, the given obstacles)
+ * eagerly and captures the stage; each bzg_planner_run (pcg = the seed's PCG64 words as in
+ * bzg_build_desc, 4 per region with keep-in regions; include rows; obstacles; start; goal) is
+ * then one graph launch and one synchronisation, with the results of bzg_build_graph +
+ * bzg_cut_graph + bzg_find_path on the same inputs.  The build's edge count stays on the
+ * device; the CSR arrays have a capacity (1.5 x the last edge count, at most every ordered
+ * pair); a call whose sampler round fell short, whose edges outgrew the capacity, whose work
+ * lists overflowed or whose obstacle list changed shape runs eagerly (*eager = 1) and
+ * re-captures.  counters as bzg_mask_copy; *num_edges = the graph's E. */
 /* keep-in regions (desc->n_regions > 0): the per-region sampler of bzg_sample_region_states --
  * N[r] states of region r from its own PCG64 stream (pcg: 4 words per region, this call's
  * seed), box lo/hi (n_regions x n), state-set rows [row_off[r], row_off[r+1]) of A / b; the N[r]
