@@ -9,8 +9,11 @@ start/goal, 50 boxes), i.e. 4.0e8 ordered pairs.
 
 metric: edge evaluations/s = V^2 / t_step (whole job, all GPUs); ms_per_step is the
 build+cut+solve latency.  ``value`` is timed with CUDA events on the library's stream
-with L2 flushed before every step; ``e2e`` times the public Python API
-(build_graph -> cut_graph -> find_path) with host inputs and the path read back.
+with L2 flushed before every step; ``e2e`` times the same call with host inputs and the
+path read back.  On one GPU the step is the captured Planner (build -> cut -> find_path
+as one CUDA graph, paths checked equal to the eager API's); the eager public API
+(build_graph -> cut_graph -> find_path, one synchronisation per call) is reported
+under "eager" and headlines with --no-planner and on several GPUs.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (row-block sharding, NCCL gather)
