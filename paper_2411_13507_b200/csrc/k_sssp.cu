@@ -143,6 +143,57 @@ __global__ void k_snap_final(unsigned long long* __restrict__ best, int nblocks,
 // Reverse reachability to vg (graph.py:433-450, _reaches_goal) in one cooperative launch: vg
 // from the device plan; sweeps over the alive edges mark src when dst is marked, a grid barrier
 // per sweep, until a sweep marks nothing.  Cached per (mask, vg) through `key` on the device.
+// Small graphs (V <= kSnapBlockV): a snap as ONE block per parameter set -- the strided scan
+// keeps each thread's first minimum, the block reduction the lowest index among equal values,
+// i.e. k_snap + k_snap_final's first argmin -- so the goal and (tube) start snaps are one
+// launch instead of six.  Block b handles parameter set first + b and writes out[b].
+constexpr long long kSnapBlockV = 16384;
+__global__ void __launch_bounds__(1024) k_snap_block(SnapParams s0, SnapParams s1, const SnapParams* __restrict__ spd,
+                                                     int first, const double* __restrict__ Vx, long long V,
+                                                     const uint8_t* __restrict__ reach, long long* __restrict__ out) {
+  const int set = first + blockIdx.x;
+  const SnapParams& sp = spd ? spd[set] : (set == 0 ? s0 : s1);
+  double val = INFINITY;
+  long long idx = -1;
+  for (long long i = threadIdx.x; i < V; i += blockDim.x) {
+    const double* v = Vx + i * sp.n;
+    bool ok = true;
+    if (sp.mode == 1) {
+      for (int k = 0; k < sp.n; ++k) {
+        const double d = __dsub_rn(v[k], sp.target[k]);
+        ok = ok && d >= sp.tlo[k] && d <= sp.thi[k];
+      }
+    } else if (sp.mode == 2) {
+      ok = reach[i] != 0;
+    }
+    if (ok) {
+      const double nv = snap_norm(v, sp);
+      if (idx < 0 || nv < val) { val = nv; idx = i; }  // ascending i: keep the first minimum
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, val, off);
+    const long long oi = __shfl_down_sync(0xffffffffu, idx, off);
+    if (oi >= 0 && (idx < 0 || ov < val || (ov == val && oi < idx))) { val = ov; idx = oi; }
+  }
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sv[w] = val; si[w] = idx; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x / 32;
+    val = lane < nw ? sv[lane] : INFINITY;
+    idx = lane < nw ? si[lane] : -1;
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, val, off);
+      const long long oi = __shfl_down_sync(0xffffffffu, idx, off);
+      if (oi >= 0 && (idx < 0 || ov < val || (ov == val && oi < idx))) { val = ov; idx = oi; }
+    }
+    if (lane == 0) out[blockIdx.x] = idx;
+  }
+}
+
 // GRID: one cooperative grid and grid barriers; else ONE thread-block cluster (the launch's
 // whole grid) and cluster barriers -- far cheaper per sweep for small graphs (k_bf_cluster).
 template <bool GRID>
@@ -795,10 +846,16 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
     BZG_CHECK_CUDA(cudaMemcpyAsync(d_sp.ptr, h_sp, 2 * sizeof(SnapParams), cudaMemcpyHostToDevice, c->stream));
     spd = d_sp.as<SnapParams>();
   }
-  snap_launch(c, g, sp[0], spd, nullptr, c->ws[WS_BEST0], plan + 0);
+  const bool small = V <= kSnapBlockV && !std::getenv("BZG_SNAP_GRID");  // (tests compare both)
+  if (small) {  // goal and, for tube snapping, the start in one launch of one block each
+    launch(c, "k_snap_block", k_snap_block, dim3(sp[1].mode == 1 ? 2 : 1), dim3(1024), 0, sp[0], sp[1], spd, 0,
+           g->vertices.as<double>(), V, (const uint8_t*)nullptr, plan);
+  } else {
+    snap_launch(c, g, sp[0], spd, nullptr, c->ws[WS_BEST0], plan + 0);
+  }
 
   if (sp[1].mode == 1) {
-    snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, nullptr, c->ws[WS_BEST1], plan + 1);
+    if (!small) snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, nullptr, c->ws[WS_BEST1], plan + 1);
   } else {
     // relaxed mid-run snap: nearest vertex that can still reach vg (graph.py:388-392); the
     // reverse reachability runs on the device (k_reach_coop), cached per (mask, vg) there
@@ -870,7 +927,11 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
       void* args[] = {&El, &Vl2, &rs, &rd, &alive, &reach, &rkey, &cpl, &rf, &dEp};
       launch_coop(c, "k_reach_coop", (const void*)k_reach_sweeps<true>, dim3(rblocks), dim3(256), args);
     }
-    snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, reach, c->ws[WS_BEST1], plan + 1);
+    if (small)
+      launch(c, "k_snap_block", k_snap_block, dim3(1), dim3(1024), 0, sp[0], sp[1], spd, 1, g->vertices.as<double>(), V,
+             (const uint8_t*)reach, plan + 1);
+    else
+      snap_launch(c, g, sp[1], spd ? spd + 1 : nullptr, reach, c->ws[WS_BEST1], plan + 1);
   }
 
   // ---- the shortest-path tree from v0 (skipped on the device when cached or trivial)

@@ -478,3 +478,34 @@ def test_reverse_reachability_schedules(ctx, golden, name, monkeypatch):
                      for s, t in cases]
     assert out["grid"] == out["cluster"]
     assert sum(p is not None for p in out["grid"]) >= 2
+
+
+@pytest.mark.parametrize("name", ["demo200", "hop1500", "m3g3_1500", "cfg2_rf2000"])
+def test_snap_block_equals_grid_snap(ctx, golden, name, monkeypatch):
+    """The one-block snap of small graphs (k_snap_block) picks the same vertices as the grid
+    snap (k_snap + k_snap_final): goal and tube / relaxed start, targets at vertices, between
+    two vertices (exact ties) and far away."""
+    g = golden(name)
+    gr, obstacles, start, goal = _build(g, ctx)
+
+    class RefMask:
+        alive = g["alive"]
+
+    V = gr.vertices
+    rng = np.random.default_rng(23)
+    cases = [(start, goal)]
+    for _ in range(10):
+        a, b = V[rng.integers(0, len(V))], V[rng.integers(0, len(V))]
+        cases += [(a, b), ((a + b) / 2, b), (a, (a + b) / 2), (a + 50.0, b)]
+    out = {}
+    for impl in ("grid", "block"):
+        if impl == "grid":
+            monkeypatch.setenv("BZG_SNAP_GRID", "1")
+        else:
+            monkeypatch.delenv("BZG_SNAP_GRID", raising=False)
+        res = []
+        for s, t in cases:
+            res.append(G.find_path(gr, RefMask(), s, t))
+            res.append(G.find_path(gr, RefMask(), s, t, position_only_snap=True, require_tube_snap=False))
+        out[impl] = res
+    assert out["grid"] == out["block"]

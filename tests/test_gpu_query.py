@@ -54,7 +54,7 @@ def test_query_equals_find_path(ctx, golden, name, mode):
     m = None if mode == "no_mask" else mask
     kw = dict(position_only_snap=True, require_tube_snap=False) if mode == "relaxed" else {}
     q = G.PathQuery(gr, m, **kw)
-    assert q.kernels_per_query >= 8
+    assert q.kernels_per_query >= 6
     n_paths = 0
     for s, t in _queries(gr, start, goal, rng):
         want = G.find_path(gr, m, s, t, **kw)
