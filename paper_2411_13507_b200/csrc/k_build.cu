@@ -185,20 +185,27 @@ __global__ void k_morton(const double* __restrict__ Vx, long long V, int n, int 
 }
 
 // projections at sorted position s (vertex perm[s]); src_ok also requires the row block
-__global__ void k_project_sorted(RowPlan rp, const double* __restrict__ F, const double* __restrict__ Vx,
+// The oracle rows F (n_F x 2n, at most 96 x 12 doubles) are staged in shared memory first: read
+// from global memory inside the per-row loops, every row was a dependent L2 round trip (~36 per
+// vertex at gamma = 2), which made this kernel latency-bound at every size (18 us for 202
+// vertices).  Same arithmetic (fma_chain over the same values).
+__global__ void k_project_sorted(RowPlan rp, const double* __restrict__ F, int nF, const double* __restrict__ Vx,
                                  const int* __restrict__ perm, long long V, int Kpad, long long r0, long long r1,
                                  double* __restrict__ a1c, double* __restrict__ a2t, uint8_t* __restrict__ src_ok,
                                  uint8_t* __restrict__ dst_ok) {
+  extern __shared__ double sF[];
+  const int n = rp.n;
+  for (int t = threadIdx.x; t < nF * 2 * n; t += blockDim.x) sF[t] = F[t];
+  __syncthreads();
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= V) return;
   const long long i = perm[s];
-  const int n = rp.n;
   double v[kMaxN];
   for (int k = 0; k < n; ++k) v[k] = Vx[i * n + k];
   for (int q = 0; q < Kpad; ++q) {
     double x1 = 0.0, x2 = 0.0;
     if (q < rp.K) {
-      const double* f = F + (size_t)rp.row_iv[q] * 2 * n;
+      const double* f = sF + (size_t)rp.row_iv[q] * 2 * n;
       x1 = fma_chain(v, f, n);
       x2 = fma_chain(v, f + n, n);
     }
@@ -206,10 +213,10 @@ __global__ void k_project_sorted(RowPlan rp, const double* __restrict__ F, const
     a2t[(long long)q * V + s] = x2;
   }
   int ok = i >= r0 && i < r1;
-  for (int q = 0; q < rp.n_src; ++q) ok &= fma_chain(v, F + (size_t)rp.row_src[q] * 2 * n, n) <= rp.th_src[q];
+  for (int q = 0; q < rp.n_src; ++q) ok &= fma_chain(v, sF + (size_t)rp.row_src[q] * 2 * n, n) <= rp.th_src[q];
   src_ok[s] = (uint8_t)ok;
   ok = 1;
-  for (int q = 0; q < rp.n_dst; ++q) ok &= fma_chain(v, F + (size_t)rp.row_dst[q] * 2 * n + n, n) <= rp.th_dst[q];
+  for (int q = 0; q < rp.n_dst; ++q) ok &= fma_chain(v, sF + (size_t)rp.row_dst[q] * 2 * n + n, n) <= rp.th_dst[q];
   dst_ok[s] = (uint8_t)ok;
 }
 
@@ -244,12 +251,17 @@ __global__ void k_group_bounds(const double* __restrict__ a, int transposed, lon
   const long long g = t / Kpad;
   const int q = (int)(t - g * Kpad);
   double mn = INFINITY, mx = -INFINITY;
+  // loads issued unconditionally (independent, pipelined by the unroll); excluded rows select
+  // the identities of fmin / fmax, so the bounds are exactly the conditional loop's
+#pragma unroll 8
   for (int l = 0; l < kTile; ++l) {
     const long long s = g * kTile + l;
-    if (s >= V || !ok[s]) continue;
-    const double v = transposed ? a[(long long)q * V + s] : a[s * Kpad + q];
-    mn = fmin(mn, v);
-    mx = fmax(mx, v);
+    const bool in = s < V;
+    const long long sc = in ? s : 0;
+    const bool use = in && ok[sc];
+    const double v = transposed ? a[(long long)q * V + sc] : a[sc * Kpad + q];
+    mn = fmin(mn, use ? v : INFINITY);
+    mx = fmax(mx, use ? v : -INFINITY);
   }
   gmin[t] = mn;
   gmax[t] = mx;
@@ -1273,7 +1285,9 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     BZG_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(c->ws[WS_SCRATCH].ptr, bytes, key.as<unsigned>(), key2.as<unsigned>(),
                                                    idx.as<int>(), perm.as<int>(), V, 0, 32, c->stream));
   }
-  launch(c, "k_project_sorted", k_project_sorted, dim3(div_up(V, 128)), dim3(128), 0, rp, dF.as<double>(),
+  ensure_dyn_smem((const void*)k_project_sorted, (size_t)nF * 2 * n * sizeof(double));
+  launch(c, "k_project_sorted", k_project_sorted, dim3(div_up(V, 128)), dim3(128), (size_t)nF * 2 * n * sizeof(double),
+         rp, dF.as<double>(), nF,
          g->vertices.as<double>(), perm.as<int>(), V, Kpad, r0, r1, a1c.as<double>(), a2t.as<double>(),
          sok.as<uint8_t>(), dok.as<uint8_t>());
   const long long ng = (V + kTile - 1) / kTile;
