@@ -1172,24 +1172,52 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
   });
 }
 
-// first obstacle (list position) whose bit row holds edge e, for the three rows of each slot
+// alive / provenance of 32 edges (one bit word) from the obstacles' outcome rows in list order:
+// the first event of an edge -- a heuristic kill or a QP-unsafe verdict, never both for one
+// obstacle -- decides its provenance (as k_mask_finalize's kh < kq, graph.py:316-340), any
+// QP-safe verdict marks a surviving edge QP_SAFE.  One thread per word, so every row word is
+// read once for 32 edges (a thread per edge re-read it 32 times in a 3 x n_obs dependent loop).
 __global__ void k_cut_combine(long long E, int n_obs, const uint32_t* __restrict__ pool, long long Wb,
                               const int* __restrict__ slots, uint8_t* __restrict__ alive, uint8_t* __restrict__ prov) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  const long long w = e >> 5;
-  const uint32_t bit = 1u << (e & 31);
-  int kh = n_obs, kq = n_obs;
-  bool saved = false;
+  const long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (w >= Wb) return;
+  uint32_t hk = 0, qk = 0, first_h = 0, saved = 0;
   for (int o = 0; o < n_obs; ++o) {
-    const uint32_t* base = pool + (size_t)slots[o] * 3 * Wb;
-    if (kh == n_obs && (base[w] & bit)) kh = o;
-    saved |= (base[Wb + w] & bit) != 0;
-    if (kq == n_obs && (base[2 * Wb + w] & bit)) kq = o;
+    const uint32_t* base = pool + (size_t)__ldg(slots + o) * 3 * Wb;
+    const uint32_t kill = base[w], qsafe = base[Wb + w], qun = base[2 * Wb + w];
+    first_h |= kill & ~(hk | qk);
+    hk |= kill;
+    qk |= qun;
+    saved |= qsafe;
   }
-  const bool dead = kh < n_obs || kq < n_obs;  // as k_mask_finalize (graph.py:316-340)
-  alive[e] = dead ? 0 : 1;
-  prov[e] = dead ? (kh < kq ? BZG_HEURISTIC_UNSAFE : BZG_QP_UNSAFE) : (saved ? BZG_QP_SAFE : BZG_HEURISTIC_SAFE);
+  const uint32_t dead = hk | qk;
+  const long long e0 = w * 32;
+  const int nb = (int)min(32ll, E - e0);
+  auto alive_of = [&](int k) -> uint32_t { return ((dead >> k) & 1u) ? 0u : 1u; };
+  auto prov_of = [&](int k) -> uint32_t {
+    const uint32_t bit = 1u << k;
+    return (dead & bit) ? ((first_h & bit) ? BZG_HEURISTIC_UNSAFE : BZG_QP_UNSAFE)
+                        : ((saved & bit) ? BZG_QP_SAFE : BZG_HEURISTIC_SAFE);
+  };
+  if (nb == 32) {  // 32 bytes each, as two 16-byte stores (the arrays are 256-byte aligned)
+    uint32_t a[8], p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      a[j] = alive_of(4 * j) | alive_of(4 * j + 1) << 8 | alive_of(4 * j + 2) << 16 | alive_of(4 * j + 3) << 24;
+      p[j] = prov_of(4 * j) | prov_of(4 * j + 1) << 8 | prov_of(4 * j + 2) << 16 | prov_of(4 * j + 3) << 24;
+    }
+    uint4* ap = reinterpret_cast<uint4*>(alive + e0);
+    uint4* pp = reinterpret_cast<uint4*>(prov + e0);
+    ap[0] = make_uint4(a[0], a[1], a[2], a[3]);
+    ap[1] = make_uint4(a[4], a[5], a[6], a[7]);
+    pp[0] = make_uint4(p[0], p[1], p[2], p[3]);
+    pp[1] = make_uint4(p[4], p[5], p[6], p[7]);
+  } else {
+    for (int k = 0; k < nb; ++k) {
+      alive[e0 + k] = (uint8_t)alive_of(k);
+      prov[e0 + k] = (uint8_t)prov_of(k);
+    }
+  }
 }
 
 // popcounts of n_rows bit rows of Wb words into out[row]
@@ -1347,7 +1375,7 @@ bool cut_graph_cached(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const
   DevBuf& d_slots = c->ws[WS_CUTSLOTS];
   d_slots.alloc(n_obs * sizeof(int), c->stream);
   BZG_CHECK_CUDA(cudaMemcpyAsync(d_slots.ptr, slots.data(), n_obs * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-  launch(c, "k_cut_combine", k_cut_combine, dim3(div_up(E, 256)), dim3(256), 0, E, n_obs,
+  launch(c, "k_cut_combine", k_cut_combine, dim3(div_up(Wb, 256)), dim3(256), 0, E, n_obs,
          (const uint32_t*)cc.pool.as<uint32_t>(), Wb, (const int*)d_slots.as<int>(), mk->alive.as<uint8_t>(),
          mk->prov.as<uint8_t>());
   long long kill = 0, qs = 0, qu = 0;

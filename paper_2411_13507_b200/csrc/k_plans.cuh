@@ -104,7 +104,7 @@ void replanner_counters(Replanner* r, const unsigned long long* h) {
 
 void replanner_combine(Replanner* r) {
   Ctx* c = r->c;
-  launch(c, "k_cut_combine", k_cut_combine, dim3(div_up(r->E, 256)), dim3(256), 0, r->E, r->n_obs,
+  launch(c, "k_cut_combine", k_cut_combine, dim3(div_up(r->Wb, 256)), dim3(256), 0, r->E, r->n_obs,
          (const uint32_t*)r->pool.as<uint32_t>(), r->Wb, (const int*)r->slots.as<int>(), r->mk.alive.as<uint8_t>(),
          r->mk.prov.as<uint8_t>());
 }
