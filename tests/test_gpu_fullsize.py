@@ -122,6 +122,34 @@ def test_cfg3_path_matches_oracle_dijkstra(cfg3):
     assert G.path_cost(g, path) == float(ref_dist)
 
 
+def test_cfg3_relaxed_snap_pull_reach(cfg3, monkeypatch):
+    """Relaxed mid-run snapping at full size (graph.py:388-392, _reaches_goal 433-450): the
+    reverse reachability of a graph this large is pulled bottom-up over the forward CSR
+    (k_reach_pull); its snapped start must be the oracle's (reverse DFS on the device's
+    graph and mask) and its paths those of the edge-sweep schedule (BZG_REACH_IMPL=grid)."""
+    w, g, mask, _ = cfg3
+    V = g.vertices
+    rng = np.random.default_rng(29)
+    kw = dict(position_only_snap=True, require_tube_snap=False)
+    cases = [(w.start, w.goal)] + [(V[rng.integers(0, len(V))], V[rng.integers(0, len(V))]) for _ in range(5)]
+    tube = w.oracle.tube.error
+    for s, t in cases[:2]:
+        want = oracle.snap(V, g.edges, mask.alive, s, t, w.spec.m, tube.lo, tube.hi, **kw)
+        got = G.find_path(g, mask, s, t, **kw)
+        assert (got is None) == (want is None)
+        if got is not None:
+            assert (got[0], got[-1]) == want
+    pull = [G.find_path(g, mask, s, t, **kw) for s, t in cases]
+    monkeypatch.setenv("BZG_REACH_IMPL", "grid")
+
+    class Fresh:  # a new device mask: no reach set cached from the pull runs
+        alive = mask.alive
+
+    sweeps = [G.find_path(g, Fresh(), s, t, **kw) for s, t in cases]
+    assert pull == sweeps
+    assert sum(p is not None for p in pull) >= 3
+
+
 # ---------------------------------------------------------------- the live reference at full size
 def _golden_or_skip(name):
     from tests.conftest import GOLDEN, load_golden

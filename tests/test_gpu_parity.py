@@ -460,7 +460,8 @@ def test_edge_cases_round2(ctx, golden):
 @pytest.mark.parametrize("name", ["demo200", "maze", "cfg2_rf2000", "hop1500"])
 def test_reverse_reachability_schedules(ctx, golden, name, monkeypatch):
     """Relaxed mid-run snapping (graph.py:388-392, _reaches_goal 433-450): the reverse
-    reachability by cooperative grid sweeps and by one thread-block cluster give the same
+    reachability by cooperative grid sweeps, by one thread-block cluster and pulled bottom-up
+    over the forward CSR (k_reach_pull) give the same
     snapped starts and paths, for many starts and goals."""
     g = golden(name)
     gr, obstacles, start, goal = _build(g, ctx)
@@ -472,11 +473,11 @@ def test_reverse_reachability_schedules(ctx, golden, name, monkeypatch):
     V = gr.vertices
     cases = [(start, goal)] + [(V[rng.integers(0, len(V))], V[rng.integers(0, len(V))]) for _ in range(12)]
     out = {}
-    for impl in ("grid", "cluster"):
+    for impl in ("grid", "cluster", "pull"):
         monkeypatch.setenv("BZG_REACH_IMPL", impl)
         out[impl] = [G.find_path(gr, RefMask(), s, t, position_only_snap=True, require_tube_snap=False)
                      for s, t in cases]
-    assert out["grid"] == out["cluster"]
+    assert out["grid"] == out["cluster"] == out["pull"]
     assert sum(p is not None for p in out["grid"]) >= 2
 
 
