@@ -30,7 +30,7 @@ def main(cfg="cfg3", reps="5"):
         alive = np.ascontiguousarray(m.alive)
 
     paths = {}
-    for impl in ("cluster", "scan", "queue", "async"):
+    for impl in os.environ.get("IMPLS", "cluster scan queue async").split():
         os.environ["BZG_BF_IMPL"] = impl
         G.find_path(g, Alive(), w.start, w.goal)
         ctx.reset_stats()
