@@ -285,48 +285,54 @@ struct RegionRowsDev {
 
 // one thread per sorted vertex: regions whose (1e-6-grown) position box misses the vertex are
 // skipped (membership implies P_0 = x1 resp. P_p = x2 lies in the region), the rest are tested
-// row by row.  Masks pre-zeroed.
+// row by row.  The thread owns its mask words (written whole, no pre-zeroing) and folds them:
+// a vertex in no region can neither start nor end an edge (src_ok / dst_ok cleared).
 __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, const int* __restrict__ perm,
                                long long V, int m, const double* __restrict__ blo, const double* __restrict__ bhi,
-                               unsigned long long* __restrict__ smask, unsigned long long* __restrict__ dmask) {
+                               unsigned long long* __restrict__ smask, unsigned long long* __restrict__ dmask,
+                               uint8_t* __restrict__ src_ok, uint8_t* __restrict__ dst_ok) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= V) return;
   const long long i = perm[s];
   const int n = rr.n;
   double v[kMaxN];
   for (int k = 0; k < n; ++k) v[k] = Vx[i * n + k];
-  for (int r = 0; r < rr.R; ++r) {
-    if (blo) {
-      bool inbox = true;
-      for (int k = 0; k < m; ++k) inbox &= (v[k] >= blo[r * m + k] - 1e-6) & (v[k] <= bhi[r * m + k] + 1e-6);
-      if (!inbox) continue;
-    }
-    int in_s = 1, in_d = 1;
-    for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q) in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
-    for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q) in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
-    const unsigned long long bit = 1ull << (r & 63);
-    if (in_s) smask[s * rr.RW + (r >> 6)] |= bit;
-    if (in_d) dmask[s * rr.RW + (r >> 6)] |= bit;
-  }
-}
-
-// vertices in no region can neither start nor end an edge
-__global__ void k_region_fold(const unsigned long long* __restrict__ smask, const unsigned long long* __restrict__ dmask,
-                              long long V, int RW, uint8_t* __restrict__ src_ok, uint8_t* __restrict__ dst_ok) {
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= V) return;
   bool any_s = false, any_d = false;
-  for (int w = 0; w < RW; ++w) {
-    any_s |= smask[s * RW + w] != 0;
-    any_d |= dmask[s * RW + w] != 0;
+  for (int w = 0; w < rr.RW; ++w) {
+    unsigned long long ms = 0, md = 0;
+    const int r1 = min(rr.R, (w + 1) * 64);
+    for (int r = w * 64; r < r1; ++r) {
+      if (blo) {
+        bool inbox = true;
+        for (int k = 0; k < m; ++k) inbox &= (v[k] >= blo[r * m + k] - 1e-6) & (v[k] <= bhi[r * m + k] + 1e-6);
+        if (!inbox) continue;
+      }
+      int in_s = 1, in_d = 1;
+      for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q) in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
+      for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q) in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
+      const unsigned long long bit = 1ull << (r & 63);
+      if (in_s) ms |= bit;
+      if (in_d) md |= bit;
+    }
+    smask[s * rr.RW + w] = ms;
+    dmask[s * rr.RW + w] = md;
+    any_s |= ms != 0;
+    any_d |= md != 0;
   }
   if (!any_s) src_ok[s] = 0;
   if (!any_d) dst_ok[s] = 0;
 }
 
-// OR of the masks over each 32-vertex group (tile / destination group cull)
+// OR of the masks over each 32-vertex group (tile / destination group cull); blockIdx.y = 1
+// handles a second (mask, ok, out) triple in the same launch
 __global__ void k_mask_or(const unsigned long long* __restrict__ mask, const uint8_t* __restrict__ ok, long long V,
-                          int RW, unsigned long long* __restrict__ out) {
+                          int RW, unsigned long long* __restrict__ out, const unsigned long long* __restrict__ mask2,
+                          const uint8_t* __restrict__ ok2, unsigned long long* __restrict__ out2) {
+  if (blockIdx.y) {
+    mask = mask2;
+    ok = ok2;
+    out = out2;
+  }
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long ng = (V + kTile - 1) / kTile;
   if (t >= ng * RW) return;
@@ -1329,17 +1335,12 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     dmask.alloc(V * rr.RW * sizeof(unsigned long long), c->stream);
     tor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
     gor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
-    BZG_CHECK_CUDA(cudaMemsetAsync(smask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
-    BZG_CHECK_CUDA(cudaMemsetAsync(dmask.ptr, 0, V * rr.RW * sizeof(unsigned long long), c->stream));
     launch(c, "k_region_masks", k_region_masks, dim3(div_up(V, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
            perm.as<int>(), V, m, rblo.as<double>(), rbhi.as<double>(), smask.as<unsigned long long>(),
-           dmask.as<unsigned long long>());
-    launch(c, "k_region_fold", k_region_fold, dim3(div_up(V, 256)), dim3(256), 0, smask.as<unsigned long long>(),
-           dmask.as<unsigned long long>(), V, rr.RW, sok.as<uint8_t>(), dok.as<uint8_t>());
-    launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256)), dim3(256), 0, smask.as<unsigned long long>(),
-           sok.as<uint8_t>(), V, rr.RW, tor.as<unsigned long long>());
-    launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256)), dim3(256), 0, dmask.as<unsigned long long>(),
-           dok.as<uint8_t>(), V, rr.RW, gor.as<unsigned long long>());
+           dmask.as<unsigned long long>(), sok.as<uint8_t>(), dok.as<uint8_t>());
+    launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256), 2), dim3(256), 0, smask.as<unsigned long long>(),
+           sok.as<uint8_t>(), V, rr.RW, tor.as<unsigned long long>(), dmask.as<unsigned long long>(),
+           dok.as<uint8_t>(), gor.as<unsigned long long>());
     rm = RegionMasks{smask.as<unsigned long long>(), dmask.as<unsigned long long>(), tor.as<unsigned long long>(),
                      gor.as<unsigned long long>(), rr.RW};
   }
@@ -1376,7 +1377,8 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     if (R > 0) {
       s_tor.alloc(ngs * rm.RW * sizeof(unsigned long long), c->stream);
       launch(c, "k_mask_or", k_mask_or, dim3(div_up(ngs * rm.RW, 256)), dim3(256), 0, s_smask.as<unsigned long long>(),
-             ok_src, Vs, rm.RW, s_tor.as<unsigned long long>());
+             ok_src, Vs, rm.RW, s_tor.as<unsigned long long>(), (const unsigned long long*)nullptr,
+             (const uint8_t*)nullptr, (unsigned long long*)nullptr);
       rms.smask = s_smask.as<unsigned long long>();
       rms.tile_or = s_tor.as<unsigned long long>();
     }
