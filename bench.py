@@ -326,9 +326,17 @@ def main():
     if args.impl == "reference":
         return reference_arm(args, rank, world)
 
+    import gc
+
     import torch
 
     from paper_2411_13507_b200 import _native as nat
+
+    # Python's cyclic GC can pause the host thread between the start event and the graph launch
+    # of a sub-millisecond step (cfg1 showed one 1.4 ms step in ten); nothing here builds
+    # reference cycles worth collecting during a few minutes of benchmarking
+    gc.collect()
+    gc.disable()
 
     # BZG_BENCH_DEVICE / BZG_DIST_BACKEND=gloo: functional check of the N>1 path with every rank
     # on one GPU and host-side collectives (never a performance number: ranks share the device)
