@@ -48,6 +48,21 @@ struct NvtxRange {
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
+// Programmatic dependent launch: every kernel of the library begins with BZG_PDL_ENTRY -- wait
+// for the preceding grid's completion (and memory flush), then let the next grid launch -- and
+// launch() marks its launches programmatic-serialisation-allowed, so a kernel's blocks are
+// scheduled while its predecessor's last wave drains instead of after it (in captured graphs,
+// a programmatic edge).  Nothing runs before the wait, so stream order is preserved; a launch
+// without the attribute (cooperative, cluster, CUB) makes the wait a no-op.  BZG_PDL=0: off.
+#define BZG_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("BZG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Set while a stream capture (bzg_query) records work: a workspace that would have to grow
 // then is an error (the graph would bake in a fresh allocation), so captures are preceded by
 // an eager warm-up that sizes every buffer.
@@ -252,8 +267,22 @@ inline void launch(Ctx* c, const char* name, void (*kern)(KArgs...), dim3 grid, 
   cudaEvent_t a = nullptr, b = nullptr;
   const bool timed = c->timed(name);
   if (timed) { a = c->take_event(); BZG_CHECK_CUDA(cudaEventRecord(a, c->stream)); }
-  kern<<<grid, block, smem, c->stream>>>(std::forward<Args>(args)...);
-  BZG_CHECK_CUDA(cudaGetLastError());
+  if (pdl_enabled()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BZG_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  } else {
+    kern<<<grid, block, smem, c->stream>>>(std::forward<Args>(args)...);
+    BZG_CHECK_CUDA(cudaGetLastError());
+  }
   c->launches++;
   if (timed) {
     b = c->take_event();

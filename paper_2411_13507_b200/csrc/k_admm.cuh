@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(128) k_qp_setup(QpParams qp, DParams dp, const
                                                   const unsigned long long* __restrict__ pend, long long n_inst,
                                                   const unsigned long long* __restrict__ d_n,
                                                   double* __restrict__ consts) {
+  BZG_PDL_ENTRY();
   using K = QpConsts<G, M, C, CANON>;
   const long long n = dev_count(n_inst, d_n);
   const double rho = qp.rho, req = qp.rho_eq, sig = qp.sigma;
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(128, 3) k_qp_admm(QpParams qp, const double* _
                                                  int* __restrict__ it_out, double* __restrict__ x_out,
                                                  double* __restrict__ zy_out, AdmmPass pass,
                                                  const unsigned long long* __restrict__ d_n) {
+  BZG_PDL_ENTRY();
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1;
   const int lane = threadIdx.x & 31;
   const double rho = UNIT ? 1.0 : qp.rho, req = qp.rho_eq, ri = UNIT ? 1.0 : 1.0 / qp.rho;

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
                                                   int* __restrict__ it_out, double* __restrict__ x_out,
                                                   double* __restrict__ zy_out,
                                                   const unsigned long long* __restrict__ d_n) {
+  BZG_PDL_ENTRY();
   using K = QpConsts<G, M, C, CANON>;
   constexpr int J = 2 * G, JH = G, NV = J + C, MC = C + J + 1;
   constexpr int R = K::R;          // stored Q rows

@@ -37,6 +37,7 @@ __global__ void k_sample_candidates(SampleParams sp, unsigned long long st_hi, u
                                     unsigned long long inc_hi, unsigned long long inc_lo, long long row0,
                                     long long count, double* __restrict__ cand, int* __restrict__ flag,
                                     const unsigned long long* __restrict__ pcg_dev) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= count) return;
   if (pcg_dev) {
@@ -62,6 +63,7 @@ __global__ void k_sample_candidates(SampleParams sp, unsigned long long st_hi, u
 __global__ void k_sample_scatter(const double* __restrict__ cand, const int* __restrict__ flag,
                                  const int* __restrict__ pos, long long count, int n, long long need,
                                  double* __restrict__ out) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= count || !flag[t]) return;
   const long long p = pos[t];
@@ -98,6 +100,7 @@ __device__ __forceinline__ int region_of(const long long* off, int R, long long 
 
 __global__ void k_sample_regions(RegionSampleDev rs, long long total, double* __restrict__ cand,
                                  int* __restrict__ flag) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= total) return;
   const int r = region_of(rs.cand_off, rs.R, t);
@@ -123,6 +126,7 @@ __global__ void k_scatter_regions(const double* __restrict__ cand, const int* __
                                   const int* __restrict__ pos, const long long* __restrict__ cand_off, int R,
                                   long long total, int n, const long long* __restrict__ dest,
                                   const long long* __restrict__ need, double* __restrict__ out) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= total || !flag[t]) return;
   const int r = region_of(cand_off, R, t);
@@ -133,6 +137,7 @@ __global__ void k_scatter_regions(const double* __restrict__ cand, const int* __
 
 __global__ void k_region_acc(const int* __restrict__ pos, const long long* __restrict__ cand_off, int R,
                              long long* __restrict__ acc) {
+  BZG_PDL_ENTRY();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < R) acc[r] = (long long)pos[cand_off[r + 1]] - (long long)pos[cand_off[r]];
 }
@@ -168,6 +173,7 @@ constexpr int kTile = 32;
 
 __global__ void k_morton(const double* __restrict__ Vx, long long V, int n, int m, double lo0, double lo1,
                          double lo2, double s0, double s1, double s2, unsigned* __restrict__ key, int* __restrict__ idx) {
+  BZG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= V) return;
   const int bits = m == 1 ? 30 : (m == 2 ? 16 : 10);
@@ -193,6 +199,7 @@ __global__ void k_project_sorted(RowPlan rp, const double* __restrict__ F, int n
                                  const int* __restrict__ perm, long long V, int Kpad, long long r0, long long r1,
                                  double* __restrict__ a1c, double* __restrict__ a2t, uint8_t* __restrict__ src_ok,
                                  uint8_t* __restrict__ dst_ok) {
+  BZG_PDL_ENTRY();
   extern __shared__ double sF[];
   const int n = rp.n;
   for (int t = threadIdx.x; t < nF * 2 * n; t += blockDim.x) sF[t] = F[t];
@@ -224,6 +231,7 @@ __global__ void k_project_sorted(RowPlan rp, const double* __restrict__ F, int n
 // vertex lies in [r0, r1) (flag + exclusive scan -> pos), then gathered so source tiles are
 // dense in the block (a tile of the full order would hold ~32 / G of them).
 __global__ void k_src_flags(const int* __restrict__ perm, long long V, long long r0, long long r1, int* __restrict__ flag) {
+  BZG_PDL_ENTRY();
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s < V) flag[s] = (perm[s] >= r0 && perm[s] < r1) ? 1 : 0;
 }
@@ -233,6 +241,7 @@ __global__ void k_src_gather(const int* __restrict__ perm, const int* __restrict
                              const unsigned long long* __restrict__ smask, int RW, int* __restrict__ perm_src,
                              double* __restrict__ a1c_src, uint8_t* __restrict__ ok_src,
                              unsigned long long* __restrict__ smask_src) {
+  BZG_PDL_ENTRY();
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= V || !flag[s]) return;
   const long long t = pos[s];
@@ -245,6 +254,7 @@ __global__ void k_src_gather(const int* __restrict__ perm, const int* __restrict
 // [min, max] per (32-vertex group, interval) over the group's valid vertices
 __global__ void k_group_bounds(const double* __restrict__ a, int transposed, long long V, int Kpad,
                                const uint8_t* __restrict__ ok, double* __restrict__ gmin, double* __restrict__ gmax) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long ng = (V + kTile - 1) / kTile;
   if (t >= ng * Kpad) return;
@@ -291,6 +301,7 @@ __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, 
                                long long V, int m, const double* __restrict__ blo, const double* __restrict__ bhi,
                                unsigned long long* __restrict__ smask, unsigned long long* __restrict__ dmask,
                                uint8_t* __restrict__ src_ok, uint8_t* __restrict__ dst_ok) {
+  BZG_PDL_ENTRY();
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= V) return;
   const long long i = perm[s];
@@ -328,6 +339,7 @@ __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, 
 __global__ void k_mask_or(const unsigned long long* __restrict__ mask, const uint8_t* __restrict__ ok, long long V,
                           int RW, unsigned long long* __restrict__ out, const unsigned long long* __restrict__ mask2,
                           const uint8_t* __restrict__ ok2, unsigned long long* __restrict__ out2) {
+  BZG_PDL_ENTRY();
   if (blockIdx.y) {
     mask = mask2;
     ok = ok2;
@@ -358,6 +370,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_tiles(
     const double* __restrict__ tmax, const double* __restrict__ gmin, const double* __restrict__ gmax, long long V,
     long long r0, long long W, uint32_t* __restrict__ bits, unsigned long long* __restrict__ rowcnt,
     RegionMasks rm, const int* __restrict__ perm_src, long long V_src) {
+  BZG_PDL_ENTRY();
   __shared__ double s_a1[kTile][K];
   __shared__ uint8_t s_ok[kTile];
   __shared__ int s_orig[kTile];
@@ -476,6 +489,7 @@ __global__ void k_tile_group_cull(Bounds bd, const double* __restrict__ tmin, co
                                   const double* __restrict__ gmin, const double* __restrict__ gmax, long long ng,
                                   int K, RegionMasks rm, int reg, unsigned long long* __restrict__ list,
                                   unsigned long long* __restrict__ n_list) {
+  BZG_PDL_ENTRY();
   const long long tile = blockIdx.y;
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   bool live = g < ng;
@@ -517,6 +531,7 @@ __global__ void __launch_bounds__(kPairThreads, 3) k_pair_list(
     const double* __restrict__ gmax, long long V, long long r0, long long W, uint32_t* __restrict__ bits,
     unsigned long long* __restrict__ rowcnt, RegionMasks rm, const unsigned long long* __restrict__ list,
     const unsigned long long* __restrict__ n_list, const int* __restrict__ perm_src, long long V_src) {
+  BZG_PDL_ENTRY();
   constexpr int NW = kPairThreads / 32, QL = (K + 31) / 32;
   // dynamic shared memory (pair_list_smem): per warp a1 tile, region masks, original ids, flags
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -648,6 +663,7 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_rows(const double* __restri
                                                           long long k, long long r0, long long W,
                                                           uint32_t* __restrict__ bits,
                                                           unsigned long long* __restrict__ rowcnt) {
+  BZG_PDL_ENTRY();
   typedef cub::BlockScan<unsigned long long, kKnnThreads> BS;
   typedef cub::BlockReduce<unsigned long long, kKnnThreads> BR;
   __shared__ unsigned hist[256];
@@ -747,6 +763,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand(DParams dp, const dou
                                                            long long r1, long long W,
                          const uint32_t* __restrict__ bits, const long long* __restrict__ rptr,
                          int* __restrict__ src, int* __restrict__ dst, double* __restrict__ cost, long long cap) {
+  BZG_PDL_ENTRY();
   // The set bits of 32 words are first listed in ascending (word, bit) order in the warp's
   // shared slice, then the lanes take one edge each, so a word with many edges does not
   // serialise its lane while the others idle.  cap: the arrays' capacity (a captured plan's,
@@ -808,6 +825,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand(DParams dp, const dou
 template <int G, int M>
 __global__ void k_points(DParams dp, const double* __restrict__ Vx, long long E, const int* __restrict__ src,
                          const int* __restrict__ dst, double* __restrict__ out) {
+  BZG_PDL_ENTRY();
   constexpr int N = G * M;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= E) return;
@@ -830,6 +848,7 @@ __global__ void k_points(DParams dp, const double* __restrict__ Vx, long long E,
 // never reads beyond the arrays of a build whose edges overflowed -- the plan reruns it)
 __global__ void k_row_ptr_global(const long long* __restrict__ local, long long V, long long r0, long long r1,
                                  long long* __restrict__ out, long long cap) {
+  BZG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i > V) return;
   const long long E = local[r1 - r0];
@@ -839,6 +858,7 @@ __global__ void k_row_ptr_global(const long long* __restrict__ local, long long 
 
 // row_ptr[i] = lower_bound(src, i) over a source-sorted edge list (gathered row blocks)
 __global__ void k_row_ptr_from_src(const int* __restrict__ src, long long E, long long V, long long* __restrict__ out) {
+  BZG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i > V) return;
   long long lo = 0, hi = E;
@@ -853,6 +873,7 @@ __global__ void k_row_ptr_from_src(const int* __restrict__ src, long long E, lon
 __global__ void k_check_edges(const double* __restrict__ F, const double* __restrict__ thresh, int n, int nF,
                               long long k, const double* __restrict__ X1, const double* __restrict__ X2,
                               uint8_t* __restrict__ out) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= k) return;
   int ok = 1;

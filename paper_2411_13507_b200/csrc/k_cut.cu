@@ -300,6 +300,7 @@ template <int G, int M>
 __global__ void k_obs_grid_extent(DParams dp, const double* __restrict__ Vx, long long E,
                                   const int* __restrict__ src, const int* __restrict__ dst, ObsGrid* __restrict__ gp,
                                   const long long* __restrict__ dE) {
+  BZG_PDL_ENTRY();
   constexpr int N = G * M;
   if (dE) E = min(E, *dE);  // a captured plan's edge count (E = its capacity)
   const long long stride = E > 65536 ? E / 65536 : 1;
@@ -331,6 +332,7 @@ template <int M>
 __global__ void k_obs_grid_masks(const ObsRec<M>* __restrict__ obs, int n_obs, int chunk,
                                  const double* __restrict__ bnd, ObsGrid* __restrict__ gpp,
                                  unsigned long long* __restrict__ masks) {
+  BZG_PDL_ENTRY();
   const double lo0 = bnd[0], lo1 = bnd[1], hi0 = bnd[2], hi1 = bnd[3];  // the obstacles' xy bounds
   const int cell = blockIdx.x * blockDim.x + threadIdx.x, ch = blockIdx.y;
   if (cell >= kGridCells * kGridCells) return;
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(kHeurThreads, 3) k_cut_heuristic(DParams dp, c
                                 unsigned long long gen_cap, unsigned long long* __restrict__ gen_pend,
                                 const ObsGrid* __restrict__ grid, const unsigned long long* __restrict__ gmask,
                                 CutBits bits, const long long* __restrict__ dE) {
+  BZG_PDL_ENTRY();
   constexpr int N = G * M;
   if (dE) E = min(E, *dE);  // a captured plan's edge count (E = its capacity)
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -633,6 +636,7 @@ __global__ void k_cut_general(DParams dp, const double* __restrict__ Vx, const i
                               int* __restrict__ first_kill, unsigned long long* __restrict__ counters,
                               unsigned long long* __restrict__ n_pend, unsigned long long cap,
                               unsigned long long* __restrict__ pend, int8_t* __restrict__ code_out, CutBits bits) {
+  BZG_PDL_ENTRY();
   constexpr int N = G * M;
   // n = min(*d_n, n_cap): the pair count of the screen, known on the device only
   const long long n = d_n ? ((long long)*d_n < n_cap ? (long long)*d_n : n_cap) : n_cap;
@@ -671,6 +675,7 @@ __global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long 
                               const unsigned long long* __restrict__ d_n, const uint8_t* __restrict__ safe,
                               int* __restrict__ qp_kill, uint8_t* __restrict__ qp_saved,
                               unsigned long long* __restrict__ counters, CutBits bits) {
+  BZG_PDL_ENTRY();
   const long long n = (long long)*d_n < n_cap ? (long long)*d_n : n_cap;
   unsigned long long s = 0, u = 0;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -702,6 +707,7 @@ __global__ void k_qp_verdicts(const unsigned long long* __restrict__ pend, long 
 __global__ void k_mask_finalize(long long E, int n_obs, const int* __restrict__ first_kill,
                                 const int* __restrict__ qp_kill, const uint8_t* __restrict__ qp_saved,
                                 uint8_t* __restrict__ alive, uint8_t* __restrict__ prov) {
+  BZG_PDL_ENTRY();
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= E) return;
   const int kh = first_kill[e], kq = qp_kill[e];
@@ -715,6 +721,7 @@ __global__ void k_mask_finalize(long long E, int n_obs, const int* __restrict__ 
 
 __global__ void k_unpack_pend(const unsigned long long* __restrict__ pend, long long n, long long* __restrict__ e,
                               int* __restrict__ o) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= n) return;
   e[t] = (long long)(pend[t] >> 20);
@@ -722,6 +729,7 @@ __global__ void k_unpack_pend(const unsigned long long* __restrict__ pend, long 
 }
 
 __global__ void k_fill_int(int* p, long long n, int v) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t < n) p[t] = v;
 }
@@ -1179,6 +1187,7 @@ void cut_graph_impl(Ctx* c, Graph* g, int n_obs, const int32_t* row_off, const d
 // read once for 32 edges (a thread per edge re-read it 32 times in a 3 x n_obs dependent loop).
 __global__ void k_cut_combine(long long E, int n_obs, const uint32_t* __restrict__ pool, long long Wb,
                               const int* __restrict__ slots, uint8_t* __restrict__ alive, uint8_t* __restrict__ prov) {
+  BZG_PDL_ENTRY();
   const long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (w >= Wb) return;
   uint32_t hk = 0, qk = 0, first_h = 0, saved = 0;
@@ -1222,6 +1231,7 @@ __global__ void k_cut_combine(long long E, int n_obs, const uint32_t* __restrict
 
 // popcounts of n_rows bit rows of Wb words into out[row]
 __global__ void k_row_popcount(const uint32_t* __restrict__ rows, long long Wb, unsigned long long* __restrict__ out) {
+  BZG_PDL_ENTRY();
   const uint32_t* r = rows + (size_t)blockIdx.x * Wb;
   unsigned long long s = 0;
   for (long long w = threadIdx.x; w < Wb; w += blockDim.x) s += __popc(r[w]);
@@ -1232,6 +1242,7 @@ __global__ void k_row_popcount(const uint32_t* __restrict__ rows, long long Wb, 
 }
 
 __global__ void k_remap_int(int* __restrict__ v, long long n, const int* __restrict__ map) {
+  BZG_PDL_ENTRY();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t < n) v[t] = map[v[t]];
 }

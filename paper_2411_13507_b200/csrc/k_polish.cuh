@@ -18,6 +18,7 @@ __global__ void k_qp_select(long long n_inst, const unsigned long long* __restri
                             double eps_cut, const int8_t* __restrict__ st, const double* __restrict__ x,
                             double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, int* __restrict__ list,
                             unsigned long long* __restrict__ n_list) {
+  BZG_PDL_ENTRY();
   constexpr int J = 2 * G, NV = J + C;
   const long long n = dev_count(n_inst, d_n);
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kPolishThreads) k_qp_polish(
     const ObsRec<M, obs_cap<C>()>* __restrict__ obs, const unsigned long long* __restrict__ pend, const int* __restrict__ list,
     long long n_list, double eps_cut, double* __restrict__ x_io, const double* __restrict__ zy,
     double* __restrict__ delta_out, uint8_t* __restrict__ safe_out, const int8_t* __restrict__ st) {
+  BZG_PDL_ENTRY();
   constexpr int J = 2 * G, NV = J + C, MC = C + J + 1, NC = J + C + 1;
   constexpr int BS = kPolishThreads;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -579,6 +581,7 @@ __global__ void __launch_bounds__(128) k_qp_polish_reg(
     const unsigned long long* __restrict__ n_list, double eps_cut, double* __restrict__ x_io,
     const double* __restrict__ zy, double* __restrict__ delta_out, uint8_t* __restrict__ safe_out,
     const int8_t* __restrict__ st) {
+  BZG_PDL_ENTRY();
   const long long n = (long long)*n_list;
   for (long long li = (long long)blockIdx.x * blockDim.x + threadIdx.x; li < n; li += (long long)gridDim.x * blockDim.x)
     polish_one_reg<G, M, C>(list[li], dp, Vx, src, dst, obs, pend, eps_cut, x_io, zy, delta_out, safe_out, st);

@@ -9,6 +9,7 @@ namespace {
 
 template <bool kFma>
 __global__ void k_probe_fp64(int iters, double seed, double* out) {
+  BZG_PDL_ENTRY();
   // 8 independent dependency chains per thread keep the FP64 pipe saturated
   double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6,
          a7 = a0 + 7;

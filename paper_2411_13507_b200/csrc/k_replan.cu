@@ -28,6 +28,7 @@ struct ProjParams {
 
 __global__ void __launch_bounds__(kProjThreads) k_project_on_path(ProjParams pp, const double* __restrict__ path,
                                                                   double* __restrict__ out) {
+  BZG_PDL_ENTRY();
   const int n = pp.m * pp.gamma, J = pp.p + 1, G2 = 2 * pp.gamma;
   double best_d = INFINITY;
   int best_k = 0x7fffffff;

@@ -71,6 +71,7 @@ __device__ __forceinline__ double snap_norm(const double* v, const SnapParams& s
 // else the by-value sp
 __global__ void k_snap(SnapParams sp_val, const SnapParams* __restrict__ spd, const double* __restrict__ Vx,
                        long long V, const uint8_t* __restrict__ reach, unsigned long long* __restrict__ best) {
+  BZG_PDL_ENTRY();
   const SnapParams& sp = spd ? *spd : sp_val;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   double val = INFINITY;
@@ -123,6 +124,7 @@ __global__ void k_snap(SnapParams sp_val, const SnapParams* __restrict__ spd, co
 }
 
 __global__ void k_snap_final(unsigned long long* __restrict__ best, int nblocks, long long* __restrict__ out) {
+  BZG_PDL_ENTRY();
   // single warp: lowest index among blocks whose local minimum equals the global minimum
   const int lane = threadIdx.x;
   const unsigned long long m = best[0];
@@ -151,6 +153,7 @@ constexpr long long kSnapBlockV = 16384;
 __global__ void __launch_bounds__(1024) k_snap_block(SnapParams s0, SnapParams s1, const SnapParams* __restrict__ spd,
                                                      int first, const double* __restrict__ Vx, long long V,
                                                      const uint8_t* __restrict__ reach, long long* __restrict__ out) {
+  BZG_PDL_ENTRY();
   const int set = first + blockIdx.x;
   const SnapParams& sp = spd ? spd[set] : (set == 0 ? s0 : s1);
   double val = INFINITY;
@@ -201,6 +204,7 @@ __global__ void k_reach_sweeps(long long E, long long V, const int* __restrict__
                                const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach,
                                long long* __restrict__ key, const long long* __restrict__ plan, int* __restrict__ flags,
                                const long long* __restrict__ dE) {
+  BZG_PDL_ENTRY();
   if (dE) E = min(E, *dE);  // a captured plan's edge count (E = its capacity)
   const long long vg = plan[0];
   if (*(volatile long long*)key == vg) return;  // uniform: the cached set is vg's
@@ -242,6 +246,7 @@ __global__ void k_reach_pull(long long V, const long long* __restrict__ fptr, co
                              const uint8_t* __restrict__ alive, uint8_t* __restrict__ reach,
                              long long* __restrict__ key, const long long* __restrict__ plan, int* __restrict__ flags,
                              const long long* __restrict__ dE) {
+  BZG_PDL_ENTRY();
   const long long vg = plan[0];
   if (*(volatile long long*)key == vg) return;  // uniform: the cached set is vg's
   cg::grid_group grid = cg::this_grid();
@@ -290,6 +295,7 @@ __global__ void k_bf_persistent(long long V, const long long* __restrict__ row_p
                                 unsigned long long* __restrict__ dist, int* __restrict__ stamp, int* __restrict__ qa,
                                 int* __restrict__ qb, int* __restrict__ counts, int max_sweeps,
                                 const long long* __restrict__ plan) {
+  BZG_PDL_ENTRY();
   if (!plan[2]) return;  // grid-uniform
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
@@ -368,6 +374,7 @@ __global__ void k_bf_scan(long long V, const long long* __restrict__ row_ptr, co
                           unsigned long long* __restrict__ dist, unsigned long long* __restrict__ prev,
                           int* __restrict__ qa, int* __restrict__ qb, int* __restrict__ counts, int max_sweeps,
                           const long long* __restrict__ plan) {
+  BZG_PDL_ENTRY();
   if (!plan[2]) return;  // grid-uniform
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31;
@@ -444,6 +451,7 @@ __global__ void __launch_bounds__(kBfCtaThreads, 1)
 k_bf_cta(long long V, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
          const double* __restrict__ cost, const uint8_t* __restrict__ alive, unsigned long long* __restrict__ dist,
          int* __restrict__ counts, int max_sweeps, const long long* __restrict__ plan) {
+  BZG_PDL_ENTRY();
   if (!plan[2]) return;  // block-uniform
   extern __shared__ unsigned long long smem_u64[];
   unsigned long long* sd = smem_u64;               // V distances (double bits)
@@ -537,6 +545,7 @@ __global__ void __launch_bounds__(kBfClusterThreads, 1)
 k_bf_cluster(long long V, long long chunk, const long long* __restrict__ row_ptr, const int* __restrict__ dst,
              const double* __restrict__ cost, const uint8_t* __restrict__ alive, unsigned long long* __restrict__ dist,
              int* __restrict__ counts, int max_sweeps, const long long* __restrict__ plan) {
+  BZG_PDL_ENTRY();
   if (!plan[2]) return;  // cluster-uniform
   cg::cluster_group cl = cg::this_cluster();  // barriers: barrier.cluster arrive.release / wait.acquire
   extern __shared__ unsigned long long smem_u64[];
@@ -620,6 +629,7 @@ k_bf_cluster(long long V, long long chunk, const long long* __restrict__ row_ptr
 }
 
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+  BZG_PDL_ENTRY();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
@@ -631,6 +641,7 @@ __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long lon
 //   tree must be (re)built, plan[3] = 1 when the mask's cached tree (tree_key = its v0) is
 //   reused.  Kernels that build the tree return at once when plan[2] == 0.
 __global__ void k_plan(long long* __restrict__ plan, long long* __restrict__ tree_key) {
+  BZG_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const long long vg = plan[0], v0 = plan[1];
   const bool trivial = v0 < 0 || v0 == vg;
@@ -648,6 +659,7 @@ __global__ void k_init_tree(long long V, const long long* __restrict__ plan, int
                             unsigned long long* __restrict__ dist, unsigned long long* __restrict__ prev,
                             int* __restrict__ stamp, int* __restrict__ parent, unsigned long long* __restrict__ pd,
                             int* __restrict__ counts, int* __restrict__ qa) {
+  BZG_PDL_ENTRY();
   if (!plan[2]) return;
   const long long v0 = plan[1];
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -680,6 +692,7 @@ __global__ void k_bf_async(long long V, const long long* __restrict__ row_ptr, c
                            const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                            unsigned long long* __restrict__ dist, int* __restrict__ inq, int* __restrict__ ring,
                            unsigned long long* __restrict__ ctr, long long Q, const long long* __restrict__ plan) {
+  BZG_PDL_ENTRY();
   if (!plan[2]) return;
   const int lane = threadIdx.x & 31;
   volatile int* vring = ring;
@@ -751,6 +764,7 @@ __global__ void k_parent_dist(long long E, const int* __restrict__ src, const in
                               const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                               const unsigned long long* __restrict__ dist, unsigned long long* __restrict__ pd,
                               const long long* __restrict__ plan, const long long* __restrict__ dE) {
+  BZG_PDL_ENTRY();
   if (dE) E = min(E, *dE);
   if (plan && !plan[2]) return;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -768,6 +782,7 @@ __global__ void k_parent_idx(long long E, const int* __restrict__ src, const int
                              const unsigned long long* __restrict__ dist, const unsigned long long* __restrict__ pd,
                              int* __restrict__ parent, const long long* __restrict__ plan,
                              const long long* __restrict__ dE) {
+  BZG_PDL_ENTRY();
   if (dE) E = min(E, *dE);
   if (plan && !plan[2]) return;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -783,6 +798,7 @@ __global__ void k_parent_idx(long long E, const int* __restrict__ src, const int
 // out[0] = path length (-1: None), out[1] = dist bits, out[2..] = the path from v0 to vg
 __global__ void k_backtrack(long long V, const long long* __restrict__ plan, const int* __restrict__ parent,
                             const unsigned long long* __restrict__ dist, long long* __restrict__ out) {
+  BZG_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const long long vg = plan[0], v0 = plan[1];
   long long* path = out + 2;
