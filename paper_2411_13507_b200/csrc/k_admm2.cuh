@@ -33,7 +33,7 @@ namespace {
 constexpr long long kAdmm2MaxInst = 4096;
 
 template <int G, int M, int C, bool CANON>
-__global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* __restrict__ consts, long long n_inst,
+__global__ void __launch_bounds__(128, 2) k_qp_admm2(QpParams qp, const double* __restrict__ consts, long long n_inst,
                                                   unsigned long long* __restrict__ next, int8_t* __restrict__ st_out,
                                                   int* __restrict__ it_out, double* __restrict__ x_out,
                                                   double* __restrict__ zy_out,
@@ -61,6 +61,10 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
   double lam[JH], zl[JH], yl[JH];
   double del[RH][CPR], zc[RH][CPR], yc[RH][CPR];
   double ze = 0.0, ye = 0.0;
+  // pipelining state: pend = the current state is an iterate whose termination test is due;
+  // cu / su / dy* = the partial convergence test, sign test and dual steps of its update
+  bool pend = false, cu = true, su = true;
+  double dyl[JH], dyc[RH][CPR], dye = 0.0;
 
   while (true) {
     // ---- refill pairs whose instance terminated (one atomic per warp)
@@ -105,18 +109,23 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
         ze = 0.0;
         ye = 0.0;
         it = 0;
+        pend = false;
       }
     }
     if (__all_sync(FULL, inst == -2)) break;
 
     // ---- a batch of iterations; every lane runs the body (the shuffles need the whole
-    // warp), lanes without an instance compute on stale state and write nothing
+    // warp), lanes without an instance compute on stale state and write nothing.
+    // Software-pipelined: iteration k+1's update is formed (into n_*) while iteration k's
+    // termination test runs on the current state -- two independent dependency chains the
+    // scheduler interleaves; when the test stops the instance, the current state (iteration
+    // k) is written and the speculative update is dropped, so iterates, iteration counts and
+    // outputs are k_qp_admm's exactly.
 #pragma unroll 1
     for (int kb = 0; kb < qp.batch; ++kb) {
       if (__all_sync(FULL, inst < 0)) break;
       const bool live = inst >= 0;
-      it += live ? 1 : 0;
-      // (R z - y), sigma delta - w, and the delta-eliminated right-hand side, per owned row
+      // ===== update chain: the next iterate from the current state
       double rdel[RH][CPR], fT[RH];
 #pragma unroll
       for (int i = 0; i < RH; ++i) {
@@ -168,24 +177,24 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
         aa[k] = p == 0 ? a[k] : oth;
         aa[JH + k] = p == 0 ? oth : a[k];
       }
-      bool sign_ok = true, conv = true;
-      double dyl[JH];
+      bool n_su = true, n_cu = true;
+      double n_lam[JH], n_zl[JH], n_yl[JH], n_dyl[JH];
 #pragma unroll
       for (int k = 0; k < JH; ++k) {
         const double zr = RELAX(a[k], zl[k]);
         const double zn = clip_nonneg(__dadd_rn(zr, yl[k]));
         const double yn = __dadd_rn(yl[k], __dsub_rn(zr, zn));
-        dyl[k] = __dsub_rn(yn, yl[k]);
-        sign_ok &= not_pos(dyl[k]);
-        lam[k] = RELAX(a[k], lam[k]);
-        zl[k] = zn;
-        yl[k] = yn;
-        conv &= fabs(__dsub_rn(lam[k], zn)) <= eps;
+        n_dyl[k] = __dsub_rn(yn, yl[k]);
+        n_su &= not_pos(n_dyl[k]);
+        n_lam[k] = RELAX(a[k], lam[k]);
+        n_zl[k] = zn;
+        n_yl[k] = yn;
+        n_cu &= fabs(__dsub_rn(n_lam[k], zn)) <= eps;
       }
       double sa = 0.0;
 #pragma unroll
       for (int j = 0; j < J; ++j) sa += aa[j];
-      double dyc[RH][CPR];
+      double n_del[RH][CPR], n_zc[RH][CPR], n_yc[RH][CPR], n_dyc[RH][CPR];
 #pragma unroll
       for (int i = 0; i < RH; ++i) {
         double qa = 0.0;
@@ -198,22 +207,22 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
           const double zr = RELAX(__dsub_rn(q, d), zc[i][l]);
           const double zn = clip_upper(__dadd_rn(zr, yc[i][l]), bb[i][l]);
           const double yn = __dadd_rn(yc[i][l], __dsub_rn(zr, zn));
-          dyc[i][l] = __dsub_rn(yn, yc[i][l]);
-          sign_ok &= not_neg(dyc[i][l]);
-          del[i][l] = RELAX(d, del[i][l]);
-          zc[i][l] = zn;
-          yc[i][l] = yn;
+          n_dyc[i][l] = __dsub_rn(yn, yc[i][l]);
+          n_su &= not_neg(n_dyc[i][l]);
+          n_del[i][l] = RELAX(d, del[i][l]);
+          n_zc[i][l] = zn;
+          n_yc[i][l] = yn;
         }
       }
-      double dye;
+      double n_ye, n_dye;
       {
         const double zr = RELAX(sa, ze);
-        const double yn = __dadd_rn(ye, __dmul_rn(req, __dsub_rn(zr, 1.0)));
-        dye = __dsub_rn(yn, ye);
-        ze = 1.0;
-        ye = yn;
+        n_ye = __dadd_rn(ye, __dmul_rn(req, __dsub_rn(zr, 1.0)));
+        n_dye = __dsub_rn(n_ye, ye);
       }
-      // termination test at the new iterate
+
+      // ===== termination test of the current state (iteration `it`; none before the first)
+      bool conv = cu;
       double la[J];
 #pragma unroll
       for (int k = 0; k < JH; ++k) {
@@ -254,12 +263,12 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
         conv &= fabs(acc) <= eps;
       }
       // combine the pair's partial tests
-      const unsigned bc = __ballot_sync(FULL, conv), bs = __ballot_sync(FULL, sign_ok);
-      conv = ((bc >> pair0) & 3u) == 3u;
-      sign_ok = ((bs >> pair0) & 3u) == 3u;
+      const unsigned bc = __ballot_sync(FULL, conv), bs = __ballot_sync(FULL, su);
+      conv = pend && ((bc >> pair0) & 3u) == 3u;
+      const bool sign_ok = ((bs >> pair0) & 3u) == 3u;
 
       int status = conv ? BZG_SOLVED : -1;
-      const bool cert = live && !conv && sign_ok;
+      const bool cert = live && pend && !conv && sign_ok;
       if (__any_sync(FULL, cert)) {
         // primal-infeasibility certificate (k_qp_admm's test, qpsolver.py:193-209), formed on
         // every lane of the warp and applied where `cert` holds
@@ -314,7 +323,7 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
         small = ((bsm >> pair0) & 3u) == 3u;
         if (cert && supp < 0.0 && dmax > 1e-13 && supp <= -lim && small) status = BZG_INFEASIBLE;
       }
-      if (status < 0 && it >= qp.max_iter) status = BZG_MAX_ITER;
+      if (pend && status < 0 && it >= qp.max_iter) status = BZG_MAX_ITER;
       if (live && status >= 0) {
         double* xo = x_out + inst * NV;
         double* zo = zy_out + inst * 2 * MC;
@@ -344,6 +353,30 @@ __global__ void __launch_bounds__(128, 4) k_qp_admm2(QpParams qp, const double* 
             }
         }
         inst = -1;
+      } else {  // commit the next iterate
+        it += live ? 1 : 0;
+        pend = true;
+        cu = n_cu;
+        su = n_su;
+#pragma unroll
+        for (int k = 0; k < JH; ++k) {
+          lam[k] = n_lam[k];
+          zl[k] = n_zl[k];
+          yl[k] = n_yl[k];
+          dyl[k] = n_dyl[k];
+        }
+#pragma unroll
+        for (int i = 0; i < RH; ++i)
+#pragma unroll
+          for (int l = 0; l < CPR; ++l) {
+            del[i][l] = n_del[i][l];
+            zc[i][l] = n_zc[i][l];
+            yc[i][l] = n_yc[i][l];
+            dyc[i][l] = n_dyc[i][l];
+          }
+        ze = 1.0;
+        ye = n_ye;
+        dye = n_dye;
       }
     }
   }
