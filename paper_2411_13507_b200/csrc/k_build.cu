@@ -293,17 +293,20 @@ struct RegionRowsDev {
   int R, RW, n;
 };
 
-// one thread per sorted vertex: regions whose (1e-6-grown) position box misses the vertex are
-// skipped (membership implies P_0 = x1 resp. P_p = x2 lies in the region), the rest are tested
-// row by row.  The thread owns its mask words (written whole, no pre-zeroing) and folds them:
-// a vertex in no region can neither start nor end an edge (src_ok / dst_ok cleared).
+// one warp per sorted vertex, one lane per region (32 at a time): regions whose (1e-6-grown)
+// position box misses the vertex are skipped (membership implies P_0 = x1 resp. P_p = x2 lies
+// in the region), the rest are tested row by row; the mask words are two ballots each.  The
+// warp writes its vertex's mask words whole (no pre-zeroing) and folds them: a vertex in no
+// region can neither start nor end an edge (src_ok / dst_ok cleared).  (One thread per vertex
+// looping over all regions was latency-bound: 93 us at cfg5-10k's 200 regions.)
 __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, const int* __restrict__ perm,
                                long long V, int m, const double* __restrict__ blo, const double* __restrict__ bhi,
                                unsigned long long* __restrict__ smask, unsigned long long* __restrict__ dmask,
                                uint8_t* __restrict__ src_ok, uint8_t* __restrict__ dst_ok) {
   BZG_PDL_ENTRY();
-  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= V) return;
+  const long long s = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= V) return;  // warp-uniform
   const long long i = perm[s];
   const int n = rr.n;
   double v[kMaxN];
@@ -311,27 +314,37 @@ __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, 
   bool any_s = false, any_d = false;
   for (int w = 0; w < rr.RW; ++w) {
     unsigned long long ms = 0, md = 0;
-    const int r1 = min(rr.R, (w + 1) * 64);
-    for (int r = w * 64; r < r1; ++r) {
-      if (blo) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = w * 64 + h * 32 + lane;
+      int in_s = 0, in_d = 0;
+      if (r < rr.R) {
         bool inbox = true;
-        for (int k = 0; k < m; ++k) inbox &= (v[k] >= blo[r * m + k] - 1e-6) & (v[k] <= bhi[r * m + k] + 1e-6);
-        if (!inbox) continue;
+        if (blo)
+          for (int k = 0; k < m; ++k) inbox &= (v[k] >= blo[r * m + k] - 1e-6) & (v[k] <= bhi[r * m + k] + 1e-6);
+        if (inbox) {
+          in_s = 1;
+          in_d = 1;
+          for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q)
+            in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
+          for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q)
+            in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
+        }
       }
-      int in_s = 1, in_d = 1;
-      for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q) in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
-      for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q) in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
-      const unsigned long long bit = 1ull << (r & 63);
-      if (in_s) ms |= bit;
-      if (in_d) md |= bit;
+      ms |= (unsigned long long)__ballot_sync(0xffffffffu, in_s) << (32 * h);
+      md |= (unsigned long long)__ballot_sync(0xffffffffu, in_d) << (32 * h);
     }
-    smask[s * rr.RW + w] = ms;
-    dmask[s * rr.RW + w] = md;
+    if (lane == 0) {
+      smask[s * rr.RW + w] = ms;
+      dmask[s * rr.RW + w] = md;
+    }
     any_s |= ms != 0;
     any_d |= md != 0;
   }
-  if (!any_s) src_ok[s] = 0;
-  if (!any_d) dst_ok[s] = 0;
+  if (lane == 0) {
+    if (!any_s) src_ok[s] = 0;
+    if (!any_d) dst_ok[s] = 0;
+  }
 }
 
 // OR of the masks over each 32-vertex group (tile / destination group cull); blockIdx.y = 1
@@ -1356,7 +1369,7 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     dmask.alloc(V * rr.RW * sizeof(unsigned long long), c->stream);
     tor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
     gor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
-    launch(c, "k_region_masks", k_region_masks, dim3(div_up(V, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
+    launch(c, "k_region_masks", k_region_masks, dim3(div_up(V * 32, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
            perm.as<int>(), V, m, rblo.as<double>(), rbhi.as<double>(), smask.as<unsigned long long>(),
            dmask.as<unsigned long long>(), sok.as<uint8_t>(), dok.as<uint8_t>());
     launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256), 2), dim3(256), 0, smask.as<unsigned long long>(),
