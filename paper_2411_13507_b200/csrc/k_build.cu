@@ -293,20 +293,25 @@ struct RegionRowsDev {
   int R, RW, n;
 };
 
-// one warp per sorted vertex, one lane per region (32 at a time): regions whose (1e-6-grown)
+// G lanes per sorted vertex (G a power of two <= 32, sized by the host so V x G fills the GPU),
+// each lane testing every G-th region of a 64-region mask word: regions whose (1e-6-grown)
 // position box misses the vertex are skipped (membership implies P_0 = x1 resp. P_p = x2 lies
-// in the region), the rest are tested row by row; the mask words are two ballots each.  The
-// warp writes its vertex's mask words whole (no pre-zeroing) and folds them: a vertex in no
+// in the region), the rest are tested row by row; the group ORs its bits by shuffles.  The
+// group writes its vertex's mask words whole (no pre-zeroing) and folds them: a vertex in no
 // region can neither start nor end an edge (src_ok / dst_ok cleared).  (One thread per vertex
-// looping over all regions was latency-bound: 93 us at cfg5-10k's 200 regions.)
+// looping over all regions was latency-bound at 10 k vertices: 93 us at cfg5-10k's 200
+// regions; one warp per vertex doubled the instructions at 100 k: 85 -> 195 us.)
 __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, const int* __restrict__ perm,
                                long long V, int m, const double* __restrict__ blo, const double* __restrict__ bhi,
                                unsigned long long* __restrict__ smask, unsigned long long* __restrict__ dmask,
-                               uint8_t* __restrict__ src_ok, uint8_t* __restrict__ dst_ok) {
+                               uint8_t* __restrict__ src_ok, uint8_t* __restrict__ dst_ok, int G) {
   BZG_PDL_ENTRY();
-  const long long s = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long s = t / G;
+  const int sub = (int)(t % G);
+  if (s >= V) return;  // uniform across the group
   const int lane = threadIdx.x & 31;
-  if (s >= V) return;  // warp-uniform
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
   const long long i = perm[s];
   const int n = rr.n;
   double v[kMaxN];
@@ -314,34 +319,33 @@ __global__ void k_region_masks(RegionRowsDev rr, const double* __restrict__ Vx, 
   bool any_s = false, any_d = false;
   for (int w = 0; w < rr.RW; ++w) {
     unsigned long long ms = 0, md = 0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = w * 64 + h * 32 + lane;
-      int in_s = 0, in_d = 0;
-      if (r < rr.R) {
-        bool inbox = true;
-        if (blo)
-          for (int k = 0; k < m; ++k) inbox &= (v[k] >= blo[r * m + k] - 1e-6) & (v[k] <= bhi[r * m + k] + 1e-6);
-        if (inbox) {
-          in_s = 1;
-          in_d = 1;
-          for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q)
-            in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
-          for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q)
-            in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
-        }
-      }
-      ms |= (unsigned long long)__ballot_sync(0xffffffffu, in_s) << (32 * h);
-      md |= (unsigned long long)__ballot_sync(0xffffffffu, in_d) << (32 * h);
+    for (int j = sub; j < 64; j += G) {
+      const int r = w * 64 + j;
+      if (r >= rr.R) break;
+      bool inbox = true;
+      if (blo)
+        for (int k = 0; k < m; ++k) inbox &= (v[k] >= blo[r * m + k] - 1e-6) & (v[k] <= bhi[r * m + k] + 1e-6);
+      if (!inbox) continue;
+      int in_s = 1, in_d = 1;
+      for (int q = rr.src_off[r]; q < rr.src_off[r + 1]; ++q)
+        in_s &= fma_chain(v, rr.src_F + (size_t)q * n, n) <= rr.src_th[q];
+      for (int q = rr.dst_off[r]; q < rr.dst_off[r + 1]; ++q)
+        in_d &= fma_chain(v, rr.dst_F + (size_t)q * n, n) <= rr.dst_th[q];
+      if (in_s) ms |= 1ull << j;
+      if (in_d) md |= 1ull << j;
     }
-    if (lane == 0) {
+    for (int off = G / 2; off > 0; off >>= 1) {
+      ms |= __shfl_xor_sync(gmask, ms, off);
+      md |= __shfl_xor_sync(gmask, md, off);
+    }
+    if (sub == 0) {
       smask[s * rr.RW + w] = ms;
       dmask[s * rr.RW + w] = md;
     }
     any_s |= ms != 0;
     any_d |= md != 0;
   }
-  if (lane == 0) {
+  if (sub == 0) {
     if (!any_s) src_ok[s] = 0;
     if (!any_d) dst_ok[s] = 0;
   }
@@ -1369,9 +1373,15 @@ bool build_pairs(Ctx* c, const bzg_build_desc* d, Graph* g, double th_shift, lon
     dmask.alloc(V * rr.RW * sizeof(unsigned long long), c->stream);
     tor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
     gor.alloc(ng * rr.RW * sizeof(unsigned long long), c->stream);
-    launch(c, "k_region_masks", k_region_masks, dim3(div_up(V * 32, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
+    // lanes per vertex: V x G up to ~1,150 threads per SM (cfg5 k_region_masks, G = 1/4/8/16/32:
+    // 10 k vertices 99/55/43/38/43 us, 100 k 93/96/111/166/247 us); BZG_REGION_LANES forces G
+    static const int g_env = std::getenv("BZG_REGION_LANES") ? std::atoi(std::getenv("BZG_REGION_LANES")) : 0;
+    int gl = 1;
+    while (gl < 32 && V * gl * 2 <= 1152ll * c->num_sms) gl *= 2;
+    if (g_env == 1 || g_env == 2 || g_env == 4 || g_env == 8 || g_env == 16 || g_env == 32) gl = g_env;
+    launch(c, "k_region_masks", k_region_masks, dim3(div_up(V * gl, 128)), dim3(128), 0, rr, g->vertices.as<double>(),
            perm.as<int>(), V, m, rblo.as<double>(), rbhi.as<double>(), smask.as<unsigned long long>(),
-           dmask.as<unsigned long long>(), sok.as<uint8_t>(), dok.as<uint8_t>());
+           dmask.as<unsigned long long>(), sok.as<uint8_t>(), dok.as<uint8_t>(), gl);
     launch(c, "k_mask_or", k_mask_or, dim3(div_up(ng * rr.RW, 256), 2), dim3(256), 0, smask.as<unsigned long long>(),
            sok.as<uint8_t>(), V, rr.RW, tor.as<unsigned long long>(), dmask.as<unsigned long long>(),
            dok.as<uint8_t>(), gor.as<unsigned long long>());
