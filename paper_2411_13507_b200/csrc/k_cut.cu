@@ -734,6 +734,26 @@ __global__ void k_fill_int(int* p, long long n, int v) {
   if (t < n) p[t] = v;
 }
 
+// The cut's per-edge state in one pass: kill = qkill = v (no obstacle yet), saved = 0; four
+// edges per thread (16-byte stores to both int arrays, one 4-byte store of flags).
+__global__ void k_cut_init(int* __restrict__ kill, int* __restrict__ qkill, uint8_t* __restrict__ saved, long long n,
+                           int v) {
+  BZG_PDL_ENTRY();
+  const long long e = 4 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+  if (e + 4 <= n) {
+    const int4 q = make_int4(v, v, v, v);
+    *reinterpret_cast<int4*>(kill + e) = q;
+    *reinterpret_cast<int4*>(qkill + e) = q;
+    *reinterpret_cast<uint32_t*>(saved + e) = 0u;
+  } else {
+    for (long long k = e; k < n; ++k) {
+      kill[k] = v;
+      qkill[k] = v;
+      saved[k] = 0;
+    }
+  }
+}
+
 // ||delta|| above which the ADMM verdict is final (see k_qp_select); BZG_POLISH_SCREEN=0
 // polishes every SOLVED instance exactly like the reference.
 double polish_screen() {
@@ -980,9 +1000,8 @@ void cut_enqueue(Ctx* c, Graph* g, const CutPrep& p, const unsigned char* d_blob
   d_gen.alloc(cc.gen_cap * sizeof(unsigned long long), c->stream);
   unsigned long long* dcnt = d_cnt.as<unsigned long long>();
   BZG_CHECK_CUDA(cudaMemsetAsync(d_cnt.ptr, 0, 16 * sizeof(unsigned long long), c->stream));
-  BZG_CHECK_CUDA(cudaMemsetAsync(d_saved.ptr, 0, std::max(E, 1ll), c->stream));
-  launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_kill.as<int>(), E, n_obs);
-  launch(c, "k_fill_int", k_fill_int, dim3(div_up(E, 256)), dim3(256), 0, d_qkill.as<int>(), E, n_obs);
+  launch(c, "k_cut_init", k_cut_init, dim3(div_up(div_up(E, 4), 256)), dim3(256), 0, d_kill.as<int>(),
+         d_qkill.as<int>(), d_saved.as<uint8_t>(), E, n_obs);
   if (cbits.kill && n_obs > 0)  // the recorded outcome rows (n_obs rows of Wb words, stride apart)
     for (uint32_t* rows : {cbits.kill, cbits.qsafe, cbits.qunsafe})
       BZG_CHECK_CUDA(cudaMemset2DAsync(rows, cbits.stride * sizeof(uint32_t), 0, cbits.Wb * sizeof(uint32_t), n_obs,
