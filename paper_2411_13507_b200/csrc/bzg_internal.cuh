@@ -115,6 +115,7 @@ enum WsSlot {
   WS_REACH_FLAGS,
   WS_SNAP, WS_BEST0, WS_BEST1, WS_NM_REACH, WS_NM_KEY, WS_NM_DIST, WS_NM_PARENT,  // find_path
   WS_OBSGRIDHDR, WS_CUTCNT, WS_CUTOBS, WS_QNEXT,                     // cut staging, counters
+  WS_TIGHT,                                                          // find_path tight in-edges
   WS_SCRATCH,                                                        // CUB temporary storage
   kWsSlots
 };

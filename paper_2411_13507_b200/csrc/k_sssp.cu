@@ -648,6 +648,7 @@ __global__ void k_plan(long long* __restrict__ plan, long long* __restrict__ tre
   const bool cached = !trivial && tree_key && *tree_key == v0;
   plan[2] = (!trivial && !cached) ? 1 : 0;
   plan[3] = cached ? 1 : 0;
+  plan[5] = 0;  // tight in-edges listed by k_parent_dist
   if (plan[2] && tree_key) *tree_key = v0;  // the tree built below is the cache from now on
 }
 
@@ -759,11 +760,15 @@ __global__ void k_bf_async(long long V, const long long* __restrict__ row_ptr, c
   }
 }
 
-// parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes)
+// parent[v] = argmin (d[u], u) over alive in-edges with fl(d[u] + c) == d[v] (two passes):
+// the first takes the min d[u] per v over the tight in-edges and lists those edges (about one
+// per reached vertex), the second picks the min u among the listed edges with d[u] == that
+// minimum -- all E edges again only if the list overflowed its capacity.
 __global__ void k_parent_dist(long long E, const int* __restrict__ src, const int* __restrict__ dst,
                               const double* __restrict__ cost, const uint8_t* __restrict__ alive,
                               const unsigned long long* __restrict__ dist, unsigned long long* __restrict__ pd,
-                              const long long* __restrict__ plan, const long long* __restrict__ dE) {
+                              const long long* __restrict__ plan, const long long* __restrict__ dE,
+                              int* __restrict__ tight, unsigned long long* __restrict__ n_tight, long long cap) {
   BZG_PDL_ENTRY();
   if (dE) E = min(E, *dE);
   if (plan && !plan[2]) return;
@@ -774,25 +779,42 @@ __global__ void k_parent_dist(long long E, const int* __restrict__ src, const in
   const unsigned long long bu = dist[u];
   if (bu >= kInfBits) return;
   const double nd = __dadd_rn(__longlong_as_double((long long)bu), cost[e]);
-  if (dbits(nd) == dist[v]) atomicMin(pd + v, bu);
+  if (dbits(nd) == dist[v]) {
+    atomicMin(pd + v, bu);
+    const unsigned long long k = atomicAdd(n_tight, 1ull);
+    if ((long long)k < cap) tight[k] = (int)e;
+  }
 }
 
-__global__ void k_parent_idx(long long E, const int* __restrict__ src, const int* __restrict__ dst,
-                             const double* __restrict__ cost, const uint8_t* __restrict__ alive,
-                             const unsigned long long* __restrict__ dist, const unsigned long long* __restrict__ pd,
-                             int* __restrict__ parent, const long long* __restrict__ plan,
-                             const long long* __restrict__ dE) {
-  BZG_PDL_ENTRY();
-  if (dE) E = min(E, *dE);
-  if (plan && !plan[2]) return;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= E) return;
+__device__ __forceinline__ void parent_edge(long long e, const int* __restrict__ src, const int* __restrict__ dst,
+                                            const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                                            const unsigned long long* __restrict__ dist,
+                                            const unsigned long long* __restrict__ pd, int* __restrict__ parent) {
   if (alive && !alive[e]) return;
   const int u = src[e], v = dst[e];
   const unsigned long long bu = dist[u];
   if (bu >= kInfBits || bu != pd[v]) return;
   const double nd = __dadd_rn(__longlong_as_double((long long)bu), cost[e]);
   if (dbits(nd) == dist[v]) atomicMin(parent + v, u);
+}
+
+__global__ void k_parent_idx(long long E, const int* __restrict__ src, const int* __restrict__ dst,
+                             const double* __restrict__ cost, const uint8_t* __restrict__ alive,
+                             const unsigned long long* __restrict__ dist, const unsigned long long* __restrict__ pd,
+                             int* __restrict__ parent, const long long* __restrict__ plan,
+                             const long long* __restrict__ dE, const int* __restrict__ tight,
+                             const unsigned long long* __restrict__ n_tight, long long cap) {
+  BZG_PDL_ENTRY();
+  if (dE) E = min(E, *dE);
+  if (plan && !plan[2]) return;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  const long long n = (long long)*n_tight;
+  if (n <= cap) {
+    for (long long k = tid; k < n; k += nt) parent_edge(tight[k], src, dst, cost, alive, dist, pd, parent);
+  } else {  // the list overflowed: every edge
+    for (long long e = tid; e < E; e += nt) parent_edge(e, src, dst, cost, alive, dist, pd, parent);
+  }
 }
 
 // out[0] = path length (-1: None), out[1] = dist bits, out[2..] = the path from v0 to vg
@@ -1136,12 +1158,19 @@ void path_enqueue(Ctx* c, Graph* g, Mask* mk, const SnapParams sp[2], const Snap
     std::fprintf(stderr, "[bzg path] vg %lld v0 %lld build %lld cached %lld; Bellman-Ford sweeps %d (V = %lld)\n",
                  hp[0], hp[1], hp[2], hp[3], hc[3], V);
   }
+  // tight in-edge list (counter plan[5], zeroed by k_plan): ~one entry per reached vertex
+  const long long tcap = std::max(1ll, std::min(E, 2 * V + 1024));
+  DevBuf& t_tight = c->ws[WS_TIGHT];
+  t_tight.alloc(tcap * sizeof(int), c->stream);
+  unsigned long long* n_tight = reinterpret_cast<unsigned long long*>(plan + 5);
   launch(c, "k_parent_dist", k_parent_dist, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, g->src.as<int>(),
          g->dst.as<int>(), g->cost.as<double>(), alive, (const unsigned long long*)dist, t_pd.as<unsigned long long>(),
-         cplan, (const long long*)g->dE);
-  launch(c, "k_parent_idx", k_parent_idx, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, g->src.as<int>(),
-         g->dst.as<int>(), g->cost.as<double>(), alive, (const unsigned long long*)dist,
-         (const unsigned long long*)t_pd.as<unsigned long long>(), parent, cplan, (const long long*)g->dE);
+         cplan, (const long long*)g->dE, t_tight.as<int>(), n_tight, tcap);
+  launch(c, "k_parent_idx", k_parent_idx,
+         dim3((unsigned)std::min<long long>(div_up(std::max(E, 1ll), 256), 8ll * c->num_sms)), dim3(256), 0, E,
+         g->src.as<int>(), g->dst.as<int>(), g->cost.as<double>(), alive, (const unsigned long long*)dist,
+         (const unsigned long long*)t_pd.as<unsigned long long>(), parent, cplan, (const long long*)g->dE,
+         (const int*)t_tight.as<int>(), (const unsigned long long*)n_tight, tcap);
 
   // ---- backtrack and the single read-back: [len, dist bits, path...], the first kHead entries
   DevBuf& d_out = c->ws[WS_SSSP_OUT];
