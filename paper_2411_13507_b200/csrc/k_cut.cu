@@ -708,15 +708,29 @@ __global__ void k_mask_finalize(long long E, int n_obs, const int* __restrict__ 
                                 const int* __restrict__ qp_kill, const uint8_t* __restrict__ qp_saved,
                                 uint8_t* __restrict__ alive, uint8_t* __restrict__ prov) {
   BZG_PDL_ENTRY();
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  const int kh = first_kill[e], kq = qp_kill[e];
-  const bool dead = kh < n_obs || kq < n_obs;
-  alive[e] = dead ? 0 : 1;
-  uint8_t p;
-  if (dead) p = kh < kq ? BZG_HEURISTIC_UNSAFE : BZG_QP_UNSAFE;
-  else p = qp_saved[e] ? BZG_QP_SAFE : BZG_HEURISTIC_SAFE;
-  prov[e] = p;
+  // four edges per thread: 16-byte loads of both kill arrays, 4-byte flag loads and stores
+  const long long e0 = 4 * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+  if (e0 >= E) return;
+  auto one = [&](int kh, int kq, uint8_t saved, uint8_t& a, uint8_t& p) {
+    const bool dead = kh < n_obs || kq < n_obs;
+    a = dead ? 0 : 1;
+    if (dead) p = kh < kq ? BZG_HEURISTIC_UNSAFE : BZG_QP_UNSAFE;
+    else p = saved ? BZG_QP_SAFE : BZG_HEURISTIC_SAFE;
+  };
+  if (e0 + 4 <= E) {
+    const int4 kh = *reinterpret_cast<const int4*>(first_kill + e0);
+    const int4 kq = *reinterpret_cast<const int4*>(qp_kill + e0);
+    const uint32_t sv = *reinterpret_cast<const uint32_t*>(qp_saved + e0);
+    uint8_t a[4], p[4];
+    one(kh.x, kq.x, (uint8_t)(sv & 0xFF), a[0], p[0]);
+    one(kh.y, kq.y, (uint8_t)((sv >> 8) & 0xFF), a[1], p[1]);
+    one(kh.z, kq.z, (uint8_t)((sv >> 16) & 0xFF), a[2], p[2]);
+    one(kh.w, kq.w, (uint8_t)(sv >> 24), a[3], p[3]);
+    *reinterpret_cast<uint32_t*>(alive + e0) = a[0] | (a[1] << 8) | (a[2] << 16) | ((uint32_t)a[3] << 24);
+    *reinterpret_cast<uint32_t*>(prov + e0) = p[0] | (p[1] << 8) | (p[2] << 16) | ((uint32_t)p[3] << 24);
+  } else {
+    for (long long e = e0; e < E; ++e) one(first_kill[e], qp_kill[e], qp_saved[e], alive[e], prov[e]);
+  }
 }
 
 __global__ void k_unpack_pend(const unsigned long long* __restrict__ pend, long long n, long long* __restrict__ e,
@@ -1067,7 +1081,7 @@ void cut_enqueue(Ctx* c, Graph* g, const CutPrep& p, const unsigned char* d_blob
            dim3(256), 0, d_pend.as<unsigned long long>(), qcap, (const unsigned long long*)(dcnt + 5),
            d_safe.as<uint8_t>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), dcnt, cbits);
   }
-  launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(std::max(E, 1ll), 256)), dim3(256), 0, E, n_obs,
+  launch(c, "k_mask_finalize", k_mask_finalize, dim3(div_up(div_up(E, 4), 256)), dim3(256), 0, E, n_obs,
          d_kill.as<int>(), d_qkill.as<int>(), d_saved.as<uint8_t>(), mk->alive.as<uint8_t>(), mk->prov.as<uint8_t>());
   BZG_CHECK_CUDA(cudaMemcpyAsync(h_cnt, d_cnt.ptr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
 }
